@@ -1,0 +1,590 @@
+/*
+ * oracle/mg_oracle.c -- TEST INFRASTRUCTURE ONLY (parity oracle).
+ *
+ * A plain, slow, obviously correct CPU fp64 implementation of the cell-centered
+ * multigrid solve of the finite-volume Poisson equation in
+ *   Bartuschat & Ruede, "Parallel Multiphysics Simulations of Charged Particles
+ *   in Microfluidic Flows", arXiv 1410.6609  (PAPER.md, cited as P:<line>).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline leg may
+ * load this library.  It shares no code with the CUDA product and the product
+ * never loads it.  Compiled with -O2 -ffp-contract=off (no FMA contraction,
+ * no fast-math); OpenMP only over independent per-cell loops, so the result
+ * is bitwise the same for any thread count.
+ *
+ * Every step follows the paper in its order and notation:
+ *   Poisson equation          -Lap Phi = rho/eps            Eq.12
+ *   7-point FV stencil        -1/dx^2 [.. 6 .. -1 ..]      Eq.13
+ *   Dirichlet/Neumann folding [0 (beta-+alpha) gamma]
+ *   charge density            Q/V on cells whose centre is in the sphere P:481
+ *   hierarchy                 coarsen while dims even
+ *   Galerkin coarsening       A_c = R A P, R average, P nearest neighbour P:514-516
+ *   magnified correction      phi += alpha P e, alpha = 2
+ *   red-black Gauss-Seidel    checkerboard half-sweeps
+ *   V(nu1,nu2)-cycles
+ *   coarsest solve by CG
+ *   residual L2 termination   Alg.1
+ * Readings where the paper is silent are listed in DESIGN.md (c1..c21 of
+ * SURVEY.md section 8(c)); each is cited at its use below.
+ */
+#include "mg_oracle.h"
+
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define MAXLEV 32
+#define ORC_PI 3.14159265358979323846
+
+typedef struct {
+  int nx, ny, nz;
+  long n;
+  double *A;          /* 7 per cell: centre, x-, x+, y-, y+, z-, z+ */
+  uint8_t *unk;       /* 1 = unknown cell, 0 = solid (masked) */
+  double *phi, *f, *r;
+} level_t;
+
+struct orc_hier {
+  int nlev;
+  level_t L[MAXLEV];
+  double h;
+  int bct[6];
+  double bcv[6];
+  int nu1, nu2;
+  double alpha;
+  double coarse_tol;
+  int coarse_maxit;
+  int last_cg_iters;
+};
+
+static inline long IDX(const level_t *L, int i, int j, int k) {
+  return ((long)i * L->ny + j) * L->nz + k;
+}
+
+/* value of a field at (i,j,k), 0 outside the level (the folded boundary
+ * coefficient is 0 there, so the value never matters) */
+static inline double get(const level_t *L, const double *v, int i, int j,
+                         int k) {
+  if (i < 0 || j < 0 || k < 0 || i >= L->nx || j >= L->ny || k >= L->nz)
+    return 0.0;
+  return v[IDX(L, i, j, k)];
+}
+
+static void level_alloc(level_t *L, int nx, int ny, int nz) {
+  L->nx = nx;
+  L->ny = ny;
+  L->nz = nz;
+  L->n = (long)nx * ny * nz;
+  L->A = (double *)calloc((size_t)L->n * 7, sizeof(double));
+  L->unk = (uint8_t *)calloc((size_t)L->n, 1);
+  L->phi = (double *)calloc((size_t)L->n, sizeof(double));
+  L->f = (double *)calloc((size_t)L->n, sizeof(double));
+  L->r = (double *)calloc((size_t)L->n, sizeof(double));
+}
+
+static void level_free(level_t *L) {
+  free(L->A);
+  free(L->unk);
+  free(L->phi);
+  free(L->f);
+  free(L->r);
+}
+
+/* Finest-level stencil: Eq.13 gives -Lap_dx = (1/dx^2)[6; -1 x 6]
+ * as the operator A of -Lap Phi = f (reading c1).  Boundary folding per
+ * direction, P:451-459 with alpha the coefficient toward the boundary:
+ *   Dirichlet: centre beta -> beta - alpha, alpha -> 0
+ *   Neumann:   centre beta -> beta + alpha, alpha -> 0
+ * A solid (masked) neighbour is a homogeneous Neumann face (reading c19). */
+static void assemble_finest(orc_hier *H) {
+  level_t *L = &H->L[0];
+  const double inv = 1.0 / (H->h * H->h);
+  const int di[6] = {-1, 1, 0, 0, 0, 0};
+  const int dj[6] = {0, 0, -1, 1, 0, 0};
+  const int dk[6] = {0, 0, 0, 0, -1, 1};
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        long c = IDX(L, i, j, k);
+        double *a = &L->A[7 * c];
+        if (!L->unk[c]) {
+          for (int q = 0; q < 7; q++) a[q] = 0.0;
+          continue;
+        }
+        double beta = 6.0 * inv;
+        for (int q = 0; q < 6; q++) {
+          double alpha = -1.0 * inv;
+          int ii = i + di[q], jj = j + dj[q], kk = k + dk[q];
+          int outside = ii < 0 || jj < 0 || kk < 0 || ii >= L->nx ||
+                        jj >= L->ny || kk >= L->nz;
+          if (outside) {
+            if (H->bct[q] == ORC_DIRICHLET)
+              beta = beta - alpha;
+            else
+              beta = beta + alpha;
+            alpha = 0.0;
+          } else if (!L->unk[IDX(L, ii, jj, kk)]) {
+            beta = beta + alpha; /* homogeneous Neumann toward a solid cell */
+            alpha = 0.0;
+          }
+          a[1 + q] = alpha;
+        }
+        a[0] = beta;
+      }
+}
+
+/* Galerkin coarsening A_c = R A P: P = nearest-neighbour
+ * (piecewise constant) injection of a coarse value to its unknown children,
+ * R = (1/8) P^T (averaging).  Written as a stencil product: entry (I,J) of
+ * R A P is (1/8) * sum over children i of I and j of J of A(i,j). */
+static void galerkin(orc_hier *H, int l) {
+  const level_t *F = &H->L[l];
+  level_t *C = &H->L[l + 1];
+  const int di[6] = {-1, 1, 0, 0, 0, 0};
+  const int dj[6] = {0, 0, -1, 1, 0, 0};
+  const int dk[6] = {0, 0, 0, 0, -1, 1};
+  for (int I = 0; I < C->nx; I++)
+    for (int J = 0; J < C->ny; J++)
+      for (int K = 0; K < C->nz; K++) {
+        long cI = IDX(C, I, J, K);
+        double s[7] = {0, 0, 0, 0, 0, 0, 0};
+        int any = 0;
+        for (int a = 0; a < 2; a++)
+          for (int b = 0; b < 2; b++)
+            for (int c = 0; c < 2; c++) {
+              int i = 2 * I + a, j = 2 * J + b, k = 2 * K + c;
+              long fi = IDX(F, i, j, k);
+              if (!F->unk[fi]) continue;
+              any = 1;
+              const double *A = &F->A[7 * fi];
+              s[0] += A[0];
+              for (int q = 0; q < 6; q++) {
+                int ii = i + di[q], jj = j + dj[q], kk = k + dk[q];
+                if (ii < 0 || jj < 0 || kk < 0 || ii >= F->nx || jj >= F->ny ||
+                    kk >= F->nz)
+                  continue; /* folded: coefficient is 0 */
+                if (!F->unk[IDX(F, ii, jj, kk)]) continue;
+                if (ii / 2 == I && jj / 2 == J && kk / 2 == K)
+                  s[0] += A[1 + q]; /* sibling: lands on the coarse diagonal */
+                else
+                  s[1 + q] += A[1 + q]; /* child of coarse neighbour I+e_q */
+              }
+            }
+        C->unk[cI] = (uint8_t)any;
+        for (int q = 0; q < 7; q++) C->A[7 * cI + q] = 0.125 * s[q];
+      }
+}
+
+orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
+                     const double *bc_value, const uint8_t *solid,
+                     int min_coarse, int max_levels) {
+  if (nx <= 0 || ny <= 0 || nz <= 0 || !(h > 0.0)) return NULL;
+  if (max_levels <= 0) max_levels = MAXLEV;
+  if (max_levels > MAXLEV) max_levels = MAXLEV;
+  orc_hier *H = (orc_hier *)calloc(1, sizeof(orc_hier));
+  H->h = h;
+  for (int q = 0; q < 6; q++) {
+    H->bct[q] = bc_type[q];
+    H->bcv[q] = bc_value[q];
+  }
+  H->nu1 = 2;
+  H->nu2 = 2;
+  H->alpha = 2.0;
+  H->coarse_tol = 1e-12;
+  H->coarse_maxit = 1000;
+  /* hierarchy (reading c9): coarsen while every dimension is even,
+   * the coarse dimensions are again even ("a multiple of two" at the
+   * coarsest level) and the smallest dimension exceeds min_coarse. */
+  int d[3] = {nx, ny, nz};
+  level_alloc(&H->L[0], d[0], d[1], d[2]);
+  H->nlev = 1;
+  while (H->nlev < max_levels) {
+    int ok = 1;
+    for (int a = 0; a < 3; a++)
+      if (d[a] % 2 != 0 || (d[a] / 2) % 2 != 0) ok = 0;
+    int mn = d[0] < d[1] ? d[0] : d[1];
+    if (d[2] < mn) mn = d[2];
+    if (mn <= min_coarse) ok = 0;
+    if (!ok) break;
+    for (int a = 0; a < 3; a++) d[a] /= 2;
+    level_alloc(&H->L[H->nlev], d[0], d[1], d[2]);
+    H->nlev++;
+  }
+  level_t *L0 = &H->L[0];
+  for (long c = 0; c < L0->n; c++) L0->unk[c] = solid ? (solid[c] ? 0 : 1) : 1;
+  assemble_finest(H);
+  for (int l = 0; l + 1 < H->nlev; l++) galerkin(H, l);
+  return H;
+}
+
+void orc_destroy(orc_hier *H) {
+  if (!H) return;
+  for (int l = 0; l < H->nlev; l++) level_free(&H->L[l]);
+  free(H);
+}
+
+int orc_num_levels(const orc_hier *H) { return H->nlev; }
+
+void orc_level_dims(const orc_hier *H, int l, int *d) {
+  d[0] = H->L[l].nx;
+  d[1] = H->L[l].ny;
+  d[2] = H->L[l].nz;
+}
+
+void orc_get_stencil(const orc_hier *H, int l, double *out) {
+  memcpy(out, H->L[l].A, sizeof(double) * 7 * H->L[l].n);
+}
+void orc_get_unknown(const orc_hier *H, int l, uint8_t *out) {
+  memcpy(out, H->L[l].unk, H->L[l].n);
+}
+void orc_get_phi(const orc_hier *H, int l, double *out) {
+  memcpy(out, H->L[l].phi, sizeof(double) * H->L[l].n);
+}
+void orc_set_phi(orc_hier *H, int l, const double *in) {
+  memcpy(H->L[l].phi, in, sizeof(double) * H->L[l].n);
+}
+void orc_get_rhs(const orc_hier *H, int l, double *out) {
+  memcpy(out, H->L[l].f, sizeof(double) * H->L[l].n);
+}
+void orc_set_rhs_raw(orc_hier *H, int l, const double *in) {
+  memcpy(H->L[l].f, in, sizeof(double) * H->L[l].n);
+}
+
+/* RHS adaptation to the BCs on the finest grid only, per
+ * direction in face order x-, x+, y-, y+, z-, z+ (P:726-729).  With alpha the
+ * unfolded coefficient toward the boundary (-1/h^2):
+ *   Dirichlet g_d:  f <- f - 2 alpha g_d                 (c3)
+ *   Neumann   g_n:  f <- f - alpha (h g_n)               (c2:
+ *                   Phi_0 - Phi_1 = h g_n, outward normal derivative)      */
+void orc_bc_adapt(orc_hier *H) {
+  level_t *L = &H->L[0];
+  const double alpha = -1.0 * (1.0 / (H->h * H->h));
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        long c = IDX(L, i, j, k);
+        if (!L->unk[c]) continue;
+        int on[6] = {i == 0, i == L->nx - 1, j == 0,
+                     j == L->ny - 1, k == 0, k == L->nz - 1};
+        for (int q = 0; q < 6; q++) {
+          if (!on[q]) continue;
+          double g = H->bcv[q];
+          if (H->bct[q] == ORC_DIRICHLET)
+            L->f[c] = L->f[c] - 2.0 * alpha * g;
+          else
+            L->f[c] = L->f[c] - alpha * (H->h * g);
+        }
+      }
+}
+
+void orc_set_rhs(orc_hier *H, const double *f) {
+  level_t *L = &H->L[0];
+  for (long c = 0; c < L->n; c++) L->f[c] = L->unk[c] ? f[c] : 0.0;
+  orc_bc_adapt(H);
+}
+
+/* "each cell whose center is overlapped"; cell centres at
+ * ((i+1/2)h, (j+1/2)h, (k+1/2)h); inclusive test |x-c|^2 <= R^2 (c13). */
+static inline int inside(int i, int j, int k, double h, double cx, double cy,
+                         double cz, double R) {
+  double dx = ((double)i + 0.5) * h - cx;
+  double dy = ((double)j + 0.5) * h - cy;
+  double dz = ((double)k + 0.5) * h - cz;
+  double d2 = (dx * dx + dy * dy) + dz * dz;
+  return d2 <= R * R;
+}
+
+static void bbox(int n, double h, double c, double R, int *lo, int *hi) {
+  /* every cell whose centre can be within R of c, plus a safety margin */
+  int a = (int)floor((c - R) / h - 0.5) - 1;
+  int b = (int)ceil((c + R) / h - 0.5) + 1;
+  if (a < 0) a = 0;
+  if (b > n - 1) b = n - 1;
+  *lo = a;
+  *hi = b;
+}
+
+long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
+                           double cy, double cz, double R) {
+  int i0, i1, j0, j1, k0, k1;
+  bbox(nx, h, cx, R, &i0, &i1);
+  bbox(ny, h, cy, R, &j0, &j1);
+  bbox(nz, h, cz, R, &k0, &k1);
+  long cnt = 0;
+  for (int i = i0; i <= i1; i++)
+    for (int j = j0; j <= j1; j++)
+      for (int k = k0; k <= k1; k++)
+        cnt += inside(i, j, k, h, cx, cy, cz, R);
+  return cnt;
+}
+
+/* charge density of uniformly charged spheres (c12):
+ *   PER_CELLS:  rho_p = Q_p / (n_p h^3)  (charge spread over the n_p cells)
+ *   PER_VOLUME: rho_p = Q_p / (4/3 pi R_p^3) (the paper's naive mapping)
+ * eps = 1 (c15), so f = rho.  Overlapping spheres add in sphere order. */
+void orc_sphere_density(int nx, int ny, int nz, double h, int n,
+                        const double *centers, const double *radii,
+                        const double *charges, int normalization,
+                        double *out) {
+  long N = (long)nx * ny * nz;
+  for (long c = 0; c < N; c++) out[c] = 0.0;
+  for (int p = 0; p < n; p++) {
+    double cx = centers[3 * p], cy = centers[3 * p + 1],
+           cz = centers[3 * p + 2], R = radii[p];
+    long np = orc_sphere_cell_count(nx, ny, nz, h, cx, cy, cz, R);
+    double rho;
+    if (normalization == ORC_PER_VOLUME)
+      rho = charges[p] / ((4.0 / 3.0) * ORC_PI * (R * R * R));
+    else {
+      if (np == 0) continue;
+      rho = charges[p] / ((double)np * (h * h * h));
+    }
+    int i0, i1, j0, j1, k0, k1;
+    bbox(nx, h, cx, R, &i0, &i1);
+    bbox(ny, h, cy, R, &j0, &j1);
+    bbox(nz, h, cz, R, &k0, &k1);
+    for (int i = i0; i <= i1; i++)
+      for (int j = j0; j <= j1; j++)
+        for (int k = k0; k <= k1; k++)
+          if (inside(i, j, k, h, cx, cy, cz, R))
+            out[((long)i * ny + j) * nz + k] += rho;
+  }
+}
+
+int orc_set_rhs_from_spheres(orc_hier *H, int n, const double *centers,
+                             const double *radii, const double *charges,
+                             int normalization) {
+  level_t *L = &H->L[0];
+  if (normalization == ORC_PER_CELLS)
+    for (int p = 0; p < n; p++)
+      if (orc_sphere_cell_count(L->nx, L->ny, L->nz, H->h, centers[3 * p],
+                                centers[3 * p + 1], centers[3 * p + 2],
+                                radii[p]) == 0)
+        return -1;
+  orc_sphere_density(L->nx, L->ny, L->nz, H->h, n, centers, radii, charges,
+                     normalization, L->f);
+  for (long c = 0; c < L->n; c++)
+    if (!L->unk[c]) L->f[c] = 0.0;
+  orc_bc_adapt(H);
+  return 0;
+}
+
+/* sum_q a_q phi_q in the fixed direction order x-, x+, y-, y+, z-, z+ */
+static inline double offdiag(const level_t *L, const double *a,
+                             const double *v, int i, int j, int k) {
+  return ((((a[1] * get(L, v, i - 1, j, k) + a[2] * get(L, v, i + 1, j, k)) +
+            a[3] * get(L, v, i, j - 1, k)) +
+           a[4] * get(L, v, i, j + 1, k)) +
+          a[5] * get(L, v, i, j, k - 1)) +
+         a[6] * get(L, v, i, j, k + 1);
+}
+
+/* Red-black Gauss-Seidel half-sweep (colour order c7): for every
+ * unknown cell with (i+j+k)%2 == color,  phi_c <- (f_c - sum_q a_q phi_q)/a_cc */
+void orc_smooth_half(orc_hier *H, int l, int color) {
+  level_t *L = &H->L[l];
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        if (((i + j + k) & 1) != color) continue;
+        long c = IDX(L, i, j, k);
+        if (!L->unk[c]) continue;
+        const double *a = &L->A[7 * c];
+        double nb = offdiag(L, a, L->phi, i, j, k);
+        L->phi[c] = (L->f[c] - nb) / a[0];
+      }
+}
+
+/* y = A x on level l (masked cells give 0) */
+void orc_apply(const orc_hier *H, int l, const double *x, double *y) {
+  const level_t *L = &H->L[l];
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        long c = IDX(L, i, j, k);
+        if (!L->unk[c]) {
+          y[c] = 0.0;
+          continue;
+        }
+        const double *a = &L->A[7 * c];
+        y[c] = a[0] * x[c] + offdiag(L, a, x, i, j, k);
+      }
+}
+
+/* r = f - A phi (unknown cells), 0 on masked cells */
+void orc_residual(const orc_hier *H, int l, double *r) {
+  const level_t *L = &H->L[l];
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        long c = IDX(L, i, j, k);
+        if (!L->unk[c]) {
+          r[c] = 0.0;
+          continue;
+        }
+        const double *a = &L->A[7 * c];
+        double Au = a[0] * L->phi[c] + offdiag(L, a, L->phi, i, j, k);
+        r[c] = L->f[c] - Au;
+      }
+}
+
+/* f_{l+1} = R r_l, R the 8-child average (reading c4).  Summation order
+ * is a fixed pairwise tree over child bits (dx,dy,dz), dz fastest. */
+void orc_restrict_residual(orc_hier *H, int l) {
+  level_t *F = &H->L[l];
+  level_t *C = &H->L[l + 1];
+  orc_residual(H, l, F->r);
+#pragma omp parallel for schedule(static)
+  for (int I = 0; I < C->nx; I++)
+    for (int J = 0; J < C->ny; J++)
+      for (int K = 0; K < C->nz; K++) {
+        double r[2][2][2];
+        for (int a = 0; a < 2; a++)
+          for (int b = 0; b < 2; b++)
+            for (int c = 0; c < 2; c++)
+              r[a][b][c] = F->r[IDX(F, 2 * I + a, 2 * J + b, 2 * K + c)];
+        double s = ((r[0][0][0] + r[0][0][1]) + (r[0][1][0] + r[0][1][1])) +
+                   ((r[1][0][0] + r[1][0][1]) + (r[1][1][0] + r[1][1][1]));
+        C->f[IDX(C, I, J, K)] = 0.125 * s;
+      }
+}
+
+/* phi_l += alpha * P e_{l+1}; P = nearest-neighbour prolongation,
+ * alpha the magnification of the coarse-grid correction (c6). */
+void orc_prolong_correct(orc_hier *H, int l, double alpha) {
+  level_t *F = &H->L[l];
+  const level_t *C = &H->L[l + 1];
+#pragma omp parallel for schedule(static)
+  for (int i = 0; i < F->nx; i++)
+    for (int j = 0; j < F->ny; j++)
+      for (int k = 0; k < F->nz; k++) {
+        long c = IDX(F, i, j, k);
+        if (!F->unk[c]) continue;
+        F->phi[c] = F->phi[c] + alpha * C->phi[IDX(C, i / 2, j / 2, k / 2)];
+      }
+}
+
+static double dot(const level_t *L, const double *x, const double *y) {
+  double s = 0.0;
+  for (long c = 0; c < L->n; c++)
+    if (L->unk[c]) s += x[c] * y[c];
+  return s;
+}
+
+/* Coarsest-grid solve by unpreconditioned CG, Hestenes-Stiefel
+ * from x = 0; stop when ||r|| <= tol ||b|| or after maxit iterations (c8).
+ * Writes the solution into phi of level l; returns the iteration count. */
+int orc_cg(orc_hier *H, int l, double tol, int maxit) {
+  level_t *L = &H->L[l];
+  long n = L->n;
+  double *x = L->phi, *b = L->f;
+  double *r = (double *)malloc(sizeof(double) * n);
+  double *p = (double *)malloc(sizeof(double) * n);
+  double *q = (double *)malloc(sizeof(double) * n);
+  for (long c = 0; c < n; c++) {
+    x[c] = 0.0;
+    r[c] = L->unk[c] ? b[c] : 0.0;
+    p[c] = r[c];
+  }
+  double rho = dot(L, r, r);
+  double bnorm = sqrt(rho);
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      orc_apply(H, l, p, q);
+      double pq = dot(L, p, q);
+      double a = rho / pq;
+      for (long c = 0; c < n; c++) {
+        x[c] = x[c] + a * p[c];
+        r[c] = r[c] - a * q[c];
+      }
+      double rho1 = dot(L, r, r);
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      double beta = rho1 / rho;
+      for (long c = 0; c < n; c++) p[c] = r[c] + beta * p[c];
+      rho = rho1;
+    }
+  }
+  free(r);
+  free(p);
+  free(q);
+  H->last_cg_iters = it;
+  return it;
+}
+
+int orc_last_cg_iters(const orc_hier *H) { return H->last_cg_iters; }
+
+void orc_set_schedule(orc_hier *H, int nu1, int nu2, double alpha,
+                      double coarse_tol, int coarse_maxit) {
+  H->nu1 = nu1;
+  H->nu2 = nu2;
+  H->alpha = alpha;
+  H->coarse_tol = coarse_tol;
+  H->coarse_maxit = coarse_maxit;
+}
+
+/* ||f - A phi||_2 on the finest level, unscaled (c10); serial sum */
+double orc_residual_norm(const orc_hier *H) {
+  const level_t *L = &H->L[0];
+  orc_residual(H, 0, L->r);
+  double s = 0.0;
+  for (long c = 0; c < L->n; c++) s += L->r[c] * L->r[c];
+  return sqrt(s);
+}
+
+/* V(nu1,nu2)-cycle: pre-smoothing, residual, restriction, coarse
+ * phi = 0, recursion, CG on the coarsest level, prolongation with magnified
+ * correction, post-smoothing.  Red then black in every sweep (c7). */
+static void vcycle_level(orc_hier *H, int l) {
+  if (l == H->nlev - 1) {
+    orc_cg(H, l, H->coarse_tol, H->coarse_maxit);
+    return;
+  }
+  for (int s = 0; s < H->nu1; s++) {
+    orc_smooth_half(H, l, 0);
+    orc_smooth_half(H, l, 1);
+  }
+  orc_restrict_residual(H, l);
+  level_t *C = &H->L[l + 1];
+  for (long c = 0; c < C->n; c++) C->phi[c] = 0.0;
+  vcycle_level(H, l + 1);
+  orc_prolong_correct(H, l, H->alpha);
+  for (int s = 0; s < H->nu2; s++) {
+    orc_smooth_half(H, l, 0);
+    orc_smooth_half(H, l, 1);
+  }
+}
+
+double orc_vcycle(orc_hier *H) {
+  vcycle_level(H, 0);
+  return orc_residual_norm(H);
+}
+
+/* Alg.1: while residual >= tol: V-cycle.  tol is relative to the
+ * initial residual (c10).  Divergence: NaN or growth > 10x in one cycle. */
+int orc_solve(orc_hier *H, double tol, int max_cycles, int *cycles_out,
+              double *hist) {
+  double r0 = orc_residual_norm(H);
+  double prev = r0;
+  if (hist) hist[0] = r0;
+  int k = 0;
+  int status = 1;
+  if (r0 == 0.0) status = 0;
+  while (status == 1 && k < max_cycles) {
+    double rk = orc_vcycle(H);
+    k++;
+    if (hist) hist[k] = rk;
+    if (!(rk == rk) || rk > 10.0 * prev) {
+      status = 2;
+      break;
+    }
+    if (rk <= tol * r0) status = 0;
+    prev = rk;
+  }
+  if (cycles_out) *cycles_out = k;
+  return status;
+}

@@ -1,0 +1,453 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test names the passage it pins.  None of the expected values comes from
+the oracle itself or from the CUDA path: they are paper-printed values
+(tests/golden/), closed forms, or independent dense/spectral constructions
+(tests/dense.py, built from ghost-cell extrapolation, not from the oracle's
+folded stencils).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import dense
+import oracle
+from conftest import read_golden
+from paper_1410_6609_b200 import workloads as W
+
+D, N = oracle.DIRICHLET, oracle.NEUMANN
+
+BC_COMBOS = [
+    ([D] * 6, [0.0] * 6),
+    ([D] * 6, [1.0, -2.0, 0.5, 3.0, -1.0, 2.0]),
+    ([N, N, D, D, N, N], [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]),          # channel
+    ([N, D, N, D, N, D], [0.25, 1.0, -0.5, -1.0, 2.0, 0.0]),      # mixed
+    ([D, N, N, N, N, N], [1.0, 0.3, -0.2, 0.1, 0.0, 0.4]),        # one Dirichlet face
+]
+
+
+# --------------------------------------------------------------------------
+# Operator + folding
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("row", read_golden("folding_1d.txt"))
+def test_folding_1d_paper_example(row):
+    """[a b g] -> [0 (b-+a) g], RHS f - 2 a g_d / f - a g_n.
+    A 4x1x1 grid with homogeneous Neumann on y and z is the 1D problem."""
+    bc, g, f1, sl, sc, sr, rhs = row
+    g, f1, sl, sc, sr, rhs = map(float, (g, f1, sl, sc, sr, rhs))
+    t = D if bc == "dirichlet" else N
+    o = oracle.Oracle((4, 1, 1), 1.0, [t, D, N, N, N, N],
+                      [g, 0.0, 0.0, 0.0, 0.0, 0.0])
+    st = o.stencil(0)[0, 0, 0]
+    assert st[1] == sl and st[0] == sc and st[2] == sr
+    assert np.all(st[3:] == 0.0)
+    f = np.zeros((4, 1, 1))
+    f[0, 0, 0] = f1
+    o.set_rhs(f)
+    assert o.rhs(0)[0, 0, 0] == rhs
+
+
+@pytest.mark.parametrize("bc", BC_COMBOS)
+def test_dense_direct_solve_8cubed(bc):
+    """Dense direct solve on 8^3 (north_star): the converged MG solution equals
+    np.linalg.solve of the ghost-cell operator to 1e-12."""
+    bt, bv = bc
+    shape, h = (8, 8, 8), 1.0 / 8
+    rng = np.random.default_rng(1)
+    f = rng.uniform(-1, 1, shape)
+    A = dense.dense_operator(shape, h, bt)
+    b = f + dense.bc_rhs_shift(shape, h, bt, bv)
+    u = np.linalg.solve(A, b.reshape(-1)).reshape(shape)
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    assert o.nlevels == 3
+    o.set_rhs(f)
+    st, cyc, hist = o.solve(1e-14, 60)
+    assert st == 0
+    err = np.linalg.norm(o.phi() - u) / np.linalg.norm(u)
+    assert err < 1e-12
+    # the folded finest stencil is the ghost-cell operator, entry by entry
+    assert np.array_equal(dense.stencil_to_dense(o.stencil(0)), A)
+
+
+@pytest.mark.parametrize("bc", BC_COMBOS[1:4])
+def test_kronecker_exact_solve(bc):
+    """Fast-diagonalisation exact solve (A = Tx(x)I(x)I + ...) on a box larger
+    than any dense matrix; MG converged to 1e-13 must match to 1e-11."""
+    bt, bv = bc
+    shape, h = (64, 32, 16), 1.0
+    rng = np.random.default_rng(7)
+    f = rng.uniform(-1, 1, shape)
+    b = f + dense.bc_rhs_shift(shape, h, bt, bv)
+    u = dense.kron_solve(b, h, bt)
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    o.set_rhs(f)
+    st, cyc, hist = o.solve(1e-13, 80)
+    assert st == 0
+    assert np.linalg.norm(o.phi() - u) / np.linalg.norm(u) < 1e-11
+
+
+def test_kronecker_channel_spheres():
+    """Config-2 recipe at reduced size: sphere RHS built by brute force here,
+    BC shift by ghost cells, exact solve by fast diagonalisation."""
+    shape = (64, 32, 32)
+    bt, bv = W.channel_bc(1.0)
+    c, q = W.random_spheres(shape, 4.0, 12, seed=3)
+    R = np.full(len(q), 4.0)
+    # brute-force density over all cells, inclusive centre test (c13)
+    x = [np.arange(n) + 0.5 for n in shape]
+    X, Y, Z = np.meshgrid(*x, indexing="ij")
+    rho = np.zeros(shape)
+    for p in range(len(q)):
+        inside = ((X - c[p, 0]) ** 2 + (Y - c[p, 1]) ** 2
+                  + (Z - c[p, 2]) ** 2) <= R[p] ** 2
+        rho[inside] += q[p] / inside.sum()
+    o = oracle.Oracle(shape, 1.0, bt, bv, min_coarse=4)
+    o.set_rhs_from_spheres(c, R, q)
+    raw = oracle.sphere_density(shape, 1.0, c, R, q)
+    assert np.allclose(raw, rho, rtol=0, atol=1e-15)
+    st, cyc, hist = o.solve(1e-13, 100)
+    assert st == 0
+    u = dense.kron_solve(rho + dense.bc_rhs_shift(shape, 1.0, bt, bv), 1.0, bt)
+    assert np.linalg.norm(o.phi() - u) / np.linalg.norm(u) < 1e-11
+
+
+# --------------------------------------------------------------------------
+# Discretisation order / closed form (config 1)
+# --------------------------------------------------------------------------
+def _c_of_h(h):
+    """sin(pi (i+1/2) h) is an exact eigenvector of the cell-centred Dirichlet
+    operator with eigenvalue 3 (4/h^2) sin^2(pi h/2), so Phi_h = c(h) u."""
+    return (math.pi * h / 2) ** 2 / math.sin(math.pi * h / 2) ** 2
+
+
+@pytest.mark.parametrize("n", [16, 32, 64])
+def test_config1_closed_form_and_order(n):
+    """O(h^2) convergence to the manufactured sin.sin.sin solution (north_star,
+    Eq.13 'up to O(dx^2) accuracy')."""
+    w = W.cfg1(n)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4)
+    o.set_rhs(w.rhs)
+    for _ in range(14):
+        o.vcycle()
+    u = w.rhs / (3.0 * np.pi ** 2)
+    phi = o.phi()
+    ch = _c_of_h(w.h)
+    assert np.abs(phi - ch * u).max() / u.max() < 1e-13 * n
+    err = np.abs(phi - u).max() / u.max()
+    assert abs(err - (ch - 1.0)) < 1e-12
+
+
+def test_config1_error_ratio_is_four():
+    errs = []
+    for n in (16, 32, 64):
+        errs.append(_c_of_h(1.0 / n) - 1.0)
+    assert abs(errs[0] / errs[1] - 4.0) < 0.01
+    assert abs(errs[1] / errs[2] - 4.0) < 0.01
+
+
+def test_error_stagnates_while_residual_falls():
+    """error to the continuous solution stops decreasing
+    once the residual is small, while the residual keeps falling."""
+    w = W.cfg1(32)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4)
+    o.set_rhs(w.rhs)
+    u = w.rhs / (3.0 * np.pi ** 2)
+    res, err = [], []
+    for _ in range(10):
+        res.append(o.vcycle())
+        err.append(np.linalg.norm(o.phi() - u) / np.linalg.norm(u))
+    assert res[-1] < 1e-6 * res[0]
+    assert res[-1] < 0.05 * res[-3]             # residual still falls ...
+    assert abs(err[-1] - err[-3]) < 1e-5 * err[-1]   # ... error does not
+    assert err[0] > err[-1]
+
+
+# --------------------------------------------------------------------------
+# Galerkin coarsening
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("bc", BC_COMBOS)
+def test_galerkin_equals_dense_RAP_and_closed_form(bc):
+    """A_c = R A P with averaging R, nearest-neighbour P.
+    Dense triple product equals the oracle's coarse stencil exactly, and for
+    box domains A_{l} = 2^{-l} S_l / h^2 with S_l the folded integer stencil
+    of the level's own grid (so alpha = 2 undoes the Galerkin factor)."""
+    bt, bv = bc
+    shape, h = (8, 8, 16), 0.5
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=1)
+    assert o.nlevels == 3
+    A = dense.stencil_to_dense(o.stencil(0))
+    for l in range(o.nlevels - 1):
+        P = dense.injection_P(o.dims(l))
+        Ac = (P.T / 8.0) @ A @ P
+        Ao = dense.stencil_to_dense(o.stencil(l + 1))
+        assert np.array_equal(Ac, Ao)
+        # closed form: the level-(l+1) ghost-cell operator with spacing h,
+        # scaled by 2^{-(l+1)}
+        S = dense.dense_operator(o.dims(l + 1), h, bt)
+        assert np.array_equal(Ao, S * 2.0 ** -(l + 1))
+        A = Ao
+
+
+def test_galerkin_with_mask_matches_dense_RAP():
+    """Masked (solid) cells: P injects only into unknown children (c19)."""
+    shape = (8, 8, 8)
+    rng = np.random.default_rng(5)
+    solid = (rng.uniform(size=shape) < 0.15).astype(np.uint8)
+    o = oracle.Oracle(shape, 1.0, [D] * 6, [0.0] * 6, solid=solid,
+                      min_coarse=1)
+    unk0 = o.unknown(0).astype(bool)
+    assert np.array_equal(unk0, ~solid.astype(bool))
+    A = dense.stencil_to_dense(o.stencil(0))
+    for l in range(o.nlevels - 1):
+        uf = o.unknown(l).astype(bool)
+        P = dense.injection_P(o.dims(l), unknown_fine=uf)
+        Ac = (P.T / 8.0) @ A @ P
+        Ao = dense.stencil_to_dense(o.stencil(l + 1))
+        assert np.allclose(Ac, Ao, rtol=0, atol=1e-14)
+        uc = o.unknown(l + 1).astype(bool).reshape(-1)
+        assert np.array_equal(uc, P.sum(axis=0) > 0)
+        A = Ao
+
+
+def test_identity_stencil_stays_identity():
+    """R I P = I (average of 8 injections)."""
+    P = dense.injection_P((4, 4, 4))
+    assert np.array_equal((P.T / 8.0) @ np.eye(64) @ P, np.eye(8))
+
+
+# --------------------------------------------------------------------------
+# Transfers, smoother, CG
+# --------------------------------------------------------------------------
+def test_restriction_average_of_children():
+    """children 1..8 -> 4.5 (averaging restriction)."""
+    o = oracle.Oracle((4, 4, 4), 1.0, [D] * 6, [0.0] * 6, min_coarse=1)
+    assert o.dims(1) == (2, 2, 2)
+    f = np.zeros((4, 4, 4))
+    f[:2, :2, :2] = np.arange(1, 9, dtype=float).reshape(2, 2, 2)
+    o.set_rhs_raw(f)
+    o.set_phi(np.zeros((4, 4, 4)))
+    o.restrict_residual(0)
+    assert o.rhs(1)[0, 0, 0] == 4.5
+    # a constant residual restricts to itself
+    o.set_rhs_raw(np.full((4, 4, 4), 0.3))
+    o.restrict_residual(0)
+    assert np.all(o.rhs(1) == 0.3)
+
+
+def test_prolongation_magnified():
+    """alpha = 2, parent 0.5 -> all 8 children += 1.0."""
+    o = oracle.Oracle((4, 4, 4), 1.0, [D] * 6, [0.0] * 6, min_coarse=1)
+    o.set_phi(np.zeros((4, 4, 4)))
+    e = np.zeros((2, 2, 2))
+    e[1, 0, 1] = 0.5
+    o.set_phi(e, 1)
+    o.prolong_correct(0, 2.0)
+    p = o.phi()
+    assert np.all(p[2:4, 0:2, 2:4] == 1.0)
+    assert p.sum() == 8.0
+
+
+def test_smoother_fixed_point_and_one_cell():
+    """the exact discrete solution is a fixed point of a
+    half-sweep (to rounding); a 1-cell problem a phi = f is solved by one."""
+    shape, h = (8, 8, 8), 1.0 / 8
+    bt, bv = BC_COMBOS[3]
+    f = np.random.default_rng(2).uniform(-1, 1, shape)
+    A = dense.dense_operator(shape, h, bt)
+    u = np.linalg.solve(A, (f + dense.bc_rhs_shift(shape, h, bt, bv)).reshape(-1))
+    u = u.reshape(shape)
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    o.set_rhs(f)
+    o.set_phi(u)
+    o.smooth_half(0, 0)
+    o.smooth_half(0, 1)
+    assert np.abs(o.phi() - u).max() < 1e-13 * np.abs(u).max()
+    one = oracle.Oracle((1, 1, 1), 1.0, [D] * 6, [0.0] * 6)
+    one.set_rhs(np.array([[[3.0]]]))
+    one.smooth_half(0, 0)
+    assert one.phi()[0, 0, 0] == 3.0 / 12.0
+
+
+def test_rbgs_half_sweep_matches_dense_splitting():
+    """One red and one black half-sweep equal the dense colour-block
+    update x_C <- D_C^{-1}(b_C - A_{C,C'} x_C') of the ghost-cell operator."""
+    shape, h = (6, 4, 8), 1.0
+    bt, bv = BC_COMBOS[3]
+    rng = np.random.default_rng(9)
+    f = rng.uniform(-1, 1, shape)
+    x0 = rng.uniform(-1, 1, shape)
+    A = dense.dense_operator(shape, h, bt)
+    b = (f + dense.bc_rhs_shift(shape, h, bt, bv)).reshape(-1)
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=100)
+    o.set_rhs(f)
+    o.set_phi(x0)
+    x = x0.reshape(-1).copy()
+    i, j, k = np.meshgrid(*[np.arange(s) for s in shape], indexing="ij")
+    col = ((i + j + k) & 1).reshape(-1)
+    for c in (0, 1):
+        o.smooth_half(0, c)
+        Dg = np.diag(A)
+        off = A @ x - Dg * x
+        xn = (b - off) / Dg
+        x = np.where(col == c, xn, x)
+        assert np.allclose(o.phi().reshape(-1), x, rtol=1e-14, atol=1e-14)
+
+
+def test_cg_two_by_two_and_zero_rhs():
+    """SPD 2x2 solved in <= 2 iterations; b = 0 -> 0 its."""
+    o = oracle.Oracle((2, 1, 1), 1.0, [D, D, N, N, N, N], [0.0] * 6)
+    assert o.nlevels == 1
+    st = o.stencil(0)
+    assert st[0, 0, 0, 0] == 3.0 and st[0, 0, 0, 2] == -1.0
+    o.set_rhs(np.array([1.0, 2.0]).reshape(2, 1, 1))
+    it = o.cg(0, 1e-14, 100)
+    assert it <= 2
+    x = np.linalg.solve(np.array([[3.0, -1.0], [-1.0, 3.0]]), [1.0, 2.0])
+    assert np.allclose(o.phi().reshape(-1), x, rtol=1e-15, atol=1e-15)
+    o.set_rhs(np.zeros((2, 1, 1)))
+    assert o.cg(0, 1e-14, 100) == 0
+    assert np.all(o.phi() == 0.0)
+
+
+# --------------------------------------------------------------------------
+# Whole V-cycle against the dense iteration matrix
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("shape,mc,bc", [
+    ((8, 8, 8), 4, BC_COMBOS[0]),
+    ((8, 8, 8), 4, BC_COMBOS[2]),
+    ((16, 8, 8), 2, BC_COMBOS[3]),
+])
+def test_vcycle_equals_dense_iteration_matrix(shape, mc, bc):
+    """V(2,2) with alpha = 2: for f = 0 and homogeneous BCs one
+    oracle V-cycle maps phi to M phi, M = post (I - a P B_c R A) pre built
+    from dense matrices.  Pins smoother order, R, P, alpha and recursion."""
+    bt = bc[0]
+    h = 1.0
+    o = oracle.Oracle(shape, h, bt, [0.0] * 6, min_coarse=mc,
+                      coarse_tol=1e-15, coarse_maxit=2000)
+    shapes = [o.dims(l) for l in range(o.nlevels)]
+    M, _ = dense.vcycle_matrices(shapes, h, bt, 2, 2, 2.0)
+    rng = np.random.default_rng(11)
+    x = rng.uniform(-1, 1, shape)
+    o.set_rhs(np.zeros(shape))
+    o.set_phi(x)
+    o.vcycle()
+    y = M @ x.reshape(-1)
+    assert np.linalg.norm(o.phi().reshape(-1) - y) <= 1e-12 * np.linalg.norm(y)
+
+
+def test_asymptotic_factor_equals_spectral_radius():
+    """The oracle's asymptotic per-cycle residual factor (f = 0, power
+    iteration) equals the spectral radius of the dense V(2,2) matrix."""
+    shape = (8, 8, 8)
+    bt = [D] * 6
+    o = oracle.Oracle(shape, 1.0, bt, [0.0] * 6, min_coarse=4,
+                      coarse_tol=1e-15, coarse_maxit=2000)
+    M, _ = dense.vcycle_matrices([o.dims(l) for l in range(o.nlevels)], 1.0,
+                                 bt, 2, 2, 2.0)
+    rho = np.abs(np.linalg.eigvals(M)).max()
+    o.set_rhs(np.zeros(shape))
+    o.set_phi(np.random.default_rng(0).uniform(-1, 1, shape))
+    r = [o.residual_norm()]
+    for _ in range(40):
+        r.append(o.vcycle())
+    fac = r[-1] / r[-2]
+    assert abs(fac - rho) < 1e-4 * rho
+    assert 0.03 < rho < 0.06
+
+
+def test_vcycle_schedules_convergence():
+    """V(1,1) 'do not converge reliably', more smoothing converges
+    fast.  Asymptotic factors on a channel: V(1,1) >> V(2,2) > V(3,3)."""
+    shape = (128, 32, 32)
+    bt, bv = W.channel_bc(0.0)
+    fac = {}
+    for nu in (1, 2, 3):
+        o = oracle.Oracle(shape, 1.0, bt, bv, min_coarse=2, nu1=nu, nu2=nu)
+        o.set_rhs(np.zeros(shape))
+        o.set_phi(np.random.default_rng(0).uniform(-1, 1, shape))
+        r = [o.residual_norm()]
+        for _ in range(12):
+            r.append(o.vcycle())
+        fac[nu] = (r[-1] / r[-5]) ** 0.25
+    assert fac[1] > 0.6
+    assert fac[2] < 0.25
+    assert fac[3] < fac[2]
+
+
+# --------------------------------------------------------------------------
+# Sphere RHS
+# --------------------------------------------------------------------------
+@pytest.mark.parametrize("row", read_golden("table1_erV.txt"))
+def test_table1_volume_mapping_error(row):
+    """Table 1 e_rV row reproduced by the centre rule."""
+    R, erv = float(row[0]), float(row[1])
+    n = oracle.sphere_cell_count((64, 64, 64), 1.0, (32.0, 32.0, 32.0), R)
+    V = 4.0 / 3.0 * math.pi * R ** 3
+    assert round(100.0 * (n - V) / V, 2) == erv
+
+
+def test_sphere_925_cells():
+    row = read_golden("sphere_925.txt")[0]
+    box, cx, cy, cz, R, cells = row
+    n = oracle.sphere_cell_count((int(box),) * 3, 1.0,
+                                 (float(cx), float(cy), float(cz)), float(R))
+    assert n == int(cells)
+
+
+def test_sphere_charge_conservation_and_per_volume():
+    """PER_CELLS spreads exactly Q over the covered cells; PER_VOLUME is the
+    paper's naive Q/V_sphere."""
+    shape = (48, 32, 40)
+    c, q = W.random_spheres(shape, 4.0, 20, seed=4)
+    R = np.full(20, 4.0)
+    rho = oracle.sphere_density(shape, 1.0, c, R, q)
+    assert abs(rho.sum() - q.sum()) < 1e-12
+    rv = oracle.sphere_density(shape, 1.0, c, R, q, oracle.PER_VOLUME)
+    V = 4.0 / 3.0 * math.pi * 64.0
+    nz = rv[rv != 0]
+    assert np.allclose(np.abs(nz), 1.0 / V, rtol=1e-15)
+    h = 0.25  # scaling: same sphere in physical units
+    rho_h = oracle.sphere_density(shape, h, c * h, R * h, q)
+    assert abs(rho_h.sum() * h ** 3 - q.sum()) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# Whole-solve properties
+# --------------------------------------------------------------------------
+def test_zero_rhs_gives_zero():
+    """zero RHS, zero BCs, zero initial guess -> 0."""
+    o = oracle.Oracle((16, 8, 8), 1.0, [D] * 6, [0.0] * 6, min_coarse=2)
+    o.set_rhs(np.zeros((16, 8, 8)))
+    st, cyc, hist = o.solve(1e-8, 5)
+    assert st == 0 and cyc == 0
+    assert np.all(o.phi() == 0.0)
+
+
+def test_power_of_two_scaling_is_bitwise():
+    """Linearity: f -> 2f gives phi -> 2 phi bitwise (exact scaling by 2 in
+    every step, CG included)."""
+    shape = (32, 16, 16)
+    f = np.random.default_rng(3).uniform(-1, 1, shape)
+    out = []
+    for s in (1.0, 2.0):
+        o = oracle.Oracle(shape, 1.0 / 16, [D] * 6, [0.0] * 6, min_coarse=2)
+        o.set_rhs(s * f)
+        for _ in range(3):
+            o.vcycle()
+        out.append(o.phi())
+    assert np.array_equal(out[1], 2.0 * out[0])
+
+
+def test_hierarchy_rule():
+    """P:502-507 (c9): coarsen while dims even, coarse dims even, min > m_c."""
+    cases = [((32, 32, 32), 4, [(32, 32, 32), (16, 16, 16), (8, 8, 8), (4, 4, 4)]),
+             ((256, 64, 64), 4, [(256, 64, 64), (128, 32, 32), (64, 16, 16),
+                                 (32, 8, 8), (16, 4, 4)]),
+             ((64, 64, 64), 8, [(64, 64, 64), (32, 32, 32), (16, 16, 16), (8, 8, 8)]),
+             ((24, 24, 24), 2, [(24, 24, 24), (12, 12, 12), (6, 6, 6)]),
+             ((5, 4, 4), 1, [(5, 4, 4)])]
+    for shape, mc, expect in cases:
+        o = oracle.Oracle(shape, 1.0, [D] * 6, [0.0] * 6, min_coarse=mc)
+        assert [o.dims(l) for l in range(o.nlevels)] == expect
