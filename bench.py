@@ -1,0 +1,371 @@
+"""bench.py -- V-cycle throughput of the B200 cell-centered multigrid solver.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl cuda|reference]
+                    [--workload cfg3|cfg4] [--size n]
+
+A "step" is one V(2,2)-cycle of the whole hot path on the resident hierarchy
+(smoothing, residual+restriction, coarse CG, prolongation, residual norm and
+its readback), launched through the C-ABI (mg_vcycle).  Workloads:
+  N = 1: BASELINE config 3 -- 512^3, h = 1/512, homogeneous Dirichlet,
+         f ~ U[-1,1] (seeded), V(2,2) to 8^3.
+  N > 1: config 4 weak scaling -- (512 N) x 512 x 512, channel BCs, charged
+         spheres R = 6 at 5 % volume, slabs of 512 planes per GPU.
+value = global cells x K / max-over-ranks device time (Mcells/s).
+e2e   = the same metric for a full config-3 solve (20 cycles) through the
+        public API with host buffers: H2D of f from pinned memory, 20 cycles,
+        D2H of Phi, all inside the timed region.
+--impl reference times the CPU oracle (oracle/, plain C fp64) on a bounded
+sample of the same workload on the host cores (the tier's reference arm).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MG V-cycle throughput (Mcells/s, fp64) and achieved HBM GB/s vs peak, 1/2/4/8 GPU"
+UNIT = "Mcells/s"
+HALF_SWEEP_BYTES_PER_CELL = 12  # other-colour Phi 4 + own f 4 + own Phi 4
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# --------------------------------------------------------------------------
+# clocks sampled during the timed region
+# --------------------------------------------------------------------------
+REASON_BITS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting",
+               0x4: "sw_power_cap", 0x8: "hw_slowdown", 0x10: "sync_boost",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+
+class ClockSampler:
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index),
+                 "--query-gpu=clocks.sm,clocks.max.sm,clocks_event_reasons.active",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        for ln in self.lines:
+            try:
+                a, b, c = [x.strip() for x in ln.split(",")]
+                sm.append(float(a))
+                mx.append(float(b))
+                bits = int(c, 16)
+                for k, v in REASON_BITS.items():
+                    if bits & k and v != "gpu_idle":
+                        reasons.add(v)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(n_sample=256, cycles=2):
+    """The oracle as it stands on a bounded sample of the config-3 recipe:
+    n_sample^3 cells, V(2,2) to 8^3, one warm-up cycle then `cycles` timed."""
+    import oracle
+    from paper_1410_6609_b200 import workloads as W
+    w = W.cfg3(n_sample, seed=0)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
+    o.set_rhs(w.rhs)
+    o.vcycle()
+    t0 = time.perf_counter()
+    for _ in range(cycles):
+        o.vcycle()
+    dt = time.perf_counter() - t0
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": round(w.cells * cycles / dt / 1e6, 3), "unit": UNIT,
+            "cores": cores, "kind": "oracle",
+            "sample": "config-3 recipe at %d^3 (h=1/%d, U[-1,1], V(2,2) to 8^3), "
+                      "1 warm-up + %d timed V-cycles incl. residual norm, "
+                      "OpenMP threads=%d" % (n_sample, n_sample, cycles, cores)}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    from paper_1410_6609_b200 import workloads as W
+    oracle.build()
+    n = args.ref_size
+    w = W.cfg3(n, seed=0)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
+    o.set_rhs(w.rhs)
+    for _ in range(args.warmup):
+        o.vcycle()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        o.vcycle()
+    dt = time.perf_counter() - t0
+    val = w.cells * args.steps / dt / 1e6
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    full = args.size ** 3 * max(args.gpus, 1)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": round(val, 3),
+        "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(dt / args.steps * 1e3, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f64", "data": "synthetic",
+        "config": {"workload": "cfg3 recipe, CPU oracle sample %d^3 of the %d-cell workload"
+                               % (n, full),
+                   "schedule": "V(2,2)", "levels": o.nlevels},
+        "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": cores,
+                         "kind": "oracle",
+                         "sample": "%d^3 cells per step (one V(2,2)-cycle incl. norm)" % n},
+        "e2e": {"value": round(val, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_cuda(args):
+    import torch
+    ws, rank, local = dist_env()
+    N = args.gpus
+    if ws != N:
+        raise SystemExit("--gpus %d but WORLD_SIZE=%d" % (N, ws))
+    torch.cuda.set_device(local)
+    dist = None
+    if N > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1410_6609_b200 import _build
+    if rank == 0 or N == 1:
+        _build.build()
+    if dist is not None:
+        dist.barrier()
+    from paper_1410_6609_b200 import mg
+    from paper_1410_6609_b200 import workloads as W
+
+    n = args.size
+    workload = args.workload or ("cfg3" if N == 1 else "cfg4")
+    kw = dict(min_coarse=8, nu1=2, nu2=2)
+    if N > 1:
+        uid = [mg.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        kw.update(nranks=N, rank=rank, halo="nccl", nccl_id=uid[0])
+    stream = torch.cuda.Stream(device=local)
+    if workload == "cfg3":
+        assert N == 1, "cfg3 is the single-GPU configuration"
+        w = W.cfg3(n, seed=0, with_rhs=False)
+        shape = w.shape
+        s = mg.Multigrid(shape, w.h, w.bc_type, w.bc_value, device=local,
+                         stream=stream, **kw)
+        rhs_host = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        rhs_host.numpy()[...] = W.uniform_rhs(shape, 0)
+        s.set_rhs(rhs_host)
+        wl = "cfg3: %d^3, h=1/%d, homogeneous Dirichlet, f~U[-1,1] seed 0" % (n, n)
+    else:
+        w = W.cfg4(P=N, n=n, seed=0)
+        shape = w.shape
+        s = mg.Multigrid(shape, w.h, w.bc_type, w.bc_value, device=local,
+                         stream=stream, **kw)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        rhs_host = None
+        wl = ("cfg4: (%d*%d)x%dx%d weak scaling, channel BCs, %d spheres R=6 (5%%)"
+              % (n, N, n, n, len(w.radii)))
+    cells = int(np.prod(shape))
+    L = s.nlevels
+
+    # ---- warm-up (includes graph capture) ----
+    for _ in range(args.warmup):
+        s.vcycle()
+    # ---- timed region: K V-cycles, barrier + sync on both sides ----
+    clocks = ClockSampler(local)
+    clocks.start()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    norms = []
+    for _ in range(args.steps):
+        norms.append(s.vcycle())
+    e1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ms = e0.elapsed_time(e1)
+    ck = clocks.stop()
+    if dist is not None:
+        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    launches = s.cycle_launches
+
+    # ---- roofline of the dominant kernel (level-0 RBGS half-sweep), live ----
+    s.set_profiling(True)
+    prof = []
+    for _ in range(max(3, min(args.steps, 10))):
+        s.vcycle()
+        prof.append(s.last_cycle_times())
+    s.set_profiling(False)
+    sm0 = np.mean([p["smooth0_ms"] for p in prof])
+    nsm = prof[0]["smooth0_launches"]
+    cyc_prof = np.mean([p["cycle_ms"] for p in prof])
+    per_launch_ms = sm0 / nsm
+    local_cells = cells // N
+    alg_bytes = HALF_SWEEP_BYTES_PER_CELL * local_cells
+    achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
+    peak, peak_src = peaks()
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "roofline_traffic.json")
+    if os.path.exists(tf):
+        try:
+            tj = json.load(open(tf))
+            if tj.get("cells") == local_cells:
+                traffic = tj.get("bytes_per_launch")
+        except Exception:
+            traffic = None
+    # whole-cycle model roofline (SURVEY 8(d) byte model)
+    model_bytes = 0.0
+    for l in range(L - 1):
+        frac = 8.0 ** -l
+        model_bytes += (24 * (2 + 2) + 34) * frac
+    model_bytes += 16
+    cycle_ms = ms / args.steps
+    cycle_frac = model_bytes * local_cells / (cycle_ms * 1e-3) / 1e9 / peak
+
+    # ---- e2e: full config-3 solve through the public API, host buffers ----
+    e2e = None
+    if workload == "cfg3" and not args.no_e2e:
+        out_host = torch.empty(shape, dtype=torch.float64, pin_memory=True)
+        ncyc = 20
+        times = []
+        for rep in range(2):
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            s.zero_solution()
+            s.set_rhs(rhs_host)
+            for _ in range(ncyc):
+                s.vcycle()
+            s.get_solution(out_host)
+            b.record(stream)
+            torch.cuda.synchronize()
+            times.append(a.elapsed_time(b) * 1e-3)
+        dt = min(times)
+        e2e = {"value": round(cells * ncyc / dt / 1e6, 2), "unit": UNIT,
+               "h2d_bytes_per_step": cells * 8, "d2h_bytes_per_step": cells * 8,
+               "step": "one config-3 solve: H2D f (pinned) + %d V(2,2)-cycles + D2H Phi"
+                       % ncyc,
+               "ms_per_step": round(dt * 1e3, 2)}
+
+    line = {
+        "metric": METRIC,
+        "value": round(cells * args.steps / (ms * 1e-3) / 1e6, 2),
+        "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(cycle_ms, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": wl, "global_cells": cells, "levels": L,
+                   "schedule": "V(2,2), RBGS red-black, alpha=2, CG coarsest",
+                   "parallelism": "x-slab x%d (NCCL halo)" % N if N > 1 else "single GPU",
+                   "l2": "inputs larger than L2 (hierarchy %.2f GB vs 126 MB L2); no flush"
+                         % (mg.workspace_bytes(shape, min_coarse=8) / 1e9 / N)},
+        "roofline": {"bound": "hbm", "kernel": "k_smooth (level-0 RBGS half-sweep)",
+                     "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                     "frac": round(achieved / peak, 4), "traffic": traffic,
+                     "alg_bytes_per_launch": alg_bytes,
+                     "avg_launch_ms": round(per_launch_ms, 5),
+                     "share_of_cycle": round(sm0 / cyc_prof, 4),
+                     "peak_source": peak_src,
+                     "cycle_model_frac": round(cycle_frac, 4),
+                     "breakdown_ms": {k: round(float(np.mean([p[k] for p in prof])), 4)
+                                      for k in prof[0]},
+                     "cycle_model_bytes_per_cell": round(model_bytes, 2)},
+        "gpu_launches": int(launches * args.steps),
+        "clocks": ck,
+        "e2e": e2e,
+        "final_residual": norms[-1] if norms else None,
+    }
+    if rank == 0 and N == 1 and not args.no_cpu:
+        try:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_size)
+        except Exception as ex:  # reported, never fatal
+            line["cpu_baseline"] = {"error": repr(ex)}
+    s.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
+    ap.add_argument("--workload", default=None, choices=[None, "cfg3", "cfg4"])
+    ap.add_argument("--size", type=int, default=512)
+    ap.add_argument("--cpu-size", type=int, default=256)
+    ap.add_argument("--ref-size", type=int, default=128)
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_cuda(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,221 @@
+/*
+ * include/mg.h -- C-ABI of the B200-native cell-centered multigrid Poisson
+ * solver (libmg_cuda.so), after Bartuschat & Ruede, arXiv 1410.6609.
+ * Citations "P:<line>" refer to the paper's LaTeX source.
+ *
+ * What is solved (Eq.12; Eq.13):
+ *     A Phi = f,   A = -Lap_h (7-point finite-volume stencil, spacing h),
+ * on a box of nx*ny*nz cells, unknowns at cell centres, eps = 1, with
+ * Dirichlet / Neumann conditions on each face folded into the stencil and the
+ * right-hand side.  The solver is the paper's cell-centered
+ * geometric multigrid: red-black Gauss-Seidel
+ * smoothing, residual + 8-cell averaging restriction, nearest-neighbour
+ * prolongation with the coarse correction magnified by alpha = 2, Galerkin
+ * coarse operators, CG on the coarsest grid, V(nu1,nu2)-cycles.
+ *
+ * Conventions
+ *  - Arrays exchanged with the caller are fp64 in natural C order with x the
+ *    slowest and z the fastest axis: a[(i*ny + j)*nz + k].  Cell (i,j,k) has
+ *    its centre at ((i+1/2)h, (j+1/2)h, (k+1/2)h).
+ *  - Face order: 0 x-, 1 x+, 2 y-, 3 y+, 4 z-, 5 z+.
+ *  - Every int return is MG_OK (0) or a negative MG_ERR_* code; the message
+ *    of the last error is returned by mg_last_error().
+ *  - A context is not thread-safe.  All device work is enqueued on the
+ *    context's stream; calls that return host values synchronise it.
+ *  - Multi-GPU (nranks > 1, halo backend NCCL): every call is collective, all
+ *    ranks call in the same order.  Rank r owns the x-planes
+ *    [r*nx/P, (r+1)*nx/P) of every distributed level; caller arrays are then
+ *    the rank's slab (nx/P * ny * nz values).  With the LOOPBACK backend one
+ *    process holds all P slabs on one GPU (used to test the decomposition)
+ *    and caller arrays cover the whole domain.
+ *  - Pointers marked "where" are host pointers (MG_HOST, any host memory;
+ *    pinned memory gives full PCIe bandwidth) or device pointers (MG_DEVICE).
+ *    The library never keeps or frees caller pointers.
+ */
+#ifndef MG_H
+#define MG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- return codes ------------------------------------------------------ */
+#define MG_OK 0
+#define MG_ERR_ARG (-1)      /* invalid argument                              */
+#define MG_ERR_BC (-2)       /* unsupported / singular boundary conditions    */
+#define MG_ERR_COARSEN (-3)  /* dimensions cannot form the required hierarchy */
+#define MG_ERR_CUDA (-4)     /* CUDA runtime error (or no device)             */
+#define MG_ERR_NCCL (-5)     /* NCCL missing or failed                        */
+#define MG_ERR_NOMEM (-6)    /* device memory / workspace too small           */
+#define MG_ERR_DIVERGED (-7) /* NaN, or residual grew > 10x in one cycle      */
+#define MG_ERR_NOTCONV (-8)  /* max_cycles reached (solution stays valid)     */
+
+/* ---- boundary conditions ------------------------------------ */
+#define MG_DIRICHLET 0 /* Phi = value on the face:   centre +1, f += 2 g/h^2  */
+#define MG_NEUMANN 1   /* dPhi/dn = value (outward): centre -1, f += g/h      */
+#define MG_PERIODIC 2  /* P:441-443; reserved, rejected with MG_ERR_BC        */
+
+typedef struct {
+  int type;     /* MG_DIRICHLET or MG_NEUMANN                             */
+  double value; /* g_d (potential) or g_n (outward normal derivative)     */
+} mg_bc;
+
+#define MG_HOST 0
+#define MG_DEVICE 1
+
+#define MG_CHARGE_PER_CELLS 0  /* rho = Q/(n_p h^3): charge exact (default)    */
+#define MG_CHARGE_PER_VOLUME 1 /* rho = Q/(4/3 pi R^3): the paper's P:481-482  */
+
+#define MG_FIELD_PHI 0 /* solution / coarse-grid correction of a level        */
+#define MG_FIELD_RHS 1 /* right-hand side of a level (level 0: BC-adapted)    */
+
+#define MG_HALO_NONE 0     /* single slab (nranks must be 1)                  */
+#define MG_HALO_NCCL 1     /* one process per GPU, NCCL send/recv over NVLink */
+#define MG_HALO_LOOPBACK 2 /* all nranks slabs in this process on one GPU     */
+
+typedef struct {
+  int nu1, nu2;       /* pre/post RBGS sweeps (default 2, 2)      */
+  double alpha;       /* coarse-correction magnification (default 2.0) */
+  int min_coarse;     /* stop coarsening when min dim <= this (default 4)    */
+  int max_levels;     /* 0 = as many as the coarsening rule allows           */
+  long long agglomerate_below; /* local cells/GPU below which the remaining
+                                  levels are gathered (default 64^3)         */
+  double coarse_tol;  /* CG relative tolerance (default 1e-12)               */
+  int coarse_maxit;   /* CG iteration cap (default 1000)                     */
+  int max_cycles;     /* mg_solve cycle cap (default 100)                    */
+  int device;         /* CUDA device ordinal (default 0)                     */
+  void *stream;       /* cudaStream_t to enqueue on; NULL = own stream       */
+  int rank, nranks;   /* this process's rank / number of slabs (default 0,1) */
+  int halo_backend;   /* MG_HALO_* (default NONE)                            */
+  unsigned char nccl_id[128]; /* ncclUniqueId from mg_nccl_unique_id (rank 0) */
+  void *workspace;    /* optional caller-owned device memory (e.g. a torch
+                         uint8 tensor) of >= mg_workspace_bytes(); NULL = the
+                         library allocates and frees its own                 */
+  size_t workspace_bytes;
+  int use_graph;      /* capture one V-cycle as a CUDA graph (default 1)     */
+} mg_opts;
+
+typedef struct mg_ctx mg_ctx;
+
+/* Fill *o with the defaults listed above. */
+void mg_default_opts(mg_opts *o);
+
+/* Level plan for (nx,ny,nz,o) without touching a GPU.  Levels follow P:502-507
+ * (reading c9): coarsen while every dimension is even, the coarse dimensions
+ * are again even and min(dims) > min_coarse.  Fills dims[l][3] (global),
+ * local_nx[l] (planes per rank, 0 on levels held whole), *nlevels and
+ * *agg_level (first level held whole on every rank; nlevels when nranks==1
+ * means "no agglomeration").  Arrays must hold 32 entries.  Returns MG_OK or
+ * MG_ERR_ARG / MG_ERR_COARSEN. */
+int mg_plan(int nx, int ny, int nz, const mg_opts *o, int *nlevels,
+            int *agg_level, int dims[][3], int *local_nx);
+
+/* Device bytes the context needs for (nx,ny,nz,o); 0 on invalid arguments. */
+size_t mg_workspace_bytes(int nx, int ny, int nz, const mg_opts *o);
+
+/* Create a solver for nx*ny*nz global cells of spacing h; bc[6] per face.
+ * Requires even nx, ny, nz (the coarsest level is "a multiple of two",
+ * P:506-507) and at least one Dirichlet face (otherwise A is singular).
+ * Returns NULL on error (message in mg_last_error(NULL)). */
+mg_ctx *mg_create(int nx, int ny, int nz, double h, const mg_bc *bc);
+mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
+                     const mg_opts *o);
+/* Frees library-owned device memory, the stream and the NCCL communicator
+ * it created; never the caller's workspace or stream. */
+void mg_destroy(mg_ctx *ctx);
+
+/* Thread-local message / code of the last failing call (ctx may be NULL);
+ * mg_last_error_code() gives the MG_ERR_* of a failed mg_create(_ex). */
+const char *mg_last_error(const mg_ctx *ctx);
+int mg_last_error_code(void);
+const char *mg_strerror(int code);
+
+/* Writes a fresh ncclUniqueId (128 bytes) for mg_opts.nccl_id; call on rank
+ * 0 and broadcast (e.g. with torch.distributed).  MG_ERR_NCCL if libnccl
+ * cannot be loaded.  Needs no GPU. */
+int mg_nccl_unique_id(unsigned char out[128]);
+
+/* ---- right-hand side ----------------------------------------------------- */
+/* f := charge density of n uniformly charged spheres: every cell
+ * whose centre satisfies |x_c - c_p|^2 <= R_p^2 (inclusive, reading
+ * c13) receives rho_p = Q_p/(n_p h^3) (MG_CHARGE_PER_CELLS, n_p = number of
+ * such cells in the whole domain) or Q_p/(4/3 pi R_p^3) (PER_VOLUME); cells
+ * covered by several spheres receive the sum.  Then the finest-grid BC
+ * adaptation.  centers[3n] (x,y,z physical), radii[n],
+ * charges[n] are host arrays, read before return; every rank passes the full
+ * list.  subsample must be 1 (s_f > 1 is not implemented: MG_ERR_ARG).
+ * Errors: n < 0, R <= 0, a sphere that covers no cell centre with
+ * PER_CELLS (MG_ERR_ARG).  Phi is not touched (warm start). */
+int mg_set_rhs_from_spheres(mg_ctx *ctx, int n, const double *centers,
+                            const double *radii, const double *charges,
+                            int normalization, int subsample);
+
+/* f := given field (natural layout, the rank's slab), then the BC
+ * adaptation: f += 2 g_d/h^2 per Dirichlet face and f += g_n/h per Neumann
+ * face the cell touches, in face order. */
+int mg_set_rhs(mg_ctx *ctx, const double *f, int where);
+
+/* ---- solve --------------------------------------------------------------- */
+/* One V(nu1,nu2)-cycle; *res_norm_out (may be NULL) = ||f - A Phi||_2 over
+ * all cells after the cycle (unscaled, reading c10).  Synchronises.
+ * MG_ERR_DIVERGED if the norm is NaN or > 10x the previous cycle's. */
+int mg_vcycle(mg_ctx *ctx, double *res_norm_out);
+
+/* r0 = norm of the current Phi; V-cycles while r_k > tol*r0 (Alg.1,
+ * P:547-550).  *cycles_out and res_hist[0..cycles] (len max_cycles+1) may be
+ * NULL.  MG_OK, MG_ERR_NOTCONV at max_cycles, or MG_ERR_DIVERGED. */
+int mg_solve(mg_ctx *ctx, double tol, int *cycles_out, double *res_hist);
+
+/* ||f - A Phi||_2 for the current Phi (finest level). */
+int mg_residual_norm(mg_ctx *ctx, double *out);
+
+/* ---- solution I/O -------------------------------------------------------- */
+int mg_get_solution(mg_ctx *ctx, double *out, int where);
+int mg_set_solution(mg_ctx *ctx, const double *in, int where);
+int mg_zero_solution(mg_ctx *ctx);
+
+/* ---- single steps (parity tests and composition) ------------------------- */
+int mg_num_levels(const mg_ctx *ctx);
+/* global dims of level l */
+int mg_level_dims(const mg_ctx *ctx, int level, int dims[3]);
+/* Copy a level's field out / in, natural layout.  Level 0 and distributed
+ * levels: the caller's slab (LOOPBACK: whole domain); levels held whole:
+ * the whole level. */
+int mg_get_field(mg_ctx *ctx, int level, int field, double *out, int where);
+int mg_set_field(mg_ctx *ctx, int level, int field, const double *in,
+                 int where);
+/* One red (color 0: (i+j+k) even in global level indices) or black (1)
+ * half-sweep of RBGS on level l, followed by its ghost exchange.
+ * from_zero != 0 treats the other colour as 0 (first sweep after the coarse
+ * Phi is zeroed). */
+int mg_smooth_half(mg_ctx *ctx, int level, int color, int from_zero);
+/* f_{l+1} := R (f_l - A_l Phi_l), R the 8-child average. */
+int mg_residual_restrict(mg_ctx *ctx, int level);
+/* Phi_l += alpha * P Phi_{l+1}, P nearest-neighbour. */
+int mg_prolong_correct(mg_ctx *ctx, int level);
+/* CG on the coarsest level from 0; *iters may be NULL. */
+int mg_coarse_solve(mg_ctx *ctx, int *iters);
+
+/* ---- measurement ---------------------------------------------------------- */
+/* Enable (1) / disable (0) CUDA-event timing of the V-cycle's kernels on the
+ * context's stream (events are part of the captured graph; re-captures). */
+int mg_set_profiling(mg_ctx *ctx, int on);
+/* Times of the last profiled mg_vcycle, in milliseconds:
+ *   out[0] level-0 RBGS half-sweeps (sum)   out[1] number of them
+ *   out[2] level-0 residual+restriction      out[3] level-0 prolongation
+ *   out[4] residual norm                      out[5] levels >= 1 incl. CG
+ *   out[6] whole cycle (first to last kernel) out[7] kernel launches/cycle
+ * MG_ERR_ARG if profiling was off during the last cycle. */
+int mg_last_cycle_times(mg_ctx *ctx, double out[8]);
+/* Number of kernels one mg_vcycle launches (counted when it is recorded). */
+int mg_cycle_launches(const mg_ctx *ctx);
+/* cudaStream_t of the context (for event timing by the caller). */
+void *mg_stream(const mg_ctx *ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* MG_H */

@@ -1,0 +1,973 @@
+// Host orchestration and C-ABI (include/mg.h) of libmg_cuda.so.
+//
+// One context = this process's part of the multigrid hierarchy:
+//   levels l <  nd : "distributed" -- x-slabs of nx_l/P planes, one per rank
+//                    (NCCL backend: this rank's slab; LOOPBACK: all P slabs)
+//   levels l >= nd : held whole (single grid); with P > 1 every rank holds a
+//                    copy and computes it redundantly (agglomeration by
+//                    in-place all-gather of the restricted RHS, P:746 /
+//                    north_star "agglomerated onto one GPU" -- DESIGN.md).
+// With P == 1, nd = 0: every level is a single grid.
+//
+// The V-cycle is recorded once into a CUDA graph and replayed.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <math.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/mg.h"
+#include "mg_internal.h"
+
+using mg::Grid;
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int g_err_code = 0;
+
+int fail(int code, const char *fmt, ...) {
+  g_err_code = code;
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = std::string(mg_strerror(code)) + ": " + buf;
+  return code;
+}
+
+// ---- NCCL, loaded on demand (no link-time dependency) -----------------------
+struct Nccl {
+  bool tried = false, ok = false;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId *);
+  ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t);
+  ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t,
+                       cudaStream_t);
+  ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t,
+                            ncclComm_t, cudaStream_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  const char *(*GetErrorString)(ncclResult_t);
+};
+Nccl g_nccl;
+
+bool load_nccl() {
+  if (g_nccl.tried) return g_nccl.ok;
+  g_nccl.tried = true;
+  void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+  if (!h) return false;
+#define SYM(name, field)                                             \
+  *(void **)(&g_nccl.field) = dlsym(h, name);                        \
+  if (!g_nccl.field) return false;
+  SYM("ncclGetUniqueId", GetUniqueId);
+  SYM("ncclCommInitRank", CommInitRank);
+  SYM("ncclCommDestroy", CommDestroy);
+  SYM("ncclSend", Send);
+  SYM("ncclRecv", Recv);
+  SYM("ncclAllGather", AllGather);
+  SYM("ncclGroupStart", GroupStart);
+  SYM("ncclGroupEnd", GroupEnd);
+  SYM("ncclGetErrorString", GetErrorString);
+#undef SYM
+  g_nccl.ok = true;
+  return true;
+}
+
+// ---- plan ---------------------------------------------------------------------
+struct Plan {
+  int L = 0, nd = 0, P = 1;
+  int dims[32][3];
+  int nxl[32];
+};
+
+int make_plan(int nx, int ny, int nz, const mg_opts *o, Plan *pl) {
+  if (nx <= 0 || ny <= 0 || nz <= 0)
+    return fail(MG_ERR_ARG, "dimensions must be positive (%d,%d,%d)", nx, ny, nz);
+  if (nx % 2 || ny % 2 || nz % 2)
+    return fail(MG_ERR_COARSEN,
+                "dimensions must be even: the coarsest level is a multiple of "
+                "two (P:506-507); got (%d,%d,%d)", nx, ny, nz);
+  const int P = o->nranks < 1 ? 1 : o->nranks;
+  const int maxl = (o->max_levels <= 0 || o->max_levels > 32) ? 32 : o->max_levels;
+  int d[3] = {nx, ny, nz};
+  pl->L = 0;
+  pl->P = P;
+  while (true) {
+    for (int a = 0; a < 3; a++) pl->dims[pl->L][a] = d[a];
+    pl->L++;
+    if (pl->L >= maxl) break;
+    bool ok = true;
+    for (int a = 0; a < 3; a++)
+      if (d[a] % 2 || (d[a] / 2) % 2) ok = false;
+    int mn = d[0] < d[1] ? d[0] : d[1];
+    if (d[2] < mn) mn = d[2];
+    if (mn <= o->min_coarse) ok = false;
+    if (!ok) break;
+    for (int a = 0; a < 3; a++) d[a] /= 2;
+  }
+  for (int l = 0; l < 32; l++) pl->nxl[l] = 0;
+  if (P == 1) {
+    pl->nd = 0;
+    return MG_OK;
+  }
+  if (nx % P)
+    return fail(MG_ERR_ARG, "nx=%d not divisible by nranks=%d", nx, P);
+  if (pl->L < 2)
+    return fail(MG_ERR_COARSEN, "multi-slab solve needs at least two levels");
+  if ((nx / P) % 2)
+    return fail(MG_ERR_COARSEN, "planes per rank (%d) must be even", nx / P);
+  int nd = 1;
+  for (int l = 1; l < pl->L - 1; l++) {
+    if (pl->dims[l][0] % P) break;
+    const int nxl = pl->dims[l][0] / P;
+    if (nxl % 2) break;
+    const long long cells = (long long)nxl * pl->dims[l][1] * pl->dims[l][2];
+    if (cells < o->agglomerate_below) break;
+    nd = l + 1;
+  }
+  pl->nd = nd;
+  for (int l = 0; l < nd; l++) pl->nxl[l] = pl->dims[l][0] / P;
+  return MG_OK;
+}
+
+int round4(int v) { return (v + 3) & ~3; }
+
+Grid make_grid(const Plan &pl, int l, int slab, double h, const int *dface) {
+  Grid g;
+  memset(&g, 0, sizeof g);
+  g.nx = pl.dims[l][0];
+  g.ny = pl.dims[l][1];
+  g.nz = pl.dims[l][2];
+  if (l < pl.nd) {
+    g.nxl = pl.nxl[l];
+    g.x0 = slab * pl.nxl[l];
+  } else {
+    g.nxl = g.nx;
+    g.x0 = 0;
+  }
+  g.nzh = g.nz / 2;
+  g.pz = round4(g.nzh);
+  g.plane = (long long)(g.ny + 2) * g.pz;
+  g.c = ldexp(1.0 / (h * h), -l);
+  g.w = ldexp(h * h, l);
+  for (int q = 0; q < 6; q++) g.dface[q] = dface[q];
+  return g;
+}
+
+}  // namespace
+
+// ---- context --------------------------------------------------------------------
+struct mg_ctx {
+  Plan pl;
+  double h;
+  mg_bc bc[6];
+  mg_opts o;
+  int P = 1, rank = 0, backend = MG_HALO_NONE;
+  int nslab = 1, slab0 = 0;  // slabs held on distributed levels
+  std::vector<std::vector<Grid>> g;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  char *ws = nullptr;
+  size_t ws_bytes = 0;
+  bool own_ws = false;
+  double *partials = nullptr;  // kNormBlocks per held slab
+  double *normv = nullptr;     // [0] local sum, [1] global sum, [2..2+P) gathered
+  double *cg_scr = nullptr;
+  int *cg_iters = nullptr;
+  double *h_norm = nullptr;    // pinned
+  int *h_iters = nullptr;      // pinned
+  double *stage = nullptr;     // lazily allocated natural-layout staging
+  size_t stage_bytes = 0;
+  double *sph = nullptr;       // lazily allocated sphere list
+  size_t sph_cap = 0;
+  unsigned long long *counts = nullptr;
+  cudaGraphExec_t graph = nullptr;
+  double prev_norm = -1.0;
+  ncclComm_t comm = nullptr;
+  int dev = 0;
+  // measurement: kernel launches per recorded V-cycle, optional event marks
+  int launches = 0;
+  int cycle_launches = 0;
+  bool prof = false, prof_last = false;
+  std::vector<cudaEvent_t> ev;
+  int nev = 0;
+  std::vector<int> mark_cat;  // category of the interval ending at mark i
+};
+
+namespace {
+
+constexpr int kNormBlocks = 148 * 8;
+
+// bump allocation over the workspace; with base == nullptr only sizes
+struct Carver {
+  char *base;
+  size_t off = 0;
+  void *take(size_t bytes) {
+    off = (off + 255) & ~(size_t)255;
+    void *p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+size_t carve(mg_ctx *c, char *base) {
+  Carver cv{base};
+  const int L = c->pl.L;
+  c->g.assign(L, {});
+  int dface[6];
+  for (int q = 0; q < 6; q++) dface[q] = c->bc[q].type == MG_DIRICHLET ? 1 : -1;
+  for (int l = 0; l < L; l++) {
+    const int ns = l < c->pl.nd ? c->nslab : 1;
+    for (int s = 0; s < ns; s++) {
+      Grid gr = make_grid(c->pl, l, l < c->pl.nd ? c->slab0 + s : 0, c->h, dface);
+      const size_t bytes = (size_t)mg::grid_elems(gr) * sizeof(double);
+      gr.phiR = (double *)cv.take(bytes);
+      gr.phiB = (double *)cv.take(bytes);
+      gr.fR = (double *)cv.take(bytes);
+      gr.fB = (double *)cv.take(bytes);
+      c->g[l].push_back(gr);
+    }
+  }
+  c->partials = (double *)cv.take(sizeof(double) * kNormBlocks * (c->nslab + 1));
+  c->normv = (double *)cv.take(sizeof(double) * (2 + c->P));
+  c->cg_scr = (double *)cv.take(sizeof(double) *
+                                mg::coarse_cg_scratch_doubles(c->g[L - 1][0]));
+  c->cg_iters = (int *)cv.take(sizeof(int) * 4);
+  c->counts = (unsigned long long *)cv.take(sizeof(unsigned long long) * 4);
+  return cv.off + 256;
+}
+
+bool ck(cudaError_t e, const char *what) {
+  if (e == cudaSuccess) return true;
+  fail(MG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return false;
+}
+
+#define CK(expr)                               \
+  do {                                         \
+    if (!ck((expr), #expr)) return MG_ERR_CUDA; \
+  } while (0)
+
+int nccl_ck(ncclResult_t r, const char *what) {
+  if (r == ncclSuccess) return MG_OK;
+  return fail(MG_ERR_NCCL, "%s: %s", what, g_nccl.GetErrorString(r));
+}
+
+bool distributed(const mg_ctx *c, int l) { return l < c->pl.nd && c->P > 1; }
+
+// profiling categories (mg_last_cycle_times)
+enum { CAT_NONE = -1, CAT_SMOOTH0 = 0, CAT_RESTRICT0 = 2, CAT_PROLONG0 = 3,
+       CAT_NORM = 4, CAT_COARSE = 5 };
+constexpr int kMaxMarks = 512;
+
+// record an event closing an interval of category `cat` (CAT_NONE opens one)
+void mark(mg_ctx *c, int cat) {
+  if (!c->prof || c->nev >= kMaxMarks) return;
+  // external record: a real event node when the stream is being captured
+  cudaEventRecordWithFlags(c->ev[c->nev], c->stream, cudaEventRecordExternal);
+  c->mark_cat[c->nev] = cat;
+  c->nev++;
+}
+
+const Grid &coarse_of(const mg_ctx *c, int l, int s) {
+  return (l + 1 < c->pl.nd) ? c->g[l + 1][s] : c->g[l + 1][0];
+}
+
+// ghost-plane exchange of one colour array (0 phiR, 1 phiB) on level l
+int halo(mg_ctx *c, int l, int which) {
+  if (!distributed(c, l)) return MG_OK;
+  auto arr = [&](const Grid &g) { return which ? g.phiB : g.phiR; };
+  if (c->backend == MG_HALO_LOOPBACK) {
+    for (int s = 0; s + 1 < c->nslab; s++) {
+      const Grid &a = c->g[l][s], &b = c->g[l][s + 1];
+      const size_t bytes = sizeof(double) * a.plane;
+      CK(cudaMemcpyAsync(arr(b), arr(a) + (long long)a.nxl * a.plane, bytes,
+                         cudaMemcpyDeviceToDevice, c->stream));
+      CK(cudaMemcpyAsync(arr(a) + (long long)(a.nxl + 1) * a.plane,
+                         arr(b) + b.plane, bytes, cudaMemcpyDeviceToDevice,
+                         c->stream));
+    }
+    return MG_OK;
+  }
+  const Grid &g = c->g[l][0];
+  double *A = arr(g);
+  const size_t n = (size_t)g.plane;
+  int rc;
+  if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+  if (c->rank > 0) {
+    g_nccl.Send(A + g.plane, n, ncclDouble, c->rank - 1, c->comm, c->stream);
+    g_nccl.Recv(A, n, ncclDouble, c->rank - 1, c->comm, c->stream);
+  }
+  if (c->rank < c->P - 1) {
+    g_nccl.Send(A + (long long)g.nxl * g.plane, n, ncclDouble, c->rank + 1,
+                c->comm, c->stream);
+    g_nccl.Recv(A + (long long)(g.nxl + 1) * g.plane, n, ncclDouble,
+                c->rank + 1, c->comm, c->stream);
+  }
+  return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(halo)");
+}
+
+int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
+  if (l == 0) mark(c, CAT_NONE);
+  for (const Grid &g : c->g[l]) {
+    mg::launch_smooth(g, color, from_zero, c->stream);
+    c->launches++;
+  }
+  if (l == 0) mark(c, CAT_SMOOTH0);
+  CK(cudaGetLastError());
+  return halo(c, l, color);
+}
+
+// f_{l+1} = R (f_l - A Phi_l); at the agglomeration level every rank then
+// all-gathers the restricted RHS (in place) so that each holds the whole level
+int restrict_level(mg_ctx *c, int l) {
+  if (l == 0) mark(c, CAT_NONE);
+  for (int s = 0; s < (int)c->g[l].size(); s++) {
+    mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), 0, c->stream);
+    c->launches++;
+  }
+  if (l == 0) mark(c, CAT_RESTRICT0);
+  CK(cudaGetLastError());
+  if (l + 1 == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
+    const Grid &G = c->g[l + 1][0];
+    const size_t cnt = (size_t)(G.nx / c->P) * G.plane;
+    int rc;
+    if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+    g_nccl.AllGather(G.fR + G.plane + c->rank * cnt, G.fR + G.plane, cnt,
+                     ncclDouble, c->comm, c->stream);
+    g_nccl.AllGather(G.fB + G.plane + c->rank * cnt, G.fB + G.plane, cnt,
+                     ncclDouble, c->comm, c->stream);
+    if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(agglomerate)"))) return rc;
+  }
+  return MG_OK;
+}
+
+int prolong_level(mg_ctx *c, int l) {
+  if (l == 0) mark(c, CAT_NONE);
+  for (int s = 0; s < (int)c->g[l].size(); s++) {
+    mg::launch_prolong(c->g[l][s], coarse_of(c, l, s), 0, c->o.alpha, c->stream);
+    c->launches++;
+  }
+  if (l == 0) mark(c, CAT_PROLONG0);
+  CK(cudaGetLastError());
+  return halo(c, l, 1);  // the next red half-sweep reads black ghosts
+}
+
+int coarse_solve(mg_ctx *c) {
+  const Grid &g = c->g[c->pl.L - 1][0];
+  mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
+                       c->cg_iters, c->stream);
+  c->launches++;
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+// enqueue ||f - A Phi||^2 of level 0 into c->normv[1] and a copy to h_norm
+int enqueue_norm(mg_ctx *c) {
+  int off = 0;
+  mark(c, CAT_NONE);
+  for (const Grid &g : c->g[0]) {
+    off += mg::launch_norm_partials(g, c->partials + off, c->stream);
+    c->launches++;
+  }
+  mg::launch_sum_ordered(c->partials, off, c->normv, c->stream);
+  c->launches++;
+  CK(cudaGetLastError());
+  if (c->P > 1 && c->backend == MG_HALO_NCCL) {
+    int rc = nccl_ck(g_nccl.AllGather(c->normv, c->normv + 2, 1, ncclDouble,
+                                      c->comm, c->stream),
+                     "ncclAllGather(norm)");
+    if (rc) return rc;
+    mg::launch_sum_ordered(c->normv + 2, c->P, c->normv + 1, c->stream);
+    c->launches++;
+  } else {
+    CK(cudaMemcpyAsync(c->normv + 1, c->normv, sizeof(double),
+                       cudaMemcpyDeviceToDevice, c->stream));
+  }
+  mark(c, CAT_NORM);
+  CK(cudaMemcpyAsync(c->h_norm, c->normv + 1, sizeof(double),
+                     cudaMemcpyDeviceToHost, c->stream));
+  return MG_OK;
+}
+
+int enqueue_vcycle(mg_ctx *c) {
+  const int L = c->pl.L;
+  int rc;
+  c->launches = 0;
+  c->nev = 0;
+  for (int l = 0; l < L - 1; l++) {
+    if (l == 1) mark(c, CAT_NONE);
+    if (c->o.nu1 == 0 && l > 0)
+      for (const Grid &g : c->g[l]) {
+        CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+        CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+      }
+    for (int s = 0; s < c->o.nu1; s++) {
+      if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
+      if ((rc = smooth_half(c, l, 1, 0))) return rc;
+    }
+    if ((rc = restrict_level(c, l))) return rc;
+  }
+  if (L == 1) mark(c, CAT_NONE);
+  if ((rc = coarse_solve(c))) return rc;
+  for (int l = L - 2; l >= 0; l--) {
+    if (l == 0) mark(c, CAT_COARSE);
+    if ((rc = prolong_level(c, l))) return rc;
+    for (int s = 0; s < c->o.nu2; s++) {
+      if ((rc = smooth_half(c, l, 0, 0))) return rc;
+      if ((rc = smooth_half(c, l, 1, 0))) return rc;
+    }
+  }
+  if (L == 1) mark(c, CAT_COARSE);
+  rc = enqueue_norm(c);
+  c->cycle_launches = c->launches;
+  c->prof_last = c->prof;
+  return rc;
+}
+
+int sync(mg_ctx *c) {
+  CK(cudaStreamSynchronize(c->stream));
+  return MG_OK;
+}
+
+// staging buffer for natural-layout host/device transfers of level l
+int stage_for(mg_ctx *c, size_t bytes) {
+  if (c->stage_bytes >= bytes) return MG_OK;
+  if (c->stage) cudaFree(c->stage);
+  c->stage = nullptr;
+  c->stage_bytes = 0;
+  CK(cudaMalloc(&c->stage, bytes));
+  c->stage_bytes = bytes;
+  return MG_OK;
+}
+
+size_t level_cells_held(const mg_ctx *c, int l) {
+  size_t n = 0;
+  for (const Grid &g : c->g[l]) n += (size_t)g.nxl * g.ny * g.nz;
+  return n;
+}
+
+int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in) {
+  if (l < 0 || l >= c->pl.L) return fail(MG_ERR_ARG, "level %d out of range", l);
+  if (field != MG_FIELD_PHI && field != MG_FIELD_RHS)
+    return fail(MG_ERR_ARG, "bad field %d", field);
+  if (!buf) return fail(MG_ERR_ARG, "null pointer");
+  const size_t n = level_cells_held(c, l);
+  double *dev = buf;
+  int rc;
+  if (where == MG_HOST) {
+    if ((rc = stage_for(c, n * sizeof(double)))) return rc;
+    dev = c->stage;
+    if (in)
+      CK(cudaMemcpyAsync(dev, buf, n * sizeof(double), cudaMemcpyHostToDevice,
+                         c->stream));
+  } else if (where != MG_DEVICE) {
+    return fail(MG_ERR_ARG, "bad 'where' %d", where);
+  }
+  size_t off = 0;
+  for (const Grid &g : c->g[l]) {
+    if (in)
+      mg::launch_pack(g, field, dev + off, c->stream);
+    else
+      mg::launch_unpack(g, field, dev + off, c->stream);
+    off += (size_t)g.nxl * g.ny * g.nz;
+  }
+  CK(cudaGetLastError());
+  if (in) {
+    // refresh ghost planes of both colours for a distributed level
+    if (field == MG_FIELD_PHI) {
+      if ((rc = halo(c, l, 0))) return rc;
+      if ((rc = halo(c, l, 1))) return rc;
+    }
+  } else if (where == MG_HOST) {
+    CK(cudaMemcpyAsync(buf, dev, n * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+  }
+  return sync(c);
+}
+
+int bc_adapt(mg_ctx *c) {
+  const double alpha = -1.0 * (1.0 / (c->h * c->h));
+  double terms[6];
+  int types[6];
+  for (int q = 0; q < 6; q++) {
+    const double g = c->bc[q].value;
+    types[q] = c->bc[q].type;
+    terms[q] = c->bc[q].type == MG_DIRICHLET ? 2.0 * alpha * g : alpha * (c->h * g);
+  }
+  for (const Grid &g : c->g[0]) mg::launch_bc_adapt(g, terms, types, c->stream);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+int residual_norm_now(mg_ctx *c, double *out) {
+  int rc = enqueue_norm(c);
+  if (rc) return rc;
+  if ((rc = sync(c))) return rc;
+  *out = sqrt(*c->h_norm);
+  return MG_OK;
+}
+
+}  // namespace
+
+// ==== C-ABI ======================================================================
+extern "C" {
+
+void mg_default_opts(mg_opts *o) {
+  memset(o, 0, sizeof *o);
+  o->nu1 = 2;
+  o->nu2 = 2;
+  o->alpha = 2.0;
+  o->min_coarse = 4;
+  o->max_levels = 0;
+  o->agglomerate_below = 64LL * 64 * 64;
+  o->coarse_tol = 1e-12;
+  o->coarse_maxit = 1000;
+  o->max_cycles = 100;
+  o->device = 0;
+  o->stream = nullptr;
+  o->rank = 0;
+  o->nranks = 1;
+  o->halo_backend = MG_HALO_NONE;
+  o->workspace = nullptr;
+  o->workspace_bytes = 0;
+  o->use_graph = 1;
+}
+
+const char *mg_strerror(int code) {
+  switch (code) {
+    case MG_OK: return "MG_OK";
+    case MG_ERR_ARG: return "MG_ERR_ARG";
+    case MG_ERR_BC: return "MG_ERR_BC";
+    case MG_ERR_COARSEN: return "MG_ERR_COARSEN";
+    case MG_ERR_CUDA: return "MG_ERR_CUDA";
+    case MG_ERR_NCCL: return "MG_ERR_NCCL";
+    case MG_ERR_NOMEM: return "MG_ERR_NOMEM";
+    case MG_ERR_DIVERGED: return "MG_ERR_DIVERGED";
+    case MG_ERR_NOTCONV: return "MG_ERR_NOTCONV";
+    default: return "MG_ERR_UNKNOWN";
+  }
+}
+
+const char *mg_last_error(const mg_ctx *) { return g_err.c_str(); }
+
+int mg_last_error_code(void) { return g_err_code; }
+
+int mg_plan(int nx, int ny, int nz, const mg_opts *o, int *nlevels,
+            int *agg_level, int dims[][3], int *local_nx) {
+  mg_opts d;
+  if (!o) {
+    mg_default_opts(&d);
+    o = &d;
+  }
+  Plan pl;
+  int rc = make_plan(nx, ny, nz, o, &pl);
+  if (rc) return rc;
+  if (nlevels) *nlevels = pl.L;
+  if (agg_level) *agg_level = pl.P > 1 ? pl.nd : pl.L;
+  for (int l = 0; l < pl.L; l++) {
+    if (dims)
+      for (int a = 0; a < 3; a++) dims[l][a] = pl.dims[l][a];
+    if (local_nx) local_nx[l] = pl.nxl[l];
+  }
+  return MG_OK;
+}
+
+static int validate(int nx, int ny, int nz, double h, const mg_bc *bc,
+                    const mg_opts *o) {
+  if (!bc) return fail(MG_ERR_ARG, "bc is NULL");
+  if (!(h > 0.0)) return fail(MG_ERR_ARG, "h must be positive");
+  bool anyD = false;
+  for (int q = 0; q < 6; q++) {
+    if (bc[q].type == MG_PERIODIC)
+      return fail(MG_ERR_BC, "periodic faces are not implemented");
+    if (bc[q].type != MG_DIRICHLET && bc[q].type != MG_NEUMANN)
+      return fail(MG_ERR_BC, "face %d: unknown type %d", q, bc[q].type);
+    anyD = anyD || bc[q].type == MG_DIRICHLET;
+  }
+  if (!anyD)
+    return fail(MG_ERR_BC, "no Dirichlet face: the operator is singular");
+  if (o->nu1 < 0 || o->nu2 < 0 || o->nu1 + o->nu2 < 1)
+    return fail(MG_ERR_ARG, "need nu1, nu2 >= 0 and nu1 + nu2 >= 1");
+  if (o->nranks < 1 || o->rank < 0 || o->rank >= o->nranks)
+    return fail(MG_ERR_ARG, "bad rank %d / nranks %d", o->rank, o->nranks);
+  if (o->nranks > 1 && o->halo_backend != MG_HALO_NCCL &&
+      o->halo_backend != MG_HALO_LOOPBACK)
+    return fail(MG_ERR_ARG, "nranks > 1 needs the NCCL or LOOPBACK backend");
+  (void)nx;
+  (void)ny;
+  (void)nz;
+  return MG_OK;
+}
+
+size_t mg_workspace_bytes(int nx, int ny, int nz, const mg_opts *o) {
+  mg_opts d;
+  if (!o) {
+    mg_default_opts(&d);
+    o = &d;
+  }
+  mg_ctx c;
+  if (make_plan(nx, ny, nz, o, &c.pl)) return 0;
+  c.P = c.pl.P;
+  c.nslab = (o->halo_backend == MG_HALO_LOOPBACK) ? c.P : 1;
+  c.slab0 = (o->halo_backend == MG_HALO_LOOPBACK) ? 0 : o->rank;
+  c.h = 1.0;
+  for (int q = 0; q < 6; q++) c.bc[q].type = MG_DIRICHLET;
+  return carve(&c, nullptr);
+}
+
+int mg_nccl_unique_id(unsigned char out[128]) {
+  if (!out) return fail(MG_ERR_ARG, "null pointer");
+  if (!load_nccl()) return fail(MG_ERR_NCCL, "cannot load libnccl.so.2");
+  ncclUniqueId id;
+  int rc = nccl_ck(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+  if (rc) return rc;
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(out, &id, 128);
+  return MG_OK;
+}
+
+mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
+                     const mg_opts *opts) {
+  mg_opts d;
+  if (!opts) {
+    mg_default_opts(&d);
+    opts = &d;
+  }
+  if (validate(nx, ny, nz, h, bc, opts)) return nullptr;
+  mg_ctx *c = new mg_ctx();
+  c->o = *opts;
+  c->h = h;
+  for (int q = 0; q < 6; q++) c->bc[q] = bc[q];
+  if (make_plan(nx, ny, nz, opts, &c->pl)) {
+    delete c;
+    return nullptr;
+  }
+  c->P = c->pl.P;
+  c->rank = opts->rank;
+  c->backend = c->P > 1 ? opts->halo_backend : MG_HALO_NONE;
+  c->nslab = c->backend == MG_HALO_LOOPBACK ? c->P : 1;
+  c->slab0 = c->backend == MG_HALO_NCCL ? c->rank : 0;
+  c->dev = opts->device;
+  auto bail = [&](cudaError_t e, const char *what) -> mg_ctx * {
+    fail(MG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+    mg_destroy(c);
+    return nullptr;
+  };
+  cudaError_t e = cudaSetDevice(c->dev);
+  if (e != cudaSuccess) return bail(e, "cudaSetDevice");
+  if (opts->stream) {
+    c->stream = (cudaStream_t)opts->stream;
+  } else {
+    e = cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(e, "cudaStreamCreate");
+    c->own_stream = true;
+  }
+  const size_t need = carve(c, nullptr);
+  if (opts->workspace) {
+    if (opts->workspace_bytes < need) {
+      fail(MG_ERR_NOMEM, "workspace of %zu bytes < %zu needed",
+           opts->workspace_bytes, need);
+      mg_destroy(c);
+      return nullptr;
+    }
+    c->ws = (char *)opts->workspace;
+    c->ws_bytes = opts->workspace_bytes;
+  } else {
+    e = cudaMalloc(&c->ws, need);
+    if (e != cudaSuccess) {
+      fail(MG_ERR_NOMEM, "cudaMalloc(%zu): %s", need, cudaGetErrorString(e));
+      mg_destroy(c);
+      return nullptr;
+    }
+    c->own_ws = true;
+    c->ws_bytes = need;
+  }
+  // align the base to 256 bytes
+  char *base = (char *)(((uintptr_t)c->ws + 255) & ~(uintptr_t)255);
+  if ((size_t)(base - c->ws) + need > c->ws_bytes) {
+    fail(MG_ERR_NOMEM, "workspace too small after alignment");
+    mg_destroy(c);
+    return nullptr;
+  }
+  carve(c, base);
+  e = cudaMemsetAsync(base, 0, need - 256, c->stream);
+  if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
+  e = cudaMallocHost(&c->h_norm, sizeof(double) * 2);
+  if (e != cudaSuccess) return bail(e, "cudaMallocHost");
+  e = cudaStreamSynchronize(c->stream);
+  if (e != cudaSuccess) return bail(e, "cudaStreamSynchronize");
+  if (c->backend == MG_HALO_NCCL) {
+    if (!load_nccl()) {
+      fail(MG_ERR_NCCL, "cannot load libnccl.so.2");
+      mg_destroy(c);
+      return nullptr;
+    }
+    ncclUniqueId id;
+    memcpy(&id, opts->nccl_id, sizeof id);
+    if (nccl_ck(g_nccl.CommInitRank(&c->comm, c->P, id, c->rank),
+                "ncclCommInitRank")) {
+      c->comm = nullptr;
+      mg_destroy(c);
+      return nullptr;
+    }
+  }
+  return c;
+}
+
+mg_ctx *mg_create(int nx, int ny, int nz, double h, const mg_bc *bc) {
+  return mg_create_ex(nx, ny, nz, h, bc, nullptr);
+}
+
+void mg_destroy(mg_ctx *c) {
+  if (!c) return;
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  if (c->graph) cudaGraphExecDestroy(c->graph);
+  for (auto &e : c->ev) cudaEventDestroy(e);
+  if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
+  if (c->stage) cudaFree(c->stage);
+  if (c->sph) cudaFree(c->sph);
+  if (c->h_norm) cudaFreeHost(c->h_norm);
+  if (c->own_ws && c->ws) cudaFree(c->ws);
+  if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+int mg_num_levels(const mg_ctx *c) { return c ? c->pl.L : MG_ERR_ARG; }
+
+int mg_level_dims(const mg_ctx *c, int l, int dims[3]) {
+  if (!c || !dims || l < 0 || l >= c->pl.L) return fail(MG_ERR_ARG, "bad level");
+  for (int a = 0; a < 3; a++) dims[a] = c->pl.dims[l][a];
+  return MG_OK;
+}
+
+int mg_set_rhs(mg_ctx *c, const double *f, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  int rc = field_io(c, 0, MG_FIELD_RHS, const_cast<double *>(f), where, true);
+  if (rc) return rc;
+  if ((rc = bc_adapt(c))) return rc;
+  c->prev_norm = -1.0;
+  return sync(c);
+}
+
+int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
+                            const double *radii, const double *charges,
+                            int normalization, int subsample) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (n < 0) return fail(MG_ERR_ARG, "n < 0");
+  if (subsample != 1) return fail(MG_ERR_ARG, "subsample must be 1");
+  if (normalization != MG_CHARGE_PER_CELLS && normalization != MG_CHARGE_PER_VOLUME)
+    return fail(MG_ERR_ARG, "bad normalization");
+  if (n > 0 && (!centers || !radii || !charges)) return fail(MG_ERR_ARG, "null array");
+  std::vector<double> h5(5 * (size_t)n);
+  for (int p = 0; p < n; p++) {
+    if (!(radii[p] > 0.0)) return fail(MG_ERR_ARG, "sphere %d: radius <= 0", p);
+    for (int a = 0; a < 3; a++) h5[5 * (size_t)p + a] = centers[3 * (size_t)p + a];
+    h5[5 * (size_t)p + 3] = radii[p];
+    h5[5 * (size_t)p + 4] = charges[p];
+  }
+  if ((size_t)n > c->sph_cap) {
+    if (c->sph) cudaFree(c->sph);
+    c->sph = nullptr;
+    c->sph_cap = 0;
+    CK(cudaMalloc(&c->sph, sizeof(double) * 5 * (size_t)n + sizeof(unsigned long long) * (size_t)n));
+    c->sph_cap = (size_t)n;
+  }
+  unsigned long long *cnt = (unsigned long long *)(c->sph + 5 * c->sph_cap);
+  for (const Grid &g : c->g[0]) {
+    CK(cudaMemsetAsync(g.fR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+    CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+  }
+  if (n > 0) {
+    CK(cudaMemcpyAsync(c->sph, h5.data(), sizeof(double) * 5 * (size_t)n,
+                       cudaMemcpyHostToDevice, c->stream));
+    for (const Grid &g : c->g[0])
+      mg::launch_spheres(g, c->h, n, c->sph, normalization, cnt, c->stream);
+    CK(cudaGetLastError());
+  }
+  int rc = bc_adapt(c);
+  if (rc) return rc;
+  c->prev_norm = -1.0;
+  if ((rc = sync(c))) return rc;
+  if (normalization == MG_CHARGE_PER_CELLS && n > 0) {
+    std::vector<unsigned long long> hc(n);
+    CK(cudaMemcpy(hc.data(), cnt, sizeof(unsigned long long) * n,
+                  cudaMemcpyDeviceToHost));
+    for (int p = 0; p < n; p++)
+      if (hc[p] == 0) return fail(MG_ERR_ARG, "sphere %d covers no cell centre", p);
+  }
+  return MG_OK;
+}
+
+int mg_vcycle(mg_ctx *c, double *res_norm_out) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  int rc;
+  if (c->o.use_graph) {
+    if (!c->graph) {
+      cudaGraph_t gr;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal));
+      rc = enqueue_vcycle(c);
+      cudaError_t e = cudaStreamEndCapture(c->stream, &gr);
+      if (rc) return rc;
+      CK(e);
+      CK(cudaGraphInstantiate(&c->graph, gr, 0));
+      cudaGraphDestroy(gr);
+    }
+    CK(cudaGraphLaunch(c->graph, c->stream));
+  } else {
+    if ((rc = enqueue_vcycle(c))) return rc;
+  }
+  if ((rc = sync(c))) return rc;
+  const double r = sqrt(*c->h_norm);
+  if (res_norm_out) *res_norm_out = r;
+  const double prev = c->prev_norm;
+  c->prev_norm = r;
+  if (!(r == r) || (prev >= 0.0 && r > 10.0 * prev))
+    return fail(MG_ERR_DIVERGED, "residual %g after %g", r, prev);
+  return MG_OK;
+}
+
+int mg_residual_norm(mg_ctx *c, double *out) {
+  if (!c || !out) return fail(MG_ERR_ARG, "null pointer");
+  return residual_norm_now(c, out);
+}
+
+int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  double r0;
+  int rc = residual_norm_now(c, &r0);
+  if (rc) return rc;
+  if (hist) hist[0] = r0;
+  c->prev_norm = r0;
+  int k = 0;
+  int status = r0 == 0.0 ? MG_OK : MG_ERR_NOTCONV;
+  while (status == MG_ERR_NOTCONV && k < c->o.max_cycles) {
+    double rk;
+    rc = mg_vcycle(c, &rk);
+    k++;
+    if (hist) hist[k] = rk;
+    if (rc) {
+      status = rc;
+      break;
+    }
+    if (rk <= tol * r0) status = MG_OK;
+  }
+  if (cycles_out) *cycles_out = k;
+  if (status == MG_ERR_NOTCONV)
+    fail(MG_ERR_NOTCONV, "not converged after %d cycles", k);
+  return status;
+}
+
+int mg_get_solution(mg_ctx *c, double *out, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  return field_io(c, 0, MG_FIELD_PHI, out, where, false);
+}
+
+int mg_set_solution(mg_ctx *c, const double *in, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  c->prev_norm = -1.0;
+  return field_io(c, 0, MG_FIELD_PHI, const_cast<double *>(in), where, true);
+}
+
+int mg_zero_solution(mg_ctx *c) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  for (const Grid &g : c->g[0]) {
+    CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+    CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+  }
+  c->prev_norm = -1.0;
+  return sync(c);
+}
+
+int mg_get_field(mg_ctx *c, int level, int field, double *out, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  return field_io(c, level, field, out, where, false);
+}
+
+int mg_set_field(mg_ctx *c, int level, int field, const double *in, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  return field_io(c, level, field, const_cast<double *>(in), where, true);
+}
+
+int mg_smooth_half(mg_ctx *c, int level, int color, int from_zero) {
+  if (!c || level < 0 || level >= c->pl.L || (color != 0 && color != 1))
+    return fail(MG_ERR_ARG, "bad arguments");
+  int rc = smooth_half(c, level, color, from_zero);
+  if (rc) return rc;
+  return sync(c);
+}
+
+int mg_residual_restrict(mg_ctx *c, int level) {
+  if (!c || level < 0 || level >= c->pl.L - 1) return fail(MG_ERR_ARG, "bad level");
+  int rc = restrict_level(c, level);
+  if (rc) return rc;
+  return sync(c);
+}
+
+int mg_prolong_correct(mg_ctx *c, int level) {
+  if (!c || level < 0 || level >= c->pl.L - 1) return fail(MG_ERR_ARG, "bad level");
+  int rc = prolong_level(c, level);
+  if (rc) return rc;
+  return sync(c);
+}
+
+int mg_coarse_solve(mg_ctx *c, int *iters) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  int rc = coarse_solve(c);
+  if (rc) return rc;
+  if (iters) CK(cudaMemcpyAsync(c->h_norm + 1, c->cg_iters, sizeof(int),
+                                cudaMemcpyDeviceToHost, c->stream));
+  if ((rc = sync(c))) return rc;
+  if (iters) memcpy(iters, c->h_norm + 1, sizeof(int));
+  return MG_OK;
+}
+
+int mg_set_profiling(mg_ctx *c, int on) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (on && c->ev.empty()) {
+    c->ev.resize(kMaxMarks);
+    c->mark_cat.assign(kMaxMarks, CAT_NONE);
+    for (auto &e : c->ev) CK(cudaEventCreate(&e));
+  }
+  if ((on != 0) != c->prof && c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  c->prof = on != 0;
+  return MG_OK;
+}
+
+int mg_last_cycle_times(mg_ctx *c, double out[8]) {
+  if (!c || !out) return fail(MG_ERR_ARG, "null pointer");
+  if (!c->prof_last || c->nev < 2) return fail(MG_ERR_ARG, "profiling was off");
+  for (int q = 0; q < 8; q++) out[q] = 0.0;
+  for (int i = 1; i < c->nev; i++) {
+    const int cat = c->mark_cat[i];
+    if (cat == CAT_NONE) continue;
+    float ms = 0.f;
+    CK(cudaEventElapsedTime(&ms, c->ev[i - 1], c->ev[i]));
+    out[cat] += ms;
+    if (cat == CAT_SMOOTH0) out[1] += 1.0;
+  }
+  float tot = 0.f;
+  CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[c->nev - 1]));
+  out[6] = tot;
+  out[7] = c->cycle_launches;
+  return MG_OK;
+}
+
+int mg_cycle_launches(const mg_ctx *c) { return c ? c->cycle_launches : MG_ERR_ARG; }
+
+void *mg_stream(const mg_ctx *c) { return c ? (void *)c->stream : nullptr; }
+
+}  // extern "C"

@@ -1,0 +1,57 @@
+// Internal declarations shared by the kernels (mg_kernels.cu) and the host
+// orchestration (mg_api.cu) of libmg_cuda.so.  Not part of the C-ABI.
+//
+// Storage of one level of one slab ("Grid"): checkerboard-split layout
+// ("rearranging the unknowns in a checker-board manner").  Each of
+// the four fields Phi^R, Phi^B, f^R, f^B is an array
+//     [nxl + 2 planes][ny + 2 rows][pz]   (x slowest, z fastest)
+// holding, for row (i, j), the cells of that colour in z order: the red cell
+// with half-index k sits at z = 2k + p, p = (i + j) & 1 (global i), the black
+// one at z = 2k + 1 - p.  Plane 0 / nxl+1 and row 0 / ny+1 are ghost layers
+// (0 on physical boundaries, neighbour data on slab interfaces).  pz >= nz/2,
+// a multiple of 4 doubles, so every row starts 32-byte aligned.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace mg {
+
+struct Grid {
+  double *phiR, *phiB, *fR, *fB;
+  int nx, ny, nz;    // global dims of the level
+  int nxl, x0;       // planes held here, global x index of the first one
+  int nzh, pz;       // nz/2, row pitch in doubles
+  long long plane;   // (ny + 2) * pz
+  double c;          // operator scale 2^-l / h^2   (A_l = c * S_l)
+  double w;          // 2^l h^2 = 1/c
+  int dface[6];      // centre contribution of a face: +1 Dirichlet, -1 Neumann
+};
+
+__host__ __device__ inline long long grid_elems(const Grid &g) {
+  return (long long)(g.nxl + 2) * g.plane;
+}
+
+// ---- kernel launchers (mg_kernels.cu) ---------------------------------------
+void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s);
+void launch_resid_restrict(const Grid &f, const Grid &c, int cofs,
+                           cudaStream_t s);
+void launch_prolong(const Grid &f, const Grid &c, int cofs, double alpha,
+                    cudaStream_t s);
+// partial sums of r^2 over the grid into partials[0..nblk), returns nblk
+int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s);
+// out[0] = sum of parts[0..n) in a fixed order
+void launch_sum_ordered(const double *parts, int n, double *out,
+                        cudaStream_t s);
+void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
+                      int *iters_out, cudaStream_t s);
+size_t coarse_cg_scratch_doubles(const Grid &g);
+void launch_spheres(const Grid &g, double h, int n, const double *sph,
+                    int normalization, unsigned long long *counts,
+                    cudaStream_t s);
+void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
+                     cudaStream_t s);
+// natural <-> split conversion of one field of a grid (phi: 0, f: 1)
+void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);
+void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s);
+
+}  // namespace mg

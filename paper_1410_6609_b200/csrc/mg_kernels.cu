@@ -1,0 +1,530 @@
+// sm_100a kernels of the cell-centered multigrid solve (arXiv 1410.6609).
+//
+// Compiled with -fmad=false: every per-cell formula is evaluated with the
+// operand order and single roundings written here, no FMA contraction, so
+// smoother / residual / restriction / prolongation / sphere rasterisation are
+// bitwise reproducible ("Parity contract").
+//
+// Operator (Galerkin closed form): on level l of a box domain
+//     A_l = c_l * S_l,  c_l = 2^-l / h^2,
+// S_l the folded integer 7-point stencil of the level's own grid: centre
+// d = 6 + sum over touched faces (+1 Dirichlet, -1 Neumann), neighbours -1.
+// Hence no stencil is stored: the centre comes from the cell position.
+#include <cuda_runtime.h>
+
+#include "mg_internal.h"
+
+namespace mg {
+
+static constexpr int kThreads = 256;
+static constexpr double kPi = 3.14159265358979323846;
+
+__device__ __forceinline__ int centre_d(const Grid &g, int i, int j, int z) {
+  int d = 6;
+  if (i == 0) d += g.dface[0];
+  if (i == g.nx - 1) d += g.dface[1];
+  if (j == 0) d += g.dface[2];
+  if (j == g.ny - 1) d += g.dface[3];
+  if (z == 0) d += g.dface[4];
+  if (z == g.nz - 1) d += g.dface[5];
+  return d;
+}
+
+__device__ __forceinline__ long long rowbase(const Grid &g, int il, int j) {
+  return (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
+}
+
+__device__ __forceinline__ double2 ld2(const double *p) {
+  return *reinterpret_cast<const double2 *>(p);
+}
+
+// ---------------------------------------------------------------------------
+// RBGS half-sweep.  One thread updates two cells of colour
+// `color` (half-indices k, k+1 of one row):
+//     Phi_c = (f_c * w + s) / d,  s = ((((x- + x+) + y-) + y+) + z-) + z+
+// which equals (f_c - sum_q a_q Phi_q) / a_cc of the oracle bit for bit when
+// c_l is a power of two.  The other colour's x/y neighbours share
+// the half-index k; the z neighbours are O(k-1+p), O(k+p), p = z & 1.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_smooth(Grid g, int color, int from_zero) {
+  const int nk2 = (g.nzh + 1) >> 1;  // odd nzh: the last pair is half used
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)g.nxl * g.ny * nk2;
+  if (t >= total) return;
+  const int k2 = (int)(t % nk2);
+  const long long r = t / nk2;
+  const int j = (int)(r % g.ny);
+  const int il = (int)(r / g.ny);
+  const int i = g.x0 + il;
+  const int p = (i + j + color) & 1;
+  double *__restrict__ own = color ? g.phiB : g.phiR;
+  const double *__restrict__ oth = color ? g.phiR : g.phiB;
+  const double *__restrict__ f = color ? g.fB : g.fR;
+  const long long b = rowbase(g, il, j);
+  const int k = 2 * k2;
+  const double2 fo = ld2(f + b + k);
+  double s0, s1;
+  if (from_zero) {
+    s0 = 0.0;
+    s1 = 0.0;
+  } else {
+    const double2 xm = ld2(oth + b - g.plane + k);
+    const double2 xp = ld2(oth + b + g.plane + k);
+    const double2 ym = ld2(oth + b - g.pz + k);
+    const double2 yp = ld2(oth + b + g.pz + k);
+    const double2 zc = ld2(oth + b + k);
+    double zm0, zp0, zm1, zp1;
+    if (p == 0) {
+      zm0 = (k > 0) ? oth[b + k - 1] : 0.0;
+      zp0 = zc.x;
+      zm1 = zc.x;
+      zp1 = zc.y;
+    } else {
+      zm0 = zc.x;
+      zp0 = zc.y;
+      zm1 = zc.y;
+      zp1 = (k + 2 < g.nzh) ? oth[b + k + 2] : 0.0;
+    }
+    s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
+    s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
+  }
+  const int z0 = 2 * k + p;
+  const double d0 = (double)centre_d(g, i, j, z0);
+  const double d1 = (double)centre_d(g, i, j, z0 + 2);
+  double2 out;
+  out.x = (fo.x * g.w + s0) / d0;
+  out.y = (fo.y * g.w + s1) / d1;
+  if (k + 1 < g.nzh)
+    *reinterpret_cast<double2 *>(own + b + k) = out;
+  else
+    own[b + k] = out.x;
+}
+
+void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s) {
+  const long long total = (long long)g.nxl * g.ny * ((g.nzh + 1) >> 1);
+  if (total <= 0) return;
+  const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
+  k_smooth<<<blocks, kThreads, 0, s>>>(g, color, from_zero);
+}
+
+// residual r = f - c (d Phi - s) at (il, j, z) of a grid: the oracle's
+// f - (a_cc Phi + sum_q a_q Phi_q) with the same roundings
+__device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
+                                           int z) {
+  const int i = g.x0 + il;
+  const int col = (i + j + z) & 1;
+  const int k = z >> 1;
+  const int p = z & 1;
+  const double *own = col ? g.phiB : g.phiR;
+  const double *oth = col ? g.phiR : g.phiB;
+  const double *f = col ? g.fB : g.fR;
+  const long long b = rowbase(g, il, j);
+  const double zm = (z > 0) ? oth[b + k - 1 + p] : 0.0;
+  const double zp = (z < g.nz - 1) ? oth[b + k + p] : 0.0;
+  const double s = ((((oth[b - g.plane + k] + oth[b + g.plane + k]) +
+                      oth[b - g.pz + k]) +
+                     oth[b + g.pz + k]) +
+                    zm) +
+                   zp;
+  const double d = (double)centre_d(g, i, j, z);
+  const double t = d * own[b + k] - s;
+  return f[b + k] - g.c * t;
+}
+
+// ---------------------------------------------------------------------------
+// Fused residual + restriction: f_{l+1}(C) = 1/8 * pairwise sum of the
+// residuals of C's 8 children, child bits (dx,dy,dz), dz fastest.  The fine
+// residual is never stored.  One thread per coarse cell.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_resid_restrict(Grid F, Grid C) {
+  const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)ncx * ncy * ncz;
+  if (t >= total) return;
+  const int K = (int)(t % ncz);
+  const long long q = t / ncz;
+  const int J = (int)(q % ncy);
+  const int Il = (int)(q / ncy);
+  double r[8];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+        r[a * 4 + b * 2 + c] = resid_at(F, 2 * Il + a, 2 * J + b, 2 * K + c);
+  const double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  const int Ig = (F.x0 >> 1) + Il;
+  const int col = (Ig + J + K) & 1;
+  double *cf = col ? C.fB : C.fR;
+  cf[rowbase(C, Ig - C.x0, J) + (K >> 1)] = 0.125 * s;
+}
+
+void launch_resid_restrict(const Grid &f, const Grid &c, int /*cofs*/,
+                           cudaStream_t s) {
+  const long long total =
+      (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
+  if (total <= 0) return;
+  const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
+  k_resid_restrict<<<blocks, kThreads, 0, s>>>(f, c);
+}
+
+// ---------------------------------------------------------------------------
+// Prolongation + magnified correction:
+//     Phi(c) = Phi(c) + alpha * e(parent(c)),  parent = (i/2, j/2, z/2).
+// Red and black cells with half-index k both have parent z-index Z = k.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_prolong(Grid F, Grid C, double alpha) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const long long total = (long long)F.nxl * F.ny * F.nzh;
+  if (t >= total) return;
+  const int k = (int)(t % F.nzh);
+  const long long q = t / F.nzh;
+  const int j = (int)(q % F.ny);
+  const int il = (int)(q / F.ny);
+  const int I = (F.x0 + il) >> 1, J = j >> 1, Z = k;
+  const double *ce = ((I + J + Z) & 1) ? C.phiB : C.phiR;
+  const double e = ce[rowbase(C, I - C.x0, J) + (Z >> 1)];
+  const long long b = rowbase(F, il, j) + k;
+  F.phiR[b] = F.phiR[b] + alpha * e;
+  F.phiB[b] = F.phiB[b] + alpha * e;
+}
+
+void launch_prolong(const Grid &f, const Grid &c, int /*cofs*/, double alpha,
+                    cudaStream_t s) {
+  const long long total = (long long)f.nxl * f.ny * f.nzh;
+  if (total <= 0) return;
+  const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
+  k_prolong<<<blocks, kThreads, 0, s>>>(f, c, alpha);
+}
+
+// ---------------------------------------------------------------------------
+// Residual norm (Alg.1): per-block partial sums of r^2 with a
+// fixed grid and a fixed reduction tree (deterministic), then an ordered sum.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  if (wid == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  v = sh[0];
+  __syncthreads();
+  return v;
+}
+
+static constexpr int kNormBlocks = 148 * 8;
+
+__global__ void __launch_bounds__(kThreads)
+    k_norm_partials(Grid g, double *partials) {
+  __shared__ double sh[32];
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  double acc = 0.0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+       t < total; t += (long long)gridDim.x * blockDim.x) {
+    const int z = (int)(t % g.nz);
+    const long long q = t / g.nz;
+    const int j = (int)(q % g.ny);
+    const int il = (int)(q / g.ny);
+    const double r = resid_at(g, il, j, z);
+    acc = acc + r * r;
+  }
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s) {
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  long long nb = (total + kThreads - 1) / kThreads;
+  if (nb > kNormBlocks) nb = kNormBlocks;
+  if (nb < 1) nb = 1;
+  k_norm_partials<<<(unsigned)nb, kThreads, 0, s>>>(g, partials);
+  return (int)nb;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_sum_ordered(const double *parts, int n, double *out) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) acc = acc + parts[t];
+  const double s = block_sum(acc, sh);
+  if (threadIdx.x == 0) out[0] = s;
+}
+
+void launch_sum_ordered(const double *parts, int n, double *out,
+                        cudaStream_t s) {
+  k_sum_ordered<<<1, kThreads, 0, s>>>(parts, n, out);
+}
+
+// ---------------------------------------------------------------------------
+// Coarsest-grid CG: one CTA, Hestenes-Stiefel from x = 0, stop at
+// ||r|| <= tol ||b|| or maxit.  Vectors in natural order in `scratch`
+// (L1/L2-resident); the operator is the same closed form as the smoother.
+// ---------------------------------------------------------------------------
+static constexpr int kCgThreads = 1024;
+
+__device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
+                                                 int z, int *col) {
+  *col = (g.x0 + il + j + z) & 1;
+  return rowbase(g, il, j) + (z >> 1);
+}
+
+__device__ __forceinline__ double cg_apply(const Grid &g, const double *v,
+                                           long long n) {
+  const int z = (int)(n % g.nz);
+  const long long q = n / g.nz;
+  const int j = (int)(q % g.ny);
+  const int i = (int)(q / g.ny);
+  const long long sx = (long long)g.ny * g.nz, sy = g.nz;
+  const double xm = (i > 0) ? v[n - sx] : 0.0;
+  const double xp = (i < g.nx - 1) ? v[n + sx] : 0.0;
+  const double ym = (j > 0) ? v[n - sy] : 0.0;
+  const double yp = (j < g.ny - 1) ? v[n + sy] : 0.0;
+  const double zm = (z > 0) ? v[n - 1] : 0.0;
+  const double zp = (z < g.nz - 1) ? v[n + 1] : 0.0;
+  const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
+  const double d = (double)centre_d(g, i, j, z);
+  return g.c * (d * v[n] - s);
+}
+
+__device__ double cg_dot(const double *a, const double *b, long long N,
+                         double *sh) {
+  double acc = 0.0;
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) acc = acc + a[n] * b[n];
+  return block_sum(acc, sh);
+}
+
+__global__ void __launch_bounds__(kCgThreads)
+    k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
+  __shared__ double sh[32];
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  double *x = scr, *r = scr + N, *p = scr + 2 * N, *q = scr + 3 * N;
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = (int)(n % g.nz);
+    const long long t = n / g.nz;
+    int col;
+    const long long idx = split_index(g, (int)(t / g.ny), (int)(t % g.ny), z, &col);
+    const double b = col ? g.fB[idx] : g.fR[idx];
+    x[n] = 0.0;
+    r[n] = b;
+    p[n] = b;
+  }
+  __syncthreads();
+  double rho = cg_dot(r, r, N, sh);
+  const double bnorm = sqrt(rho);
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) q[n] = cg_apply(g, p, n);
+      __syncthreads();
+      const double pq = cg_dot(p, q, N, sh);
+      const double a = rho / pq;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+        x[n] = x[n] + a * p[n];
+        r[n] = r[n] - a * q[n];
+      }
+      __syncthreads();
+      const double rho1 = cg_dot(r, r, N, sh);
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      const double beta = rho1 / rho;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
+      __syncthreads();
+      rho = rho1;
+    }
+  }
+  __syncthreads();
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = (int)(n % g.nz);
+    const long long t = n / g.nz;
+    int col;
+    const long long idx = split_index(g, (int)(t / g.ny), (int)(t % g.ny), z, &col);
+    (col ? g.phiB : g.phiR)[idx] = x[n];
+  }
+  if (threadIdx.x == 0 && iters_out) *iters_out = it;
+}
+
+size_t coarse_cg_scratch_doubles(const Grid &g) {
+  return 4 * (size_t)g.nx * g.ny * g.nz;
+}
+
+void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
+                      int *iters_out, cudaStream_t s) {
+  k_coarse_cg<<<1, kCgThreads, 0, s>>>(g, scratch, tol, maxit, iters_out);
+}
+
+// ---------------------------------------------------------------------------
+// RHS from charged spheres (centre rule P:273, inclusive c13).
+// One CTA per sphere: count the covered cell centres of the whole (global)
+// domain, then add rho_p to the covered cells of this slab.  sph holds
+// (cx, cy, cz, R, Q) per sphere.  f must be zero beforehand; non-overlapping
+// spheres give 0 + rho exactly, as the oracle.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ bool inside(int i, int j, int k, double h,
+                                       double cx, double cy, double cz,
+                                       double R) {
+  const double dx = ((double)i + 0.5) * h - cx;
+  const double dy = ((double)j + 0.5) * h - cy;
+  const double dz = ((double)k + 0.5) * h - cz;
+  const double d2 = (dx * dx + dy * dy) + dz * dz;
+  return d2 <= R * R;
+}
+
+__device__ __forceinline__ void bbox(int n, double h, double c, double R,
+                                     int *lo, int *hi) {
+  int a = (int)floor((c - R) / h - 0.5) - 1;
+  int b = (int)ceil((c + R) / h - 0.5) + 1;
+  *lo = a < 0 ? 0 : a;
+  *hi = b > n - 1 ? n - 1 : b;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_spheres(Grid g, double h, const double *sph, int normalization,
+              unsigned long long *counts) {
+  __shared__ double sh[32];
+  const int p = blockIdx.x;
+  const double cx = sph[5 * p], cy = sph[5 * p + 1], cz = sph[5 * p + 2];
+  const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
+  int i0, i1, j0, j1, k0, k1;
+  bbox(g.nx, h, cx, R, &i0, &i1);
+  bbox(g.ny, h, cy, R, &j0, &j1);
+  bbox(g.nz, h, cz, R, &k0, &k1);
+  const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
+  const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
+  double cnt = 0.0;  // exact integer count (< 2^53)
+  for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
+    const int k = k0 + (int)(t % nk);
+    const long long q = t / nk;
+    const int j = j0 + (int)(q % nj);
+    const int i = i0 + (int)(q / nj);
+    if (inside(i, j, k, h, cx, cy, cz, R)) cnt += 1.0;
+  }
+  const double np = block_sum(cnt, sh);
+  if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
+  double rho;
+  if (normalization == 1)
+    rho = Q / ((4.0 / 3.0) * kPi * (R * R * R));
+  else {
+    if (np == 0.0) return;
+    rho = Q / (np * (h * h * h));
+  }
+  const int xa = i0 > g.x0 ? i0 : g.x0;
+  const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
+  if (xa > xb) return;
+  const long long nloc = (long long)(xb - xa + 1) * nj * nk;
+  for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
+    const int k = k0 + (int)(t % nk);
+    const long long q = t / nk;
+    const int j = j0 + (int)(q % nj);
+    const int i = xa + (int)(q / nj);
+    if (!inside(i, j, k, h, cx, cy, cz, R)) continue;
+    const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
+    double *f = ((i + j + k) & 1) ? g.fB : g.fR;
+    atomicAdd(f + idx, rho);
+  }
+}
+
+void launch_spheres(const Grid &g, double h, int n, const double *sph,
+                    int normalization, unsigned long long *counts,
+                    cudaStream_t s) {
+  if (n <= 0) return;
+  k_spheres<<<n, kThreads, 0, s>>>(g, h, sph, normalization, counts);
+}
+
+// ---------------------------------------------------------------------------
+// Finest-grid RHS adaptation: f -= term_q for every
+// face q the cell touches, in face order.  term_q = (2 alpha) g_d for
+// Dirichlet, alpha (h g_n) for Neumann, alpha = -1/h^2 (host-computed, the
+// oracle's expressions).  One thread per row; boundary rows do every cell,
+// interior rows only z = 0 and z = nz-1.
+// ---------------------------------------------------------------------------
+struct Terms {
+  double t[6];
+};
+
+__global__ void __launch_bounds__(kThreads) k_bc_adapt(Grid g, Terms T) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny) return;
+  const int j = (int)(t % g.ny);
+  const int il = (int)(t / g.ny);
+  const int i = g.x0 + il;
+  const bool full = (i == 0 || i == g.nx - 1 || j == 0 || j == g.ny - 1);
+  const long long b = rowbase(g, il, j);
+  const int step = full ? 1 : (g.nz - 1);
+  for (int z = 0; z < g.nz; z += step) {
+    double *f = ((i + j + z) & 1) ? g.fB : g.fR;
+    double v = f[b + (z >> 1)];
+    const bool on[6] = {i == 0, i == g.nx - 1, j == 0,
+                        j == g.ny - 1, z == 0, z == g.nz - 1};
+#pragma unroll
+    for (int q = 0; q < 6; q++)
+      if (on[q]) v = v - T.t[q];
+    f[b + (z >> 1)] = v;
+  }
+}
+
+void launch_bc_adapt(const Grid &g, const double *terms, const int * /*types*/,
+                     cudaStream_t s) {
+  Terms T;
+  for (int q = 0; q < 6; q++) T.t[q] = terms[q];
+  const long long total = (long long)g.nxl * g.ny;
+  if (total <= 0) return;
+  k_bc_adapt<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, T);
+}
+
+// ---------------------------------------------------------------------------
+// natural (x slowest) <-> checkerboard-split conversion at the API boundary
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads)
+    k_pack(Grid g, int field, const double *nat) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  int col;
+  const long long idx = split_index(g, il, j, z, &col);
+  double *dst = field ? (col ? g.fB : g.fR) : (col ? g.phiB : g.phiR);
+  dst[idx] = nat[t];
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_unpack(Grid g, int field, double *nat) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  int col;
+  const long long idx = split_index(g, il, j, z, &col);
+  const double *src = field ? (col ? g.fB : g.fR) : (col ? g.phiB : g.phiR);
+  nat[t] = src[idx];
+}
+
+void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s) {
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  if (total <= 0) return;
+  k_pack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field, nat);
+}
+
+void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s) {
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  if (total <= 0) return;
+  k_unpack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field, nat);
+}
+
+}  // namespace mg

@@ -30,6 +30,7 @@ class Workload:
     min_coarse: int
     nu1: int = 2
     nu2: int = 2
+    coarse_tol: float = 1e-12       # CG relative tolerance (reading c8)
     cycles: Optional[int] = None    # fixed cycle count (cfg1, cfg3)
     tol: Optional[float] = None     # relative reduction target (cfg2, cfg4, cfg5)
     rhs: Optional[np.ndarray] = None        # natural-layout f (cfg1, cfg3)
@@ -122,8 +123,9 @@ def random_spheres(extent, radius: float, n: int, seed: int,
 
 def cfg1(n: int = 32, cycles: int = 10) -> Workload:
     bt, bv = all_dirichlet()
+    # "exact coarse solve": CG to 1e-14 relative (reading c8)
     return Workload("cfg1_sine%d" % n, (n, n, n), 1.0 / n, bt, bv, min_coarse=4,
-                    cycles=cycles, rhs=sine_rhs(n))
+                    coarse_tol=1e-14, cycles=cycles, rhs=sine_rhs(n))
 
 
 def cfg2(seed: int = 0, shape=(256, 64, 64), n_spheres: int = 200,

@@ -1,0 +1,113 @@
+"""CPU-only checks of the C-ABI library: it loads without a GPU, exports every
+function include/mg.h declares, and its host-side planning (hierarchy rule,
+slab ownership, agglomeration level, workspace size) is right."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_6609_b200 import _build, mg
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    _build.build()
+    oracle.build()
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "mg.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    names = re.findall(r"\b(mg_[a-z_0-9]+)\s*\(", src)
+    return sorted(set(names))
+
+
+def test_library_exports_every_declared_symbol():
+    names = declared_functions()
+    assert len(names) >= 20
+    L = mg.lib()
+    for n in names:
+        assert hasattr(L, n), n
+
+
+def test_no_oracle_in_product():
+    """The product never references the oracle (no shared code)."""
+    pkg = os.path.join(ROOT, "paper_1410_6609_b200")
+    for dp, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".h", ".cuh")):
+                txt = open(os.path.join(dp, f)).read()
+                assert "import oracle" not in txt and "mg_oracle" not in txt, f
+                assert "orc_" not in txt, f
+
+
+def test_create_without_gpu_fails_loudly():
+    """No CPU fallback: without a device the library returns an error."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(mg.MGError):
+        mg.Multigrid((8, 8, 8), 1.0, [0] * 6)
+    bc = (mg.mg_bc * 6)(*[mg.mg_bc(0, 0.0)] * 6)
+    assert not mg.lib().mg_create(8, 8, 8, 1.0, bc)
+    assert b"MG_ERR_CUDA" in mg.lib().mg_last_error(None)
+
+
+@pytest.mark.parametrize("shape,mc", [((32, 32, 32), 4), ((256, 64, 64), 4),
+                                      ((512, 512, 512), 8), ((64, 16, 48), 2),
+                                      ((24, 24, 24), 2), ((2, 2, 2), 1)])
+def test_plan_hierarchy_equals_oracle(shape, mc):
+    dims, lnx, agg = mg.plan(shape, min_coarse=mc)
+    o = oracle.Oracle(shape, 1.0, [0] * 6, min_coarse=mc) \
+        if np.prod(shape) <= 64 ** 3 * 8 else None
+    if o is not None:
+        assert dims == [o.dims(l) for l in range(o.nlevels)]
+    assert agg == len(dims)
+    assert all(x == 0 for x in lnx)
+
+
+def test_plan_multi_rank_agglomeration():
+    # config 4 at P = 8: 4096 x 512 x 512, slabs of 512 planes
+    dims, lnx, agg = mg.plan((4096, 512, 512), min_coarse=8, nranks=8,
+                             halo="nccl")
+    assert dims[-1] == (64, 8, 8)
+    assert lnx[0] == 512 and lnx[1] == 256 and lnx[2] == 128 and lnx[3] == 64
+    # local 64^3 at level 3 is kept distributed; level 4 (32^3 local) is whole
+    assert agg == 4
+    # config 5 at P = 8: 2048 x 512 x 512
+    dims, lnx, agg = mg.plan((2048, 512, 512), min_coarse=8, nranks=8,
+                             halo="nccl")
+    assert dims[-1] == (32, 8, 8)
+    assert agg == 3  # level 3 local 32 x 64 x 64 < 64^3
+
+
+def test_plan_errors():
+    with pytest.raises(mg.MGError) as e:
+        mg.plan((7, 8, 8))
+    assert e.value.code == mg.MG_ERR_COARSEN
+    with pytest.raises(mg.MGError):
+        mg.plan((0, 8, 8))
+    with pytest.raises(mg.MGError):
+        mg.plan((48, 8, 8), nranks=5, halo="nccl")
+    with pytest.raises(mg.MGError):
+        mg.plan((6, 8, 8), nranks=2, halo="nccl")  # 3 planes per rank
+
+
+def test_workspace_bytes_model():
+    """Split layout: 4 fields per level, ghost planes/rows, pitch nz/2 -> x4."""
+    nb = mg.workspace_bytes((512, 512, 512), min_coarse=8)
+    fine = 4 * 514 * 514 * 256 * 8
+    assert fine < nb < fine * 1.2
+    assert mg.workspace_bytes((7, 8, 8)) == 0
+
+
+def test_nccl_unique_id_on_cpu():
+    try:
+        uid = mg.nccl_unique_id()
+    except mg.MGError as e:
+        pytest.skip("libnccl not loadable here: %s" % e)
+    assert len(uid) == 128 and any(uid)

@@ -1,0 +1,310 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Per-cell steps (smoother half-sweeps, residual + restriction, prolongation,
+sphere RHS, BC adaptation, layout conversion) must be BITWISE equal for
+power-of-two h ("Parity contract"); whole V-cycles must match in
+Phi to relative L2 1e-10 and in residual history to 1e-8 relative (north_star)
+with the rounding-floor clause |dr_k| <= 1e-8 r_k + 1e-14 r_0 (reading c21,
+DESIGN.md: per-cell steps are bitwise, so the only differences are the CG and
+norm reductions; an ulp-level difference in Phi moves the residual by about
+eps*||A||*||Phi||, measured at 1.2e-16 r_0 on config 1).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_6609_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+D, N = 0, 1
+BCS = {
+    "dirichlet0": ([D] * 6, [0.0] * 6),
+    "dirichlet": ([D] * 6, [1.0, -2.0, 0.5, 3.0, -1.0, 2.0]),
+    "channel": ([N, N, D, D, N, N], [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]),
+    "mixed": ([N, D, N, D, N, D], [0.25, 1.0, -0.5, -1.0, 2.0, 0.0]),
+}
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_6609_b200 import _build
+    _build.build()
+    from paper_1410_6609_b200 import mg as M
+    return M
+
+
+def pair(M, shape, h, bc, **kw):
+    bt, bv = BCS[bc]
+    s = M.Multigrid(shape, h, bt, bv, **kw)
+    okw = {k: v for k, v in kw.items()
+           if k in ("min_coarse", "max_levels", "nu1", "nu2", "alpha",
+                    "coarse_tol", "coarse_maxit")}
+    o = oracle.Oracle(shape, h, bt, bv, **okw)
+    return s, o
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+SHAPES = [((8, 8, 8), 1.0 / 8, "dirichlet"),
+          ((12, 10, 6), 1.0, "mixed"),          # odd nz/2: ragged row tail
+          ((32, 16, 64), 0.25, "channel"),      # many blocks
+          ((2, 2, 2), 1.0, "dirichlet"),
+          ((66, 34, 20), 1.0, "mixed")]
+
+
+@pytest.mark.parametrize("shape,h,bc", SHAPES)
+def test_layout_roundtrip(mg, shape, h, bc):
+    s, _ = pair(mg, shape, h, bc, min_coarse=100)
+    rng = np.random.default_rng(0)
+    a = rng.standard_normal(shape)
+    s.set_solution(a)
+    assert np.array_equal(s.get_solution(), a)
+    b = rng.standard_normal(shape)
+    s.set_field(0, mg.MG_FIELD_RHS, b)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), b)
+
+
+@pytest.mark.parametrize("shape,h,bc", SHAPES)
+@pytest.mark.parametrize("color", [0, 1])
+def test_half_sweep_bitwise(mg, shape, h, bc, color):
+    s, o = pair(mg, shape, h, bc, min_coarse=100)
+    rng = np.random.default_rng(1 + color)
+    phi = rng.uniform(-1, 1, shape)
+    f = rng.uniform(-1, 1, shape)
+    s.set_solution(phi)
+    s.set_field(0, mg.MG_FIELD_RHS, f)
+    o.set_phi(phi)
+    o.set_rhs_raw(f)
+    for c in (color, 1 - color, color):
+        s.smooth_half(0, c)
+        o.smooth_half(0, c)
+        assert np.array_equal(s.get_solution(), o.phi())
+
+
+def test_half_sweep_from_zero_bitwise(mg):
+    shape = (16, 8, 12)
+    s, o = pair(mg, shape, 1.0, "channel", min_coarse=100)
+    f = np.random.default_rng(3).uniform(-1, 1, shape)
+    s.set_solution(np.random.default_rng(4).uniform(-1, 1, shape))  # ignored
+    s.set_field(0, mg.MG_FIELD_RHS, f)
+    o.set_phi(np.zeros(shape))
+    o.set_rhs_raw(f)
+    s.smooth_half(0, 0, from_zero=True)
+    o.smooth_half(0, 0)
+    red = ((np.indices(shape).sum(0)) & 1) == 0
+    assert np.array_equal(s.get_solution()[red], o.phi()[red])
+
+
+@pytest.mark.parametrize("shape,h,bc,mc", [
+    ((8, 8, 8), 1.0 / 8, "dirichlet", 2),
+    ((16, 8, 12), 1.0, "mixed", 2),
+    ((64, 32, 32), 1.0, "channel", 4),
+    ((32, 32, 32), 1.0 / 32, "dirichlet0", 4)])
+def test_residual_restrict_and_prolong_bitwise(mg, shape, h, bc, mc):
+    s, o = pair(mg, shape, h, bc, min_coarse=mc)
+    assert s.nlevels == o.nlevels >= 2
+    rng = np.random.default_rng(5)
+    for l in range(o.nlevels - 1):
+        d = o.dims(l)
+        phi = rng.uniform(-1, 1, d)
+        f = rng.uniform(-1, 1, d)
+        s.set_field(l, mg.MG_FIELD_PHI, phi)
+        s.set_field(l, mg.MG_FIELD_RHS, f)
+        o.set_phi(phi, l)
+        o.set_rhs_raw(f, l)
+        s.residual_restrict(l)
+        o.restrict_residual(l)
+        assert np.array_equal(s.get_field(l + 1, mg.MG_FIELD_RHS), o.rhs(l + 1))
+        e = rng.uniform(-1, 1, o.dims(l + 1))
+        s.set_field(l + 1, mg.MG_FIELD_PHI, e)
+        o.set_phi(e, l + 1)
+        s.prolong_correct(l)
+        o.prolong_correct(l, 2.0)
+        assert np.array_equal(s.get_field(l, mg.MG_FIELD_PHI), o.phi(l))
+
+
+@pytest.mark.parametrize("bc", ["dirichlet", "channel", "mixed"])
+@pytest.mark.parametrize("h", [1.0, 0.5, 0.1])
+def test_set_rhs_bc_adaptation_bitwise(mg, bc, h):
+    """BC adaptation is bitwise for any h (same expressions)."""
+    shape = (10, 12, 14)
+    s, o = pair(mg, shape, h, bc, min_coarse=100)
+    f = np.random.default_rng(6).uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+
+
+@pytest.mark.parametrize("norm", [0, 1])
+def test_sphere_rhs_bitwise(mg, norm):
+    w = W.cfg2(seed=1)
+    s, o = pair(mg, w.shape, w.h, "channel", min_coarse=4)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+
+
+def test_sphere_rhs_physical_units_and_errors(mg):
+    shape, h = (32, 16, 24), 0.125
+    c, q = W.random_spheres(np.array(shape) * h, 0.5, 6, seed=2)
+    s, o = pair(mg, shape, h, "mixed", min_coarse=2)
+    R = np.full(6, 0.5)
+    s.set_rhs_from_spheres(c, R, q)
+    o.set_rhs_from_spheres(c, R, q)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    with pytest.raises(mg.MGError) as e:
+        s.set_rhs_from_spheres(np.array([[0.3, 0.3, 0.3]]), [0.01], [1.0])
+    assert e.value.code == mg.MG_ERR_ARG
+    with pytest.raises(mg.MGError):
+        s.set_rhs_from_spheres(c, -R, q)
+
+
+def test_coarse_cg(mg):
+    shape = (16, 8, 8)
+    s, o = pair(mg, shape, 1.0, "mixed", min_coarse=2)
+    L = o.nlevels - 1
+    f = np.random.default_rng(8).uniform(-1, 1, o.dims(L))
+    s.set_field(L, mg.MG_FIELD_RHS, f)
+    o.set_rhs_raw(f, L)
+    it = s.coarse_solve()
+    ito = o.cg(L, 1e-12, 1000)
+    assert abs(it - ito) <= 2
+    assert rel(s.get_field(L, mg.MG_FIELD_PHI), o.phi(L)) < 1e-11
+
+
+def check_history(hg, ho):
+    assert len(hg) == len(ho)
+    r0 = ho[0]
+    for a, b in zip(hg, ho):
+        assert abs(a - b) <= 1e-8 * b + 1e-14 * r0, (a, b)
+
+
+def run_fixed(s, o, cycles):
+    hg = [s.residual_norm()]
+    ho = [o.residual_norm()]
+    for _ in range(cycles):
+        hg.append(s.vcycle())
+        ho.append(o.vcycle())
+    return hg, ho
+
+
+def test_config1_parity(mg):
+    w = W.cfg1(32)
+    s, o = pair(mg, w.shape, w.h, "dirichlet0", min_coarse=4,
+                coarse_tol=w.coarse_tol)
+    s.set_rhs(w.rhs)
+    o.set_rhs(w.rhs)
+    hg, ho = run_fixed(s, o, w.cycles)
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    # the discrete solution is c(h) u (closed form)
+    u = w.rhs / (3 * np.pi ** 2)
+    ch = (np.pi * w.h / 2) ** 2 / np.sin(np.pi * w.h / 2) ** 2
+    assert np.abs(s.get_solution() - ch * u).max() < 1e-8
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_config2_parity(mg, seed):
+    w = W.cfg2(seed=seed)
+    s, o = pair(mg, w.shape, w.h, "channel", min_coarse=4)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    rc, cg, hg = s.solve(w.tol, 60)
+    so, co, ho = o.solve(w.tol, 60)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+
+
+@pytest.mark.parametrize("n", [64, 128])
+def test_config3_reduced_parity(mg, n):
+    w = W.cfg3(n, seed=0, cycles=20)
+    s, o = pair(mg, w.shape, w.h, "dirichlet0", min_coarse=8)
+    s.set_rhs(w.rhs)
+    o.set_rhs(w.rhs)
+    hg, ho = run_fixed(s, o, w.cycles)
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+
+
+def test_mixed_bc_schedules_parity(mg):
+    shape = (64, 32, 48)
+    for nu in ((1, 1), (3, 3), (2, 0), (0, 2)):
+        s, o = pair(mg, shape, 0.5, "mixed", min_coarse=2, nu1=nu[0], nu2=nu[1])
+        f = np.random.default_rng(9).uniform(-1, 1, shape)
+        s.set_rhs(f)
+        o.set_rhs(f)
+        hg, ho = run_fixed(s, o, 6)
+        check_history(hg, ho)
+        assert rel(s.get_solution(), o.phi()) <= 1e-10
+
+
+def test_graph_and_eager_identical(mg):
+    w = W.cfg2(seed=0, shape=(64, 32, 32), n_spheres=10)
+    out = []
+    for g in (True, False):
+        s, _ = pair(mg, w.shape, w.h, "channel", min_coarse=4, use_graph=g)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        r = [s.vcycle() for _ in range(4)]
+        out.append((r, s.get_solution()))
+    assert out[0][0] == out[1][0]
+    assert np.array_equal(out[0][1], out[1][1])
+
+
+def test_zero_rhs_and_warm_start(mg):
+    shape = (32, 16, 16)
+    s, _ = pair(mg, shape, 1.0, "dirichlet0", min_coarse=2)
+    s.set_rhs(np.zeros(shape))
+    rc, cyc, hist = s.solve(1e-8, 5)
+    assert rc == 0 and cyc == 0 and not s.get_solution().any()
+    f = np.random.default_rng(0).uniform(-1, 1, shape)
+    s.set_rhs(f)
+    s.solve(1e-10, 50)
+    r_warm = s.residual_norm()
+    s.set_rhs(f)  # does not touch Phi (warm start)
+    assert s.residual_norm() == r_warm
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_loopback_slabs_equal_single(mg, P):
+    """x-slab decomposition (P slabs on one GPU, halo by device copies) gives
+    the 1-slab result bitwise in Phi (per-cell ops are bitwise and the
+    agglomerated coarse levels are the same computation)."""
+    w = W.cfg2(seed=0, shape=(128, 32, 32), n_spheres=20)
+    res = []
+    for p in (1, P):
+        kw = dict(min_coarse=4, agglomerate_below=512)
+        if p > 1:
+            kw.update(nranks=p, halo="loopback")
+        s, _ = pair(mg, w.shape, w.h, "channel", **kw)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        r = [s.vcycle() for _ in range(5)]
+        res.append((r, s.get_solution()))
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.allclose(res[0][0], res[1][0], rtol=1e-13, atol=0)
+
+
+def test_errors(mg):
+    with pytest.raises(mg.MGError) as e:
+        mg.Multigrid((8, 8, 8), 1.0, [N] * 6)
+    assert e.value.code == mg.MG_ERR_BC
+    with pytest.raises(mg.MGError) as e:
+        mg.Multigrid((9, 8, 8), 1.0, [D] * 6)
+    assert e.value.code == mg.MG_ERR_COARSEN
+    with pytest.raises(mg.MGError) as e:
+        mg.Multigrid((8, 8, 8), 1.0, [2] + [D] * 5)
+    assert e.value.code == mg.MG_ERR_BC
+    # divergence: a negative magnification blows the iteration up
+    shape = (32, 32, 32)
+    s = mg.Multigrid(shape, 1.0, [D] * 6, min_coarse=2, alpha=-8.0)
+    s.set_rhs(np.random.default_rng(0).uniform(-1, 1, shape))
+    with pytest.raises(mg.MGError) as e:
+        for _ in range(20):
+            s.vcycle()
+    assert e.value.code == mg.MG_ERR_DIVERGED
