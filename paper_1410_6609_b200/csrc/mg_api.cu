@@ -16,6 +16,7 @@
 #include <nccl.h>
 #include <stdarg.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <string>
@@ -167,8 +168,17 @@ Grid make_grid(const Plan &pl, int l, int slab, double h, const int *dface) {
 }  // namespace
 
 // ---- context --------------------------------------------------------------------
+// TMA descriptors of a grid's two Phi arrays (for the marching half-sweep)
+struct TmPair {
+  alignas(64) unsigned char r[128];
+  alignas(64) unsigned char b[128];
+  bool ok = false;
+};
+
 struct mg_ctx {
   Plan pl;
+  std::vector<std::vector<TmPair>> tm;
+  int use_march = 1;
   double h;
   mg_bc bc[6];
   mg_opts o;
@@ -319,8 +329,13 @@ int halo(mg_ctx *c, int l, int which) {
 
 int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
   if (l == 0) mark(c, CAT_NONE);
-  for (const Grid &g : c->g[l]) {
-    mg::launch_smooth(g, color, from_zero, c->stream);
+  for (size_t s = 0; s < c->g[l].size(); s++) {
+    const Grid &g = c->g[l][s];
+    const TmPair &t = c->tm[l][s];
+    if (!from_zero && t.ok && c->use_march)
+      mg::launch_smooth_march(g, color ? t.r : t.b, color, c->stream);
+    else
+      mg::launch_smooth(g, color, from_zero, c->stream);
     c->launches++;
   }
   if (l == 0) mark(c, CAT_SMOOTH0);
@@ -701,6 +716,17 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
     return nullptr;
   }
   carve(c, base);
+  c->tm.assign(c->pl.L, {});
+  for (int l = 0; l < c->pl.L; l++) {
+    c->tm[l].resize(c->g[l].size());
+    for (size_t s = 0; s < c->g[l].size(); s++) {
+      const Grid &g = c->g[l][s];
+      TmPair &t = c->tm[l][s];
+      t.ok = mg::march_supported(g) && mg::make_tmap_field(g, g.phiR, t.r) &&
+             mg::make_tmap_field(g, g.phiB, t.b);
+    }
+  }
+  if (getenv("MG_NO_MARCH")) c->use_march = 0;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
   e = cudaMallocHost(&c->h_norm, sizeof(double) * 2);

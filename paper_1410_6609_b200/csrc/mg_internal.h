@@ -50,6 +50,11 @@ void launch_spheres(const Grid &g, double h, int n, const double *sph,
                     cudaStream_t s);
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);
+// plane-marching TMA half-sweep (mg_march.cu)
+bool march_supported(const Grid &g);
+bool make_tmap_field(const Grid &g, const double *base, void *out128);
+void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
+                         cudaStream_t s);
 // natural <-> split conversion of one field of a grid (phi: 0, f: 1)
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);
 void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s);

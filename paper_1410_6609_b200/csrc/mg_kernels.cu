@@ -227,26 +227,73 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
 
 static constexpr int kNormBlocks = 148 * 8;
 
+// residual of the two cells of colour `col` at half-indices k, k+1 of row
+// (il, j): same expression as resid_at, vectorised along the row
+__device__ __forceinline__ void resid_pair(const Grid &g, int il, int j, int k,
+                                           int col, double &r0, double &r1) {
+  const int i = g.x0 + il;
+  const int p = (i + j + col) & 1;  // own cells at z = 2k + p, 2k + 2 + p
+  const double *own = col ? g.phiB : g.phiR;
+  const double *oth = col ? g.phiR : g.phiB;
+  const double *f = col ? g.fB : g.fR;
+  const long long b = rowbase(g, il, j);
+  const double2 xm = ld2(oth + b - g.plane + k);
+  const double2 xp = ld2(oth + b + g.plane + k);
+  const double2 ym = ld2(oth + b - g.pz + k);
+  const double2 yp = ld2(oth + b + g.pz + k);
+  const double2 zc = ld2(oth + b + k);
+  const double2 u = ld2(own + b + k);
+  const double2 fo = ld2(f + b + k);
+  double zm0, zp0, zm1, zp1;
+  if (p == 0) {
+    zm0 = (k > 0) ? oth[b + k - 1] : 0.0;
+    zp0 = zc.x;
+    zm1 = zc.x;
+    zp1 = zc.y;
+  } else {
+    zm0 = zc.x;
+    zp0 = zc.y;
+    zm1 = zc.y;
+    zp1 = (k + 2 < g.nzh) ? oth[b + k + 2] : 0.0;
+  }
+  const double s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
+  const double s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
+  const int z0 = 2 * k + p;
+  const double d0 = (double)centre_d(g, i, j, z0);
+  const double d1 = (double)centre_d(g, i, j, z0 + 2);
+  const double t0 = d0 * u.x - s0;
+  const double t1 = d1 * u.y - s1;
+  r0 = fo.x - g.c * t0;
+  r1 = (k + 1 < g.nzh) ? fo.y - g.c * t1 : 0.0;
+}
+
+// one thread per (row, double2 position), both colours: 4 cells
 __global__ void __launch_bounds__(kThreads)
     k_norm_partials(Grid g, double *partials) {
   __shared__ double sh[32];
-  const long long total = (long long)g.nxl * g.ny * g.nz;
+  const int nk2 = (g.nzh + 1) >> 1;
+  const long long total = (long long)g.nxl * g.ny * nk2;
   double acc = 0.0;
   for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
        t < total; t += (long long)gridDim.x * blockDim.x) {
-    const int z = (int)(t % g.nz);
-    const long long q = t / g.nz;
-    const int j = (int)(q % g.ny);
-    const int il = (int)(q / g.ny);
-    const double r = resid_at(g, il, j, z);
-    acc = acc + r * r;
+    const int k2 = (int)(t % nk2);
+    const long long r = t / nk2;
+    const int j = (int)(r % g.ny);
+    const int il = (int)(r / g.ny);
+    double a0, a1, b0, b1;
+    resid_pair(g, il, j, 2 * k2, 0, a0, a1);
+    resid_pair(g, il, j, 2 * k2, 1, b0, b1);
+    acc = acc + a0 * a0;
+    acc = acc + a1 * a1;
+    acc = acc + b0 * b0;
+    acc = acc + b1 * b1;
   }
   const double s = block_sum(acc, sh);
   if (threadIdx.x == 0) partials[blockIdx.x] = s;
 }
 
 int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s) {
-  const long long total = (long long)g.nxl * g.ny * g.nz;
+  const long long total = (long long)g.nxl * g.ny * ((g.nzh + 1) >> 1);
   long long nb = (total + kThreads - 1) / kThreads;
   if (nb > kNormBlocks) nb = kNormBlocks;
   if (nb < 1) nb = 1;

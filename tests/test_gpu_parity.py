@@ -55,7 +55,13 @@ SHAPES = [((8, 8, 8), 1.0 / 8, "dirichlet"),
           ((12, 10, 6), 1.0, "mixed"),          # odd nz/2: ragged row tail
           ((32, 16, 64), 0.25, "channel"),      # many blocks
           ((2, 2, 2), 1.0, "dirichlet"),
-          ((66, 34, 20), 1.0, "mixed")]
+          ((66, 34, 20), 1.0, "mixed"),
+          # marching TMA kernel (nz/2 >= 64): full/partial row tiles and
+          # x-chunks, pitch not a multiple of 8, 1..4 chunks per lane
+          ((20, 16, 128), 1.0 / 16, "dirichlet"),
+          ((34, 12, 256), 1.0, "mixed"),
+          ((18, 24, 136), 0.5, "channel"),
+          ((4, 8, 512), 1.0, "mixed")]
 
 
 @pytest.mark.parametrize("shape,h,bc", SHAPES)
