@@ -170,9 +170,11 @@ Grid make_grid(const Plan &pl, int l, int slab, double h, const int *dface) {
 // ---- context --------------------------------------------------------------------
 // TMA descriptors of a grid's two Phi arrays (for the marching half-sweep)
 struct TmPair {
-  alignas(64) unsigned char r[128];
+  alignas(64) unsigned char r[128];   // whole-row boxes (half-sweeps)
   alignas(64) unsigned char b[128];
-  bool ok = false;
+  alignas(64) unsigned char rr[128];  // z-tiled boxes (residual kernels)
+  alignas(64) unsigned char rb[128];
+  bool ok = false, ok_resid = false;
 };
 
 struct mg_ctx {
@@ -248,7 +250,12 @@ size_t carve(mg_ctx *c, char *base) {
       c->g[l].push_back(gr);
     }
   }
-  c->partials = (double *)cv.take(sizeof(double) * kNormBlocks * (c->nslab + 1));
+  size_t npart = kNormBlocks;
+  for (const Grid &g : c->g[0]) {
+    const size_t nb = (size_t)mg::norm_march_blocks(g);
+    npart += nb > (size_t)kNormBlocks ? nb : (size_t)kNormBlocks;
+  }
+  c->partials = (double *)cv.take(sizeof(double) * npart);
   c->normv = (double *)cv.take(sizeof(double) * (2 + c->P));
   c->cg_scr = (double *)cv.take(sizeof(double) *
                                 mg::coarse_cg_scratch_doubles(c->g[L - 1][0]));
@@ -348,7 +355,12 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
 int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
   for (int s = 0; s < (int)c->g[l].size(); s++) {
-    mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), 0, c->stream);
+    const TmPair &t = c->tm[l][s];
+    if (t.ok_resid && c->use_march)
+      mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
+                                      c->stream);
+    else
+      mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), 0, c->stream);
     c->launches++;
   }
   if (l == 0) mark(c, CAT_RESTRICT0);
@@ -378,6 +390,27 @@ int prolong_level(mg_ctx *c, int l) {
   return halo(c, l, 1);  // the next red half-sweep reads black ghosts
 }
 
+// can level l use the fused prolongation + first post-smoothing red sweep?
+bool can_fuse_prolong(const mg_ctx *c, int l) {
+  if (!c->use_march || c->o.nu2 < 1) return false;
+  for (const TmPair &t : c->tm[l])
+    if (!t.ok) return false;
+  return true;
+}
+
+// Phi_l += alpha P Phi_{l+1} fused with the red half-sweep that follows it
+int prolong_red_level(mg_ctx *c, int l) {
+  if (l == 0) mark(c, CAT_NONE);
+  for (int s = 0; s < (int)c->g[l].size(); s++) {
+    mg::launch_prolong_smooth_march(c->g[l][s], coarse_of(c, l, s),
+                                    c->tm[l][s].b, 0, c->o.alpha, c->stream);
+    c->launches++;
+  }
+  if (l == 0) mark(c, CAT_PROLONG0);
+  CK(cudaGetLastError());
+  return halo(c, l, 0);  // black is recomputed by the next half-sweep
+}
+
 int coarse_solve(mg_ctx *c) {
   const Grid &g = c->g[c->pl.L - 1][0];
   mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
@@ -391,8 +424,15 @@ int coarse_solve(mg_ctx *c) {
 int enqueue_norm(mg_ctx *c) {
   int off = 0;
   mark(c, CAT_NONE);
-  for (const Grid &g : c->g[0]) {
-    off += mg::launch_norm_partials(g, c->partials + off, c->stream);
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    const Grid &g = c->g[0][s];
+    const TmPair &t = c->tm[0][s];
+    if (t.ok_resid && c->use_march) {
+      mg::launch_norm_march(g, t.rr, t.rb, c->partials + off, c->stream);
+      off += mg::norm_march_blocks(g);
+    } else {
+      off += mg::launch_norm_partials(g, c->partials + off, c->stream);
+    }
     c->launches++;
   }
   mg::launch_sum_ordered(c->partials, off, c->normv, c->stream);
@@ -437,9 +477,15 @@ int enqueue_vcycle(mg_ctx *c) {
   if ((rc = coarse_solve(c))) return rc;
   for (int l = L - 2; l >= 0; l--) {
     if (l == 0) mark(c, CAT_COARSE);
-    if ((rc = prolong_level(c, l))) return rc;
+    const bool fuse = can_fuse_prolong(c, l);
+    if (fuse) {
+      if ((rc = prolong_red_level(c, l))) return rc;
+    } else {
+      if ((rc = prolong_level(c, l))) return rc;
+    }
     for (int s = 0; s < c->o.nu2; s++) {
-      if ((rc = smooth_half(c, l, 0, 0))) return rc;
+      if (!(fuse && s == 0))
+        if ((rc = smooth_half(c, l, 0, 0))) return rc;
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
     }
   }
@@ -724,6 +770,9 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
       TmPair &t = c->tm[l][s];
       t.ok = mg::march_supported(g) && mg::make_tmap_field(g, g.phiR, t.r) &&
              mg::make_tmap_field(g, g.phiB, t.b);
+      t.ok_resid = mg::resid_march_supported(g) &&
+                   mg::make_tmap_resid(g, g.phiR, t.rr) &&
+                   mg::make_tmap_resid(g, g.phiB, t.rb);
     }
   }
   if (getenv("MG_NO_MARCH")) c->use_march = 0;

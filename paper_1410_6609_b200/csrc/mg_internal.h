@@ -55,6 +55,18 @@ bool march_supported(const Grid &g);
 bool make_tmap_field(const Grid &g, const double *base, void *out128);
 void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
                          cudaStream_t s);
+// prolongation of the other colour fused with the half-sweep of `color`
+void launch_prolong_smooth_march(const Grid &g, const Grid &c,
+                                 const void *tm_oth128, int color, double alpha,
+                                 cudaStream_t s);
+// residual kernels (two rings, z-tiled boxes)
+bool resid_march_supported(const Grid &g);
+bool make_tmap_resid(const Grid &g, const double *base, void *out128);
+void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
+                                 const void *tmB, cudaStream_t s);
+int norm_march_blocks(const Grid &g);
+void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
+                       double *partials, cudaStream_t s);
 // natural <-> split conversion of one field of a grid (phi: 0, f: 1)
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);
 void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s);

@@ -1,17 +1,26 @@
-// Plane-marching RBGS half-sweep for sm_100a with TMA-staged neighbours.
+// Plane-marching kernels for sm_100a with TMA-staged neighbours.
 //
-// The dominant kernel of the V-cycle.  A CTA owns
-// TY rows (j) of one x-chunk of ICH planes and marches along x.  The other
-// colour's planes -- rows j0-1 .. j0+TY (one ghost/halo row each side), the
-// whole row in z -- stream into a 5-slot shared-memory ring with
-// cp.async.bulk.tensor (TMA) completing on per-slot mbarriers, issued three
-// planes ahead by one thread.  Each value of the other colour therefore
-// crosses L2->SM once per CTA (plus 2/TY halo rows), instead of ~5 times for
-// the direct-load kernel; own f is prefetched one plane ahead in registers
-// and own Phi is written with 16-byte stores.
+// A CTA owns TY rows (j) of one x-chunk of ICH planes and marches along x.
+// Neighbour planes -- rows j0-1 .. j0+TY (one halo row each side) -- stream
+// into shared-memory rings with cp.async.bulk.tensor (TMA) completing on
+// per-slot mbarriers, issued three planes ahead by one thread.  Every
+// neighbour value therefore crosses L2->SM once per CTA (plus 2/TY halo
+// rows) instead of ~5 times for direct loads; own f is prefetched one plane
+// ahead in registers and results are written with 16-byte stores.
 //
-// The per-cell arithmetic is exactly that of k_smooth (bitwise identical):
-//     Phi_c = (f_c * w + s) / d,  s = ((((x- + x+) + y-) + y+) + z-) + z+
+//   k_smooth_march<false>  RBGS half-sweep, the dominant kernel
+//   k_smooth_march<true>   prolongation + magnified correction of the other
+//                          colour fused with the half-sweep
+//                          that follows it (the first post-smoothing red
+//                          sweep): red cells are overwritten by that sweep,
+//                          so only black needs the correction -- the result
+//                          equals prolong-then-sweep bit for bit.
+//   k_resid_march<RESTRICT> residual + 8-child averaging restriction
+//   k_resid_march<NORM>     residual norm partial sums (Alg.1)
+//
+// Per-cell arithmetic is exactly that of mg_kernels.cu (bitwise identical):
+//     Phi_c = (f_c * w + s) / d,  r_c = f_c - c (d Phi_c - s),
+//     s = ((((x- + x+) + y-) + y+) + z-) + z+.
 #include <cuda.h>
 #include <cuda_runtime.h>
 
@@ -25,6 +34,7 @@ constexpr int kTY = 8;        // rows per CTA (one warp per row)
 constexpr int kICH = 16;      // planes per CTA
 constexpr int kSlots = 5;     // ring depth: planes q-1, q, q+1 in use, 2 in flight
 constexpr int kThreadsM = kTY * 32;
+constexpr int kZT = 128;      // z-tile (half-entries) of the residual kernels
 
 __device__ __forceinline__ unsigned smem_u32(const void *p) {
   return (unsigned)__cvta_generic_to_shared(p);
@@ -68,6 +78,10 @@ __device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm,
       : "memory");
 }
 
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 __device__ __forceinline__ int centre_dm(const Grid &g, int i, int j, int z) {
   int d = 6;
   if (i == 0) d += g.dface[0];
@@ -79,17 +93,49 @@ __device__ __forceinline__ int centre_dm(const Grid &g, int i, int j, int z) {
   return d;
 }
 
+__host__ __device__ inline int round128(int bytes) { return (bytes + 127) / 128 * 128; }
+
+// smoother ring slot: (TY + 2) rows of pz doubles
 __host__ __device__ inline int slot_doubles(int pz) {
-  // (TY + 2) rows of pz doubles, rounded up to 128 bytes
-  return (((kTY + 2) * pz * 8 + 127) / 128) * 128 / 8;
+  return round128((kTY + 2) * pz * 8) / 8;
+}
+
+// residual kernels: z-tiles of ZT half-entries.  A row of pz <= ZT + 3 is
+// one tile loaded whole (box = pz); longer rows are cut into tiles whose TMA
+// box (ZT + 4 wide, start a multiple of 4) lies inside [0, pz): the z-halo
+// element of a seam comes from the overlap, never from out-of-bounds reads.
+constexpr int kZB = kZT + 4;
+__host__ __device__ inline bool rsingle(const Grid &g) { return g.nzh <= kZT; }
+__host__ __device__ inline int rbox0(const Grid &g) { return rsingle(g) ? g.pz : kZB; }
+__host__ __device__ inline int rntiles(const Grid &g) {
+  return rsingle(g) ? 1 : (g.nzh + kZT - 1) / kZT;
+}
+__host__ __device__ inline int rtile_c0(const Grid &g, int kz0) {
+  if (rsingle(g)) return 0;
+  int c0 = kz0 - 4;
+  if (c0 < 0) c0 = 0;
+  if (c0 > g.pz - kZB) c0 = g.pz - kZB;
+  return c0;
+}
+// residual ring slot: (TY + 2) rows of rbox0 doubles
+__host__ __device__ inline int rslot_doubles() {
+  return round128((kTY + 2) * kZB * 8) / 8;
+}
+
+__device__ __forceinline__ double2 lds2(const double *p) {
+  return *reinterpret_cast<const double2 *>(p);
 }
 
 }  // namespace
 
+// ============================================================================
+// half-sweep (optionally fused with the prolongation of the other colour)
 // one TMA box = (pz doubles) x (TY+2 rows) x (1 plane)
+// ============================================================================
+template <bool PROLONG>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
-                   int color) {
+                   int color, Grid C, double alpha) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int pz = g.pz;
   const int sd = slot_doubles(pz);
@@ -127,6 +173,41 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   const double *__restrict__ fown = color ? g.fB : g.fR;
   const int nch = (g.nzh + 63) >> 6;  // 64 half-entries per warp pass
 
+  // PROLONG: add alpha * e(parent) to the ring copy of local plane il (rows
+  // j0-1 .. j0+TY).  The corrected other colour is NOT written back: the
+  // half-sweep of the other colour that follows overwrites every one of its
+  // cells without reading them (and a write-back would race with the TMA
+  // halo reads of neighbouring CTAs).
+  auto correct = [&](int q) {
+    const int il = i0 - 1 + q;
+    const int i = g.x0 + il;
+    if (i < 0 || i >= g.nx) return;  // physical ghost plane stays 0
+    double *slot = ring + (size_t)(q % kSlots) * sd;
+    const int I = i >> 1;
+    for (int rr = warp; rr < kTY + 2; rr += kTY) {
+      const int jj = j0 - 1 + rr;
+      if (jj < 0 || jj >= g.ny) continue;
+      const int J = jj >> 1;
+      const long long cb = (long long)(I - C.x0 + 1) * C.plane +
+                           (long long)(J + 1) * C.pz;
+      double *row = slot + rr * pz;
+      for (int k = 2 * lane; k < g.nzh; k += 64) {
+        // parents of half-indices k, k+1 are coarse z = k, k+1: one red and
+        // one black coarse cell at coarse half-index k/2
+        const int c0 = (I + J + k) & 1;
+        const double e0 = (c0 ? C.phiB : C.phiR)[cb + (k >> 1)];
+        const double e1 = (c0 ? C.phiR : C.phiB)[cb + (k >> 1)];
+        double2 v = lds2(row + k);
+        v.x = v.x + alpha * e0;
+        v.y = v.y + alpha * e1;
+        if (k + 1 < g.nzh)
+          *reinterpret_cast<double2 *>(row + k) = v;
+        else
+          row[k] = v.x;
+      }
+    }
+  };
+
   // f of the first plane into registers
   double2 fr[4];
 #pragma unroll
@@ -140,9 +221,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   for (int il = i0; il < i1; il++) {
     const int q = il - i0 + 1;  // ring index of the current plane
     __syncthreads();            // everybody is done with plane q-2's slot
-    if (threadIdx.x == 0 && q + 3 < nplanes && q + 3 >= 4) {
+    if (threadIdx.x == 0 && q + 3 < nplanes) {
       const int s = (q + 3) % kSlots;
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      fence_proxy_async();
       mbar_expect_tx(&bars[s], box_bytes);
       tma_load_3d(ring + (size_t)s * sd, &tm_oth, 0, j0, i0 + q + 3, &bars[s]);
     }
@@ -152,6 +233,14 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       mbar_wait(&bars[1], 0);
     }
     mbar_wait(&bars[(q + 1) % kSlots], ((q + 1) / kSlots) & 1);
+    if (PROLONG) {
+      if (q == 1) {
+        correct(0);
+        correct(1);
+      }
+      correct(q + 1);
+      __syncthreads();
+    }
 
     // prefetch f of the next plane
     double2 fn[4];
@@ -174,11 +263,11 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       for (int c = 0; c < 4; c++) {
         const int k = 2 * lane + 64 * c;
         if (c >= nch || k >= g.nzh) continue;
-        const double2 a = *reinterpret_cast<const double2 *>(xm + k);
-        const double2 b = *reinterpret_cast<const double2 *>(xp + k);
-        const double2 ym = *reinterpret_cast<const double2 *>(cur - pz + k);
-        const double2 yp = *reinterpret_cast<const double2 *>(cur + pz + k);
-        const double2 zc = *reinterpret_cast<const double2 *>(cur + k);
+        const double2 a = lds2(xm + k);
+        const double2 b = lds2(xp + k);
+        const double2 ym = lds2(cur - pz + k);
+        const double2 yp = lds2(cur + pz + k);
+        const double2 zc = lds2(cur + k);
         double zm0, zp0, zm1, zp1;
         if (p == 0) {
           zm0 = (k > 0) ? cur[k - 1] : 0.0;
@@ -207,6 +296,220 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     }
 #pragma unroll
     for (int c = 0; c < 4; c++) fr[c] = fn[c];
+  }
+}
+
+// ============================================================================
+// residual kernels: two rings (Phi^R, Phi^B), z-tiles of ZT half-entries with
+// one halo element each side; box = (ZT+2) x (TY+2 rows) x (1 plane)
+// ============================================================================
+enum { MODE_RESTRICT = 0, MODE_NORM = 1 };
+
+template <int MODE>
+__global__ void __launch_bounds__(kThreadsM, 2)
+    k_resid_march(Grid g, const __grid_constant__ CUtensorMap tmR,
+                  const __grid_constant__ CUtensorMap tmB, Grid C,
+                  double *partials) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int W = rbox0(g);  // smem row width = TMA box width
+  const int sd = rslot_doubles();
+  double *ringR = reinterpret_cast<double *>(smem);
+  double *ringB = ringR + (size_t)kSlots * sd;
+  double *xch = ringB + (size_t)kSlots * sd;  // [TY/2][ZT] row-pair exchange
+  unsigned long long *bars =
+      reinterpret_cast<unsigned long long *>(xch + (kTY / 2) * kZT);
+  __shared__ double red_sh[32];
+  const unsigned box_bytes = (unsigned)((kTY + 2) * W * 8);
+
+  const int nzt = rntiles(g);
+  const int nrt = (g.ny + kTY - 1) / kTY;
+  int b = blockIdx.x;
+  const int zt = b % nzt;
+  b /= nzt;
+  const int rt = b % nrt;
+  const int xc = b / nrt;
+  const int kz0 = zt * kZT;
+  const int c0z = rtile_c0(g, kz0);
+  const int zoff = kz0 - c0z;  // smem column of half-index kz0
+  const int j0 = rt * kTY;
+  const int i0 = xc * kICH;
+  const int i1 = min(i0 + kICH, g.nxl);
+  const int nplanes = (i1 - i0) + 2;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kSlots; s++) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int q) {
+    const int s = q % kSlots;
+    mbar_expect_tx(&bars[s], 2 * box_bytes);
+    tma_load_3d(ringR + (size_t)s * sd, &tmR, c0z, j0, i0 + q, &bars[s]);
+    tma_load_3d(ringB + (size_t)s * sd, &tmB, c0z, j0, i0 + q, &bars[s]);
+  };
+  if (threadIdx.x == 0) {
+    const int np = nplanes < 4 ? nplanes : 4;
+    for (int q = 0; q < np; q++) issue(q);
+  }
+
+  const int j = j0 + warp;
+  const bool row_ok = j < g.ny;
+  double acc = 0.0;
+  double sdx0[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // restriction, even plane
+
+  // f of both colours, first plane
+  double2 fR[2], fB[2];
+#pragma unroll
+  for (int c = 0; c < 2; c++) {
+    const int k = kz0 + 2 * lane + 64 * c;
+    if (row_ok && k < g.nzh) {
+      const long long o = (long long)(i0 + 1) * g.plane + (long long)(j + 1) * g.pz + k;
+      fR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
+      fB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+    }
+  }
+
+  for (int il = i0; il < i1; il++) {
+    const int q = il - i0 + 1;
+    __syncthreads();
+    if (threadIdx.x == 0 && q + 3 < nplanes) {
+      fence_proxy_async();
+      issue(q + 3);
+    }
+    if (q == 1) {
+      mbar_wait(&bars[0], 0);
+      mbar_wait(&bars[1], 0);
+    }
+    mbar_wait(&bars[(q + 1) % kSlots], ((q + 1) / kSlots) & 1);
+
+    double2 nR[2], nB[2];
+    const bool more = il + 1 < i1;
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      const int k = kz0 + 2 * lane + 64 * c;
+      if (more && row_ok && k < g.nzh) {
+        const long long o = (long long)(il + 2) * g.plane + (long long)(j + 1) * g.pz + k;
+        nR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
+        nB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+      }
+    }
+    const int i = g.x0 + il;
+    double pr[2][2];  // [chunk][element] red + black pair sums (restriction)
+#pragma unroll
+    for (int c = 0; c < 2; c++) pr[c][0] = pr[c][1] = 0.0;
+    if (row_ok) {
+      const size_t oc = (size_t)(q % kSlots) * sd + (warp + 1) * W + zoff;
+      const size_t om = (size_t)((q - 1) % kSlots) * sd + (warp + 1) * W + zoff;
+      const size_t op = (size_t)((q + 1) % kSlots) * sd + (warp + 1) * W + zoff;
+#pragma unroll
+      for (int c = 0; c < 2; c++) {
+        const int kl = 2 * lane + 64 * c;  // tile-relative half-index
+        const int k = kz0 + kl;
+        if (k >= g.nzh) continue;
+        double r[2][2];  // [colour][element]
+#pragma unroll
+        for (int col = 0; col < 2; col++) {
+          const double *O = col ? ringR : ringB;  // other colour's ring
+          const double *M = col ? ringB : ringR;  // own colour's ring
+          const int p = (i + j + col) & 1;
+          const double2 a = lds2(O + om + kl);
+          const double2 bb = lds2(O + op + kl);
+          const double2 ym = lds2(O + oc - W + kl);
+          const double2 yp = lds2(O + oc + W + kl);
+          const double2 zc = lds2(O + oc + kl);
+          const double2 u = lds2(M + oc + kl);
+          // z neighbours; the halo element is 0 outside the level
+          double zm0, zp0, zm1, zp1;
+          if (p == 0) {
+            zm0 = (k > 0) ? O[oc + kl - 1] : 0.0;
+            zp0 = zc.x;
+            zm1 = zc.x;
+            zp1 = zc.y;
+          } else {
+            zm0 = zc.x;
+            zp0 = zc.y;
+            zm1 = zc.y;
+            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : 0.0;
+          }
+          const double s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
+          const double s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
+          const int z0 = 2 * k + p;
+          const double d0 = (double)centre_dm(g, i, j, z0);
+          const double d1 = (double)centre_dm(g, i, j, z0 + 2);
+          const double t0 = d0 * u.x - s0;
+          const double t1 = d1 * u.y - s1;
+          const double2 fo = col ? fB[c] : fR[c];
+          r[col][0] = fo.x - g.c * t0;
+          r[col][1] = (k + 1 < g.nzh) ? fo.y - g.c * t1 : 0.0;
+        }
+        if (MODE == MODE_NORM) {
+          acc = acc + r[0][0] * r[0][0];
+          acc = acc + r[0][1] * r[0][1];
+          acc = acc + r[1][0] * r[1][0];
+          acc = acc + r[1][1] * r[1][1];
+        } else {
+          // z-children of coarse K = k are the red and black cells at
+          // half-index k (commutative pair: r_dz0 + r_dz1)
+          pr[c][0] = r[0][0] + r[1][0];
+          pr[c][1] = r[0][1] + r[1][1];
+        }
+      }
+    }
+    if (MODE == MODE_RESTRICT) {
+      // y-children: rows 2J (even warp) + 2J+1 (odd warp), in that order
+      if (warp & 1) {
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const int kl = 2 * lane + 64 * c;
+          xch[(warp >> 1) * kZT + kl] = pr[c][0];
+          xch[(warp >> 1) * kZT + kl + 1] = pr[c][1];
+        }
+      }
+      __syncthreads();
+      if (!(warp & 1) && row_ok) {
+        const bool odd_plane = (il & 1);
+        const int J = j >> 1;
+        const int I = i >> 1;
+#pragma unroll
+        for (int c = 0; c < 2; c++) {
+          const int kl = 2 * lane + 64 * c;
+          const int k = kz0 + kl;
+          if (k >= g.nzh) continue;
+          const double s0 = pr[c][0] + xch[(warp >> 1) * kZT + kl];
+          const double s1 = pr[c][1] + xch[(warp >> 1) * kZT + kl + 1];
+          if (!odd_plane) {
+            sdx0[c][0] = s0;
+            sdx0[c][1] = s1;
+          } else {
+            // coarse cells K = k and k+1: one of each colour at K/2 = k/2
+            const long long cb = (long long)(I - C.x0 + 1) * C.plane +
+                                 (long long)(J + 1) * C.pz + (k >> 1);
+            const int c0 = (I + J + k) & 1;
+            (c0 ? C.fB : C.fR)[cb] = 0.125 * (sdx0[c][0] + s0);
+            if (k + 1 < g.nzh) (c0 ? C.fR : C.fB)[cb] = 0.125 * (sdx0[c][1] + s1);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < 2; c++) {
+      fR[c] = nR[c];
+      fB[c] = nB[c];
+    }
+  }
+  if (MODE == MODE_NORM) {
+    // deterministic block reduction
+    double v = acc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) red_sh[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0.0;
+      for (int w = 0; w < kTY; w++) s = s + red_sh[w];
+      partials[blockIdx.x] = s;
+    }
   }
 }
 
@@ -239,18 +542,24 @@ bool march_supported(const Grid &g) {
          get_encode() != nullptr;
 }
 
-size_t march_smem_bytes(const Grid &g) {
+static size_t smooth_smem_bytes(const Grid &g) {
   return (size_t)kSlots * slot_doubles(g.pz) * 8 + kSlots * 8;
 }
 
-bool make_tmap_field(const Grid &g, const double *base, void *out128) {
+static size_t resid_smem_bytes() {
+  return (size_t)2 * kSlots * rslot_doubles() * 8 + (kTY / 2) * kZT * 8 +
+         kSlots * 8;
+}
+
+static bool encode(const Grid &g, const double *base, void *out128,
+                   cuuint32_t box0) {
   PFN_encodeTiled enc = get_encode();
   if (!enc) return false;
   CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(out128);
   cuuint64_t dims[3] = {(cuuint64_t)g.pz, (cuuint64_t)(g.ny + 2),
                         (cuuint64_t)(g.nxl + 2)};
   cuuint64_t strides[2] = {(cuuint64_t)g.pz * 8, (cuuint64_t)g.plane * 8};
-  cuuint32_t box[3] = {(cuuint32_t)g.pz, (cuuint32_t)(kTY + 2), 1};
+  cuuint32_t box[3] = {box0, (cuuint32_t)(kTY + 2), 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                    const_cast<double *>(base), dims, strides, box, es,
@@ -260,20 +569,77 @@ bool make_tmap_field(const Grid &g, const double *base, void *out128) {
   return r == CUDA_SUCCESS;
 }
 
+bool make_tmap_field(const Grid &g, const double *base, void *out128) {
+  return encode(g, base, out128, (cuuint32_t)g.pz);
+}
+
+bool make_tmap_resid(const Grid &g, const double *base, void *out128) {
+  return encode(g, base, out128, (cuuint32_t)rbox0(g));
+}
+
+// raise a kernel's dynamic shared-memory limit to `bytes` (once per size)
+template <typename K>
+static void set_smem(K kernel, size_t bytes, size_t *configured) {
+  if (bytes > *configured) {
+    cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)bytes);
+    *configured = bytes;
+  }
+}
+
 void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
                          cudaStream_t s) {
   const int nrt = (g.ny + kTY - 1) / kTY;
   const int nxc = (g.nxl + kICH - 1) / kICH;
-  const size_t smem = march_smem_bytes(g);
+  const size_t smem = smooth_smem_bytes(g);
   static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(k_smooth_march,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    configured = smem;
-  }
+  set_smem(k_smooth_march<false>, smem, &configured);
   const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm_oth128);
-  k_smooth_march<<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color);
+  k_smooth_march<false><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, g, 0.0);
+}
+
+void launch_prolong_smooth_march(const Grid &g, const Grid &c,
+                                 const void *tm_oth128, int color, double alpha,
+                                 cudaStream_t s) {
+  const int nrt = (g.ny + kTY - 1) / kTY;
+  const int nxc = (g.nxl + kICH - 1) / kICH;
+  const size_t smem = smooth_smem_bytes(g);
+  static size_t configured = 0;
+  set_smem(k_smooth_march<true>, smem, &configured);
+  const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm_oth128);
+  k_smooth_march<true><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
+}
+
+static int resid_blocks(const Grid &g) {
+  const int nzt = rntiles(g);
+  const int nrt = (g.ny + kTY - 1) / kTY;
+  const int nxc = (g.nxl + kICH - 1) / kICH;
+  return nzt * nrt * nxc;
+}
+
+bool resid_march_supported(const Grid &g) {
+  return g.nzh >= 64 && g.pz <= 256 && g.ny >= kTY && g.nxl >= 2 &&
+         (g.nxl % 2) == 0 && (g.ny % 2) == 0 && get_encode() != nullptr;
+}
+
+void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
+                                 const void *tmB, cudaStream_t s) {
+  static size_t configured = 0;
+  set_smem(k_resid_march<MODE_RESTRICT>, resid_smem_bytes(), &configured);
+  k_resid_march<MODE_RESTRICT><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
+      g, *reinterpret_cast<const CUtensorMap *>(tmR),
+      *reinterpret_cast<const CUtensorMap *>(tmB), c, nullptr);
+}
+
+int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
+
+void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
+                       double *partials, cudaStream_t s) {
+  static size_t configured = 0;
+  set_smem(k_resid_march<MODE_NORM>, resid_smem_bytes(), &configured);
+  k_resid_march<MODE_NORM><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
+      g, *reinterpret_cast<const CUtensorMap *>(tmR),
+      *reinterpret_cast<const CUtensorMap *>(tmB), g, partials);
 }
 
 }  // namespace mg

@@ -111,7 +111,11 @@ def test_half_sweep_from_zero_bitwise(mg):
     ((8, 8, 8), 1.0 / 8, "dirichlet", 2),
     ((16, 8, 12), 1.0, "mixed", 2),
     ((64, 32, 32), 1.0, "channel", 4),
-    ((32, 32, 32), 1.0 / 32, "dirichlet0", 4)])
+    ((32, 32, 32), 1.0 / 32, "dirichlet0", 4),
+    # z-tiled TMA residual+restriction kernel (nz/2 >= 64), 1 and 2 z-tiles
+    ((32, 16, 128), 1.0, "mixed", 2),
+    ((16, 24, 512), 0.5, "channel", 2),
+    ((48, 8, 136), 1.0, "dirichlet", 2)])
 def test_residual_restrict_and_prolong_bitwise(mg, shape, h, bc, mc):
     s, o = pair(mg, shape, h, bc, min_coarse=mc)
     assert s.nlevels == o.nlevels >= 2
@@ -314,3 +318,36 @@ def test_errors(mg):
         for _ in range(20):
             s.vcycle()
     assert e.value.code == mg.MG_ERR_DIVERGED
+
+
+@pytest.mark.parametrize("shape,bc", [((32, 24, 256), "mixed"),
+                                      ((64, 16, 128), "channel"),
+                                      ((16, 16, 512), "dirichlet")])
+def test_march_kernels_equal_direct_kernels(mg, shape, bc, monkeypatch):
+    """The TMA-marching kernels (half-sweep, prolongation fused with the
+    first post-smoothing red sweep, residual+restriction, norm) give the same
+    V-cycle iterates as the direct-load kernels, bit for bit."""
+    f = np.random.default_rng(12).uniform(-1, 1, shape)
+    out = []
+    for no_march in (False, True):
+        if no_march:
+            monkeypatch.setenv("MG_NO_MARCH", "1")
+        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2)
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(3)]
+        out.append((r, s.get_solution()))
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
+
+
+def test_march_norm_matches_oracle(mg):
+    shape = (48, 16, 256)
+    s, o = pair(mg, shape, 1.0, "mixed", min_coarse=2)
+    rng = np.random.default_rng(13)
+    phi = rng.uniform(-1, 1, shape)
+    f = rng.uniform(-1, 1, shape)
+    s.set_solution(phi)
+    s.set_rhs(f)
+    o.set_phi(phi)
+    o.set_rhs(f)
+    assert abs(s.residual_norm() - o.residual_norm()) <= 1e-13 * o.residual_norm()
