@@ -317,10 +317,14 @@ void launch_sum_ordered(const double *parts, int n, double *out,
 
 // ---------------------------------------------------------------------------
 // Coarsest-grid CG: one CTA, Hestenes-Stiefel from x = 0, stop at
-// ||r|| <= tol ||b|| or maxit.  Vectors in natural order in `scratch`
-// (L1/L2-resident); the operator is the same closed form as the smoother.
+// ||r|| <= tol ||b|| or maxit.  Vectors in natural order, in shared memory
+// when they fit (else in `scratch`, L1/L2-resident); the operator is the same
+// closed form as the smoother.  Dot products: per-thread partials in a fixed
+// order, warp shuffle tree, then every thread sums the warp partials in
+// warp order (one barrier per dot; two alternating partial arrays).
 // ---------------------------------------------------------------------------
 static constexpr int kCgThreads = 1024;
+static constexpr long long kCgSmemMax = 6144;  // unknowns with smem vectors
 
 __device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
                                                  int z, int *col) {
@@ -346,18 +350,27 @@ __device__ __forceinline__ double cg_apply(const Grid &g, const double *v,
   return g.c * (d * v[n] - s);
 }
 
-__device__ double cg_dot(const double *a, const double *b, long long N,
-                         double *sh) {
-  double acc = 0.0;
-  for (long long n = threadIdx.x; n < N; n += blockDim.x) acc = acc + a[n] * b[n];
-  return block_sum(acc, sh);
+// sum over the block of per-thread values; one barrier; all threads get it
+__device__ __forceinline__ double cg_allsum(double v, double *part) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double s = 0.0;
+  for (int w = 0; w < nw; w++) s = s + part[w];
+  return s;
 }
 
 __global__ void __launch_bounds__(kCgThreads)
     k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
-  __shared__ double sh[32];
+  extern __shared__ double cg_sm[];
+  __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
-  double *x = scr, *r = scr + N, *p = scr + 2 * N, *q = scr + 3 * N;
+  double *base = (N <= kCgSmemMax) ? cg_sm : scr;
+  double *x = base, *r = base + N, *p = base + 2 * N, *q = base + 3 * N;
+  int pb = 0;
+  double acc = 0.0;
   for (long long n = threadIdx.x; n < N; n += blockDim.x) {
     const int z = (int)(n % g.nz);
     const long long t = n / g.nz;
@@ -367,28 +380,37 @@ __global__ void __launch_bounds__(kCgThreads)
     x[n] = 0.0;
     r[n] = b;
     p[n] = b;
+    acc = acc + b * b;
   }
-  __syncthreads();
-  double rho = cg_dot(r, r, N, sh);
+  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes p
+  pb ^= 1;
   const double bnorm = sqrt(rho);
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
-      for (long long n = threadIdx.x; n < N; n += blockDim.x) q[n] = cg_apply(g, p, n);
-      __syncthreads();
-      const double pq = cg_dot(p, q, N, sh);
+      acc = 0.0;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+        const double qn = cg_apply(g, p, n);
+        q[n] = qn;
+        acc = acc + p[n] * qn;
+      }
+      const double pq = cg_allsum(acc, part[pb]);
+      pb ^= 1;
       const double a = rho / pq;
+      acc = 0.0;
       for (long long n = threadIdx.x; n < N; n += blockDim.x) {
         x[n] = x[n] + a * p[n];
-        r[n] = r[n] - a * q[n];
+        const double rn = r[n] - a * q[n];
+        r[n] = rn;
+        acc = acc + rn * rn;
       }
-      __syncthreads();
-      const double rho1 = cg_dot(r, r, N, sh);
+      const double rho1 = cg_allsum(acc, part[pb]);
+      pb ^= 1;
       it++;
       if (sqrt(rho1) <= tol * bnorm) break;
       const double beta = rho1 / rho;
       for (long long n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
-      __syncthreads();
+      __syncthreads();  // p complete before the next matrix-vector product
       rho = rho1;
     }
   }
@@ -409,7 +431,20 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
 
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
-  k_coarse_cg<<<1, kCgThreads, 0, s>>>(g, scratch, tol, maxit, iters_out);
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  int threads = (int)((N + 31) / 32 * 32);
+  if (threads > kCgThreads) threads = kCgThreads;
+  size_t smem = 0;
+  if (N <= kCgSmemMax) {
+    smem = 4 * (size_t)N * sizeof(double);
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+      cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem);
+      configured = smem;
+    }
+  }
+  k_coarse_cg<<<1, threads, smem, s>>>(g, scratch, tol, maxit, iters_out);
 }
 
 // ---------------------------------------------------------------------------

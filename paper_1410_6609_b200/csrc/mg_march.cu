@@ -177,36 +177,58 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   // j0-1 .. j0+TY).  The corrected other colour is NOT written back: the
   // half-sweep of the other colour that follows overwrites every one of its
   // cells without reading them (and a write-back would race with the TMA
-  // halo reads of neighbouring CTAs).
-  auto correct = [&](int q) {
-    const int il = i0 - 1 + q;
-    const int i = g.x0 + il;
-    if (i < 0 || i >= g.nx) return;  // physical ghost plane stays 0
-    double *slot = ring + (size_t)(q % kSlots) * sd;
+  // halo reads of neighbouring CTAs).  The coarse values are loaded one plane
+  // ahead (load_e) so their latency hides behind the previous plane's work.
+  // Work split: task t = (row rr, 64-wide chunk c), t = warp + TY*m.
+  constexpr int kMaxTask = (kTY + 2) * 4;
+  constexpr int kTPW = (kMaxTask + kTY - 1) / kTY;  // tasks per warp
+  const int ntask = (kTY + 2) * nch;
+  auto load_e = [&](int q, double2 *E) {
+    const int i = g.x0 + i0 - 1 + q;
     const int I = i >> 1;
-    for (int rr = warp; rr < kTY + 2; rr += kTY) {
+#pragma unroll
+    for (int m = 0; m < kTPW; m++) {
+      const int t = warp + kTY * m;
+      E[m] = make_double2(0.0, 0.0);
+      if (!PROLONG || t >= ntask || i < 0 || i >= g.nx) continue;
+      const int rr = t / nch, c = t % nch;
       const int jj = j0 - 1 + rr;
-      if (jj < 0 || jj >= g.ny) continue;
+      const int k = 2 * lane + 64 * c;
+      if (jj < 0 || jj >= g.ny || k >= g.nzh) continue;
       const int J = jj >> 1;
+      // parents of half-indices k, k+1 are coarse z = k, k+1: one red and
+      // one black coarse cell at coarse half-index k/2
       const long long cb = (long long)(I - C.x0 + 1) * C.plane +
-                           (long long)(J + 1) * C.pz;
-      double *row = slot + rr * pz;
-      for (int k = 2 * lane; k < g.nzh; k += 64) {
-        // parents of half-indices k, k+1 are coarse z = k, k+1: one red and
-        // one black coarse cell at coarse half-index k/2
-        const int c0 = (I + J + k) & 1;
-        const double e0 = (c0 ? C.phiB : C.phiR)[cb + (k >> 1)];
-        const double e1 = (c0 ? C.phiR : C.phiB)[cb + (k >> 1)];
-        double2 v = lds2(row + k);
-        v.x = v.x + alpha * e0;
-        v.y = v.y + alpha * e1;
-        if (k + 1 < g.nzh)
-          *reinterpret_cast<double2 *>(row + k) = v;
-        else
-          row[k] = v.x;
-      }
+                           (long long)(J + 1) * C.pz + (k >> 1);
+      const int c0 = (I + J + k) & 1;
+      E[m].x = (c0 ? C.phiB : C.phiR)[cb];
+      E[m].y = (c0 ? C.phiR : C.phiB)[cb];
     }
   };
+  auto apply_e = [&](int q, const double2 *E) {
+    const int i = g.x0 + i0 - 1 + q;
+    if (i < 0 || i >= g.nx) return;  // physical ghost plane stays 0
+    double *slot = ring + (size_t)(q % kSlots) * sd;
+#pragma unroll
+    for (int m = 0; m < kTPW; m++) {
+      const int t = warp + kTY * m;
+      if (t >= ntask) continue;
+      const int rr = t / nch, c = t % nch;
+      const int jj = j0 - 1 + rr;
+      const int k = 2 * lane + 64 * c;
+      if (jj < 0 || jj >= g.ny || k >= g.nzh) continue;
+      double *row = slot + rr * pz;
+      double2 v = lds2(row + k);
+      v.x = v.x + alpha * E[m].x;
+      v.y = v.y + alpha * E[m].y;
+      if (k + 1 < g.nzh)
+        *reinterpret_cast<double2 *>(row + k) = v;
+      else
+        row[k] = v.x;
+    }
+  };
+  double2 E[kTPW];
+  if (PROLONG && nplanes > 2) load_e(2, E);
 
   // f of the first plane into registers
   double2 fr[4];
@@ -235,10 +257,14 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     mbar_wait(&bars[(q + 1) % kSlots], ((q + 1) / kSlots) & 1);
     if (PROLONG) {
       if (q == 1) {
-        correct(0);
-        correct(1);
+        double2 E0[kTPW];
+        load_e(0, E0);
+        apply_e(0, E0);
+        load_e(1, E0);
+        apply_e(1, E0);
       }
-      correct(q + 1);
+      apply_e(q + 1, E);
+      if (q + 2 < nplanes) load_e(q + 2, E);
       __syncthreads();
     }
 
