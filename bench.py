@@ -193,9 +193,9 @@ def run_cuda(args):
     workload = args.workload or ("cfg3" if N == 1 else "cfg4")
     kw = dict(min_coarse=8, nu1=2, nu2=2)
     if N > 1:
-        uid = [mg.nccl_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(uid, src=0)
-        kw.update(nranks=N, rank=rank, halo="nccl", nccl_id=uid[0])
+        from paper_1410_6609_b200 import dist as D
+        uid = D.share_nccl_id(rank, mg.nccl_unique_id)
+        kw.update(nranks=N, rank=rank, halo="nccl", nccl_id=uid)
     stream = torch.cuda.Stream(device=local)
     if workload == "cfg3":
         assert N == 1, "cfg3 is the single-GPU configuration"
@@ -241,9 +241,8 @@ def run_cuda(args):
     ms = e0.elapsed_time(e1)
     ck = clocks.stop()
     if dist is not None:
-        t = torch.tensor([ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        from paper_1410_6609_b200 import dist as D
+        ms = D.max_over_ranks(ms, device="cuda")
     launches = s.cycle_launches
 
     # ---- roofline of the dominant kernel (level-0 RBGS half-sweep), live ----

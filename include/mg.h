@@ -138,6 +138,21 @@ const char *mg_strerror(int code);
  * cannot be loaded.  Needs no GPU. */
 int mg_nccl_unique_id(unsigned char out[128]);
 
+/* ---- solid mask (config 5) -------------------------------------------------- */
+/* Mark solid cells (solid[i] != 0), natural layout of the WHOLE domain
+ * (nx*ny*nz bytes, every rank passes the full array).  Solid cells are not
+ * unknowns, their f is 0, and the faces between fluid and solid cells are
+ * homogeneous Neumann (reading c19).  Coarse operators are the
+ * Galerkin R A P of the masked operator, held in the exact
+ * face-transmissibility form.  Switches the context to the
+ * variable-coefficient kernels.  solid == NULL removes the mask.  Call before
+ * setting the RHS (the RHS is re-zeroed on solid cells). */
+int mg_set_mask(mg_ctx *ctx, const uint8_t *solid, int where);
+/* The operator of level l as 7 coefficients per cell [centre, x-, x+, y-, y+,
+ * z-, z+] (natural layout, the caller's part as mg_get_field), zeros on solid
+ * cells.  For tests against the oracle's Galerkin stencils. */
+int mg_get_stencil(mg_ctx *ctx, int level, double *out, int where);
+
 /* ---- right-hand side ----------------------------------------------------- */
 /* f := charge density of n uniformly charged spheres: every cell
  * whose centre satisfies |x_c - c_p|^2 <= R_p^2 (inclusive, reading

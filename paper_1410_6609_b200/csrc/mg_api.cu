@@ -181,6 +181,8 @@ struct mg_ctx {
   Plan pl;
   std::vector<std::vector<TmPair>> tm;
   int use_march = 1;
+  bool masked = false;            // solid mask set (variable coefficients)
+  std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   double h;
   mg_bc bc[6];
   mg_opts o;
@@ -339,7 +341,9 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
   for (size_t s = 0; s < c->g[l].size(); s++) {
     const Grid &g = c->g[l][s];
     const TmPair &t = c->tm[l][s];
-    if (!from_zero && t.ok && c->use_march)
+    if (c->masked)
+      mg::launch_smooth_var(g, color, from_zero, c->stream);
+    else if (!from_zero && t.ok && c->use_march)
       mg::launch_smooth_march(g, color ? t.r : t.b, color, c->stream);
     else
       mg::launch_smooth(g, color, from_zero, c->stream);
@@ -356,7 +360,9 @@ int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
   for (int s = 0; s < (int)c->g[l].size(); s++) {
     const TmPair &t = c->tm[l][s];
-    if (t.ok_resid && c->use_march)
+    if (c->masked)
+      mg::launch_resid_restrict_var(c->g[l][s], coarse_of(c, l, s), c->stream);
+    else if (t.ok_resid && c->use_march)
       mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
                                       c->stream);
     else
@@ -382,7 +388,10 @@ int restrict_level(mg_ctx *c, int l) {
 int prolong_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
   for (int s = 0; s < (int)c->g[l].size(); s++) {
-    mg::launch_prolong(c->g[l][s], coarse_of(c, l, s), 0, c->o.alpha, c->stream);
+    if (c->masked)
+      mg::launch_prolong_var(c->g[l][s], coarse_of(c, l, s), c->o.alpha, c->stream);
+    else
+      mg::launch_prolong(c->g[l][s], coarse_of(c, l, s), 0, c->o.alpha, c->stream);
     c->launches++;
   }
   if (l == 0) mark(c, CAT_PROLONG0);
@@ -392,7 +401,7 @@ int prolong_level(mg_ctx *c, int l) {
 
 // can level l use the fused prolongation + first post-smoothing red sweep?
 bool can_fuse_prolong(const mg_ctx *c, int l) {
-  if (!c->use_march || c->o.nu2 < 1) return false;
+  if (!c->use_march || c->masked || c->o.nu2 < 1) return false;
   for (const TmPair &t : c->tm[l])
     if (!t.ok) return false;
   return true;
@@ -413,8 +422,12 @@ int prolong_red_level(mg_ctx *c, int l) {
 
 int coarse_solve(mg_ctx *c) {
   const Grid &g = c->g[c->pl.L - 1][0];
-  mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
-                       c->cg_iters, c->stream);
+  if (c->masked)
+    mg::launch_coarse_cg_var(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
+                             c->cg_iters, c->stream);
+  else
+    mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
+                         c->cg_iters, c->stream);
   c->launches++;
   CK(cudaGetLastError());
   return MG_OK;
@@ -427,7 +440,9 @@ int enqueue_norm(mg_ctx *c) {
   for (size_t s = 0; s < c->g[0].size(); s++) {
     const Grid &g = c->g[0][s];
     const TmPair &t = c->tm[0][s];
-    if (t.ok_resid && c->use_march) {
+    if (c->masked) {
+      off += mg::launch_norm_partials_var(g, c->partials + off, c->stream);
+    } else if (t.ok_resid && c->use_march) {
       mg::launch_norm_march(g, t.rr, t.rb, c->partials + off, c->stream);
       off += mg::norm_march_blocks(g);
     } else {
@@ -566,9 +581,23 @@ int bc_adapt(mg_ctx *c) {
     types[q] = c->bc[q].type;
     terms[q] = c->bc[q].type == MG_DIRICHLET ? 2.0 * alpha * g : alpha * (c->h * g);
   }
-  for (const Grid &g : c->g[0]) mg::launch_bc_adapt(g, terms, types, c->stream);
+  for (const Grid &g : c->g[0]) {
+    mg::launch_zero_solid(g, c->stream);  // masked cells are not unknowns
+    mg::launch_bc_adapt(g, terms, types, c->stream);
+  }
   CK(cudaGetLastError());
   return MG_OK;
+}
+
+void free_mask(mg_ctx *c) {
+  for (void *p : c->mask_bufs) cudaFree(p);
+  c->mask_bufs.clear();
+  for (auto &lv : c->g)
+    for (Grid &g : lv) {
+      g.codeR = g.codeB = nullptr;
+      g.coefR = g.coefB = nullptr;
+    }
+  c->masked = false;
 }
 
 int residual_norm_now(mg_ctx *c, double *out) {
@@ -812,6 +841,7 @@ void mg_destroy(mg_ctx *c) {
   if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
   if (c->stage) cudaFree(c->stage);
   if (c->sph) cudaFree(c->sph);
+  for (void *p : c->mask_bufs) cudaFree(p);
   if (c->h_norm) cudaFreeHost(c->h_norm);
   if (c->own_ws && c->ws) cudaFree(c->ws);
   if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
@@ -1005,6 +1035,99 @@ int mg_coarse_solve(mg_ctx *c, int *iters) {
   if ((rc = sync(c))) return rc;
   if (iters) memcpy(iters, c->h_norm + 1, sizeof(int));
   return MG_OK;
+}
+
+int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  CK(cudaStreamSynchronize(c->stream));
+  if (c->graph) {
+    cudaGraphExecDestroy(c->graph);
+    c->graph = nullptr;
+  }
+  free_mask(c);
+  if (!solid) return MG_OK;
+  const size_t N = (size_t)c->pl.dims[0][0] * c->pl.dims[0][1] * c->pl.dims[0][2];
+  unsigned char *dmask = nullptr;
+  CK(cudaMalloc(&dmask, N));
+  c->mask_bufs.push_back(dmask);
+  CK(cudaMemcpyAsync(dmask, solid, N,
+                     where == MG_DEVICE ? cudaMemcpyDeviceToDevice
+                                        : cudaMemcpyHostToDevice,
+                     c->stream));
+  for (int l = 0; l < c->pl.L; l++)
+    for (Grid &g : c->g[l]) {
+      const size_t ne = (size_t)mg::grid_elems(g);
+      if (l == 0) {
+        unsigned char *r = nullptr, *b = nullptr;
+        CK(cudaMalloc(&r, ne));
+        c->mask_bufs.push_back(r);
+        CK(cudaMalloc(&b, ne));
+        c->mask_bufs.push_back(b);
+        CK(cudaMemsetAsync(r, 0, ne, c->stream));
+        CK(cudaMemsetAsync(b, 0, ne, c->stream));
+        g.codeR = r;
+        g.codeB = b;
+      } else {
+        float *r = nullptr, *b = nullptr;
+        CK(cudaMalloc(&r, ne * 8 * sizeof(float)));
+        c->mask_bufs.push_back(r);
+        CK(cudaMalloc(&b, ne * 8 * sizeof(float)));
+        c->mask_bufs.push_back(b);
+        CK(cudaMemsetAsync(r, 0, ne * 8 * sizeof(float), c->stream));
+        CK(cudaMemsetAsync(b, 0, ne * 8 * sizeof(float), c->stream));
+        g.coefR = r;
+        g.coefB = b;
+      }
+    }
+  for (Grid &g : c->g[0])
+    mg::launch_mask_codes(g, dmask, const_cast<unsigned char *>(g.codeR),
+                          const_cast<unsigned char *>(g.codeB), c->stream);
+  for (int l = 0; l + 1 < c->pl.L; l++) {
+    for (int s = 0; s < (int)c->g[l].size(); s++) {
+      const Grid &cg = coarse_of(c, l, s);
+      mg::launch_coarse_coef(c->g[l][s], cg, const_cast<float *>(cg.coefR),
+                             const_cast<float *>(cg.coefB), c->stream);
+    }
+    if (l + 1 == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
+      const Grid &G = c->g[l + 1][0];
+      const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
+      float *R = const_cast<float *>(G.coefR), *B = const_cast<float *>(G.coefB);
+      int rc;
+      if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+      g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
+                       ncclFloat, c->comm, c->stream);
+      g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
+                       ncclFloat, c->comm, c->stream);
+      if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef)"))) return rc;
+    }
+  }
+  CK(cudaGetLastError());
+  c->masked = true;
+  // masked cells are not unknowns: clear their f
+  for (const Grid &g : c->g[0]) mg::launch_zero_solid(g, c->stream);
+  c->prev_norm = -1.0;
+  return sync(c);
+}
+
+int mg_get_stencil(mg_ctx *c, int l, double *out, int where) {
+  if (!c || !out || l < 0 || l >= c->pl.L) return fail(MG_ERR_ARG, "bad arguments");
+  const size_t n = level_cells_held(c, l);
+  double *dev = out;
+  int rc;
+  if (where == MG_HOST) {
+    if ((rc = stage_for(c, 7 * n * sizeof(double)))) return rc;
+    dev = c->stage;
+  }
+  size_t off = 0;
+  for (const Grid &g : c->g[l]) {
+    mg::launch_get_stencil(g, dev + 7 * off, c->stream);
+    off += (size_t)g.nxl * g.ny * g.nz;
+  }
+  CK(cudaGetLastError());
+  if (where == MG_HOST)
+    CK(cudaMemcpyAsync(out, dev, 7 * n * sizeof(double), cudaMemcpyDeviceToHost,
+                       c->stream));
+  return sync(c);
 }
 
 int mg_set_profiling(mg_ctx *c, int on) {

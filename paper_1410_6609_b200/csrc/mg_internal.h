@@ -25,6 +25,14 @@ struct Grid {
   double c;          // operator scale 2^-l / h^2   (A_l = c * S_l)
   double w;          // 2^l h^2 = 1/c
   int dface[6];      // centre contribution of a face: +1 Dirichlet, -1 Neumann
+  // solid mask (config 5), null on box domains.  Galerkin operator in face-
+  // transmissibility form: a_q = -c kappa_q, a_cc = c (sum kappa + 2 delta).
+  //   level 0:  code[e] bits 0-5 = kappa_q in {0,1} (face order x-,x+,y-,y+,
+  //             z-,z+), bit 6 = fluid; delta from the Dirichlet faces touched
+  //   level>0:  coef[8 e + q] = kappa_q (q < 6), coef[8 e + 6] = sum kappa +
+  //             2 delta (0 = solid), coef[8 e + 7] = delta  (all dyadic, exact)
+  const unsigned char *codeR, *codeB;
+  const float *coefR, *coefB;
 };
 
 __host__ __device__ inline long long grid_elems(const Grid &g) {
@@ -67,6 +75,21 @@ void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
 int norm_march_blocks(const Grid &g);
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s);
+// masked (variable-coefficient) path, mg_mask.cu
+void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
+                       unsigned char *codeR, unsigned char *codeB,
+                       cudaStream_t s);
+void launch_coarse_coef(const Grid &f, const Grid &c, float *coefR,
+                        float *coefB, cudaStream_t s);
+void launch_smooth_var(const Grid &g, int color, int from_zero, cudaStream_t s);
+void launch_resid_restrict_var(const Grid &f, const Grid &c, cudaStream_t s);
+void launch_prolong_var(const Grid &f, const Grid &c, double alpha,
+                        cudaStream_t s);
+int launch_norm_partials_var(const Grid &g, double *partials, cudaStream_t s);
+void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
+                          int *iters_out, cudaStream_t s);
+void launch_zero_solid(const Grid &g, cudaStream_t s);
+void launch_get_stencil(const Grid &g, double *out7, cudaStream_t s);
 // natural <-> split conversion of one field of a grid (phi: 0, f: 1)
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);
 void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s);

@@ -546,6 +546,9 @@ __global__ void __launch_bounds__(kThreads) k_bc_adapt(Grid g, Terms T) {
   const long long b = rowbase(g, il, j);
   const int step = full ? 1 : (g.nz - 1);
   for (int z = 0; z < g.nz; z += step) {
+    // masked cells are not unknowns (their f stays 0)
+    if (g.codeR && !((((i + j + z) & 1) ? g.codeB : g.codeR)[b + (z >> 1)] & 64))
+      continue;
     double *f = ((i + j + z) & 1) ? g.fB : g.fR;
     double v = f[b + (z >> 1)];
     const bool on[6] = {i == 0, i == g.nx - 1, j == 0,

@@ -1,0 +1,487 @@
+// Variable-coefficient (solid-mask) kernels for sm_100a: config 5.
+//
+// With solid cells (P:653-697 flags; reading c19: a masked cell is not an
+// unknown and its faces are homogeneous Neumann) the Galerkin operator
+// R A P of every level has an exact face-transmissibility form:
+//     a_q  = -c_l * kappa_q,   kappa_q = (# fluid-fluid fine face pairs
+//                                        across the coarse face) / 4^l,
+//     a_cc =  c_l * (sum_q kappa_q + 2 delta),   delta = (# fluid fine cells
+//                                        on Dirichlet faces of the block) / 4^l
+// (row sums are preserved by R A P because P 1 = 1 on fluid cells).  Every
+// coefficient is a dyadic rational with <= 13 significant bits, exact in
+// fp32 and fp64, so the GPU values equal the oracle's generic RAP stencils
+// bit for bit.  Level 0 stores one byte per cell (6 face bits + fluid bit),
+// coarse levels 8 floats per cell: kappa[6], D = sum kappa + 2 delta, delta.
+//
+// Per-cell arithmetic (bitwise equal to the oracle's (f - sum a_q phi_q)/a_cc
+// when c_l is a power of two):
+//     t   = ((((k0 x- + k1 x+) + k2 y-) + k3 y+) + k4 z-) + k5 z+
+//     Phi = (f w + t) / D,       r = f - c (D Phi - t)
+#include <cuda_runtime.h>
+
+#include "mg_internal.h"
+
+namespace mg {
+
+namespace {
+
+constexpr int kT = 256;
+
+__device__ __forceinline__ long long rb(const Grid &g, int il, int j) {
+  return (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
+}
+
+__device__ __forceinline__ int ndir(const Grid &g, int i, int j, int z) {
+  int n = 0;
+  if (i == 0 && g.dface[0] > 0) n++;
+  if (i == g.nx - 1 && g.dface[1] > 0) n++;
+  if (j == 0 && g.dface[2] > 0) n++;
+  if (j == g.ny - 1 && g.dface[3] > 0) n++;
+  if (z == 0 && g.dface[4] > 0) n++;
+  if (z == g.nz - 1 && g.dface[5] > 0) n++;
+  return n;
+}
+
+struct Coef {
+  double k[6];
+  double D;      // 0 for solid cells
+  double delta;
+};
+
+// coefficients of the cell of colour col at split element e, global (i,j,z)
+__device__ __forceinline__ void coef_at(const Grid &g, int col, long long e,
+                                        int i, int j, int z, Coef &C) {
+  if (g.coefR == nullptr) {
+    const unsigned cd = (col ? g.codeB : g.codeR)[e];
+    int n = 0;
+#pragma unroll
+    for (int q = 0; q < 6; q++) {
+      const int b = (cd >> q) & 1;
+      C.k[q] = b ? 1.0 : 0.0;
+      n += b;
+    }
+    if (cd & 64) {
+      C.delta = (double)ndir(g, i, j, z);
+      C.D = (double)n + 2.0 * C.delta;
+    } else {
+      C.delta = 0.0;
+      C.D = 0.0;
+    }
+  } else {
+    const float *r = (col ? g.coefB : g.coefR) + 8 * e;
+#pragma unroll
+    for (int q = 0; q < 6; q++) C.k[q] = (double)r[q];
+    C.D = (double)r[6];
+    C.delta = (double)r[7];
+  }
+}
+
+// t = sum_q kappa_q phi_q of the cell (il, j, z) (other colour array O)
+__device__ __forceinline__ double nbsum(const Grid &g, const double *O,
+                                        long long e, int z, const Coef &C) {
+  const int p = z & 1;
+  const double xm = O[e - g.plane], xp = O[e + g.plane];
+  const double ym = O[e - g.pz], yp = O[e + g.pz];
+  const double zm = (z > 0) ? O[e - 1 + p] : 0.0;
+  const double zp = (z < g.nz - 1) ? O[e + p] : 0.0;
+  return ((((C.k[0] * xm + C.k[1] * xp) + C.k[2] * ym) + C.k[3] * yp) +
+          C.k[4] * zm) +
+         C.k[5] * zp;
+}
+
+__device__ __forceinline__ double resid_var(const Grid &g, int il, int j, int z) {
+  const int i = g.x0 + il;
+  const int col = (i + j + z) & 1;
+  const long long e = rb(g, il, j) + (z >> 1);
+  Coef C;
+  coef_at(g, col, e, i, j, z, C);
+  if (C.D == 0.0) return 0.0;
+  const double *own = col ? g.phiB : g.phiR;
+  const double *oth = col ? g.phiR : g.phiB;
+  const double *f = col ? g.fB : g.fR;
+  const double t = nbsum(g, oth, e, z, C);
+  const double u = C.D * own[e] - t;
+  return f[e] - g.c * u;
+}
+
+__device__ __forceinline__ double block_sum_m(double v, double *sh) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  v = (threadIdx.x < nw) ? sh[threadIdx.x] : 0.0;
+  if (wid == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) sh[0] = v;
+  }
+  __syncthreads();
+  v = sh[0];
+  __syncthreads();
+  return v;
+}
+
+inline unsigned nblk(long long n) { return (unsigned)((n + kT - 1) / kT); }
+
+}  // namespace
+
+// ---- level-0 face codes from the global solid mask ---------------------------
+__global__ void __launch_bounds__(kT)
+    k_mask_codes(Grid g, const unsigned char *solid, unsigned char *codeR,
+                 unsigned char *codeB) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  auto fluid = [&](int a, int b, int c) -> bool {
+    if (a < 0 || b < 0 || c < 0 || a >= g.nx || b >= g.ny || c >= g.nz) return false;
+    return solid[((long long)a * g.ny + b) * g.nz + c] == 0;
+  };
+  unsigned char cd = 0;
+  if (fluid(i, j, z)) {
+    cd = 64;
+    if (fluid(i - 1, j, z)) cd |= 1;
+    if (fluid(i + 1, j, z)) cd |= 2;
+    if (fluid(i, j - 1, z)) cd |= 4;
+    if (fluid(i, j + 1, z)) cd |= 8;
+    if (fluid(i, j, z - 1)) cd |= 16;
+    if (fluid(i, j, z + 1)) cd |= 32;
+  }
+  (((i + j + z) & 1) ? codeB : codeR)[rb(g, il, j) + (z >> 1)] = cd;
+}
+
+void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
+                       unsigned char *codeR, unsigned char *codeB,
+                       cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0) k_mask_codes<<<nblk(n), kT, 0, s>>>(g, solid_global, codeR, codeB);
+}
+
+// ---- Galerkin coarse coefficients (face-transmissibility form) ---------------
+__global__ void __launch_bounds__(kT)
+    k_coarse_coef(Grid F, Grid C, float *coefR, float *coefB) {
+  const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)ncx * ncy * ncz) return;
+  const int K = (int)(t % ncz);
+  const long long q = t / ncz;
+  const int J = (int)(q % ncy);
+  const int Il = (int)(q / ncy);
+  float kap[6] = {0, 0, 0, 0, 0, 0};
+  float del = 0.f;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++)
+      for (int c = 0; c < 2; c++) {
+        const int il = 2 * Il + a, j = 2 * J + b, z = 2 * K + c;
+        const int i = F.x0 + il;
+        const int col = (i + j + z) & 1;
+        Coef cf;
+        coef_at(F, col, rb(F, il, j) + (z >> 1), i, j, z, cf);
+        // child faces on the coarse cell's boundary: x- (a=0), x+ (a=1), ...
+        kap[a == 0 ? 0 : 1] += (float)cf.k[a == 0 ? 0 : 1];
+        kap[b == 0 ? 2 : 3] += (float)cf.k[b == 0 ? 2 : 3];
+        kap[c == 0 ? 4 : 5] += (float)cf.k[c == 0 ? 4 : 5];
+        del += (float)cf.delta;
+      }
+  float D = 0.f;
+#pragma unroll
+  for (int r = 0; r < 6; r++) {
+    kap[r] *= 0.25f;
+    D += kap[r];
+  }
+  del *= 0.25f;
+  D += 2.f * del;
+  const int Ig = (F.x0 >> 1) + Il;
+  const int col = (Ig + J + K) & 1;
+  float *out = (col ? coefB : coefR) + 8 * (rb(C, Ig - C.x0, J) + (K >> 1));
+#pragma unroll
+  for (int r = 0; r < 6; r++) out[r] = kap[r];
+  out[6] = D;
+  out[7] = del;
+}
+
+void launch_coarse_coef(const Grid &f, const Grid &c, float *coefR,
+                        float *coefB, cudaStream_t s) {
+  const long long n = (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
+  if (n > 0) k_coarse_coef<<<nblk(n), kT, 0, s>>>(f, c, coefR, coefB);
+}
+
+// ---- RBGS half-sweep, variable coefficients -----------------------------------
+__global__ void __launch_bounds__(kT)
+    k_smooth_var(Grid g, int color, int from_zero) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nzh) return;
+  const int k = (int)(t % g.nzh);
+  const long long q = t / g.nzh;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  const int p = (i + j + color) & 1;
+  const int z = 2 * k + p;
+  if (z >= g.nz) return;
+  const long long e = rb(g, il, j) + k;
+  Coef C;
+  coef_at(g, color, e, i, j, z, C);
+  if (C.D == 0.0) return;  // solid: not an unknown
+  const double *oth = color ? g.phiR : g.phiB;
+  const double *f = color ? g.fB : g.fR;
+  double *own = color ? g.phiB : g.phiR;
+  const double tsum = from_zero ? 0.0 : nbsum(g, oth, e, z, C);
+  own[e] = (f[e] * g.w + tsum) / C.D;
+}
+
+void launch_smooth_var(const Grid &g, int color, int from_zero, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nzh;
+  if (n > 0) k_smooth_var<<<nblk(n), kT, 0, s>>>(g, color, from_zero);
+}
+
+// ---- residual + restriction ----------------------------------------------------
+__global__ void __launch_bounds__(kT) k_resid_restrict_var(Grid F, Grid C) {
+  const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)ncx * ncy * ncz) return;
+  const int K = (int)(t % ncz);
+  const long long q = t / ncz;
+  const int J = (int)(q % ncy);
+  const int Il = (int)(q / ncy);
+  double r[8];
+#pragma unroll
+  for (int a = 0; a < 2; a++)
+#pragma unroll
+    for (int b = 0; b < 2; b++)
+#pragma unroll
+      for (int c = 0; c < 2; c++)
+        r[a * 4 + b * 2 + c] = resid_var(F, 2 * Il + a, 2 * J + b, 2 * K + c);
+  const double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+  const int Ig = (F.x0 >> 1) + Il;
+  const int col = (Ig + J + K) & 1;
+  (col ? C.fB : C.fR)[rb(C, Ig - C.x0, J) + (K >> 1)] = 0.125 * s;
+}
+
+void launch_resid_restrict_var(const Grid &f, const Grid &c, cudaStream_t s) {
+  const long long n = (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
+  if (n > 0) k_resid_restrict_var<<<nblk(n), kT, 0, s>>>(f, c);
+}
+
+// ---- prolongation + magnified correction, fluid cells only --------------------
+__global__ void __launch_bounds__(kT) k_prolong_var(Grid F, Grid C, double alpha) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)F.nxl * F.ny * F.nz) return;
+  const int z = (int)(t % F.nz);
+  const long long q = t / F.nz;
+  const int j = (int)(q % F.ny);
+  const int il = (int)(q / F.ny);
+  const int i = F.x0 + il;
+  const int col = (i + j + z) & 1;
+  const long long e = rb(F, il, j) + (z >> 1);
+  Coef cf;
+  coef_at(F, col, e, i, j, z, cf);
+  if (cf.D == 0.0) return;
+  const int I = i >> 1, J = j >> 1, Z = z >> 1;
+  const double ec = (((I + J + Z) & 1) ? C.phiB : C.phiR)[rb(C, I - C.x0, J) + (Z >> 1)];
+  double *u = col ? F.phiB : F.phiR;
+  u[e] = u[e] + alpha * ec;
+}
+
+void launch_prolong_var(const Grid &f, const Grid &c, double alpha, cudaStream_t s) {
+  const long long n = (long long)f.nxl * f.ny * f.nz;
+  if (n > 0) k_prolong_var<<<nblk(n), kT, 0, s>>>(f, c, alpha);
+}
+
+// ---- residual norm partials -------------------------------------------------------
+static constexpr int kNormBlocksV = 148 * 8;
+
+__global__ void __launch_bounds__(kT) k_norm_var(Grid g, double *partials) {
+  __shared__ double sh[32];
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  double acc = 0.0;
+  for (long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x; t < total;
+       t += (long long)gridDim.x * blockDim.x) {
+    const int z = (int)(t % g.nz);
+    const long long q = t / g.nz;
+    const int j = (int)(q % g.ny);
+    const int il = (int)(q / g.ny);
+    const double r = resid_var(g, il, j, z);
+    acc = acc + r * r;
+  }
+  const double s = block_sum_m(acc, sh);
+  if (threadIdx.x == 0) partials[blockIdx.x] = s;
+}
+
+int launch_norm_partials_var(const Grid &g, double *partials, cudaStream_t s) {
+  const long long total = (long long)g.nxl * g.ny * g.nz;
+  long long nb = (total + kT - 1) / kT;
+  if (nb > kNormBlocksV) nb = kNormBlocksV;
+  if (nb < 1) nb = 1;
+  k_norm_var<<<(unsigned)nb, kT, 0, s>>>(g, partials);
+  return (int)nb;
+}
+
+// ---- coarsest-grid CG, variable coefficients (one CTA, vectors in scratch) -----
+__device__ __forceinline__ double cg_sum_v(double v, double *part) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  double s = 0.0;
+  for (int w = 0; w < nw; w++) s = s + part[w];
+  return s;
+}
+
+__device__ __forceinline__ double cg_apply_var(const Grid &g, const double *v,
+                                               long long n) {
+  const int z = (int)(n % g.nz);
+  const long long q = n / g.nz;
+  const int j = (int)(q % g.ny);
+  const int i = (int)(q / g.ny);
+  const int col = (i + j + z) & 1;
+  Coef C;
+  coef_at(g, col, rb(g, i, j) + (z >> 1), i, j, z, C);
+  if (C.D == 0.0) return 0.0;
+  const long long sx = (long long)g.ny * g.nz, sy = g.nz;
+  const double xm = (i > 0) ? v[n - sx] : 0.0;
+  const double xp = (i < g.nx - 1) ? v[n + sx] : 0.0;
+  const double ym = (j > 0) ? v[n - sy] : 0.0;
+  const double yp = (j < g.ny - 1) ? v[n + sy] : 0.0;
+  const double zm = (z > 0) ? v[n - 1] : 0.0;
+  const double zp = (z < g.nz - 1) ? v[n + 1] : 0.0;
+  const double t = ((((C.k[0] * xm + C.k[1] * xp) + C.k[2] * ym) + C.k[3] * yp) +
+                    C.k[4] * zm) +
+                   C.k[5] * zp;
+  return g.c * (C.D * v[n] - t);
+}
+
+__global__ void __launch_bounds__(1024)
+    k_coarse_cg_var(Grid g, double *scr, double tol, int maxit, int *iters_out) {
+  __shared__ double part[2][32];
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  double *x = scr, *r = scr + N, *p = scr + 2 * N, *q = scr + 3 * N;
+  int pb = 0;
+  double acc = 0.0;
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = (int)(n % g.nz);
+    const long long t = n / g.nz;
+    const int j = (int)(t % g.ny), i = (int)(t / g.ny);
+    const int col = (i + j + z) & 1;
+    const long long e = rb(g, i, j) + (z >> 1);
+    Coef C;
+    coef_at(g, col, e, i, j, z, C);
+    const double b = (C.D == 0.0) ? 0.0 : (col ? g.fB[e] : g.fR[e]);
+    x[n] = 0.0;
+    r[n] = b;
+    p[n] = b;
+    acc = acc + b * b;
+  }
+  double rho = cg_sum_v(acc, part[pb]);
+  pb ^= 1;
+  const double bnorm = sqrt(rho);
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      acc = 0.0;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+        const double qn = cg_apply_var(g, p, n);
+        q[n] = qn;
+        acc = acc + p[n] * qn;
+      }
+      const double pq = cg_sum_v(acc, part[pb]);
+      pb ^= 1;
+      const double a = rho / pq;
+      acc = 0.0;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+        x[n] = x[n] + a * p[n];
+        const double rn = r[n] - a * q[n];
+        r[n] = rn;
+        acc = acc + rn * rn;
+      }
+      const double rho1 = cg_sum_v(acc, part[pb]);
+      pb ^= 1;
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      const double beta = rho1 / rho;
+      for (long long n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
+      __syncthreads();
+      rho = rho1;
+    }
+  }
+  __syncthreads();
+  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = (int)(n % g.nz);
+    const long long t = n / g.nz;
+    const int j = (int)(t % g.ny), i = (int)(t / g.ny);
+    const int col = (i + j + z) & 1;
+    (col ? g.phiB : g.phiR)[rb(g, i, j) + (z >> 1)] = x[n];
+  }
+  if (threadIdx.x == 0 && iters_out) *iters_out = it;
+}
+
+void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
+                          int *iters_out, cudaStream_t s) {
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  int threads = (int)((N + 31) / 32 * 32);
+  if (threads > 1024) threads = 1024;
+  k_coarse_cg_var<<<1, threads, 0, s>>>(g, scratch, tol, maxit, iters_out);
+}
+
+// ---- f := 0 on solid cells (the oracle's "masked cells are not unknowns") -----
+__global__ void __launch_bounds__(kT) k_zero_solid(Grid g) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  const int col = (i + j + z) & 1;
+  const long long e = rb(g, il, j) + (z >> 1);
+  Coef C;
+  coef_at(g, col, e, i, j, z, C);
+  if (C.D == 0.0) (col ? g.fB : g.fR)[e] = 0.0;
+}
+
+void launch_zero_solid(const Grid &g, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0 && (g.codeR || g.coefR)) k_zero_solid<<<nblk(n), kT, 0, s>>>(g);
+}
+
+// ---- operator of a level as 7 coefficients per cell, natural layout ------------
+__global__ void __launch_bounds__(kT) k_get_stencil(Grid g, double *out) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  double *o = out + 7 * t;
+  if (g.codeR || g.coefR) {
+    const int col = (i + j + z) & 1;
+    Coef C;
+    coef_at(g, col, rb(g, il, j) + (z >> 1), i, j, z, C);
+    o[0] = g.c * C.D;
+    for (int r = 0; r < 6; r++) o[1 + r] = (C.D == 0.0) ? 0.0 : -g.c * C.k[r];
+  } else {
+    int d = 6;
+    const bool on[6] = {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, z == 0,
+                        z == g.nz - 1};
+    for (int r = 0; r < 6; r++) {
+      if (on[r]) d += g.dface[r];
+      o[1 + r] = on[r] ? 0.0 : -g.c;
+    }
+    o[0] = g.c * (double)d;
+  }
+}
+
+void launch_get_stencil(const Grid &g, double *out7, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0) k_get_stencil<<<nblk(n), kT, 0, s>>>(g, out7);
+}
+
+}  // namespace mg

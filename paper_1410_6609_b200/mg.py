@@ -118,6 +118,8 @@ def lib():
         L.mg_residual_restrict.argtypes = [P, i]
         L.mg_prolong_correct.argtypes = [P, i]
         L.mg_coarse_solve.argtypes = [P, ip]
+        L.mg_set_mask.argtypes = [P, dp, i]
+        L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
         L.mg_cycle_launches.argtypes = [P]
@@ -311,6 +313,21 @@ class Multigrid:
     def set_field(self, level, field, a):
         ptr, where = self._io_args(a)
         _check(lib().mg_set_field(self._ctx, level, field, ptr, where), self._ctx)
+
+    def set_mask(self, solid):
+        """Solid cells (nonzero) of the WHOLE domain, natural layout."""
+        if solid is None:
+            _check(lib().mg_set_mask(self._ctx, None, MG_HOST), self._ctx)
+            return
+        a = np.ascontiguousarray(solid, dtype=np.uint8)
+        self._mask_keep = a
+        _check(lib().mg_set_mask(self._ctx, a.ctypes.data, MG_HOST), self._ctx)
+
+    def get_stencil(self, level=0):
+        out = np.empty(self.local_shape(level) + (7,), np.float64)
+        _check(lib().mg_get_stencil(self._ctx, level, out.ctypes.data, MG_HOST),
+               self._ctx)
+        return out
 
     # -- solve ----------------------------------------------------------------
     def vcycle(self) -> float:

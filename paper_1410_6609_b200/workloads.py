@@ -37,6 +37,7 @@ class Workload:
     centers: Optional[np.ndarray] = None    # (n, 3) physical coordinates
     radii: Optional[np.ndarray] = None
     charges: Optional[np.ndarray] = None
+    solid: Optional[np.ndarray] = None      # uint8 mask, natural layout (cfg5)
 
     @property
     def cells(self) -> int:
@@ -161,3 +162,41 @@ def cfg4(P: int = 1, n: int = 512, seed: int = 0, radius: float = 6.0,
     return Workload("cfg4_weak_P%d_%d" % (P, n), shape, 1.0, bt, bv,
                     min_coarse=8, tol=tol, centers=c,
                     radii=np.full(ns, radius), charges=q)
+
+
+def beam_box(shape):
+    """Config 5 solid beam (reading c17): x in [3/4 nx, nx), y in
+    [232/512 ny, 280/512 ny), all z -- the beam splitting the last quarter of
+    the bifurcating channel."""
+    nx, ny, nz = shape
+    x0 = (3 * nx) // 4
+    y0 = int(round(232 * ny / 512))
+    y1 = max(int(round(280 * ny / 512)), y0 + 1)
+    return (x0, nx), (y0, y1), (0, nz)
+
+
+def beam_mask(shape) -> np.ndarray:
+    (x0, x1), (y0, y1), (z0, z1) = beam_box(shape)
+    m = np.zeros(tuple(shape), np.uint8)
+    m[x0:x1, y0:y1, z0:z1] = 1
+    return m
+
+
+def cfg5(scale: int = 1, seed: int = 0, radius: float = 4.0,
+         n_spheres: Optional[int] = None, tol: float = 1e-8) -> Workload:
+    """Strong scaling: 2048 x 512 x 512 (divided by `scale`), h = 1, beam
+    mask, Dirichlet 0 / 1 on the y = 0 / y = ny walls (full length), homogeneous
+    Neumann elsewhere and on the beam walls; 50,000 spheres of radius 4 outside
+    the beam (scaled by the volume), charges +-1; V(3,3) to 1e-8."""
+    shape = (2048 // scale, 512 // scale, 512 // scale)
+    bt, bv = channel_bc(1.0)
+    if n_spheres is None:
+        n_spheres = max(1, int(round(50000 / scale ** 3)))
+    box = beam_box(shape)
+    c, q = random_spheres(shape, radius, n_spheres, seed,
+                          exclude_box=tuple((float(a), float(b)) for a, b in box))
+    w = Workload("cfg5_beam_%dx%dx%d" % shape, shape, 1.0, bt, bv,
+                 min_coarse=8, nu1=3, nu2=3, tol=tol, centers=c,
+                 radii=np.full(n_spheres, radius), charges=q)
+    w.solid = beam_mask(shape)
+    return w

@@ -351,3 +351,94 @@ def test_march_norm_matches_oracle(mg):
     o.set_phi(phi)
     o.set_rhs(f)
     assert abs(s.residual_norm() - o.residual_norm()) <= 1e-13 * o.residual_norm()
+
+
+
+# --------------------------------------------------------------------------
+# config 5: solid mask, variable (Galerkin) coefficients
+# --------------------------------------------------------------------------
+def mask_pair(M, shape, solid, bc="channel", **kw):
+    bt, bv = BCS[bc]
+    s = M.Multigrid(shape, 1.0, bt, bv, **kw)
+    s.set_mask(solid)
+    okw = {k: v for k, v in kw.items()
+           if k in ("min_coarse", "nu1", "nu2", "coarse_tol", "coarse_maxit")}
+    o = oracle.Oracle(shape, 1.0, bt, bv, solid=solid, **okw)
+    return s, o
+
+
+def random_mask(shape, frac, seed):
+    return (np.random.default_rng(seed).uniform(size=shape) < frac).astype(np.uint8)
+
+
+@pytest.mark.parametrize("kind", ["random", "beam"])
+def test_mask_operators_equal_oracle_galerkin(mg, kind):
+    """The GPU's face-transmissibility coarse operators equal the oracle's
+    generic R A P stencils exactly on every level."""
+    shape = (32, 16, 32)
+    solid = random_mask(shape, 0.2, 1) if kind == "random" else W.beam_mask(shape)
+    s, o = mask_pair(mg, shape, solid, min_coarse=1)
+    assert s.nlevels == o.nlevels
+    for l in range(o.nlevels):
+        assert np.array_equal(s.get_stencil(l), o.stencil(l)), l
+
+
+def test_mask_steps_bitwise(mg):
+    shape = (32, 16, 32)
+    solid = random_mask(shape, 0.15, 2)
+    s, o = mask_pair(mg, shape, solid, bc="mixed", min_coarse=2)
+    rng = np.random.default_rng(3)
+    for l in range(o.nlevels - 1):
+        d = o.dims(l)
+        phi = rng.uniform(-1, 1, d)
+        f = rng.uniform(-1, 1, d)
+        s.set_field(l, mg.MG_FIELD_PHI, phi)
+        s.set_field(l, mg.MG_FIELD_RHS, f)
+        o.set_phi(phi, l)
+        o.set_rhs_raw(f, l)
+        for c in (0, 1, 0):
+            s.smooth_half(l, c)
+            o.smooth_half(l, c)
+            assert np.array_equal(s.get_field(l, mg.MG_FIELD_PHI), o.phi(l))
+        s.residual_restrict(l)
+        o.restrict_residual(l)
+        assert np.array_equal(s.get_field(l + 1, mg.MG_FIELD_RHS), o.rhs(l + 1))
+        e = rng.uniform(-1, 1, o.dims(l + 1))
+        s.set_field(l + 1, mg.MG_FIELD_PHI, e)
+        o.set_phi(e, l + 1)
+        s.prolong_correct(l)
+        o.prolong_correct(l, 2.0)
+        assert np.array_equal(s.get_field(l, mg.MG_FIELD_PHI), o.phi(l))
+
+
+def test_config5_reduced_parity(mg):
+    """Config-5 recipe at 1/16 scale: beam mask, electrodes, spheres outside
+    the beam, V(3,3) to 1e-8."""
+    w = W.cfg5(scale=16, n_spheres=60)
+    s, o = mask_pair(mg, w.shape, w.solid, min_coarse=w.min_coarse, nu1=3, nu2=3)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    rc, cg, hg = s.solve(w.tol, 80)
+    so, co, ho = o.solve(w.tol, 80)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    assert not s.get_solution()[w.solid.astype(bool)].any()
+
+
+def test_mask_loopback_equals_single(mg):
+    w = W.cfg5(scale=16, n_spheres=40)
+    res = []
+    for p in (1, 4):
+        kw = dict(min_coarse=8, nu1=3, nu2=3, agglomerate_below=256)
+        if p > 1:
+            kw.update(nranks=p, halo="loopback")
+        bt, bv = BCS["channel"]
+        s = mg.Multigrid(w.shape, 1.0, bt, bv, **kw)
+        s.set_mask(w.solid)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        r = [s.vcycle() for _ in range(4)]
+        res.append((r, s.get_solution()))
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.allclose(res[0][0], res[1][0], rtol=1e-13, atol=0)

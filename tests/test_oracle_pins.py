@@ -451,3 +451,60 @@ def test_hierarchy_rule():
     for shape, mc, expect in cases:
         o = oracle.Oracle(shape, 1.0, [D] * 6, [0.0] * 6, min_coarse=mc)
         assert [o.dims(l) for l in range(o.nlevels)] == expect
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_masked_galerkin_face_transmissibility_form(seed):
+    """R A P with a solid mask (reading c19) equals, on every level,
+    a_q = -c_l kappa_q with kappa_q = (# fluid-fluid fine face pairs across the
+    coarse face) / 4^l and a_cc = c_l (sum kappa + 2 delta), delta = (# fluid
+    fine cells on Dirichlet faces of the block) / 4^l -- counted here by brute
+    force on the fine mask (the form the CUDA path stores)."""
+    shape = (16, 8, 16)
+    bt = [N, N, D, D, N, D]
+    solid = (np.random.default_rng(seed).uniform(size=shape) < 0.2).astype(np.uint8)
+    o = oracle.Oracle(shape, 0.5, bt, [0.0] * 6, solid=solid, min_coarse=1)
+    fl = ~solid.astype(bool)
+    nx, ny, nz = shape
+    for l in range(o.nlevels):
+        b = 2 ** l
+        cx, cy, cz = o.dims(l)
+        st = o.stencil(l)
+        unk = o.unknown(l).astype(bool)
+        c = 2.0 ** -l / 0.25
+        for I in range(cx):
+            for J in range(cy):
+                for K in range(cz):
+                    if not unk[I, J, K]:
+                        continue
+                    blk = (slice(I * b, I * b + b), slice(J * b, J * b + b),
+                           slice(K * b, K * b + b))
+                    kap = []
+                    for ax in range(3):
+                        for side in (0, 1):
+                            sl = list(blk)
+                            edge = (I, J, K)[ax] * b + (0 if side == 0 else b - 1)
+                            nb = edge + (-1 if side == 0 else 1)
+                            lim = shape[ax]
+                            sl[ax] = slice(edge, edge + 1)
+                            inner = fl[tuple(sl)]
+                            if 0 <= nb < lim:
+                                sl[ax] = slice(nb, nb + 1)
+                                kap.append((inner & fl[tuple(sl)]).sum() / 4.0 ** l)
+                            else:
+                                kap.append(0.0)
+                    delta = 0.0
+                    for q in range(6):
+                        if bt[q] != D:
+                            continue
+                        ax, side = divmod(q, 2)
+                        if (I, J, K)[ax] != (0 if side == 0 else (cx, cy, cz)[ax] - 1):
+                            continue
+                        sl = list(blk)
+                        edge = 0 if side == 0 else shape[ax] - 1
+                        sl[ax] = slice(edge, edge + 1)
+                        delta += fl[tuple(sl)].sum() / 4.0 ** l
+                    assert st[I, J, K, 0] == c * (sum(kap) + 2 * delta)
+                    for q in range(6):
+                        assert st[I, J, K, 1 + q] == -c * kap[q] or (
+                            kap[q] == 0 and st[I, J, K, 1 + q] == 0)
