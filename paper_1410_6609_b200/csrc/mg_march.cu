@@ -31,7 +31,7 @@ namespace mg {
 namespace {
 
 constexpr int kTY = 8;        // rows per CTA (one warp per row)
-constexpr int kICH = 16;      // planes per CTA
+constexpr int kICH = 16;      // max planes per CTA (x-chunk)
 constexpr int kSlots = 5;     // ring depth: planes q-1, q, q+1 in use, 2 in flight
 constexpr int kThreadsM = kTY * 32;
 constexpr int kZT = 128;      // z-tile (half-entries) of the residual kernels
@@ -122,6 +122,15 @@ __host__ __device__ inline int rslot_doubles() {
   return round128((kTY + 2) * kZB * 8) / 8;
 }
 
+// x-chunk length: 16 planes, halved (down to 2, even for the restriction
+// pairs) while the grid would have fewer than ~8 CTAs per SM
+__host__ __device__ inline int chunk_planes(int nxl, int tiles_per_plane_set) {
+  int ich = kICH;
+  while (ich > 2 && (long long)((nxl + ich - 1) / ich) * tiles_per_plane_set < 148 * 8)
+    ich >>= 1;
+  return ich;
+}
+
 __device__ __forceinline__ double2 lds2(const double *p) {
   return *reinterpret_cast<const double2 *>(p);
 }
@@ -132,7 +141,7 @@ __device__ __forceinline__ double2 lds2(const double *p) {
 // half-sweep (optionally fused with the prolongation of the other colour)
 // one TMA box = (pz doubles) x (TY+2 rows) x (1 plane)
 // ============================================================================
-template <bool PROLONG>
+template <bool PROLONG, int NCH>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
                    int color, Grid C, double alpha) {
@@ -145,11 +154,12 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   const unsigned box_bytes = (unsigned)((kTY + 2) * pz * 8);
 
   const int nrt = (g.ny + kTY - 1) / kTY;
+  const int ich = chunk_planes(g.nxl, nrt);
   const int rt = blockIdx.x % nrt;
   const int xc = blockIdx.x / nrt;
   const int j0 = rt * kTY;
-  const int i0 = xc * kICH;
-  const int i1 = min(i0 + kICH, g.nxl);
+  const int i0 = xc * ich;
+  const int i1 = min(i0 + ich, g.nxl);
   const int nplanes = (i1 - i0) + 2;  // local planes i0-1 .. i1
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -171,7 +181,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   const bool row_ok = j < g.ny;
   double *__restrict__ own = color ? g.phiB : g.phiR;
   const double *__restrict__ fown = color ? g.fB : g.fR;
-  const int nch = (g.nzh + 63) >> 6;  // 64 half-entries per warp pass
+  constexpr int nch = NCH;  // 64 half-entries per warp pass, ceil(nzh/64)
 
   // PROLONG: add alpha * e(parent) to the ring copy of local plane il (rows
   // j0-1 .. j0+TY).  The corrected other colour is NOT written back: the
@@ -180,9 +190,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   // halo reads of neighbouring CTAs).  The coarse values are loaded one plane
   // ahead (load_e) so their latency hides behind the previous plane's work.
   // Work split: task t = (row rr, 64-wide chunk c), t = warp + TY*m.
-  constexpr int kMaxTask = (kTY + 2) * 4;
-  constexpr int kTPW = (kMaxTask + kTY - 1) / kTY;  // tasks per warp
-  const int ntask = (kTY + 2) * nch;
+  constexpr int ntask = (kTY + 2) * NCH;
+  constexpr int kTPW = (ntask + kTY - 1) / kTY;  // tasks per warp
   auto load_e = [&](int q, double2 *E) {
     const int i = g.x0 + i0 - 1 + q;
     const int I = i >> 1;
@@ -231,11 +240,11 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   if (PROLONG && nplanes > 2) load_e(2, E);
 
   // f of the first plane into registers
-  double2 fr[4];
+  double2 fr[NCH];
 #pragma unroll
-  for (int c = 0; c < 4; c++) {
+  for (int c = 0; c < NCH; c++) {
     const int k = 2 * lane + 64 * c;
-    if (c < nch && row_ok && k < g.nzh)
+    if (row_ok && k < g.nzh)
       fr[c] = *reinterpret_cast<const double2 *>(
           fown + (long long)(i0 + 1) * g.plane + (long long)(j + 1) * pz + k);
   }
@@ -269,12 +278,12 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     }
 
     // prefetch f of the next plane
-    double2 fn[4];
+    double2 fn[NCH];
     const bool more = il + 1 < i1;
 #pragma unroll
-    for (int c = 0; c < 4; c++) {
+    for (int c = 0; c < NCH; c++) {
       const int k = 2 * lane + 64 * c;
-      if (more && c < nch && row_ok && k < g.nzh)
+      if (more && row_ok && k < g.nzh)
         fn[c] = *reinterpret_cast<const double2 *>(
             fown + (long long)(il + 2) * g.plane + (long long)(j + 1) * pz + k);
     }
@@ -286,9 +295,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const int p = (i + j + color) & 1;
       double *orow = own + (long long)(il + 1) * g.plane + (long long)(j + 1) * pz;
 #pragma unroll
-      for (int c = 0; c < 4; c++) {
+      for (int c = 0; c < NCH; c++) {
         const int k = 2 * lane + 64 * c;
-        if (c >= nch || k >= g.nzh) continue;
+        if (k >= g.nzh) continue;
         const double2 a = lds2(xm + k);
         const double2 b = lds2(xp + k);
         const double2 ym = lds2(cur - pz + k);
@@ -321,7 +330,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       }
     }
 #pragma unroll
-    for (int c = 0; c < 4; c++) fr[c] = fn[c];
+    for (int c = 0; c < NCH; c++) fr[c] = fn[c];
   }
 }
 
@@ -354,12 +363,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   b /= nzt;
   const int rt = b % nrt;
   const int xc = b / nrt;
+  const int ich = chunk_planes(g.nxl, nrt * nzt);
   const int kz0 = zt * kZT;
   const int c0z = rtile_c0(g, kz0);
   const int zoff = kz0 - c0z;  // smem column of half-index kz0
   const int j0 = rt * kTY;
-  const int i0 = xc * kICH;
-  const int i1 = min(i0 + kICH, g.nxl);
+  const int i0 = xc * ich;
+  const int i1 = min(i0 + ich, g.nxl);
   const int nplanes = (i1 - i0) + 2;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -613,33 +623,46 @@ static void set_smem(K kernel, size_t bytes, size_t *configured) {
   }
 }
 
-void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
-                         cudaStream_t s) {
+template <bool P, int NCH>
+static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
+                      int color, double alpha, cudaStream_t s) {
   const int nrt = (g.ny + kTY - 1) / kTY;
-  const int nxc = (g.nxl + kICH - 1) / kICH;
+  const int ich = chunk_planes(g.nxl, nrt);
+  const int nxc = (g.nxl + ich - 1) / ich;
   const size_t smem = smooth_smem_bytes(g);
   static size_t configured = 0;
-  set_smem(k_smooth_march<false>, smem, &configured);
-  const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm_oth128);
-  k_smooth_march<false><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, g, 0.0);
+  set_smem(k_smooth_march<P, NCH>, smem, &configured);
+  k_smooth_march<P, NCH><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
+}
+
+template <bool P>
+static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
+                        int color, double alpha, cudaStream_t s) {
+  const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm128);
+  switch ((g.nzh + 63) >> 6) {
+    case 1: launch_sm<P, 1>(g, c, tm, color, alpha, s); break;
+    case 2: launch_sm<P, 2>(g, c, tm, color, alpha, s); break;
+    case 3: launch_sm<P, 3>(g, c, tm, color, alpha, s); break;
+    default: launch_sm<P, 4>(g, c, tm, color, alpha, s); break;
+  }
+}
+
+void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
+                         cudaStream_t s) {
+  launch_sm_n<false>(g, g, tm_oth128, color, 0.0, s);
 }
 
 void launch_prolong_smooth_march(const Grid &g, const Grid &c,
                                  const void *tm_oth128, int color, double alpha,
                                  cudaStream_t s) {
-  const int nrt = (g.ny + kTY - 1) / kTY;
-  const int nxc = (g.nxl + kICH - 1) / kICH;
-  const size_t smem = smooth_smem_bytes(g);
-  static size_t configured = 0;
-  set_smem(k_smooth_march<true>, smem, &configured);
-  const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm_oth128);
-  k_smooth_march<true><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
+  launch_sm_n<true>(g, c, tm_oth128, color, alpha, s);
 }
 
 static int resid_blocks(const Grid &g) {
   const int nzt = rntiles(g);
   const int nrt = (g.ny + kTY - 1) / kTY;
-  const int nxc = (g.nxl + kICH - 1) / kICH;
+  const int ich = chunk_planes(g.nxl, nrt * nzt);
+  const int nxc = (g.nxl + ich - 1) / ich;
   return nzt * nrt * nxc;
 }
 
