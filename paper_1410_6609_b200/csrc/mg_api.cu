@@ -174,13 +174,15 @@ struct TmPair {
   alignas(64) unsigned char b[128];
   alignas(64) unsigned char rr[128];  // z-tiled boxes (residual kernels)
   alignas(64) unsigned char rb[128];
-  bool ok = false, ok_resid = false;
+  alignas(64) unsigned char r12[128]; // 12-row red boxes (fused kernels)
+  bool ok = false, ok_resid = false, ok_fused = false;
 };
 
 struct mg_ctx {
   Plan pl;
   std::vector<std::vector<TmPair>> tm;
   int use_march = 1;
+  int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
   bool masked = false;            // solid mask set (variable coefficients)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   double h;
@@ -399,6 +401,25 @@ int prolong_level(mg_ctx *c, int l) {
   return halo(c, l, 1);  // the next red half-sweep reads black ghosts
 }
 
+// can level l use the fused last-black + residual epilogue kernels?
+bool can_fuse_resid(const mg_ctx *c, int l) {
+  if (!c->use_march || !c->use_fused || c->masked || distributed(c, l)) return false;
+  for (const TmPair &t : c->tm[l])
+    if (!t.ok_fused) return false;
+  return c->g[l].size() == 1;
+}
+
+// last pre-smoothing black half-sweep fused with f_{l+1} = R(f_l - A Phi_l)
+int black_restrict_level(mg_ctx *c, int l) {
+  if (l == 0) mark(c, CAT_NONE);
+  mg::launch_black_restrict(c->g[l][0], coarse_of(c, l, 0), c->tm[l][0].r12,
+                            c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_RESTRICT0);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
 // can level l use the fused prolongation + first post-smoothing red sweep?
 bool can_fuse_prolong(const mg_ctx *c, int l) {
   if (!c->use_march || c->masked || c->o.nu2 < 1) return false;
@@ -482,11 +503,17 @@ int enqueue_vcycle(mg_ctx *c) {
         CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
         CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
       }
+    const bool fuse_r = c->o.nu1 >= 1 && can_fuse_resid(c, l);
     for (int s = 0; s < c->o.nu1; s++) {
       if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
+      if (fuse_r && s == c->o.nu1 - 1) break;
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
     }
-    if ((rc = restrict_level(c, l))) return rc;
+    if (fuse_r) {
+      if ((rc = black_restrict_level(c, l))) return rc;
+    } else {
+      if ((rc = restrict_level(c, l))) return rc;
+    }
   }
   if (L == 1) mark(c, CAT_NONE);
   if ((rc = coarse_solve(c))) return rc;
@@ -498,10 +525,29 @@ int enqueue_vcycle(mg_ctx *c) {
     } else {
       if ((rc = prolong_level(c, l))) return rc;
     }
+    const bool fuse_n = l == 0 && c->o.nu2 >= 1 && can_fuse_resid(c, 0);
     for (int s = 0; s < c->o.nu2; s++) {
       if (!(fuse && s == 0))
         if ((rc = smooth_half(c, l, 0, 0))) return rc;
+      if (fuse_n && s == c->o.nu2 - 1) break;
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
+    }
+    if (fuse_n) {  // last black half-sweep + residual norm in one pass
+      mark(c, CAT_NONE);
+      const int nb = mg::launch_black_norm(c->g[0][0], c->tm[0][0].r12,
+                                           c->partials, c->stream);
+      c->launches++;
+      mg::launch_sum_ordered(c->partials, nb, c->normv, c->stream);
+      c->launches++;
+      CK(cudaGetLastError());
+      CK(cudaMemcpyAsync(c->normv + 1, c->normv, sizeof(double),
+                         cudaMemcpyDeviceToDevice, c->stream));
+      mark(c, CAT_NORM);
+      CK(cudaMemcpyAsync(c->h_norm, c->normv + 1, sizeof(double),
+                         cudaMemcpyDeviceToHost, c->stream));
+      c->cycle_launches = c->launches;
+      c->prof_last = c->prof;
+      return MG_OK;
     }
   }
   if (L == 1) mark(c, CAT_COARSE);
@@ -802,9 +848,12 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
       t.ok_resid = mg::resid_march_supported(g) &&
                    mg::make_tmap_resid(g, g.phiR, t.rr) &&
                    mg::make_tmap_resid(g, g.phiB, t.rb);
+      t.ok_fused = t.ok_resid && mg::fused_supported(g) &&
+                   mg::make_tmap_red12(g, g.phiR, t.r12);
     }
   }
   if (getenv("MG_NO_MARCH")) c->use_march = 0;
+  if (getenv("MG_FUSED")) c->use_fused = 1;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
   e = cudaMallocHost(&c->h_norm, sizeof(double) * 2);

@@ -75,6 +75,15 @@ void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
 int norm_march_blocks(const Grid &g);
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s);
+bool encode_box(const Grid &g, const double *base, void *out128, unsigned box0,
+                unsigned box1);
+// fused last black half-sweep + residual epilogue (mg_fused.cu)
+bool fused_supported(const Grid &g);
+bool make_tmap_red12(const Grid &g, const double *base, void *out128);
+void launch_black_restrict(const Grid &g, const Grid &c, const void *tm_red12,
+                           cudaStream_t s);
+int launch_black_norm(const Grid &g, const void *tm_red12, double *partials,
+                      cudaStream_t s);
 // masked (variable-coefficient) path, mg_mask.cu
 void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
                        unsigned char *codeR, unsigned char *codeB,

@@ -25,117 +25,10 @@
 #include <cuda_runtime.h>
 
 #include "mg_internal.h"
+#include "mg_tma.cuh"
 
 namespace mg {
 
-namespace {
-
-constexpr int kTY = 8;        // rows per CTA (one warp per row)
-constexpr int kICH = 16;      // max planes per CTA (x-chunk)
-constexpr int kSlots = 5;     // ring depth: planes q-1, q, q+1 in use, 2 in flight
-constexpr int kThreadsM = kTY * 32;
-constexpr int kZT = 128;      // z-tile (half-entries) of the residual kernels
-
-__device__ __forceinline__ unsigned smem_u32(const void *p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned cnt) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(cnt));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long *bar,
-                                               unsigned bytes) {
-  asm volatile(
-      "mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-          smem_u32(bar)),
-      "r"(bytes)
-      : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(unsigned long long *bar,
-                                          unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_3d(void *dst, const CUtensorMap *tm,
-                                            int c0, int c1, int c2,
-                                            unsigned long long *bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::"
-      "bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-      "l"(reinterpret_cast<unsigned long long>(tm)), "r"(c0), "r"(c1), "r"(c2),
-      "r"(smem_u32(bar))
-      : "memory");
-}
-
-__device__ __forceinline__ void fence_proxy_async() {
-  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-__device__ __forceinline__ int centre_dm(const Grid &g, int i, int j, int z) {
-  int d = 6;
-  if (i == 0) d += g.dface[0];
-  if (i == g.nx - 1) d += g.dface[1];
-  if (j == 0) d += g.dface[2];
-  if (j == g.ny - 1) d += g.dface[3];
-  if (z == 0) d += g.dface[4];
-  if (z == g.nz - 1) d += g.dface[5];
-  return d;
-}
-
-__host__ __device__ inline int round128(int bytes) { return (bytes + 127) / 128 * 128; }
-
-// smoother ring slot: (TY + 2) rows of pz doubles
-__host__ __device__ inline int slot_doubles(int pz) {
-  return round128((kTY + 2) * pz * 8) / 8;
-}
-
-// residual kernels: z-tiles of ZT half-entries.  A row of pz <= ZT + 3 is
-// one tile loaded whole (box = pz); longer rows are cut into tiles whose TMA
-// box (ZT + 4 wide, start a multiple of 4) lies inside [0, pz): the z-halo
-// element of a seam comes from the overlap, never from out-of-bounds reads.
-constexpr int kZB = kZT + 4;
-__host__ __device__ inline bool rsingle(const Grid &g) { return g.nzh <= kZT; }
-__host__ __device__ inline int rbox0(const Grid &g) { return rsingle(g) ? g.pz : kZB; }
-__host__ __device__ inline int rntiles(const Grid &g) {
-  return rsingle(g) ? 1 : (g.nzh + kZT - 1) / kZT;
-}
-__host__ __device__ inline int rtile_c0(const Grid &g, int kz0) {
-  if (rsingle(g)) return 0;
-  int c0 = kz0 - 4;
-  if (c0 < 0) c0 = 0;
-  if (c0 > g.pz - kZB) c0 = g.pz - kZB;
-  return c0;
-}
-// residual ring slot: (TY + 2) rows of rbox0 doubles
-__host__ __device__ inline int rslot_doubles() {
-  return round128((kTY + 2) * kZB * 8) / 8;
-}
-
-// x-chunk length: 16 planes, halved (down to 2, even for the restriction
-// pairs) while the grid would have fewer than ~8 CTAs per SM
-__host__ __device__ inline int chunk_planes(int nxl, int tiles_per_plane_set) {
-  int ich = kICH;
-  while (ich > 2 && (long long)((nxl + ich - 1) / ich) * tiles_per_plane_set < 148 * 8)
-    ich >>= 1;
-  return ich;
-}
-
-__device__ __forceinline__ double2 lds2(const double *p) {
-  return *reinterpret_cast<const double2 *>(p);
-}
-
-}  // namespace
 
 // ============================================================================
 // half-sweep (optionally fused with the prolongation of the other colour)
@@ -596,6 +489,24 @@ static bool encode(const Grid &g, const double *base, void *out128,
                         (cuuint64_t)(g.nxl + 2)};
   cuuint64_t strides[2] = {(cuuint64_t)g.pz * 8, (cuuint64_t)g.plane * 8};
   cuuint32_t box[3] = {box0, (cuuint32_t)(kTY + 2), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
+                   const_cast<double *>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+bool encode_box(const Grid &g, const double *base, void *out128, unsigned box0,
+                unsigned box1) {
+  PFN_encodeTiled enc = get_encode();
+  if (!enc) return false;
+  CUtensorMap *tm = reinterpret_cast<CUtensorMap *>(out128);
+  cuuint64_t dims[3] = {(cuuint64_t)g.pz, (cuuint64_t)(g.ny + 2),
+                        (cuuint64_t)(g.nxl + 2)};
+  cuuint64_t strides[2] = {(cuuint64_t)g.pz * 8, (cuuint64_t)g.plane * 8};
+  cuuint32_t box[3] = {box0, box1, 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3,
                    const_cast<double *>(base), dims, strides, box, es,

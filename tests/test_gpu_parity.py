@@ -322,13 +322,19 @@ def test_errors(mg):
 
 @pytest.mark.parametrize("shape,bc", [((32, 24, 256), "mixed"),
                                       ((64, 16, 128), "channel"),
-                                      ((16, 16, 512), "dirichlet")])
-def test_march_kernels_equal_direct_kernels(mg, shape, bc, monkeypatch):
+                                      ((16, 16, 512), "dirichlet"),
+                                      ((36, 20, 264), "channel"),
+                                      ((128, 64, 128), "mixed")])
+@pytest.mark.parametrize("fused", [False, True])
+def test_march_kernels_equal_direct_kernels(mg, shape, bc, fused, monkeypatch):
     """The TMA-marching kernels (half-sweep, prolongation fused with the
-    first post-smoothing red sweep, residual+restriction, norm) give the same
+    first post-smoothing red sweep, residual+restriction, norm, and with
+    MG_FUSED=1 the last-black + residual epilogue kernels) give the same
     V-cycle iterates as the direct-load kernels, bit for bit."""
     f = np.random.default_rng(12).uniform(-1, 1, shape)
     out = []
+    if fused:
+        monkeypatch.setenv("MG_FUSED", "1")
     for no_march in (False, True):
         if no_march:
             monkeypatch.setenv("MG_NO_MARCH", "1")
