@@ -207,6 +207,19 @@ def run_cuda(args):
         rhs_host.numpy()[...] = W.uniform_rhs(shape, 0)
         s.set_rhs(rhs_host)
         wl = "cfg3: %d^3, h=1/%d, homogeneous Dirichlet, f~U[-1,1] seed 0" % (n, n)
+    elif workload == "cfg5":
+        # strong scaling: 2048 x 512 x 512 total (scaled by --size/512)
+        sc = 512 // n
+        w = W.cfg5(scale=sc)
+        shape = w.shape
+        kw.update(nu1=3, nu2=3)
+        s = mg.Multigrid(shape, w.h, w.bc_type, w.bc_value, device=local,
+                         stream=stream, **kw)
+        s.set_mask(w.solid)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        rhs_host = None
+        wl = ("cfg5: %dx%dx%d bifurcating channel (beam mask), electrodes 0/1, "
+              "%d spheres R=4, V(3,3)" % (shape + (len(w.radii),)))
     else:
         w = W.cfg4(P=N, n=n, seed=0)
         shape = w.shape
@@ -271,9 +284,10 @@ def run_cuda(args):
             traffic = None
     # whole-cycle model roofline (SURVEY 8(d) byte model)
     model_bytes = 0.0
+    nsw = 6 if workload == "cfg5" else 4
     for l in range(L - 1):
         frac = 8.0 ** -l
-        model_bytes += (24 * (2 + 2) + 34) * frac
+        model_bytes += (24 * nsw + 34) * frac
     model_bytes += 16
     cycle_ms = ms / args.steps
     cycle_frac = model_bytes * local_cells / (cycle_ms * 1e-3) / 1e9 / peak
@@ -309,10 +323,12 @@ def run_cuda(args):
         "value": round(cells * args.steps / (ms * 1e-3) / 1e6, 2),
         "unit": UNIT, "n_gpus": N, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(cycle_ms, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "scaling": "strong" if workload == "cfg5" else "weak",
+        "vs_baseline": None, "dtype": "f64",
         "data": "synthetic",
         "config": {"workload": wl, "global_cells": cells, "levels": L,
-                   "schedule": "V(2,2), RBGS red-black, alpha=2, CG coarsest",
+                   "schedule": ("V(3,3)" if workload == "cfg5" else "V(2,2)")
+                               + ", RBGS red-black, alpha=2, CG coarsest",
                    "parallelism": "x-slab x%d (NCCL halo)" % N if N > 1 else "single GPU",
                    "l2": "inputs larger than L2 (hierarchy %.2f GB vs 126 MB L2); no flush"
                          % (mg.workspace_bytes(shape, min_coarse=8) / 1e9 / N)},
@@ -352,7 +368,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
-    ap.add_argument("--workload", default=None, choices=[None, "cfg3", "cfg4"])
+    ap.add_argument("--workload", default=None, choices=[None, "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--size", type=int, default=512)
     ap.add_argument("--cpu-size", type=int, default=256)
     ap.add_argument("--ref-size", type=int, default=128)
