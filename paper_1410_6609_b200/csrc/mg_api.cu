@@ -343,7 +343,7 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
   for (size_t s = 0; s < c->g[l].size(); s++) {
     const Grid &g = c->g[l][s];
     const TmPair &t = c->tm[l][s];
-    if (c->masked)
+    if (c->masked && !(g.codeR && !from_zero && t.ok && c->use_march))
       mg::launch_smooth_var(g, color, from_zero, c->stream);
     else if (!from_zero && t.ok && c->use_march)
       mg::launch_smooth_march(g, color ? t.r : t.b, color, c->stream);
@@ -362,7 +362,7 @@ int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
   for (int s = 0; s < (int)c->g[l].size(); s++) {
     const TmPair &t = c->tm[l][s];
-    if (c->masked)
+    if (c->masked && !(c->g[l][s].codeR && t.ok_resid && c->use_march))
       mg::launch_resid_restrict_var(c->g[l][s], coarse_of(c, l, s), c->stream);
     else if (t.ok_resid && c->use_march)
       mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
@@ -422,9 +422,11 @@ int black_restrict_level(mg_ctx *c, int l) {
 
 // can level l use the fused prolongation + first post-smoothing red sweep?
 bool can_fuse_prolong(const mg_ctx *c, int l) {
-  if (!c->use_march || c->masked || c->o.nu2 < 1) return false;
-  for (const TmPair &t : c->tm[l])
-    if (!t.ok) return false;
+  if (!c->use_march || c->o.nu2 < 1) return false;
+  for (size_t s = 0; s < c->tm[l].size(); s++) {
+    if (!c->tm[l][s].ok) return false;
+    if (c->masked && !c->g[l][s].codeR) return false;  // float records: no
+  }
   return true;
 }
 
@@ -461,7 +463,7 @@ int enqueue_norm(mg_ctx *c) {
   for (size_t s = 0; s < c->g[0].size(); s++) {
     const Grid &g = c->g[0][s];
     const TmPair &t = c->tm[0][s];
-    if (c->masked) {
+    if (c->masked && !(g.codeR && t.ok_resid && c->use_march)) {
       off += mg::launch_norm_partials_var(g, c->partials + off, c->stream);
     } else if (t.ok_resid && c->use_march) {
       mg::launch_norm_march(g, t.rr, t.rb, c->partials + off, c->stream);
@@ -1149,6 +1151,35 @@ int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
                        ncclFloat, c->comm, c->stream);
       if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef)"))) return rc;
     }
+    // level l+1 aligned with the mask (every kappa 0 or 1)?  then byte codes
+    int *dfail = nullptr;
+    CK(cudaMalloc(&dfail, sizeof(int)));
+    c->mask_bufs.push_back(dfail);
+    CK(cudaMemsetAsync(dfail, 0, sizeof(int), c->stream));
+    std::vector<std::pair<unsigned char *, unsigned char *>> codes;
+    for (Grid &g : c->g[l + 1]) {
+      const size_t ne = (size_t)mg::grid_elems(g);
+      unsigned char *r = nullptr, *b = nullptr;
+      CK(cudaMalloc(&r, ne));
+      c->mask_bufs.push_back(r);
+      CK(cudaMalloc(&b, ne));
+      c->mask_bufs.push_back(b);
+      CK(cudaMemsetAsync(r, 0, ne, c->stream));
+      CK(cudaMemsetAsync(b, 0, ne, c->stream));
+      mg::launch_coef_to_code(g, r, b, dfail, c->stream);
+      codes.push_back({r, b});
+    }
+    int hfail = 1;
+    CK(cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost,
+                       c->stream));
+    CK(cudaStreamSynchronize(c->stream));
+    if (!hfail && !getenv("MG_NO_MASK_CODES"))
+      for (size_t s = 0; s < c->g[l + 1].size(); s++) {
+        Grid &g = c->g[l + 1][s];
+        g.codeR = codes[s].first;
+        g.codeB = codes[s].second;
+        g.coefR = g.coefB = nullptr;
+      }
   }
   CK(cudaGetLastError());
   c->masked = true;

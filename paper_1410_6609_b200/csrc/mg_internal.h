@@ -90,6 +90,8 @@ void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
                        cudaStream_t s);
 void launch_coarse_coef(const Grid &f, const Grid &c, float *coefR,
                         float *coefB, cudaStream_t s);
+void launch_coef_to_code(const Grid &g, unsigned char *codeR,
+                         unsigned char *codeB, int *fail, cudaStream_t s);
 void launch_smooth_var(const Grid &g, int color, int from_zero, cudaStream_t s);
 void launch_resid_restrict_var(const Grid &f, const Grid &c, cudaStream_t s);
 void launch_prolong_var(const Grid &f, const Grid &c, double alpha,

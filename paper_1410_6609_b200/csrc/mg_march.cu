@@ -34,7 +34,7 @@ namespace mg {
 // half-sweep (optionally fused with the prolongation of the other colour)
 // one TMA box = (pz doubles) x (TY+2 rows) x (1 plane)
 // ============================================================================
-template <bool PROLONG, int NCH>
+template <bool PROLONG, int NCH, bool MASK>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
                    int color, Grid C, double alpha) {
@@ -105,6 +105,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const int c0 = (I + J + k) & 1;
       E[m].x = (c0 ? C.phiB : C.phiR)[cb];
       E[m].y = (c0 ? C.phiR : C.phiB)[cb];
+      if (MASK) {  // solid cells of the other colour get no correction
+        const unsigned char *oc = (color ? g.codeR : g.codeB) +
+                                  (long long)(i0 + q) * g.plane +
+                                  (long long)(jj + 1) * pz + k;
+        if (!(oc[0] & 64)) E[m].x = 0.0;
+        if (k + 1 < g.nzh && !(oc[1] & 64)) E[m].y = 0.0;
+      }
     }
   };
   auto apply_e = [&](int q, const double2 *E) {
@@ -208,18 +215,36 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           zm1 = zc.y;
           zp1 = (k + 2 < g.nzh) ? cur[k + 2] : 0.0;
         }
-        const double s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
-        const double s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
         const int z0 = 2 * k + p;
-        const double d0 = (double)centre_dm(g, i, j, z0);
-        const double d1 = (double)centre_dm(g, i, j, z0 + 2);
+        double s0, s1, d0, d1;
+        unsigned cd0 = 64, cd1 = 64;
+        if (MASK) {
+          const unsigned char *oc = (color ? g.codeB : g.codeR) +
+                                    (long long)(il + 1) * g.plane +
+                                    (long long)(j + 1) * pz + k;
+          const unsigned cc2 = *reinterpret_cast<const unsigned short *>(oc);
+          cd0 = cc2 & 0xffu;
+          cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
+          s0 = ksum(cd0, a.x, b.x, ym.x, yp.x, zm0, zp0);
+          s1 = ksum(cd1, a.y, b.y, ym.y, yp.y, zm1, zp1);
+          d0 = kdiag(g, cd0, i, j, z0);
+          d1 = kdiag(g, cd1, i, j, z0 + 2);
+        } else {
+          s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
+          s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
+          d0 = (double)centre_dm(g, i, j, z0);
+          d1 = (double)centre_dm(g, i, j, z0 + 2);
+        }
         double2 out;
         out.x = (fr[c].x * g.w + s0) / d0;
         out.y = (fr[c].y * g.w + s1) / d1;
-        if (k + 1 < g.nzh)
+        const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
+        if (both)
           *reinterpret_cast<double2 *>(orow + k) = out;
-        else
-          orow[k] = out.x;
+        else {  // ragged row end or a solid cell (not an unknown: untouched)
+          if (cd0 & 64) orow[k] = out.x;
+          if (k + 1 < g.nzh && (cd1 & 64)) orow[k + 1] = out.y;
+        }
       }
     }
 #pragma unroll
@@ -233,7 +258,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
 // ============================================================================
 enum { MODE_RESTRICT = 0, MODE_NORM = 1 };
 
-template <int MODE>
+template <int MODE, bool MASK>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_resid_march(Grid g, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmB, Grid C,
@@ -361,16 +386,31 @@ __global__ void __launch_bounds__(kThreadsM, 2)
             zm1 = zc.y;
             zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : 0.0;
           }
-          const double s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
-          const double s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
           const int z0 = 2 * k + p;
-          const double d0 = (double)centre_dm(g, i, j, z0);
-          const double d1 = (double)centre_dm(g, i, j, z0 + 2);
+          double s0, s1, d0, d1;
+          unsigned cd0 = 64, cd1 = 64;
+          if (MASK) {
+            const unsigned char *oc = (col ? g.codeB : g.codeR) +
+                                      (long long)(il + 1) * g.plane +
+                                      (long long)(j + 1) * g.pz + k;
+            const unsigned cc2 = *reinterpret_cast<const unsigned short *>(oc);
+            cd0 = cc2 & 0xffu;
+            cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
+            s0 = ksum(cd0, a.x, bb.x, ym.x, yp.x, zm0, zp0);
+            s1 = ksum(cd1, a.y, bb.y, ym.y, yp.y, zm1, zp1);
+            d0 = kdiag(g, cd0, i, j, z0);
+            d1 = kdiag(g, cd1, i, j, z0 + 2);
+          } else {
+            s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
+            s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
+            d0 = (double)centre_dm(g, i, j, z0);
+            d1 = (double)centre_dm(g, i, j, z0 + 2);
+          }
           const double t0 = d0 * u.x - s0;
           const double t1 = d1 * u.y - s1;
           const double2 fo = col ? fB[c] : fR[c];
-          r[col][0] = fo.x - g.c * t0;
-          r[col][1] = (k + 1 < g.nzh) ? fo.y - g.c * t1 : 0.0;
+          r[col][0] = (cd0 & 64) ? fo.x - g.c * t0 : 0.0;
+          r[col][1] = (k + 1 < g.nzh && (cd1 & 64)) ? fo.y - g.c * t1 : 0.0;
         }
         if (MODE == MODE_NORM) {
           acc = acc + r[0][0] * r[0][0];
@@ -534,7 +574,7 @@ static void set_smem(K kernel, size_t bytes, size_t *configured) {
   }
 }
 
-template <bool P, int NCH>
+template <bool P, int NCH, bool M>
 static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
                       int color, double alpha, cudaStream_t s) {
   const int nrt = (g.ny + kTY - 1) / kTY;
@@ -542,31 +582,37 @@ static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
   const int nxc = (g.nxl + ich - 1) / ich;
   const size_t smem = smooth_smem_bytes(g);
   static size_t configured = 0;
-  set_smem(k_smooth_march<P, NCH>, smem, &configured);
-  k_smooth_march<P, NCH><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
+  set_smem(k_smooth_march<P, NCH, M>, smem, &configured);
+  k_smooth_march<P, NCH, M><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
 }
 
-template <bool P>
+template <bool P, bool M>
 static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
                         int color, double alpha, cudaStream_t s) {
   const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm128);
   switch ((g.nzh + 63) >> 6) {
-    case 1: launch_sm<P, 1>(g, c, tm, color, alpha, s); break;
-    case 2: launch_sm<P, 2>(g, c, tm, color, alpha, s); break;
-    case 3: launch_sm<P, 3>(g, c, tm, color, alpha, s); break;
-    default: launch_sm<P, 4>(g, c, tm, color, alpha, s); break;
+    case 1: launch_sm<P, 1, M>(g, c, tm, color, alpha, s); break;
+    case 2: launch_sm<P, 2, M>(g, c, tm, color, alpha, s); break;
+    case 3: launch_sm<P, 3, M>(g, c, tm, color, alpha, s); break;
+    default: launch_sm<P, 4, M>(g, c, tm, color, alpha, s); break;
   }
 }
 
 void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
                          cudaStream_t s) {
-  launch_sm_n<false>(g, g, tm_oth128, color, 0.0, s);
+  if (g.codeR)
+    launch_sm_n<false, true>(g, g, tm_oth128, color, 0.0, s);
+  else
+    launch_sm_n<false, false>(g, g, tm_oth128, color, 0.0, s);
 }
 
 void launch_prolong_smooth_march(const Grid &g, const Grid &c,
                                  const void *tm_oth128, int color, double alpha,
                                  cudaStream_t s) {
-  launch_sm_n<true>(g, c, tm_oth128, color, alpha, s);
+  if (g.codeR)
+    launch_sm_n<true, true>(g, c, tm_oth128, color, alpha, s);
+  else
+    launch_sm_n<true, false>(g, c, tm_oth128, color, alpha, s);
 }
 
 static int resid_blocks(const Grid &g) {
@@ -582,24 +628,32 @@ bool resid_march_supported(const Grid &g) {
          (g.nxl % 2) == 0 && (g.ny % 2) == 0 && get_encode() != nullptr;
 }
 
+template <int MODE, bool M>
+static void launch_rm(const Grid &g, const Grid &c, const void *tmR,
+                      const void *tmB, double *partials, cudaStream_t s) {
+  static size_t configured = 0;
+  set_smem(k_resid_march<MODE, M>, resid_smem_bytes(), &configured);
+  k_resid_march<MODE, M><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
+      g, *reinterpret_cast<const CUtensorMap *>(tmR),
+      *reinterpret_cast<const CUtensorMap *>(tmB), c, partials);
+}
+
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
                                  const void *tmB, cudaStream_t s) {
-  static size_t configured = 0;
-  set_smem(k_resid_march<MODE_RESTRICT>, resid_smem_bytes(), &configured);
-  k_resid_march<MODE_RESTRICT><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
-      g, *reinterpret_cast<const CUtensorMap *>(tmR),
-      *reinterpret_cast<const CUtensorMap *>(tmB), c, nullptr);
+  if (g.codeR)
+    launch_rm<MODE_RESTRICT, true>(g, c, tmR, tmB, nullptr, s);
+  else
+    launch_rm<MODE_RESTRICT, false>(g, c, tmR, tmB, nullptr, s);
 }
 
 int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
 
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s) {
-  static size_t configured = 0;
-  set_smem(k_resid_march<MODE_NORM>, resid_smem_bytes(), &configured);
-  k_resid_march<MODE_NORM><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
-      g, *reinterpret_cast<const CUtensorMap *>(tmR),
-      *reinterpret_cast<const CUtensorMap *>(tmB), g, partials);
+  if (g.codeR)
+    launch_rm<MODE_NORM, true>(g, g, tmR, tmB, partials, s);
+  else
+    launch_rm<MODE_NORM, false>(g, g, tmR, tmB, partials, s);
 }
 
 }  // namespace mg

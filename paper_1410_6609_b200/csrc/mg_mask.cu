@@ -212,6 +212,45 @@ void launch_coarse_coef(const Grid &f, const Grid &c, float *coefR,
   if (n > 0) k_coarse_coef<<<nblk(n), kT, 0, s>>>(f, c, coefR, coefB);
 }
 
+// ---- float records -> byte codes, when every kappa is 0 or 1 ------------------
+// (the mask is aligned with this level's cells: then the level can use the
+// byte-code marching kernels).  *fail is set if any cell is not representable.
+__global__ void __launch_bounds__(kT)
+    k_coef_to_code(Grid g, unsigned char *codeR, unsigned char *codeB, int *fail) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  const int col = (i + j + z) & 1;
+  const long long e = rb(g, il, j) + (z >> 1);
+  const float *r = (col ? g.coefB : g.coefR) + 8 * e;
+  unsigned char cd = 0;
+  if (r[6] != 0.f) {
+    cd = 64;
+    int n = 0;
+    for (int f = 0; f < 6; f++) {
+      if (r[f] == 1.f) {
+        cd |= (unsigned char)(1 << f);
+        n++;
+      } else if (r[f] != 0.f) {
+        atomicOr(fail, 1);
+      }
+    }
+    const int nd = ndir(g, i, j, z);
+    if (r[7] != (float)nd || r[6] != (float)(n + 2 * nd)) atomicOr(fail, 1);
+  }
+  (col ? codeB : codeR)[e] = cd;
+}
+
+void launch_coef_to_code(const Grid &g, unsigned char *codeR, unsigned char *codeB,
+                         int *fail, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0) k_coef_to_code<<<nblk(n), kT, 0, s>>>(g, codeR, codeB, fail);
+}
+
 // ---- RBGS half-sweep, variable coefficients -----------------------------------
 __global__ void __launch_bounds__(kT)
     k_smooth_var(Grid g, int color, int from_zero) {

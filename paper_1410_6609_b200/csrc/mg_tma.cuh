@@ -72,6 +72,32 @@ __device__ __forceinline__ int centre_dm(const Grid &g, int i, int j, int z) {
   return d;
 }
 
+// masked levels with byte codes (bits 0-5 kappa in {0,1} for faces x-,x+,
+// y-,y+,z-,z+, bit 6 fluid): number of Dirichlet faces the cell touches,
+// and t = sum_q kappa_q phi_q in the fixed face order (kappa as 0.0 / 1.0,
+// the same products and order as the variable-coefficient kernels)
+__device__ __forceinline__ int ndir_m(const Grid &g, int i, int j, int z) {
+  return (i == 0 && g.dface[0] > 0) + (i == g.nx - 1 && g.dface[1] > 0) +
+         (j == 0 && g.dface[2] > 0) + (j == g.ny - 1 && g.dface[3] > 0) +
+         (z == 0 && g.dface[4] > 0) + (z == g.nz - 1 && g.dface[5] > 0);
+}
+
+// kappa in {0,1}: kappa*phi is phi or a signed zero; selecting +0 instead
+// changes at most the sign of an exactly-zero sum, never a nonzero value
+__device__ __forceinline__ double ksum(unsigned cd, double xm, double xp,
+                                       double ym, double yp, double zm,
+                                       double zp) {
+  const double t0 = (cd & 1) ? xm : 0.0, t1 = (cd & 2) ? xp : 0.0;
+  const double t2 = (cd & 4) ? ym : 0.0, t3 = (cd & 8) ? yp : 0.0;
+  const double t4 = (cd & 16) ? zm : 0.0, t5 = (cd & 32) ? zp : 0.0;
+  return ((((t0 + t1) + t2) + t3) + t4) + t5;
+}
+
+__device__ __forceinline__ double kdiag(const Grid &g, unsigned cd, int i, int j,
+                                        int z) {
+  return (double)(__popc(cd & 63u) + 2 * ndir_m(g, i, j, z));
+}
+
 __host__ __device__ inline int round128(int bytes) { return (bytes + 127) / 128 * 128; }
 
 // smoother ring slot: (TY + 2) rows of pz doubles

@@ -448,3 +448,42 @@ def test_mask_loopback_equals_single(mg):
         res.append((r, s.get_solution()))
     assert np.array_equal(res[0][1], res[1][1])
     assert np.allclose(res[0][0], res[1][0], rtol=1e-13, atol=0)
+
+
+@pytest.mark.parametrize("scale", [4])
+def test_config5_march_codes_parity(mg, scale):
+    """Config-5 recipe at 1/4 scale (512x128x128): levels aligned with the beam
+    use byte face codes and the TMA-marching kernels (nz/2 = 64); V(3,3) to
+    1e-8 against the oracle."""
+    w = W.cfg5(scale=scale, n_spheres=400)
+    s, o = mask_pair(mg, w.shape, w.solid, min_coarse=w.min_coarse, nu1=3, nu2=3)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    rc, cg, hg = s.solve(w.tol, 40)
+    so, co, ho = o.solve(w.tol, 40)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    for l in range(o.nlevels):
+        assert np.array_equal(s.get_stencil(l), o.stencil(l)), l
+
+
+@pytest.mark.parametrize("codes", [True, False])
+def test_mask_march_equals_var_kernels(mg, codes, monkeypatch):
+    """Masked V-cycles: byte-code marching kernels == variable-coefficient
+    direct kernels, bit for bit (random mask: coarse levels not aligned)."""
+    shape = (32, 16, 256)
+    solid = random_mask(shape, 0.1, 7) if not codes else W.beam_mask(shape)
+    f = np.random.default_rng(14).uniform(-1, 1, shape)
+    out = []
+    for no_march in (False, True):
+        if no_march:
+            monkeypatch.setenv("MG_NO_MARCH", "1")
+        bt, bv = BCS["channel"]
+        s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=2, nu1=3, nu2=3)
+        s.set_mask(solid)
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(3)]
+        out.append((r, s.get_solution()))
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
