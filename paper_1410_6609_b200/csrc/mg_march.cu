@@ -139,14 +139,19 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   double2 E[kTPW];
   if (PROLONG && nplanes > 2) load_e(2, E);
 
-  // f of the first plane into registers
+  // f (and, masked, the own face codes) of the first plane into registers
   double2 fr[NCH];
+  unsigned cr[NCH];
+  const unsigned char *__restrict__ cown = color ? g.codeB : g.codeR;
 #pragma unroll
   for (int c = 0; c < NCH; c++) {
     const int k = 2 * lane + 64 * c;
-    if (row_ok && k < g.nzh)
-      fr[c] = *reinterpret_cast<const double2 *>(
-          fown + (long long)(i0 + 1) * g.plane + (long long)(j + 1) * pz + k);
+    cr[c] = 0x4040u;
+    if (row_ok && k < g.nzh) {
+      const long long o = (long long)(i0 + 1) * g.plane + (long long)(j + 1) * pz + k;
+      fr[c] = *reinterpret_cast<const double2 *>(fown + o);
+      if (MASK) cr[c] = *reinterpret_cast<const unsigned short *>(cown + o);
+    }
   }
 
   for (int il = i0; il < i1; il++) {
@@ -179,13 +184,17 @@ __global__ void __launch_bounds__(kThreadsM, 2)
 
     // prefetch f of the next plane
     double2 fn[NCH];
+    unsigned cn[NCH];
     const bool more = il + 1 < i1;
 #pragma unroll
     for (int c = 0; c < NCH; c++) {
       const int k = 2 * lane + 64 * c;
-      if (more && row_ok && k < g.nzh)
-        fn[c] = *reinterpret_cast<const double2 *>(
-            fown + (long long)(il + 2) * g.plane + (long long)(j + 1) * pz + k);
+      cn[c] = 0x4040u;
+      if (more && row_ok && k < g.nzh) {
+        const long long o = (long long)(il + 2) * g.plane + (long long)(j + 1) * pz + k;
+        fn[c] = *reinterpret_cast<const double2 *>(fown + o);
+        if (MASK) cn[c] = *reinterpret_cast<const unsigned short *>(cown + o);
+      }
     }
     if (row_ok) {
       const double *cur = ring + (size_t)(q % kSlots) * sd + (warp + 1) * pz;
@@ -219,10 +228,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         double s0, s1, d0, d1;
         unsigned cd0 = 64, cd1 = 64;
         if (MASK) {
-          const unsigned char *oc = (color ? g.codeB : g.codeR) +
-                                    (long long)(il + 1) * g.plane +
-                                    (long long)(j + 1) * pz + k;
-          const unsigned cc2 = *reinterpret_cast<const unsigned short *>(oc);
+          const unsigned cc2 = cr[c];
           cd0 = cc2 & 0xffu;
           cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
           s0 = ksum(cd0, a.x, b.x, ym.x, yp.x, zm0, zp0);
@@ -248,7 +254,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       }
     }
 #pragma unroll
-    for (int c = 0; c < NCH; c++) fr[c] = fn[c];
+    for (int c = 0; c < NCH; c++) {
+      fr[c] = fn[c];
+      cr[c] = cn[c];
+    }
   }
 }
 
@@ -312,8 +321,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   double acc = 0.0;
   double sdx0[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // restriction, even plane
 
-  // f of both colours, first plane
+  // f (and, masked, face codes) of both colours, first plane
   double2 fR[2], fB[2];
+  unsigned cR[2] = {0x4040u, 0x4040u}, cB[2] = {0x4040u, 0x4040u};
 #pragma unroll
   for (int c = 0; c < 2; c++) {
     const int k = kz0 + 2 * lane + 64 * c;
@@ -321,6 +331,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const long long o = (long long)(i0 + 1) * g.plane + (long long)(j + 1) * g.pz + k;
       fR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
       fB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+      if (MASK) {
+        cR[c] = *reinterpret_cast<const unsigned short *>(g.codeR + o);
+        cB[c] = *reinterpret_cast<const unsigned short *>(g.codeB + o);
+      }
     }
   }
 
@@ -338,6 +352,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     mbar_wait(&bars[(q + 1) % kSlots], ((q + 1) / kSlots) & 1);
 
     double2 nR[2], nB[2];
+    unsigned ncR[2] = {0x4040u, 0x4040u}, ncB[2] = {0x4040u, 0x4040u};
     const bool more = il + 1 < i1;
 #pragma unroll
     for (int c = 0; c < 2; c++) {
@@ -346,6 +361,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const long long o = (long long)(il + 2) * g.plane + (long long)(j + 1) * g.pz + k;
         nR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
         nB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+        if (MASK) {
+          ncR[c] = *reinterpret_cast<const unsigned short *>(g.codeR + o);
+          ncB[c] = *reinterpret_cast<const unsigned short *>(g.codeB + o);
+        }
       }
     }
     const int i = g.x0 + il;
@@ -390,10 +409,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           double s0, s1, d0, d1;
           unsigned cd0 = 64, cd1 = 64;
           if (MASK) {
-            const unsigned char *oc = (col ? g.codeB : g.codeR) +
-                                      (long long)(il + 1) * g.plane +
-                                      (long long)(j + 1) * g.pz + k;
-            const unsigned cc2 = *reinterpret_cast<const unsigned short *>(oc);
+            const unsigned cc2 = col ? cB[c] : cR[c];
             cd0 = cc2 & 0xffu;
             cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
             s0 = ksum(cd0, a.x, bb.x, ym.x, yp.x, zm0, zp0);
@@ -465,6 +481,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     for (int c = 0; c < 2; c++) {
       fR[c] = nR[c];
       fB[c] = nB[c];
+      cR[c] = ncR[c];
+      cB[c] = ncB[c];
     }
   }
   if (MODE == MODE_NORM) {
