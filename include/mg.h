@@ -148,6 +148,17 @@ int mg_nccl_unique_id(unsigned char out[128]);
  * variable-coefficient kernels.  solid == NULL removes the mask.  Call before
  * setting the RHS (the RHS is re-zeroed on solid cells). */
 int mg_set_mask(mg_ctx *ctx, const uint8_t *solid, int where);
+/* Boundary patch (config 5's paper-faithful partial-length electrodes,
+ * reading c17): on face `face` the cells with in-face coordinates
+ * a in [a0,a1), b in [b0,b1) get BC (type, value).  In-face coordinates are
+ * the two other axes in (x,y,z) order (x faces: (y,z); y faces: (x,z);
+ * z faces: (x,y)), global indices.  Switches the context to the
+ * variable-coefficient kernels (level-0 coefficient records) and rebuilds the
+ * Galerkin hierarchy; set the RHS afterwards (its BC adaptation uses the
+ * patch values).  MG_ERR_ARG for a rectangle outside the face, MG_ERR_BC for
+ * a type other than Dirichlet / Neumann. */
+int mg_set_bc_patch(mg_ctx *ctx, int face, int a0, int a1, int b0, int b1,
+                    int type, double value);
 /* The operator of level l as 7 coefficients per cell [centre, x-, x+, y-, y+,
  * z-, z+] (natural layout, the caller's part as mg_get_field), zeros on solid
  * cells.  For tests against the oracle's Galerkin stencils. */

@@ -81,6 +81,7 @@ def lib():
         L.orc_vcycle.argtypes = [P]
         L.orc_solve.argtypes = [P, d, i, ip, dp]
         L.orc_last_cg_iters.argtypes = [P]
+        L.orc_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         _lib = L
     return _lib
 
@@ -163,6 +164,11 @@ class Oracle:
         lib().orc_get_unknown(self._h, l,
                               out.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)))
         return out
+
+    def set_bc_patch(self, face, a0, a1, b0, b1, bc_type, value):
+        if lib().orc_set_bc_patch(self._h, face, a0, a1, b0, b1, int(bc_type),
+                                  float(value)) != 0:
+            raise ValueError("oracle: bad patch")
 
     # -- fields ------------------------------------------------------------
     def phi(self, l=0) -> np.ndarray:

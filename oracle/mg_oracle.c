@@ -50,6 +50,11 @@ struct orc_hier {
   double h;
   int bct[6];
   double bcv[6];
+  /* per face-cell BC (patches, "specified in input files"):
+   * face q has area A_q, cell (a,b) in the two remaining axes in (x,y,z)
+   * order; NULL = the face-uniform bct/bcv */
+  int *fty[6];
+  double *fva[6];
   int nu1, nu2;
   double alpha;
   double coarse_tol;
@@ -59,6 +64,22 @@ struct orc_hier {
 
 static inline long IDX(const level_t *L, int i, int j, int k) {
   return ((long)i * L->ny + j) * L->nz + k;
+}
+
+/* in-face coordinates of cell (i,j,k) on face q: the two other axes, in
+ * (x,y,z) order; index a*nb + b with nb the extent of the second one */
+static inline long face_index(const level_t *L, int q, int i, int j, int k) {
+  if (q < 2) return (long)j * L->nz + k;
+  if (q < 4) return (long)i * L->nz + k;
+  return (long)i * L->ny + j;
+}
+
+static inline int face_type(const orc_hier *H, int q, int i, int j, int k) {
+  return H->fty[q] ? H->fty[q][face_index(&H->L[0], q, i, j, k)] : H->bct[q];
+}
+
+static inline double face_value(const orc_hier *H, int q, int i, int j, int k) {
+  return H->fva[q] ? H->fva[q][face_index(&H->L[0], q, i, j, k)] : H->bcv[q];
 }
 
 /* value of a field at (i,j,k), 0 outside the level (the folded boundary
@@ -118,7 +139,7 @@ static void assemble_finest(orc_hier *H) {
           int outside = ii < 0 || jj < 0 || kk < 0 || ii >= L->nx ||
                         jj >= L->ny || kk >= L->nz;
           if (outside) {
-            if (H->bct[q] == ORC_DIRICHLET)
+            if (face_type(H, q, i, j, k) == ORC_DIRICHLET)
               beta = beta - alpha;
             else
               beta = beta + alpha;
@@ -220,7 +241,41 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
 void orc_destroy(orc_hier *H) {
   if (!H) return;
   for (int l = 0; l < H->nlev; l++) level_free(&H->L[l]);
+  for (int q = 0; q < 6; q++) {
+    free(H->fty[q]);
+    free(H->fva[q]);
+  }
   free(H);
+}
+
+/* Boundary patch (config 5's partial-length electrodes, reading c17): on face
+ * q the cells with in-face coordinates a in [a0,a1), b in [b0,b1) get BC
+ * (type, value).  Re-assembles the finest stencil and every Galerkin level;
+ * the caller re-sets the RHS (its BC adaptation uses the patches). */
+int orc_set_bc_patch(orc_hier *H, int q, int a0, int a1, int b0, int b1,
+                     int type, double value) {
+  level_t *L = &H->L[0];
+  if (q < 0 || q > 5) return -1;
+  const int ext[3] = {L->nx, L->ny, L->nz};
+  const int ax = q / 2;
+  const int na = ext[ax == 0 ? 1 : 0], nb = ext[ax == 2 ? 1 : 2];
+  if (a0 < 0 || b0 < 0 || a1 > na || b1 > nb || a0 > a1 || b0 > b1) return -1;
+  if (!H->fty[q]) {
+    H->fty[q] = (int *)malloc(sizeof(int) * (size_t)na * nb);
+    H->fva[q] = (double *)malloc(sizeof(double) * (size_t)na * nb);
+    for (long c = 0; c < (long)na * nb; c++) {
+      H->fty[q][c] = H->bct[q];
+      H->fva[q][c] = H->bcv[q];
+    }
+  }
+  for (int a = a0; a < a1; a++)
+    for (int b = b0; b < b1; b++) {
+      H->fty[q][(long)a * nb + b] = type;
+      H->fva[q][(long)a * nb + b] = value;
+    }
+  assemble_finest(H);
+  for (int l = 0; l + 1 < H->nlev; l++) galerkin(H, l);
+  return 0;
 }
 
 int orc_num_levels(const orc_hier *H) { return H->nlev; }
@@ -268,8 +323,8 @@ void orc_bc_adapt(orc_hier *H) {
                      j == L->ny - 1, k == 0, k == L->nz - 1};
         for (int q = 0; q < 6; q++) {
           if (!on[q]) continue;
-          double g = H->bcv[q];
-          if (H->bct[q] == ORC_DIRICHLET)
+          double g = face_value(H, q, i, j, k);
+          if (face_type(H, q, i, j, k) == ORC_DIRICHLET)
             L->f[c] = L->f[c] - 2.0 * alpha * g;
           else
             L->f[c] = L->f[c] - alpha * (H->h * g);

@@ -35,6 +35,9 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
                      const double *bc_value, const uint8_t *solid,
                      int min_coarse, int max_levels);
 void orc_destroy(orc_hier *H);
+/* per-face-cell boundary patch; returns 0 or -1 (bad arguments) */
+int orc_set_bc_patch(orc_hier *H, int face, int a0, int a1, int b0, int b1,
+                     int type, double value);
 
 int orc_num_levels(const orc_hier *H);
 void orc_level_dims(const orc_hier *H, int l, int *dims3);

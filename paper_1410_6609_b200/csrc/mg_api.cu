@@ -183,8 +183,13 @@ struct mg_ctx {
   std::vector<std::vector<TmPair>> tm;
   int use_march = 1;
   int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
-  bool masked = false;            // solid mask set (variable coefficients)
+  bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
+  std::vector<uint8_t> solid_h;   // global solid mask (empty: none)
+  bool patched = false;           // per-face-cell BCs set (mg_set_bc_patch)
+  std::vector<uint8_t> fty_h[6];  // face-cell BC types
+  std::vector<double> fva_h[6];   // face-cell BC values
+  mg::FaceBC fbc{};               // device copies (patched only)
   double h;
   mg_bc bc[6];
   mg_opts o;
@@ -631,7 +636,10 @@ int bc_adapt(mg_ctx *c) {
   }
   for (const Grid &g : c->g[0]) {
     mg::launch_zero_solid(g, c->stream);  // masked cells are not unknowns
-    mg::launch_bc_adapt(g, terms, types, c->stream);
+    if (c->patched)
+      mg::launch_bc_adapt_faces(g, c->fbc, alpha, c->h, c->stream);
+    else
+      mg::launch_bc_adapt(g, terms, types, c->stream);
   }
   CK(cudaGetLastError());
   return MG_OK;
@@ -1088,76 +1096,89 @@ int mg_coarse_solve(mg_ctx *c, int *iters) {
   return MG_OK;
 }
 
-int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
-  if (!c) return fail(MG_ERR_ARG, "null ctx");
+}  // extern "C"
+
+namespace {
+
+// (Re)build the variable-coefficient representation from the solid mask and
+// the face-cell BCs: level-0 float records (mask + patch types), Galerkin
+// coarse records level by level, and byte codes on every level whose records
+// all have kappa in {0,1} and position-derived delta.
+int rebuild_coefficients(mg_ctx *c) {
   CK(cudaStreamSynchronize(c->stream));
   if (c->graph) {
     cudaGraphExecDestroy(c->graph);
     c->graph = nullptr;
   }
   free_mask(c);
-  if (!solid) return MG_OK;
-  const size_t N = (size_t)c->pl.dims[0][0] * c->pl.dims[0][1] * c->pl.dims[0][2];
+  c->fbc = mg::FaceBC{};
+  if (c->solid_h.empty() && !c->patched) return MG_OK;
   unsigned char *dmask = nullptr;
-  CK(cudaMalloc(&dmask, N));
-  c->mask_bufs.push_back(dmask);
-  CK(cudaMemcpyAsync(dmask, solid, N,
-                     where == MG_DEVICE ? cudaMemcpyDeviceToDevice
-                                        : cudaMemcpyHostToDevice,
-                     c->stream));
+  if (!c->solid_h.empty()) {
+    CK(cudaMalloc(&dmask, c->solid_h.size()));
+    c->mask_bufs.push_back(dmask);
+    CK(cudaMemcpyAsync(dmask, c->solid_h.data(), c->solid_h.size(),
+                       cudaMemcpyHostToDevice, c->stream));
+  }
+  if (c->patched)
+    for (int q = 0; q < 6; q++) {
+      unsigned char *t = nullptr;
+      double *v = nullptr;
+      CK(cudaMalloc(&t, c->fty_h[q].size()));
+      c->mask_bufs.push_back(t);
+      CK(cudaMalloc(&v, c->fva_h[q].size() * sizeof(double)));
+      c->mask_bufs.push_back(v);
+      CK(cudaMemcpyAsync(t, c->fty_h[q].data(), c->fty_h[q].size(),
+                         cudaMemcpyHostToDevice, c->stream));
+      CK(cudaMemcpyAsync(v, c->fva_h[q].data(), c->fva_h[q].size() * sizeof(double),
+                         cudaMemcpyHostToDevice, c->stream));
+      c->fbc.ty[q] = t;
+      c->fbc.va[q] = v;
+    }
+  // float records on every level
   for (int l = 0; l < c->pl.L; l++)
     for (Grid &g : c->g[l]) {
       const size_t ne = (size_t)mg::grid_elems(g);
-      if (l == 0) {
-        unsigned char *r = nullptr, *b = nullptr;
-        CK(cudaMalloc(&r, ne));
-        c->mask_bufs.push_back(r);
-        CK(cudaMalloc(&b, ne));
-        c->mask_bufs.push_back(b);
-        CK(cudaMemsetAsync(r, 0, ne, c->stream));
-        CK(cudaMemsetAsync(b, 0, ne, c->stream));
-        g.codeR = r;
-        g.codeB = b;
-      } else {
-        float *r = nullptr, *b = nullptr;
-        CK(cudaMalloc(&r, ne * 8 * sizeof(float)));
-        c->mask_bufs.push_back(r);
-        CK(cudaMalloc(&b, ne * 8 * sizeof(float)));
-        c->mask_bufs.push_back(b);
-        CK(cudaMemsetAsync(r, 0, ne * 8 * sizeof(float), c->stream));
-        CK(cudaMemsetAsync(b, 0, ne * 8 * sizeof(float), c->stream));
-        g.coefR = r;
-        g.coefB = b;
-      }
+      float *r = nullptr, *b = nullptr;
+      CK(cudaMalloc(&r, ne * 8 * sizeof(float)));
+      c->mask_bufs.push_back(r);
+      CK(cudaMalloc(&b, ne * 8 * sizeof(float)));
+      c->mask_bufs.push_back(b);
+      CK(cudaMemsetAsync(r, 0, ne * 8 * sizeof(float), c->stream));
+      CK(cudaMemsetAsync(b, 0, ne * 8 * sizeof(float), c->stream));
+      g.coefR = r;
+      g.coefB = b;
     }
   for (Grid &g : c->g[0])
-    mg::launch_mask_codes(g, dmask, const_cast<unsigned char *>(g.codeR),
-                          const_cast<unsigned char *>(g.codeB), c->stream);
-  for (int l = 0; l + 1 < c->pl.L; l++) {
-    for (int s = 0; s < (int)c->g[l].size(); s++) {
-      const Grid &cg = coarse_of(c, l, s);
-      mg::launch_coarse_coef(c->g[l][s], cg, const_cast<float *>(cg.coefR),
-                             const_cast<float *>(cg.coefB), c->stream);
+    mg::launch_level0_coef(g, dmask, c->fbc, const_cast<float *>(g.coefR),
+                           const_cast<float *>(g.coefB), c->stream);
+  int *dfail = nullptr;
+  CK(cudaMalloc(&dfail, sizeof(int)));
+  c->mask_bufs.push_back(dfail);
+  for (int l = 0; l < c->pl.L; l++) {
+    if (l > 0) {
+      for (int s = 0; s < (int)c->g[l - 1].size(); s++) {
+        const Grid &cg = coarse_of(c, l - 1, s);
+        mg::launch_coarse_coef(c->g[l - 1][s], cg, const_cast<float *>(cg.coefR),
+                               const_cast<float *>(cg.coefB), c->stream);
+      }
+      if (l == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
+        const Grid &G = c->g[l][0];
+        const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
+        float *R = const_cast<float *>(G.coefR), *B = const_cast<float *>(G.coefB);
+        int rc;
+        if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+        g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
+                         ncclFloat, c->comm, c->stream);
+        g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
+                         ncclFloat, c->comm, c->stream);
+        if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef)"))) return rc;
+      }
     }
-    if (l + 1 == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
-      const Grid &G = c->g[l + 1][0];
-      const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
-      float *R = const_cast<float *>(G.coefR), *B = const_cast<float *>(G.coefB);
-      int rc;
-      if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-      g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
-                       ncclFloat, c->comm, c->stream);
-      g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
-                       ncclFloat, c->comm, c->stream);
-      if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef)"))) return rc;
-    }
-    // level l+1 aligned with the mask (every kappa 0 or 1)?  then byte codes
-    int *dfail = nullptr;
-    CK(cudaMalloc(&dfail, sizeof(int)));
-    c->mask_bufs.push_back(dfail);
+    // level l aligned (every kappa 0 or 1, delta from the position)?  codes
     CK(cudaMemsetAsync(dfail, 0, sizeof(int), c->stream));
     std::vector<std::pair<unsigned char *, unsigned char *>> codes;
-    for (Grid &g : c->g[l + 1]) {
+    for (Grid &g : c->g[l]) {
       const size_t ne = (size_t)mg::grid_elems(g);
       unsigned char *r = nullptr, *b = nullptr;
       CK(cudaMalloc(&r, ne));
@@ -1174,8 +1195,8 @@ int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
     if (!hfail && !getenv("MG_NO_MASK_CODES"))
-      for (size_t s = 0; s < c->g[l + 1].size(); s++) {
-        Grid &g = c->g[l + 1][s];
+      for (size_t s = 0; s < c->g[l].size(); s++) {
+        Grid &g = c->g[l][s];
         g.codeR = codes[s].first;
         g.codeB = codes[s].second;
         g.coefR = g.coefB = nullptr;
@@ -1183,10 +1204,57 @@ int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
   }
   CK(cudaGetLastError());
   c->masked = true;
-  // masked cells are not unknowns: clear their f
   for (const Grid &g : c->g[0]) mg::launch_zero_solid(g, c->stream);
   c->prev_norm = -1.0;
   return sync(c);
+}
+
+}  // namespace
+
+extern "C" {
+
+int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  const size_t N = (size_t)c->pl.dims[0][0] * c->pl.dims[0][1] * c->pl.dims[0][2];
+  if (!solid) {
+    c->solid_h.clear();
+  } else {
+    c->solid_h.resize(N);
+    if (where == MG_DEVICE)
+      CK(cudaMemcpy(c->solid_h.data(), solid, N, cudaMemcpyDeviceToHost));
+    else
+      memcpy(c->solid_h.data(), solid, N);
+  }
+  return rebuild_coefficients(c);
+}
+
+int mg_set_bc_patch(mg_ctx *c, int face, int a0, int a1, int b0, int b1,
+                    int type, double value) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (face < 0 || face > 5) return fail(MG_ERR_ARG, "bad face %d", face);
+  if (type != MG_DIRICHLET && type != MG_NEUMANN)
+    return fail(MG_ERR_BC, "patch type must be Dirichlet or Neumann");
+  const int ext[3] = {c->pl.dims[0][0], c->pl.dims[0][1], c->pl.dims[0][2]};
+  const int ax = face / 2;
+  const int na = ext[ax == 0 ? 1 : 0], nb = ext[ax == 2 ? 1 : 2];
+  if (a0 < 0 || b0 < 0 || a1 > na || b1 > nb || a0 > a1 || b0 > b1)
+    return fail(MG_ERR_ARG, "patch [%d,%d)x[%d,%d) outside face %d (%dx%d)", a0,
+                a1, b0, b1, face, na, nb);
+  if (!c->patched) {
+    for (int q = 0; q < 6; q++) {
+      const int aq = q / 2;
+      const size_t n = (size_t)ext[aq == 0 ? 1 : 0] * ext[aq == 2 ? 1 : 2];
+      c->fty_h[q].assign(n, (uint8_t)c->bc[q].type);
+      c->fva_h[q].assign(n, c->bc[q].value);
+    }
+    c->patched = true;
+  }
+  for (int x = a0; x < a1; x++)
+    for (int y = b0; y < b1; y++) {
+      c->fty_h[face][(size_t)x * nb + y] = (uint8_t)type;
+      c->fva_h[face][(size_t)x * nb + y] = value;
+    }
+  return rebuild_coefficients(c);
 }
 
 int mg_get_stencil(mg_ctx *c, int l, double *out, int where) {

@@ -84,6 +84,18 @@ void launch_black_restrict(const Grid &g, const Grid &c, const void *tm_red12,
                            cudaStream_t s);
 int launch_black_norm(const Grid &g, const void *tm_red12, double *partials,
                       cudaStream_t s);
+// per-face-cell boundary conditions (mg_set_bc_patch); null = face-uniform.
+// Face q cell (a, b): q<2 -> (j, z), q<4 -> (i, z), else (i, j); index a*nb+b
+struct FaceBC {
+  const unsigned char *ty[6];  // MG_DIRICHLET / MG_NEUMANN per face cell
+  const double *va[6];         // g_d / g_n per face cell
+};
+// level-0 float coefficient records from the mask (nullable) and face BCs
+void launch_level0_coef(const Grid &g, const unsigned char *solid_global,
+                        const FaceBC &fb, float *coefR, float *coefB,
+                        cudaStream_t s);
+void launch_bc_adapt_faces(const Grid &g, const FaceBC &fb, double alpha,
+                           double h, cudaStream_t s);
 // masked (variable-coefficient) path, mg_mask.cu
 void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
                        unsigned char *codeR, unsigned char *codeB,

@@ -163,6 +163,102 @@ void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
   if (n > 0) k_mask_codes<<<nblk(n), kT, 0, s>>>(g, solid_global, codeR, codeB);
 }
 
+// ---- level-0 records from mask + per-face-cell BCs ------------------------------
+__device__ __forceinline__ long long face_idx(const Grid &g, int q, int i, int j,
+                                              int z) {
+  if (q < 2) return (long long)j * g.nz + z;
+  if (q < 4) return (long long)i * g.nz + z;
+  return (long long)i * g.ny + j;
+}
+
+__device__ __forceinline__ bool face_dirichlet(const Grid &g, const FaceBC &fb,
+                                               int q, int i, int j, int z) {
+  if (fb.ty[q]) return fb.ty[q][face_idx(g, q, i, j, z)] == 0;
+  return g.dface[q] > 0;
+}
+
+__global__ void __launch_bounds__(kT)
+    k_level0_coef(Grid g, const unsigned char *solid, FaceBC fb, float *coefR,
+                  float *coefB) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  auto fluid = [&](int a, int b, int c) -> bool {
+    return !solid || solid[((long long)a * g.ny + b) * g.nz + c] == 0;
+  };
+  float rec[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (fluid(i, j, z)) {
+    const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0},
+              dk[6] = {0, 0, 0, 0, -1, 1};
+    float D = 0.f, del = 0.f;
+    for (int f = 0; f < 6; f++) {
+      const int a = i + di[f], b = j + dj[f], c = z + dk[f];
+      if (a < 0 || b < 0 || c < 0 || a >= g.nx || b >= g.ny || c >= g.nz) {
+        if (face_dirichlet(g, fb, f, i, j, z)) del += 1.f;
+      } else if (fluid(a, b, c)) {
+        rec[f] = 1.f;
+        D += 1.f;
+      }
+    }
+    rec[6] = D + 2.f * del;
+    rec[7] = del;
+  }
+  const int col = (i + j + z) & 1;
+  float *out = (col ? coefB : coefR) + 8 * (rb(g, il, j) + (z >> 1));
+  for (int r = 0; r < 8; r++) out[r] = rec[r];
+}
+
+void launch_level0_coef(const Grid &g, const unsigned char *solid_global,
+                        const FaceBC &fb, float *coefR, float *coefB,
+                        cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0) k_level0_coef<<<nblk(n), kT, 0, s>>>(g, solid_global, fb, coefR, coefB);
+}
+
+// ---- finest-grid RHS adaptation with per-face-cell BCs ---------------
+// same expressions as the uniform kernel: f -= (2 alpha) g (Dirichlet) or
+// alpha (h g) (Neumann), in face order; solid cells skipped
+__global__ void __launch_bounds__(kT)
+    k_bc_adapt_faces(Grid g, FaceBC fb, double alpha, double h) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny) return;
+  const int j = (int)(t % g.ny);
+  const int il = (int)(t / g.ny);
+  const int i = g.x0 + il;
+  const bool full = (i == 0 || i == g.nx - 1 || j == 0 || j == g.ny - 1);
+  const long long b = rb(g, il, j);
+  const int step = full ? 1 : (g.nz - 1 > 0 ? g.nz - 1 : 1);
+  for (int z = 0; z < g.nz; z += step) {
+    const int col = (i + j + z) & 1;
+    const long long e = b + (z >> 1);
+    Coef C;
+    coef_at(g, col, e, i, j, z, C);
+    if (C.D == 0.0) continue;
+    double *f = col ? g.fB : g.fR;
+    double v = f[e];
+    const bool on[6] = {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, z == 0,
+                        z == g.nz - 1};
+    for (int q = 0; q < 6; q++) {
+      if (!on[q]) continue;
+      const long long fi = face_idx(g, q, i, j, z);
+      const bool dir = fb.ty[q] ? fb.ty[q][fi] == 0 : g.dface[q] > 0;
+      const double gv = fb.va[q][fi];
+      v = dir ? v - 2.0 * alpha * gv : v - alpha * (h * gv);
+    }
+    f[e] = v;
+  }
+}
+
+void launch_bc_adapt_faces(const Grid &g, const FaceBC &fb, double alpha,
+                           double h, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny;
+  if (n > 0) k_bc_adapt_faces<<<nblk(n), kT, 0, s>>>(g, fb, alpha, h);
+}
+
 // ---- Galerkin coarse coefficients (face-transmissibility form) ---------------
 __global__ void __launch_bounds__(kT)
     k_coarse_coef(Grid F, Grid C, float *coefR, float *coefB) {

@@ -119,6 +119,7 @@ def lib():
         L.mg_prolong_correct.argtypes = [P, i]
         L.mg_coarse_solve.argtypes = [P, ip]
         L.mg_set_mask.argtypes = [P, dp, i]
+        L.mg_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
@@ -322,6 +323,12 @@ class Multigrid:
         a = np.ascontiguousarray(solid, dtype=np.uint8)
         self._mask_keep = a
         _check(lib().mg_set_mask(self._ctx, a.ctypes.data, MG_HOST), self._ctx)
+
+    def set_bc_patch(self, face, a0, a1, b0, b1, bc_type, value):
+        """Per-face-cell BC on a rectangle of face `face` (include/mg.h)."""
+        _check(lib().mg_set_bc_patch(self._ctx, int(face), int(a0), int(a1),
+                                     int(b0), int(b1), int(bc_type),
+                                     float(value)), self._ctx)
 
     def get_stencil(self, level=0):
         out = np.empty(self.local_shape(level) + (7,), np.float64)

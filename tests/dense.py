@@ -19,7 +19,9 @@ DIRICHLET, NEUMANN = 0, 1
 
 
 def _ghost_pad(u, h, bc_type, bc_value, homogeneous):
-    """Pad u by one ghost layer per face with the paper's extrapolation."""
+    """Pad u by one ghost layer per face with the paper's extrapolation.
+    bc_type[face] / bc_value[face] may be scalars or arrays over the face
+    (the two other axes in (x,y,z) order): per-face-cell patches."""
     p = np.pad(u, 1)
     for face in range(6):
         ax, side = divmod(face, 2)
@@ -31,10 +33,9 @@ def _ghost_pad(u, h, bc_type, bc_value, homogeneous):
         else:
             sl_g[ax], sl_1[ax] = -1, -2
         inner = p[tuple(sl_1)]
-        if bc_type[face] == DIRICHLET:
-            p[tuple(sl_g)] = 2.0 * g - inner
-        else:
-            p[tuple(sl_g)] = inner + h * g
+        t = np.broadcast_to(np.asarray(bc_type[face]), inner.shape)
+        gg = np.broadcast_to(np.asarray(g, dtype=float), inner.shape)
+        p[tuple(sl_g)] = np.where(t == DIRICHLET, 2.0 * gg - inner, inner + h * gg)
     return p
 
 

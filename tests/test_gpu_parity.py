@@ -487,3 +487,32 @@ def test_mask_march_equals_var_kernels(mg, codes, monkeypatch):
         out.append((r, s.get_solution()))
     assert np.array_equal(out[0][1], out[1][1])
     assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
+
+
+
+def test_bc_patch_parity(mg):
+    """mg_set_bc_patch (partial-length electrodes, paper-faithful config-5
+    variant, reading c17): operators on every level, RHS, and a V(3,3) solve
+    match the oracle; combined with the beam mask."""
+    w = W.cfg5(scale=16, n_spheres=40)
+    nx = w.shape[0]
+    bt, bv = BCS["channel"]
+    s = mg.Multigrid(w.shape, 1.0, bt, bv, min_coarse=8, nu1=3, nu2=3)
+    o = oracle.Oracle(w.shape, 1.0, bt, bv, solid=w.solid, min_coarse=8,
+                      nu1=3, nu2=3)
+    s.set_mask(w.solid)
+    for face in (2, 3):  # electrodes only on the first 3/4 of the channel
+        s.set_bc_patch(face, 3 * nx // 4, nx, 0, w.shape[2], N, 0.0)
+        o.set_bc_patch(face, 3 * nx // 4, nx, 0, w.shape[2], N, 0.0)
+    for l in range(o.nlevels):
+        assert np.array_equal(s.get_stencil(l), o.stencil(l)), l
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    rc, cg, hg = s.solve(1e-8, 60)
+    so, co, ho = o.solve(1e-8, 60)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    with pytest.raises(mg.MGError):
+        s.set_bc_patch(2, 0, nx + 1, 0, 1, D, 0.0)

@@ -508,3 +508,43 @@ def test_masked_galerkin_face_transmissibility_form(seed):
                     for q in range(6):
                         assert st[I, J, K, 1 + q] == -c * kap[q] or (
                             kap[q] == 0 and st[I, J, K, 1 + q] == 0)
+
+
+def test_bc_patch_dense_direct_solve():
+    """Partial-length electrodes (reading c17): per-face-cell Dirichlet /
+    Neumann patches give the operator and RHS of the ghost-cell construction
+    with per-cell extrapolation -- dense solve on 8x8x8."""
+    shape, h = (8, 8, 8), 0.5
+    bt = [N, N, D, D, N, N]
+    bv = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    # y- face (x,z): Dirichlet 0 only for x < 6 (electrode ends), Neumann 0.5 after
+    o.set_bc_patch(2, 6, 8, 0, 8, N, 0.5)
+    # y+ face: Dirichlet 1 only for x < 6, z in [2, 8)
+    o.set_bc_patch(3, 6, 8, 0, 8, N, 0.0)
+    o.set_bc_patch(3, 0, 6, 0, 2, N, -0.25)
+    ty = [np.full((8, 8), t) for t in bt]
+    va = [np.full((8, 8), v) for v in bv]
+    ty[2][6:, :] = N
+    va[2][6:, :] = 0.5
+    ty[3][6:, :] = N
+    va[3][6:, :] = 0.0
+    ty[3][:6, :2] = N
+    va[3][:6, :2] = -0.25
+    n = 512
+    A = np.zeros((n, n))
+    e = np.zeros(n)
+    for cidx in range(n):
+        e[cidx] = 1.0
+        A[:, cidx] = dense.neg_laplacian_ghost(e.reshape(shape), h, ty,
+                                               [0.0] * 6).reshape(-1)
+        e[cidx] = 0.0
+    assert np.array_equal(dense.stencil_to_dense(o.stencil(0)), A)
+    f = np.random.default_rng(4).uniform(-1, 1, shape)
+    b = f - dense.neg_laplacian_ghost(np.zeros(shape), h, ty, va,
+                                      homogeneous=False)
+    u = np.linalg.solve(A, b.reshape(-1)).reshape(shape)
+    o.set_rhs(f)
+    st, cyc, hist = o.solve(1e-14, 80)
+    assert st == 0
+    assert np.linalg.norm(o.phi() - u) / np.linalg.norm(u) < 1e-12
