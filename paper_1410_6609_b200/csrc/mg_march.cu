@@ -85,32 +85,45 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   // Work split: task t = (row rr, 64-wide chunk c), t = warp + TY*m.
   constexpr int ntask = (kTY + 2) * NCH;
   constexpr int kTPW = (ntask + kTY - 1) / kTY;  // tasks per warp
+  // per-task constants (task t = warp + TY*m: row rr = t / NCH, chunk t % NCH)
+  int tRow[kTPW], tK[kTPW], tCoff[kTPW], tJp[kTPW];
+  bool tOk[kTPW];
+#pragma unroll
+  for (int m = 0; m < kTPW; m++) {
+    const int t = warp + kTY * m;
+    const int rr = t / NCH, c = t % NCH;
+    const int jj = j0 - 1 + rr;
+    const int k = 2 * lane + 64 * c;
+    tOk[m] = PROLONG && t < ntask && jj >= 0 && jj < g.ny && k < g.nzh;
+    tRow[m] = rr * pz;
+    tK[m] = k;
+    const int J = jj >> 1;
+    tCoff[m] = (J + 1) * C.pz + (k >> 1);
+    tJp[m] = J & 1;
+  }
   auto load_e = [&](int q, double2 *E) {
     const int i = g.x0 + i0 - 1 + q;
+    const bool pok = i >= 0 && i < g.nx;
     const int I = i >> 1;
+    const long long poff = (long long)(I - C.x0 + 1) * C.plane;
+    const int Ip = I & 1;
 #pragma unroll
     for (int m = 0; m < kTPW; m++) {
-      const int t = warp + kTY * m;
       E[m] = make_double2(0.0, 0.0);
-      if (!PROLONG || t >= ntask || i < 0 || i >= g.nx) continue;
-      const int rr = t / nch, c = t % nch;
-      const int jj = j0 - 1 + rr;
-      const int k = 2 * lane + 64 * c;
-      if (jj < 0 || jj >= g.ny || k >= g.nzh) continue;
-      const int J = jj >> 1;
+      if (!(pok && tOk[m])) continue;
       // parents of half-indices k, k+1 are coarse z = k, k+1: one red and
-      // one black coarse cell at coarse half-index k/2
-      const long long cb = (long long)(I - C.x0 + 1) * C.plane +
-                           (long long)(J + 1) * C.pz + (k >> 1);
-      const int c0 = (I + J + k) & 1;
+      // one black coarse cell at coarse half-index k/2 (k even)
+      const int c0 = (Ip + tJp[m]) & 1;
+      const long long cb = poff + tCoff[m];
       E[m].x = (c0 ? C.phiB : C.phiR)[cb];
       E[m].y = (c0 ? C.phiR : C.phiB)[cb];
       if (MASK) {  // solid cells of the other colour get no correction
+        // (array plane i0+q, array row jj+1 = j0+rr, element k)
         const unsigned char *oc = (color ? g.codeR : g.codeB) +
                                   (long long)(i0 + q) * g.plane +
-                                  (long long)(jj + 1) * pz + k;
+                                  (long long)j0 * pz + tRow[m] + tK[m];
         if (!(oc[0] & 64)) E[m].x = 0.0;
-        if (k + 1 < g.nzh && !(oc[1] & 64)) E[m].y = 0.0;
+        if (tK[m] + 1 < g.nzh && !(oc[1] & 64)) E[m].y = 0.0;
       }
     }
   };
@@ -120,13 +133,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     double *slot = ring + (size_t)(q % kSlots) * sd;
 #pragma unroll
     for (int m = 0; m < kTPW; m++) {
-      const int t = warp + kTY * m;
-      if (t >= ntask) continue;
-      const int rr = t / nch, c = t % nch;
-      const int jj = j0 - 1 + rr;
-      const int k = 2 * lane + 64 * c;
-      if (jj < 0 || jj >= g.ny || k >= g.nzh) continue;
-      double *row = slot + rr * pz;
+      if (!tOk[m]) continue;
+      double *row = slot + tRow[m];
+      const int k = tK[m];
       double2 v = lds2(row + k);
       v.x = v.x + alpha * E[m].x;
       v.y = v.y + alpha * E[m].y;
