@@ -367,32 +367,53 @@ __global__ void __launch_bounds__(kCgThreads)
   extern __shared__ double cg_sm[];
   __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
-  double *base = (N <= kCgSmemMax) ? cg_sm : scr;
+  const bool in_smem = N <= kCgSmemMax;
+  double *base = in_smem ? cg_sm : scr;
   double *x = base, *r = base + N, *p = base + 2 * N, *q = base + 3 * N;
+  // per-element geometry, computed once: neighbour-validity bits (x-,x+,y-,
+  // y+,z-,z+) and the centre d (closed-form operator A = c (d - neighbours))
+  unsigned char *nb = reinterpret_cast<unsigned char *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
+  signed char *dc = reinterpret_cast<signed char *>(nb + N);
+  const long long sx = (long long)g.ny * g.nz, sy = g.nz;
   int pb = 0;
   double acc = 0.0;
   for (long long n = threadIdx.x; n < N; n += blockDim.x) {
     const int z = (int)(n % g.nz);
     const long long t = n / g.nz;
+    const int j = (int)(t % g.ny), i = (int)(t / g.ny);
+    nb[n] = (unsigned char)((i > 0) | ((i < g.nx - 1) << 1) | ((j > 0) << 2) |
+                            ((j < g.ny - 1) << 3) | ((z > 0) << 4) |
+                            ((z < g.nz - 1) << 5));
+    dc[n] = (signed char)centre_d(g, i, j, z);
     int col;
-    const long long idx = split_index(g, (int)(t / g.ny), (int)(t % g.ny), z, &col);
+    const long long idx = split_index(g, i, j, z, &col);
     const double b = col ? g.fB[idx] : g.fR[idx];
     x[n] = 0.0;
     r[n] = b;
     p[n] = b;
     acc = acc + b * b;
   }
-  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes p
+  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes p, nb, dc
   pb ^= 1;
   const double bnorm = sqrt(rho);
+  const double c = g.c;
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
       acc = 0.0;
       for (long long n = threadIdx.x; n < N; n += blockDim.x) {
-        const double qn = cg_apply(g, p, n);
+        const unsigned m = nb[n];
+        const double xm = (m & 1) ? p[n - sx] : 0.0;
+        const double xp = (m & 2) ? p[n + sx] : 0.0;
+        const double ym = (m & 4) ? p[n - sy] : 0.0;
+        const double yp = (m & 8) ? p[n + sy] : 0.0;
+        const double zm = (m & 16) ? p[n - 1] : 0.0;
+        const double zp = (m & 32) ? p[n + 1] : 0.0;
+        const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
+        const double pn = p[n];
+        const double qn = c * ((double)dc[n] * pn - s);
         q[n] = qn;
-        acc = acc + p[n] * qn;
+        acc = acc + pn * qn;
       }
       const double pq = cg_allsum(acc, part[pb]);
       pb ^= 1;
@@ -426,17 +447,20 @@ __global__ void __launch_bounds__(kCgThreads)
 }
 
 size_t coarse_cg_scratch_doubles(const Grid &g) {
-  return 4 * (size_t)g.nx * g.ny * g.nz;
+  // x, r, p, q + one byte of neighbour bits and one of centre per element
+  return 5 * (size_t)g.nx * g.ny * g.nz;
 }
 
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
+  // 256 threads: enough for <= 16 elements per thread at the coarsest sizes,
+  // few warps in each block reduction
   int threads = (int)((N + 31) / 32 * 32);
-  if (threads > kCgThreads) threads = kCgThreads;
+  if (threads > 256) threads = 256;
   size_t smem = 0;
   if (N <= kCgSmemMax) {
-    smem = 4 * (size_t)N * sizeof(double);
+    smem = 4 * (size_t)N * sizeof(double) + 2 * (size_t)N;
     static size_t configured = 48 * 1024;
     if (smem > configured) {
       cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize,
