@@ -159,22 +159,33 @@ int mg_set_mask(mg_ctx *ctx, const uint8_t *solid, int where);
  * a type other than Dirichlet / Neumann. */
 int mg_set_bc_patch(mg_ctx *ctx, int face, int a0, int a1, int b0, int b1,
                     int type, double value);
+/* Per-cell boundary values on face `face` (the face's BC type unchanged):
+ * values[a*nb + b] for the face cells in the in-face order of
+ * mg_set_bc_patch (na x nb = the two other global extents).  For analytic
+ * Dirichlet data, e.g. the charged-sphere validation (Eq.18).
+ * The operator is unchanged (only the RHS adaptation uses the values); set
+ * the RHS afterwards. */
+int mg_set_face_values(mg_ctx *ctx, int face, const double *values);
 /* The operator of level l as 7 coefficients per cell [centre, x-, x+, y-, y+,
  * z-, z+] (natural layout, the caller's part as mg_get_field), zeros on solid
  * cells.  For tests against the oracle's Galerkin stencils. */
 int mg_get_stencil(mg_ctx *ctx, int level, double *out, int where);
 
 /* ---- right-hand side ----------------------------------------------------- */
-/* f := charge density of n uniformly charged spheres: every cell
- * whose centre satisfies |x_c - c_p|^2 <= R_p^2 (inclusive, reading
- * c13) receives rho_p = Q_p/(n_p h^3) (MG_CHARGE_PER_CELLS, n_p = number of
- * such cells in the whole domain) or Q_p/(4/3 pi R_p^3) (PER_VOLUME); cells
- * covered by several spheres receive the sum.  Then the finest-grid BC
- * adaptation.  centers[3n] (x,y,z physical), radii[n],
- * charges[n] are host arrays, read before return; every rank passes the full
- * list.  subsample must be 1 (s_f > 1 is not implemented: MG_ERR_ARG).
- * Errors: n < 0, R <= 0, a sphere that covers no cell centre with
- * PER_CELLS (MG_ERR_ARG).  Phi is not touched (warm start). */
+/* f := charge density of n uniformly charged spheres.  Each cell
+ * is subdivided into s^3 sub-cells (subsampling factor s = `subsample`,
+ * 1..16; s = 1 is the plain rule "each cell whose center is
+ * overlapped") and cnt = number of sub-cell centres with
+ * |x - c_p|^2 <= R_p^2 (inclusive, reading c13).  The cell receives
+ * (Q_p cnt)/(n_p h^3) (MG_CHARGE_PER_CELLS, n_p = covered sub-cells of the
+ * whole domain: the charge is exact) or (Q_p/(4/3 pi R_p^3)) (cnt/s^3)
+ * (PER_VOLUME, the paper's volume-fraction mapping); cells covered by
+ * several spheres receive the sum.  Then the finest-grid BC adaptation
+ * (P:731-732).  centers[3n] (x,y,z physical), radii[n], charges[n] are host
+ * arrays, read before return; every rank passes the full list.
+ * Errors: n < 0, R <= 0, subsample outside 1..16, a sphere that covers no
+ * sub-cell centre with PER_CELLS (MG_ERR_ARG).  Phi is not touched (warm
+ * start). */
 int mg_set_rhs_from_spheres(mg_ctx *ctx, int n, const double *centers,
                             const double *radii, const double *charges,
                             int normalization, int subsample);

@@ -82,6 +82,11 @@ def lib():
         L.orc_solve.argtypes = [P, d, i, ip, dp]
         L.orc_last_cg_iters.argtypes = [P]
         L.orc_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
+        L.orc_set_face_values.argtypes = [P, i, dp]
+        L.orc_sphere_subcount.restype = ctypes.c_long
+        L.orc_sphere_subcount.argtypes = [i, i, i, d, i, d, d, d, d]
+        L.orc_sphere_density_sub.argtypes = [i, i, i, d, i, i, dp, dp, dp, i, dp]
+        L.orc_set_rhs_from_spheres_sub.argtypes = [P, i, dp, dp, dp, i, i]
         _lib = L
     return _lib
 
@@ -94,22 +99,24 @@ def _f64(a):
     return np.ascontiguousarray(a, dtype=np.float64)
 
 
-def sphere_cell_count(shape, h, center, radius) -> int:
+def sphere_cell_count(shape, h, center, radius, subsample=1) -> int:
+    """Covered cells (s = 1) or covered sub-cells (s > 1) of one sphere."""
     nx, ny, nz = shape
-    return int(lib().orc_sphere_cell_count(nx, ny, nz, float(h),
-                                           float(center[0]), float(center[1]),
-                                           float(center[2]), float(radius)))
+    return int(lib().orc_sphere_subcount(nx, ny, nz, float(h), int(subsample),
+                                         float(center[0]), float(center[1]),
+                                         float(center[2]), float(radius)))
 
 
 def sphere_density(shape, h, centers, radii, charges,
-                   normalization=PER_CELLS) -> np.ndarray:
+                   normalization=PER_CELLS, subsample=1) -> np.ndarray:
     nx, ny, nz = shape
     c = _f64(centers).reshape(-1)
     r = _f64(radii)
     q = _f64(charges)
     out = np.empty((nx, ny, nz), np.float64)
-    lib().orc_sphere_density(nx, ny, nz, float(h), len(r), _dp(c), _dp(r),
-                             _dp(q), int(normalization), _dp(out))
+    lib().orc_sphere_density_sub(nx, ny, nz, float(h), int(subsample), len(r),
+                                 _dp(c), _dp(r), _dp(q), int(normalization),
+                                 _dp(out))
     return out
 
 
@@ -170,6 +177,11 @@ class Oracle:
                                   float(value)) != 0:
             raise ValueError("oracle: bad patch")
 
+    def set_face_values(self, face, values):
+        v = _f64(values).reshape(-1)
+        if lib().orc_set_face_values(self._h, int(face), _dp(v)) != 0:
+            raise ValueError("oracle: bad face")
+
     # -- fields ------------------------------------------------------------
     def phi(self, l=0) -> np.ndarray:
         out = np.empty(self.dims(l), np.float64)
@@ -197,12 +209,13 @@ class Oracle:
         lib().orc_set_rhs(self._h, _dp(f))
 
     def set_rhs_from_spheres(self, centers, radii, charges,
-                             normalization=PER_CELLS):
+                             normalization=PER_CELLS, subsample=1):
         c = _f64(centers).reshape(-1)
         r = _f64(radii)
         q = _f64(charges)
-        rc = lib().orc_set_rhs_from_spheres(self._h, len(r), _dp(c), _dp(r),
-                                            _dp(q), int(normalization))
+        rc = lib().orc_set_rhs_from_spheres_sub(self._h, len(r), _dp(c), _dp(r),
+                                                _dp(q), int(normalization),
+                                                int(subsample))
         if rc != 0:
             raise ValueError("oracle: a sphere covers no cell centre")
 

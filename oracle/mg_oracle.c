@@ -248,6 +248,23 @@ void orc_destroy(orc_hier *H) {
   free(H);
 }
 
+/* per-cell values on face q, the face's BC type unchanged (analytic
+ * Dirichlet data of the charged-sphere validation) */
+int orc_set_face_values(orc_hier *H, int q, const double *values) {
+  level_t *L = &H->L[0];
+  if (q < 0 || q > 5) return -1;
+  const int ext[3] = {L->nx, L->ny, L->nz};
+  const int ax = q / 2;
+  const long n = (long)ext[ax == 0 ? 1 : 0] * ext[ax == 2 ? 1 : 2];
+  if (!H->fty[q]) {
+    H->fty[q] = (int *)malloc(sizeof(int) * (size_t)n);
+    H->fva[q] = (double *)malloc(sizeof(double) * (size_t)n);
+    for (long c = 0; c < n; c++) H->fty[q][c] = H->bct[q];
+  }
+  for (long c = 0; c < n; c++) H->fva[q][c] = values[c];
+  return 0;
+}
+
 /* Boundary patch (config 5's partial-length electrodes, reading c17): on face
  * q the cells with in-face coordinates a in [a0,a1), b in [b0,b1) get BC
  * (type, value).  Re-assembles the finest stencil and every Galerkin level;
@@ -359,8 +376,23 @@ static void bbox(int n, double h, double c, double R, int *lo, int *hi) {
   *hi = b;
 }
 
-long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
-                           double cy, double cz, double R) {
+/* Subsampling (Table 4): "equidistantly subdivides a cell and
+ * counts the overlapped subvolumes" -- the s^3 sub-cell centres of cell
+ * (i,j,k) are ((i s + a + 1/2) h/s, ...), a = 0..s-1, tested with the same
+ * inclusive rule.  s = 1 is the plain centre rule (hs = h exactly). */
+static inline int sub_count(int i, int j, int k, int s, double hs, double cx,
+                            double cy, double cz, double R) {
+  int cnt = 0;
+  for (int a = 0; a < s; a++)
+    for (int b = 0; b < s; b++)
+      for (int c = 0; c < s; c++)
+        cnt += inside(i * s + a, j * s + b, k * s + c, hs, cx, cy, cz, R);
+  return cnt;
+}
+
+long orc_sphere_subcount(int nx, int ny, int nz, double h, int s, double cx,
+                         double cy, double cz, double R) {
+  const double hs = h / (double)s;
   int i0, i1, j0, j1, k0, k1;
   bbox(nx, h, cx, R, &i0, &i1);
   bbox(ny, h, cy, R, &j0, &j1);
@@ -369,59 +401,84 @@ long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
   for (int i = i0; i <= i1; i++)
     for (int j = j0; j <= j1; j++)
       for (int k = k0; k <= k1; k++)
-        cnt += inside(i, j, k, h, cx, cy, cz, R);
+        cnt += sub_count(i, j, k, s, hs, cx, cy, cz, R);
   return cnt;
 }
 
-/* charge density of uniformly charged spheres (c12):
- *   PER_CELLS:  rho_p = Q_p / (n_p h^3)  (charge spread over the n_p cells)
- *   PER_VOLUME: rho_p = Q_p / (4/3 pi R_p^3) (the paper's naive mapping)
+long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
+                           double cy, double cz, double R) {
+  return orc_sphere_subcount(nx, ny, nz, h, 1, cx, cy, cz, R);
+}
+
+/* charge density of uniformly charged spheres (c12), subsampling
+ * factor s, n_p = number of covered sub-cells of the domain:
+ *   PER_CELLS:  cell value = (Q_p cnt) / (n_p h^3)       (charge exact)
+ *   PER_VOLUME: cell value = (Q_p / (4/3 pi R^3)) (cnt / s^3)  (the paper's)
  * eps = 1 (c15), so f = rho.  Overlapping spheres add in sphere order. */
-void orc_sphere_density(int nx, int ny, int nz, double h, int n,
-                        const double *centers, const double *radii,
-                        const double *charges, int normalization,
-                        double *out) {
+void orc_sphere_density_sub(int nx, int ny, int nz, double h, int s, int n,
+                            const double *centers, const double *radii,
+                            const double *charges, int normalization,
+                            double *out) {
   long N = (long)nx * ny * nz;
+  const double hs = h / (double)s;
   for (long c = 0; c < N; c++) out[c] = 0.0;
   for (int p = 0; p < n; p++) {
     double cx = centers[3 * p], cy = centers[3 * p + 1],
-           cz = centers[3 * p + 2], R = radii[p];
-    long np = orc_sphere_cell_count(nx, ny, nz, h, cx, cy, cz, R);
-    double rho;
-    if (normalization == ORC_PER_VOLUME)
-      rho = charges[p] / ((4.0 / 3.0) * ORC_PI * (R * R * R));
-    else {
-      if (np == 0) continue;
-      rho = charges[p] / ((double)np * (h * h * h));
-    }
+           cz = centers[3 * p + 2], R = radii[p], Q = charges[p];
+    long np = orc_sphere_subcount(nx, ny, nz, h, s, cx, cy, cz, R);
+    if (normalization != ORC_PER_VOLUME && np == 0) continue;
+    const double rho0 = Q / ((4.0 / 3.0) * ORC_PI * (R * R * R));
     int i0, i1, j0, j1, k0, k1;
     bbox(nx, h, cx, R, &i0, &i1);
     bbox(ny, h, cy, R, &j0, &j1);
     bbox(nz, h, cz, R, &k0, &k1);
     for (int i = i0; i <= i1; i++)
       for (int j = j0; j <= j1; j++)
-        for (int k = k0; k <= k1; k++)
-          if (inside(i, j, k, h, cx, cy, cz, R))
-            out[((long)i * ny + j) * nz + k] += rho;
+        for (int k = k0; k <= k1; k++) {
+          const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+          if (!cnt) continue;
+          double v;
+          if (normalization == ORC_PER_VOLUME)
+            v = rho0 * ((double)cnt / (double)(s * s * s));
+          else
+            v = (Q * (double)cnt) / ((double)np * (h * h * h));
+          out[((long)i * ny + j) * nz + k] += v;
+        }
   }
+}
+
+void orc_sphere_density(int nx, int ny, int nz, double h, int n,
+                        const double *centers, const double *radii,
+                        const double *charges, int normalization,
+                        double *out) {
+  orc_sphere_density_sub(nx, ny, nz, h, 1, n, centers, radii, charges,
+                         normalization, out);
+}
+
+int orc_set_rhs_from_spheres_sub(orc_hier *H, int n, const double *centers,
+                                 const double *radii, const double *charges,
+                                 int normalization, int s) {
+  level_t *L = &H->L[0];
+  if (s < 1) return -1;
+  if (normalization == ORC_PER_CELLS)
+    for (int p = 0; p < n; p++)
+      if (orc_sphere_subcount(L->nx, L->ny, L->nz, H->h, s, centers[3 * p],
+                              centers[3 * p + 1], centers[3 * p + 2],
+                              radii[p]) == 0)
+        return -1;
+  orc_sphere_density_sub(L->nx, L->ny, L->nz, H->h, s, n, centers, radii,
+                         charges, normalization, L->f);
+  for (long c = 0; c < L->n; c++)
+    if (!L->unk[c]) L->f[c] = 0.0;
+  orc_bc_adapt(H);
+  return 0;
 }
 
 int orc_set_rhs_from_spheres(orc_hier *H, int n, const double *centers,
                              const double *radii, const double *charges,
                              int normalization) {
-  level_t *L = &H->L[0];
-  if (normalization == ORC_PER_CELLS)
-    for (int p = 0; p < n; p++)
-      if (orc_sphere_cell_count(L->nx, L->ny, L->nz, H->h, centers[3 * p],
-                                centers[3 * p + 1], centers[3 * p + 2],
-                                radii[p]) == 0)
-        return -1;
-  orc_sphere_density(L->nx, L->ny, L->nz, H->h, n, centers, radii, charges,
-                     normalization, L->f);
-  for (long c = 0; c < L->n; c++)
-    if (!L->unk[c]) L->f[c] = 0.0;
-  orc_bc_adapt(H);
-  return 0;
+  return orc_set_rhs_from_spheres_sub(H, n, centers, radii, charges,
+                                      normalization, 1);
 }
 
 /* sum_q a_q phi_q in the fixed direction order x-, x+, y-, y+, z-, z+ */

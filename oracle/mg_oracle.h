@@ -35,6 +35,8 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
                      const double *bc_value, const uint8_t *solid,
                      int min_coarse, int max_levels);
 void orc_destroy(orc_hier *H);
+/* per-cell values of face q (type unchanged); 0 or -1 */
+int orc_set_face_values(orc_hier *H, int face, const double *values);
 /* per-face-cell boundary patch; returns 0 or -1 (bad arguments) */
 int orc_set_bc_patch(orc_hier *H, int face, int a0, int a1, int b0, int b1,
                      int type, double value);
@@ -64,6 +66,16 @@ void orc_sphere_density(int nx, int ny, int nz, double h, int n,
                         const double *centers, const double *radii,
                         const double *charges, int normalization, double *out);
 void orc_bc_adapt(orc_hier *H);
+/* subsampling factor s: s^3 sub-cell centres per cell */
+long orc_sphere_subcount(int nx, int ny, int nz, double h, int s, double cx,
+                         double cy, double cz, double R);
+void orc_sphere_density_sub(int nx, int ny, int nz, double h, int s, int n,
+                            const double *centers, const double *radii,
+                            const double *charges, int normalization,
+                            double *out);
+int orc_set_rhs_from_spheres_sub(orc_hier *H, int n, const double *centers,
+                                 const double *radii, const double *charges,
+                                 int normalization, int s);
 
 /* single steps of the method on level l */
 void orc_smooth_half(orc_hier *H, int l, int color);

@@ -186,7 +186,8 @@ struct mg_ctx {
   bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   std::vector<uint8_t> solid_h;   // global solid mask (empty: none)
-  bool patched = false;           // per-face-cell BCs set (mg_set_bc_patch)
+  bool patched = false;           // per-face-cell BC arrays in use
+  bool types_uniform = true;      // every face cell has its face's BC type
   std::vector<uint8_t> fty_h[6];  // face-cell BC types
   std::vector<double> fva_h[6];   // face-cell BC values
   mg::FaceBC fbc{};               // device copies (patched only)
@@ -929,7 +930,8 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
                             int normalization, int subsample) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (n < 0) return fail(MG_ERR_ARG, "n < 0");
-  if (subsample != 1) return fail(MG_ERR_ARG, "subsample must be 1");
+  if (subsample < 1 || subsample > 16)
+    return fail(MG_ERR_ARG, "subsample must be in 1..16");
   if (normalization != MG_CHARGE_PER_CELLS && normalization != MG_CHARGE_PER_VOLUME)
     return fail(MG_ERR_ARG, "bad normalization");
   if (n > 0 && (!centers || !radii || !charges)) return fail(MG_ERR_ARG, "null array");
@@ -956,7 +958,8 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     CK(cudaMemcpyAsync(c->sph, h5.data(), sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
     for (const Grid &g : c->g[0])
-      mg::launch_spheres(g, c->h, n, c->sph, normalization, cnt, c->stream);
+      mg::launch_spheres(g, c->h, subsample, n, c->sph, normalization, cnt,
+                         c->stream);
     CK(cudaGetLastError());
   }
   int rc = bc_adapt(c);
@@ -1113,6 +1116,7 @@ int rebuild_coefficients(mg_ctx *c) {
   free_mask(c);
   c->fbc = mg::FaceBC{};
   if (c->solid_h.empty() && !c->patched) return MG_OK;
+  const bool need_var = !c->solid_h.empty() || !c->types_uniform;
   unsigned char *dmask = nullptr;
   if (!c->solid_h.empty()) {
     CK(cudaMalloc(&dmask, c->solid_h.size()));
@@ -1135,6 +1139,10 @@ int rebuild_coefficients(mg_ctx *c) {
       c->fbc.ty[q] = t;
       c->fbc.va[q] = v;
     }
+  if (!need_var) {  // only boundary values vary: box-domain operator, RHS only
+    c->prev_norm = -1.0;
+    return sync(c);
+  }
   // float records on every level
   for (int l = 0; l < c->pl.L; l++)
     for (Grid &g : c->g[l]) {
@@ -1228,6 +1236,18 @@ int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
   return rebuild_coefficients(c);
 }
 
+static void init_face_arrays(mg_ctx *c) {
+  if (c->patched) return;
+  const int ext[3] = {c->pl.dims[0][0], c->pl.dims[0][1], c->pl.dims[0][2]};
+  for (int q = 0; q < 6; q++) {
+    const int aq = q / 2;
+    const size_t n = (size_t)ext[aq == 0 ? 1 : 0] * ext[aq == 2 ? 1 : 2];
+    c->fty_h[q].assign(n, (uint8_t)c->bc[q].type);
+    c->fva_h[q].assign(n, c->bc[q].value);
+  }
+  c->patched = true;
+}
+
 int mg_set_bc_patch(mg_ctx *c, int face, int a0, int a1, int b0, int b1,
                     int type, double value) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
@@ -1240,20 +1260,24 @@ int mg_set_bc_patch(mg_ctx *c, int face, int a0, int a1, int b0, int b1,
   if (a0 < 0 || b0 < 0 || a1 > na || b1 > nb || a0 > a1 || b0 > b1)
     return fail(MG_ERR_ARG, "patch [%d,%d)x[%d,%d) outside face %d (%dx%d)", a0,
                 a1, b0, b1, face, na, nb);
-  if (!c->patched) {
-    for (int q = 0; q < 6; q++) {
-      const int aq = q / 2;
-      const size_t n = (size_t)ext[aq == 0 ? 1 : 0] * ext[aq == 2 ? 1 : 2];
-      c->fty_h[q].assign(n, (uint8_t)c->bc[q].type);
-      c->fva_h[q].assign(n, c->bc[q].value);
-    }
-    c->patched = true;
-  }
+  init_face_arrays(c);
   for (int x = a0; x < a1; x++)
     for (int y = b0; y < b1; y++) {
       c->fty_h[face][(size_t)x * nb + y] = (uint8_t)type;
       c->fva_h[face][(size_t)x * nb + y] = value;
     }
+  c->types_uniform = true;
+  for (int q = 0; q < 6; q++)
+    for (uint8_t t : c->fty_h[q])
+      if (t != (uint8_t)c->bc[q].type) c->types_uniform = false;
+  return rebuild_coefficients(c);
+}
+
+int mg_set_face_values(mg_ctx *c, int face, const double *values) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (face < 0 || face > 5 || !values) return fail(MG_ERR_ARG, "bad arguments");
+  init_face_arrays(c);
+  memcpy(c->fva_h[face].data(), values, c->fva_h[face].size() * sizeof(double));
   return rebuild_coefficients(c);
 }
 

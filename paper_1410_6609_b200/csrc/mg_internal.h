@@ -53,9 +53,9 @@ void launch_sum_ordered(const double *parts, int n, double *out,
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s);
 size_t coarse_cg_scratch_doubles(const Grid &g);
-void launch_spheres(const Grid &g, double h, int n, const double *sph,
-                    int normalization, unsigned long long *counts,
-                    cudaStream_t s);
+void launch_spheres(const Grid &g, double h, int subsample, int n,
+                    const double *sph, int normalization,
+                    unsigned long long *counts, cudaStream_t s);
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);
 // plane-marching TMA half-sweep (mg_march.cu)

@@ -496,13 +496,28 @@ __device__ __forceinline__ void bbox(int n, double h, double c, double R,
   *hi = b > n - 1 ? n - 1 : b;
 }
 
+// subsampling: covered sub-cell centres of cell (i,j,k), the s^3
+// centres ((i s + a + 1/2) h/s, ...) with the same inclusive test (s = 1: the
+// plain centre rule, hs = h exactly)
+__device__ __forceinline__ int sub_count(int i, int j, int k, int s, double hs,
+                                         double cx, double cy, double cz,
+                                         double R) {
+  int cnt = 0;
+  for (int a = 0; a < s; a++)
+    for (int b = 0; b < s; b++)
+      for (int c = 0; c < s; c++)
+        cnt += inside(i * s + a, j * s + b, k * s + c, hs, cx, cy, cz, R) ? 1 : 0;
+  return cnt;
+}
+
 __global__ void __launch_bounds__(kThreads)
-    k_spheres(Grid g, double h, const double *sph, int normalization,
+    k_spheres(Grid g, double h, int s, const double *sph, int normalization,
               unsigned long long *counts) {
   __shared__ double sh[32];
   const int p = blockIdx.x;
   const double cx = sph[5 * p], cy = sph[5 * p + 1], cz = sph[5 * p + 2];
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
+  const double hs = h / (double)s;
   int i0, i1, j0, j1, k0, k1;
   bbox(g.nx, h, cx, R, &i0, &i1);
   bbox(g.ny, h, cy, R, &j0, &j1);
@@ -515,17 +530,12 @@ __global__ void __launch_bounds__(kThreads)
     const long long q = t / nk;
     const int j = j0 + (int)(q % nj);
     const int i = i0 + (int)(q / nj);
-    if (inside(i, j, k, h, cx, cy, cz, R)) cnt += 1.0;
+    cnt += (double)sub_count(i, j, k, s, hs, cx, cy, cz, R);
   }
   const double np = block_sum(cnt, sh);
   if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
-  double rho;
-  if (normalization == 1)
-    rho = Q / ((4.0 / 3.0) * kPi * (R * R * R));
-  else {
-    if (np == 0.0) return;
-    rho = Q / (np * (h * h * h));
-  }
+  if (normalization != 1 && np == 0.0) return;
+  const double rho0 = Q / ((4.0 / 3.0) * kPi * (R * R * R));
   const int xa = i0 > g.x0 ? i0 : g.x0;
   const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
   if (xa > xb) return;
@@ -535,18 +545,23 @@ __global__ void __launch_bounds__(kThreads)
     const long long q = t / nk;
     const int j = j0 + (int)(q % nj);
     const int i = xa + (int)(q / nj);
-    if (!inside(i, j, k, h, cx, cy, cz, R)) continue;
+    const int c = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+    if (!c) continue;
+    // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3)
+    const double v = (normalization == 1)
+                         ? rho0 * ((double)c / (double)(s * s * s))
+                         : (Q * (double)c) / (np * (h * h * h));
     const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
     double *f = ((i + j + k) & 1) ? g.fB : g.fR;
-    atomicAdd(f + idx, rho);
+    atomicAdd(f + idx, v);
   }
 }
 
-void launch_spheres(const Grid &g, double h, int n, const double *sph,
+void launch_spheres(const Grid &g, double h, int s, int n, const double *sph,
                     int normalization, unsigned long long *counts,
-                    cudaStream_t s) {
+                    cudaStream_t st) {
   if (n <= 0) return;
-  k_spheres<<<n, kThreads, 0, s>>>(g, h, sph, normalization, counts);
+  k_spheres<<<n, kThreads, 0, st>>>(g, h, s, sph, normalization, counts);
 }
 
 // ---------------------------------------------------------------------------

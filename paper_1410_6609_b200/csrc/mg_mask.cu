@@ -235,9 +235,11 @@ __global__ void __launch_bounds__(kT)
   for (int z = 0; z < g.nz; z += step) {
     const int col = (i + j + z) & 1;
     const long long e = b + (z >> 1);
-    Coef C;
-    coef_at(g, col, e, i, j, z, C);
-    if (C.D == 0.0) continue;
+    if (g.codeR || g.coefR) {  // masked cells are not unknowns
+      Coef C;
+      coef_at(g, col, e, i, j, z, C);
+      if (C.D == 0.0) continue;
+    }
     double *f = col ? g.fB : g.fR;
     double v = f[e];
     const bool on[6] = {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, z == 0,

@@ -120,6 +120,7 @@ def lib():
         L.mg_coarse_solve.argtypes = [P, ip]
         L.mg_set_mask.argtypes = [P, dp, i]
         L.mg_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
+        L.mg_set_face_values.argtypes = [P, i, dp]
         L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
@@ -329,6 +330,12 @@ class Multigrid:
         _check(lib().mg_set_bc_patch(self._ctx, int(face), int(a0), int(a1),
                                      int(b0), int(b1), int(bc_type),
                                      float(value)), self._ctx)
+
+    def set_face_values(self, face, values):
+        """Per-cell boundary values of face `face` (in-face (a, b) order)."""
+        v = np.ascontiguousarray(values, np.float64)
+        _check(lib().mg_set_face_values(self._ctx, int(face), v.ctypes.data),
+               self._ctx)
 
     def get_stencil(self, level=0):
         out = np.empty(self.local_shape(level) + (7,), np.float64)

@@ -152,11 +152,15 @@ def test_set_rhs_bc_adaptation_bitwise(mg, bc, h):
 
 
 @pytest.mark.parametrize("norm", [0, 1])
-def test_sphere_rhs_bitwise(mg, norm):
+@pytest.mark.parametrize("sub", [1, 2, 3])
+def test_sphere_rhs_bitwise(mg, norm, sub):
+    """Sphere RHS incl. subsampling s_f bitwise vs the oracle."""
     w = W.cfg2(seed=1)
     s, o = pair(mg, w.shape, w.h, "channel", min_coarse=4)
-    s.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm)
-    o.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm,
+                           subsample=sub)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges, normalization=norm,
+                           subsample=sub)
     assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
 
 
@@ -516,3 +520,79 @@ def test_bc_patch_parity(mg):
     assert rel(s.get_solution(), o.phi()) <= 1e-10
     with pytest.raises(mg.MGError):
         s.set_bc_patch(2, 0, nx + 1, 0, 1, D, 0.0)
+
+
+
+def face_centres(shape, h, face):
+    """Physical points of the boundary faces of the face cells, (a, b) order."""
+    nx, ny, nz = shape
+    ax = face // 2
+    ext = [nx, ny, nz]
+    others = [d for d in range(3) if d != ax]
+    a = (np.arange(ext[others[0]]) + 0.5) * h
+    b = (np.arange(ext[others[1]]) + 0.5) * h
+    A, B = np.meshgrid(a, b, indexing="ij")
+    X = [None, None, None]
+    X[others[0]], X[others[1]] = A, B
+    X[ax] = np.full(A.shape, 0.0 if face % 2 == 0 else ext[ax] * h)
+    return X
+
+
+def test_face_values_parity(mg):
+    """Per-cell boundary values (mg_set_face_values) on mixed faces: RHS
+    adaptation bitwise, solve parity with the oracle."""
+    shape = (32, 16, 24)
+    bt, bv = BCS["mixed"]
+    s, o = pair(mg, shape, 0.5, "mixed", min_coarse=2)
+    rng = np.random.default_rng(21)
+    for q in range(6):
+        X = face_centres(shape, 0.5, q)
+        vals = np.sin(X[0]) * np.cos(X[1]) + X[2] + rng.uniform(-0.1, 0.1, X[0].shape)
+        s.set_face_values(q, vals)
+        o.set_face_values(q, vals)
+    f = rng.uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    rc, cg, hg = s.solve(1e-10, 60)
+    so, co, ho = o.solve(1e-10, 60)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+
+
+def sphere_potential(X, c, R, Q):
+    """Eq.18 (PAPER.md:1048-1057) with eps = 1."""
+    r = np.sqrt((X[0] - c[0]) ** 2 + (X[1] - c[1]) ** 2 + (X[2] - c[2]) ** 2)
+    out = np.where(r >= R, Q / (4 * np.pi * np.maximum(r, 1e-300)),
+                   Q / (4 * np.pi) / (2 * R) * (3 - (r / R) ** 2))
+    return out
+
+
+def test_charged_sphere_potential_table4(mg):
+    """Charged-sphere validation (Table 4): analytic
+    Dirichlet data (Eq.18) on every boundary face cell, the paper's naive
+    volume mapping with subsampling; the relative potential error is "well
+    below 2 % in the L2 norm for all sphere sizes" and shrinks with s_f
+    (PAPER.md:1124-1127).  128^3, R = 6 at an off-centre position."""
+    n, h, R, Q = 128, 1.0, 6.0, 1.0
+    shape = (n, n, n)
+    c = np.array([64.23, 63.81, 64.37])
+    x = (np.arange(n) + 0.5) * h
+    Xc = np.meshgrid(x, x, x, indexing="ij")
+    exact = sphere_potential(Xc, c, R, Q)
+    errs = {}
+    for sf in (1, 3):
+        s = mg.Multigrid(shape, h, [D] * 6, [0.0] * 6, min_coarse=8)
+        for q in range(6):
+            s.set_face_values(q, sphere_potential(face_centres(shape, h, q), c, R, Q))
+        s.set_rhs_from_spheres(c[None, :], [R], [Q],
+                               normalization=mg.MG_CHARGE_PER_VOLUME, subsample=sf)
+        rc, cyc, hist = s.solve(1e-10, 40)
+        assert rc == 0
+        e = (s.get_solution() - exact) / exact
+        errs[sf] = (float(np.sqrt(np.mean(e ** 2))), float(np.abs(e).max()))
+        s.close()
+    assert errs[1][0] < 0.02 and errs[3][0] < 0.02
+    assert errs[3][0] < errs[1][0]
+    assert errs[1][1] < 0.11 and errs[3][1] < errs[1][1]
