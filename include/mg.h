@@ -195,6 +195,20 @@ int mg_set_rhs_from_spheres(mg_ctx *ctx, int n, const double *centers,
  * face the cell touches, in face order. */
 int mg_set_rhs(mg_ctx *ctx, const double *f, int where);
 
+/* ---- Coulomb force ------------------------------------------ */
+/* Electrostatic force on each of n spheres from the current Phi (Eq.14,
+ * P:466-471): F_p = -h^3 sum_b grad Phi(x_b) rho_p(x_b) over the cells of
+ * sphere p, rho_p its own charge density with the mapping of
+ * mg_set_rhs_from_spheres (normalization, subsample = the force subsampling
+ * factor s_F of Table 5), grad Phi the isotropic D3Q19 gradient (Eq.15,
+ * P:472-478; central / one-sided differences where a D3Q19 neighbour is
+ * outside the domain or solid, reading d6).  Host arrays; forces_out[3n].
+ * Collective for NCCL contexts (partial sums all-gathered, summed in rank
+ * order).  Errors as mg_set_rhs_from_spheres. */
+int mg_coulomb_forces(mg_ctx *ctx, int n, const double *centers,
+                      const double *radii, const double *charges,
+                      int normalization, int subsample, double *forces_out);
+
 /* ---- solve --------------------------------------------------------------- */
 /* One V(nu1,nu2)-cycle; *res_norm_out (may be NULL) = ||f - A Phi||_2 over
  * all cells after the cycle (unscaled, reading c10).  Synchronises.

@@ -83,6 +83,8 @@ def lib():
         L.orc_last_cg_iters.argtypes = [P]
         L.orc_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.orc_set_face_values.argtypes = [P, i, dp]
+        L.orc_gradient.argtypes = [P, dp, i, i, i, dp]
+        L.orc_coulomb_forces.argtypes = [P, i, dp, dp, dp, i, i, dp]
         L.orc_sphere_subcount.restype = ctypes.c_long
         L.orc_sphere_subcount.argtypes = [i, i, i, d, i, d, d, d, d]
         L.orc_sphere_density_sub.argtypes = [i, i, i, d, i, i, dp, dp, dp, i, dp]
@@ -181,6 +183,24 @@ class Oracle:
         v = _f64(values).reshape(-1)
         if lib().orc_set_face_values(self._h, int(face), _dp(v)) != 0:
             raise ValueError("oracle: bad face")
+
+    def gradient(self, phi, i, j, k):
+        """Isotropic D3Q19 gradient (Eq.15) of level-0 field phi at a cell."""
+        phi = _f64(phi)
+        g = np.empty(3)
+        lib().orc_gradient(self._h, _dp(phi), int(i), int(j), int(k), _dp(g))
+        return g
+
+    def coulomb_forces(self, centers, radii, charges, normalization=PER_CELLS,
+                       subsample=1):
+        """Eq.14 forces (n, 3) of the spheres on the current Phi."""
+        c = _f64(centers).reshape(-1)
+        r = _f64(radii)
+        q = _f64(charges)
+        out = np.empty(3 * len(r))
+        lib().orc_coulomb_forces(self._h, len(r), _dp(c), _dp(r), _dp(q),
+                                 int(normalization), int(subsample), _dp(out))
+        return out.reshape(-1, 3)
 
     # -- fields ------------------------------------------------------------
     def phi(self, l=0) -> np.ndarray:

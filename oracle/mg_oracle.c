@@ -481,6 +481,106 @@ int orc_set_rhs_from_spheres(orc_hier *H, int n, const double *centers,
                                       normalization, 1);
 }
 
+/* ---- Coulomb force (Eq.14) with the isotropic D3Q19 gradient
+ * (Eq.15), §8(f) N2 -------------------------------------------
+ * grad Phi(x_b) = (1/w_1) sum_{q=2..19} w_q Phi(x_b + e_q) e_q / dx^2 with the
+ * D3Q19 weights w_1 = 1/3, faces 1/18, edges 1/36.  Per component:
+ * S = sum_q w_q c_q Phi_q in the fixed order of ORC_Q19 (terms with c_q = 0
+ * skipped), g = (3 S) / h.  Reading d6 (the paper only says "where
+ * possible"): the D3Q19 stencil is used where all 18 neighbours are fluid
+ * cells of the domain; otherwise, per axis, the central difference
+ * (Phi_+ - Phi_-) / (2h) if both axis neighbours are, else the one-sided
+ * first-order difference toward the valid one, else 0. */
+static const int ORC_Q19[18][3] = {
+    {1, 0, 0},  {-1, 0, 0}, {0, 1, 0},   {0, -1, 0}, {0, 0, 1},  {0, 0, -1},
+    {1, 1, 0},  {-1, -1, 0}, {1, -1, 0}, {-1, 1, 0}, {1, 0, 1},  {-1, 0, -1},
+    {1, 0, -1}, {-1, 0, 1}, {0, 1, 1},   {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
+
+static inline int valid_cell(const level_t *L, int i, int j, int k) {
+  return i >= 0 && j >= 0 && k >= 0 && i < L->nx && j < L->ny && k < L->nz &&
+         L->unk[IDX(L, i, j, k)];
+}
+
+void orc_gradient(const orc_hier *H, const double *phi, int i, int j, int k,
+                  double *g) {
+  const level_t *L = &H->L[0];
+  const double h = H->h;
+  int all = 1;
+  for (int q = 0; q < 18; q++)
+    if (!valid_cell(L, i + ORC_Q19[q][0], j + ORC_Q19[q][1], k + ORC_Q19[q][2]))
+      all = 0;
+  if (all) {
+    for (int a = 0; a < 3; a++) {
+      double S = 0.0;
+      for (int q = 0; q < 18; q++) {
+        const int c = ORC_Q19[q][a];
+        if (c == 0) continue;
+        const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
+        const double v = phi[IDX(L, i + ORC_Q19[q][0], j + ORC_Q19[q][1],
+                                 k + ORC_Q19[q][2])];
+        S = c > 0 ? S + w * v : S - w * v;
+      }
+      g[a] = (3.0 * S) / h;
+    }
+    return;
+  }
+  for (int a = 0; a < 3; a++) {
+    int dp[3] = {0, 0, 0}, dm[3] = {0, 0, 0};
+    dp[a] = 1;
+    dm[a] = -1;
+    const int vp = valid_cell(L, i + dp[0], j + dp[1], k + dp[2]);
+    const int vm = valid_cell(L, i + dm[0], j + dm[1], k + dm[2]);
+    const double c0 = phi[IDX(L, i, j, k)];
+    if (vp && vm)
+      g[a] = (phi[IDX(L, i + dp[0], j + dp[1], k + dp[2])] -
+              phi[IDX(L, i + dm[0], j + dm[1], k + dm[2])]) / (2.0 * h);
+    else if (vp)
+      g[a] = (phi[IDX(L, i + dp[0], j + dp[1], k + dp[2])] - c0) / h;
+    else if (vm)
+      g[a] = (c0 - phi[IDX(L, i + dm[0], j + dm[1], k + dm[2])]) / h;
+    else
+      g[a] = 0.0;
+  }
+}
+
+/* F_p = -dx^3 sum_b grad Phi(x_b) rho_p(x_b) over the cells of sphere p, rho_p
+ * its own (subsampled, s) charge density (the mapping of
+ * orc_sphere_density_sub); the sum runs over the bounding box in (i,j,k)
+ * order.  forces[3p..3p+2]. */
+int orc_coulomb_forces(const orc_hier *H, int n, const double *centers,
+                       const double *radii, const double *charges,
+                       int normalization, int s, double *forces) {
+  const level_t *L = &H->L[0];
+  const double h = H->h, hs = h / (double)s;
+  for (int p = 0; p < n; p++) {
+    const double cx = centers[3 * p], cy = centers[3 * p + 1],
+                 cz = centers[3 * p + 2], R = radii[p], Q = charges[p];
+    const long np = orc_sphere_subcount(L->nx, L->ny, L->nz, h, s, cx, cy, cz, R);
+    double F[3] = {0.0, 0.0, 0.0};
+    if (np > 0 || normalization == ORC_PER_VOLUME) {
+      const double rho0 = Q / ((4.0 / 3.0) * ORC_PI * (R * R * R));
+      int i0, i1, j0, j1, k0, k1;
+      bbox(L->nx, h, cx, R, &i0, &i1);
+      bbox(L->ny, h, cy, R, &j0, &j1);
+      bbox(L->nz, h, cz, R, &k0, &k1);
+      for (int i = i0; i <= i1; i++)
+        for (int j = j0; j <= j1; j++)
+          for (int k = k0; k <= k1; k++) {
+            const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+            if (!cnt || !L->unk[IDX(L, i, j, k)]) continue;
+            const double rho = normalization == ORC_PER_VOLUME
+                                   ? rho0 * ((double)cnt / (double)(s * s * s))
+                                   : (Q * (double)cnt) / ((double)np * (h * h * h));
+            double g[3];
+            orc_gradient(H, L->phi, i, j, k, g);
+            for (int a = 0; a < 3; a++) F[a] = F[a] + g[a] * rho;
+          }
+    }
+    for (int a = 0; a < 3; a++) forces[3 * p + a] = -(h * h * h) * F[a];
+  }
+  return 0;
+}
+
 /* sum_q a_q phi_q in the fixed direction order x-, x+, y-, y+, z-, z+ */
 static inline double offdiag(const level_t *L, const double *a,
                              const double *v, int i, int j, int k) {

@@ -85,6 +85,14 @@ void orc_prolong_correct(orc_hier *H, int l, double alpha);   /* P:516, P:521 */
 int orc_cg(orc_hier *H, int l, double tol, int maxit);        /* P:746 */
 void orc_apply(const orc_hier *H, int l, const double *x, double *y); /* y = A x */
 
+/* Coulomb force (Eq.14) with the isotropic D3Q19 gradient (Eq.15) of the
+ * current level-0 Phi; gradient g[3] at cell (i,j,k) */
+void orc_gradient(const orc_hier *H, const double *phi, int i, int j, int k,
+                  double *g);
+int orc_coulomb_forces(const orc_hier *H, int n, const double *centers,
+                       const double *radii, const double *charges,
+                       int normalization, int s, double *forces);
+
 /* whole cycles */
 void orc_set_schedule(orc_hier *H, int nu1, int nu2, double alpha,
                       double coarse_tol, int coarse_maxit);

@@ -191,6 +191,7 @@ struct mg_ctx {
   std::vector<uint8_t> fty_h[6];  // face-cell BC types
   std::vector<double> fva_h[6];   // face-cell BC values
   mg::FaceBC fbc{};               // device copies (patched only)
+  unsigned char *dsolid = nullptr;  // device copy of the global solid mask
   double h;
   mg_bc bc[6];
   mg_opts o;
@@ -1115,6 +1116,7 @@ int rebuild_coefficients(mg_ctx *c) {
   }
   free_mask(c);
   c->fbc = mg::FaceBC{};
+  c->dsolid = nullptr;
   if (c->solid_h.empty() && !c->patched) return MG_OK;
   const bool need_var = !c->solid_h.empty() || !c->types_uniform;
   unsigned char *dmask = nullptr;
@@ -1123,6 +1125,7 @@ int rebuild_coefficients(mg_ctx *c) {
     c->mask_bufs.push_back(dmask);
     CK(cudaMemcpyAsync(dmask, c->solid_h.data(), c->solid_h.size(),
                        cudaMemcpyHostToDevice, c->stream));
+    c->dsolid = dmask;
   }
   if (c->patched)
     for (int q = 0; q < 6; q++) {
@@ -1279,6 +1282,69 @@ int mg_set_face_values(mg_ctx *c, int face, const double *values) {
   init_face_arrays(c);
   memcpy(c->fva_h[face].data(), values, c->fva_h[face].size() * sizeof(double));
   return rebuild_coefficients(c);
+}
+
+int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
+                      const double *radii, const double *charges,
+                      int normalization, int subsample, double *forces_out) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (n < 0 || (n > 0 && (!centers || !radii || !charges || !forces_out)))
+    return fail(MG_ERR_ARG, "bad arrays");
+  if (subsample < 1 || subsample > 16)
+    return fail(MG_ERR_ARG, "subsample must be in 1..16");
+  if (normalization != MG_CHARGE_PER_CELLS && normalization != MG_CHARGE_PER_VOLUME)
+    return fail(MG_ERR_ARG, "bad normalization");
+  if (n == 0) return MG_OK;
+  std::vector<double> h5(5 * (size_t)n);
+  for (int p = 0; p < n; p++) {
+    if (!(radii[p] > 0.0)) return fail(MG_ERR_ARG, "sphere %d: radius <= 0", p);
+    for (int q = 0; q < 3; q++) h5[5 * (size_t)p + q] = centers[3 * (size_t)p + q];
+    h5[5 * (size_t)p + 3] = radii[p];
+    h5[5 * (size_t)p + 4] = charges[p];
+  }
+  int rc;
+  // both colours' ghost planes current (the gradient reads across slabs)
+  if ((rc = halo(c, 0, 0)) || (rc = halo(c, 0, 1))) return rc;
+  const size_t ns = c->g[0].size();
+  const size_t nrow = 3 * (size_t)n;
+  // device: sphere list + per-slab partials (+ all-gathered partials)
+  double *buf = nullptr;
+  const size_t nb = 5 * (size_t)n + nrow * (ns + (size_t)c->P);
+  CK(cudaMalloc(&buf, nb * sizeof(double)));
+  double *dsph = buf, *dpart = buf + 5 * (size_t)n, *dall = dpart + nrow * ns;
+  std::vector<double> hp;
+  if (cudaMemcpyAsync(dsph, h5.data(), 5 * (size_t)n * sizeof(double),
+                      cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
+    cudaFree(buf);
+    return fail(MG_ERR_CUDA, "copy of the sphere list failed");
+  }
+  for (size_t s = 0; s < ns; s++)
+    mg::launch_coulomb(c->g[0][s], c->dsolid, c->h, subsample, n, dsph,
+                       normalization, dpart + nrow * s, c->stream);
+  size_t nparts = ns;
+  double *src = dpart;
+  if (c->P > 1 && c->backend == MG_HALO_NCCL) {
+    rc = nccl_ck(g_nccl.AllGather(dpart, dall, nrow, ncclDouble, c->comm, c->stream),
+                 "ncclAllGather(forces)");
+    nparts = (size_t)c->P;
+    src = dall;
+  }
+  if (!rc) {
+    hp.resize(nrow * nparts);
+    if (cudaMemcpyAsync(hp.data(), src, hp.size() * sizeof(double),
+                        cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+        cudaStreamSynchronize(c->stream) != cudaSuccess)
+      rc = fail(MG_ERR_CUDA, "force readback failed");
+  }
+  cudaFree(buf);
+  if (rc) return rc;
+  const double h3 = c->h * c->h * c->h;
+  for (size_t r = 0; r < nrow; r++) {
+    double s = 0.0;
+    for (size_t k = 0; k < nparts; k++) s = s + hp[k * nrow + r];  // slab order
+    forces_out[r] = -h3 * s;
+  }
+  return MG_OK;
 }
 
 int mg_get_stencil(mg_ctx *c, int l, double *out, int where) {

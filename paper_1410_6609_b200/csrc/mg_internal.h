@@ -96,6 +96,10 @@ void launch_level0_coef(const Grid &g, const unsigned char *solid_global,
                         cudaStream_t s);
 void launch_bc_adapt_faces(const Grid &g, const FaceBC &fb, double alpha,
                            double h, cudaStream_t s);
+// Coulomb force partial sums (mg_force.cu): part[3p+a] = sum_b g_a rho_p
+void launch_coulomb(const Grid &g, const unsigned char *solid_global, double h,
+                    int subsample, int n, const double *sph, int normalization,
+                    double *partials, cudaStream_t s);
 // masked (variable-coefficient) path, mg_mask.cu
 void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
                        unsigned char *codeR, unsigned char *codeB,

@@ -121,6 +121,7 @@ def lib():
         L.mg_set_mask.argtypes = [P, dp, i]
         L.mg_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.mg_set_face_values.argtypes = [P, i, dp]
+        L.mg_coulomb_forces.argtypes = [P, i, dp, dp, dp, i, i, dp]
         L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
@@ -290,6 +291,18 @@ class Multigrid:
                                              _host_ptr(r), _host_ptr(q),
                                              normalization, subsample),
                self._ctx)
+
+    def coulomb_forces(self, centers, radii, charges,
+                       normalization=MG_CHARGE_PER_CELLS, subsample=1):
+        """Eq.14 forces (n, 3) on the spheres from the current solution."""
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        r = np.ascontiguousarray(radii, np.float64)
+        q = np.ascontiguousarray(charges, np.float64)
+        out = np.empty(3 * len(r), np.float64)
+        _check(lib().mg_coulomb_forces(self._ctx, len(r), _host_ptr(c),
+                                       _host_ptr(r), _host_ptr(q), normalization,
+                                       subsample, _host_ptr(out)), self._ctx)
+        return out.reshape(-1, 3)
 
     def get_solution(self, out=None):
         if out is None:

@@ -596,3 +596,151 @@ def test_charged_sphere_potential_table4(mg):
     assert errs[1][0] < 0.02 and errs[3][0] < 0.02
     assert errs[3][0] < errs[1][0]
     assert errs[1][1] < 0.11 and errs[3][1] < errs[1][1]
+
+
+# --------------------------------------------------------------------------
+# Coulomb force (Eq.14) with the D3Q19 gradient (Eq.15)
+# --------------------------------------------------------------------------
+def force_spheres(shape, h):
+    """Spheres inside, touching each wall / corner, straddling slab planes,
+    partly outside the domain, and one smaller than a cell."""
+    L = np.array(shape) * h
+    c = [L * [0.31, 0.52, 0.47], L * [0.5, 0.5, 0.5], [0.9 * h, 0.6 * h, 0.5 * L[2]],
+         [L[0] - 0.7 * h, L[1] - 1.1 * h, L[2] - 0.4 * h], L * [0.25, 0.9, 0.1],
+         [0.5 * L[0] + 0.1 * h, -0.8 * h, 0.6 * L[2]], L * [0.75, 0.3, 0.66]]
+    r = [3.3 * h, 4.0 * h, 2.2 * h, 1.9 * h, 2.6 * h, 2.0 * h, 0.3 * h]
+    q = [1.0, -2.5, 0.7, 1.3, -0.4, 2.0, 0.9]
+    return np.array(c), np.array(r), np.array(q)
+
+
+@pytest.mark.parametrize("norm", [0, 1])
+@pytest.mark.parametrize("sub", [1, 2, 3])
+def test_coulomb_forces_parity(mg, norm, sub):
+    """GPU forces == oracle forces on the same Phi (sums differ only in
+    order: relative 1e-12)."""
+    shape, h = (48, 40, 36), 0.5
+    s, o = pair(mg, shape, h, "mixed", min_coarse=2)
+    rng = np.random.default_rng(31 + sub)
+    x = [(np.arange(n) + 0.5) * h for n in shape]
+    X = np.meshgrid(*x, indexing="ij")
+    phi = np.sin(0.3 * X[0]) * np.cos(0.2 * X[1]) + 0.1 * X[2] \
+        + 0.05 * rng.uniform(-1, 1, shape)
+    s.set_solution(phi)
+    o.set_phi(phi)
+    c, r, q = force_spheres(shape, h)
+    Fg = s.coulomb_forces(c, r, q, normalization=norm, subsample=sub)
+    Fo = o.coulomb_forces(c, r, q, normalization=norm, subsample=sub)
+    assert Fg.shape == (len(r), 3)
+    assert np.abs(Fo).max() > 0
+    assert np.allclose(Fg, Fo, rtol=1e-12, atol=1e-12 * np.abs(Fo).max())
+
+
+def test_coulomb_forces_after_solve_and_masked(mg):
+    """Forces on a solved config-5 (masked) potential: solid cells carry no
+    force and are not gradient neighbours (reading d6)."""
+    w = W.cfg5(scale=16, n_spheres=40)
+    s, o = mask_pair(mg, w.shape, w.solid, min_coarse=w.min_coarse, nu1=3, nu2=3)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    s.solve(w.tol, 60)
+    o.solve(w.tol, 60)
+    # sample positions touching the beam as well as the given spheres
+    c = np.concatenate([w.centers, [[w.shape[0] * 0.5, w.shape[1] * 0.5,
+                                     w.shape[2] * 0.5]]])
+    r = np.concatenate([w.radii, [5.0]])
+    q = np.concatenate([w.charges, [1.0]])
+    Fg = s.coulomb_forces(c, r, q)
+    o_phi = o.phi()
+    o.set_phi(s.get_solution())       # same Phi: isolate the force step
+    Fo = o.coulomb_forces(c, r, q)
+    assert np.allclose(Fg, Fo, rtol=1e-12, atol=1e-12 * np.abs(Fo).max())
+    o.set_phi(o_phi)
+    Fo2 = o.coulomb_forces(c, r, q)   # and the oracle's own solve
+    assert np.allclose(Fg, Fo2, rtol=1e-7, atol=1e-7 * np.abs(Fo2).max())
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_coulomb_forces_loopback_slabs(mg, P):
+    """x-slab split: spheres straddling slab planes read the ghost planes;
+    partial sums combined in slab order equal the single-slab result."""
+    shape, h = (48, 40, 36), 0.5
+    rng = np.random.default_rng(5)
+    phi = rng.uniform(-1, 1, shape)
+    c, r, q = force_spheres(shape, h)
+    c = np.concatenate([c, [[8.0, 10.0, 9.0], [16.0, 10.0, 9.0]]])  # x = 16, 32 cells
+    r = np.concatenate([r, [3.0, 2.5]])
+    q = np.concatenate([q, [1.0, -1.0]])
+    out = []
+    for p in (1, P):
+        kw = dict(min_coarse=2, agglomerate_below=64)
+        if p > 1:
+            kw.update(nranks=p, halo="loopback")
+        bt, bv = BCS["mixed"]
+        s = mg.Multigrid(shape, h, bt, bv, **kw)
+        s.set_solution(phi)
+        out.append(s.coulomb_forces(c, r, q, subsample=2))
+        s.close()
+    assert np.allclose(out[0], out[1], rtol=1e-13, atol=1e-13 * np.abs(out[0]).max())
+
+
+def test_coulomb_force_errors(mg):
+    s, _ = pair(mg, (8, 8, 8), 1.0, "dirichlet")
+    c, r, q = np.zeros((1, 3)) + 4.0, np.array([2.0]), np.array([1.0])
+    assert s.coulomb_forces(np.zeros((0, 3)), [], []).shape == (0, 3)
+    with pytest.raises(mg.MGError):
+        s.coulomb_forces(c, r, q, subsample=0)
+    with pytest.raises(mg.MGError):
+        s.coulomb_forces(c, [-1.0], q)
+    with pytest.raises(mg.MGError):
+        s.coulomb_forces(c, r, q, normalization=7)
+
+
+def worst_volume_position(shape, h, R, sub, n_try, seed):
+    """Near-centre position with the largest |e_rV| for subsampling `sub`
+    (the paper's placement)."""
+    rng = np.random.default_rng(seed)
+    best, pos = -1.0, None
+    V = 4.0 / 3.0 * np.pi * R ** 3
+    for _ in range(n_try):
+        cpos = (np.array(shape) // 2 + rng.uniform(0, 1, 3)) * h
+        n = oracle.sphere_cell_count(shape, h, cpos, R, sub)
+        e = n * (h / sub) ** 3 / V - 1.0
+        if abs(e) > best:
+            best, pos, ev = abs(e), cpos, e
+    return pos, ev
+
+
+def test_coulomb_force_homogeneous_field_table5(mg):
+    """Table 5 setup: charged sphere in a homogeneous
+    field (Phi_W = 0, Phi_E = -10, homogeneous Neumann elsewhere), naive
+    volume mapping.  The field part of the discrete solution is exactly
+    linear and the D3Q19 gradient is exact on it, so with s_Phi = s_F the
+    relative force error equals the volume-mapping error e_rV of the
+    position ("e_rFC is equal to e_rVmax for same subsampling factors",
+    PAPER.md:1142) up to the small image self-force; for unequal factors it
+    "changes only slightly" (|e| within the paper's 7.1 % table maximum)."""
+    n, h, Q = 128, 1.0, 1.0
+    shape = (n, n, n)
+    bt = [D, D, N, N, N, N]
+    bv = [0.0, -10.0, 0.0, 0.0, 0.0, 0.0]
+    F0 = Q * 10.0 / (n * h)
+    for R in (4.0, 6.0):
+        for sF in (1, 2, 3):
+            c, ev = worst_volume_position(shape, h, R, sF, 300, int(10 * R) + sF)
+            for sP in (1, 2, 3):
+                s = mg.Multigrid(shape, h, bt, bv, min_coarse=8)
+                s.set_rhs_from_spheres(c[None, :], [R], [Q],
+                                       normalization=mg.MG_CHARGE_PER_VOLUME,
+                                       subsample=sP)
+                rc, _, _ = s.solve(1e-12, 60)
+                assert rc == 0
+                F = s.coulomb_forces(c[None, :], [R], [Q],
+                                     normalization=mg.MG_CHARGE_PER_VOLUME,
+                                     subsample=sF)[0]
+                s.close()
+                e = (F[0] - F0) / F0
+                assert abs(F[1]) < 0.05 * F0 and abs(F[2]) < 0.05 * F0
+                if sP == sF:
+                    assert abs(e - ev) < 2e-3, (R, sF, e, ev)
+                else:
+                    assert abs(e) < 0.08, (R, sF, sP, e)

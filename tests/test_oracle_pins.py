@@ -598,3 +598,64 @@ def test_subsampled_density_conservation():
         tot = sum(q[p] * oracle.sphere_cell_count(shape, 1.0, c[p], 3.5, s)
                   / s ** 3 / V for p in range(10))
         assert abs(rv.sum() - tot) < 1e-12
+
+
+# --------------------------------------------------------------------------
+# Coulomb force + isotropic gradient (Eq.14-15) -- §8(f) N2
+# --------------------------------------------------------------------------
+def test_isotropic_gradient_exact_for_quadratics():
+    """Eq.15 with the D3Q19 weights: sum_q w_q c_q = 0, sum_q w_q c_q c_q^T
+    = I/3 and vanishing third moments make it exact for polynomials of degree
+    2 (SPEC.md:397-398 linear case; quadratic by the third moment)."""
+    shape, h = (10, 12, 14), 0.5
+    o = oracle.Oracle(shape, h, [D] * 6, [0.0] * 6)
+    X = np.meshgrid(*[(np.arange(n) + 0.5) * h for n in shape], indexing="ij")
+    a = np.array([1.0, -2.0, 3.0])
+    lin = a[0] * X[0] + a[1] * X[1] + a[2] * X[2] + 0.7
+    quad = X[0] ** 2 - 2 * X[1] * X[2] + X[2] ** 2
+    for (i, j, k) in [(4, 5, 6), (1, 1, 1), (8, 10, 12)]:
+        assert np.allclose(o.gradient(lin, i, j, k), a, rtol=0, atol=1e-12)
+        x, y, z = X[0][i, j, k], X[1][i, j, k], X[2][i, j, k]
+        assert np.allclose(o.gradient(quad, i, j, k), [2 * x, -2 * z, 2 * z - 2 * y],
+                           rtol=0, atol=1e-11)
+    assert np.allclose(o.gradient(np.full(shape, 3.0), 5, 5, 5), 0.0, atol=1e-14)
+
+
+def test_isotropic_gradient_second_order():
+    """Cubic field: the Eq.15 gradient converges with O(dx^2)."""
+    errs = []
+    for n in (16, 32, 64):
+        h = 1.0 / n
+        o = oracle.Oracle((n, n, n), h, [D] * 6, [0.0] * 6)
+        x = (np.arange(n) + 0.5) * h
+        X = np.meshgrid(x, x, x, indexing="ij")
+        f = np.sin(2 * X[0]) * np.cos(X[1]) + X[2] ** 3
+        i = j = k = n // 2
+        g = o.gradient(f, i, j, k)
+        ex = [2 * np.cos(2 * x[i]) * np.cos(x[j]), -np.sin(2 * x[i]) * np.sin(x[j]),
+              3 * x[k] ** 2]
+        errs.append(np.abs(g - ex).max())
+    assert 3.5 < errs[0] / errs[1] < 4.5 and 3.5 < errs[1] / errs[2] < 4.5
+
+
+def test_coulomb_force_in_prescribed_linear_potential():
+    """Eq.14 on Phi = a.x: F = -h^3 sum_b grad Phi rho_b = -Q a exactly for
+    the charge-exact mapping (any subsampling), and -Q (n_sub/s^3)/V a for the
+    paper's volume mapping: the force error equals the volume mapping error
+    (Table 5 diagonal)."""
+    shape, h = (40, 40, 40), 1.0
+    o = oracle.Oracle(shape, h, [D] * 6, [0.0] * 6)
+    X = np.meshgrid(*[(np.arange(n) + 0.5) * h for n in shape], indexing="ij")
+    a = np.array([0.3, -0.1, 0.05])
+    o.set_phi(a[0] * X[0] + a[1] * X[1] + a[2] * X[2])
+    c = np.array([[20.3, 19.7, 20.1], [10.2, 28.9, 15.5]])
+    R = np.array([6.0, 4.0])
+    q = np.array([2.0, -1.5])
+    for sf in (1, 2, 3):
+        F = o.coulomb_forces(c, R, q, subsample=sf)
+        assert np.allclose(F, -q[:, None] * a[None, :], rtol=1e-12, atol=1e-14)
+        Fv = o.coulomb_forces(c, R, q, oracle.PER_VOLUME, sf)
+        for p in range(2):
+            frac = oracle.sphere_cell_count(shape, h, c[p], R[p], sf) / sf ** 3 \
+                / (4 / 3 * math.pi * R[p] ** 3)
+            assert np.allclose(Fv[p], -q[p] * frac * a, rtol=1e-12, atol=1e-14)
