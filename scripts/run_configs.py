@@ -6,7 +6,7 @@ throughput, asymptotic residual-reduction factor; for the configs the CPU
 oracle finishes in reasonable time (1, 2, reduced 3/4/5) the GPU result is
 compared with the oracle (Phi rel-L2, residual history).
 
-usage: python scripts/run_configs.py [--out profiles/r01_configs.md] [--full]
+usage: python scripts/run_configs.py [--out gpurun_out/r01_configs.md] [--full]
 """
 import argparse
 import json
@@ -85,7 +85,7 @@ def factor(hist):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_configs.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "r01_configs.md"))
     ap.add_argument("--full", action="store_true",
                     help="also run configs 3/4/5 at full size on the GPU")
     a = ap.parse_args()

@@ -6,7 +6,7 @@ domain centre), analytic Dirichlet data (Eq.18, eps = 1) on every boundary
 face cell, the paper's naive mapping Q/V x (overlap fraction), subsampling
 s_f.  Reports e_rV at that position, ||e_rPhi||_L2 = sqrt(mean(e^2)) and
 ||e_rPhi||_inf (signed) next to the paper's Table 4.
-usage: python scripts/table4_validation.py [--out profiles/r01_table4.md]
+usage: python scripts/table4_validation.py [--out gpurun_out/r01_table4.md]
 """
 import argparse
 import math
@@ -31,7 +31,7 @@ PAPER = {  # R: s_f: (mean|erV|, erVmax, L2, inf)  -- Table 4
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_table4.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "r01_table4.md"))
     ap.add_argument("--n", type=int, default=256)
     ap.add_argument("--samples", type=int, default=3000)
     a = ap.parse_args()
