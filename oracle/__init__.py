@@ -23,6 +23,7 @@ SRC_PATH = os.path.join(_HERE, "mg_oracle.c")
 
 DIRICHLET = 0
 NEUMANN = 1
+PERIODIC = 2
 PER_CELLS = 0
 PER_VOLUME = 1
 
@@ -198,8 +199,10 @@ class Oracle:
         r = _f64(radii)
         q = _f64(charges)
         out = np.empty(3 * len(r))
-        lib().orc_coulomb_forces(self._h, len(r), _dp(c), _dp(r), _dp(q),
-                                 int(normalization), int(subsample), _dp(out))
+        if lib().orc_coulomb_forces(self._h, len(r), _dp(c), _dp(r), _dp(q),
+                                    int(normalization), int(subsample),
+                                    _dp(out)) != 0:
+            raise ValueError("oracle: bad sphere on a periodic axis")
         return out.reshape(-1, 3)
 
     # -- fields ------------------------------------------------------------
@@ -237,7 +240,8 @@ class Oracle:
                                                 _dp(q), int(normalization),
                                                 int(subsample))
         if rc != 0:
-            raise ValueError("oracle: a sphere covers no cell centre")
+            raise ValueError("oracle: a sphere covers no cell centre, or violates "
+                             "the periodic-axis rule")
 
     # -- steps -------------------------------------------------------------
     def smooth_half(self, l, color):

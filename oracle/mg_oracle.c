@@ -42,6 +42,7 @@ typedef struct {
   double *A;          /* 7 per cell: centre, x-, x+, y-, y+, z-, z+ */
   uint8_t *unk;       /* 1 = unknown cell, 0 = solid (masked) */
   double *phi, *f, *r;
+  int per[3];         /* periodic axes, same on every level */
 } level_t;
 
 struct orc_hier {
@@ -50,6 +51,7 @@ struct orc_hier {
   double h;
   int bct[6];
   double bcv[6];
+  int per[3]; /* periodic axes */
   /* per face-cell BC (patches, "specified in input files"):
    * face q has area A_q, cell (a,b) in the two remaining axes in (x,y,z)
    * order; NULL = the face-uniform bct/bcv */
@@ -82,10 +84,24 @@ static inline double face_value(const orc_hier *H, int q, int i, int j, int k) {
   return H->fva[q] ? H->fva[q][face_index(&H->L[0], q, i, j, k)] : H->bcv[q];
 }
 
+/* Periodic BCs "cyclically extend the domain ... by accessing unknowns in
+ * cells at opposite sides of the domain": an index one past a
+ * periodic face wraps to the opposite side. */
+static inline int wrap(int i, int n, int per) {
+  if (!per) return i;
+  if (i < 0) return i + n;
+  if (i >= n) return i - n;
+  return i;
+}
+
 /* value of a field at (i,j,k), 0 outside the level (the folded boundary
- * coefficient is 0 there, so the value never matters) */
+ * coefficient is 0 there, so the value never matters); wrapped
+ * on periodic axes */
 static inline double get(const level_t *L, const double *v, int i, int j,
                          int k) {
+  i = wrap(i, L->nx, L->per[0]);
+  j = wrap(j, L->ny, L->per[1]);
+  k = wrap(k, L->nz, L->per[2]);
   if (i < 0 || j < 0 || k < 0 || i >= L->nx || j >= L->ny || k >= L->nz)
     return 0.0;
   return v[IDX(L, i, j, k)];
@@ -135,7 +151,9 @@ static void assemble_finest(orc_hier *H) {
         double beta = 6.0 * inv;
         for (int q = 0; q < 6; q++) {
           double alpha = -1.0 * inv;
-          int ii = i + di[q], jj = j + dj[q], kk = k + dk[q];
+          int ii = wrap(i + di[q], L->nx, L->per[0]);
+          int jj = wrap(j + dj[q], L->ny, L->per[1]);
+          int kk = wrap(k + dk[q], L->nz, L->per[2]);
           int outside = ii < 0 || jj < 0 || kk < 0 || ii >= L->nx ||
                         jj >= L->ny || kk >= L->nz;
           if (outside) {
@@ -180,7 +198,9 @@ static void galerkin(orc_hier *H, int l) {
               const double *A = &F->A[7 * fi];
               s[0] += A[0];
               for (int q = 0; q < 6; q++) {
-                int ii = i + di[q], jj = j + dj[q], kk = k + dk[q];
+                int ii = wrap(i + di[q], F->nx, F->per[0]);
+                int jj = wrap(j + dj[q], F->ny, F->per[1]);
+                int kk = wrap(k + dk[q], F->nz, F->per[2]);
                 if (ii < 0 || jj < 0 || kk < 0 || ii >= F->nx || jj >= F->ny ||
                     kk >= F->nz)
                   continue; /* folded: coefficient is 0 */
@@ -202,12 +222,22 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
   if (nx <= 0 || ny <= 0 || nz <= 0 || !(h > 0.0)) return NULL;
   if (max_levels <= 0) max_levels = MAXLEV;
   if (max_levels > MAXLEV) max_levels = MAXLEV;
+  /* periodic faces come in pairs: an axis is periodic on both sides or on
+   * neither ("cyclically extend the domain") */
+  int per[3];
+  for (int a = 0; a < 3; a++) {
+    const int lo = bc_type[2 * a] == ORC_PERIODIC;
+    const int hi = bc_type[2 * a + 1] == ORC_PERIODIC;
+    if (lo != hi) return NULL;
+    per[a] = lo;
+  }
   orc_hier *H = (orc_hier *)calloc(1, sizeof(orc_hier));
   H->h = h;
   for (int q = 0; q < 6; q++) {
     H->bct[q] = bc_type[q];
     H->bcv[q] = bc_value[q];
   }
+  for (int a = 0; a < 3; a++) H->per[a] = per[a];
   H->nu1 = 2;
   H->nu2 = 2;
   H->alpha = 2.0;
@@ -219,6 +249,7 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
   int d[3] = {nx, ny, nz};
   level_alloc(&H->L[0], d[0], d[1], d[2]);
   H->nlev = 1;
+  for (int a = 0; a < 3; a++) H->L[0].per[a] = per[a];
   while (H->nlev < max_levels) {
     int ok = 1;
     for (int a = 0; a < 3; a++)
@@ -229,6 +260,7 @@ orc_hier *orc_create(int nx, int ny, int nz, double h, const int *bc_type,
     if (!ok) break;
     for (int a = 0; a < 3; a++) d[a] /= 2;
     level_alloc(&H->L[H->nlev], d[0], d[1], d[2]);
+    for (int a = 0; a < 3; a++) H->L[H->nlev].per[a] = per[a];
     H->nlev++;
   }
   level_t *L0 = &H->L[0];
@@ -252,7 +284,7 @@ void orc_destroy(orc_hier *H) {
  * Dirichlet data of the charged-sphere validation) */
 int orc_set_face_values(orc_hier *H, int q, const double *values) {
   level_t *L = &H->L[0];
-  if (q < 0 || q > 5) return -1;
+  if (q < 0 || q > 5 || H->per[q / 2]) return -1;
   const int ext[3] = {L->nx, L->ny, L->nz};
   const int ax = q / 2;
   const long n = (long)ext[ax == 0 ? 1 : 0] * ext[ax == 2 ? 1 : 2];
@@ -272,7 +304,7 @@ int orc_set_face_values(orc_hier *H, int q, const double *values) {
 int orc_set_bc_patch(orc_hier *H, int q, int a0, int a1, int b0, int b1,
                      int type, double value) {
   level_t *L = &H->L[0];
-  if (q < 0 || q > 5) return -1;
+  if (q < 0 || q > 5 || H->per[q / 2] || type == ORC_PERIODIC) return -1;
   const int ext[3] = {L->nx, L->ny, L->nz};
   const int ax = q / 2;
   const int na = ext[ax == 0 ? 1 : 0], nb = ext[ax == 2 ? 1 : 2];
@@ -339,7 +371,7 @@ void orc_bc_adapt(orc_hier *H) {
         int on[6] = {i == 0, i == L->nx - 1, j == 0,
                      j == L->ny - 1, k == 0, k == L->nz - 1};
         for (int q = 0; q < 6; q++) {
-          if (!on[q]) continue;
+          if (!on[q] || H->per[q / 2]) continue; /* periodic: no boundary */
           double g = face_value(H, q, i, j, k);
           if (face_type(H, q, i, j, k) == ORC_DIRICHLET)
             L->f[c] = L->f[c] - 2.0 * alpha * g;
@@ -390,7 +422,27 @@ static inline int sub_count(int i, int j, int k, int s, double hs, double cx,
   return cnt;
 }
 
-long orc_sphere_subcount(int nx, int ny, int nz, double h, int s, double cx,
+/* Periodic images of a sphere (the domain is cyclically
+ * extended): centres c + m (n h) with m in {-1, 0, 1} on periodic axes (m = 0
+ * leaves the coordinate untouched), in (mx, my, mz) lexicographic order.
+ * With 2R + 2h <= n h on every periodic axis (checked by the callers) no
+ * cell is reached by two images.  per == NULL: no periodic axis. */
+static int sphere_images(const int *per, int nx, int ny, int nz, double h,
+                         double cx, double cy, double cz, double img[27][3]) {
+  const int px = per ? per[0] : 0, py = per ? per[1] : 0, pz = per ? per[2] : 0;
+  int n = 0;
+  for (int mx = -px; mx <= px; mx++)
+    for (int my = -py; my <= py; my++)
+      for (int mz = -pz; mz <= pz; mz++) {
+        img[n][0] = mx ? cx + (double)mx * ((double)nx * h) : cx;
+        img[n][1] = my ? cy + (double)my * ((double)ny * h) : cy;
+        img[n][2] = mz ? cz + (double)mz * ((double)nz * h) : cz;
+        n++;
+      }
+  return n;
+}
+
+static long subcount_one(int nx, int ny, int nz, double h, int s, double cx,
                          double cy, double cz, double R) {
   const double hs = h / (double)s;
   int i0, i1, j0, j1, k0, k1;
@@ -405,6 +457,22 @@ long orc_sphere_subcount(int nx, int ny, int nz, double h, int s, double cx,
   return cnt;
 }
 
+/* covered sub-cells of the domain, summed over the periodic images */
+static long subcount_per(const int *per, int nx, int ny, int nz, double h,
+                         int s, double cx, double cy, double cz, double R) {
+  double img[27][3];
+  const int ni = sphere_images(per, nx, ny, nz, h, cx, cy, cz, img);
+  long cnt = 0;
+  for (int m = 0; m < ni; m++)
+    cnt += subcount_one(nx, ny, nz, h, s, img[m][0], img[m][1], img[m][2], R);
+  return cnt;
+}
+
+long orc_sphere_subcount(int nx, int ny, int nz, double h, int s, double cx,
+                         double cy, double cz, double R) {
+  return subcount_one(nx, ny, nz, h, s, cx, cy, cz, R);
+}
+
 long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
                            double cy, double cz, double R) {
   return orc_sphere_subcount(nx, ny, nz, h, 1, cx, cy, cz, R);
@@ -415,36 +483,66 @@ long orc_sphere_cell_count(int nx, int ny, int nz, double h, double cx,
  *   PER_CELLS:  cell value = (Q_p cnt) / (n_p h^3)       (charge exact)
  *   PER_VOLUME: cell value = (Q_p / (4/3 pi R^3)) (cnt / s^3)  (the paper's)
  * eps = 1 (c15), so f = rho.  Overlapping spheres add in sphere order. */
-void orc_sphere_density_sub(int nx, int ny, int nz, double h, int s, int n,
-                            const double *centers, const double *radii,
-                            const double *charges, int normalization,
-                            double *out) {
+static void density_per(const int *per, int nx, int ny, int nz, double h,
+                        int s, int n, const double *centers,
+                        const double *radii, const double *charges,
+                        int normalization, double *out) {
   long N = (long)nx * ny * nz;
   const double hs = h / (double)s;
   for (long c = 0; c < N; c++) out[c] = 0.0;
   for (int p = 0; p < n; p++) {
-    double cx = centers[3 * p], cy = centers[3 * p + 1],
-           cz = centers[3 * p + 2], R = radii[p], Q = charges[p];
-    long np = orc_sphere_subcount(nx, ny, nz, h, s, cx, cy, cz, R);
+    double R = radii[p], Q = charges[p];
+    double img[27][3];
+    const int ni = sphere_images(per, nx, ny, nz, h, centers[3 * p],
+                                 centers[3 * p + 1], centers[3 * p + 2], img);
+    long np = subcount_per(per, nx, ny, nz, h, s, centers[3 * p],
+                           centers[3 * p + 1], centers[3 * p + 2], R);
     if (normalization != ORC_PER_VOLUME && np == 0) continue;
     const double rho0 = Q / ((4.0 / 3.0) * ORC_PI * (R * R * R));
-    int i0, i1, j0, j1, k0, k1;
-    bbox(nx, h, cx, R, &i0, &i1);
-    bbox(ny, h, cy, R, &j0, &j1);
-    bbox(nz, h, cz, R, &k0, &k1);
-    for (int i = i0; i <= i1; i++)
-      for (int j = j0; j <= j1; j++)
-        for (int k = k0; k <= k1; k++) {
-          const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
-          if (!cnt) continue;
-          double v;
-          if (normalization == ORC_PER_VOLUME)
-            v = rho0 * ((double)cnt / (double)(s * s * s));
-          else
-            v = (Q * (double)cnt) / ((double)np * (h * h * h));
-          out[((long)i * ny + j) * nz + k] += v;
-        }
+    for (int m = 0; m < ni; m++) {
+      const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+      int i0, i1, j0, j1, k0, k1;
+      bbox(nx, h, cx, R, &i0, &i1);
+      bbox(ny, h, cy, R, &j0, &j1);
+      bbox(nz, h, cz, R, &k0, &k1);
+      for (int i = i0; i <= i1; i++)
+        for (int j = j0; j <= j1; j++)
+          for (int k = k0; k <= k1; k++) {
+            const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+            if (!cnt) continue;
+            double v;
+            if (normalization == ORC_PER_VOLUME)
+              v = rho0 * ((double)cnt / (double)(s * s * s));
+            else
+              v = (Q * (double)cnt) / ((double)np * (h * h * h));
+            out[((long)i * ny + j) * nz + k] += v;
+          }
+    }
   }
+}
+
+void orc_sphere_density_sub(int nx, int ny, int nz, double h, int s, int n,
+                            const double *centers, const double *radii,
+                            const double *charges, int normalization,
+                            double *out) {
+  density_per(NULL, nx, ny, nz, h, s, n, centers, radii, charges,
+              normalization, out);
+}
+
+/* spheres on a periodic axis: centre in [0, n h) and 2R + 2h <= n h, so the
+ * images are disjoint (sphere_images); 0 or -1 */
+static int check_periodic_spheres(const orc_hier *H, int n,
+                                  const double *centers, const double *radii) {
+  const level_t *L = &H->L[0];
+  const int ext[3] = {L->nx, L->ny, L->nz};
+  for (int p = 0; p < n; p++)
+    for (int a = 0; a < 3; a++) {
+      if (!H->per[a]) continue;
+      const double len = (double)ext[a] * H->h, c = centers[3 * p + a];
+      if (!(c >= 0.0 && c < len) || !(2.0 * radii[p] + 2.0 * H->h <= len))
+        return -1;
+    }
+  return 0;
 }
 
 void orc_sphere_density(int nx, int ny, int nz, double h, int n,
@@ -460,14 +558,14 @@ int orc_set_rhs_from_spheres_sub(orc_hier *H, int n, const double *centers,
                                  int normalization, int s) {
   level_t *L = &H->L[0];
   if (s < 1) return -1;
+  if (check_periodic_spheres(H, n, centers, radii)) return -1;
   if (normalization == ORC_PER_CELLS)
     for (int p = 0; p < n; p++)
-      if (orc_sphere_subcount(L->nx, L->ny, L->nz, H->h, s, centers[3 * p],
-                              centers[3 * p + 1], centers[3 * p + 2],
-                              radii[p]) == 0)
+      if (subcount_per(H->per, L->nx, L->ny, L->nz, H->h, s, centers[3 * p],
+                       centers[3 * p + 1], centers[3 * p + 2], radii[p]) == 0)
         return -1;
-  orc_sphere_density_sub(L->nx, L->ny, L->nz, H->h, s, n, centers, radii,
-                         charges, normalization, L->f);
+  density_per(H->per, L->nx, L->ny, L->nz, H->h, s, n, centers, radii,
+              charges, normalization, L->f);
   for (long c = 0; c < L->n; c++)
     if (!L->unk[c]) L->f[c] = 0.0;
   orc_bc_adapt(H);
@@ -497,8 +595,18 @@ static const int ORC_Q19[18][3] = {
     {1, 0, -1}, {-1, 0, 1}, {0, 1, 1},   {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
 
 static inline int valid_cell(const level_t *L, int i, int j, int k) {
+  i = wrap(i, L->nx, L->per[0]);
+  j = wrap(j, L->ny, L->per[1]);
+  k = wrap(k, L->nz, L->per[2]);
   return i >= 0 && j >= 0 && k >= 0 && i < L->nx && j < L->ny && k < L->nz &&
          L->unk[IDX(L, i, j, k)];
+}
+
+/* phi at a (valid) cell, wrapped on periodic axes */
+static inline double phi_w(const level_t *L, const double *phi, int i, int j,
+                           int k) {
+  return phi[IDX(L, wrap(i, L->nx, L->per[0]), wrap(j, L->ny, L->per[1]),
+                 wrap(k, L->nz, L->per[2]))];
 }
 
 void orc_gradient(const orc_hier *H, const double *phi, int i, int j, int k,
@@ -516,8 +624,8 @@ void orc_gradient(const orc_hier *H, const double *phi, int i, int j, int k,
         const int c = ORC_Q19[q][a];
         if (c == 0) continue;
         const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
-        const double v = phi[IDX(L, i + ORC_Q19[q][0], j + ORC_Q19[q][1],
-                                 k + ORC_Q19[q][2])];
+        const double v = phi_w(L, phi, i + ORC_Q19[q][0], j + ORC_Q19[q][1],
+                               k + ORC_Q19[q][2]);
         S = c > 0 ? S + w * v : S - w * v;
       }
       g[a] = (3.0 * S) / h;
@@ -532,12 +640,12 @@ void orc_gradient(const orc_hier *H, const double *phi, int i, int j, int k,
     const int vm = valid_cell(L, i + dm[0], j + dm[1], k + dm[2]);
     const double c0 = phi[IDX(L, i, j, k)];
     if (vp && vm)
-      g[a] = (phi[IDX(L, i + dp[0], j + dp[1], k + dp[2])] -
-              phi[IDX(L, i + dm[0], j + dm[1], k + dm[2])]) / (2.0 * h);
+      g[a] = (phi_w(L, phi, i + dp[0], j + dp[1], k + dp[2]) -
+              phi_w(L, phi, i + dm[0], j + dm[1], k + dm[2])) / (2.0 * h);
     else if (vp)
-      g[a] = (phi[IDX(L, i + dp[0], j + dp[1], k + dp[2])] - c0) / h;
+      g[a] = (phi_w(L, phi, i + dp[0], j + dp[1], k + dp[2]) - c0) / h;
     else if (vm)
-      g[a] = (c0 - phi[IDX(L, i + dm[0], j + dm[1], k + dm[2])]) / h;
+      g[a] = (c0 - phi_w(L, phi, i + dm[0], j + dm[1], k + dm[2])) / h;
     else
       g[a] = 0.0;
   }
@@ -552,29 +660,38 @@ int orc_coulomb_forces(const orc_hier *H, int n, const double *centers,
                        int normalization, int s, double *forces) {
   const level_t *L = &H->L[0];
   const double h = H->h, hs = h / (double)s;
+  if (check_periodic_spheres(H, n, centers, radii)) return -1;
   for (int p = 0; p < n; p++) {
-    const double cx = centers[3 * p], cy = centers[3 * p + 1],
-                 cz = centers[3 * p + 2], R = radii[p], Q = charges[p];
-    const long np = orc_sphere_subcount(L->nx, L->ny, L->nz, h, s, cx, cy, cz, R);
+    const double R = radii[p], Q = charges[p];
+    double img[27][3];
+    const int ni = sphere_images(H->per, L->nx, L->ny, L->nz, h, centers[3 * p],
+                                 centers[3 * p + 1], centers[3 * p + 2], img);
+    const long np = subcount_per(H->per, L->nx, L->ny, L->nz, h, s,
+                                 centers[3 * p], centers[3 * p + 1],
+                                 centers[3 * p + 2], R);
     double F[3] = {0.0, 0.0, 0.0};
     if (np > 0 || normalization == ORC_PER_VOLUME) {
       const double rho0 = Q / ((4.0 / 3.0) * ORC_PI * (R * R * R));
-      int i0, i1, j0, j1, k0, k1;
-      bbox(L->nx, h, cx, R, &i0, &i1);
-      bbox(L->ny, h, cy, R, &j0, &j1);
-      bbox(L->nz, h, cz, R, &k0, &k1);
-      for (int i = i0; i <= i1; i++)
-        for (int j = j0; j <= j1; j++)
-          for (int k = k0; k <= k1; k++) {
-            const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
-            if (!cnt || !L->unk[IDX(L, i, j, k)]) continue;
-            const double rho = normalization == ORC_PER_VOLUME
-                                   ? rho0 * ((double)cnt / (double)(s * s * s))
-                                   : (Q * (double)cnt) / ((double)np * (h * h * h));
-            double g[3];
-            orc_gradient(H, L->phi, i, j, k, g);
-            for (int a = 0; a < 3; a++) F[a] = F[a] + g[a] * rho;
-          }
+      for (int m = 0; m < ni; m++) {
+        const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+        int i0, i1, j0, j1, k0, k1;
+        bbox(L->nx, h, cx, R, &i0, &i1);
+        bbox(L->ny, h, cy, R, &j0, &j1);
+        bbox(L->nz, h, cz, R, &k0, &k1);
+        for (int i = i0; i <= i1; i++)
+          for (int j = j0; j <= j1; j++)
+            for (int k = k0; k <= k1; k++) {
+              const int cnt = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+              if (!cnt || !L->unk[IDX(L, i, j, k)]) continue;
+              const double rho =
+                  normalization == ORC_PER_VOLUME
+                      ? rho0 * ((double)cnt / (double)(s * s * s))
+                      : (Q * (double)cnt) / ((double)np * (h * h * h));
+              double g[3];
+              orc_gradient(H, L->phi, i, j, k, g);
+              for (int a = 0; a < 3; a++) F[a] = F[a] + g[a] * rho;
+            }
+      }
     }
     for (int a = 0; a < 3; a++) forces[3 * p + a] = -(h * h * h) * F[a];
   }

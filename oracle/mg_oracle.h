@@ -22,6 +22,7 @@ extern "C" {
 
 #define ORC_DIRICHLET 0
 #define ORC_NEUMANN 1
+#define ORC_PERIODIC 2 /* both faces of an axis */
 
 #define ORC_PER_CELLS 0  /* rho = Q / (n_p h^3)      (reading c12, default)  */
 #define ORC_PER_VOLUME 1 /* rho = Q / (4/3 pi R^3)   (paper's naive map P:481) */

@@ -8,6 +8,8 @@ with ghost cells whose values follow the paper's extrapolation rules
     Dirichlet:  Phi_ghost = 2 g_d - Phi_1
     Neumann:    Phi_ghost = Phi_1 + h g_n     (reading c2, outward normal)
 
+    Periodic:   Phi_ghost = Phi on the opposite side
+
 so the folded stencil of the oracle and the ghost-cell form here are two
 different constructions of the same operator.
 """
@@ -15,7 +17,7 @@ from __future__ import annotations
 
 import numpy as np
 
-DIRICHLET, NEUMANN = 0, 1
+DIRICHLET, NEUMANN, PERIODIC = 0, 1, 2
 
 
 def _ghost_pad(u, h, bc_type, bc_value, homogeneous):
@@ -33,6 +35,11 @@ def _ghost_pad(u, h, bc_type, bc_value, homogeneous):
         else:
             sl_g[ax], sl_1[ax] = -1, -2
         inner = p[tuple(sl_1)]
+        if np.all(np.asarray(bc_type[face]) == PERIODIC):
+            sl_o = [slice(1, -1)] * 3  # the opposite side's last cell layer
+            sl_o[ax] = -2 if side == 0 else 1
+            p[tuple(sl_g)] = p[tuple(sl_o)]
+            continue
         t = np.broadcast_to(np.asarray(bc_type[face]), inner.shape)
         gg = np.broadcast_to(np.asarray(g, dtype=float), inner.shape)
         p[tuple(sl_g)] = np.where(t == DIRICHLET, 2.0 * gg - inner, inner + h * gg)
@@ -69,7 +76,8 @@ def bc_rhs_shift(shape, h, bc_type, bc_value):
 
 
 def tridiag_1d(n, h, lo, hi):
-    """1D ghost-cell operator along one axis (ends: D -> 3, N -> 1 over h^2)."""
+    """1D ghost-cell operator along one axis (ends: D -> 3, N -> 1 over h^2;
+    periodic: circulant)."""
     T = np.zeros((n, n))
     for i in range(n):
         T[i, i] = 2.0
@@ -79,6 +87,10 @@ def tridiag_1d(n, h, lo, hi):
             T[i, i + 1] = -1.0
     # end rows (2 u_1 - ghost - u_2): Dirichlet ghost = -u_1 -> 3,
     # Neumann ghost = +u_1 -> 1
+    if lo == PERIODIC:  # circulant: the ends couple to each other
+        T[0, -1] += -1.0
+        T[-1, 0] += -1.0
+        return T / (h * h)
     T[0, 0] = 3.0 if lo == DIRICHLET else 1.0
     T[-1, -1] = 3.0 if hi == DIRICHLET else 1.0
     return T / (h * h)
@@ -116,8 +128,9 @@ def injection_P(fine_shape, unknown_fine=None, unknown_coarse=None):
     return P
 
 
-def stencil_to_dense(st):
-    """Dense matrix from a 7-per-cell stencil field [c, x-, x+, y-, y+, z-, z+]."""
+def stencil_to_dense(st, per=(False, False, False)):
+    """Dense matrix from a 7-per-cell stencil field [c, x-, x+, y-, y+, z-, z+];
+    neighbours across a periodic axis wrap to the opposite side."""
     nx, ny, nz, _ = st.shape
     n = nx * ny * nz
     A = np.zeros((n, n))
@@ -129,6 +142,12 @@ def stencil_to_dense(st):
                 A[r, r] += st[i, j, k, 0]
                 for q, (a, b, c) in enumerate(off):
                     ii, jj, kk = i + a, j + b, k + c
+                    if per[0]:
+                        ii %= nx
+                    if per[1]:
+                        jj %= ny
+                    if per[2]:
+                        kk %= nz
                     if 0 <= ii < nx and 0 <= jj < ny and 0 <= kk < nz:
                         A[r, (ii * ny + jj) * nz + kk] += st[i, j, k, 1 + q]
                     else:
