@@ -247,12 +247,16 @@ size_t carve(mg_ctx *c, char *base) {
   Carver cv{base};
   const int L = c->pl.L;
   c->g.assign(L, {});
+  // centre contribution of a face: Dirichlet +1, Neumann -1, periodic 0
   int dface[6];
-  for (int q = 0; q < 6; q++) dface[q] = c->bc[q].type == MG_DIRICHLET ? 1 : -1;
+  for (int q = 0; q < 6; q++)
+    dface[q] = c->bc[q].type == MG_DIRICHLET ? 1 : (c->bc[q].type == MG_NEUMANN ? -1 : 0);
   for (int l = 0; l < L; l++) {
     const int ns = l < c->pl.nd ? c->nslab : 1;
     for (int s = 0; s < ns; s++) {
       Grid gr = make_grid(c->pl, l, l < c->pl.nd ? c->slab0 + s : 0, c->h, dface);
+      for (int a = 0; a < 3; a++) gr.per[a] = c->bc[2 * a].type == MG_PERIODIC;
+      gr.gx = gr.per[0] && gr.nxl == gr.nx;  // whole grid: own x ghosts
       const size_t bytes = (size_t)mg::grid_elems(gr) * sizeof(double);
       gr.phiR = (double *)cv.take(bytes);
       gr.phiB = (double *)cv.take(bytes);
@@ -311,13 +315,28 @@ const Grid &coarse_of(const mg_ctx *c, int l, int s) {
   return (l + 1 < c->pl.nd) ? c->g[l + 1][s] : c->g[l + 1][0];
 }
 
-// ghost-plane exchange of one colour array (0 phiR, 1 phiB) on level l
+bool periodic_x(const mg_ctx *c) { return c->bc[0].type == MG_PERIODIC; }
+bool any_periodic(const mg_ctx *c) {
+  for (int q = 0; q < 6; q++)
+    if (c->bc[q].type == MG_PERIODIC) return true;
+  return false;
+}
+
+// ghost-plane exchange of one colour array (0 phiR, 1 phiB) on level l.  On a
+// periodic x axis the first and last slabs are neighbours too (P:692-693:
+// "processes are configured in a periodic arrangement").  Every rank posts
+// its sends / receives in the same order -- (last plane -> right, left ghost
+// <- left), then (first plane -> left, right ghost <- right) -- so that
+// repeated peers (P = 2 with wrap) match message by message.
 int halo(mg_ctx *c, int l, int which) {
   if (!distributed(c, l)) return MG_OK;
   auto arr = [&](const Grid &g) { return which ? g.phiB : g.phiR; };
+  const bool wrap = periodic_x(c);
   if (c->backend == MG_HALO_LOOPBACK) {
-    for (int s = 0; s + 1 < c->nslab; s++) {
-      const Grid &a = c->g[l][s], &b = c->g[l][s + 1];
+    const int ns = c->nslab;
+    for (int s = 0; s < ns; s++) {
+      if (s + 1 == ns && !wrap) break;
+      const Grid &a = c->g[l][s], &b = c->g[l][(s + 1) % ns];
       const size_t bytes = sizeof(double) * a.plane;
       CK(cudaMemcpyAsync(arr(b), arr(a) + (long long)a.nxl * a.plane, bytes,
                          cudaMemcpyDeviceToDevice, c->stream));
@@ -330,19 +349,30 @@ int halo(mg_ctx *c, int l, int which) {
   const Grid &g = c->g[l][0];
   double *A = arr(g);
   const size_t n = (size_t)g.plane;
+  const int P = c->P, r = c->rank;
+  const int left = r > 0 ? r - 1 : (wrap ? P - 1 : -1);
+  const int right = r < P - 1 ? r + 1 : (wrap ? 0 : -1);
   int rc;
   if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-  if (c->rank > 0) {
-    g_nccl.Send(A + g.plane, n, ncclDouble, c->rank - 1, c->comm, c->stream);
-    g_nccl.Recv(A, n, ncclDouble, c->rank - 1, c->comm, c->stream);
-  }
-  if (c->rank < c->P - 1) {
-    g_nccl.Send(A + (long long)g.nxl * g.plane, n, ncclDouble, c->rank + 1,
+  if (right >= 0)
+    g_nccl.Send(A + (long long)g.nxl * g.plane, n, ncclDouble, right, c->comm,
+                c->stream);
+  if (left >= 0) g_nccl.Recv(A, n, ncclDouble, left, c->comm, c->stream);
+  if (left >= 0) g_nccl.Send(A + g.plane, n, ncclDouble, left, c->comm, c->stream);
+  if (right >= 0)
+    g_nccl.Recv(A + (long long)(g.nxl + 1) * g.plane, n, ncclDouble, right,
                 c->comm, c->stream);
-    g_nccl.Recv(A + (long long)(g.nxl + 1) * g.plane, n, ncclDouble,
-                c->rank + 1, c->comm, c->stream);
-  }
   return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(halo)");
+}
+
+// periodic ghost rows / planes of the grids of level l held here, for the
+// writers of Phi that do not store ghost copies (prolongation, CG, copy-in)
+void periodic_fill(mg_ctx *c, int l) {
+  for (const Grid &g : c->g[l]) {
+    if (!(g.gx || g.per[1])) continue;
+    mg::launch_periodic_fill(g, c->stream);
+    c->launches++;
+  }
 }
 
 int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
@@ -403,6 +433,7 @@ int prolong_level(mg_ctx *c, int l) {
       mg::launch_prolong(c->g[l][s], coarse_of(c, l, s), 0, c->o.alpha, c->stream);
     c->launches++;
   }
+  periodic_fill(c, l);
   if (l == 0) mark(c, CAT_PROLONG0);
   CK(cudaGetLastError());
   return halo(c, l, 1);  // the next red half-sweep reads black ghosts
@@ -410,7 +441,9 @@ int prolong_level(mg_ctx *c, int l) {
 
 // can level l use the fused last-black + residual epilogue kernels?
 bool can_fuse_resid(const mg_ctx *c, int l) {
-  if (!c->use_march || !c->use_fused || c->masked || distributed(c, l)) return false;
+  if (!c->use_march || !c->use_fused || c->masked || distributed(c, l) ||
+      any_periodic(c))
+    return false;
   for (const TmPair &t : c->tm[l])
     if (!t.ok_fused) return false;
   return c->g[l].size() == 1;
@@ -459,6 +492,7 @@ int coarse_solve(mg_ctx *c) {
     mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
                          c->cg_iters, c->stream);
   c->launches++;
+  periodic_fill(c, c->pl.L - 1);  // the prolongation reads coarse ghosts
   CK(cudaGetLastError());
   return MG_OK;
 }
@@ -615,8 +649,11 @@ int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in) {
   }
   CK(cudaGetLastError());
   if (in) {
-    // refresh ghost planes of both colours for a distributed level
+    // refresh ghost planes of both colours for a distributed level, and the
+    // periodic ghosts of grids held whole
     if (field == MG_FIELD_PHI) {
+      periodic_fill(c, l);
+      CK(cudaGetLastError());
       if ((rc = halo(c, l, 0))) return rc;
       if ((rc = halo(c, l, 1))) return rc;
     }
@@ -663,6 +700,21 @@ int residual_norm_now(mg_ctx *c, double *out) {
   if (rc) return rc;
   if ((rc = sync(c))) return rc;
   *out = sqrt(*c->h_norm);
+  return MG_OK;
+}
+
+// spheres on a periodic axis: centre in [0, n h) and 2R + 2h <= n h, so the
+// periodic images of a sphere cover disjoint cells (mg.h)
+int check_sphere(const mg_ctx *c, int p, const double *ctr, double R) {
+  if (!(R > 0.0)) return fail(MG_ERR_ARG, "sphere %d: radius <= 0", p);
+  for (int a = 0; a < 3; a++) {
+    if (c->bc[2 * a].type != MG_PERIODIC) continue;
+    const double len = (double)c->pl.dims[0][a] * c->h;
+    if (!(ctr[a] >= 0.0 && ctr[a] < len) || !(2.0 * R + 2.0 * c->h <= len))
+      return fail(MG_ERR_ARG,
+                  "sphere %d on periodic axis %d: need centre in [0, %g) and "
+                  "2R + 2h <= %g", p, a, len, len);
+  }
   return MG_OK;
 }
 
@@ -737,12 +789,14 @@ static int validate(int nx, int ny, int nz, double h, const mg_bc *bc,
   if (!(h > 0.0)) return fail(MG_ERR_ARG, "h must be positive");
   bool anyD = false;
   for (int q = 0; q < 6; q++) {
-    if (bc[q].type == MG_PERIODIC)
-      return fail(MG_ERR_BC, "periodic faces are not implemented");
-    if (bc[q].type != MG_DIRICHLET && bc[q].type != MG_NEUMANN)
+    if (bc[q].type != MG_DIRICHLET && bc[q].type != MG_NEUMANN &&
+        bc[q].type != MG_PERIODIC)
       return fail(MG_ERR_BC, "face %d: unknown type %d", q, bc[q].type);
     anyD = anyD || bc[q].type == MG_DIRICHLET;
   }
+  for (int a = 0; a < 3; a++)
+    if ((bc[2 * a].type == MG_PERIODIC) != (bc[2 * a + 1].type == MG_PERIODIC))
+      return fail(MG_ERR_BC, "axis %d: periodic faces come in pairs (P:441-443)", a);
   if (!anyD)
     return fail(MG_ERR_BC, "no Dirichlet face: the operator is singular");
   if (o->nu1 < 0 || o->nu2 < 0 || o->nu1 + o->nu2 < 1)
@@ -938,7 +992,7 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   if (n > 0 && (!centers || !radii || !charges)) return fail(MG_ERR_ARG, "null array");
   std::vector<double> h5(5 * (size_t)n);
   for (int p = 0; p < n; p++) {
-    if (!(radii[p] > 0.0)) return fail(MG_ERR_ARG, "sphere %d: radius <= 0", p);
+    if (int rc = check_sphere(c, p, centers + 3 * (size_t)p, radii[p])) return rc;
     for (int a = 0; a < 3; a++) h5[5 * (size_t)p + a] = centers[3 * (size_t)p + a];
     h5[5 * (size_t)p + 3] = radii[p];
     h5[5 * (size_t)p + 4] = charges[p];
@@ -1226,6 +1280,9 @@ extern "C" {
 
 int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (solid && any_periodic(c))
+    return fail(MG_ERR_BC, "a solid mask on a domain with periodic faces is "
+                           "not supported");
   const size_t N = (size_t)c->pl.dims[0][0] * c->pl.dims[0][1] * c->pl.dims[0][2];
   if (!solid) {
     c->solid_h.clear();
@@ -1257,6 +1314,9 @@ int mg_set_bc_patch(mg_ctx *c, int face, int a0, int a1, int b0, int b1,
   if (face < 0 || face > 5) return fail(MG_ERR_ARG, "bad face %d", face);
   if (type != MG_DIRICHLET && type != MG_NEUMANN)
     return fail(MG_ERR_BC, "patch type must be Dirichlet or Neumann");
+  if (any_periodic(c))
+    return fail(MG_ERR_BC, "boundary patches on a domain with periodic faces "
+                           "are not supported");
   const int ext[3] = {c->pl.dims[0][0], c->pl.dims[0][1], c->pl.dims[0][2]};
   const int ax = face / 2;
   const int na = ext[ax == 0 ? 1 : 0], nb = ext[ax == 2 ? 1 : 2];
@@ -1279,6 +1339,8 @@ int mg_set_bc_patch(mg_ctx *c, int face, int a0, int a1, int b0, int b1,
 int mg_set_face_values(mg_ctx *c, int face, const double *values) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (face < 0 || face > 5 || !values) return fail(MG_ERR_ARG, "bad arguments");
+  if (c->bc[face].type == MG_PERIODIC)
+    return fail(MG_ERR_BC, "face %d is periodic: it has no boundary values", face);
   init_face_arrays(c);
   memcpy(c->fva_h[face].data(), values, c->fva_h[face].size() * sizeof(double));
   return rebuild_coefficients(c);
@@ -1297,7 +1359,7 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
   if (n == 0) return MG_OK;
   std::vector<double> h5(5 * (size_t)n);
   for (int p = 0; p < n; p++) {
-    if (!(radii[p] > 0.0)) return fail(MG_ERR_ARG, "sphere %d: radius <= 0", p);
+    if (int rc = check_sphere(c, p, centers + 3 * (size_t)p, radii[p])) return rc;
     for (int q = 0; q < 3; q++) h5[5 * (size_t)p + q] = centers[3 * (size_t)p + q];
     h5[5 * (size_t)p + 3] = radii[p];
     h5[5 * (size_t)p + 4] = charges[p];

@@ -54,18 +54,47 @@ __device__ __forceinline__ void bbox_f(int n, double h, double c, double R,
   *hi = b > n - 1 ? n - 1 : b;
 }
 
-// fluid cell of the (global) domain?  solid: global natural-layout mask or null
+__device__ __forceinline__ int wrapi(int i, int n, int per) {
+  return !per ? i : (i < 0 ? i + n : (i >= n ? i - n : i));
+}
+
+// fluid cell of the (global) domain?  solid: global natural-layout mask or
+// null.  Periodic axes: the opposite side's cell.
 __device__ __forceinline__ bool valid_cell(const Grid &g, const unsigned char *solid,
                                            int i, int j, int k) {
+  i = wrapi(i, g.nx, g.per[0]);
+  j = wrapi(j, g.ny, g.per[1]);
+  k = wrapi(k, g.nz, g.per[2]);
   if (i < 0 || j < 0 || k < 0 || i >= g.nx || j >= g.ny || k >= g.nz) return false;
   return !solid || solid[((long long)i * g.ny + j) * g.nz + k] == 0;
 }
 
-// level-0 Phi at global cell (i, j, k) held by this slab (incl. ghost planes)
+// level-0 Phi at global cell (i, j, k) held by this slab (incl. ghost planes:
+// an x index one past the slab is its ghost plane, which on a periodic x
+// axis holds the opposite side's plane; y and z wrap explicitly)
 __device__ __forceinline__ double phi_at(const Grid &g, int i, int j, int k) {
+  j = wrapi(j, g.ny, g.per[1]);
+  k = wrapi(k, g.nz, g.per[2]);
+  const int iw = wrapi(i, g.nx, g.per[0]);  // colour of the cell it mirrors
   const long long e = (long long)(i - g.x0 + 1) * g.plane +
                       (long long)(j + 1) * g.pz + (k >> 1);
-  return (((i + j + k) & 1) ? g.phiB : g.phiR)[e];
+  return (((iw + j + k) & 1) ? g.phiB : g.phiR)[e];
+}
+
+// periodic images of a sphere centre: the enumeration of k_spheres / the
+// oracle (m in {-1,0,1} on periodic axes, (mx,my,mz) lexicographic)
+__device__ __forceinline__ int images_f(const Grid &g, double h, double cx,
+                                        double cy, double cz, double img[27][3]) {
+  int n = 0;
+  for (int mx = -g.per[0]; mx <= g.per[0]; mx++)
+    for (int my = -g.per[1]; my <= g.per[1]; my++)
+      for (int mz = -g.per[2]; mz <= g.per[2]; mz++) {
+        img[n][0] = mx ? cx + (double)mx * ((double)g.nx * h) : cx;
+        img[n][1] = my ? cy + (double)my * ((double)g.ny * h) : cy;
+        img[n][2] = mz ? cz + (double)mz * ((double)g.nz * h) : cz;
+        n++;
+      }
+  return n;
 }
 
 __device__ void gradient(const Grid &g, const unsigned char *solid, double h,
@@ -128,30 +157,41 @@ __global__ void __launch_bounds__(kTF)
               const double *sph, int normalization, double *part) {
   __shared__ double sh[32];
   const int p = blockIdx.x;
-  const double cx = sph[5 * p], cy = sph[5 * p + 1], cz = sph[5 * p + 2];
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
   const double hs = h / (double)s;
-  int i0, i1, j0, j1, k0, k1;
-  bbox_f(g.nx, h, cx, R, &i0, &i1);
-  bbox_f(g.ny, h, cy, R, &j0, &j1);
-  bbox_f(g.nz, h, cz, R, &k0, &k1);
-  const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-  const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
+  double img[27][3];
+  const int nimg = images_f(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
   double cnt = 0.0;
-  for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
-    const int k = k0 + (int)(t % nk);
-    const long long q = t / nk;
-    const int j = j0 + (int)(q % nj);
-    const int i = i0 + (int)(q / nj);
-    cnt += (double)subcnt(i, j, k, s, hs, cx, cy, cz, R);
+  for (int m = 0; m < nimg; m++) {
+    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+    int i0, i1, j0, j1, k0, k1;
+    bbox_f(g.nx, h, cx, R, &i0, &i1);
+    bbox_f(g.ny, h, cy, R, &j0, &j1);
+    bbox_f(g.nz, h, cz, R, &k0, &k1);
+    const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
+    const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
+    for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
+      const int k = k0 + (int)(t % nk);
+      const long long q = t / nk;
+      const int j = j0 + (int)(q % nj);
+      const int i = i0 + (int)(q / nj);
+      cnt += (double)subcnt(i, j, k, s, hs, cx, cy, cz, R);
+    }
   }
   const double np = bsum(cnt, sh);
   double F[3] = {0.0, 0.0, 0.0};
-  const int xa = i0 > g.x0 ? i0 : g.x0;
-  const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
   const bool any = np > 0.0 || normalization == 1;
-  if (any && xa <= xb) {
-    const double rho0 = Q / ((4.0 / 3.0) * 3.14159265358979323846 * (R * R * R));
+  const double rho0 = Q / ((4.0 / 3.0) * 3.14159265358979323846 * (R * R * R));
+  for (int m = 0; any && m < nimg; m++) {
+    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+    int i0, i1, j0, j1, k0, k1;
+    bbox_f(g.nx, h, cx, R, &i0, &i1);
+    bbox_f(g.ny, h, cy, R, &j0, &j1);
+    bbox_f(g.nz, h, cz, R, &k0, &k1);
+    const int nj = j1 - j0 + 1, nk = k1 - k0 + 1;
+    const int xa = i0 > g.x0 ? i0 : g.x0;
+    const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
+    if (xa > xb || nj <= 0 || nk <= 0) continue;
     const long long nloc = (long long)(xb - xa + 1) * nj * nk;
     for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
       const int k = k0 + (int)(t % nk);

@@ -33,10 +33,61 @@ struct Grid {
   //             2 delta (0 = solid), coef[8 e + 7] = delta  (all dyadic, exact)
   const unsigned char *codeR, *codeB;
   const float *coefR, *coefB;
+  // periodic axes ("accessing unknowns in cells at opposite sides
+  // of the domain"): per[a] = 1 for a periodic axis (dface = 0 on its faces).
+  // Ghost layers then hold the opposite side's cells: rows 0 / ny+1 mirror
+  // rows ny / 1 (y periodic); planes 0 / nxl+1 mirror planes nxl / 1 when
+  // the grid is held whole (gx = 1), otherwise the halo exchange wraps.  z
+  // has no ghosts: kernels wrap the half-index of z neighbours (per[2]).
+  int per[3];
+  int gx;  // x periodic and the grid held whole: its writers fill x ghosts
 };
 
 __host__ __device__ inline long long grid_elems(const Grid &g) {
   return (long long)(g.nxl + 2) * g.plane;
+}
+
+// Periodic ghost copies of a value just written at (il, j, half-index k) of a
+// colour array: the same colour array at the mirrored plane / row (nx, ny
+// even keep the colour; corners when both apply).  Writers of Phi call this
+// so that every reader finds current ghosts; the colour written is never
+// read by the kernel writing it.
+template <typename T>
+__device__ __forceinline__ void ghost_copies(const Grid &g, double *arr, int il,
+                                             int j, int k, T v) {
+  const bool ex = g.gx && (il == 0 || il == g.nxl - 1);
+  const bool ey = g.per[1] && (j == 0 || j == g.ny - 1);
+  if (!(ex || ey)) return;
+  // target planes / rows: the cell's own, then the mirrors (-1: none)
+  const int pl[3] = {il + 1, (g.gx && il == 0) ? g.nxl + 1 : -1,
+                     (g.gx && il == g.nxl - 1) ? 0 : -1};
+  const int rw[3] = {j + 1, (g.per[1] && j == 0) ? g.ny + 1 : -1,
+                     (g.per[1] && j == g.ny - 1) ? 0 : -1};
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int b = 0; b < 3; b++)
+      if ((a || b) && pl[a] >= 0 && rw[b] >= 0)
+        *reinterpret_cast<T *>(arr + (long long)pl[a] * g.plane +
+                               (long long)rw[b] * g.pz + k) = v;
+}
+
+// other-colour z neighbours of the own cells at half-indices k, k+1 of a row
+// (red cells at z = 2k + p): zm0 = z-1 of the first, zp1 = z+1 of the second;
+// the others are the row's entries k and k+1.  Outside the level: 0 (folded
+// boundary) or, on a periodic z axis, the opposite end of the row.
+__device__ __forceinline__ double z_lo(const Grid &g, const double *row, int k) {
+  return (k > 0) ? row[k - 1] : (g.per[2] ? row[g.nzh - 1] : 0.0);
+}
+__device__ __forceinline__ double z_hi(const Grid &g, const double *row, int k) {
+  return (k + 2 < g.nzh) ? row[k + 2] : (g.per[2] ? row[0] : 0.0);
+}
+// z+1 of the FIRST own cell (p = 1) is the entry k+1; when k is the row's
+// last half-index (odd nzh) that entry is padding (0, the folded boundary),
+// and on a periodic z axis it is the row's first entry instead
+__device__ __forceinline__ double z_hi0(const Grid &g, const double *row, int k,
+                                        double next) {
+  return (g.per[2] && k + 1 >= g.nzh) ? row[0] : next;
 }
 
 // ---- kernel launchers (mg_kernels.cu) ---------------------------------------
@@ -119,6 +170,9 @@ void launch_zero_solid(const Grid &g, cudaStream_t s);
 void launch_get_stencil(const Grid &g, double *out7, cudaStream_t s);
 // natural <-> split conversion of one field of a grid (phi: 0, f: 1)
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);
+// refresh the periodic ghost rows / planes of both Phi colours from the
+// interior (after writers that do not store ghost copies themselves)
+void launch_periodic_fill(const Grid &g, cudaStream_t s);
 void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s);
 
 }  // namespace mg

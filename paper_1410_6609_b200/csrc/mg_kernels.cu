@@ -76,15 +76,15 @@ __global__ void __launch_bounds__(kThreads)
     const double2 zc = ld2(oth + b + k);
     double zm0, zp0, zm1, zp1;
     if (p == 0) {
-      zm0 = (k > 0) ? oth[b + k - 1] : 0.0;
+      zm0 = z_lo(g, oth + b, k);
       zp0 = zc.x;
       zm1 = zc.x;
       zp1 = zc.y;
     } else {
       zm0 = zc.x;
-      zp0 = zc.y;
+      zp0 = z_hi0(g, oth + b, k, zc.y);
       zm1 = zc.y;
-      zp1 = (k + 2 < g.nzh) ? oth[b + k + 2] : 0.0;
+      zp1 = z_hi(g, oth + b, k);
     }
     s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
     s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
@@ -95,10 +95,13 @@ __global__ void __launch_bounds__(kThreads)
   double2 out;
   out.x = (fo.x * g.w + s0) / d0;
   out.y = (fo.y * g.w + s1) / d1;
-  if (k + 1 < g.nzh)
+  if (k + 1 < g.nzh) {
     *reinterpret_cast<double2 *>(own + b + k) = out;
-  else
+    ghost_copies(g, own, il, j, k, out);
+  } else {
     own[b + k] = out.x;
+    ghost_copies(g, own, il, j, k, out.x);
+  }
 }
 
 void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s) {
@@ -120,8 +123,10 @@ __device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
   const double *oth = col ? g.phiR : g.phiB;
   const double *f = col ? g.fB : g.fR;
   const long long b = rowbase(g, il, j);
-  const double zm = (z > 0) ? oth[b + k - 1 + p] : 0.0;
-  const double zp = (z < g.nz - 1) ? oth[b + k + p] : 0.0;
+  // z-1 / z+1 are the other colour's half-indices k-1+p / k+p; on a
+  // periodic z axis z = -1 / nz wrap to nz-1 / 0 (half-indices nzh-1 / 0)
+  const double zm = (z > 0) ? oth[b + k - 1 + p] : (g.per[2] ? oth[b + g.nzh - 1] : 0.0);
+  const double zp = (z < g.nz - 1) ? oth[b + k + p] : (g.per[2] ? oth[b] : 0.0);
   const double s = ((((oth[b - g.plane + k] + oth[b + g.plane + k]) +
                       oth[b - g.pz + k]) +
                      oth[b + g.pz + k]) +
@@ -246,15 +251,15 @@ __device__ __forceinline__ void resid_pair(const Grid &g, int il, int j, int k,
   const double2 fo = ld2(f + b + k);
   double zm0, zp0, zm1, zp1;
   if (p == 0) {
-    zm0 = (k > 0) ? oth[b + k - 1] : 0.0;
+    zm0 = z_lo(g, oth + b, k);
     zp0 = zc.x;
     zm1 = zc.x;
     zp1 = zc.y;
   } else {
     zm0 = zc.x;
-    zp0 = zc.y;
+    zp0 = z_hi0(g, oth + b, k, zc.y);
     zm1 = zc.y;
-    zp1 = (k + 2 < g.nzh) ? oth[b + k + 2] : 0.0;
+    zp1 = z_hi(g, oth + b, k);
   }
   const double s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
   const double s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
@@ -332,24 +337,6 @@ __device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
   return rowbase(g, il, j) + (z >> 1);
 }
 
-__device__ __forceinline__ double cg_apply(const Grid &g, const double *v,
-                                           long long n) {
-  const int z = (int)(n % g.nz);
-  const long long q = n / g.nz;
-  const int j = (int)(q % g.ny);
-  const int i = (int)(q / g.ny);
-  const long long sx = (long long)g.ny * g.nz, sy = g.nz;
-  const double xm = (i > 0) ? v[n - sx] : 0.0;
-  const double xp = (i < g.nx - 1) ? v[n + sx] : 0.0;
-  const double ym = (j > 0) ? v[n - sy] : 0.0;
-  const double yp = (j < g.ny - 1) ? v[n + sy] : 0.0;
-  const double zm = (z > 0) ? v[n - 1] : 0.0;
-  const double zp = (z < g.nz - 1) ? v[n + 1] : 0.0;
-  const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
-  const double d = (double)centre_d(g, i, j, z);
-  return g.c * (d * v[n] - s);
-}
-
 // sum over the block of per-thread values; one barrier; all threads get it
 __device__ __forceinline__ double cg_allsum(double v, double *part) {
 #pragma unroll
@@ -370,20 +357,27 @@ __global__ void __launch_bounds__(kCgThreads)
   const bool in_smem = N <= kCgSmemMax;
   double *base = in_smem ? cg_sm : scr;
   double *x = base, *r = base + N, *p = base + 2 * N, *q = base + 3 * N;
-  // per-element geometry, computed once: neighbour-validity bits (x-,x+,y-,
-  // y+,z-,z+) and the centre d (closed-form operator A = c (d - neighbours))
-  unsigned char *nb = reinterpret_cast<unsigned char *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
+  // per-element geometry, computed once: neighbour bits (x-,x+,y-,y+,z-,z+):
+  // bits 0-5 neighbour inside the level, bits 6-11 neighbour across a
+  // periodic face (the opposite side's cell); and the centre d
+  // (closed-form operator A = c (d - neighbours))
+  unsigned short *nb = reinterpret_cast<unsigned short *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
   signed char *dc = reinterpret_cast<signed char *>(nb + N);
   const long long sx = (long long)g.ny * g.nz, sy = g.nz;
+  const long long wx = (long long)(g.nx - 1) * sx, wy = (long long)(g.ny - 1) * sy,
+                  wz = g.nz - 1;
   int pb = 0;
   double acc = 0.0;
   for (long long n = threadIdx.x; n < N; n += blockDim.x) {
     const int z = (int)(n % g.nz);
     const long long t = n / g.nz;
     const int j = (int)(t % g.ny), i = (int)(t / g.ny);
-    nb[n] = (unsigned char)((i > 0) | ((i < g.nx - 1) << 1) | ((j > 0) << 2) |
-                            ((j < g.ny - 1) << 3) | ((z > 0) << 4) |
-                            ((z < g.nz - 1) << 5));
+    const int in[6] = {i > 0, i < g.nx - 1, j > 0, j < g.ny - 1, z > 0, z < g.nz - 1};
+    unsigned m = 0;
+#pragma unroll
+    for (int q = 0; q < 6; q++)
+      m |= in[q] ? (1u << q) : (g.per[q >> 1] ? (64u << q) : 0u);
+    nb[n] = (unsigned short)m;
     dc[n] = (signed char)centre_d(g, i, j, z);
     int col;
     const long long idx = split_index(g, i, j, z, &col);
@@ -403,12 +397,12 @@ __global__ void __launch_bounds__(kCgThreads)
       acc = 0.0;
       for (long long n = threadIdx.x; n < N; n += blockDim.x) {
         const unsigned m = nb[n];
-        const double xm = (m & 1) ? p[n - sx] : 0.0;
-        const double xp = (m & 2) ? p[n + sx] : 0.0;
-        const double ym = (m & 4) ? p[n - sy] : 0.0;
-        const double yp = (m & 8) ? p[n + sy] : 0.0;
-        const double zm = (m & 16) ? p[n - 1] : 0.0;
-        const double zp = (m & 32) ? p[n + 1] : 0.0;
+        const double xm = (m & 1) ? p[n - sx] : ((m & 64) ? p[n + wx] : 0.0);
+        const double xp = (m & 2) ? p[n + sx] : ((m & 128) ? p[n - wx] : 0.0);
+        const double ym = (m & 4) ? p[n - sy] : ((m & 256) ? p[n + wy] : 0.0);
+        const double yp = (m & 8) ? p[n + sy] : ((m & 512) ? p[n - wy] : 0.0);
+        const double zm = (m & 16) ? p[n - 1] : ((m & 1024) ? p[n + wz] : 0.0);
+        const double zp = (m & 32) ? p[n + 1] : ((m & 2048) ? p[n - wz] : 0.0);
         const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
         const double pn = p[n];
         const double qn = c * ((double)dc[n] * pn - s);
@@ -447,7 +441,7 @@ __global__ void __launch_bounds__(kCgThreads)
 }
 
 size_t coarse_cg_scratch_doubles(const Grid &g) {
-  // x, r, p, q + one byte of neighbour bits and one of centre per element
+  // x, r, p, q + two bytes of neighbour bits and one of centre per element
   return 5 * (size_t)g.nx * g.ny * g.nz;
 }
 
@@ -460,7 +454,7 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
   if (threads > 256) threads = 256;
   size_t smem = 0;
   if (N <= kCgSmemMax) {
-    smem = 4 * (size_t)N * sizeof(double) + 2 * (size_t)N;
+    smem = 4 * (size_t)N * sizeof(double) + 3 * (size_t)N;
     static size_t configured = 48 * 1024;
     if (smem > configured) {
       cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -510,50 +504,82 @@ __device__ __forceinline__ int sub_count(int i, int j, int k, int s, double hs,
   return cnt;
 }
 
+// periodic images of a sphere centre (the domain cyclically
+// extended): m in {-1, 0, 1} on periodic axes, image centre c + m (n h) (the
+// coordinate untouched for m = 0), (mx, my, mz) lexicographic -- the
+// oracle's enumeration.  The host checks 2R + 2h <= n h on periodic axes, so
+// no cell is reached by two images.
+__device__ __forceinline__ int sphere_images(const Grid &g, double h, double cx,
+                                             double cy, double cz,
+                                             double img[27][3]) {
+  int n = 0;
+  for (int mx = -g.per[0]; mx <= g.per[0]; mx++)
+    for (int my = -g.per[1]; my <= g.per[1]; my++)
+      for (int mz = -g.per[2]; mz <= g.per[2]; mz++) {
+        img[n][0] = mx ? cx + (double)mx * ((double)g.nx * h) : cx;
+        img[n][1] = my ? cy + (double)my * ((double)g.ny * h) : cy;
+        img[n][2] = mz ? cz + (double)mz * ((double)g.nz * h) : cz;
+        n++;
+      }
+  return n;
+}
+
 __global__ void __launch_bounds__(kThreads)
     k_spheres(Grid g, double h, int s, const double *sph, int normalization,
               unsigned long long *counts) {
   __shared__ double sh[32];
   const int p = blockIdx.x;
-  const double cx = sph[5 * p], cy = sph[5 * p + 1], cz = sph[5 * p + 2];
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
   const double hs = h / (double)s;
-  int i0, i1, j0, j1, k0, k1;
-  bbox(g.nx, h, cx, R, &i0, &i1);
-  bbox(g.ny, h, cy, R, &j0, &j1);
-  bbox(g.nz, h, cz, R, &k0, &k1);
-  const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-  const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
+  double img[27][3];
+  const int nimg = sphere_images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
   double cnt = 0.0;  // exact integer count (< 2^53)
-  for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
-    const int k = k0 + (int)(t % nk);
-    const long long q = t / nk;
-    const int j = j0 + (int)(q % nj);
-    const int i = i0 + (int)(q / nj);
-    cnt += (double)sub_count(i, j, k, s, hs, cx, cy, cz, R);
+  for (int m = 0; m < nimg; m++) {
+    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+    int i0, i1, j0, j1, k0, k1;
+    bbox(g.nx, h, cx, R, &i0, &i1);
+    bbox(g.ny, h, cy, R, &j0, &j1);
+    bbox(g.nz, h, cz, R, &k0, &k1);
+    const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
+    const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
+    for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
+      const int k = k0 + (int)(t % nk);
+      const long long q = t / nk;
+      const int j = j0 + (int)(q % nj);
+      const int i = i0 + (int)(q / nj);
+      cnt += (double)sub_count(i, j, k, s, hs, cx, cy, cz, R);
+    }
   }
   const double np = block_sum(cnt, sh);
   if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
   if (normalization != 1 && np == 0.0) return;
   const double rho0 = Q / ((4.0 / 3.0) * kPi * (R * R * R));
-  const int xa = i0 > g.x0 ? i0 : g.x0;
-  const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
-  if (xa > xb) return;
-  const long long nloc = (long long)(xb - xa + 1) * nj * nk;
-  for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
-    const int k = k0 + (int)(t % nk);
-    const long long q = t / nk;
-    const int j = j0 + (int)(q % nj);
-    const int i = xa + (int)(q / nj);
-    const int c = sub_count(i, j, k, s, hs, cx, cy, cz, R);
-    if (!c) continue;
-    // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3)
-    const double v = (normalization == 1)
-                         ? rho0 * ((double)c / (double)(s * s * s))
-                         : (Q * (double)c) / (np * (h * h * h));
-    const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
-    double *f = ((i + j + k) & 1) ? g.fB : g.fR;
-    atomicAdd(f + idx, v);
+  for (int m = 0; m < nimg; m++) {
+    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
+    int i0, i1, j0, j1, k0, k1;
+    bbox(g.nx, h, cx, R, &i0, &i1);
+    bbox(g.ny, h, cy, R, &j0, &j1);
+    bbox(g.nz, h, cz, R, &k0, &k1);
+    const int nj = j1 - j0 + 1, nk = k1 - k0 + 1;
+    const int xa = i0 > g.x0 ? i0 : g.x0;
+    const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
+    if (xa > xb || nj <= 0 || nk <= 0) continue;
+    const long long nloc = (long long)(xb - xa + 1) * nj * nk;
+    for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
+      const int k = k0 + (int)(t % nk);
+      const long long q = t / nk;
+      const int j = j0 + (int)(q % nj);
+      const int i = xa + (int)(q / nj);
+      const int c = sub_count(i, j, k, s, hs, cx, cy, cz, R);
+      if (!c) continue;
+      // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3)
+      const double v = (normalization == 1)
+                           ? rho0 * ((double)c / (double)(s * s * s))
+                           : (Q * (double)c) / (np * (h * h * h));
+      const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
+      double *f = ((i + j + k) & 1) ? g.fB : g.fR;
+      atomicAdd(f + idx, v);
+    }
   }
 }
 
@@ -594,7 +620,7 @@ __global__ void __launch_bounds__(kThreads) k_bc_adapt(Grid g, Terms T) {
                         j == g.ny - 1, z == 0, z == g.nz - 1};
 #pragma unroll
     for (int q = 0; q < 6; q++)
-      if (on[q]) v = v - T.t[q];
+      if (on[q] && !g.per[q >> 1]) v = v - T.t[q];  // periodic: no boundary
     f[b + (z >> 1)] = v;
   }
 }
@@ -649,6 +675,48 @@ void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * g.nz;
   if (total <= 0) return;
   k_unpack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field, nat);
+}
+
+// ---------------------------------------------------------------------------
+// Periodic ghost refresh ("near boundary values are then
+// copied to the periodic neighbour's ghost layer"): every ghost element of
+// both Phi colours that mirrors an interior cell is copied from it -- ghost
+// rows 0 / ny+1 of the interior planes (y periodic) and the whole ghost
+// planes 0 / nxl+1 incl. their ghost rows (x periodic, grid held whole).
+// Sources are interior elements only, so one pass needs no ordering.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) k_periodic_fill(Grid g) {
+  const long long rowsx = g.gx ? 2LL * (g.ny + 2) : 0;        // planes 0, nxl+1
+  const long long rowsy = g.per[1] ? 2LL * g.nxl : 0;          // rows 0, ny+1
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (rowsx + rowsy) * g.nzh) return;
+  const int k = (int)(t % g.nzh);
+  const long long r = t / g.nzh;
+  int ap, ar;  // ghost element's array plane / row
+  if (r < rowsx) {
+    ap = (r / (g.ny + 2)) ? g.nxl + 1 : 0;
+    ar = (int)(r % (g.ny + 2));
+  } else {
+    const long long q = r - rowsx;
+    ap = 1 + (int)(q >> 1);
+    ar = (q & 1) ? g.ny + 1 : 0;
+  }
+  int sp = ap, sr = ar;  // its interior source
+  if (g.gx) sp = ap == 0 ? g.nxl : (ap == g.nxl + 1 ? 1 : ap);
+  if (g.per[1]) sr = ar == 0 ? g.ny : (ar == g.ny + 1 ? 1 : ar);
+  if (sr == 0 || sr == g.ny + 1) return;  // non-periodic ghost row: stays 0
+  const long long dst = (long long)ap * g.plane + (long long)ar * g.pz + k;
+  const long long src = (long long)sp * g.plane + (long long)sr * g.pz + k;
+  g.phiR[dst] = g.phiR[src];
+  g.phiB[dst] = g.phiB[src];
+}
+
+void launch_periodic_fill(const Grid &g, cudaStream_t s) {
+  if (!(g.gx || g.per[1])) return;
+  const long long rows = (g.gx ? 2LL * (g.ny + 2) : 0) + (g.per[1] ? 2LL * g.nxl : 0);
+  const long long total = rows * g.nzh;
+  if (total <= 0) return;
+  k_periodic_fill<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g);
 }
 
 }  // namespace mg

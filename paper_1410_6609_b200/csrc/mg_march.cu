@@ -94,7 +94,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     const int rr = t / NCH, c = t % NCH;
     const int jj = j0 - 1 + rr;
     const int k = 2 * lane + 64 * c;
-    tOk[m] = PROLONG && t < ntask && jj >= 0 && jj < g.ny && k < g.nzh;
+    // rows of the level, plus (y periodic) the ghost rows -1 / ny that hold
+    // the opposite side's cells and need their parents' correction too
+    tOk[m] = PROLONG && t < ntask && k < g.nzh &&
+             (g.per[1] ? (jj >= -1 && jj <= g.ny) : (jj >= 0 && jj < g.ny));
     tRow[m] = rr * pz;
     tK[m] = k;
     const int J = jj >> 1;
@@ -103,7 +106,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   }
   auto load_e = [&](int q, double2 *E) {
     const int i = g.x0 + i0 - 1 + q;
-    const bool pok = i >= 0 && i < g.nx;
+    // x periodic: ghost planes -1 / nx hold the opposite side's cells, their
+    // parents sit in the coarse ghost planes (I = -1 / nx/2), kept current
+    const bool pok = g.per[0] || (i >= 0 && i < g.nx);
     const int I = i >> 1;
     const long long poff = (long long)(I - C.x0 + 1) * C.plane;
     const int Ip = I & 1;
@@ -129,7 +134,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   };
   auto apply_e = [&](int q, const double2 *E) {
     const int i = g.x0 + i0 - 1 + q;
-    if (i < 0 || i >= g.nx) return;  // physical ghost plane stays 0
+    if (!g.per[0] && (i < 0 || i >= g.nx)) return;  // physical ghost: stays 0
     double *slot = ring + (size_t)(q % kSlots) * sd;
 #pragma unroll
     for (int m = 0; m < kTPW; m++) {
@@ -223,15 +228,15 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const double2 zc = lds2(cur + k);
         double zm0, zp0, zm1, zp1;
         if (p == 0) {
-          zm0 = (k > 0) ? cur[k - 1] : 0.0;
+          zm0 = z_lo(g, cur, k);
           zp0 = zc.x;
           zm1 = zc.x;
           zp1 = zc.y;
         } else {
           zm0 = zc.x;
-          zp0 = zc.y;
+          zp0 = z_hi0(g, cur, k, zc.y);
           zm1 = zc.y;
-          zp1 = (k + 2 < g.nzh) ? cur[k + 2] : 0.0;
+          zp1 = z_hi(g, cur, k);
         }
         const int z0 = 2 * k + p;
         double s0, s1, d0, d1;
@@ -254,11 +259,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         out.x = (fr[c].x * g.w + s0) / d0;
         out.y = (fr[c].y * g.w + s1) / d1;
         const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
-        if (both)
+        if (both) {
           *reinterpret_cast<double2 *>(orow + k) = out;
-        else {  // ragged row end or a solid cell (not an unknown: untouched)
+          if (!MASK) ghost_copies(g, own, il, j, k, out);
+        } else {  // ragged row end or a solid cell (not an unknown: untouched)
           if (cd0 & 64) orow[k] = out.x;
           if (k + 1 < g.nzh && (cd1 & 64)) orow[k + 1] = out.y;
+          if (!MASK) ghost_copies(g, own, il, j, k, out.x);
         }
       }
     }
@@ -401,18 +408,22 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           const double2 yp = lds2(O + oc + W + kl);
           const double2 zc = lds2(O + oc + kl);
           const double2 u = lds2(M + oc + kl);
-          // z neighbours; the halo element is 0 outside the level
+          // z neighbours; the halo element is 0 outside the level, or on a
+          // periodic z axis the row's opposite end (not in this z-tile: a
+          // direct load of the other colour, unchanged during this kernel)
           double zm0, zp0, zm1, zp1;
+          const double *Og = (col ? g.phiR : g.phiB) +
+                             (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
           if (p == 0) {
-            zm0 = (k > 0) ? O[oc + kl - 1] : 0.0;
+            zm0 = (k > 0) ? O[oc + kl - 1] : (g.per[2] ? Og[g.nzh - 1] : 0.0);
             zp0 = zc.x;
             zm1 = zc.x;
             zp1 = zc.y;
           } else {
             zm0 = zc.x;
-            zp0 = zc.y;
+            zp0 = (g.per[2] && k + 1 >= g.nzh) ? Og[0] : zc.y;
             zm1 = zc.y;
-            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : 0.0;
+            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : (g.per[2] ? Og[0] : 0.0);
           }
           const int z0 = 2 * k + p;
           double s0, s1, d0, d1;

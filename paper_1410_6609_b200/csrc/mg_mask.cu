@@ -245,7 +245,7 @@ __global__ void __launch_bounds__(kT)
     const bool on[6] = {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, z == 0,
                         z == g.nz - 1};
     for (int q = 0; q < 6; q++) {
-      if (!on[q]) continue;
+      if (!on[q] || g.per[q >> 1]) continue;  // periodic: no boundary term
       const long long fi = face_idx(g, q, i, j, z);
       const bool dir = fb.ty[q] ? fb.ty[q][fi] == 0 : g.dface[q] > 0;
       const double gv = fb.va[q][fi];

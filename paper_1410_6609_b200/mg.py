@@ -30,6 +30,7 @@ MG_ERR_NOTCONV = -8
 MG_DIRICHLET = 0
 MG_NEUMANN = 1
 MG_PERIODIC = 2
+MG_PERIODIC = 2
 MG_HOST = 0
 MG_DEVICE = 1
 MG_CHARGE_PER_CELLS = 0
