@@ -56,11 +56,14 @@ extern "C" {
 /* ---- boundary conditions ------------------------------------ */
 #define MG_DIRICHLET 0 /* Phi = value on the face:   centre +1, f += 2 g/h^2  */
 #define MG_NEUMANN 1   /* dPhi/dn = value (outward): centre -1, f += g/h      */
-#define MG_PERIODIC 2  /* P:441-443; reserved, rejected with MG_ERR_BC        */
+#define MG_PERIODIC 2  /* P:441-443 "cyclically extend the domain": both
+                          faces of an axis; centre and RHS untouched, the
+                          neighbour is the opposite side's cell            */
 
 typedef struct {
-  int type;     /* MG_DIRICHLET or MG_NEUMANN                             */
-  double value; /* g_d (potential) or g_n (outward normal derivative)     */
+  int type;     /* MG_DIRICHLET, MG_NEUMANN or MG_PERIODIC                */
+  double value; /* g_d (potential) or g_n (outward normal derivative);
+                   ignored on periodic faces                              */
 } mg_bc;
 
 #define MG_HOST 0
@@ -119,6 +122,12 @@ size_t mg_workspace_bytes(int nx, int ny, int nz, const mg_opts *o);
 /* Create a solver for nx*ny*nz global cells of spacing h; bc[6] per face.
  * Requires even nx, ny, nz (the coarsest level is "a multiple of two",
  * P:506-507) and at least one Dirichlet face (otherwise A is singular).
+ * Periodic faces come in pairs (both faces of an axis, else
+ * MG_ERR_BC); every level keeps the periodicity (the Galerkin operator of a
+ * periodic grid is again periodic), the ghost layers of periodic axes hold
+ * the opposite side's cells, and with nranks > 1 a periodic x axis makes
+ * the first and last ranks halo neighbours.  A solid mask or boundary
+ * patches cannot be combined with periodic faces (MG_ERR_BC).
  * Returns NULL on error (message in mg_last_error(NULL)). */
 mg_ctx *mg_create(int nx, int ny, int nz, double h, const mg_bc *bc);
 mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
@@ -137,6 +146,24 @@ const char *mg_strerror(int code);
  * 0 and broadcast (e.g. with torch.distributed).  MG_ERR_NCCL if libnccl
  * cannot be loaded.  Needs no GPU. */
 int mg_nccl_unique_id(unsigned char out[128]);
+
+/* Ghost-plane exchange schedule of one colour array on a distributed level
+ * (periodic x: "processes are configured in a periodic
+ * arrangement"): the ordered point-to-point operations rank
+ * `rank` of `nranks` posts in one NCCL group.  ops[k] = {MG_OP_SEND or
+ * MG_OP_RECV, peer rank, plane} with plane one of MG_PLANE_FIRST / _LAST
+ * (first / last own x-plane) or MG_GHOST_LO / _HI (ghost plane before /
+ * after the slab).  Every rank posts (send last -> right, recv lo-ghost <-
+ * left, send first -> left, recv hi-ghost <- right), so that repeated peers
+ * (2 ranks with periodic x) match message by message.  Returns the number
+ * of operations (0..4) or MG_ERR_ARG.  Pure host logic, no GPU. */
+#define MG_OP_SEND 0
+#define MG_OP_RECV 1
+#define MG_PLANE_FIRST 1
+#define MG_PLANE_LAST 2
+#define MG_GHOST_LO 3
+#define MG_GHOST_HI 4
+int mg_halo_schedule(int nranks, int rank, int periodic_x, int ops[4][3]);
 
 /* ---- solid mask (config 5) -------------------------------------------------- */
 /* Mark solid cells (solid[i] != 0), natural layout of the WHOLE domain
@@ -164,7 +191,7 @@ int mg_set_bc_patch(mg_ctx *ctx, int face, int a0, int a1, int b0, int b1,
  * mg_set_bc_patch (na x nb = the two other global extents).  For analytic
  * Dirichlet data, e.g. the charged-sphere validation (Eq.18).
  * The operator is unchanged (only the RHS adaptation uses the values); set
- * the RHS afterwards. */
+ * the RHS afterwards.  MG_ERR_BC on a periodic face (it has no boundary). */
 int mg_set_face_values(mg_ctx *ctx, int face, const double *values);
 /* The operator of level l as 7 coefficients per cell [centre, x-, x+, y-, y+,
  * z-, z+] (natural layout, the caller's part as mg_get_field), zeros on solid
@@ -172,7 +199,10 @@ int mg_set_face_values(mg_ctx *ctx, int face, const double *values);
 int mg_get_stencil(mg_ctx *ctx, int level, double *out, int where);
 
 /* ---- right-hand side ----------------------------------------------------- */
-/* f := charge density of n uniformly charged spheres.  Each cell
+/* f := charge density of n uniformly charged spheres.  On a
+ * periodic axis a sphere also covers the cells of its periodic images
+ * (centre +- n h); there the centre must lie in [0, n h) and 2R + 2h <= n h
+ * (the images then reach disjoint cells), else MG_ERR_ARG.  Each cell
  * is subdivided into s^3 sub-cells (subsampling factor s = `subsample`,
  * 1..16; s = 1 is the plain rule "each cell whose center is
  * overlapped") and cnt = number of sub-cell centres with

@@ -349,19 +349,21 @@ int halo(mg_ctx *c, int l, int which) {
   const Grid &g = c->g[l][0];
   double *A = arr(g);
   const size_t n = (size_t)g.plane;
-  const int P = c->P, r = c->rank;
-  const int left = r > 0 ? r - 1 : (wrap ? P - 1 : -1);
-  const int right = r < P - 1 ? r + 1 : (wrap ? 0 : -1);
+  int ops[4][3];
+  const int nops = mg_halo_schedule(c->P, c->rank, wrap ? 1 : 0, ops);
   int rc;
   if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-  if (right >= 0)
-    g_nccl.Send(A + (long long)g.nxl * g.plane, n, ncclDouble, right, c->comm,
-                c->stream);
-  if (left >= 0) g_nccl.Recv(A, n, ncclDouble, left, c->comm, c->stream);
-  if (left >= 0) g_nccl.Send(A + g.plane, n, ncclDouble, left, c->comm, c->stream);
-  if (right >= 0)
-    g_nccl.Recv(A + (long long)(g.nxl + 1) * g.plane, n, ncclDouble, right,
-                c->comm, c->stream);
+  for (int k = 0; k < nops; k++) {
+    const int pl = ops[k][2] == MG_PLANE_FIRST  ? 1
+                   : ops[k][2] == MG_PLANE_LAST ? g.nxl
+                   : ops[k][2] == MG_GHOST_LO   ? 0
+                                                : g.nxl + 1;
+    double *buf = A + (long long)pl * g.plane;
+    if (ops[k][0] == MG_OP_SEND)
+      g_nccl.Send(buf, n, ncclDouble, ops[k][1], c->comm, c->stream);
+    else
+      g_nccl.Recv(buf, n, ncclDouble, ops[k][1], c->comm, c->stream);
+  }
   return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(halo)");
 }
 
@@ -760,6 +762,25 @@ const char *mg_strerror(int code) {
 }
 
 const char *mg_last_error(const mg_ctx *) { return g_err.c_str(); }
+
+int mg_halo_schedule(int nranks, int rank, int periodic_x, int ops[4][3]) {
+  if (nranks < 1 || rank < 0 || rank >= nranks || !ops) return MG_ERR_ARG;
+  const int left = rank > 0 ? rank - 1 : (periodic_x ? nranks - 1 : -1);
+  const int right = rank < nranks - 1 ? rank + 1 : (periodic_x ? 0 : -1);
+  int n = 0;
+  auto put = [&](int op, int peer, int plane) {
+    ops[n][0] = op;
+    ops[n][1] = peer;
+    ops[n][2] = plane;
+    n++;
+  };
+  if (nranks == 1) return 0;
+  if (right >= 0) put(MG_OP_SEND, right, MG_PLANE_LAST);
+  if (left >= 0) put(MG_OP_RECV, left, MG_GHOST_LO);
+  if (left >= 0) put(MG_OP_SEND, left, MG_PLANE_FIRST);
+  if (right >= 0) put(MG_OP_RECV, right, MG_GHOST_HI);
+  return n;
+}
 
 int mg_last_error_code(void) { return g_err_code; }
 

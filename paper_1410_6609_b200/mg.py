@@ -103,6 +103,7 @@ def lib():
         L.mg_strerror.argtypes = [i]
         L.mg_strerror.restype = ctypes.c_char_p
         L.mg_nccl_unique_id.argtypes = [ctypes.c_ubyte * 128]
+        L.mg_halo_schedule.argtypes = [i, i, i, ctypes.c_int * 12]
         L.mg_set_rhs_from_spheres.argtypes = [P, i, dp, dp, dp, i, i]
         L.mg_set_rhs.argtypes = [P, dp, i]
         L.mg_vcycle.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
@@ -138,6 +139,20 @@ def _check(rc, ctx=None):
         msg = lib().mg_last_error(ctx).decode()
         raise MGError(rc, msg)
     return rc
+
+
+MG_OP_SEND, MG_OP_RECV = 0, 1
+MG_PLANE_FIRST, MG_PLANE_LAST, MG_GHOST_LO, MG_GHOST_HI = 1, 2, 3, 4
+
+
+def halo_schedule(nranks: int, rank: int, periodic_x: bool):
+    """Ordered ghost-plane operations [(op, peer, plane), ...] the library
+    posts in one NCCL group on this rank (mg_halo_schedule; host logic)."""
+    ops = (ctypes.c_int * 12)()
+    n = lib().mg_halo_schedule(int(nranks), int(rank), 1 if periodic_x else 0, ops)
+    if n < 0:
+        raise MGError(n, "bad rank / nranks")
+    return [tuple(ops[3 * k:3 * k + 3]) for k in range(n)]
 
 
 def default_opts() -> mg_opts:
