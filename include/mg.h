@@ -239,6 +239,25 @@ int mg_coulomb_forces(mg_ctx *ctx, int n, const double *centers,
                       const double *radii, const double *charges,
                       int normalization, int subsample, double *forces_out);
 
+/* ---- time stepping ------------------------------------------- */
+/* The potential part of one time step of Alg.1 for spheres at
+ * their current positions: f := their charge density (exactly
+ * mg_set_rhs_from_spheres(normalization, subsample)); V-cycles from the
+ * current Phi (warm start: "later steps only update the previous solution",
+ * P:1321-1322) -- exactly `cycles` of them if cycles > 0 (the paper's
+ * regime: 5 V(3,3) at the first step, then 1), or, with cycles == 0, while
+ * ||f - A Phi||_2 > abs_tol (Alg.1 "while residual >= tol"; an
+ * absolute norm, as the paper monitors 1.5e-8), at most
+ * max_cycles; then, if forces_out != NULL, the Coulomb forces of the same
+ * spheres on the new Phi (mg_coulomb_forces with force_subsample; forces
+ * [3n]).  *cycles_out and *res_out (post-step residual norm) may be NULL.
+ * Returns MG_OK, MG_ERR_NOTCONV (cycles == 0 and max_cycles reached; forces
+ * are still computed), or the errors of the calls it makes. */
+int mg_timestep(mg_ctx *ctx, int n, const double *centers, const double *radii,
+                const double *charges, int normalization, int subsample,
+                int cycles, double abs_tol, double *forces_out,
+                int force_subsample, int *cycles_out, double *res_out);
+
 /* ---- solve --------------------------------------------------------------- */
 /* One V(nu1,nu2)-cycle; *res_norm_out (may be NULL) = ||f - A Phi||_2 over
  * all cells after the cycle (unscaled, reading c10).  Synchronises.

@@ -213,6 +213,8 @@ struct mg_ctx {
   size_t stage_bytes = 0;
   double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
+  double *fbuf = nullptr;      // force step: sphere list + partial sums
+  size_t fbuf_cap = 0;         // (doubles), grown on demand, kept
   unsigned long long *counts = nullptr;
   cudaGraphExec_t graph = nullptr;
   double prev_norm = -1.0;
@@ -977,6 +979,7 @@ void mg_destroy(mg_ctx *c) {
   if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
   if (c->stage) cudaFree(c->stage);
   if (c->sph) cudaFree(c->sph);
+  if (c->fbuf) cudaFree(c->fbuf);
   for (void *p : c->mask_bufs) cudaFree(p);
   if (c->h_norm) cudaFreeHost(c->h_norm);
   if (c->own_ws && c->ws) cudaFree(c->ws);
@@ -1020,6 +1023,7 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   }
   if ((size_t)n > c->sph_cap) {
     if (c->sph) cudaFree(c->sph);
+  if (c->fbuf) cudaFree(c->fbuf);
     c->sph = nullptr;
     c->sph_cap = 0;
     CK(cudaMalloc(&c->sph, sizeof(double) * 5 * (size_t)n + sizeof(unsigned long long) * (size_t)n));
@@ -1391,16 +1395,21 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
   const size_t ns = c->g[0].size();
   const size_t nrow = 3 * (size_t)n;
   // device: sphere list + per-slab partials (+ all-gathered partials)
-  double *buf = nullptr;
   const size_t nb = 5 * (size_t)n + nrow * (ns + (size_t)c->P);
-  CK(cudaMalloc(&buf, nb * sizeof(double)));
+  if (nb > c->fbuf_cap) {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->fbuf) cudaFree(c->fbuf);
+    c->fbuf = nullptr;
+    c->fbuf_cap = 0;
+    CK(cudaMalloc(&c->fbuf, nb * sizeof(double)));
+    c->fbuf_cap = nb;
+  }
+  double *buf = c->fbuf;
   double *dsph = buf, *dpart = buf + 5 * (size_t)n, *dall = dpart + nrow * ns;
   std::vector<double> hp;
   if (cudaMemcpyAsync(dsph, h5.data(), 5 * (size_t)n * sizeof(double),
-                      cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
-    cudaFree(buf);
+                      cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
     return fail(MG_ERR_CUDA, "copy of the sphere list failed");
-  }
   for (size_t s = 0; s < ns; s++)
     mg::launch_coulomb(c->g[0][s], c->dsolid, c->h, subsample, n, dsph,
                        normalization, dpart + nrow * s, c->stream);
@@ -1419,7 +1428,6 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
         cudaStreamSynchronize(c->stream) != cudaSuccess)
       rc = fail(MG_ERR_CUDA, "force readback failed");
   }
-  cudaFree(buf);
   if (rc) return rc;
   const double h3 = c->h * c->h * c->h;
   for (size_t r = 0; r < nrow; r++) {
@@ -1428,6 +1436,43 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
     forces_out[r] = -h3 * s;
   }
   return MG_OK;
+}
+
+int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
+                const double *charges, int normalization, int subsample,
+                int cycles, double abs_tol, double *forces_out,
+                int force_subsample, int *cycles_out, double *res_out) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (cycles < 0) return fail(MG_ERR_ARG, "cycles < 0");
+  if (cycles == 0 && !(abs_tol > 0.0))
+    return fail(MG_ERR_ARG, "cycles == 0 needs abs_tol > 0");
+  int rc = mg_set_rhs_from_spheres(c, n, centers, radii, charges,
+                                   normalization, subsample);
+  if (rc) return rc;
+  int k = 0;
+  double r = -1.0;
+  if (cycles > 0) {
+    for (; k < cycles; k++)
+      if ((rc = mg_vcycle(c, &r))) break;
+  } else {  // Alg.1: while residual >= tol, perform a V-cycle
+    if ((rc = residual_norm_now(c, &r))) return rc;
+    c->prev_norm = r;
+    while (r > abs_tol && k < c->o.max_cycles) {
+      k++;
+      if ((rc = mg_vcycle(c, &r))) break;
+    }
+    if (!rc && r > abs_tol)
+      rc = fail(MG_ERR_NOTCONV, "residual %g > %g after %d cycles", r, abs_tol, k);
+  }
+  if (cycles_out) *cycles_out = k;
+  if (res_out) *res_out = r;
+  if (rc && rc != MG_ERR_NOTCONV) return rc;
+  if (forces_out) {
+    const int frc = mg_coulomb_forces(c, n, centers, radii, charges,
+                                      normalization, force_subsample, forces_out);
+    if (frc) return frc;
+  }
+  return rc;
 }
 
 int mg_get_stencil(mg_ctx *c, int l, double *out, int where) {

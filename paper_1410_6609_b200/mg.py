@@ -124,6 +124,8 @@ def lib():
         L.mg_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.mg_set_face_values.argtypes = [P, i, dp]
         L.mg_coulomb_forces.argtypes = [P, i, dp, dp, dp, i, i, dp]
+        L.mg_timestep.argtypes = [P, i, dp, dp, dp, i, i, i, d, dp, i, ip,
+                                  ctypes.POINTER(ctypes.c_double)]
         L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
@@ -319,6 +321,29 @@ class Multigrid:
                                        _host_ptr(r), _host_ptr(q), normalization,
                                        subsample, _host_ptr(out)), self._ctx)
         return out.reshape(-1, 3)
+
+    def timestep(self, centers, radii, charges, cycles=1, abs_tol=0.0,
+                 normalization=MG_CHARGE_PER_CELLS, subsample=1, forces=True,
+                 force_subsample=None, raise_notconv=True):
+        """One time step of Alg.1's potential part (mg_timestep): RHS from
+        the spheres, `cycles` warm-started V-cycles (or, cycles=0, cycles
+        until ||r|| <= abs_tol), then the Coulomb forces.  Returns
+        (forces (n, 3) or None, cycles run, final residual norm)."""
+        c = np.ascontiguousarray(centers, np.float64).reshape(-1)
+        r = np.ascontiguousarray(radii, np.float64)
+        q = np.ascontiguousarray(charges, np.float64)
+        out = np.empty(3 * len(r), np.float64) if forces else None
+        cyc = ctypes.c_int(0)
+        res = ctypes.c_double(0.0)
+        fs = subsample if force_subsample is None else force_subsample
+        rc = lib().mg_timestep(self._ctx, len(r), _host_ptr(c), _host_ptr(r),
+                               _host_ptr(q), normalization, subsample,
+                               int(cycles), float(abs_tol),
+                               _host_ptr(out) if forces else None, int(fs),
+                               ctypes.byref(cyc), ctypes.byref(res))
+        if rc != MG_OK and (rc != MG_ERR_NOTCONV or raise_notconv):
+            _check(rc, self._ctx)
+        return (out.reshape(-1, 3) if forces else None), cyc.value, res.value
 
     def get_solution(self, out=None):
         if out is None:

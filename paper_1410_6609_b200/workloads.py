@@ -18,6 +18,7 @@ import numpy as np
 
 DIRICHLET = 0
 NEUMANN = 1
+PERIODIC = 2
 
 
 @dataclasses.dataclass
@@ -120,6 +121,51 @@ def random_spheres(extent, radius: float, n: int, seed: int,
         k += 1
     charges = rng.choice(np.array([-1.0, 1.0]), size=n)
     return out, charges
+
+
+def periodic_channel_bc(phi_top: float = 1.0):
+    """The config-2/4 channel with periodic flow (x) and span (z) axes
+    (P:441-443): Dirichlet 0 / phi_top on the y walls."""
+    return ([PERIODIC, PERIODIC, DIRICHLET, DIRICHLET, PERIODIC, PERIODIC],
+            [0.0, 0.0, 0.0, phi_top, 0.0, 0.0])
+
+
+def move_spheres(centers, radii, extent, step: int, seed: int = 0,
+                 amplitude: float = 0.05, periodic=(False, False, False)):
+    """Synthetic particle motion of the time-stepping regime (SURVEY 8(f)
+    N3).  In the paper the spheres move under the LBM / pe coupling of
+    Alg.1 (out of scope here); this generator only supplies positions:
+    step `step` displaces every centre by a vector with components drawn
+    from U[-amplitude, amplitude] (default_rng((seed, step))), then reflects
+    it into [R, L - R] on wall axes or wraps it into [0, L) on periodic
+    axes.  Deterministic per (seed, step); overlaps are not prevented
+    (charge densities of overlapping spheres add, mg.h)."""
+    c = np.array(centers, np.float64, copy=True)
+    R = np.asarray(radii, np.float64)
+    L = np.asarray(extent, np.float64)
+    rng = np.random.default_rng((int(seed), int(step)))
+    c += rng.uniform(-amplitude, amplitude, c.shape)
+    for a in range(3):
+        if periodic[a]:
+            c[:, a] = np.mod(c[:, a], L[a])
+            c[c[:, a] >= L[a], a] = 0.0
+        else:
+            lo, hi = R, L[a] - R
+            c[:, a] = np.where(c[:, a] < lo, 2 * lo - c[:, a], c[:, a])
+            c[:, a] = np.where(c[:, a] > hi, 2 * hi - c[:, a], c[:, a])
+    return c
+
+
+def timestep_workload(n: int = 512, seed: int = 0) -> Workload:
+    """The paper's scaling regime on config 4's single-GPU
+    box: 512^3 channel, spheres R = 6 at 5 % volume (cfg4), RHS and force
+    subsampling factor 2, V(3,3)-cycles, coarsest 8^3; 5 cycles at
+    the first time step, then 1 per step."""
+    w = cfg4(P=1, n=n, seed=seed)
+    w.name = "timestep_%d" % n
+    w.nu1 = w.nu2 = 3
+    w.cycles = 1
+    return w
 
 
 def cfg1(n: int = 32, cycles: int = 10) -> Workload:

@@ -111,3 +111,23 @@ def test_nccl_unique_id_on_cpu():
     except mg.MGError as e:
         pytest.skip("libnccl not loadable here: %s" % e)
     assert len(uid) == 128 and any(uid)
+
+
+def test_move_spheres_generator():
+    """Synthetic motion for the time-stepping regime: deterministic per
+    (seed, step), bounded displacement, reflected into [R, L-R] on wall axes,
+    wrapped into [0, L) on periodic axes."""
+    from paper_1410_6609_b200 import workloads as W
+    w = W.timestep_workload(n=64, seed=1)
+    L = np.array(w.shape, float)
+    a = W.move_spheres(w.centers, w.radii, L, 3, seed=9, amplitude=0.5)
+    b = W.move_spheres(w.centers, w.radii, L, 3, seed=9, amplitude=0.5)
+    assert np.array_equal(a, b)
+    assert not np.array_equal(a, W.move_spheres(w.centers, w.radii, L, 4, seed=9))
+    assert np.abs(a - w.centers).max() <= 0.5 + 1e-12
+    R = w.radii[:, None]
+    assert np.all(a >= R) and np.all(a <= L - R)
+    c = np.array([[0.1, 32.0, 63.95]])
+    p = W.move_spheres(c, [6.0], L, 1, seed=0, amplitude=0.2,
+                       periodic=(True, False, True))
+    assert np.all((p[:, [0, 2]] >= 0) & (p[:, [0, 2]] < L[[0, 2]]))

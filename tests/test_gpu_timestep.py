@@ -1,0 +1,131 @@
+"""Time-stepping regime (Alg.1)
+through the C-ABI's mg_timestep, against the oracle doing the same steps:
+RHS from the moved spheres (subsampling 2), warm-started V(3,3)
+cycles (5 at the first step, then 1), Coulomb forces.
+
+Per step: residual within the history clause of test_gpu_parity.py, Phi
+rel-L2 <= 1e-10, forces rel 1e-9 (they are sums over the solved Phi, which
+agrees to ~1e-13; the force sums differ only in order).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_6609_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_6609_b200 import _build
+    _build.build()
+    from paper_1410_6609_b200 import mg as M
+    return M
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def run_steps(mg, w, steps, periodic=(False, False, False), sub=2,
+              amplitude=0.3):
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value,
+                     min_coarse=w.min_coarse, nu1=3, nu2=3)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value,
+                      min_coarse=w.min_coarse, nu1=3, nu2=3)
+    c = w.centers
+    out = []
+    for k in range(steps):
+        if k:
+            c = W.move_spheres(c, w.radii, np.array(w.shape) * w.h, k,
+                               seed=7, amplitude=amplitude, periodic=periodic)
+        cyc = 5 if k == 0 else 1
+        Fg, ncyc, rg = s.timestep(c, w.radii, w.charges, cycles=cyc,
+                                  subsample=sub)
+        o.set_rhs_from_spheres(c, w.radii, w.charges, subsample=sub)
+        ro = None
+        for _ in range(cyc):
+            ro = o.vcycle()
+        Fo = o.coulomb_forces(c, w.radii, w.charges, subsample=sub)
+        out.append((ncyc, rg, ro, Fg, Fo, s.get_solution(), o.phi()))
+    return out
+
+
+def test_timestep_parity_channel(mg):
+    w = W.timestep_workload(n=64, seed=1)
+    assert len(w.radii) == 14
+    res = run_steps(mg, w, 5)
+    r0 = res[0][2]
+    for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
+        assert ncyc == (5 if k == 0 else 1)
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (k, rg, ro)
+        assert rel(pg, po) <= 1e-10
+        assert np.abs(Fo).max() > 0
+        assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
+    # warm start: one V(3,3) per step keeps the residual near the first
+    # solve's level while the spheres move
+    assert max(r[1] for r in res[1:]) < 50 * res[0][1]
+
+
+def test_timestep_parity_periodic_channel(mg):
+    """Periodic flow / span axes: moving spheres wrap around (images)."""
+    w = W.timestep_workload(n=64, seed=2)
+    w.bc_type, w.bc_value = W.periodic_channel_bc(1.0)
+    c = w.centers.copy()
+    c[0] = [0.4, 20.0, 63.7]            # straddles the x and z faces
+    w.centers = c
+    res = run_steps(mg, w, 4, periodic=(True, False, True), amplitude=0.8)
+    r0 = res[0][2]
+    for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (k, rg, ro)
+        assert rel(pg, po) <= 1e-10
+        assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
+
+
+def test_timestep_tolerance_mode(mg):
+    """cycles = 0: V-cycles while ||r|| > abs_tol (Alg.1), the
+    same count as the oracle's loop."""
+    w = W.timestep_workload(n=64, seed=3)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8,
+                     nu1=3, nu2=3)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8,
+                      nu1=3, nu2=3)
+    tol = 1.5e-8     # the paper's monitored bound
+    c = w.centers
+    r0 = None
+    for k in range(3):
+        if k:
+            c = W.move_spheres(c, w.radii, np.array(w.shape), k, seed=4,
+                               amplitude=0.5)
+        _, ncyc, rg = s.timestep(c, w.radii, w.charges, cycles=0, abs_tol=tol,
+                                 subsample=2, forces=False)
+        o.set_rhs_from_spheres(c, w.radii, w.charges, subsample=2)
+        r = o.residual_norm()
+        r0 = r if r0 is None else r0     # floor clause scale (reading c21)
+        n = 0
+        while r > tol:
+            r = o.vcycle()
+            n += 1
+        assert ncyc == n and rg <= tol
+        assert abs(rg - r) <= 1e-8 * r + 1e-14 * r0
+
+
+def test_timestep_errors(mg):
+    w = W.timestep_workload(n=32, seed=0)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4)
+    with pytest.raises(mg.MGError) as e:
+        s.timestep(w.centers, w.radii, w.charges, cycles=-1)
+    assert e.value.code == mg.MG_ERR_ARG
+    with pytest.raises(mg.MGError) as e:
+        s.timestep(w.centers, w.radii, w.charges, cycles=0, abs_tol=0.0)
+    assert e.value.code == mg.MG_ERR_ARG
+    # an unreachable tolerance: NOTCONV, forces still returned on request
+    s2 = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4,
+                      max_cycles=2)
+    F, n, r = s2.timestep(w.centers, w.radii, w.charges, cycles=0,
+                          abs_tol=1e-300, raise_notconv=False)
+    assert n == 2 and F.shape == (len(w.radii), 3)
