@@ -131,6 +131,65 @@ def cpu_baseline(n_sample=256, cycles=2):
                       "OpenMP threads=%d" % (n_sample, n_sample, cycles, cores)}
 
 
+def timestep_regime(mg, W, stream, local, steps=10, warm=2):
+    """The paper's own use of the solver (Alg.1): per time step
+    the spheres move, f is re-set from them (subsampling 2), one
+    warm-started V(3,3)-cycle updates Phi (5 at the first step)
+    and the Coulomb forces are computed (Eq.14-15) -- one mg_timestep call.
+    Metric: the paper's MLUPS, cells whose Poisson problem is solved per
+    second.  Positions are generated before the timed region
+    (they stand in for the LBM / pe motion, which is out of scope)."""
+    import torch
+    w = W.timestep_workload(n=512, seed=0)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, device=local,
+                     stream=stream, min_coarse=8, nu1=3, nu2=3)
+    L = np.array(w.shape) * w.h
+    pos = [w.centers]
+    for k in range(1, steps + warm + 1):
+        pos.append(W.move_spheres(pos[-1], w.radii, L, k, seed=0, amplitude=0.005))
+    s.timestep(pos[0], w.radii, w.charges, cycles=5, subsample=2)  # first step
+    for k in range(1, warm + 1):
+        s.timestep(pos[k], w.radii, w.charges, cycles=1, subsample=2)
+    torch.cuda.synchronize()
+    a = torch.cuda.Event(enable_timing=True)
+    b = torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    res = []
+    for k in range(warm + 1, warm + 1 + steps):
+        _, _, r = s.timestep(pos[k], w.radii, w.charges, cycles=1, subsample=2)
+        res.append(r)
+    b.record(stream)
+    torch.cuda.synchronize()
+    ms = a.elapsed_time(b) / steps
+    # breakdown of one step: RHS, V(3,3)-cycle (incl. norm), forces
+    parts = {"rhs_ms": [], "vcycle_ms": [], "forces_ms": []}
+    for k in range(warm + 1, warm + 4):
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ev[0].record(stream)
+        s.set_rhs_from_spheres(pos[k], w.radii, w.charges, subsample=2)
+        ev[1].record(stream)
+        s.vcycle()
+        ev[2].record(stream)
+        s.coulomb_forces(pos[k], w.radii, w.charges, subsample=2)
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        for i, key in enumerate(parts):
+            parts[key].append(ev[i].elapsed_time(ev[i + 1]))
+    s.close()
+    cells = w.cells
+    return {"metric": "MLUPS per time step (paper's MG metric, P:1303-1306)",
+            "value": round(cells / (ms * 1e-3) / 1e6, 1), "unit": "MLUPS",
+            "ms_per_step": round(ms, 3), "steps": steps,
+            "step": "mg_timestep: f from %d moved spheres R=6 (s_f=2) + 1 V(3,3)-"
+                    "cycle (warm start) + residual norm + Coulomb forces (s_f=2)"
+                    % len(w.radii),
+            "workload": "cfg4 box 512^3, channel BCs, 5%% spheres, 7 levels",
+            "residual_mean": float(np.mean(res)), "residual_max": float(np.max(res)),
+            "breakdown_ms": {k: round(float(np.mean(v)), 3) for k, v in parts.items()},
+            "paper_context": "91.8 MLUPS per SuperMUC node, 16 Sandy Bridge cores "
+                             "(P:1346); context only"}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -348,12 +407,17 @@ def run_cuda(args):
         "e2e": e2e,
         "final_residual": norms[-1] if norms else None,
     }
+    s.close()
+    if N == 1 and workload == "cfg3" and not args.no_ts:
+        try:
+            line["timestep_regime"] = timestep_regime(mg, W, stream, local)
+        except Exception as ex:  # reported, never fatal
+            line["timestep_regime"] = {"error": repr(ex)}
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.cpu_size)
         except Exception as ex:  # reported, never fatal
             line["cpu_baseline"] = {"error": repr(ex)}
-    s.close()
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
@@ -374,6 +438,8 @@ def main():
     ap.add_argument("--ref-size", type=int, default=128)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-ts", action="store_true",
+                    help="skip the time-stepping regime measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

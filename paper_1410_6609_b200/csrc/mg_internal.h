@@ -75,19 +75,27 @@ __device__ __forceinline__ void ghost_copies(const Grid &g, double *arr, int il,
 // other-colour z neighbours of the own cells at half-indices k, k+1 of a row
 // (red cells at z = 2k + p): zm0 = z-1 of the first, zp1 = z+1 of the second;
 // the others are the row's entries k and k+1.  Outside the level: 0 (folded
-// boundary) or, on a periodic z axis, the opposite end of the row.
+// boundary) or, on a periodic z axis, the opposite end of the row.  PER is a
+// compile-time switch: box-domain kernels carry no periodic logic at all.
+template <bool PER>
 __device__ __forceinline__ double z_lo(const Grid &g, const double *row, int k) {
-  return (k > 0) ? row[k - 1] : (g.per[2] ? row[g.nzh - 1] : 0.0);
+  return (k > 0) ? row[k - 1] : ((PER && g.per[2]) ? row[g.nzh - 1] : 0.0);
 }
+template <bool PER>
 __device__ __forceinline__ double z_hi(const Grid &g, const double *row, int k) {
-  return (k + 2 < g.nzh) ? row[k + 2] : (g.per[2] ? row[0] : 0.0);
+  return (k + 2 < g.nzh) ? row[k + 2] : ((PER && g.per[2]) ? row[0] : 0.0);
 }
 // z+1 of the FIRST own cell (p = 1) is the entry k+1; when k is the row's
 // last half-index (odd nzh) that entry is padding (0, the folded boundary),
 // and on a periodic z axis it is the row's first entry instead
+template <bool PER>
 __device__ __forceinline__ double z_hi0(const Grid &g, const double *row, int k,
                                         double next) {
-  return (g.per[2] && k + 1 >= g.nzh) ? row[0] : next;
+  return (PER && g.per[2] && k + 1 >= g.nzh) ? row[0] : next;
+}
+
+__host__ __device__ inline bool is_periodic(const Grid &g) {
+  return g.per[0] || g.per[1] || g.per[2];
 }
 
 // ---- kernel launchers (mg_kernels.cu) ---------------------------------------

@@ -12,6 +12,8 @@
 // Hence no stencil is stored: the centre comes from the cell position.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "mg_internal.h"
 
 namespace mg {
@@ -46,6 +48,7 @@ __device__ __forceinline__ double2 ld2(const double *p) {
 // c_l is a power of two.  The other colour's x/y neighbours share
 // the half-index k; the z neighbours are O(k-1+p), O(k+p), p = z & 1.
 // ---------------------------------------------------------------------------
+template <bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_smooth(Grid g, int color, int from_zero) {
   const int nk2 = (g.nzh + 1) >> 1;  // odd nzh: the last pair is half used
@@ -76,15 +79,15 @@ __global__ void __launch_bounds__(kThreads)
     const double2 zc = ld2(oth + b + k);
     double zm0, zp0, zm1, zp1;
     if (p == 0) {
-      zm0 = z_lo(g, oth + b, k);
+      zm0 = z_lo<PER>(g, oth + b, k);
       zp0 = zc.x;
       zm1 = zc.x;
       zp1 = zc.y;
     } else {
       zm0 = zc.x;
-      zp0 = z_hi0(g, oth + b, k, zc.y);
+      zp0 = z_hi0<PER>(g, oth + b, k, zc.y);
       zm1 = zc.y;
-      zp1 = z_hi(g, oth + b, k);
+      zp1 = z_hi<PER>(g, oth + b, k);
     }
     s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
     s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
@@ -97,10 +100,10 @@ __global__ void __launch_bounds__(kThreads)
   out.y = (fo.y * g.w + s1) / d1;
   if (k + 1 < g.nzh) {
     *reinterpret_cast<double2 *>(own + b + k) = out;
-    ghost_copies(g, own, il, j, k, out);
+    if (PER) ghost_copies(g, own, il, j, k, out);
   } else {
     own[b + k] = out.x;
-    ghost_copies(g, own, il, j, k, out.x);
+    if (PER) ghost_copies(g, own, il, j, k, out.x);
   }
 }
 
@@ -108,11 +111,15 @@ void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * ((g.nzh + 1) >> 1);
   if (total <= 0) return;
   const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
-  k_smooth<<<blocks, kThreads, 0, s>>>(g, color, from_zero);
+  if (is_periodic(g))
+    k_smooth<true><<<blocks, kThreads, 0, s>>>(g, color, from_zero);
+  else
+    k_smooth<false><<<blocks, kThreads, 0, s>>>(g, color, from_zero);
 }
 
 // residual r = f - c (d Phi - s) at (il, j, z) of a grid: the oracle's
 // f - (a_cc Phi + sum_q a_q Phi_q) with the same roundings
+template <bool PER>
 __device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
                                            int z) {
   const int i = g.x0 + il;
@@ -125,8 +132,8 @@ __device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
   const long long b = rowbase(g, il, j);
   // z-1 / z+1 are the other colour's half-indices k-1+p / k+p; on a
   // periodic z axis z = -1 / nz wrap to nz-1 / 0 (half-indices nzh-1 / 0)
-  const double zm = (z > 0) ? oth[b + k - 1 + p] : (g.per[2] ? oth[b + g.nzh - 1] : 0.0);
-  const double zp = (z < g.nz - 1) ? oth[b + k + p] : (g.per[2] ? oth[b] : 0.0);
+  const double zm = (z > 0) ? oth[b + k - 1 + p] : ((PER && g.per[2]) ? oth[b + g.nzh - 1] : 0.0);
+  const double zp = (z < g.nz - 1) ? oth[b + k + p] : ((PER && g.per[2]) ? oth[b] : 0.0);
   const double s = ((((oth[b - g.plane + k] + oth[b + g.plane + k]) +
                       oth[b - g.pz + k]) +
                      oth[b + g.pz + k]) +
@@ -142,6 +149,7 @@ __device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
 // residuals of C's 8 children, child bits (dx,dy,dz), dz fastest.  The fine
 // residual is never stored.  One thread per coarse cell.
 // ---------------------------------------------------------------------------
+template <bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_resid_restrict(Grid F, Grid C) {
   const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
@@ -159,7 +167,7 @@ __global__ void __launch_bounds__(kThreads)
     for (int b = 0; b < 2; b++)
 #pragma unroll
       for (int c = 0; c < 2; c++)
-        r[a * 4 + b * 2 + c] = resid_at(F, 2 * Il + a, 2 * J + b, 2 * K + c);
+        r[a * 4 + b * 2 + c] = resid_at<PER>(F, 2 * Il + a, 2 * J + b, 2 * K + c);
   const double s = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
   const int Ig = (F.x0 >> 1) + Il;
   const int col = (Ig + J + K) & 1;
@@ -173,7 +181,10 @@ void launch_resid_restrict(const Grid &f, const Grid &c, int /*cofs*/,
       (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
   if (total <= 0) return;
   const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
-  k_resid_restrict<<<blocks, kThreads, 0, s>>>(f, c);
+  if (is_periodic(f))
+    k_resid_restrict<true><<<blocks, kThreads, 0, s>>>(f, c);
+  else
+    k_resid_restrict<false><<<blocks, kThreads, 0, s>>>(f, c);
 }
 
 // ---------------------------------------------------------------------------
@@ -234,6 +245,7 @@ static constexpr int kNormBlocks = 148 * 8;
 
 // residual of the two cells of colour `col` at half-indices k, k+1 of row
 // (il, j): same expression as resid_at, vectorised along the row
+template <bool PER>
 __device__ __forceinline__ void resid_pair(const Grid &g, int il, int j, int k,
                                            int col, double &r0, double &r1) {
   const int i = g.x0 + il;
@@ -251,15 +263,15 @@ __device__ __forceinline__ void resid_pair(const Grid &g, int il, int j, int k,
   const double2 fo = ld2(f + b + k);
   double zm0, zp0, zm1, zp1;
   if (p == 0) {
-    zm0 = z_lo(g, oth + b, k);
+    zm0 = z_lo<PER>(g, oth + b, k);
     zp0 = zc.x;
     zm1 = zc.x;
     zp1 = zc.y;
   } else {
     zm0 = zc.x;
-    zp0 = z_hi0(g, oth + b, k, zc.y);
+    zp0 = z_hi0<PER>(g, oth + b, k, zc.y);
     zm1 = zc.y;
-    zp1 = z_hi(g, oth + b, k);
+    zp1 = z_hi<PER>(g, oth + b, k);
   }
   const double s0 = ((((xm.x + xp.x) + ym.x) + yp.x) + zm0) + zp0;
   const double s1 = ((((xm.y + xp.y) + ym.y) + yp.y) + zm1) + zp1;
@@ -273,6 +285,7 @@ __device__ __forceinline__ void resid_pair(const Grid &g, int il, int j, int k,
 }
 
 // one thread per (row, double2 position), both colours: 4 cells
+template <bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_norm_partials(Grid g, double *partials) {
   __shared__ double sh[32];
@@ -286,8 +299,8 @@ __global__ void __launch_bounds__(kThreads)
     const int j = (int)(r % g.ny);
     const int il = (int)(r / g.ny);
     double a0, a1, b0, b1;
-    resid_pair(g, il, j, 2 * k2, 0, a0, a1);
-    resid_pair(g, il, j, 2 * k2, 1, b0, b1);
+    resid_pair<PER>(g, il, j, 2 * k2, 0, a0, a1);
+    resid_pair<PER>(g, il, j, 2 * k2, 1, b0, b1);
     acc = acc + a0 * a0;
     acc = acc + a1 * a1;
     acc = acc + b0 * b0;
@@ -302,7 +315,10 @@ int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s) {
   long long nb = (total + kThreads - 1) / kThreads;
   if (nb > kNormBlocks) nb = kNormBlocks;
   if (nb < 1) nb = 1;
-  k_norm_partials<<<(unsigned)nb, kThreads, 0, s>>>(g, partials);
+  if (is_periodic(g))
+    k_norm_partials<true><<<(unsigned)nb, kThreads, 0, s>>>(g, partials);
+  else
+    k_norm_partials<false><<<(unsigned)nb, kThreads, 0, s>>>(g, partials);
   return (int)nb;
 }
 
@@ -349,8 +365,10 @@ __device__ __forceinline__ double cg_allsum(double v, double *part) {
   return s;
 }
 
+template <bool PER>
 __global__ void __launch_bounds__(kCgThreads)
     k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
+  using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
   extern __shared__ double cg_sm[];
   __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
@@ -361,7 +379,7 @@ __global__ void __launch_bounds__(kCgThreads)
   // bits 0-5 neighbour inside the level, bits 6-11 neighbour across a
   // periodic face (the opposite side's cell); and the centre d
   // (closed-form operator A = c (d - neighbours))
-  unsigned short *nb = reinterpret_cast<unsigned short *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
+  NB *nb = reinterpret_cast<NB *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
   signed char *dc = reinterpret_cast<signed char *>(nb + N);
   const long long sx = (long long)g.ny * g.nz, sy = g.nz;
   const long long wx = (long long)(g.nx - 1) * sx, wy = (long long)(g.ny - 1) * sy,
@@ -376,8 +394,8 @@ __global__ void __launch_bounds__(kCgThreads)
     unsigned m = 0;
 #pragma unroll
     for (int q = 0; q < 6; q++)
-      m |= in[q] ? (1u << q) : (g.per[q >> 1] ? (64u << q) : 0u);
-    nb[n] = (unsigned short)m;
+      m |= in[q] ? (1u << q) : ((PER && g.per[q >> 1]) ? (64u << q) : 0u);
+    nb[n] = (NB)m;
     dc[n] = (signed char)centre_d(g, i, j, z);
     int col;
     const long long idx = split_index(g, i, j, z, &col);
@@ -397,12 +415,12 @@ __global__ void __launch_bounds__(kCgThreads)
       acc = 0.0;
       for (long long n = threadIdx.x; n < N; n += blockDim.x) {
         const unsigned m = nb[n];
-        const double xm = (m & 1) ? p[n - sx] : ((m & 64) ? p[n + wx] : 0.0);
-        const double xp = (m & 2) ? p[n + sx] : ((m & 128) ? p[n - wx] : 0.0);
-        const double ym = (m & 4) ? p[n - sy] : ((m & 256) ? p[n + wy] : 0.0);
-        const double yp = (m & 8) ? p[n + sy] : ((m & 512) ? p[n - wy] : 0.0);
-        const double zm = (m & 16) ? p[n - 1] : ((m & 1024) ? p[n + wz] : 0.0);
-        const double zp = (m & 32) ? p[n + 1] : ((m & 2048) ? p[n - wz] : 0.0);
+        const double xm = (m & 1) ? p[n - sx] : ((PER && (m & 64)) ? p[n + wx] : 0.0);
+        const double xp = (m & 2) ? p[n + sx] : ((PER && (m & 128)) ? p[n - wx] : 0.0);
+        const double ym = (m & 4) ? p[n - sy] : ((PER && (m & 256)) ? p[n + wy] : 0.0);
+        const double yp = (m & 8) ? p[n + sy] : ((PER && (m & 512)) ? p[n - wy] : 0.0);
+        const double zm = (m & 16) ? p[n - 1] : ((PER && (m & 1024)) ? p[n + wz] : 0.0);
+        const double zp = (m & 32) ? p[n + 1] : ((PER && (m & 2048)) ? p[n - wz] : 0.0);
         const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
         const double pn = p[n];
         const double qn = c * ((double)dc[n] * pn - s);
@@ -445,7 +463,8 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
   return 5 * (size_t)g.nx * g.ny * g.nz;
 }
 
-void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
+template <bool PER>
+static void launch_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
   // 256 threads: enough for <= 16 elements per thread at the coarsest sizes,
@@ -454,15 +473,24 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
   if (threads > 256) threads = 256;
   size_t smem = 0;
   if (N <= kCgSmemMax) {
-    smem = 4 * (size_t)N * sizeof(double) + 3 * (size_t)N;
+    // x, r, p, q + neighbour bits (1 byte; 2 with periodic wrap) + centre
+    smem = 4 * (size_t)N * sizeof(double) + (PER ? 3 : 2) * (size_t)N;
     static size_t configured = 48 * 1024;
     if (smem > configured) {
-      cudaFuncSetAttribute(k_coarse_cg, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)smem);
+      cudaFuncSetAttribute(k_coarse_cg<PER>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured = smem;
     }
   }
-  k_coarse_cg<<<1, threads, smem, s>>>(g, scratch, tol, maxit, iters_out);
+  k_coarse_cg<PER><<<1, threads, smem, s>>>(g, scratch, tol, maxit, iters_out);
+}
+
+void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
+                      int *iters_out, cudaStream_t s) {
+  if (is_periodic(g))
+    launch_cg<true>(g, scratch, tol, maxit, iters_out, s);
+  else
+    launch_cg<false>(g, scratch, tol, maxit, iters_out, s);
 }
 
 // ---------------------------------------------------------------------------

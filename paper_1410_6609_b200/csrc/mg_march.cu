@@ -34,10 +34,16 @@ namespace mg {
 // half-sweep (optionally fused with the prolongation of the other colour)
 // one TMA box = (pz doubles) x (TY+2 rows) x (1 plane)
 // ============================================================================
-template <bool PROLONG, int NCH, bool MASK>
+// VAR: 0 box domain, 1 solid mask (byte codes), 2 periodic axes -- compile-
+// time variants, so the box-domain kernel carries neither code path
+enum { VAR_BOX = 0, VAR_MASK = 1, VAR_PER = 2 };
+
+template <bool PROLONG, int NCH, int VAR>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
                    int color, Grid C, double alpha) {
+  constexpr bool MASK = VAR == VAR_MASK;
+  constexpr bool PER = VAR == VAR_PER;
   extern __shared__ __align__(128) unsigned char smem[];
   const int pz = g.pz;
   const int sd = slot_doubles(pz);
@@ -97,7 +103,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     // rows of the level, plus (y periodic) the ghost rows -1 / ny that hold
     // the opposite side's cells and need their parents' correction too
     tOk[m] = PROLONG && t < ntask && k < g.nzh &&
-             (g.per[1] ? (jj >= -1 && jj <= g.ny) : (jj >= 0 && jj < g.ny));
+             ((PER && g.per[1]) ? (jj >= -1 && jj <= g.ny) : (jj >= 0 && jj < g.ny));
     tRow[m] = rr * pz;
     tK[m] = k;
     const int J = jj >> 1;
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     const int i = g.x0 + i0 - 1 + q;
     // x periodic: ghost planes -1 / nx hold the opposite side's cells, their
     // parents sit in the coarse ghost planes (I = -1 / nx/2), kept current
-    const bool pok = g.per[0] || (i >= 0 && i < g.nx);
+    const bool pok = (PER && g.per[0]) || (i >= 0 && i < g.nx);
     const int I = i >> 1;
     const long long poff = (long long)(I - C.x0 + 1) * C.plane;
     const int Ip = I & 1;
@@ -134,7 +140,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   };
   auto apply_e = [&](int q, const double2 *E) {
     const int i = g.x0 + i0 - 1 + q;
-    if (!g.per[0] && (i < 0 || i >= g.nx)) return;  // physical ghost: stays 0
+    if (!(PER && g.per[0]) && (i < 0 || i >= g.nx)) return;  // physical ghost: 0
     double *slot = ring + (size_t)(q % kSlots) * sd;
 #pragma unroll
     for (int m = 0; m < kTPW; m++) {
@@ -228,15 +234,15 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const double2 zc = lds2(cur + k);
         double zm0, zp0, zm1, zp1;
         if (p == 0) {
-          zm0 = z_lo(g, cur, k);
+          zm0 = z_lo<PER>(g, cur, k);
           zp0 = zc.x;
           zm1 = zc.x;
           zp1 = zc.y;
         } else {
           zm0 = zc.x;
-          zp0 = z_hi0(g, cur, k, zc.y);
+          zp0 = z_hi0<PER>(g, cur, k, zc.y);
           zm1 = zc.y;
-          zp1 = z_hi(g, cur, k);
+          zp1 = z_hi<PER>(g, cur, k);
         }
         const int z0 = 2 * k + p;
         double s0, s1, d0, d1;
@@ -261,11 +267,11 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
         if (both) {
           *reinterpret_cast<double2 *>(orow + k) = out;
-          if (!MASK) ghost_copies(g, own, il, j, k, out);
+          if (PER) ghost_copies(g, own, il, j, k, out);
         } else {  // ragged row end or a solid cell (not an unknown: untouched)
           if (cd0 & 64) orow[k] = out.x;
           if (k + 1 < g.nzh && (cd1 & 64)) orow[k + 1] = out.y;
-          if (!MASK) ghost_copies(g, own, il, j, k, out.x);
+          if (PER) ghost_copies(g, own, il, j, k, out.x);
         }
       }
     }
@@ -283,11 +289,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
 // ============================================================================
 enum { MODE_RESTRICT = 0, MODE_NORM = 1 };
 
-template <int MODE, bool MASK>
+template <int MODE, int VAR>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_resid_march(Grid g, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmB, Grid C,
                   double *partials) {
+  constexpr bool MASK = VAR == VAR_MASK;
+  constexpr bool PER = VAR == VAR_PER;
   extern __shared__ __align__(128) unsigned char smem[];
   const int W = rbox0(g);  // smem row width = TMA box width
   const int sd = rslot_doubles();
@@ -412,18 +420,19 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           // periodic z axis the row's opposite end (not in this z-tile: a
           // direct load of the other colour, unchanged during this kernel)
           double zm0, zp0, zm1, zp1;
+          const bool zper = PER && g.per[2];
           const double *Og = (col ? g.phiR : g.phiB) +
                              (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
           if (p == 0) {
-            zm0 = (k > 0) ? O[oc + kl - 1] : (g.per[2] ? Og[g.nzh - 1] : 0.0);
+            zm0 = (k > 0) ? O[oc + kl - 1] : (zper ? Og[g.nzh - 1] : 0.0);
             zp0 = zc.x;
             zm1 = zc.x;
             zp1 = zc.y;
           } else {
             zm0 = zc.x;
-            zp0 = (g.per[2] && k + 1 >= g.nzh) ? Og[0] : zc.y;
+            zp0 = (zper && k + 1 >= g.nzh) ? Og[0] : zc.y;
             zm1 = zc.y;
-            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : (g.per[2] ? Og[0] : 0.0);
+            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : (zper ? Og[0] : 0.0);
           }
           const int z0 = 2 * k + p;
           double s0, s1, d0, d1;
@@ -612,7 +621,7 @@ static void set_smem(K kernel, size_t bytes, size_t *configured) {
   }
 }
 
-template <bool P, int NCH, bool M>
+template <bool P, int NCH, int M>
 static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
                       int color, double alpha, cudaStream_t s) {
   const int nrt = (g.ny + kTY - 1) / kTY;
@@ -624,7 +633,7 @@ static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
   k_smooth_march<P, NCH, M><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
 }
 
-template <bool P, bool M>
+template <bool P, int M>
 static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
                         int color, double alpha, cudaStream_t s) {
   const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm128);
@@ -636,21 +645,27 @@ static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
   }
 }
 
+static int variant(const Grid &g) {
+  return g.codeR ? VAR_MASK : (is_periodic(g) ? VAR_PER : VAR_BOX);
+}
+
 void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
                          cudaStream_t s) {
-  if (g.codeR)
-    launch_sm_n<false, true>(g, g, tm_oth128, color, 0.0, s);
-  else
-    launch_sm_n<false, false>(g, g, tm_oth128, color, 0.0, s);
+  switch (variant(g)) {
+    case VAR_MASK: launch_sm_n<false, VAR_MASK>(g, g, tm_oth128, color, 0.0, s); break;
+    case VAR_PER: launch_sm_n<false, VAR_PER>(g, g, tm_oth128, color, 0.0, s); break;
+    default: launch_sm_n<false, VAR_BOX>(g, g, tm_oth128, color, 0.0, s); break;
+  }
 }
 
 void launch_prolong_smooth_march(const Grid &g, const Grid &c,
                                  const void *tm_oth128, int color, double alpha,
                                  cudaStream_t s) {
-  if (g.codeR)
-    launch_sm_n<true, true>(g, c, tm_oth128, color, alpha, s);
-  else
-    launch_sm_n<true, false>(g, c, tm_oth128, color, alpha, s);
+  switch (variant(g)) {
+    case VAR_MASK: launch_sm_n<true, VAR_MASK>(g, c, tm_oth128, color, alpha, s); break;
+    case VAR_PER: launch_sm_n<true, VAR_PER>(g, c, tm_oth128, color, alpha, s); break;
+    default: launch_sm_n<true, VAR_BOX>(g, c, tm_oth128, color, alpha, s); break;
+  }
 }
 
 static int resid_blocks(const Grid &g) {
@@ -666,7 +681,7 @@ bool resid_march_supported(const Grid &g) {
          (g.nxl % 2) == 0 && (g.ny % 2) == 0 && get_encode() != nullptr;
 }
 
-template <int MODE, bool M>
+template <int MODE, int M>
 static void launch_rm(const Grid &g, const Grid &c, const void *tmR,
                       const void *tmB, double *partials, cudaStream_t s) {
   static size_t configured = 0;
@@ -678,20 +693,22 @@ static void launch_rm(const Grid &g, const Grid &c, const void *tmR,
 
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
                                  const void *tmB, cudaStream_t s) {
-  if (g.codeR)
-    launch_rm<MODE_RESTRICT, true>(g, c, tmR, tmB, nullptr, s);
-  else
-    launch_rm<MODE_RESTRICT, false>(g, c, tmR, tmB, nullptr, s);
+  switch (variant(g)) {
+    case VAR_MASK: launch_rm<MODE_RESTRICT, VAR_MASK>(g, c, tmR, tmB, nullptr, s); break;
+    case VAR_PER: launch_rm<MODE_RESTRICT, VAR_PER>(g, c, tmR, tmB, nullptr, s); break;
+    default: launch_rm<MODE_RESTRICT, VAR_BOX>(g, c, tmR, tmB, nullptr, s); break;
+  }
 }
 
 int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
 
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s) {
-  if (g.codeR)
-    launch_rm<MODE_NORM, true>(g, g, tmR, tmB, partials, s);
-  else
-    launch_rm<MODE_NORM, false>(g, g, tmR, tmB, partials, s);
+  switch (variant(g)) {
+    case VAR_MASK: launch_rm<MODE_NORM, VAR_MASK>(g, g, tmR, tmB, partials, s); break;
+    case VAR_PER: launch_rm<MODE_NORM, VAR_PER>(g, g, tmR, tmB, partials, s); break;
+    default: launch_rm<MODE_NORM, VAR_BOX>(g, g, tmR, tmB, partials, s); break;
+  }
 }
 
 }  // namespace mg
