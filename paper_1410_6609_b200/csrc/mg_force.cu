@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include "mg_internal.h"
+#include "mg_sphere.cuh"
 
 namespace mg {
 
@@ -22,36 +23,14 @@ namespace {
 
 constexpr int kTF = 256;
 
-__constant__ int kQ19[18][3] = {
-    {1, 0, 0},  {-1, 0, 0}, {0, 1, 0},   {0, -1, 0}, {0, 0, 1},  {0, 0, -1},
-    {1, 1, 0},  {-1, -1, 0}, {1, -1, 0}, {-1, 1, 0}, {1, 0, 1},  {-1, 0, -1},
-    {1, 0, -1}, {-1, 0, 1}, {0, 1, 1},   {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
-
-__device__ __forceinline__ bool insph(int i, int j, int k, double h, double cx,
-                                      double cy, double cz, double R) {
-  const double dx = ((double)i + 0.5) * h - cx;
-  const double dy = ((double)j + 0.5) * h - cy;
-  const double dz = ((double)k + 0.5) * h - cz;
-  const double d2 = (dx * dx + dy * dy) + dz * dz;
-  return d2 <= R * R;
-}
-
-__device__ __forceinline__ int subcnt(int i, int j, int k, int s, double hs,
-                                      double cx, double cy, double cz, double R) {
-  int c = 0;
-  for (int a = 0; a < s; a++)
-    for (int b = 0; b < s; b++)
-      for (int d = 0; d < s; d++)
-        c += insph(i * s + a, j * s + b, k * s + d, hs, cx, cy, cz, R) ? 1 : 0;
-  return c;
-}
-
-__device__ __forceinline__ void bbox_f(int n, double h, double c, double R,
-                                       int *lo, int *hi) {
-  int a = (int)floor((c - R) / h - 0.5) - 1;
-  int b = (int)ceil((c + R) / h - 0.5) + 1;
-  *lo = a < 0 ? 0 : a;
-  *hi = b > n - 1 ? n - 1 : b;
+// D3Q19 directions e_q (q = 2..19 of Eq.15, rest direction omitted), as a
+// constexpr function so that the unrolled loops fold every component
+__host__ __device__ constexpr int kq(int q, int a) {
+  const int t[18][3] = {
+      {1, 0, 0},  {-1, 0, 0}, {0, 1, 0},   {0, -1, 0}, {0, 0, 1},  {0, 0, -1},
+      {1, 1, 0},  {-1, -1, 0}, {1, -1, 0}, {-1, 1, 0}, {1, 0, 1},  {-1, 0, -1},
+      {1, 0, -1}, {-1, 0, 1}, {0, 1, 1},   {0, -1, -1}, {0, 1, -1}, {0, -1, 1}};
+  return t[q][a];
 }
 
 __device__ __forceinline__ int wrapi(int i, int n, int per) {
@@ -81,45 +60,36 @@ __device__ __forceinline__ double phi_at(const Grid &g, int i, int j, int k) {
   return (((iw + j + k) & 1) ? g.phiB : g.phiR)[e];
 }
 
-// periodic images of a sphere centre: the enumeration of k_spheres / the
-// oracle (m in {-1,0,1} on periodic axes, (mx,my,mz) lexicographic)
-__device__ __forceinline__ int images_f(const Grid &g, double h, double cx,
-                                        double cy, double cz, double img[27][3]) {
-  int n = 0;
-  for (int mx = -g.per[0]; mx <= g.per[0]; mx++)
-    for (int my = -g.per[1]; my <= g.per[1]; my++)
-      for (int mz = -g.per[2]; mz <= g.per[2]; mz++) {
-        img[n][0] = mx ? cx + (double)mx * ((double)g.nx * h) : cx;
-        img[n][1] = my ? cy + (double)my * ((double)g.ny * h) : cy;
-        img[n][2] = mz ? cz + (double)mz * ((double)g.nz * h) : cz;
-        n++;
-      }
-  return n;
-}
-
-__device__ void gradient(const Grid &g, const unsigned char *solid, double h,
-                         int i, int j, int k, double *gr) {
+// LD(i, j, k): Phi at a global cell
+template <class LD>
+__device__ __forceinline__ void gradient(const Grid &g, const unsigned char *solid,
+                                         double h, int i, int j, int k, double *gr,
+                                         const LD &ld) {
   bool all = true;
 #pragma unroll
   for (int q = 0; q < 18; q++)
-    all = all && valid_cell(g, solid, i + kQ19[q][0], j + kQ19[q][1], k + kQ19[q][2]);
+    all = all && valid_cell(g, solid, i + kq(q, 0), j + kq(q, 1), k + kq(q, 2));
   if (all) {
+    // per component the oracle's sum S_a = sum_q (+-) w_q Phi_q in the fixed
+    // q order (terms with c_q = 0 skipped): each neighbour is loaded once and
+    // added to the components it contributes to, in q order per component
+    double S[3] = {0.0, 0.0, 0.0};
 #pragma unroll
-    for (int a = 0; a < 3; a++) {
-      double S = 0.0;
+    for (int q = 0; q < 18; q++) {
+      const double v = ld(i + kq(q, 0), j + kq(q, 1), k + kq(q, 2));
+      const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
 #pragma unroll
-      for (int q = 0; q < 18; q++) {
-        const int c = kQ19[q][a];
+      for (int a = 0; a < 3; a++) {
+        const int c = kq(q, a);
         if (c == 0) continue;
-        const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
-        const double v = phi_at(g, i + kQ19[q][0], j + kQ19[q][1], k + kQ19[q][2]);
-        S = c > 0 ? S + w * v : S - w * v;
+        S[a] = c > 0 ? S[a] + w * v : S[a] - w * v;
       }
-      gr[a] = (3.0 * S) / h;
     }
+#pragma unroll
+    for (int a = 0; a < 3; a++) gr[a] = (3.0 * S[a]) / h;
     return;
   }
-  const double c0 = phi_at(g, i, j, k);
+  const double c0 = ld(i, j, k);
 #pragma unroll
   for (int a = 0; a < 3; a++) {
     const int pi = i + (a == 0), pj = j + (a == 1), pk = k + (a == 2);
@@ -127,11 +97,11 @@ __device__ void gradient(const Grid &g, const unsigned char *solid, double h,
     const bool vp = valid_cell(g, solid, pi, pj, pk);
     const bool vm = valid_cell(g, solid, mi, mj, mk);
     if (vp && vm)
-      gr[a] = (phi_at(g, pi, pj, pk) - phi_at(g, mi, mj, mk)) / (2.0 * h);
+      gr[a] = (ld(pi, pj, pk) - ld(mi, mj, mk)) / (2.0 * h);
     else if (vp)
-      gr[a] = (phi_at(g, pi, pj, pk) - c0) / h;
+      gr[a] = (ld(pi, pj, pk) - c0) / h;
     else if (vm)
-      gr[a] = (c0 - phi_at(g, mi, mj, mk)) / h;
+      gr[a] = (c0 - ld(mi, mj, mk)) / h;
     else
       gr[a] = 0.0;
   }
@@ -156,57 +126,55 @@ __global__ void __launch_bounds__(kTF)
     k_coulomb(Grid g, const unsigned char *solid, double h, int s,
               const double *sph, int normalization, double *part) {
   __shared__ double sh[32];
+  __shared__ sph::Tab tab;
   const int p = blockIdx.x;
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
+  const double R2 = R * R;
   const double hs = h / (double)s;
   double img[27][3];
-  const int nimg = images_f(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
-  double cnt = 0.0;
+  const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
+  long long cnt = 0;  // threads own (j, k) columns of the box, walk along x
   for (int m = 0; m < nimg; m++) {
-    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
-    int i0, i1, j0, j1, k0, k1;
-    bbox_f(g.nx, h, cx, R, &i0, &i1);
-    bbox_f(g.ny, h, cy, R, &j0, &j1);
-    bbox_f(g.nz, h, cz, R, &k0, &k1);
-    const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-    const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
-    for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
-      const int k = k0 + (int)(t % nk);
-      const long long q = t / nk;
-      const int j = j0 + (int)(q % nj);
-      const int i = i0 + (int)(q / nj);
-      cnt += (double)subcnt(i, j, k, s, hs, cx, cy, cz, R);
+    const sph::Box bx = sph::box_of(g, h, img[m], R);
+    if (bx.cells() == 0) continue;
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
+    const int ncol = bx.n[1] * bx.n[2];
+    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+      const int cj = col / bx.n[2], ck = col % bx.n[2];
+      for (int ci = 0; ci < bx.n[0]; ci++)
+        cnt += tb ? sph::count_tab(tab, ci, cj, ck, s, R2)
+                  : sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s,
+                                   hs, img[m][0], img[m][1], img[m][2], R);
     }
   }
-  const double np = bsum(cnt, sh);
+  const double np = bsum((double)cnt, sh);
   double F[3] = {0.0, 0.0, 0.0};
   const bool any = np > 0.0 || normalization == 1;
   const double rho0 = Q / ((4.0 / 3.0) * 3.14159265358979323846 * (R * R * R));
   for (int m = 0; any && m < nimg; m++) {
-    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
-    int i0, i1, j0, j1, k0, k1;
-    bbox_f(g.nx, h, cx, R, &i0, &i1);
-    bbox_f(g.ny, h, cy, R, &j0, &j1);
-    bbox_f(g.nz, h, cz, R, &k0, &k1);
-    const int nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-    const int xa = i0 > g.x0 ? i0 : g.x0;
-    const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
-    if (xa > xb || nj <= 0 || nk <= 0) continue;
-    const long long nloc = (long long)(xb - xa + 1) * nj * nk;
-    for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
-      const int k = k0 + (int)(t % nk);
-      const long long q = t / nk;
-      const int j = j0 + (int)(q % nj);
-      const int i = xa + (int)(q / nj);
-      const int c = subcnt(i, j, k, s, hs, cx, cy, cz, R);
-      if (!c || !valid_cell(g, solid, i, j, k)) continue;
-      const double rho = (normalization == 1)
-                             ? rho0 * ((double)c / (double)(s * s * s))
-                             : (Q * (double)c) / (np * (h * h * h));
-      double gr[3];
-      gradient(g, solid, h, i, j, k, gr);
+    const sph::Box bx = sph::box_of(g, h, img[m], R);
+    const int xa = bx.lo[0] > g.x0 ? bx.lo[0] : g.x0;
+    const int xb = min(bx.lo[0] + bx.n[0] - 1, g.x0 + g.nxl - 1);
+    if (bx.cells() == 0 || xa > xb) continue;
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
+    auto ld_glb = [&](int x, int y, int z) { return phi_at(g, x, y, z); };
+    const int ncol = bx.n[1] * bx.n[2];
+    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+      const int cj = col / bx.n[2], ck = col % bx.n[2];
+      const int j = bx.lo[1] + cj, k = bx.lo[2] + ck;
+      for (int i = xa; i <= xb; i++) {
+        const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
+                         : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
+                                          img[m][2], R);
+        if (!c || !valid_cell(g, solid, i, j, k)) continue;
+        const double rho = (normalization == 1)
+                               ? rho0 * ((double)c / (double)(s * s * s))
+                               : (Q * (double)c) / (np * (h * h * h));
+        double gr[3];
+        gradient(g, solid, h, i, j, k, gr, ld_glb);
 #pragma unroll
-      for (int a = 0; a < 3; a++) F[a] = F[a] + gr[a] * rho;
+        for (int a = 0; a < 3; a++) F[a] = F[a] + gr[a] * rho;
+      }
     }
   }
 #pragma unroll

@@ -15,6 +15,7 @@
 #include <type_traits>
 
 #include "mg_internal.h"
+#include "mg_sphere.cuh"
 
 namespace mg {
 
@@ -494,119 +495,77 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
 }
 
 // ---------------------------------------------------------------------------
-// RHS from charged spheres (centre rule P:273, inclusive c13).
-// One CTA per sphere: count the covered cell centres of the whole (global)
-// domain, then add rho_p to the covered cells of this slab.  sph holds
-// (cx, cy, cz, R, Q) per sphere.  f must be zero beforehand; non-overlapping
-// spheres give 0 + rho exactly, as the oracle.
+// RHS from charged spheres (centre rule P:273, inclusive c13;
+// subsampling P:485-489; periodic images P:441-443).  One CTA per sphere:
+// count the covered sub-cells of the whole (global) domain over all images,
+// then add rho_p to the covered cells of this slab.  The inside tests use
+// per-axis tables of squared distances (mg_sphere.cuh, bitwise the direct
+// test).  sph holds (cx, cy, cz, R, Q) per sphere.  f must be zero
+// beforehand; non-overlapping spheres give 0 + rho exactly, as the oracle.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ bool inside(int i, int j, int k, double h,
-                                       double cx, double cy, double cz,
-                                       double R) {
-  const double dx = ((double)i + 0.5) * h - cx;
-  const double dy = ((double)j + 0.5) * h - cy;
-  const double dz = ((double)k + 0.5) * h - cz;
-  const double d2 = (dx * dx + dy * dy) + dz * dz;
-  return d2 <= R * R;
-}
-
-__device__ __forceinline__ void bbox(int n, double h, double c, double R,
-                                     int *lo, int *hi) {
-  int a = (int)floor((c - R) / h - 0.5) - 1;
-  int b = (int)ceil((c + R) / h - 0.5) + 1;
-  *lo = a < 0 ? 0 : a;
-  *hi = b > n - 1 ? n - 1 : b;
-}
-
-// subsampling: covered sub-cell centres of cell (i,j,k), the s^3
-// centres ((i s + a + 1/2) h/s, ...) with the same inclusive test (s = 1: the
-// plain centre rule, hs = h exactly)
-__device__ __forceinline__ int sub_count(int i, int j, int k, int s, double hs,
-                                         double cx, double cy, double cz,
-                                         double R) {
-  int cnt = 0;
-  for (int a = 0; a < s; a++)
-    for (int b = 0; b < s; b++)
-      for (int c = 0; c < s; c++)
-        cnt += inside(i * s + a, j * s + b, k * s + c, hs, cx, cy, cz, R) ? 1 : 0;
-  return cnt;
-}
-
-// periodic images of a sphere centre (the domain cyclically
-// extended): m in {-1, 0, 1} on periodic axes, image centre c + m (n h) (the
-// coordinate untouched for m = 0), (mx, my, mz) lexicographic -- the
-// oracle's enumeration.  The host checks 2R + 2h <= n h on periodic axes, so
-// no cell is reached by two images.
-__device__ __forceinline__ int sphere_images(const Grid &g, double h, double cx,
-                                             double cy, double cz,
-                                             double img[27][3]) {
-  int n = 0;
-  for (int mx = -g.per[0]; mx <= g.per[0]; mx++)
-    for (int my = -g.per[1]; my <= g.per[1]; my++)
-      for (int mz = -g.per[2]; mz <= g.per[2]; mz++) {
-        img[n][0] = mx ? cx + (double)mx * ((double)g.nx * h) : cx;
-        img[n][1] = my ? cy + (double)my * ((double)g.ny * h) : cy;
-        img[n][2] = mz ? cz + (double)mz * ((double)g.nz * h) : cz;
-        n++;
-      }
-  return n;
-}
-
 __global__ void __launch_bounds__(kThreads)
     k_spheres(Grid g, double h, int s, const double *sph, int normalization,
               unsigned long long *counts) {
   __shared__ double sh[32];
+  __shared__ sph::Tab tab;
+  __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
   const int p = blockIdx.x;
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
+  const double R2 = R * R;
   const double hs = h / (double)s;
+  const int s3 = s * s * s;
   double img[27][3];
-  const int nimg = sphere_images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
-  double cnt = 0.0;  // exact integer count (< 2^53)
+  const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
+  // threads own (j, k) columns of the box and walk along x: no per-cell
+  // index division; integer counts are exact in any order
+  long long cnt = 0;
   for (int m = 0; m < nimg; m++) {
-    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
-    int i0, i1, j0, j1, k0, k1;
-    bbox(g.nx, h, cx, R, &i0, &i1);
-    bbox(g.ny, h, cy, R, &j0, &j1);
-    bbox(g.nz, h, cz, R, &k0, &k1);
-    const int ni = i1 - i0 + 1, nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-    const long long nbox = (ni > 0 && nj > 0 && nk > 0) ? (long long)ni * nj * nk : 0;
-    for (long long t = threadIdx.x; t < nbox; t += blockDim.x) {
-      const int k = k0 + (int)(t % nk);
-      const long long q = t / nk;
-      const int j = j0 + (int)(q % nj);
-      const int i = i0 + (int)(q / nj);
-      cnt += (double)sub_count(i, j, k, s, hs, cx, cy, cz, R);
+    const sph::Box bx = sph::box_of(g, h, img[m], R);
+    if (bx.cells() == 0) continue;
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
+    const int ncol = bx.n[1] * bx.n[2];
+    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+      const int cj = col / bx.n[2], ck = col % bx.n[2];
+      for (int ci = 0; ci < bx.n[0]; ci++)
+        cnt += tb ? sph::count_tab(tab, ci, cj, ck, s, R2)
+                  : sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s,
+                                   hs, img[m][0], img[m][1], img[m][2], R);
     }
   }
-  const double np = block_sum(cnt, sh);
+  const double np = block_sum((double)cnt, sh);
   if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
   if (normalization != 1 && np == 0.0) return;
   const double rho0 = Q / ((4.0 / 3.0) * kPi * (R * R * R));
+  // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3), per
+  // possible count (tabulated when s^3 < kVal)
+  auto value = [&](int c) {
+    return (normalization == 1) ? rho0 * ((double)c / (double)s3)
+                                : (Q * (double)c) / (np * (h * h * h));
+  };
+  const bool vtab = s3 < sph::kVal;
+  if (vtab)
+    for (int c = threadIdx.x; c <= s3; c += blockDim.x) vt[c] = value(c);
   for (int m = 0; m < nimg; m++) {
-    const double cx = img[m][0], cy = img[m][1], cz = img[m][2];
-    int i0, i1, j0, j1, k0, k1;
-    bbox(g.nx, h, cx, R, &i0, &i1);
-    bbox(g.ny, h, cy, R, &j0, &j1);
-    bbox(g.nz, h, cz, R, &k0, &k1);
-    const int nj = j1 - j0 + 1, nk = k1 - k0 + 1;
-    const int xa = i0 > g.x0 ? i0 : g.x0;
-    const int xb = i1 < g.x0 + g.nxl - 1 ? i1 : g.x0 + g.nxl - 1;
-    if (xa > xb || nj <= 0 || nk <= 0) continue;
-    const long long nloc = (long long)(xb - xa + 1) * nj * nk;
-    for (long long t = threadIdx.x; t < nloc; t += blockDim.x) {
-      const int k = k0 + (int)(t % nk);
-      const long long q = t / nk;
-      const int j = j0 + (int)(q % nj);
-      const int i = xa + (int)(q / nj);
-      const int c = sub_count(i, j, k, s, hs, cx, cy, cz, R);
-      if (!c) continue;
-      // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3)
-      const double v = (normalization == 1)
-                           ? rho0 * ((double)c / (double)(s * s * s))
-                           : (Q * (double)c) / (np * (h * h * h));
-      const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
-      double *f = ((i + j + k) & 1) ? g.fB : g.fR;
-      atomicAdd(f + idx, v);
+    sph::Box bx = sph::box_of(g, h, img[m], R);
+    // this slab's planes of the box
+    const int xa = bx.lo[0] > g.x0 ? bx.lo[0] : g.x0;
+    const int xb = min(bx.lo[0] + bx.n[0] - 1, g.x0 + g.nxl - 1);
+    if (bx.cells() == 0 || xa > xb) continue;
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]);  // (also publishes vt)
+    const int ncol = bx.n[1] * bx.n[2];
+    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+      const int cj = col / bx.n[2], ck = col % bx.n[2];
+      const int j = bx.lo[1] + cj, k = bx.lo[2] + ck;
+      for (int i = xa; i <= xb; i++) {
+        const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
+                         : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
+                                          img[m][2], R);
+        if (!c) continue;
+        const double v = vtab ? vt[c] : value(c);
+        const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
+        double *f = ((i + j + k) & 1) ? g.fB : g.fR;
+        atomicAdd(f + idx, v);
+      }
     }
   }
 }
@@ -629,37 +588,80 @@ struct Terms {
   double t[6];
 };
 
-__global__ void __launch_bounds__(kThreads) k_bc_adapt(Grid g, Terms T) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)g.nxl * g.ny) return;
-  const int j = (int)(t % g.ny);
-  const int il = (int)(t / g.ny);
+__device__ __forceinline__ void bc_cell(const Grid &g, const Terms &T, int il,
+                                        int j, int z) {
   const int i = g.x0 + il;
-  const bool full = (i == 0 || i == g.nx - 1 || j == 0 || j == g.ny - 1);
-  const long long b = rowbase(g, il, j);
-  const int step = full ? 1 : (g.nz - 1);
-  for (int z = 0; z < g.nz; z += step) {
-    // masked cells are not unknowns (their f stays 0)
-    if (g.codeR && !((((i + j + z) & 1) ? g.codeB : g.codeR)[b + (z >> 1)] & 64))
-      continue;
-    double *f = ((i + j + z) & 1) ? g.fB : g.fR;
-    double v = f[b + (z >> 1)];
-    const bool on[6] = {i == 0, i == g.nx - 1, j == 0,
-                        j == g.ny - 1, z == 0, z == g.nz - 1};
+  const long long e = rowbase(g, il, j) + (z >> 1);
+  // masked cells are not unknowns (their f stays 0)
+  if (g.codeR && !((((i + j + z) & 1) ? g.codeB : g.codeR)[e] & 64)) return;
+  double *f = ((i + j + z) & 1) ? g.fB : g.fR;
+  double v = f[e];
+  const bool on[6] = {i == 0, i == g.nx - 1, j == 0,
+                      j == g.ny - 1, z == 0, z == g.nz - 1};
 #pragma unroll
-    for (int q = 0; q < 6; q++)
-      if (on[q] && !g.per[q >> 1]) v = v - T.t[q];  // periodic: no boundary
-    f[b + (z >> 1)] = v;
+  for (int q = 0; q < 6; q++)
+    if (on[q] && !g.per[q >> 1]) v = v - T.t[q];  // periodic: no boundary
+  f[e] = v;
+}
+
+// every boundary cell exactly once, one thread per cell (each cell's face
+// terms in face order in that thread):
+//   part A: z = 0 and z = nz-1 of every row            (rows x 2)
+//   part B: rows j = 0, ny-1 of every plane, 0 < z < nz-1   (nxl x 2 x (nz-2))
+//   part C: planes i = 0, nx-1 held here, 0 < j < ny-1, 0 < z < nz-1
+__global__ void __launch_bounds__(kThreads)
+    k_bc_adapt(Grid g, Terms T, long long nA, long long nB, int pc0, int pc1) {
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int nzi = g.nz - 2;
+  if (t < nA) {
+    const int side = (int)(t & 1);
+    const long long r = t >> 1;
+    const int j = (int)(r % g.ny), il = (int)(r / g.ny);
+    if (side && g.nz == 1) return;
+    bc_cell(g, T, il, j, side ? g.nz - 1 : 0);
+    return;
   }
+  t -= nA;
+  if (t < nB) {
+    const int z = 1 + (int)(t % nzi);
+    const long long r = t / nzi;
+    const int side = (int)(r & 1), il = (int)(r >> 1);
+    if (side && g.ny == 1) return;
+    bc_cell(g, T, il, side ? g.ny - 1 : 0, z);
+    return;
+  }
+  t -= nB;
+  const long long per_plane = (long long)(g.ny - 2) * nzi;
+  const int z = 1 + (int)(t % nzi);
+  const long long r = t / nzi;
+  const int j = 1 + (int)(r % (g.ny - 2));
+  const int pl = (int)(r / (g.ny - 2));  // 0: plane pc0, 1: plane pc1
+  if (per_plane <= 0 || pl > 1) return;
+  const int il = pl ? pc1 : pc0;
+  if (il < 0 || (pl && pc1 == pc0)) return;
+  bc_cell(g, T, il, j, z);
 }
 
 void launch_bc_adapt(const Grid &g, const double *terms, const int * /*types*/,
                      cudaStream_t s) {
   Terms T;
   for (int q = 0; q < 6; q++) T.t[q] = terms[q];
-  const long long total = (long long)g.nxl * g.ny;
-  if (total <= 0) return;
-  k_bc_adapt<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, T);
+  const long long nzi = g.nz > 2 ? g.nz - 2 : 0;
+  const long long nA = 2LL * g.nxl * g.ny;
+  const long long nB = g.ny > 0 ? 2LL * g.nxl * nzi : 0;
+  // local planes of the x faces held by this slab (-1: none)
+  const int pc0 = (g.x0 == 0) ? 0 : -1;
+  const int pc1 = (g.x0 + g.nxl == g.nx) ? g.nxl - 1 : -1;
+  const long long nC = (g.ny > 2 ? 2LL * (g.ny - 2) * nzi : 0);
+  const long long total = nA + nB + nC;
+  if (g.nxl <= 0 || total <= 0) return;
+  int a0 = pc0, a1 = pc1;
+  if (a0 < 0) {  // only the last plane: put it first
+    a0 = a1;
+    a1 = -1;
+  }
+  k_bc_adapt<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(
+      g, T, nA, nB, a0, a1 < 0 ? a0 : a1);
 }
 
 // ---------------------------------------------------------------------------
