@@ -84,6 +84,7 @@ def lib():
         L.orc_last_cg_iters.argtypes = [P]
         L.orc_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.orc_set_face_values.argtypes = [P, i, dp]
+        L.orc_set_permittivity.argtypes = [P, dp]
         L.orc_gradient.argtypes = [P, dp, i, i, i, dp]
         L.orc_coulomb_forces.argtypes = [P, i, dp, dp, dp, i, i, dp]
         L.orc_sphere_subcount.restype = ctypes.c_long
@@ -179,6 +180,17 @@ class Oracle:
         if lib().orc_set_bc_patch(self._h, face, a0, a1, b0, b1, int(bc_type),
                                   float(value)) != 0:
             raise ValueError("oracle: bad patch")
+
+    def set_permittivity(self, eps):
+        """Cell permittivity (natural layout), None = constant 1 (N4)."""
+        if eps is None:
+            rc = lib().orc_set_permittivity(self._h, None)
+        else:
+            self._eps = _f64(eps)
+            assert self._eps.shape == self.dims(0)
+            rc = lib().orc_set_permittivity(self._h, _dp(self._eps))
+        if rc != 0:
+            raise ValueError("oracle: permittivity must be > 0")
 
     def set_face_values(self, face, values):
         v = _f64(values).reshape(-1)

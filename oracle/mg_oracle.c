@@ -57,6 +57,9 @@ struct orc_hier {
    * order; NULL = the face-uniform bct/bcv */
   int *fty[6];
   double *fva[6];
+  /* cell permittivity (N4, natural layout of level 0); NULL = constant 1,
+   * the paper's "spatially constant permittivity" */
+  double *eps;
   int nu1, nu2;
   double alpha;
   double coarse_tol;
@@ -133,7 +136,14 @@ static void level_free(level_t *L) {
  *   Dirichlet: centre beta -> beta - alpha, alpha -> 0
  *   Neumann:   centre beta -> beta + alpha, alpha -> 0
  * A solid (masked) neighbour is a homogeneous Neumann face (reading c19). */
+static void assemble_finest_eps(orc_hier *H);
+static void galerkin(orc_hier *H, int l);
+
 static void assemble_finest(orc_hier *H) {
+  if (H->eps) {
+    assemble_finest_eps(H);
+    return;
+  }
   level_t *L = &H->L[0];
   const double inv = 1.0 / (H->h * H->h);
   const int di[6] = {-1, 1, 0, 0, 0, 0};
@@ -170,6 +180,66 @@ static void assemble_finest(orc_hier *H) {
         }
         a[0] = beta;
       }
+}
+
+/* Variable permittivity (the solver "is extensible for
+ * discontinuous dielectricity coefficients ... by Galerkin coarsening",
+ * P:513-516; "jumping dielectricity coefficients"):
+ * -div(eps grad Phi) = rho, finite volumes on the same cells.
+ * Reading d10: the flux across the face between cells c and n uses the
+ * harmonic mean eps_f = (2 eps_c eps_n) / (eps_c + eps_n) (flux continuity
+ * for a coefficient constant per cell); a boundary face uses eps_c, folded as
+ * P:451-459 with alpha = -eps_c/h^2: Dirichlet adds 2 eps_c/h^2 to the
+ * centre, Neumann nothing; a solid neighbour is a homogeneous Neumann face.
+ * The centre sums the face terms in face order. */
+static void assemble_finest_eps(orc_hier *H) {
+  level_t *L = &H->L[0];
+  const double inv = 1.0 / (H->h * H->h);
+  const int di[6] = {-1, 1, 0, 0, 0, 0};
+  const int dj[6] = {0, 0, -1, 1, 0, 0};
+  const int dk[6] = {0, 0, 0, 0, -1, 1};
+  for (int i = 0; i < L->nx; i++)
+    for (int j = 0; j < L->ny; j++)
+      for (int k = 0; k < L->nz; k++) {
+        long c = IDX(L, i, j, k);
+        double *a = &L->A[7 * c];
+        for (int q = 0; q < 7; q++) a[q] = 0.0;
+        if (!L->unk[c]) continue;
+        const double ec = H->eps[c];
+        double beta = 0.0;
+        for (int q = 0; q < 6; q++) {
+          int ii = wrap(i + di[q], L->nx, L->per[0]);
+          int jj = wrap(j + dj[q], L->ny, L->per[1]);
+          int kk = wrap(k + dk[q], L->nz, L->per[2]);
+          int outside = ii < 0 || jj < 0 || kk < 0 || ii >= L->nx ||
+                        jj >= L->ny || kk >= L->nz;
+          if (outside) {
+            if (face_type(H, q, i, j, k) == ORC_DIRICHLET)
+              beta = beta + 2.0 * (ec * inv);
+          } else if (L->unk[IDX(L, ii, jj, kk)]) {
+            const double en = H->eps[IDX(L, ii, jj, kk)];
+            const double ef = (2.0 * ec * en) / (ec + en);
+            beta = beta + ef * inv;
+            a[1 + q] = -(ef * inv);
+          }
+        }
+        a[0] = beta;
+      }
+}
+
+int orc_set_permittivity(orc_hier *H, const double *eps) {
+  level_t *L = &H->L[0];
+  free(H->eps);
+  H->eps = NULL;
+  if (eps) {
+    for (long c = 0; c < L->n; c++)
+      if (!(eps[c] > 0.0)) return -1;
+    H->eps = (double *)malloc(sizeof(double) * (size_t)L->n);
+    memcpy(H->eps, eps, sizeof(double) * (size_t)L->n);
+  }
+  assemble_finest(H);
+  for (int l = 0; l + 1 < H->nlev; l++) galerkin(H, l);
+  return 0;
 }
 
 /* Galerkin coarsening A_c = R A P: P = nearest-neighbour
@@ -277,6 +347,7 @@ void orc_destroy(orc_hier *H) {
     free(H->fty[q]);
     free(H->fva[q]);
   }
+  free(H->eps);
   free(H);
 }
 
@@ -362,12 +433,15 @@ void orc_set_rhs_raw(orc_hier *H, int l, const double *in) {
  *                   Phi_0 - Phi_1 = h g_n, outward normal derivative)      */
 void orc_bc_adapt(orc_hier *H) {
   level_t *L = &H->L[0];
-  const double alpha = -1.0 * (1.0 / (H->h * H->h));
+  const double inv = 1.0 / (H->h * H->h);
+  const double alpha1 = -1.0 * inv;
   for (int i = 0; i < L->nx; i++)
     for (int j = 0; j < L->ny; j++)
       for (int k = 0; k < L->nz; k++) {
         long c = IDX(L, i, j, k);
         if (!L->unk[c]) continue;
+        /* variable permittivity (d10): alpha = -eps_c / h^2 */
+        const double alpha = H->eps ? -(H->eps[c] * inv) : alpha1;
         int on[6] = {i == 0, i == L->nx - 1, j == 0,
                      j == L->ny - 1, k == 0, k == L->nz - 1};
         for (int q = 0; q < 6; q++) {

@@ -42,6 +42,11 @@ int orc_set_face_values(orc_hier *H, int face, const double *values);
 int orc_set_bc_patch(orc_hier *H, int face, int a0, int a1, int b0, int b1,
                      int type, double value);
 
+/* cell permittivity eps[nx*ny*nz] > 0 (natural layout), NULL = constant 1;
+ * re-assembles the finest operator and every Galerkin level (N4, d10).
+ * Set the RHS afterwards (its BC adaptation uses eps).  0 or -1. */
+int orc_set_permittivity(orc_hier *H, const double *eps);
+
 int orc_num_levels(const orc_hier *H);
 void orc_level_dims(const orc_hier *H, int l, int *dims3);
 

@@ -166,11 +166,12 @@ def rbgs_matrix(A, shape, color):
     return np.eye(A.shape[0]) - (sel / D)[:, None] * A
 
 
-def vcycle_matrices(shapes, h, bc_type, nu1, nu2, alpha):
+def vcycle_matrices(shapes, h, bc_type, nu1, nu2, alpha, A0=None):
     """Dense V-cycle error-propagation matrix M_0 and approximate inverse B_0
     for a hierarchy of box levels `shapes` (finest first), Galerkin coarse
-    operators A_{l+1} = R A_l P with R = P^T / 8, exact coarsest solve."""
-    A = [dense_operator(shapes[0], h, bc_type)]
+    operators A_{l+1} = R A_l P with R = P^T / 8, exact coarsest solve.
+    A0: the finest operator (default: the constant-coefficient one)."""
+    A = [dense_operator(shapes[0], h, bc_type) if A0 is None else A0]
     Ps = []
     for l in range(len(shapes) - 1):
         P = injection_P(shapes[l])
@@ -189,3 +190,43 @@ def vcycle_matrices(shapes, h, bc_type, nu1, nu2, alpha):
         M = post @ cgc @ pre
         B = (I - M) @ np.linalg.inv(A[l])
     return M, A
+
+
+def flux_operator_eps(shape, h, bc_type, eps, bc_value=None):
+    """Variable-permittivity finite-volume operator -div(eps grad) (N4) built
+    from fluxes: the flux between cells c and n is eps_f (u_c - u_n) / h^2
+    with eps_f the harmonic mean of the two cells' eps; across a boundary
+    face the ghost cell carries eps_c and the paper's extrapolated value
+    (Dirichlet 2 g - u_c, Neumann u_c + h g).  Returns the dense matrix of
+    the homogeneous operator and the RHS shift b of the inhomogeneous BCs
+    (A u = f + b).  Independent of the oracle's folded stencil."""
+    nx, ny, nz = shape
+    n = nx * ny * nz
+    A = np.zeros((n, n))
+    b = np.zeros(n)
+    g = [0.0] * 6 if bc_value is None else bc_value
+    idx = np.arange(n).reshape(shape)
+    offs = [(-1, 0, 0), (1, 0, 0), (0, -1, 0), (0, 1, 0), (0, 0, -1), (0, 0, 1)]
+    for i in range(nx):
+        for j in range(ny):
+            for k in range(nz):
+                c = idx[i, j, k]
+                ec = eps[i, j, k]
+                for f, (a, bb, cc) in enumerate(offs):
+                    ii, jj, kk = i + a, j + bb, k + cc
+                    per = bc_type[f] == PERIODIC
+                    if per:
+                        ii, jj, kk = ii % nx, jj % ny, kk % nz
+                    if 0 <= ii < nx and 0 <= jj < ny and 0 <= kk < nz:
+                        en = eps[ii, jj, kk]
+                        ef = 2.0 * ec * en / (ec + en)
+                        A[c, c] += ef / h ** 2
+                        A[c, idx[ii, jj, kk]] -= ef / h ** 2
+                    elif bc_type[f] == DIRICHLET:
+                        # ghost 2 g - u_c: eps_c (u_c - (2 g - u_c)) / h^2
+                        A[c, c] += 2.0 * ec / h ** 2
+                        b[c] += 2.0 * ec * g[f] / h ** 2
+                    else:
+                        # Neumann ghost u_c + h g: eps_c (u_c - u_c - h g) / h^2
+                        b[c] += ec * g[f] / h
+    return A, b
