@@ -193,6 +193,19 @@ int mg_set_bc_patch(mg_ctx *ctx, int face, int a0, int a1, int b0, int b1,
  * The operator is unchanged (only the RHS adaptation uses the values); set
  * the RHS afterwards.  MG_ERR_BC on a periodic face (it has no boundary). */
 int mg_set_face_values(mg_ctx *ctx, int face, const double *values);
+/* Variable (jumping) permittivity (the solver "is extensible
+ * for discontinuous dielectricity coefficients ... by Galerkin coarsening",
+ * P:513-516): solves -div(eps grad Phi) = rho with eps[i] > 0 per
+ * cell (natural layout of the WHOLE domain, every rank passes the full
+ * array; NULL = constant 1, the paper's P:386-389).  Reading d10: face flux
+ * eps_f (Phi_c - Phi_n)/h^2 with the harmonic mean eps_f = 2 eps_c eps_n /
+ * (eps_c + eps_n); boundary faces use eps_c (Dirichlet: centre + 2 eps_c/h^2,
+ * f += 2 eps_c g/h^2; Neumann: f += eps_c g/h); coarse levels are the
+ * Galerkin R A P.  Combines with mg_set_mask / mg_set_bc_patch; not with
+ * periodic faces (MG_ERR_BC).  eps <= 0 -> MG_ERR_ARG.  Switches the context
+ * to the variable-coefficient kernels (fp64 records, 64 B per cell and
+ * level); set the RHS afterwards. */
+int mg_set_permittivity(mg_ctx *ctx, const double *eps, int where);
 /* The operator of level l as 7 coefficients per cell [centre, x-, x+, y-, y+,
  * z-, z+] (natural layout, the caller's part as mg_get_field), zeros on solid
  * cells.  For tests against the oracle's Galerkin stencils. */

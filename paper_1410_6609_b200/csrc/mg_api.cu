@@ -186,6 +186,7 @@ struct mg_ctx {
   bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   std::vector<uint8_t> solid_h;   // global solid mask (empty: none)
+  std::vector<double> eps_h;      // global cell permittivity (empty: 1)
   bool patched = false;           // per-face-cell BC arrays in use
   bool types_uniform = true;      // every face cell has its face's BC type
   std::vector<uint8_t> fty_h[6];  // face-cell BC types
@@ -695,6 +696,7 @@ void free_mask(mg_ctx *c) {
     for (Grid &g : lv) {
       g.codeR = g.codeB = nullptr;
       g.coefR = g.coefB = nullptr;
+      g.c64R = g.c64B = nullptr;
     }
   c->masked = false;
 }
@@ -1196,8 +1198,8 @@ int rebuild_coefficients(mg_ctx *c) {
   free_mask(c);
   c->fbc = mg::FaceBC{};
   c->dsolid = nullptr;
-  if (c->solid_h.empty() && !c->patched) return MG_OK;
-  const bool need_var = !c->solid_h.empty() || !c->types_uniform;
+  if (c->solid_h.empty() && !c->patched && c->eps_h.empty()) return MG_OK;
+  const bool need_var = !c->solid_h.empty() || !c->types_uniform || !c->eps_h.empty();
   unsigned char *dmask = nullptr;
   if (!c->solid_h.empty()) {
     CK(cudaMalloc(&dmask, c->solid_h.size()));
@@ -1222,6 +1224,55 @@ int rebuild_coefficients(mg_ctx *c) {
       c->fbc.va[q] = v;
     }
   if (!need_var) {  // only boundary values vary: box-domain operator, RHS only
+    c->prev_norm = -1.0;
+    return sync(c);
+  }
+  if (!c->eps_h.empty()) {
+    // variable permittivity (N4): fp64 records on every level, level 0 from
+    // eps, coarse levels by Galerkin R A P in the oracle's order
+    double *deps = nullptr;
+    CK(cudaMalloc(&deps, c->eps_h.size() * sizeof(double)));
+    c->mask_bufs.push_back(deps);
+    CK(cudaMemcpyAsync(deps, c->eps_h.data(), c->eps_h.size() * sizeof(double),
+                       cudaMemcpyHostToDevice, c->stream));
+    for (int l = 0; l < c->pl.L; l++)
+      for (Grid &g : c->g[l]) {
+        const size_t nb = (size_t)mg::grid_elems(g) * 8 * sizeof(double);
+        double *r = nullptr, *b = nullptr;
+        CK(cudaMalloc(&r, nb));
+        c->mask_bufs.push_back(r);
+        CK(cudaMalloc(&b, nb));
+        c->mask_bufs.push_back(b);
+        CK(cudaMemsetAsync(r, 0, nb, c->stream));
+        CK(cudaMemsetAsync(b, 0, nb, c->stream));
+        g.c64R = r;
+        g.c64B = b;
+      }
+    for (Grid &g : c->g[0])
+      mg::launch_level0_coef64(g, dmask, deps, c->fbc, const_cast<double *>(g.c64R),
+                               const_cast<double *>(g.c64B), c->stream);
+    for (int l = 1; l < c->pl.L; l++) {
+      for (int s = 0; s < (int)c->g[l - 1].size(); s++) {
+        const Grid &cg = coarse_of(c, l - 1, s);
+        mg::launch_coarse_coef64(c->g[l - 1][s], cg, const_cast<double *>(cg.c64R),
+                                 const_cast<double *>(cg.c64B), c->stream);
+      }
+      if (l == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
+        const Grid &G = c->g[l][0];
+        const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
+        double *R = const_cast<double *>(G.c64R), *B = const_cast<double *>(G.c64B);
+        int rc;
+        if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+        g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
+                         ncclDouble, c->comm, c->stream);
+        g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
+                         ncclDouble, c->comm, c->stream);
+        if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef64)"))) return rc;
+      }
+    }
+    CK(cudaGetLastError());
+    c->masked = true;
+    for (const Grid &g : c->g[0]) mg::launch_zero_solid(g, c->stream);
     c->prev_norm = -1.0;
     return sync(c);
   }
@@ -1318,6 +1369,32 @@ int mg_set_mask(mg_ctx *c, const uint8_t *solid, int where) {
     else
       memcpy(c->solid_h.data(), solid, N);
   }
+  return rebuild_coefficients(c);
+}
+
+static void init_face_arrays(mg_ctx *c);
+
+int mg_set_permittivity(mg_ctx *c, const double *eps, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  const size_t N = (size_t)c->pl.dims[0][0] * c->pl.dims[0][1] * c->pl.dims[0][2];
+  if (!eps) {
+    c->eps_h.clear();
+    return rebuild_coefficients(c);
+  }
+  if (any_periodic(c))
+    return fail(MG_ERR_BC, "a variable permittivity on a domain with periodic "
+                           "faces is not supported");
+  std::vector<double> e(N);
+  if (where == MG_DEVICE)
+    CK(cudaMemcpy(e.data(), eps, N * sizeof(double), cudaMemcpyDeviceToHost));
+  else if (where == MG_HOST)
+    memcpy(e.data(), eps, N * sizeof(double));
+  else
+    return fail(MG_ERR_ARG, "bad 'where' %d", where);
+  for (size_t k = 0; k < N; k++)
+    if (!(e[k] > 0.0)) return fail(MG_ERR_ARG, "eps[%zu] = %g is not > 0", k, e[k]);
+  c->eps_h.swap(e);
+  init_face_arrays(c);  // the eps-weighted RHS adaptation runs per face cell
   return rebuild_coefficients(c);
 }
 

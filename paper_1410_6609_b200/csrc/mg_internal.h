@@ -33,6 +33,10 @@ struct Grid {
   //             2 delta (0 = solid), coef[8 e + 7] = delta  (all dyadic, exact)
   const unsigned char *codeR, *codeB;
   const float *coefR, *coefB;
+  // variable permittivity (N4, reading d10): fp64 records per cell
+  // [kappa_q (6), D, eps_c (level 0) / 0]: a_q = -c kappa_q, a_cc = c D, with
+  // real-valued kappa (harmonic face means on level 0, Galerkin R A P below)
+  const double *c64R, *c64B;
   // periodic axes ("accessing unknowns in cells at opposite sides
   // of the domain"): per[a] = 1 for a periodic axis (dface = 0 on its faces).
   // Ghost layers then hold the opposite side's cells: rows 0 / ny+1 mirror
@@ -175,6 +179,13 @@ int launch_norm_partials_var(const Grid &g, double *partials, cudaStream_t s);
 void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
                           int *iters_out, cudaStream_t s);
 void launch_zero_solid(const Grid &g, cudaStream_t s);
+// fp64 records (permittivity): level 0 from eps (+ mask, face BC types), and
+// Galerkin R A P in the oracle's summation order for the coarse levels
+void launch_level0_coef64(const Grid &g, const unsigned char *solid_global,
+                          const double *eps_global, const FaceBC &fb,
+                          double *recR, double *recB, cudaStream_t s);
+void launch_coarse_coef64(const Grid &f, const Grid &c, double *recR,
+                          double *recB, cudaStream_t s);
 void launch_get_stencil(const Grid &g, double *out7, cudaStream_t s);
 // natural <-> split conversion of one field of a grid (phi: 0, f: 1)
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s);

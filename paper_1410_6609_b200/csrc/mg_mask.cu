@@ -51,7 +51,13 @@ struct Coef {
 // coefficients of the cell of colour col at split element e, global (i,j,z)
 __device__ __forceinline__ void coef_at(const Grid &g, int col, long long e,
                                         int i, int j, int z, Coef &C) {
-  if (g.coefR == nullptr) {
+  if (g.c64R) {  // permittivity: fp64 records
+    const double *r = (col ? g.c64B : g.c64R) + 8 * e;
+#pragma unroll
+    for (int q = 0; q < 6; q++) C.k[q] = r[q];
+    C.D = r[6];
+    C.delta = r[7];
+  } else if (g.coefR == nullptr) {
     const unsigned cd = (col ? g.codeB : g.codeR)[e];
     int n = 0;
 #pragma unroll
@@ -235,13 +241,16 @@ __global__ void __launch_bounds__(kT)
   for (int z = 0; z < g.nz; z += step) {
     const int col = (i + j + z) & 1;
     const long long e = b + (z >> 1);
-    if (g.codeR || g.coefR) {  // masked cells are not unknowns
+    if (g.codeR || g.coefR || g.c64R) {  // masked cells are not unknowns
       Coef C;
       coef_at(g, col, e, i, j, z, C);
       if (C.D == 0.0) continue;
     }
     double *f = col ? g.fB : g.fR;
     double v = f[e];
+    // variable permittivity (d10): alpha = -eps_c / h^2, the oracle's form
+    const double al =
+        g.c64R ? -((col ? g.c64B : g.c64R)[8 * e + 7] * (1.0 / (h * h))) : alpha;
     const bool on[6] = {i == 0, i == g.nx - 1, j == 0, j == g.ny - 1, z == 0,
                         z == g.nz - 1};
     for (int q = 0; q < 6; q++) {
@@ -249,7 +258,7 @@ __global__ void __launch_bounds__(kT)
       const long long fi = face_idx(g, q, i, j, z);
       const bool dir = fb.ty[q] ? fb.ty[q][fi] == 0 : g.dface[q] > 0;
       const double gv = fb.va[q][fi];
-      v = dir ? v - 2.0 * alpha * gv : v - alpha * (h * gv);
+      v = dir ? v - 2.0 * al * gv : v - al * (h * gv);
     }
     f[e] = v;
   }
@@ -308,6 +317,109 @@ void launch_coarse_coef(const Grid &f, const Grid &c, float *coefR,
                         float *coefB, cudaStream_t s) {
   const long long n = (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
   if (n > 0) k_coarse_coef<<<nblk(n), kT, 0, s>>>(f, c, coefR, coefB);
+}
+
+// ---- fp64 records for a variable permittivity (N4, reading d10) ----------------
+// level 0, the oracle's assemble_finest_eps in kappa units (a = -kappa / h^2,
+// a_cc = D / h^2, exact scalings for power-of-two h): per face in order x-,
+// x+, y-, y+, z-, z+: fluid neighbour kappa = (2 eps_c eps_n)/(eps_c + eps_n)
+// and D += kappa; Dirichlet boundary D += 2 eps_c; Neumann / solid nothing.
+__global__ void __launch_bounds__(kT)
+    k_level0_coef64(Grid g, const unsigned char *solid, const double *eps,
+                    FaceBC fb, double *recR, double *recB) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)g.nxl * g.ny * g.nz) return;
+  const int z = (int)(t % g.nz);
+  const long long q = t / g.nz;
+  const int j = (int)(q % g.ny);
+  const int il = (int)(q / g.ny);
+  const int i = g.x0 + il;
+  auto gidx = [&](int a, int b, int c) { return ((long long)a * g.ny + b) * g.nz + c; };
+  auto fluid = [&](int a, int b, int c) -> bool {
+    return !solid || solid[gidx(a, b, c)] == 0;
+  };
+  double rec[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  if (fluid(i, j, z)) {
+    const int di[6] = {-1, 1, 0, 0, 0, 0}, dj[6] = {0, 0, -1, 1, 0, 0},
+              dk[6] = {0, 0, 0, 0, -1, 1};
+    const double ec = eps[gidx(i, j, z)];
+    double D = 0.0;
+    for (int f = 0; f < 6; f++) {
+      const int a = i + di[f], b = j + dj[f], c = z + dk[f];
+      if (a < 0 || b < 0 || c < 0 || a >= g.nx || b >= g.ny || c >= g.nz) {
+        if (face_dirichlet(g, fb, f, i, j, z)) D = D + 2.0 * ec;
+      } else if (fluid(a, b, c)) {
+        const double en = eps[gidx(a, b, c)];
+        const double ef = (2.0 * ec * en) / (ec + en);
+        rec[f] = ef;
+        D = D + ef;
+      }
+    }
+    rec[6] = D;
+    rec[7] = ec;
+  }
+  const int col = (i + j + z) & 1;
+  double *out = (col ? recB : recR) + 8 * (rb(g, il, j) + (z >> 1));
+  for (int r = 0; r < 8; r++) out[r] = rec[r];
+}
+
+void launch_level0_coef64(const Grid &g, const unsigned char *solid_global,
+                          const double *eps_global, const FaceBC &fb,
+                          double *recR, double *recB, cudaStream_t s) {
+  const long long n = (long long)g.nxl * g.ny * g.nz;
+  if (n > 0)
+    k_level0_coef64<<<nblk(n), kT, 0, s>>>(g, solid_global, eps_global, fb, recR, recB);
+}
+
+// Galerkin R A P in the oracle's order (galerkin(): children
+// (a,b,c) lexicographic, per child its centre then faces x-..z+; a face to a
+// sibling adds to the centre, any other to that face), in kappa units: the
+// fine centre D and -kappa of sibling faces into sD, kappa into sK[q]; the
+// coarse record is 0.25 * (sD, sK) (= 1/8 and the level scale 2, exact).
+// kappa = 0 (boundary / solid neighbour) adds an exact zero.
+__global__ void __launch_bounds__(kT)
+    k_coarse_coef64(Grid F, Grid C, double *recR, double *recB) {
+  const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (long long)ncx * ncy * ncz) return;
+  const int K = (int)(t % ncz);
+  const long long q = t / ncz;
+  const int J = (int)(q % ncy);
+  const int Il = (int)(q / ncy);
+  double sD = 0.0, sK[6] = {0, 0, 0, 0, 0, 0};
+  bool any = false;
+  for (int a = 0; a < 2; a++)
+    for (int b = 0; b < 2; b++)
+      for (int c = 0; c < 2; c++) {
+        const int il = 2 * Il + a, j = 2 * J + b, z = 2 * K + c;
+        const int i = F.x0 + il;
+        const int col = (i + j + z) & 1;
+        const double *r = (col ? F.c64B : F.c64R) + 8 * (rb(F, il, j) + (z >> 1));
+        if (r[6] == 0.0) continue;  // solid: not an unknown
+        any = true;
+        sD = sD + r[6];
+        const bool sib[6] = {a == 1, a == 0, b == 1, b == 0, c == 1, c == 0};
+#pragma unroll
+        for (int f = 0; f < 6; f++) {
+          if (r[f] == 0.0) continue;  // boundary or solid neighbour
+          if (sib[f])
+            sD = sD - r[f];
+          else
+            sK[f] = sK[f] + r[f];
+        }
+      }
+  const int Ig = (F.x0 >> 1) + Il;
+  const int col = (Ig + J + K) & 1;
+  double *out = (col ? recB : recR) + 8 * (rb(C, Ig - C.x0, J) + (K >> 1));
+  for (int f = 0; f < 6; f++) out[f] = any ? 0.25 * sK[f] : 0.0;
+  out[6] = any ? 0.25 * sD : 0.0;
+  out[7] = 0.0;
+}
+
+void launch_coarse_coef64(const Grid &f, const Grid &c, double *recR,
+                          double *recB, cudaStream_t s) {
+  const long long n = (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
+  if (n > 0) k_coarse_coef64<<<nblk(n), kT, 0, s>>>(f, c, recR, recB);
 }
 
 // ---- float records -> byte codes, when every kappa is 0 or 1 ------------------
@@ -585,7 +697,7 @@ __global__ void __launch_bounds__(kT) k_zero_solid(Grid g) {
 
 void launch_zero_solid(const Grid &g, cudaStream_t s) {
   const long long n = (long long)g.nxl * g.ny * g.nz;
-  if (n > 0 && (g.codeR || g.coefR)) k_zero_solid<<<nblk(n), kT, 0, s>>>(g);
+  if (n > 0 && (g.codeR || g.coefR || g.c64R)) k_zero_solid<<<nblk(n), kT, 0, s>>>(g);
 }
 
 // ---- operator of a level as 7 coefficients per cell, natural layout ------------
@@ -598,7 +710,7 @@ __global__ void __launch_bounds__(kT) k_get_stencil(Grid g, double *out) {
   const int il = (int)(q / g.ny);
   const int i = g.x0 + il;
   double *o = out + 7 * t;
-  if (g.codeR || g.coefR) {
+  if (g.codeR || g.coefR || g.c64R) {
     const int col = (i + j + z) & 1;
     Coef C;
     coef_at(g, col, rb(g, il, j) + (z >> 1), i, j, z, C);

@@ -123,6 +123,7 @@ def lib():
         L.mg_set_mask.argtypes = [P, dp, i]
         L.mg_set_bc_patch.argtypes = [P, i, i, i, i, i, i, d]
         L.mg_set_face_values.argtypes = [P, i, dp]
+        L.mg_set_permittivity.argtypes = [P, dp, i]
         L.mg_coulomb_forces.argtypes = [P, i, dp, dp, dp, i, i, dp]
         L.mg_timestep.argtypes = [P, i, dp, dp, dp, i, i, i, d, dp, i, ip,
                                   ctypes.POINTER(ctypes.c_double)]
@@ -384,6 +385,15 @@ class Multigrid:
         _check(lib().mg_set_bc_patch(self._ctx, int(face), int(a0), int(a1),
                                      int(b0), int(b1), int(bc_type),
                                      float(value)), self._ctx)
+
+    def set_permittivity(self, eps):
+        """Cell permittivity (whole domain, natural layout); None = 1."""
+        if eps is None:
+            _check(lib().mg_set_permittivity(self._ctx, None, MG_HOST), self._ctx)
+            return
+        e = np.ascontiguousarray(eps, np.float64)
+        _check(lib().mg_set_permittivity(self._ctx, _host_ptr(e), MG_HOST),
+               self._ctx)
 
     def set_face_values(self, face, values):
         """Per-cell boundary values of face `face` (in-face (a, b) order)."""
