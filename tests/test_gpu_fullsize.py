@@ -1,0 +1,161 @@
+"""Parity at BASELINE.json's full sizes, in the launch configuration bench.py
+times (one B200; CUDA graph; the default kernels).
+
+* config 3 (512^3, 20 V(2,2)-cycles) and config 4 at P = 1 (512^3 channel +
+  7,417 spheres, V(2,2) to 1e-8): the CPU oracle runs the same schedule at
+  full size (about 15 GB of host memory, tens of seconds on the box's
+  cores); Phi rel-L2 <= 1e-10 and the residual-history clause.
+* config 5 (2048 x 512 x 512, beam mask + 50,000 spheres, V(3,3)): too large
+  for a whole-grid oracle run inside the test budget, so sampled outputs are
+  checked one by one: for each sampled cell (or coarse cell) the oracle runs
+  the same step on a small box cut around it (the domain's BC types where the
+  box touches the domain boundary, the same solid cells), which determines
+  that cell's result exactly -- bitwise equality with the full-size GPU step.
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_6609_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_6609_b200 import _build
+    _build.build()
+    from paper_1410_6609_b200 import mg as M
+    return M
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def check_history(hg, ho):
+    assert len(hg) == len(ho)
+    r0 = ho[0]
+    for a, b in zip(hg, ho):
+        assert abs(a - b) <= 1e-8 * b + 1e-14 * r0, (a, b)
+
+
+def bench_solver(mg, w, **kw):
+    """The context bench.py times: own torch stream, graph capture, m_c = 8."""
+    import torch
+    stream = torch.cuda.Stream()
+    return mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, stream=stream,
+                        min_coarse=w.min_coarse, nu1=w.nu1, nu2=w.nu2, **kw)
+
+
+def test_config3_full_size_parity(mg):
+    w = W.cfg3(512, seed=0, cycles=20)
+    s = bench_solver(mg, w)
+    s.set_rhs(w.rhs)
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(w.cycles)]
+    pg = s.get_solution()
+    s.close()
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
+    o.set_rhs(w.rhs)
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(w.cycles)]
+    check_history(hg, ho)
+    assert rel(pg, o.phi()) <= 1e-10
+
+
+def test_config4_full_size_parity(mg):
+    w = W.cfg4(P=1, n=512, seed=0)
+    s = bench_solver(mg, w)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    rc, cg, hg = s.solve(w.tol, 40)
+    pg = s.get_solution()
+    s.close()
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    so, co, ho = o.solve(w.tol, 40)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(pg, o.phi()) <= 1e-10
+
+
+# --------------------------------------------------------------------------
+# sampled checks at config-5 size
+# --------------------------------------------------------------------------
+def local_box(shape, lo, hi, w, solid):
+    """Oracle on the sub-box [lo, hi) of the domain: the domain's BC types on
+    box faces that lie on the domain boundary, Dirichlet 0 on cut faces
+    (they only affect the box's outer cells, never the sampled one)."""
+    bt, bv = [], []
+    for a in range(3):
+        for side, at_edge in ((0, lo[a] == 0), (1, hi[a] == shape[a])):
+            q = 2 * a + side
+            bt.append(w.bc_type[q] if at_edge else 0)
+            bv.append(w.bc_value[q] if at_edge else 0.0)
+    sl = tuple(slice(lo[a], hi[a]) for a in range(3))
+    sub = tuple(hi[a] - lo[a] for a in range(3))
+    o = oracle.Oracle(sub, w.h, bt, bv, solid=np.ascontiguousarray(solid[sl]),
+                      min_coarse=1, max_levels=2, nu1=w.nu1, nu2=w.nu2)
+    return o, sl
+
+
+def test_config5_full_size_sampled_steps(mg):
+    w = W.cfg5(scale=1)
+    s = bench_solver(mg, w)
+    s.set_mask(w.solid)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    for _ in range(2):
+        s.vcycle()
+    phi0 = s.get_solution()
+    f0 = s.get_field(0, mg.MG_FIELD_RHS)
+    rng = np.random.default_rng(17)
+    shape = w.shape
+    # samples: random cells, plus cells at the domain faces and the beam
+    (bx0, _), (by0, by1), _ = W.beam_box(shape)
+    pts = [tuple(rng.integers(0, n) for n in shape) for _ in range(150)]
+    pts += [(0, 5, 7), (shape[0] - 1, 100, 3), (77, 0, 511), (1000, 511, 0),
+            (bx0 - 1, by0, 200), (bx0 + 3, by0 - 1, 9), (1800, by1, 300),
+            (2047, 511, 511)]
+
+    # (1) one red half-sweep on the full grid (TMA marching kernel)
+    s.smooth_half(0, 0)
+    phi1 = s.get_solution()
+    checked = 0
+    for (i, j, k) in pts:
+        if (i + j + k) & 1 or w.solid[i, j, k]:
+            continue
+        lo = [max(0, x - 1) for x in (i, j, k)]
+        hi = [min(n, x + 2) for x, n in zip((i, j, k), shape)]
+        o, sl = local_box(shape, lo, hi, w, w.solid)
+        o.set_phi(np.ascontiguousarray(phi0[sl]))
+        o.set_rhs_raw(np.ascontiguousarray(f0[sl]))
+        col = (lo[0] + lo[1] + lo[2]) & 1  # local parity of a global red cell
+        o.smooth_half(0, col)
+        assert o.phi()[i - lo[0], j - lo[1], k - lo[2]] == phi1[i, j, k], (i, j, k)
+        checked += 1
+    assert checked >= 60
+
+    # (2) residual + restriction of the full grid (TMA residual kernel)
+    s.residual_restrict(0)
+    f1 = s.get_field(1, mg.MG_FIELD_RHS)
+    checked = 0
+    for (i, j, k) in pts:
+        I, J, K = i // 2, j // 2, k // 2
+        lo, hi = [], []
+        for X, n in zip((I, J, K), shape):
+            a = min(max(0, 2 * X - 2), n - 8)
+            a -= a & 1
+            lo.append(a)
+            hi.append(a + 8)
+        o, sl = local_box(shape, lo, hi, w, w.solid)
+        assert o.nlevels == 2
+        o.set_phi(np.ascontiguousarray(phi1[sl]))
+        o.set_rhs_raw(np.ascontiguousarray(f0[sl]))
+        o.restrict_residual(0)
+        got = f1[I, J, K]
+        exp = o.rhs(1)[I - lo[0] // 2, J - lo[1] // 2, K - lo[2] // 2]
+        assert got == exp, (I, J, K, got, exp)
+        checked += 1
+    assert checked == len(pts)
+    s.close()
