@@ -326,10 +326,13 @@ def run_cuda(args):
     s.set_profiling(False)
     sm0 = np.mean([p["smooth0_ms"] for p in prof])
     nsm = prof[0]["smooth0_launches"]
+    hs_per_launch = prof[0]["smooth0_halfsweeps"] / nsm  # 4: temporally blocked
     cyc_prof = np.mean([p["cycle_ms"] for p in prof])
     per_launch_ms = sm0 / nsm
     local_cells = cells // N
-    alg_bytes = HALF_SWEEP_BYTES_PER_CELL * local_cells
+    # SURVEY 8(d) per-unit figure (12 B per cell and half-sweep) x the
+    # half-sweeps one launch performs
+    alg_bytes = int(HALF_SWEEP_BYTES_PER_CELL * hs_per_launch * local_cells)
     achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
@@ -337,7 +340,8 @@ def run_cuda(args):
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
-            if tj.get("cells") == local_cells:
+            kname = "k_sweep4" if hs_per_launch == 4 else "k_smooth_march"
+            if tj.get("cells") == local_cells and tj.get("kernel") == kname:
                 traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
@@ -391,7 +395,11 @@ def run_cuda(args):
                    "parallelism": "x-slab x%d (NCCL halo)" % N if N > 1 else "single GPU",
                    "l2": "inputs larger than L2 (hierarchy %.2f GB vs 126 MB L2); no flush"
                          % (mg.workspace_bytes(shape, min_coarse=8) / 1e9 / N)},
-        "roofline": {"bound": "hbm", "kernel": "k_smooth (level-0 RBGS half-sweep)",
+        "roofline": {"bound": "hbm",
+                     "kernel": ("k_sweep4 (level-0 V(2,2) pre-smoothing pass: 4 RBGS "
+                                "half-sweeps, temporally blocked)" if hs_per_launch == 4
+                                else "k_smooth_march (level-0 RBGS half-sweep)"),
+                     "halfsweeps_per_launch": int(hs_per_launch),
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes,

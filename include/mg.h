@@ -323,6 +323,13 @@ int mg_set_profiling(mg_ctx *ctx, int on);
  *   out[6] whole cycle (first to last kernel) out[7] kernel launches/cycle
  * MG_ERR_ARG if profiling was off during the last cycle. */
 int mg_last_cycle_times(mg_ctx *ctx, double out[8]);
+/* As mg_last_cycle_times, n >= 10 outputs, plus
+ *   out[8] level-0 smoothing launches timed in out[0]
+ *   out[9] level-0 half-sweeps they perform (4 per launch with the
+ *          temporally blocked V(2,2) passes; 1 otherwise)
+ * With the temporally blocked passes out[0] times the pre-smoothing pass and
+ * out[3] the prolongation + post-smoothing pass of level 0. */
+int mg_last_cycle_times_ex(mg_ctx *ctx, double *out, int n);
 /* Number of kernels one mg_vcycle launches (counted when it is recorded). */
 int mg_cycle_launches(const mg_ctx *ctx);
 /* cudaStream_t of the context (for event timing by the caller). */

@@ -175,7 +175,10 @@ struct TmPair {
   alignas(64) unsigned char rr[128];  // z-tiled boxes (residual kernels)
   alignas(64) unsigned char rb[128];
   alignas(64) unsigned char r12[128]; // 12-row red boxes (fused kernels)
-  bool ok = false, ok_resid = false, ok_fused = false;
+  alignas(64) unsigned char t4a[256]; // temporally blocked pass: input phiB
+  alignas(64) unsigned char t4b[256]; //                         input phiB2
+  alignas(64) unsigned char rb2[128]; // z-tiled boxes of phiB2 (residual)
+  bool ok = false, ok_resid = false, ok_fused = false, ok_t4 = false;
 };
 
 struct mg_ctx {
@@ -183,6 +186,8 @@ struct mg_ctx {
   std::vector<std::vector<TmPair>> tm;
   int use_march = 1;
   int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
+  int use_t4 = 0;     // temporally blocked V(2,2) passes (opt-in: MG_T4=1)
+  int t4_ty = 16;     // their tile rows (MG_T4_TY=8|16)
   bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   std::vector<uint8_t> solid_h;   // global solid mask (empty: none)
@@ -246,6 +251,14 @@ struct Carver {
   }
 };
 
+// the temporally blocked V(2,2) passes (mg_t4.cu) are opt-in: correct and
+// bitwise equal, but slower than four marching half-sweeps on B200 today
+// (DESIGN.md); their second black arrays are only carved when requested
+bool t4_requested() {
+  const char *e = getenv("MG_T4");
+  return e && atoi(e) != 0;
+}
+
 size_t carve(mg_ctx *c, char *base) {
   Carver cv{base};
   const int L = c->pl.L;
@@ -265,6 +278,10 @@ size_t carve(mg_ctx *c, char *base) {
       gr.phiB = (double *)cv.take(bytes);
       gr.fR = (double *)cv.take(bytes);
       gr.fB = (double *)cv.take(bytes);
+      // second black array for the temporally blocked passes (levels held
+      // whole: one slab, or agglomerated)
+      gr.phiB2 = (gr.nxl == gr.nx && t4_requested()) ? (double *)cv.take(bytes)
+                                                      : nullptr;
       c->g[l].push_back(gr);
     }
   }
@@ -539,6 +556,52 @@ int enqueue_norm(mg_ctx *c) {
   return MG_OK;
 }
 
+// temporally blocked V(2,2) passes on level l (mg_t4.cu)?
+bool use_t4(const mg_ctx *c, int l) {
+  if (!c->use_t4 || !c->use_march || c->masked || any_periodic(c)) return false;
+  if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
+  const Grid &g = c->g[l][0];
+  // large levels only: on the small ones the per-half-sweep kernels (or their
+  // launch latency) cost less than the wavefront's halo work
+  return c->tm[l][0].ok_t4 && mg::sweep4_supported(g) && g.nzh >= 64 && g.ny >= 32;
+}
+
+// pre-smoothing (4 half-sweeps) -> red in phiR, black in phiB2; then
+// f_{l+1} = R (f_l - A_l Phi_l) reading black from phiB2
+int t4_pre_restrict(mg_ctx *c, int l) {
+  const Grid &g = c->g[l][0];
+  const TmPair &t = c->tm[l][0];
+  Grid go = g;
+  go.phiB = g.phiB2;
+  if (l == 0) mark(c, CAT_NONE);
+  mg::launch_sweep4(go, g, t.t4a, false, l > 0, 0.0, c->t4_ty, c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_SMOOTH0);
+  CK(cudaGetLastError());
+  const Grid &cg = coarse_of(c, l, 0);
+  if (t.ok_resid && c->use_march)
+    mg::launch_resid_restrict_march(go, cg, t.rr, t.rb2, c->stream);
+  else
+    mg::launch_resid_restrict(go, cg, 0, c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_RESTRICT0);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+// prolongation + magnified correction of the black from phiB2, then the 4
+// post-smoothing half-sweeps -> red in phiR, black back in phiB
+int t4_prolong_post(mg_ctx *c, int l) {
+  const Grid &g = c->g[l][0];
+  if (l == 0) mark(c, CAT_NONE);
+  mg::launch_sweep4(g, coarse_of(c, l, 0), c->tm[l][0].t4b, true, false, c->o.alpha,
+                    c->t4_ty, c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_PROLONG0);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
 int enqueue_vcycle(mg_ctx *c) {
   const int L = c->pl.L;
   int rc;
@@ -551,6 +614,10 @@ int enqueue_vcycle(mg_ctx *c) {
         CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
         CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
       }
+    if (use_t4(c, l)) {
+      if ((rc = t4_pre_restrict(c, l))) return rc;
+      continue;
+    }
     const bool fuse_r = c->o.nu1 >= 1 && can_fuse_resid(c, l);
     for (int s = 0; s < c->o.nu1; s++) {
       if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
@@ -567,6 +634,10 @@ int enqueue_vcycle(mg_ctx *c) {
   if ((rc = coarse_solve(c))) return rc;
   for (int l = L - 2; l >= 0; l--) {
     if (l == 0) mark(c, CAT_COARSE);
+    if (use_t4(c, l)) {
+      if ((rc = t4_prolong_post(c, l))) return rc;
+      continue;
+    }
     const bool fuse = can_fuse_prolong(c, l);
     if (fuse) {
       if ((rc = prolong_red_level(c, l))) return rc;
@@ -941,10 +1012,16 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
                    mg::make_tmap_resid(g, g.phiB, t.rb);
       t.ok_fused = t.ok_resid && mg::fused_supported(g) &&
                    mg::make_tmap_red12(g, g.phiR, t.r12);
+      t.ok_t4 = g.phiB2 && mg::sweep4_supported(g) &&
+                mg::make_tmap_sweep4(g, g.phiB, t.t4a) &&
+                mg::make_tmap_sweep4(g, g.phiB2, t.t4b) &&
+                (!t.ok_resid || mg::make_tmap_resid(g, g.phiB2, t.rb2));
     }
   }
   if (getenv("MG_NO_MARCH")) c->use_march = 0;
   if (getenv("MG_FUSED")) c->use_fused = 1;
+  if (t4_requested()) c->use_t4 = 1;
+  if (const char *e = getenv("MG_T4_TY")) c->t4_ty = atoi(e) == 8 ? 8 : 16;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
   e = cudaMallocHost(&c->h_norm, sizeof(double) * 2);
@@ -1604,6 +1681,15 @@ int mg_last_cycle_times(mg_ctx *c, double out[8]) {
   CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[c->nev - 1]));
   out[6] = tot;
   out[7] = c->cycle_launches;
+  return MG_OK;
+}
+
+int mg_last_cycle_times_ex(mg_ctx *c, double *out, int n) {
+  if (!c || !out || n < 10) return fail(MG_ERR_ARG, "need 10 outputs");
+  int rc = mg_last_cycle_times(c, out);
+  if (rc) return rc;
+  out[8] = out[1];                               // level-0 smoothing launches
+  out[9] = out[1] * (use_t4(c, 0) ? 4.0 : 1.0);  // level-0 half-sweeps in them
   return MG_OK;
 }
 

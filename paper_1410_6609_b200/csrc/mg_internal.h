@@ -45,6 +45,10 @@ struct Grid {
   // has no ghosts: kernels wrap the half-index of z neighbours (per[2]).
   int per[3];
   int gx;  // x periodic and the grid held whole: its writers fill x ghosts
+  // second black array (temporally blocked smoother, mg_t4.cu): the fused
+  // pre-smoothing pass writes its final black values here, the fused
+  // post-smoothing pass reads them back (null: not allocated)
+  double *phiB2;
 };
 
 __host__ __device__ inline long long grid_elems(const Grid &g) {
@@ -147,6 +151,16 @@ void launch_black_restrict(const Grid &g, const Grid &c, const void *tm_red12,
                            cudaStream_t s);
 int launch_black_norm(const Grid &g, const void *tm_red12, double *partials,
                       cudaStream_t s);
+// temporally blocked V(2,2) smoothing pass (mg_t4.cu): 4 half-sweeps
+// (red, black, red, black) in one kernel; reads black from the array of
+// tm256 (two tensor maps: 8- and 16-row tiles), writes red to g.phiR and the
+// final black to g.phiB.  prolong: first add alpha * e(parent) to the input
+// black; from_zero: the input black is 0 (first pre-smoothing on a coarse
+// level).  ty: tile rows (8 or 16).
+bool sweep4_supported(const Grid &g);
+bool make_tmap_sweep4(const Grid &g, const double *base, void *out256);
+void launch_sweep4(const Grid &g, const Grid &c, const void *tm256, bool prolong,
+                   bool from_zero, double alpha, int ty, cudaStream_t s);
 // per-face-cell boundary conditions (mg_set_bc_patch); null = face-uniform.
 // Face q cell (a, b): q<2 -> (j, z), q<4 -> (i, z), else (i, j); index a*nb+b
 struct FaceBC {

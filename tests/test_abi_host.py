@@ -98,10 +98,16 @@ def test_plan_errors():
 
 
 def test_workspace_bytes_model():
-    """Split layout: 4 fields per level, ghost planes/rows, pitch nz/2 -> x4."""
+    """Split layout: 4 fields per level (the opt-in temporally blocked
+    passes, MG_T4=1, add a second black array), ghost planes/rows, pitch
+    nz/2 -> x4."""
     nb = mg.workspace_bytes((512, 512, 512), min_coarse=8)
     fine = 4 * 514 * 514 * 256 * 8
     assert fine < nb < fine * 1.2
+    nb2 = mg.workspace_bytes((1024, 512, 512), min_coarse=8, nranks=2,
+                             halo="nccl")
+    slab = 4 * 514 * 514 * 256 * 8
+    assert slab < nb2 < slab * 1.2
     assert mg.workspace_bytes((7, 8, 8)) == 0
 
 

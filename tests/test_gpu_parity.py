@@ -744,3 +744,27 @@ def test_coulomb_force_homogeneous_field_table5(mg):
                     assert abs(e - ev) < 2e-3, (R, sF, e, ev)
                 else:
                     assert abs(e) < 0.08, (R, sF, sP, e)
+
+
+@pytest.mark.parametrize("shape,bc,h", [((256, 128, 128), "mixed", 1.0),
+                                        ((128, 64, 256), "channel", 0.5),
+                                        ((64, 96, 130), "dirichlet", 0.25)])
+def test_temporal_blocking_equals_half_sweeps(mg, shape, bc, h, monkeypatch):
+    """The temporally blocked V(2,2) passes (opt-in MG_T4=1: 4 half-sweeps
+    per kernel, its own reciprocal-based correctly rounded division) give the
+    same V-cycle iterates as the one-half-sweep-per-kernel path, bit for
+    bit."""
+    f = np.random.default_rng(21).uniform(-1, 1, shape)
+    out = []
+    for t4 in (True, False):
+        if t4:
+            monkeypatch.setenv("MG_T4", "1")
+        else:
+            monkeypatch.delenv("MG_T4")
+        s, _ = pair(mg, shape, h, bc, min_coarse=2)
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(3)]
+        out.append((r, s.get_solution()))
+        s.close()
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][0] == out[1][0]
