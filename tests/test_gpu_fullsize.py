@@ -5,6 +5,8 @@ times (one B200; CUDA graph; the default kernels).
   7,417 spheres, V(2,2) to 1e-8): the CPU oracle runs the same schedule at
   full size (about 15 GB of host memory, tens of seconds on the box's
   cores); Phi rel-L2 <= 1e-10 and the residual-history clause.
+* 1024^3 (the largest cube kept on one B200 here): cycle reduction and
+  sampled half-sweep cells, as for config 5.
 * config 5 (2048 x 512 x 512, beam mask + 50,000 spheres, V(3,3)): too large
   for a whole-grid oracle run inside the test budget, so sampled outputs are
   checked one by one: for each sampled cell (or coarse cell) the oracle runs
@@ -158,4 +160,42 @@ def test_config5_full_size_sampled_steps(mg):
         assert got == exp, (I, J, K, got, exp)
         checked += 1
     assert checked == len(pts)
+    s.close()
+
+
+def test_max_size_1024_cubed_sampled(mg):
+    """The largest cube that fits comfortably on one B200 (1024^3 = 1.07e9
+    cells, ~20 GB of hierarchy; 64-bit offsets everywhere): two V(2,2)
+    cycles reduce the residual like the 512^3 case (property), and sampled
+    cells of a full-grid black half-sweep equal the oracle's cut-box results
+    bitwise."""
+    n = 1024
+    w = W.cfg3(n, seed=3, cycles=2, with_rhs=False)
+    s = bench_solver(mg, w)
+    f = np.random.default_rng(3).uniform(-1, 1, w.shape)
+    s.set_rhs(f)
+    r = [s.residual_norm()] + [s.vcycle() for _ in range(2)]
+    assert r[1] < 0.5 * r[0] and r[2] < 0.3 * r[1]
+    phi0 = s.get_solution()
+    s.smooth_half(0, 1)
+    phi1 = s.get_solution()
+    rng = np.random.default_rng(5)
+    pts = [tuple(int(x) for x in rng.integers(0, n, 3)) for _ in range(60)]
+    pts += [(0, 0, 1), (n - 1, n - 1, n - 2), (n - 1, 0, n - 1), (512, 1023, 0)]
+    checked = 0
+    for (i, j, k) in pts:
+        if not (i + j + k) & 1:
+            continue
+        lo = [max(0, x - 1) for x in (i, j, k)]
+        hi = [min(n, x + 2) for x in (i, j, k)]
+        sl = tuple(slice(a, b) for a, b in zip(lo, hi))
+        bt = [0] * 6   # all faces Dirichlet 0 (config 3); cut faces likewise
+        o = oracle.Oracle(tuple(b - a for a, b in zip(lo, hi)), w.h, bt, [0.0] * 6,
+                          min_coarse=1, max_levels=1)
+        o.set_phi(np.ascontiguousarray(phi0[sl]))
+        o.set_rhs_raw(np.ascontiguousarray(f[sl]))
+        o.smooth_half(0, 1 ^ ((lo[0] + lo[1] + lo[2]) & 1))
+        assert o.phi()[i - lo[0], j - lo[1], k - lo[2]] == phi1[i, j, k], (i, j, k)
+        checked += 1
+    assert checked >= 20
     s.close()
