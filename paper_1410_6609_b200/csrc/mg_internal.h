@@ -102,6 +102,27 @@ __device__ __forceinline__ double z_hi0(const Grid &g, const double *row, int k,
   return (PER && g.per[2] && k + 1 >= g.nzh) ? row[0] : next;
 }
 
+// Correctly rounded a / d for a small positive integer d (a smoother's
+// centre, 1..15) from rd = RN(1/d): q0 = RN(a rd) is within 2 ulp of a/d;
+// one FMA residual step brings it within 1 ulp, and the final Markstein step
+// q = RN(q1 + RN(a - d q1) rd) -- exact residual by the FMA, rd within half
+// an ulp of 1/d -- is RN(a/d) (no overflow / underflow at the smoothers'
+// magnitudes).  Bitwise equal to IEEE a / d (except possibly the sign of an
+// exact zero) at a quarter of the instructions; the half-sweep parity tests
+// and test_temporal_blocking_equals_half_sweeps check it against `/`.
+__device__ __forceinline__ double div_small(double a, double d, double rd) {
+  const double q0 = __dmul_rn(a, rd);
+  const double r0 = __fma_rn(-q0, d, a);
+  const double q1 = __fma_rn(r0, rd, q0);
+  const double r1 = __fma_rn(-q1, d, a);
+  return __fma_rn(r1, rd, q1);
+}
+
+// RN(1/d) for d = 0..15 into a shared table (IEEE division; entry 0 unused)
+__device__ __forceinline__ void fill_rcp16(double *rcp) {
+  if (threadIdx.x < 16) rcp[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
+}
+
 __host__ __device__ inline bool is_periodic(const Grid &g) {
   return g.per[0] || g.per[1] || g.per[2];
 }

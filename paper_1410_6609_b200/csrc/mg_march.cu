@@ -62,6 +62,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   const int nplanes = (i1 - i0) + 2;  // local planes i0-1 .. i1
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
+  __shared__ double rcp[PROLONG ? 1 : 16];  // RN(1/d) for the exact division
+  if (!PROLONG) fill_rcp16(rcp);
   if (threadIdx.x == 0) {
     for (int s = 0; s < kSlots; s++) mbar_init(&bars[s], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -262,8 +264,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           d1 = (double)centre_dm(g, i, j, z0 + 2);
         }
         double2 out;
-        out.x = (fr[c].x * g.w + s0) / d0;
-        out.y = (fr[c].y * g.w + s1) / d1;
+        if (PROLONG) {  // (measured: the IEEE division schedules better here)
+          out.x = (fr[c].x * g.w + s0) / d0;
+          out.y = (fr[c].y * g.w + s1) / d1;
+        } else {
+          out.x = div_small(fr[c].x * g.w + s0, d0, rcp[(int)d0]);
+          out.y = div_small(fr[c].y * g.w + s1, d1, rcp[(int)d1]);
+        }
         const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
         if (both) {
           *reinterpret_cast<double2 *>(orow + k) = out;

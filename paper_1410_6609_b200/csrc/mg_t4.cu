@@ -66,23 +66,6 @@ struct T4 {
   static constexpr size_t smem = (size_t)total * 8 + kSlots4 * 8;
 };
 
-// Correctly rounded a / d for a small positive integer d (the smoother's
-// centre, 1..12) from rd = RN(1/d): q0 = RN(a rd) is within 2 ulp of a/d;
-// one FMA residual step brings it within half an ulp plus a tiny error
-// (within 1 ulp), and the final Markstein step q = RN(q1 + RN(a - d q1) rd)
-// -- exact residual by the FMA, rd within half an ulp of 1/d -- is RN(a/d)
-// (no overflow / underflow for the smoother's values).  Bitwise equal to
-// IEEE a / d except possibly the sign of an exact zero; checked against the
-// hardware division by tests/test_gpu_parity.py (bitwise half-sweeps) and
-// test_t4_division_exact.
-__device__ __forceinline__ double div_small(double a, double d, double rd) {
-  const double q0 = __dmul_rn(a, rd);
-  const double r0 = __fma_rn(-q0, d, a);
-  const double q1 = __fma_rn(r0, rd, q0);
-  const double r1 = __fma_rn(-q1, d, a);
-  return __fma_rn(r1, rd, q1);
-}
-
 }  // namespace
 
 // g: the level (phiR written, phiB = output black buffer); tmB: the input
@@ -123,7 +106,7 @@ __global__ void __launch_bounds__(TY * 32, (TY <= 8) ? 2 : 1)
     for (int e = threadIdx.x; e < kSlots4 * T::tile(0); e += T::NT) sb[e] = 0.0;
   // RN(1/d) for the possible centres d = 0..12 (IEEE division, once)
   __shared__ double rcp[16];
-  if (threadIdx.x < 16) rcp[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
+  fill_rcp16(rcp);
   __syncthreads();
   if (!FROMZERO && threadIdx.x == 0)
     for (int t = tfirst; t <= min(tfirst + 2, tlast); t++) issue(t);
