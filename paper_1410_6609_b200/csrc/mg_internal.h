@@ -118,6 +118,13 @@ __device__ __forceinline__ double div_small(double a, double d, double rd) {
   return __fma_rn(r1, rd, q1);
 }
 
+// a / d for a centre d: the exact reciprocal path for the interior centre 6
+// (RN(1/6) is a compile-time constant), IEEE division on boundary cells
+__device__ __forceinline__ double div_centre(double a, double d) {
+  constexpr double kRcp6 = 1.0 / 6.0;
+  return d == 6.0 ? div_small(a, 6.0, kRcp6) : a / d;
+}
+
 // RN(1/d) for d = 0..15 into a shared table (IEEE division; entry 0 unused)
 __device__ __forceinline__ void fill_rcp16(double *rcp) {
   if (threadIdx.x < 16) rcp[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
