@@ -130,14 +130,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const long long cb = poff + tCoff[m];
       E[m].x = (c0 ? C.phiB : C.phiR)[cb];
       E[m].y = (c0 ? C.phiR : C.phiB)[cb];
-      if (MASK) {  // solid cells of the other colour get no correction
-        // (array plane i0+q, array row jj+1 = j0+rr, element k)
-        const unsigned char *oc = (color ? g.codeR : g.codeB) +
-                                  (long long)(i0 + q) * g.plane +
-                                  (long long)j0 * pz + tRow[m] + tK[m];
-        if (!(oc[0] & 64)) E[m].x = 0.0;
-        if (tK[m] + 1 < g.nzh && !(oc[1] & 64)) E[m].y = 0.0;
-      }
+      // (MASK: a solid cell of the other colour may receive a correction in
+      // this smem copy -- it is never written back, and the red update
+      // weights a solid neighbour by kappa = 0, so its value is unused)
     }
   };
   auto apply_e = [&](int q, const double2 *E) {

@@ -671,9 +671,118 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
+// The same CG with everything in shared memory (coarsest levels up to
+// kCgVarSmem unknowns): per element the 6 kappa and D (doubles), neighbour
+// bits, and the four vectors; one CTA of 256 threads.  Identical arithmetic
+// to k_coarse_cg_var (neighbour order, products, the fixed reduction tree).
+static constexpr int kCgVarSmem = 2304;  // 11 doubles + 1 byte per unknown
+
+__global__ void __launch_bounds__(256)
+    k_coarse_cg_var_smem(Grid g, double tol, int maxit, int *iters_out) {
+  extern __shared__ double sm[];
+  __shared__ double part[2][32];
+  const int N = g.nx * g.ny * g.nz;
+  double *x = sm, *r = sm + N, *p = sm + 2 * N, *q = sm + 3 * N;
+  double *kap = sm + 4 * N;   // [6][N]
+  double *Dd = sm + 10 * N;   // [N]
+  unsigned char *nb = reinterpret_cast<unsigned char *>(sm + 11 * N);
+  const int sx = g.ny * g.nz, sy = g.nz;
+  int pb = 0;
+  double acc = 0.0;
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = n % g.nz;
+    const int t = n / g.nz;
+    const int j = t % g.ny, i = t / g.ny;
+    const int col = (i + j + z) & 1;
+    const long long e = rb(g, i, j) + (z >> 1);
+    Coef C;
+    coef_at(g, col, e, i, j, z, C);
+    for (int f = 0; f < 6; f++) kap[f * N + n] = C.k[f];
+    Dd[n] = C.D;
+    nb[n] = (unsigned char)((i > 0) | ((i < g.nx - 1) << 1) | ((j > 0) << 2) |
+                            ((j < g.ny - 1) << 3) | ((z > 0) << 4) |
+                            ((z < g.nz - 1) << 5));
+    const double b = (C.D == 0.0) ? 0.0 : (col ? g.fB[e] : g.fR[e]);
+    x[n] = 0.0;
+    r[n] = b;
+    p[n] = b;
+    acc = acc + b * b;
+  }
+  double rho = cg_sum_v(acc, part[pb]);  // barrier also publishes the arrays
+  pb ^= 1;
+  const double bnorm = sqrt(rho);
+  const double c = g.c;
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      acc = 0.0;
+      for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        double qn = 0.0;
+        const double pn = p[n];
+        if (Dd[n] != 0.0) {
+          const unsigned m = nb[n];
+          const double xm = (m & 1) ? p[n - sx] : 0.0;
+          const double xp = (m & 2) ? p[n + sx] : 0.0;
+          const double ym = (m & 4) ? p[n - sy] : 0.0;
+          const double yp = (m & 8) ? p[n + sy] : 0.0;
+          const double zm = (m & 16) ? p[n - 1] : 0.0;
+          const double zp = (m & 32) ? p[n + 1] : 0.0;
+          const double t = ((((kap[n] * xm + kap[N + n] * xp) + kap[2 * N + n] * ym) +
+                             kap[3 * N + n] * yp) +
+                            kap[4 * N + n] * zm) +
+                           kap[5 * N + n] * zp;
+          qn = c * (Dd[n] * pn - t);
+        }
+        q[n] = qn;
+        acc = acc + pn * qn;
+      }
+      const double pq = cg_sum_v(acc, part[pb]);
+      pb ^= 1;
+      const double a = rho / pq;
+      acc = 0.0;
+      for (int n = threadIdx.x; n < N; n += blockDim.x) {
+        x[n] = x[n] + a * p[n];
+        const double rn = r[n] - a * q[n];
+        r[n] = rn;
+        acc = acc + rn * rn;
+      }
+      const double rho1 = cg_sum_v(acc, part[pb]);
+      pb ^= 1;
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      const double beta = rho1 / rho;
+      for (int n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
+      __syncthreads();
+      rho = rho1;
+    }
+  }
+  __syncthreads();
+  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+    const int z = n % g.nz;
+    const int t = n / g.nz;
+    const int j = t % g.ny, i = t / g.ny;
+    const int col = (i + j + z) & 1;
+    (col ? g.phiB : g.phiR)[rb(g, i, j) + (z >> 1)] = x[n];
+  }
+  if (threadIdx.x == 0 && iters_out) *iters_out = it;
+}
+
 void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
                           int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
+  if (N <= kCgVarSmem) {
+    const size_t smem = 11 * (size_t)N * sizeof(double) + (size_t)N;
+    static size_t configured = 48 * 1024;
+    if (smem > configured) {
+      cudaFuncSetAttribute(k_coarse_cg_var_smem,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      configured = smem;
+    }
+    int threads = (int)((N + 31) / 32 * 32);
+    if (threads > 256) threads = 256;
+    k_coarse_cg_var_smem<<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
+    return;
+  }
   int threads = (int)((N + 31) / 32 * 32);
   if (threads > 1024) threads = 1024;
   k_coarse_cg_var<<<1, threads, 0, s>>>(g, scratch, tol, maxit, iters_out);
