@@ -82,7 +82,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   const bool row_ok = j < g.ny;
   double *__restrict__ own = color ? g.phiB : g.phiR;
   const double *__restrict__ fown = color ? g.fB : g.fR;
-  constexpr int nch = NCH;  // 64 half-entries per warp pass, ceil(nzh/64)
+  // NCH: lane chunks of 64 half-entries per warp pass, ceil(nzh / 64)
 
   // PROLONG: add alpha * e(parent) to the ring copy of local plane il (rows
   // j0-1 .. j0+TY).  The corrected other colour is NOT written back: the
