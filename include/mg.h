@@ -277,6 +277,22 @@ int mg_timestep(mg_ctx *ctx, int n, const double *centers, const double *radii,
  * MG_ERR_DIVERGED if the norm is NaN or > 10x the previous cycle's. */
 int mg_vcycle(mg_ctx *ctx, double *res_norm_out);
 
+/* Asynchronous fixed-count solve, for pipelining independent problems:
+ * f := the given field (natural layout, the rank's slab; BC adaptation as
+ * mg_set_rhs), Phi := 0, `cycles` V-cycles, then Phi copied to phi_out
+ * (natural layout; may be NULL).  Returns after enqueueing (no host
+ * synchronisation).  Host buffers (MG_HOST, pinned for real overlap) move on
+ * two library copy streams through three staging slots, so the upload of the
+ * next problem and the download of the previous one overlap this problem's
+ * cycles, which stay on the context's stream.  The caller keeps f and
+ * phi_out alive until mg_wait; no per-cycle divergence check. */
+int mg_solve_async(mg_ctx *ctx, const double *f, int where_f, double *phi_out,
+                   int where_phi, int cycles);
+/* Synchronise the context's streams (compute and copies); *res_norm_out
+ * (may be NULL) = the residual norm after the last V-cycle.
+ * MG_ERR_DIVERGED if it is NaN. */
+int mg_wait(mg_ctx *ctx, double *res_norm_out);
+
 /* r0 = norm of the current Phi; V-cycles while r_k > tol*r0 (Alg.1,
  * P:547-550).  *cycles_out and res_hist[0..cycles] (len max_cycles+1) may be
  * NULL.  MG_OK, MG_ERR_NOTCONV at max_cycles, or MG_ERR_DIVERGED. */

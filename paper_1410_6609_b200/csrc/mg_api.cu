@@ -213,10 +213,20 @@ struct mg_ctx {
   double *normv = nullptr;     // [0] local sum, [1] global sum, [2..2+P) gathered
   double *cg_scr = nullptr;
   int *cg_iters = nullptr;
-  double *h_norm = nullptr;    // pinned
+  double *h_norm = nullptr;    // pinned, mapped
+  double *h_norm_dev = nullptr;  // its device view (written by k_publish)
   int *h_iters = nullptr;      // pinned
   double *stage = nullptr;     // lazily allocated natural-layout staging
   size_t stage_bytes = 0;
+  // mg_solve_async pipeline: three staging slots (upload of problem k+1,
+  // download of problem k-1 and the current problem's unpack never share
+  // one), copy streams, slot events
+  double *astg[3] = {nullptr, nullptr, nullptr};
+  size_t astg_bytes = 0;
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  cudaEvent_t ev_in[3] = {}, ev_out[3] = {}, ev_d2h[3] = {};
+  bool d2h_used[3] = {false, false, false};
+  unsigned long long async_k = 0;
   double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
   double *fbuf = nullptr;      // force step: sphere list + partial sums
@@ -546,13 +556,13 @@ int enqueue_norm(mg_ctx *c) {
     if (rc) return rc;
     mg::launch_sum_ordered(c->normv + 2, c->P, c->normv + 1, c->stream);
     c->launches++;
+    mg::launch_publish(c->normv + 1, c->normv + 1, c->h_norm_dev, c->stream);
   } else {
-    CK(cudaMemcpyAsync(c->normv + 1, c->normv, sizeof(double),
-                       cudaMemcpyDeviceToDevice, c->stream));
+    mg::launch_publish(c->normv, c->normv + 1, c->h_norm_dev, c->stream);
   }
+  c->launches++;
   mark(c, CAT_NORM);
-  CK(cudaMemcpyAsync(c->h_norm, c->normv + 1, sizeof(double),
-                     cudaMemcpyDeviceToHost, c->stream));
+  CK(cudaGetLastError());
   return MG_OK;
 }
 
@@ -658,12 +668,10 @@ int enqueue_vcycle(mg_ctx *c) {
       c->launches++;
       mg::launch_sum_ordered(c->partials, nb, c->normv, c->stream);
       c->launches++;
+      mg::launch_publish(c->normv, c->normv + 1, c->h_norm_dev, c->stream);
+      c->launches++;
       CK(cudaGetLastError());
-      CK(cudaMemcpyAsync(c->normv + 1, c->normv, sizeof(double),
-                         cudaMemcpyDeviceToDevice, c->stream));
       mark(c, CAT_NORM);
-      CK(cudaMemcpyAsync(c->h_norm, c->normv + 1, sizeof(double),
-                         cudaMemcpyDeviceToHost, c->stream));
       c->cycle_launches = c->launches;
       c->prof_last = c->prof;
       return MG_OK;
@@ -698,7 +706,8 @@ size_t level_cells_held(const mg_ctx *c, int l) {
   return n;
 }
 
-int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in) {
+int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in,
+             bool do_sync = true) {
   if (l < 0 || l >= c->pl.L) return fail(MG_ERR_ARG, "level %d out of range", l);
   if (field != MG_FIELD_PHI && field != MG_FIELD_RHS)
     return fail(MG_ERR_ARG, "bad field %d", field);
@@ -737,7 +746,7 @@ int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in) {
     CK(cudaMemcpyAsync(buf, dev, n * sizeof(double), cudaMemcpyDeviceToHost,
                        c->stream));
   }
-  return sync(c);
+  return do_sync ? sync(c) : MG_OK;
 }
 
 int bc_adapt(mg_ctx *c) {
@@ -1024,8 +1033,10 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
   if (const char *e = getenv("MG_T4_TY")) c->t4_ty = atoi(e) == 8 ? 8 : 16;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
-  e = cudaMallocHost(&c->h_norm, sizeof(double) * 2);
-  if (e != cudaSuccess) return bail(e, "cudaMallocHost");
+  e = cudaHostAlloc(&c->h_norm, sizeof(double) * 2, cudaHostAllocMapped);
+  if (e != cudaSuccess) return bail(e, "cudaHostAlloc");
+  e = cudaHostGetDevicePointer(&c->h_norm_dev, c->h_norm, 0);
+  if (e != cudaSuccess) return bail(e, "cudaHostGetDevicePointer");
   e = cudaStreamSynchronize(c->stream);
   if (e != cudaSuccess) return bail(e, "cudaStreamSynchronize");
   if (c->backend == MG_HALO_NCCL) {
@@ -1057,6 +1068,16 @@ void mg_destroy(mg_ctx *c) {
   for (auto &e : c->ev) cudaEventDestroy(e);
   if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
   if (c->stage) cudaFree(c->stage);
+  if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
+  if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
+  for (int q = 0; q < 3; q++) {
+    if (c->astg[q]) cudaFree(c->astg[q]);
+    if (c->ev_in[q]) cudaEventDestroy(c->ev_in[q]);
+    if (c->ev_out[q]) cudaEventDestroy(c->ev_out[q]);
+    if (c->ev_d2h[q]) cudaEventDestroy(c->ev_d2h[q]);
+  }
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   if (c->sph) cudaFree(c->sph);
   if (c->fbuf) cudaFree(c->fbuf);
   for (void *p : c->mask_bufs) cudaFree(p);
@@ -1135,8 +1156,8 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   return MG_OK;
 }
 
-int mg_vcycle(mg_ctx *c, double *res_norm_out) {
-  if (!c) return fail(MG_ERR_ARG, "null ctx");
+// enqueue one V-cycle (graph launch, recorded on first use); no host sync
+static int enqueue_cycle(mg_ctx *c) {
   int rc;
   if (c->o.use_graph) {
     if (!c->graph) {
@@ -1150,9 +1171,125 @@ int mg_vcycle(mg_ctx *c, double *res_norm_out) {
       cudaGraphDestroy(gr);
     }
     CK(cudaGraphLaunch(c->graph, c->stream));
-  } else {
-    if ((rc = enqueue_vcycle(c))) return rc;
+    return MG_OK;
   }
+  return enqueue_vcycle(c);
+}
+
+// natural <-> split conversion of level 0 from / to a device buffer
+static int pack0(mg_ctx *c, int field, const double *dev) {
+  size_t off = 0;
+  for (const Grid &g : c->g[0]) {
+    mg::launch_pack(g, field, dev + off, c->stream);
+    off += (size_t)g.nxl * g.ny * g.nz;
+  }
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+static int unpack0(mg_ctx *c, int field, double *dev) {
+  size_t off = 0;
+  for (const Grid &g : c->g[0]) {
+    mg::launch_unpack(g, field, dev + off, c->stream);
+    off += (size_t)g.nxl * g.ny * g.nz;
+  }
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
+static int async_setup(mg_ctx *c, size_t bytes) {
+  if (!c->s_h2d) {
+    CK(cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking));
+    for (int q = 0; q < 3; q++) {
+      CK(cudaEventCreateWithFlags(&c->ev_in[q], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_out[q], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_d2h[q], cudaEventDisableTiming));
+    }
+  }
+  if (c->astg_bytes < bytes) {
+    CK(cudaStreamSynchronize(c->stream));
+    CK(cudaStreamSynchronize(c->s_h2d));
+    CK(cudaStreamSynchronize(c->s_d2h));
+    for (int q = 0; q < 3; q++) {
+      if (c->astg[q]) cudaFree(c->astg[q]);
+      c->astg[q] = nullptr;
+      c->d2h_used[q] = false;
+    }
+    c->astg_bytes = 0;
+    for (int q = 0; q < 3; q++) CK(cudaMalloc(&c->astg[q], bytes));
+    c->astg_bytes = bytes;
+  }
+  return MG_OK;
+}
+
+// Pipeline of independent solves: problem k uses staging slot k % 3.  The
+// H2D of its f runs on the context's h2d stream (after the D2H that last
+// used the slot), the cycles on the context's stream, the D2H of Phi on the
+// d2h stream -- so problem k+1's upload and problem k-1's download overlap
+// problem k's cycles, while the cycles of consecutive problems stay
+// serialised on one stream.
+int mg_solve_async(mg_ctx *c, const double *f, int where_f, double *phi_out,
+                   int where_phi, int cycles) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (cycles < 0) return fail(MG_ERR_ARG, "cycles < 0");
+  if (!f) return fail(MG_ERR_ARG, "null f");
+  if ((where_f != MG_HOST && where_f != MG_DEVICE) ||
+      (phi_out && where_phi != MG_HOST && where_phi != MG_DEVICE))
+    return fail(MG_ERR_ARG, "bad 'where'");
+  const size_t n = level_cells_held(c, 0);
+  int rc;
+  if ((rc = async_setup(c, n * sizeof(double)))) return rc;
+  const int q = (int)(c->async_k++ % 3);
+  double *stg = c->astg[q];
+  if (where_f == MG_HOST) {
+    if (c->d2h_used[q]) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[q], 0));
+    CK(cudaMemcpyAsync(stg, f, n * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d));
+    CK(cudaEventRecord(c->ev_in[q], c->s_h2d));
+    CK(cudaStreamWaitEvent(c->stream, c->ev_in[q], 0));
+    if ((rc = pack0(c, MG_FIELD_RHS, stg))) return rc;
+  } else if ((rc = pack0(c, MG_FIELD_RHS, f))) {
+    return rc;
+  }
+  if ((rc = bc_adapt(c))) return rc;
+  for (const Grid &g : c->g[0]) {
+    CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+    CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+  }
+  c->prev_norm = -1.0;
+  for (int k = 0; k < cycles; k++)
+    if ((rc = enqueue_cycle(c))) return rc;
+  if (phi_out) {
+    if (where_phi == MG_HOST) {
+      if ((rc = unpack0(c, MG_FIELD_PHI, stg))) return rc;
+      CK(cudaEventRecord(c->ev_out[q], c->stream));
+      CK(cudaStreamWaitEvent(c->s_d2h, c->ev_out[q], 0));
+      CK(cudaMemcpyAsync(phi_out, stg, n * sizeof(double), cudaMemcpyDeviceToHost,
+                         c->s_d2h));
+      CK(cudaEventRecord(c->ev_d2h[q], c->s_d2h));
+      c->d2h_used[q] = true;
+    } else if ((rc = unpack0(c, MG_FIELD_PHI, phi_out))) {
+      return rc;
+    }
+  }
+  return MG_OK;
+}
+
+int mg_wait(mg_ctx *c, double *res_norm_out) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  int rc = sync(c);
+  if (rc) return rc;
+  if (c->s_d2h) CK(cudaStreamSynchronize(c->s_d2h));
+  if (c->s_h2d) CK(cudaStreamSynchronize(c->s_h2d));
+  const double r = sqrt(*c->h_norm);
+  if (res_norm_out) *res_norm_out = r;
+  if (!(r == r)) return fail(MG_ERR_DIVERGED, "residual is NaN");
+  return MG_OK;
+}
+
+int mg_vcycle(mg_ctx *c, double *res_norm_out) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  int rc;
+  if ((rc = enqueue_cycle(c))) return rc;
   if ((rc = sync(c))) return rc;
   const double r = sqrt(*c->h_norm);
   if (res_norm_out) *res_norm_out = r;

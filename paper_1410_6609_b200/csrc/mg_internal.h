@@ -145,6 +145,10 @@ int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s);
 // out[0] = sum of parts[0..n) in a fixed order
 void launch_sum_ordered(const double *parts, int n, double *out,
                         cudaStream_t s);
+// dev_dst[0] = host_dst[0] = src[0] (host_dst: device view of mapped pinned
+// host memory)
+void launch_publish(const double *src, double *dev_dst, double *host_dst,
+                    cudaStream_t s);
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s);
 size_t coarse_cg_scratch_doubles(const Grid &g);

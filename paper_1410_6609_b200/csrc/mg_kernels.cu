@@ -340,6 +340,21 @@ void launch_sum_ordered(const double *parts, int n, double *out,
   k_sum_ordered<<<1, kThreads, 0, s>>>(parts, n, out);
 }
 
+// dev_dst[0] = host_dst[0] = src[0]; host_dst is mapped pinned memory, so
+// the value reaches the host without a copy-engine transfer (which would
+// queue behind bulk copies on the same engine)
+__global__ void k_publish(const double *src, double *dev_dst, double *host_dst) {
+  const double v = src[0];
+  dev_dst[0] = v;
+  host_dst[0] = v;
+  __threadfence_system();
+}
+
+void launch_publish(const double *src, double *dev_dst, double *host_dst,
+                    cudaStream_t s) {
+  k_publish<<<1, 1, 0, s>>>(src, dev_dst, host_dst);
+}
+
 // ---------------------------------------------------------------------------
 // Coarsest-grid CG: one CTA, Hestenes-Stiefel from x = 0, stop at
 // ||r|| <= tol ||b|| or maxit.  Vectors in natural order, in shared memory

@@ -107,6 +107,8 @@ def lib():
         L.mg_set_rhs_from_spheres.argtypes = [P, i, dp, dp, dp, i, i]
         L.mg_set_rhs.argtypes = [P, dp, i]
         L.mg_vcycle.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+        L.mg_solve_async.argtypes = [P, dp, i, dp, i, i]
+        L.mg_wait.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_solve.argtypes = [P, d, ip, dp]
         L.mg_residual_norm.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_get_solution.argtypes = [P, dp, i]
@@ -323,6 +325,30 @@ class Multigrid:
                                        _host_ptr(r), _host_ptr(q), normalization,
                                        subsample, _host_ptr(out)), self._ctx)
         return out.reshape(-1, 3)
+
+    def solve_async(self, f, phi_out, cycles: int):
+        """Enqueue f -> Phi = 0 -> `cycles` V-cycles -> phi_out on the
+        context's stream without host synchronisation (mg_solve_async); use
+        pinned host tensors (or CUDA tensors) to overlap transfers with the
+        cycles of another context.  Call wait() before reading phi_out."""
+        fp, fw = self._io_args_nosync(f)
+        pp, pw = self._io_args_nosync(phi_out)
+        _check(lib().mg_solve_async(self._ctx, fp, fw, pp, pw, int(cycles)),
+               self._ctx)
+
+    def wait(self) -> float:
+        r = ctypes.c_double(0.0)
+        _check(lib().mg_wait(self._ctx, ctypes.byref(r)), self._ctx)
+        return r.value
+
+    def _io_args_nosync(self, a):
+        torch = self._torch
+        if isinstance(a, torch.Tensor):
+            assert a.dtype == torch.float64 and a.is_contiguous()
+            return a.data_ptr(), (MG_DEVICE if a.is_cuda else MG_HOST)
+        assert isinstance(a, np.ndarray) and a.dtype == np.float64 \
+            and a.flags["C_CONTIGUOUS"]
+        return _host_ptr(a), MG_HOST
 
     def timestep(self, centers, radii, charges, cycles=1, abs_tol=0.0,
                  normalization=MG_CHARGE_PER_CELLS, subsample=1, forces=True,
