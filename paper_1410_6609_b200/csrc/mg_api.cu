@@ -1662,9 +1662,24 @@ int mg_set_face_values(mg_ctx *c, int face, const double *values) {
   return rebuild_coefficients(c);
 }
 
+static int coulomb_forces(mg_ctx *c, int n, const double *centers,
+                          const double *radii, const double *charges,
+                          int normalization, int subsample, double *forces_out,
+                          const unsigned long long *counts);
+
 int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
                       const double *radii, const double *charges,
                       int normalization, int subsample, double *forces_out) {
+  return coulomb_forces(c, n, centers, radii, charges, normalization, subsample,
+                        forces_out, nullptr);
+}
+
+// counts: the per-sphere covered sub-cell counts on the device if the RHS of
+// the same spheres was just set with the same subsampling (mg_timestep)
+static int coulomb_forces(mg_ctx *c, int n, const double *centers,
+                          const double *radii, const double *charges,
+                          int normalization, int subsample, double *forces_out,
+                          const unsigned long long *counts) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (n < 0 || (n > 0 && (!centers || !radii || !charges || !forces_out)))
     return fail(MG_ERR_ARG, "bad arrays");
@@ -1703,7 +1718,7 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
     return fail(MG_ERR_CUDA, "copy of the sphere list failed");
   for (size_t s = 0; s < ns; s++)
     mg::launch_coulomb(c->g[0][s], c->dsolid, c->h, subsample, n, dsph,
-                       normalization, dpart + nrow * s, c->stream);
+                       normalization, dpart + nrow * s, counts, c->stream);
   size_t nparts = ns;
   double *src = dpart;
   if (c->P > 1 && c->backend == MG_HALO_NCCL) {
@@ -1759,8 +1774,13 @@ int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
   if (res_out) *res_out = r;
   if (rc && rc != MG_ERR_NOTCONV) return rc;
   if (forces_out) {
-    const int frc = mg_coulomb_forces(c, n, centers, radii, charges,
-                                      normalization, force_subsample, forces_out);
+    // the RHS kernel counted the spheres' covered sub-cells already
+    const unsigned long long *cnt =
+        (force_subsample == subsample && n > 0)
+            ? reinterpret_cast<const unsigned long long *>(c->sph + 5 * c->sph_cap)
+            : nullptr;
+    const int frc = coulomb_forces(c, n, centers, radii, charges, normalization,
+                                   force_subsample, forces_out, cnt);
     if (frc) return frc;
   }
   return rc;

@@ -107,6 +107,34 @@ __device__ __forceinline__ void gradient(const Grid &g, const unsigned char *sol
   }
 }
 
+// The all-valid D3Q19 gradient of gradient() for a cell whose 18 neighbours
+// are known to be fluid cells of the domain (no mask, no periodic wrap, box
+// inside the level): the same loads in the same q order, addressed directly
+// in the split layout (neighbour colour = own colour ^ parity of the offset).
+__device__ __forceinline__ void gradient_interior(const Grid &g, double h, int i,
+                                                  int j, int k, double *gr) {
+  const long long base = (long long)(i - g.x0 + 1) * g.plane + (long long)(j + 1) * g.pz;
+  const int kh[3] = {(k - 1) >> 1, k >> 1, (k + 1) >> 1};
+  const int c0 = (i + j + k) & 1;
+  double S[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+  for (int q = 0; q < 18; q++) {
+    const int di = kq(q, 0), dj = kq(q, 1), dk = kq(q, 2);
+    const int col = c0 ^ ((di + dj + dk) & 1);
+    const double *arr = col ? g.phiB : g.phiR;
+    const double v = arr[base + di * g.plane + dj * g.pz + kh[dk + 1]];
+    const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) {
+      const int c = kq(q, a);
+      if (c == 0) continue;
+      S[a] = c > 0 ? S[a] + w * v : S[a] - w * v;
+    }
+  }
+#pragma unroll
+  for (int a = 0; a < 3; a++) gr[a] = (3.0 * S[a]) / h;
+}
+
 __device__ __forceinline__ double bsum(double v, double *sh) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
@@ -120,11 +148,33 @@ __device__ __forceinline__ double bsum(double v, double *sh) {
   return s;
 }
 
+// the three force components reduced together (one barrier pair), each in
+// the fixed warp-shuffle tree + warp order of bsum
+__device__ __forceinline__ void bsum3(double *v, double (*sh)[32]) {
+#pragma unroll
+  for (int a = 0; a < 3; a++)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v[a] += __shfl_down_sync(0xffffffffu, v[a], o);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0)
+    for (int a = 0; a < 3; a++) sh[a][wid] = v[a];
+  __syncthreads();
+  for (int a = 0; a < 3; a++) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s = s + sh[a][w];
+    v[a] = s;
+  }
+}
+
 }  // namespace
 
+// counts: the global covered sub-cell count of each sphere if already known
+// (the RHS kernel of the same step, same subsampling), else null
 __global__ void __launch_bounds__(kTF)
     k_coulomb(Grid g, const unsigned char *solid, double h, int s,
-              const double *sph, int normalization, double *part) {
+              const double *sph, int normalization, double *part,
+              const unsigned long long *counts) {
   __shared__ double sh[32];
   __shared__ sph::Tab tab;
   const int p = blockIdx.x;
@@ -134,7 +184,7 @@ __global__ void __launch_bounds__(kTF)
   double img[27][3];
   const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
   long long cnt = 0;  // threads own (j, k) columns of the box, walk along x
-  for (int m = 0; m < nimg; m++) {
+  for (int m = 0; !counts && m < nimg; m++) {
     const sph::Box bx = sph::box_of(g, h, img[m], R);
     if (bx.cells() == 0) continue;
     const bool tb = sph::tables(tab, bx, s, hs, img[m]);
@@ -147,7 +197,7 @@ __global__ void __launch_bounds__(kTF)
                                    hs, img[m][0], img[m][1], img[m][2], R);
     }
   }
-  const double np = bsum((double)cnt, sh);
+  const double np = counts ? (double)counts[p] : bsum((double)cnt, sh);
   double F[3] = {0.0, 0.0, 0.0};
   const bool any = np > 0.0 || normalization == 1;
   const double rho0 = Q / ((4.0 / 3.0) * 3.14159265358979323846 * (R * R * R));
@@ -158,6 +208,11 @@ __global__ void __launch_bounds__(kTF)
     if (bx.cells() == 0 || xa > xb) continue;
     const bool tb = sph::tables(tab, bx, s, hs, img[m]);
     auto ld_glb = [&](int x, int y, int z) { return phi_at(g, x, y, z); };
+    // every cell of this box (and its D3Q19 neighbours) inside the level,
+    // no mask, no wrap: the direct-addressed gradient applies to all of them
+    const bool interior = !solid && !is_periodic(g) && xa - 1 >= 0 && xb + 1 < g.nx &&
+                          bx.lo[1] - 1 >= 0 && bx.lo[1] + bx.n[1] < g.ny &&
+                          bx.lo[2] - 1 >= 0 && bx.lo[2] + bx.n[2] < g.nz;
     const int ncol = bx.n[1] * bx.n[2];
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
@@ -166,30 +221,33 @@ __global__ void __launch_bounds__(kTF)
         const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
                          : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
                                           img[m][2], R);
-        if (!c || !valid_cell(g, solid, i, j, k)) continue;
+        if (!c || (!interior && !valid_cell(g, solid, i, j, k))) continue;
         const double rho = (normalization == 1)
                                ? rho0 * ((double)c / (double)(s * s * s))
                                : (Q * (double)c) / (np * (h * h * h));
         double gr[3];
-        gradient(g, solid, h, i, j, k, gr, ld_glb);
+        if (interior)
+          gradient_interior(g, h, i, j, k, gr);
+        else
+          gradient(g, solid, h, i, j, k, gr, ld_glb);
 #pragma unroll
         for (int a = 0; a < 3; a++) F[a] = F[a] + gr[a] * rho;
       }
     }
   }
-#pragma unroll
-  for (int a = 0; a < 3; a++) {
-    const double v = bsum(F[a], sh);
-    if (threadIdx.x == 0) part[3 * p + a] = v;
-  }
+  __shared__ double sh3[3][32];
+  bsum3(F, sh3);
+  if (threadIdx.x == 0)
+    for (int a = 0; a < 3; a++) part[3 * p + a] = F[a];
 }
 
 void launch_coulomb(const Grid &g, const unsigned char *solid_global, double h,
                     int subsample, int n, const double *sph, int normalization,
-                    double *partials, cudaStream_t s) {
+                    double *partials, const unsigned long long *counts,
+                    cudaStream_t s) {
   if (n <= 0) return;
   k_coulomb<<<n, kTF, 0, s>>>(g, solid_global, h, subsample, sph, normalization,
-                              partials);
+                              partials, counts);
 }
 
 }  // namespace mg

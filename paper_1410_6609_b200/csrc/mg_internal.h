@@ -206,9 +206,12 @@ void launch_level0_coef(const Grid &g, const unsigned char *solid_global,
 void launch_bc_adapt_faces(const Grid &g, const FaceBC &fb, double alpha,
                            double h, cudaStream_t s);
 // Coulomb force partial sums (mg_force.cu): part[3p+a] = sum_b g_a rho_p
+// counts: per-sphere global covered sub-cell counts if known (the same
+// step's RHS with the same subsampling), else null (counted here)
 void launch_coulomb(const Grid &g, const unsigned char *solid_global, double h,
                     int subsample, int n, const double *sph, int normalization,
-                    double *partials, cudaStream_t s);
+                    double *partials, const unsigned long long *counts,
+                    cudaStream_t s);
 // masked (variable-coefficient) path, mg_mask.cu
 void launch_mask_codes(const Grid &g, const unsigned char *solid_global,
                        unsigned char *codeR, unsigned char *codeB,
