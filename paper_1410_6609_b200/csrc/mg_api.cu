@@ -187,6 +187,13 @@ struct mg_ctx {
   int use_march = 1;
   int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
   int use_t4 = 0;     // temporally blocked V(2,2) passes (opt-in: MG_T4=1)
+  // multi-slab overlap (MG_NO_OVERLAP=1: off): boundary planes first, the
+  // ghost exchange on s_comm while the interior planes are swept
+  int overlap = 1;
+  cudaStream_t s_comm = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  std::vector<std::vector<Grid>> vlo, vhi, vin;   // per level, slab: views
+  std::vector<std::vector<TmPair>> tmin;          // TMA maps of the interior views
   int t4_ty = 16;     // their tile rows (MG_T4_TY=8|16)
   bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
@@ -358,8 +365,9 @@ bool any_periodic(const mg_ctx *c) {
 // its sends / receives in the same order -- (last plane -> right, left ghost
 // <- left), then (first plane -> left, right ghost <- right) -- so that
 // repeated peers (P = 2 with wrap) match message by message.
-int halo(mg_ctx *c, int l, int which) {
+int halo(mg_ctx *c, int l, int which, cudaStream_t st = nullptr) {
   if (!distributed(c, l)) return MG_OK;
+  if (!st) st = c->stream;
   auto arr = [&](const Grid &g) { return which ? g.phiB : g.phiR; };
   const bool wrap = periodic_x(c);
   if (c->backend == MG_HALO_LOOPBACK) {
@@ -369,10 +377,10 @@ int halo(mg_ctx *c, int l, int which) {
       const Grid &a = c->g[l][s], &b = c->g[l][(s + 1) % ns];
       const size_t bytes = sizeof(double) * a.plane;
       CK(cudaMemcpyAsync(arr(b), arr(a) + (long long)a.nxl * a.plane, bytes,
-                         cudaMemcpyDeviceToDevice, c->stream));
+                         cudaMemcpyDeviceToDevice, st));
       CK(cudaMemcpyAsync(arr(a) + (long long)(a.nxl + 1) * a.plane,
                          arr(b) + b.plane, bytes, cudaMemcpyDeviceToDevice,
-                         c->stream));
+                         st));
     }
     return MG_OK;
   }
@@ -390,9 +398,9 @@ int halo(mg_ctx *c, int l, int which) {
                                                 : g.nxl + 1;
     double *buf = A + (long long)pl * g.plane;
     if (ops[k][0] == MG_OP_SEND)
-      g_nccl.Send(buf, n, ncclDouble, ops[k][1], c->comm, c->stream);
+      g_nccl.Send(buf, n, ncclDouble, ops[k][1], c->comm, st);
     else
-      g_nccl.Recv(buf, n, ncclDouble, ops[k][1], c->comm, c->stream);
+      g_nccl.Recv(buf, n, ncclDouble, ops[k][1], c->comm, st);
   }
   return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(halo)");
 }
@@ -407,7 +415,63 @@ void periodic_fill(mg_ctx *c, int l) {
   }
 }
 
+// plane-range view of a slab grid: planes [pb, pb + n) as a slab of n planes
+Grid plane_view(const Grid &g, int pb, int n) {
+  Grid v = g;
+  const long long off = (long long)pb * g.plane;
+  v.phiR += off;
+  v.phiB += off;
+  v.fR += off;
+  v.fB += off;
+  v.phiB2 = nullptr;
+  v.nxl = n;
+  v.x0 = g.x0 + pb;
+  return v;
+}
+
+// overlap the ghost exchange of level l with the interior planes?
+bool overlap_level(const mg_ctx *c, int l) {
+  return c->overlap && distributed(c, l) && !c->masked && !c->vin.empty() &&
+         !c->vin[l].empty();
+}
+
+// half-sweep of a distributed level with the exchange overlapped: the two
+// boundary planes of every slab first (the planes the neighbours need), then
+// the exchange on s_comm while the interior planes are swept; the next step
+// waits for the exchange (its boundary planes read the received ghosts).
+int smooth_half_overlap(mg_ctx *c, int l, int color, int from_zero) {
+  for (size_t s = 0; s < c->g[l].size(); s++) {
+    mg::launch_smooth(c->vlo[l][s], color, from_zero, c->stream);
+    mg::launch_smooth(c->vhi[l][s], color, from_zero, c->stream);
+    c->launches += 2;
+  }
+  CK(cudaGetLastError());
+  CK(cudaEventRecord(c->ev_fork, c->stream));
+  CK(cudaStreamWaitEvent(c->s_comm, c->ev_fork, 0));
+  int rc = halo(c, l, color, c->s_comm);
+  if (rc) return rc;
+  CK(cudaEventRecord(c->ev_join, c->s_comm));
+  for (size_t s = 0; s < c->g[l].size(); s++) {
+    const Grid &v = c->vin[l][s];
+    const TmPair &t = c->tmin[l][s];
+    if (!from_zero && t.ok && c->use_march)
+      mg::launch_smooth_march(v, color ? t.r : t.b, color, c->stream);
+    else
+      mg::launch_smooth(v, color, from_zero, c->stream);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  CK(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  return MG_OK;
+}
+
 int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
+  if (overlap_level(c, l)) {
+    if (l == 0) mark(c, CAT_NONE);
+    int rc = smooth_half_overlap(c, l, color, from_zero);
+    if (l == 0) mark(c, CAT_SMOOTH0);
+    return rc;
+  }
   if (l == 0) mark(c, CAT_NONE);
   for (size_t s = 0; s < c->g[l].size(); s++) {
     const Grid &g = c->g[l][s];
@@ -1027,6 +1091,36 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
                 (!t.ok_resid || mg::make_tmap_resid(g, g.phiB2, t.rb2));
     }
   }
+  // multi-slab overlap: views of the boundary / interior planes of every
+  // distributed level (slabs of >= 4 planes), a communication stream
+  if (c->P > 1 && !getenv("MG_NO_OVERLAP")) {
+    c->vlo.assign(c->pl.L, {});
+    c->vhi.assign(c->pl.L, {});
+    c->vin.assign(c->pl.L, {});
+    c->tmin.assign(c->pl.L, {});
+    for (int l = 0; l < c->pl.nd; l++) {
+      if (c->g[l][0].nxl < 4) continue;
+      c->tmin[l].resize(c->g[l].size());
+      for (size_t s = 0; s < c->g[l].size(); s++) {
+        const Grid &g = c->g[l][s];
+        c->vlo[l].push_back(plane_view(g, 0, 1));
+        c->vhi[l].push_back(plane_view(g, g.nxl - 1, 1));
+        const Grid vi = plane_view(g, 1, g.nxl - 2);
+        c->vin[l].push_back(vi);
+        TmPair &t = c->tmin[l][s];
+        t.ok = mg::march_supported(vi) && mg::make_tmap_field(vi, vi.phiR, t.r) &&
+               mg::make_tmap_field(vi, vi.phiB, t.b);
+      }
+    }
+    e = cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking);
+    if (e != cudaSuccess) return bail(e, "cudaStreamCreate(comm)");
+    e = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(e, "cudaEventCreate");
+    e = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(e, "cudaEventCreate");
+  } else {
+    c->overlap = 0;
+  }
   if (getenv("MG_NO_MARCH")) c->use_march = 0;
   if (getenv("MG_FUSED")) c->use_fused = 1;
   if (t4_requested()) c->use_t4 = 1;
@@ -1068,6 +1162,12 @@ void mg_destroy(mg_ctx *c) {
   for (auto &e : c->ev) cudaEventDestroy(e);
   if (c->comm && g_nccl.ok) g_nccl.CommDestroy(c->comm);
   if (c->stage) cudaFree(c->stage);
+  if (c->s_comm) {
+    cudaStreamSynchronize(c->s_comm);
+    cudaStreamDestroy(c->s_comm);
+  }
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
   for (int q = 0; q < 3; q++) {
