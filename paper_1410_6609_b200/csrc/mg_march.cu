@@ -404,6 +404,21 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const size_t oc = (size_t)(q % kSlots) * sd + (warp + 1) * W + zoff;
       const size_t om = (size_t)((q - 1) % kSlots) * sd + (warp + 1) * W + zoff;
       const size_t op = (size_t)((q + 1) % kSlots) * sd + (warp + 1) * W + zoff;
+      // periodic z: the other colour's row ends (half-indices nzh-1 and 0),
+      // loaded once per row and plane by the tiles at the row ends (a
+      // warp-uniform broadcast load; the arrays are not written here)
+      double wlo[2] = {0.0, 0.0}, whi[2] = {0.0, 0.0};  // [own colour]
+      if (PER && g.per[2]) {
+        const long long ro = (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
+        if (zt == 0) {
+          wlo[0] = g.phiB[ro + g.nzh - 1];
+          wlo[1] = g.phiR[ro + g.nzh - 1];
+        }
+        if (zt == nzt - 1) {
+          whi[0] = g.phiB[ro];
+          whi[1] = g.phiR[ro];
+        }
+      }
 #pragma unroll
       for (int c = 0; c < 2; c++) {
         const int kl = 2 * lane + 64 * c;  // tile-relative half-index
@@ -425,19 +440,16 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           // periodic z axis the row's opposite end (not in this z-tile: a
           // direct load of the other colour, unchanged during this kernel)
           double zm0, zp0, zm1, zp1;
-          const bool zper = PER && g.per[2];
-          const double *Og = (col ? g.phiR : g.phiB) +
-                             (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
           if (p == 0) {
-            zm0 = (k > 0) ? O[oc + kl - 1] : (zper ? Og[g.nzh - 1] : 0.0);
+            zm0 = (k > 0) ? O[oc + kl - 1] : wlo[col];
             zp0 = zc.x;
             zm1 = zc.x;
             zp1 = zc.y;
           } else {
             zm0 = zc.x;
-            zp0 = (zper && k + 1 >= g.nzh) ? Og[0] : zc.y;
+            zp0 = (PER && g.per[2] && k + 1 >= g.nzh) ? whi[col] : zc.y;
             zm1 = zc.y;
-            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : (zper ? Og[0] : 0.0);
+            zp1 = (k + 2 < g.nzh) ? O[oc + kl + 2] : whi[col];
           }
           const int z0 = 2 * k + p;
           double s0, s1, d0, d1;
