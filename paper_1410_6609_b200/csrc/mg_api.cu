@@ -178,7 +178,9 @@ struct TmPair {
   alignas(64) unsigned char t4a[256]; // temporally blocked pass: input phiB
   alignas(64) unsigned char t4b[256]; //                         input phiB2
   alignas(64) unsigned char rb2[128]; // z-tiled boxes of phiB2 (residual)
-  bool ok = false, ok_resid = false, ok_fused = false, ok_t4 = false;
+  alignas(64) unsigned char s2a[128]; // full-sweep kernel: input phiB
+  alignas(64) unsigned char s2b[128]; //                   input phiB2
+  bool ok = false, ok_resid = false, ok_fused = false, ok_t4 = false, ok_s2 = false;
 };
 
 struct mg_ctx {
@@ -187,6 +189,7 @@ struct mg_ctx {
   int use_march = 1;
   int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
   int use_t4 = 0;     // temporally blocked V(2,2) passes (opt-in: MG_T4=1)
+  int use_s2 = 0;     // one full sweep (red + black) per kernel (MG_S2=1)
   // multi-slab overlap (MG_NO_OVERLAP=1: off): boundary planes first, the
   // ghost exchange on s_comm while the interior planes are swept
   int overlap = 1;
@@ -275,6 +278,10 @@ bool t4_requested() {
   const char *e = getenv("MG_T4");
   return e && atoi(e) != 0;
 }
+bool s2_requested() {
+  const char *e = getenv("MG_S2");
+  return e && atoi(e) != 0;
+}
 
 size_t carve(mg_ctx *c, char *base) {
   Carver cv{base};
@@ -297,8 +304,9 @@ size_t carve(mg_ctx *c, char *base) {
       gr.fB = (double *)cv.take(bytes);
       // second black array for the temporally blocked passes (levels held
       // whole: one slab, or agglomerated)
-      gr.phiB2 = (gr.nxl == gr.nx && t4_requested()) ? (double *)cv.take(bytes)
-                                                      : nullptr;
+      gr.phiB2 = (gr.nxl == gr.nx && (t4_requested() || s2_requested()))
+                     ? (double *)cv.take(bytes)
+                     : nullptr;
       c->g[l].push_back(gr);
     }
   }
@@ -640,6 +648,42 @@ bool use_t4(const mg_ctx *c, int l) {
   return c->tm[l][0].ok_t4 && mg::sweep4_supported(g) && g.nzh >= 64 && g.ny >= 32;
 }
 
+// full-sweep kernels (mg_sweep2.cu) on level l?  V(2,2) only: the two
+// sweeps of a pass alternate the black arrays (phiB -> phiB2 -> phiB)
+bool use_s2(const mg_ctx *c, int l) {
+  if (!c->use_s2 || !c->use_march || c->masked || any_periodic(c)) return false;
+  if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
+  return c->tm[l][0].ok_s2 && mg::sweep2_supported(c->g[l][0]);
+}
+
+int s2_pre(mg_ctx *c, int l) {
+  const Grid &g = c->g[l][0];
+  const TmPair &t = c->tm[l][0];
+  if (l == 0) mark(c, CAT_NONE);
+  mg::launch_sweep2(g, g, t.s2a, g.phiB2, false, l > 0, 0.0, c->stream);
+  if (l == 0) mark(c, CAT_SMOOTH0);
+  mg::launch_sweep2(g, g, t.s2b, g.phiB, false, false, 0.0, c->stream);
+  c->launches += 2;
+  if (l == 0) mark(c, CAT_SMOOTH0);
+  CK(cudaGetLastError());
+  return restrict_level(c, l);
+}
+
+int s2_post(mg_ctx *c, int l) {
+  const Grid &g = c->g[l][0];
+  const TmPair &t = c->tm[l][0];
+  if (l == 0) mark(c, CAT_NONE);
+  mg::launch_sweep2(g, coarse_of(c, l, 0), t.s2a, g.phiB2, true, false, c->o.alpha,
+                    c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_PROLONG0);
+  mg::launch_sweep2(g, g, t.s2b, g.phiB, false, false, 0.0, c->stream);
+  c->launches++;
+  if (l == 0) mark(c, CAT_SMOOTH0);
+  CK(cudaGetLastError());
+  return MG_OK;
+}
+
 // pre-smoothing (4 half-sweeps) -> red in phiR, black in phiB2; then
 // f_{l+1} = R (f_l - A_l Phi_l) reading black from phiB2
 int t4_pre_restrict(mg_ctx *c, int l) {
@@ -692,6 +736,10 @@ int enqueue_vcycle(mg_ctx *c) {
       if ((rc = t4_pre_restrict(c, l))) return rc;
       continue;
     }
+    if (use_s2(c, l)) {
+      if ((rc = s2_pre(c, l))) return rc;
+      continue;
+    }
     const bool fuse_r = c->o.nu1 >= 1 && can_fuse_resid(c, l);
     for (int s = 0; s < c->o.nu1; s++) {
       if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
@@ -710,6 +758,10 @@ int enqueue_vcycle(mg_ctx *c) {
     if (l == 0) mark(c, CAT_COARSE);
     if (use_t4(c, l)) {
       if ((rc = t4_prolong_post(c, l))) return rc;
+      continue;
+    }
+    if (use_s2(c, l)) {
+      if ((rc = s2_post(c, l))) return rc;
       continue;
     }
     const bool fuse = can_fuse_prolong(c, l);
@@ -1085,6 +1137,9 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
                    mg::make_tmap_resid(g, g.phiB, t.rb);
       t.ok_fused = t.ok_resid && mg::fused_supported(g) &&
                    mg::make_tmap_red12(g, g.phiR, t.r12);
+      t.ok_s2 = g.phiB2 && mg::sweep2_supported(g) &&
+                mg::make_tmap_sweep2(g, g.phiB, t.s2a) &&
+                mg::make_tmap_sweep2(g, g.phiB2, t.s2b);
       t.ok_t4 = g.phiB2 && mg::sweep4_supported(g) &&
                 mg::make_tmap_sweep4(g, g.phiB, t.t4a) &&
                 mg::make_tmap_sweep4(g, g.phiB2, t.t4b) &&
@@ -1124,6 +1179,7 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
   if (getenv("MG_NO_MARCH")) c->use_march = 0;
   if (getenv("MG_FUSED")) c->use_fused = 1;
   if (t4_requested()) c->use_t4 = 1;
+  if (s2_requested()) c->use_s2 = 1;
   if (const char *e = getenv("MG_T4_TY")) c->t4_ty = atoi(e) == 8 ? 8 : 16;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
@@ -1946,7 +2002,7 @@ int mg_last_cycle_times_ex(mg_ctx *c, double *out, int n) {
   int rc = mg_last_cycle_times(c, out);
   if (rc) return rc;
   out[8] = out[1];                               // level-0 smoothing launches
-  out[9] = out[1] * (use_t4(c, 0) ? 4.0 : 1.0);  // level-0 half-sweeps in them
+  out[9] = out[1] * (use_t4(c, 0) ? 4.0 : (use_s2(c, 0) ? 2.0 : 1.0));
   return MG_OK;
 }
 

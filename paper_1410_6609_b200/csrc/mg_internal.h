@@ -193,6 +193,12 @@ bool sweep4_supported(const Grid &g);
 bool make_tmap_sweep4(const Grid &g, const double *base, void *out256);
 void launch_sweep4(const Grid &g, const Grid &c, const void *tm256, bool prolong,
                    bool from_zero, double alpha, int ty, cudaStream_t s);
+// one full RBGS sweep (red then black) per kernel (mg_sweep2.cu): black read
+// through tm_in128 (box 136 x 12), red written to g.phiR, black to bout
+bool sweep2_supported(const Grid &g);
+bool make_tmap_sweep2(const Grid &g, const double *base, void *out128);
+void launch_sweep2(const Grid &g, const Grid &c, const void *tm_in128, double *bout,
+                   bool prolong, bool from_zero, double alpha, cudaStream_t s);
 // per-face-cell boundary conditions (mg_set_bc_patch); null = face-uniform.
 // Face q cell (a, b): q<2 -> (j, z), q<4 -> (i, z), else (i, j); index a*nb+b
 struct FaceBC {
