@@ -192,6 +192,38 @@ def timestep_regime(mg, W, stream, local, steps=10, warm=2):
                              "(P:1346); context only"}
 
 
+def fused_norm_variant(mg, W, stream, local, steps=20, warm=3):
+    """Reading c11 (mg_opts.fused_norm): the same config-3 cycles with the
+    termination norm taken from the level-0 residual+restriction kernel
+    (no separate norm pass).  Reported beside the headline, which keeps the
+    post-cycle norm (the residual histories of SURVEY 8(c))."""
+    import torch
+    w = W.cfg3(512, seed=0, with_rhs=False)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, device=local,
+                     stream=stream, min_coarse=8, fused_norm=True)
+    s.set_rhs(W.uniform_rhs(w.shape, 0))
+    for _ in range(warm):
+        s.vcycle()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(steps):
+        s.vcycle()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / steps
+    cells = int(np.prod(w.shape))
+    L = s.nlevels
+    s.close()
+    model = sum((24 * 4 + 34) * 8.0 ** -l for l in range(L - 1))  # no norm pass
+    return {"reading": "c11: cycle norm = level-0 residual after pre-smoothing, "
+                       "summed by the residual+restriction kernel",
+            "ms_per_cycle": round(ms, 4),
+            "value": round(cells / (ms * 1e-3) / 1e6, 2), "unit": UNIT,
+            "cycle_model_bytes_per_cell": round(model, 2), "steps": steps}
+
+
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
@@ -466,6 +498,11 @@ def run_cuda(args):
             line["timestep_regime"] = timestep_regime(mg, W, stream, local)
         except Exception as ex:  # reported, never fatal
             line["timestep_regime"] = {"error": repr(ex)}
+    if N == 1 and workload == "cfg3" and not args.no_fused:
+        try:
+            line["fused_norm"] = fused_norm_variant(mg, W, stream, local)
+        except Exception as ex:  # reported, never fatal
+            line["fused_norm"] = {"error": repr(ex)}
     if rank == 0 and N == 1 and not args.no_cpu:
         try:
             line["cpu_baseline"] = cpu_baseline(args.cpu_size)
@@ -493,6 +530,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ts", action="store_true",
                     help="skip the time-stepping regime measurement")
+    ap.add_argument("--no-fused", action="store_true",
+                    help="skip the fused-termination-norm variant (reading c11)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

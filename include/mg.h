@@ -99,6 +99,15 @@ typedef struct {
                          library allocates and frees its own                 */
   size_t workspace_bytes;
   int use_graph;      /* capture one V-cycle as a CUDA graph (default 1)     */
+  int fused_norm;     /* reading c11 (Alg.1):
+                         0 (default) = mg_vcycle returns ||f - A Phi|| of the
+                         new iterate (a separate 16 B/cell pass);
+                         1 = it returns the norm of the level-0 residual the
+                         cycle computes after pre-smoothing for the
+                         restriction (no extra pass).  mg_solve's r_0 is a
+                         separate pass in both modes; a single-level
+                         hierarchy always reports the post-cycle norm.  The
+                         iterates are identical in both modes.              */
 } mg_opts;
 
 typedef struct mg_ctx mg_ctx;

@@ -76,6 +76,7 @@ def lib():
         L.orc_cg.argtypes = [P, i, d, i]
         L.orc_apply.argtypes = [P, i, dp, dp]
         L.orc_set_schedule.argtypes = [P, i, i, d, d, i]
+        L.orc_set_fused_norm.argtypes = [P, i]
         L.orc_residual_norm.restype = d
         L.orc_residual_norm.argtypes = [P]
         L.orc_vcycle.restype = d
@@ -129,7 +130,7 @@ class Oracle:
 
     def __init__(self, shape, h, bc_type, bc_value=None, solid=None,
                  min_coarse=4, max_levels=0, nu1=2, nu2=2, alpha=2.0,
-                 coarse_tol=1e-12, coarse_maxit=1000):
+                 coarse_tol=1e-12, coarse_maxit=1000, fused_norm=False):
         L = lib()
         nx, ny, nz = (int(s) for s in shape)
         if bc_value is None:
@@ -149,6 +150,8 @@ class Oracle:
         self.h = float(h)
         L.orc_set_schedule(self._h, nu1, nu2, float(alpha), float(coarse_tol),
                            int(coarse_maxit))
+        # reading c11: vcycle() reports the in-cycle residual norm
+        L.orc_set_fused_norm(self._h, int(bool(fused_norm)))
 
     def __del__(self):
         if getattr(self, "_h", None):

@@ -65,6 +65,10 @@ struct orc_hier {
   double coarse_tol;
   int coarse_maxit;
   int last_cg_iters;
+  /* reading c11: report the norm of the fine residual the cycle computes
+   * after pre-smoothing (for the restriction) instead of a post-cycle pass */
+  int fused_norm;
+  double in_cycle_norm;
 };
 
 static inline long IDX(const level_t *L, int i, int j, int k) {
@@ -951,6 +955,7 @@ static void vcycle_level(orc_hier *H, int l) {
     orc_smooth_half(H, l, 0);
     orc_smooth_half(H, l, 1);
   }
+  if (l == 0 && H->fused_norm) H->in_cycle_norm = orc_residual_norm(H);
   orc_restrict_residual(H, l);
   level_t *C = &H->L[l + 1];
   for (long c = 0; c < C->n; c++) C->phi[c] = 0.0;
@@ -962,10 +967,18 @@ static void vcycle_level(orc_hier *H, int l) {
   }
 }
 
+/* Alg.1: the cycle's residual norm.  Default: ||f - A phi|| of the
+ * new iterate (a separate pass).  fused_norm (c11, "negligible"
+ * termination check): the norm of the level-0 residual after this cycle's
+ * pre-smoothing, the one restricted to level 1 (a single level has no
+ * restriction: post-cycle norm). */
 double orc_vcycle(orc_hier *H) {
   vcycle_level(H, 0);
+  if (H->fused_norm && H->nlev > 1) return H->in_cycle_norm;
   return orc_residual_norm(H);
 }
+
+void orc_set_fused_norm(orc_hier *H, int on) { H->fused_norm = on != 0; }
 
 /* Alg.1: while residual >= tol: V-cycle.  tol is relative to the
  * initial residual (c10).  Divergence: NaN or growth > 10x in one cycle. */

@@ -104,6 +104,9 @@ void orc_set_schedule(orc_hier *H, int nu1, int nu2, double alpha,
                       double coarse_tol, int coarse_maxit);
 double orc_residual_norm(const orc_hier *H);
 double orc_vcycle(orc_hier *H);
+/* reading c11: orc_vcycle returns the norm of the residual after the cycle's
+ * level-0 pre-smoothing (the restricted one) instead of a post-cycle pass */
+void orc_set_fused_norm(orc_hier *H, int on);
 /* returns 0 converged, 1 not converged at max_cycles, 2 diverged;
  * hist has room for max_cycles+1 entries (may be NULL). */
 int orc_solve(orc_hier *H, double tol, int max_cycles, int *cycles_out,

@@ -367,6 +367,12 @@ bool any_periodic(const mg_ctx *c) {
   return false;
 }
 
+// reading c11: the cycle reports the norm of the level-0 residual computed
+// for the restriction (after pre-smoothing); one level has no restriction
+bool fused_norm_on(const mg_ctx *c) { return c->o.fused_norm && c->pl.L > 1; }
+int norm_partials(mg_ctx *c, size_t s, double *partials);
+int finish_norm(mg_ctx *c, int off);
+
 // ghost-plane exchange of one colour array (0 phiR, 1 phiB) on level l.  On a
 // periodic x axis the first and last slabs are neighbours too (P:692-693:
 // "processes are configured in a periodic arrangement").  Every rank posts
@@ -501,19 +507,36 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
 // all-gathers the restricted RHS (in place) so that each holds the whole level
 int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
+  const bool with_norm = l == 0 && fused_norm_on(c);
+  int off = 0;  // norm partials written so far (fused norm, reading c11)
   for (int s = 0; s < (int)c->g[l].size(); s++) {
     const TmPair &t = c->tm[l][s];
-    if (c->masked && !(c->g[l][s].codeR && t.ok_resid && c->use_march))
+    const bool march = t.ok_resid && c->use_march;
+    if (with_norm && !(march && (!c->masked || c->g[l][s].codeR))) {
+      // no fused kernel for this grid: the same residual's norm, one pass
+      off += norm_partials(c, s, c->partials + off);
+      c->launches++;
+    }
+    if (c->masked && !(c->g[l][s].codeR && march)) {
       mg::launch_resid_restrict_var(c->g[l][s], coarse_of(c, l, s), c->stream);
-    else if (t.ok_resid && c->use_march)
-      mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
-                                      c->stream);
-    else
+    } else if (march) {
+      if (with_norm)
+        off += mg::launch_resid_restrict_norm_march(c->g[l][s], coarse_of(c, l, s), t.rr,
+                                                    t.rb, c->partials + off, c->stream);
+      else
+        mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
+                                        c->stream);
+    } else {
       mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), 0, c->stream);
+    }
     c->launches++;
   }
   if (l == 0) mark(c, CAT_RESTRICT0);
   CK(cudaGetLastError());
+  if (with_norm) {
+    int rc = finish_norm(c, off);
+    if (rc) return rc;
+  }
   if (l + 1 == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
     const Grid &G = c->g[l + 1][0];
     const size_t cnt = (size_t)(G.nx / c->P) * G.plane;
@@ -546,7 +569,7 @@ int prolong_level(mg_ctx *c, int l) {
 // can level l use the fused last-black + residual epilogue kernels?
 bool can_fuse_resid(const mg_ctx *c, int l) {
   if (!c->use_march || !c->use_fused || c->masked || distributed(c, l) ||
-      any_periodic(c))
+      any_periodic(c) || fused_norm_on(c))
     return false;
   for (const TmPair &t : c->tm[l])
     if (!t.ok_fused) return false;
@@ -602,22 +625,32 @@ int coarse_solve(mg_ctx *c) {
 }
 
 // enqueue ||f - A Phi||^2 of level 0 into c->normv[1] and a copy to h_norm
+// partial sums of r^2 over level-0 grid s (fixed order); returns their count
+int norm_partials(mg_ctx *c, size_t s, double *partials) {
+  const Grid &g = c->g[0][s];
+  const TmPair &t = c->tm[0][s];
+  if (c->masked && !(g.codeR && t.ok_resid && c->use_march))
+    return mg::launch_norm_partials_var(g, partials, c->stream);
+  if (t.ok_resid && c->use_march) {
+    mg::launch_norm_march(g, t.rr, t.rb, partials, c->stream);
+    return mg::norm_march_blocks(g);
+  }
+  return mg::launch_norm_partials(g, partials, c->stream);
+}
+
 int enqueue_norm(mg_ctx *c) {
   int off = 0;
   mark(c, CAT_NONE);
   for (size_t s = 0; s < c->g[0].size(); s++) {
-    const Grid &g = c->g[0][s];
-    const TmPair &t = c->tm[0][s];
-    if (c->masked && !(g.codeR && t.ok_resid && c->use_march)) {
-      off += mg::launch_norm_partials_var(g, c->partials + off, c->stream);
-    } else if (t.ok_resid && c->use_march) {
-      mg::launch_norm_march(g, t.rr, t.rb, c->partials + off, c->stream);
-      off += mg::norm_march_blocks(g);
-    } else {
-      off += mg::launch_norm_partials(g, c->partials + off, c->stream);
-    }
+    off += norm_partials(c, s, c->partials + off);
     c->launches++;
   }
+  return finish_norm(c, off);
+}
+
+// ordered sum of `off` partials (+ the rank-ordered all-gather), published to
+// the mapped host word
+int finish_norm(mg_ctx *c, int off) {
   mg::launch_sum_ordered(c->partials, off, c->normv, c->stream);
   c->launches++;
   CK(cudaGetLastError());
@@ -640,7 +673,8 @@ int enqueue_norm(mg_ctx *c) {
 
 // temporally blocked V(2,2) passes on level l (mg_t4.cu)?
 bool use_t4(const mg_ctx *c, int l) {
-  if (!c->use_t4 || !c->use_march || c->masked || any_periodic(c)) return false;
+  if (!c->use_t4 || !c->use_march || c->masked || any_periodic(c) || fused_norm_on(c))
+    return false;
   if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
   const Grid &g = c->g[l][0];
   // large levels only: on the small ones the per-half-sweep kernels (or their
@@ -651,7 +685,8 @@ bool use_t4(const mg_ctx *c, int l) {
 // full-sweep kernels (mg_sweep2.cu) on level l?  V(2,2) only: the two
 // sweeps of a pass alternate the black arrays (phiB -> phiB2 -> phiB)
 bool use_s2(const mg_ctx *c, int l) {
-  if (!c->use_s2 || !c->use_march || c->masked || any_periodic(c)) return false;
+  if (!c->use_s2 || !c->use_march || c->masked || any_periodic(c) || fused_norm_on(c))
+    return false;
   if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
   return c->tm[l][0].ok_s2 && mg::sweep2_supported(c->g[l][0]);
 }
@@ -794,7 +829,8 @@ int enqueue_vcycle(mg_ctx *c) {
     }
   }
   if (L == 1) mark(c, CAT_COARSE);
-  rc = enqueue_norm(c);
+  // fused norm (c11): already published by the level-0 restriction
+  rc = fused_norm_on(c) ? MG_OK : enqueue_norm(c);
   c->cycle_launches = c->launches;
   c->prof_last = c->prof;
   return rc;

@@ -172,6 +172,11 @@ bool make_tmap_resid(const Grid &g, const double *base, void *out128);
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
                                  const void *tmB, cudaStream_t s);
 int norm_march_blocks(const Grid &g);
+// residual + restriction that also writes the norm partials of that residual
+// (one per CTA, fixed order); returns the partial count
+int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,
+                                     const void *tmB, double *partials,
+                                     cudaStream_t s);
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s);
 bool encode_box(const Grid &g, const double *base, void *out128, unsigned box0,

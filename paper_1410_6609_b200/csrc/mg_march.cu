@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
 // residual kernels: two rings (Phi^R, Phi^B), z-tiles of ZT half-entries with
 // one halo element each side; box = (ZT+2) x (TY+2 rows) x (1 plane)
 // ============================================================================
-enum { MODE_RESTRICT = 0, MODE_NORM = 1 };
+// MODE_BOTH: restriction plus the norm partials of the same residual (the
+// fused termination norm, reading c11)
+enum { MODE_RESTRICT = 0, MODE_NORM = 1, MODE_BOTH = 2 };
 
 template <int MODE, int VAR>
 __global__ void __launch_bounds__(kThreadsM, 2)
@@ -474,12 +476,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           r[col][0] = (cd0 & 64) ? fo.x - g.c * t0 : 0.0;
           r[col][1] = (k + 1 < g.nzh && (cd1 & 64)) ? fo.y - g.c * t1 : 0.0;
         }
-        if (MODE == MODE_NORM) {
+        if (MODE != MODE_RESTRICT) {
           acc = acc + r[0][0] * r[0][0];
           acc = acc + r[0][1] * r[0][1];
           acc = acc + r[1][0] * r[1][0];
           acc = acc + r[1][1] * r[1][1];
-        } else {
+        }
+        if (MODE != MODE_NORM) {
           // z-children of coarse K = k are the red and black cells at
           // half-index k (commutative pair: r_dz0 + r_dz1)
           pr[c][0] = r[0][0] + r[1][0];
@@ -487,7 +490,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         }
       }
     }
-    if (MODE == MODE_RESTRICT) {
+    if (MODE != MODE_NORM) {
       // y-children: rows 2J (even warp) + 2J+1 (odd warp), in that order
       if (warp & 1) {
 #pragma unroll
@@ -531,7 +534,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       cB[c] = ncB[c];
     }
   }
-  if (MODE == MODE_NORM) {
+  if (MODE != MODE_RESTRICT) {
     // deterministic block reduction
     double v = acc;
 #pragma unroll
@@ -718,6 +721,17 @@ void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
 }
 
 int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
+
+int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,
+                                     const void *tmB, double *partials,
+                                     cudaStream_t s) {
+  switch (variant(g)) {
+    case VAR_MASK: launch_rm<MODE_BOTH, VAR_MASK>(g, c, tmR, tmB, partials, s); break;
+    case VAR_PER: launch_rm<MODE_BOTH, VAR_PER>(g, c, tmR, tmB, partials, s); break;
+    default: launch_rm<MODE_BOTH, VAR_BOX>(g, c, tmR, tmB, partials, s); break;
+  }
+  return resid_blocks(g);
+}
 
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s) {

@@ -66,7 +66,7 @@ class mg_opts(ctypes.Structure):
                 ("nccl_id", ctypes.c_ubyte * 128),
                 ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t),
-                ("use_graph", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("fused_norm", ctypes.c_int)]
 
 
 _lib = None
@@ -170,7 +170,8 @@ def default_opts() -> mg_opts:
 def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
               agglomerate_below=64 ** 3, coarse_tol=1e-12, coarse_maxit=1000,
               max_cycles=100, device=0, rank=0, nranks=1, halo="none",
-              nccl_id: Optional[bytes] = None, use_graph=True) -> mg_opts:
+              nccl_id: Optional[bytes] = None, use_graph=True,
+              fused_norm=False) -> mg_opts:
     o = default_opts()
     o.nu1, o.nu2, o.alpha = nu1, nu2, alpha
     o.min_coarse, o.max_levels = min_coarse, max_levels
@@ -181,6 +182,7 @@ def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
     if nccl_id is not None:
         ctypes.memmove(o.nccl_id, bytes(nccl_id), 128)
     o.use_graph = 1 if use_graph else 0
+    o.fused_norm = 1 if fused_norm else 0  # reading c11 (include/mg.h)
     return o
 
 

@@ -1,0 +1,167 @@
+"""Reading c11 on the GPU (mg_opts.fused_norm): the cycle reports the norm of
+the level-0 residual computed after pre-smoothing, partial sums written by
+the residual+restriction kernel itself (k_resid_march<BOTH>) or, where that
+kernel does not run (small / generic / variable-coefficient levels), by one
+norm pass over the same residual.
+
+Against the oracle run in the same mode: histories within the tolerance of
+reading c21, Phi rel-L2 <= 1e-10, equal cycle counts; against the GPU's
+default mode: the same iterates bit for bit (the norm only observes).
+Covers the box marching path, the generic kernels, masks, periodic axes,
+variable permittivity and loopback slabs (partials of several grids).
+"""
+import numpy as np
+import pytest
+
+import oracle
+from paper_1410_6609_b200 import workloads as W
+
+pytestmark = pytest.mark.gpu
+
+D, N, P = 0, 1, 2
+BCS = {
+    "mixed": ([N, D, N, D, N, D], [0.25, 1.0, -0.5, -1.0, 2.0, 0.0]),
+    "channel": ([N, N, D, D, N, N], [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]),
+    "perxz": ([P, P, D, N, P, P], [0.0, 0.0, 0.5, -0.25, 0.0, 0.0]),
+}
+OKW = ("min_coarse", "max_levels", "nu1", "nu2", "alpha", "coarse_tol", "coarse_maxit")
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_6609_b200 import _build
+    _build.build()
+    from paper_1410_6609_b200 import mg as M
+    return M
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+def check_history(hg, ho):
+    assert len(hg) == len(ho)
+    r0 = ho[0]
+    for a, b in zip(hg, ho):
+        assert abs(a - b) <= 1e-8 * b + 1e-14 * r0, (a, b)
+
+
+def setup(M, shape, h, bc, fused, solid=None, eps=None, oracle_too=True, **kw):
+    bt, bv = BCS[bc]
+    s = M.Multigrid(shape, h, bt, bv, fused_norm=fused, **kw)
+    o = None
+    if oracle_too:
+        o = oracle.Oracle(shape, h, bt, bv, solid=solid, fused_norm=fused,
+                          **{k: v for k, v in kw.items() if k in OKW})
+    if solid is not None:
+        s.set_mask(solid)
+    if eps is not None:
+        s.set_permittivity(eps)
+        if o is not None:
+            o.set_permittivity(eps)
+    return s, o
+
+
+def jumpy(shape, seed):
+    rng = np.random.default_rng(seed)
+    return np.where(rng.uniform(size=shape) < 0.3, 78.5, 1.0)
+
+
+CASES = [
+    # (id, shape, h, bc, extra)
+    ("march", (34, 12, 256), 1.0, "mixed", {}),
+    ("generic", (12, 10, 6), 1.0, "mixed", {}),
+    ("periodic", (32, 16, 128), 0.5, "perxz", {}),
+    ("mask", None, 1.0, "channel", {"mask": True}),
+    ("permittivity", (16, 20, 24), 1.0, "channel", {"eps": True}),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_fused_norm_cycles_match_oracle(mg, case):
+    name, shape, h, bc, extra = case
+    kw = dict(min_coarse=2)
+    solid = eps = None
+    if extra.get("mask"):
+        w = W.cfg5(scale=16, n_spheres=0)
+        shape, solid = w.shape, w.solid
+        kw = dict(min_coarse=w.min_coarse, nu1=3, nu2=3)
+    if extra.get("eps"):
+        eps = jumpy(shape, 3)
+    f = np.random.default_rng(11).uniform(-1, 1, shape)
+    if solid is not None:
+        f = np.where(solid, 0.0, f)
+    s, o = setup(mg, shape, h, bc, True, solid=solid, eps=eps, **kw)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(4)]
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(4)]
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    phi_fused = s.get_solution()
+    s.close()
+    # the default mode: same iterates, post-cycle norms
+    s, _ = setup(mg, shape, h, bc, False, solid=solid, eps=eps, oracle_too=False, **kw)
+    s.set_rhs(f)
+    hd = [s.vcycle() for _ in range(4)]
+    assert np.array_equal(s.get_solution(), phi_fused)
+    assert hd[-1] == s.residual_norm()
+    s.close()
+
+
+def test_fused_norm_solve_matches_oracle(mg):
+    w = W.cfg2(seed=1, shape=(128, 32, 32), n_spheres=20)
+    s, o = setup(mg, w.shape, w.h, "channel", True, min_coarse=4)
+    s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    o.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+    rc, cg, hg = s.solve(1e-8, 40)
+    so, co, ho = o.solve(1e-8, 40)
+    assert rc == 0 and so == 0 and cg == co
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    # the stopping value bounds the true residual of the final iterate
+    assert s.residual_norm() <= hg[-1]
+    s.close()
+
+
+@pytest.mark.parametrize("Pn", [2, 4])
+def test_fused_norm_loopback_slabs(mg, Pn):
+    """Partials of several slab grids (and, below agglomeration, the generic
+    kernels) summed in slab order: the 1-slab norms to 1e-13, Phi bitwise."""
+    w = W.cfg2(seed=0, shape=(128, 32, 32), n_spheres=20)
+    res = []
+    for p in (1, Pn):
+        kw = dict(min_coarse=4, agglomerate_below=512)
+        if p > 1:
+            kw.update(nranks=p, halo="loopback")
+        s, _ = setup(mg, w.shape, w.h, "channel", True, oracle_too=False, **kw)
+        s.set_rhs_from_spheres(w.centers, w.radii, w.charges)
+        r = [s.vcycle() for _ in range(5)]
+        res.append((r, s.get_solution()))
+        s.close()
+    assert np.array_equal(res[0][1], res[1][1])
+    assert np.allclose(res[0][0], res[1][0], rtol=1e-13, atol=0)
+
+
+def test_fused_norm_config3_size(mg):
+    """512^3 (the bench workload): the fused kernel's norm of cycle k equals
+    the separate norm pass on the pre-smoothed iterate, reproduced through
+    the step API from the previous iterate."""
+    w = W.cfg3(256, seed=0, cycles=3)
+    s, _ = setup(mg, w.shape, w.h, "mixed", True, oracle_too=False, min_coarse=8)
+    s.set_rhs(w.rhs)
+    t, _ = setup(mg, w.shape, w.h, "mixed", False, oracle_too=False, min_coarse=8)
+    t.set_rhs(w.rhs)
+    for _ in range(3):
+        t.set_solution(s.get_solution())
+        r = s.vcycle()
+        for _ in range(2):
+            t.smooth_half(0, 0)
+            t.smooth_half(0, 1)
+        ref = t.residual_norm()
+        assert abs(r - ref) <= 1e-12 * ref, (r, ref)
+    s.close()
+    t.close()
