@@ -235,9 +235,12 @@ int mg_get_stencil(mg_ctx *ctx, int level, double *out, int where);
  * several spheres receive the sum.  Then the finest-grid BC adaptation
  * (P:731-732).  centers[3n] (x,y,z physical), radii[n], charges[n] are host
  * arrays, read before return; every rank passes the full list.
- * Errors: n < 0, R <= 0, subsample outside 1..16, a sphere that covers no
- * sub-cell centre with PER_CELLS (MG_ERR_ARG).  Phi is not touched (warm
- * start). */
+ * Errors: n < 0, R <= 0, subsample outside 1..16, a bad normalization or
+ * periodic-axis placement (MG_ERR_ARG before anything is written: f keeps
+ * its previous value); a sphere that covers no sub-cell centre with
+ * PER_CELLS (MG_ERR_ARG, detected by the mapping itself: f then holds the
+ * other spheres' density -- set it again).  Phi is not touched (warm start,
+ * P:1321-1322). */
 int mg_set_rhs_from_spheres(mg_ctx *ctx, int n, const double *centers,
                             const double *radii, const double *charges,
                             int normalization, int subsample);

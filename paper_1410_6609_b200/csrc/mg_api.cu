@@ -1315,7 +1315,6 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   }
   if ((size_t)n > c->sph_cap) {
     if (c->sph) cudaFree(c->sph);
-  if (c->fbuf) cudaFree(c->fbuf);
     c->sph = nullptr;
     c->sph_cap = 0;
     CK(cudaMalloc(&c->sph, sizeof(double) * 5 * (size_t)n + sizeof(unsigned long long) * (size_t)n));
