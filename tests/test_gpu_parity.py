@@ -635,6 +635,26 @@ def test_coulomb_forces_parity(mg, norm, sub):
     assert np.allclose(Fg, Fo, rtol=1e-12, atol=1e-12 * np.abs(Fo).max())
 
 
+def test_coulomb_forces_config4_recipe(mg):
+    """The time-stepping regime's force step (config-4 recipe: R = 6 at 5 %
+    volume, s_F = 2) on a 128 x 96 x 96 box: mostly interior spheres, which
+    take the staged-gradient path, plus wall-touching ones."""
+    shape = (128, 96, 96)
+    w = W.cfg4(P=1, n=96, seed=2)
+    c, q = W.random_spheres(shape, 6.0, 120, seed=4)
+    r = np.full(len(q), 6.0)
+    s, o = pair(mg, shape, 1.0, "channel", min_coarse=4)
+    s.set_rhs_from_spheres(c, r, q, subsample=2)
+    for _ in range(4):
+        s.vcycle()
+    o.set_phi(s.get_solution())
+    Fg = s.coulomb_forces(c, r, q, subsample=2)
+    Fo = o.coulomb_forces(c, r, q, subsample=2)
+    assert np.abs(Fo).max() > 0
+    assert np.allclose(Fg, Fo, rtol=1e-12, atol=1e-12 * np.abs(Fo).max())
+    del w
+
+
 def test_coulomb_forces_after_solve_and_masked(mg):
     """Forces on a solved config-5 (masked) potential: solid cells carry no
     force and are not gradient neighbours (reading d6)."""
