@@ -1,5 +1,6 @@
 """Per-phase times of config-3 V-cycles (CUDA events between the level-0
-phases, profiling mode): python scripts/cycle_times.py [n] [cycles]"""
+phases, profiling mode): python scripts/cycle_times.py [n] [cycles] [fused]
+(fused = 1: mg_opts.fused_norm, reading c11)"""
 import os
 import sys
 
@@ -11,8 +12,9 @@ from paper_1410_6609_b200 import workloads as W  # noqa: E402
 
 n = int(sys.argv[1]) if len(sys.argv) > 1 else 512
 cycles = int(sys.argv[2]) if len(sys.argv) > 2 else 8
+fused = len(sys.argv) > 3 and sys.argv[3] == "1"
 w = W.cfg3(n, seed=0, with_rhs=False)
-s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
+s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8, fused_norm=fused)
 s.set_rhs(W.uniform_rhs(w.shape, 0))
 for _ in range(3):
     s.vcycle()
