@@ -244,7 +244,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const int z0 = 2 * k + p;
         double s0, s1, d0, d1;
         unsigned cd0 = 64, cd1 = 64;
-        if (MASK) {
+        if (MASK && !__all_sync(__activemask(), cr[c] == kOpenPair)) {
           const unsigned cc2 = cr[c];
           cd0 = cc2 & 0xffu;
           cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
@@ -252,6 +252,14 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           s1 = ksum(cd1, a.y, b.y, ym.y, yp.y, zm1, zp1);
           d0 = kdiag(g, cd0, i, j, z0);
           d1 = kdiag(g, cd1, i, j, z0 + 2);
+        } else if (MASK) {
+          // the whole warp on fluid cells with all six faces open (the bulk
+          // of a masked level): kappa = 1 everywhere and no domain face, so
+          // ksum is the plain sum and kdiag = popc(63) = 6 -- the same bits
+          if (k + 1 >= g.nzh) cd1 = 0u;
+          s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
+          s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
+          d0 = d1 = 6.0;
         } else {
           s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
           s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
@@ -426,6 +434,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const int kl = 2 * lane + 64 * c;  // tile-relative half-index
         const int k = kz0 + kl;
         if (k >= g.nzh) continue;
+        // the warp's cells of both colours all fluid with six open faces:
+        // the plain-box arithmetic gives the same bits (see the smoother)
+        const bool open =
+            MASK && __all_sync(__activemask(), cR[c] == kOpenPair && cB[c] == kOpenPair);
         double r[2][2];  // [colour][element]
 #pragma unroll
         for (int col = 0; col < 2; col++) {
@@ -456,7 +468,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           const int z0 = 2 * k + p;
           double s0, s1, d0, d1;
           unsigned cd0 = 64, cd1 = 64;
-          if (MASK) {
+          if (MASK && !open) {
             const unsigned cc2 = col ? cB[c] : cR[c];
             cd0 = cc2 & 0xffu;
             cd1 = (k + 1 < g.nzh) ? (cc2 >> 8) : 0u;
@@ -464,6 +476,11 @@ __global__ void __launch_bounds__(kThreadsM, 2)
             s1 = ksum(cd1, a.y, bb.y, ym.y, yp.y, zm1, zp1);
             d0 = kdiag(g, cd0, i, j, z0);
             d1 = kdiag(g, cd1, i, j, z0 + 2);
+          } else if (MASK) {
+            if (k + 1 >= g.nzh) cd1 = 0u;
+            s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
+            s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
+            d0 = d1 = 6.0;
           } else {
             s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
             s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;

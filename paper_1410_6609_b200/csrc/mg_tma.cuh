@@ -84,6 +84,10 @@ __device__ __forceinline__ int ndir_m(const Grid &g, int i, int j, int z) {
 
 // kappa in {0,1}: kappa*phi is phi or a signed zero; selecting +0 instead
 // changes at most the sign of an exactly-zero sum, never a nonzero value
+// face codes of a pair of fluid cells with all six faces open (kappa = 1):
+// 0x7F per cell (bit 6 fluid, bits 0-5 the faces)
+constexpr unsigned kOpenPair = 0x7F7Fu;
+
 __device__ __forceinline__ double ksum(unsigned cd, double xm, double xp,
                                        double ym, double yp, double zm,
                                        double zp) {
