@@ -377,6 +377,25 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     }
   }
 
+  // periodic z: the other colour's row ends (half-indices nzh-1 and 0) of
+  // plane il, [wlo(own R), wlo(own B), whi(own R), whi(own B)], read by the
+  // tiles at the row ends with direct loads (the arrays are not written
+  // here), one plane ahead so that their latency hides behind a plane
+  double wr[4] = {0.0, 0.0, 0.0, 0.0};
+  auto load_wrap = [&](int il, double *w) {
+    if (!(PER && g.per[2]) || !row_ok) return;
+    const long long ro = (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
+    if (zt == 0) {
+      w[0] = g.phiB[ro + g.nzh - 1];
+      w[1] = g.phiR[ro + g.nzh - 1];
+    }
+    if (zt == nzt - 1) {
+      w[2] = g.phiB[ro];
+      w[3] = g.phiR[ro];
+    }
+  };
+  if (PER) load_wrap(i0, wr);
+
   for (int il = i0; il < i1; il++) {
     const int q = il - i0 + 1;
     __syncthreads();
@@ -393,6 +412,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     double2 nR[2], nB[2];
     unsigned ncR[2] = {0x4040u, 0x4040u}, ncB[2] = {0x4040u, 0x4040u};
     const bool more = il + 1 < i1;
+    double nwr[4] = {0.0, 0.0, 0.0, 0.0};
+    if (PER && more) load_wrap(il + 1, nwr);
 #pragma unroll
     for (int c = 0; c < 2; c++) {
       const int k = kz0 + 2 * lane + 64 * c;
@@ -414,21 +435,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const size_t oc = (size_t)(q % kSlots) * sd + (warp + 1) * W + zoff;
       const size_t om = (size_t)((q - 1) % kSlots) * sd + (warp + 1) * W + zoff;
       const size_t op = (size_t)((q + 1) % kSlots) * sd + (warp + 1) * W + zoff;
-      // periodic z: the other colour's row ends (half-indices nzh-1 and 0),
-      // loaded once per row and plane by the tiles at the row ends (a
-      // warp-uniform broadcast load; the arrays are not written here)
-      double wlo[2] = {0.0, 0.0}, whi[2] = {0.0, 0.0};  // [own colour]
-      if (PER && g.per[2]) {
-        const long long ro = (long long)(il + 1) * g.plane + (long long)(j + 1) * g.pz;
-        if (zt == 0) {
-          wlo[0] = g.phiB[ro + g.nzh - 1];
-          wlo[1] = g.phiR[ro + g.nzh - 1];
-        }
-        if (zt == nzt - 1) {
-          whi[0] = g.phiB[ro];
-          whi[1] = g.phiR[ro];
-        }
-      }
+      const double wlo[2] = {wr[0], wr[1]}, whi[2] = {wr[2], wr[3]};  // [own colour]
 #pragma unroll
       for (int c = 0; c < 2; c++) {
         const int kl = 2 * lane + 64 * c;  // tile-relative half-index
@@ -550,6 +557,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       cR[c] = ncR[c];
       cB[c] = ncB[c];
     }
+    if (PER)
+#pragma unroll
+      for (int e = 0; e < 4; e++) wr[e] = nwr[e];
   }
   if (MODE != MODE_RESTRICT) {
     // deterministic block reduction
