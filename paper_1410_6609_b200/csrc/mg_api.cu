@@ -929,6 +929,7 @@ void free_mask(mg_ctx *c) {
       g.codeR = g.codeB = nullptr;
       g.coefR = g.coefB = nullptr;
       g.c64R = g.c64B = nullptr;
+      g.all_unknown = 0;
     }
   c->masked = false;
 }
@@ -1652,6 +1653,7 @@ int rebuild_coefficients(mg_ctx *c) {
         CK(cudaMemsetAsync(b, 0, nb, c->stream));
         g.c64R = r;
         g.c64B = b;
+        g.all_unknown = dmask == nullptr;
       }
     for (Grid &g : c->g[0])
       mg::launch_level0_coef64(g, dmask, deps, c->fbc, const_cast<double *>(g.c64R),

@@ -37,6 +37,9 @@ struct Grid {
   // [kappa_q (6), D, eps_c (level 0) / 0]: a_q = -c kappa_q, a_cc = c D, with
   // real-valued kappa (harmonic face means on level 0, Galerkin R A P below)
   const double *c64R, *c64B;
+  // every cell of the level is an unknown (records without a solid mask):
+  // kernels that only need the unknown flag skip the records
+  int all_unknown;
   // periodic axes ("accessing unknowns in cells at opposite sides
   // of the domain"): per[a] = 1 for a periodic axis (dface = 0 on its faces).
   // Ghost layers then hold the opposite side's cells: rows 0 / ny+1 mirror

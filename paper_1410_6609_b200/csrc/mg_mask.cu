@@ -51,12 +51,17 @@ struct Coef {
 // coefficients of the cell of colour col at split element e, global (i,j,z)
 __device__ __forceinline__ void coef_at(const Grid &g, int col, long long e,
                                         int i, int j, int z, Coef &C) {
-  if (g.c64R) {  // permittivity: fp64 records
-    const double *r = (col ? g.c64B : g.c64R) + 8 * e;
-#pragma unroll
-    for (int q = 0; q < 6; q++) C.k[q] = r[q];
-    C.D = r[6];
-    C.delta = r[7];
+  if (g.c64R) {  // permittivity: fp64 records, 64-byte aligned, 16-byte loads
+    const double2 *r = reinterpret_cast<const double2 *>((col ? g.c64B : g.c64R) + 8 * e);
+    const double2 r0 = r[0], r1 = r[1], r2 = r[2], r3 = r[3];
+    C.k[0] = r0.x;
+    C.k[1] = r0.y;
+    C.k[2] = r1.x;
+    C.k[3] = r1.y;
+    C.k[4] = r2.x;
+    C.k[5] = r2.y;
+    C.D = r3.x;
+    C.delta = r3.y;
   } else if (g.coefR == nullptr) {
     const unsigned cd = (col ? g.codeB : g.codeR)[e];
     int n = 0;
@@ -73,12 +78,17 @@ __device__ __forceinline__ void coef_at(const Grid &g, int col, long long e,
       C.delta = 0.0;
       C.D = 0.0;
     }
-  } else {
-    const float *r = (col ? g.coefB : g.coefR) + 8 * e;
-#pragma unroll
-    for (int q = 0; q < 6; q++) C.k[q] = (double)r[q];
-    C.D = (double)r[6];
-    C.delta = (double)r[7];
+  } else {  // float records, 32-byte aligned, 16-byte loads
+    const float4 *r = reinterpret_cast<const float4 *>((col ? g.coefB : g.coefR) + 8 * e);
+    const float4 r0 = r[0], r1 = r[1];
+    C.k[0] = (double)r0.x;
+    C.k[1] = (double)r0.y;
+    C.k[2] = (double)r0.z;
+    C.k[3] = (double)r0.w;
+    C.k[4] = (double)r1.x;
+    C.k[5] = (double)r1.y;
+    C.D = (double)r1.z;
+    C.delta = (double)r1.w;
   }
 }
 
@@ -529,9 +539,11 @@ __global__ void __launch_bounds__(kT) k_prolong_var(Grid F, Grid C, double alpha
   const int i = F.x0 + il;
   const int col = (i + j + z) & 1;
   const long long e = rb(F, il, j) + (z >> 1);
-  Coef cf;
-  coef_at(F, col, e, i, j, z, cf);
-  if (cf.D == 0.0) return;
+  if (!F.all_unknown) {  // unknowns only; without a mask all cells are
+    Coef cf;
+    coef_at(F, col, e, i, j, z, cf);
+    if (cf.D == 0.0) return;
+  }
   const int I = i >> 1, J = j >> 1, Z = z >> 1;
   const double ec = (((I + J + Z) & 1) ? C.phiB : C.phiR)[rb(C, I - C.x0, J) + (Z >> 1)];
   double *u = col ? F.phiB : F.phiR;
