@@ -529,30 +529,33 @@ void launch_resid_restrict_var(const Grid &f, const Grid &c, cudaStream_t s) {
 }
 
 // ---- prolongation + magnified correction, fluid cells only --------------------
+// one CTA per fine row (il, j), threads along z (no 64-bit index division)
 __global__ void __launch_bounds__(kT) k_prolong_var(Grid F, Grid C, double alpha) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)F.nxl * F.ny * F.nz) return;
-  const int z = (int)(t % F.nz);
-  const long long q = t / F.nz;
-  const int j = (int)(q % F.ny);
-  const int il = (int)(q / F.ny);
+  const int j = (int)(blockIdx.x % (unsigned)F.ny);
+  const int il = (int)(blockIdx.x / (unsigned)F.ny);
   const int i = F.x0 + il;
-  const int col = (i + j + z) & 1;
-  const long long e = rb(F, il, j) + (z >> 1);
-  if (!F.all_unknown) {  // unknowns only; without a mask all cells are
-    Coef cf;
-    coef_at(F, col, e, i, j, z, cf);
-    if (cf.D == 0.0) return;
+  const int I = i >> 1, J = j >> 1;
+  const long long rf = rb(F, il, j), rc = rb(C, I - C.x0, J);
+  for (int z = threadIdx.x; z < F.nz; z += blockDim.x) {
+    const int col = (i + j + z) & 1;
+    const long long e = rf + (z >> 1);
+    if (!F.all_unknown) {  // unknowns only; without a mask all cells are
+      Coef cf;
+      coef_at(F, col, e, i, j, z, cf);
+      if (cf.D == 0.0) continue;
+    }
+    const int Z = z >> 1;
+    const double ec = (((I + J + Z) & 1) ? C.phiB : C.phiR)[rc + (Z >> 1)];
+    double *u = col ? F.phiB : F.phiR;
+    u[e] = u[e] + alpha * ec;
   }
-  const int I = i >> 1, J = j >> 1, Z = z >> 1;
-  const double ec = (((I + J + Z) & 1) ? C.phiB : C.phiR)[rb(C, I - C.x0, J) + (Z >> 1)];
-  double *u = col ? F.phiB : F.phiR;
-  u[e] = u[e] + alpha * ec;
 }
 
 void launch_prolong_var(const Grid &f, const Grid &c, double alpha, cudaStream_t s) {
-  const long long n = (long long)f.nxl * f.ny * f.nz;
-  if (n > 0) k_prolong_var<<<nblk(n), kT, 0, s>>>(f, c, alpha);
+  const long long rows = (long long)f.nxl * f.ny;
+  if (rows > 0 && f.nz > 0)
+    k_prolong_var<<<(unsigned)rows, f.nz < kT ? ((f.nz + 31) / 32) * 32 : kT, 0, s>>>(
+        f, c, alpha);
 }
 
 // ---- residual norm partials -------------------------------------------------------
