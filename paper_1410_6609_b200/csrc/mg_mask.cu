@@ -474,30 +474,34 @@ void launch_coef_to_code(const Grid &g, unsigned char *codeR, unsigned char *cod
 // ---- RBGS half-sweep, variable coefficients -----------------------------------
 __global__ void __launch_bounds__(kT)
     k_smooth_var(Grid g, int color, int from_zero) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)g.nxl * g.ny * g.nzh) return;
-  const int k = (int)(t % g.nzh);
-  const long long q = t / g.nzh;
-  const int j = (int)(q % g.ny);
-  const int il = (int)(q / g.ny);
+  // one CTA per row (il, j), threads along the half-index k
+  const int j = (int)(blockIdx.x % (unsigned)g.ny);
+  const int il = (int)(blockIdx.x / (unsigned)g.ny);
   const int i = g.x0 + il;
   const int p = (i + j + color) & 1;
-  const int z = 2 * k + p;
-  if (z >= g.nz) return;
-  const long long e = rb(g, il, j) + k;
-  Coef C;
-  coef_at(g, color, e, i, j, z, C);
-  if (C.D == 0.0) return;  // solid: not an unknown
+  const long long r0 = rb(g, il, j);
   const double *oth = color ? g.phiR : g.phiB;
   const double *f = color ? g.fB : g.fR;
   double *own = color ? g.phiB : g.phiR;
-  const double tsum = from_zero ? 0.0 : nbsum(g, oth, e, z, C);
-  own[e] = (f[e] * g.w + tsum) / C.D;
+  for (int k = threadIdx.x; k < g.nzh; k += blockDim.x) {
+    const int z = 2 * k + p;
+    if (z >= g.nz) break;
+    const long long e = r0 + k;
+    Coef C;
+    coef_at(g, color, e, i, j, z, C);
+    if (C.D == 0.0) continue;  // solid: not an unknown
+    const double tsum = from_zero ? 0.0 : nbsum(g, oth, e, z, C);
+    own[e] = (f[e] * g.w + tsum) / C.D;
+  }
 }
 
+// threads per row-CTA: the row's half-indices rounded up to a warp, <= kT
+inline unsigned row_threads(int n) { return n < kT ? (unsigned)((n + 31) / 32 * 32) : kT; }
+
 void launch_smooth_var(const Grid &g, int color, int from_zero, cudaStream_t s) {
-  const long long n = (long long)g.nxl * g.ny * g.nzh;
-  if (n > 0) k_smooth_var<<<nblk(n), kT, 0, s>>>(g, color, from_zero);
+  const long long rows = (long long)g.nxl * g.ny;
+  if (rows > 0 && g.nzh > 0)
+    k_smooth_var<<<(unsigned)rows, row_threads(g.nzh), 0, s>>>(g, color, from_zero);
 }
 
 // ---- residual + restriction ----------------------------------------------------
@@ -554,8 +558,7 @@ __global__ void __launch_bounds__(kT) k_prolong_var(Grid F, Grid C, double alpha
 void launch_prolong_var(const Grid &f, const Grid &c, double alpha, cudaStream_t s) {
   const long long rows = (long long)f.nxl * f.ny;
   if (rows > 0 && f.nz > 0)
-    k_prolong_var<<<(unsigned)rows, f.nz < kT ? ((f.nz + 31) / 32) * 32 : kT, 0, s>>>(
-        f, c, alpha);
+    k_prolong_var<<<(unsigned)rows, row_threads(f.nz), 0, s>>>(f, c, alpha);
 }
 
 // ---- residual norm partials -------------------------------------------------------
