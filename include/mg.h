@@ -300,6 +300,17 @@ int mg_vcycle(mg_ctx *ctx, double *res_norm_out);
  * phi_out alive until mg_wait; no per-cycle divergence check. */
 int mg_solve_async(mg_ctx *ctx, const double *f, int where_f, double *phi_out,
                    int where_phi, int cycles);
+/* Copy-out of the current level-0 Phi (natural layout, the rank's slab)
+ * without host synchronisation: the conversion from the split layout is
+ * enqueued on the context's stream into one of the library's three staging
+ * slots and, for where = MG_HOST, the device-to-host copy on the library's
+ * copy stream, so that it overlaps the work enqueued next (e.g. the next
+ * time step's RHS and cycles).  `out` (pinned host memory for overlap, or
+ * device memory) must stay alive and unread until mg_wait.  A fourth call
+ * before mg_wait reuses the first call's slot after its copy finished.
+ * Errors: null ctx / out, bad `where` (MG_ERR_ARG). */
+int mg_get_solution_async(mg_ctx *ctx, double *out, int where);
+
 /* Synchronise the context's streams (compute and copies); *res_norm_out
  * (may be NULL) = the residual norm after the last V-cycle.
  * MG_ERR_DIVERGED if it is NaN. */

@@ -1337,14 +1337,14 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   int rc = bc_adapt(c);
   if (rc) return rc;
   c->prev_norm = -1.0;
+  // the empty-sphere check reads back through mapped memory: a copy-engine
+  // transfer would queue behind a pending bulk download (get_solution_async)
+  const bool check = normalization == MG_CHARGE_PER_CELLS && n > 0;
+  if (check) mg::launch_first_empty(cnt, n, c->h_norm_dev + 1, c->stream);
+  CK(cudaGetLastError());
   if ((rc = sync(c))) return rc;
-  if (normalization == MG_CHARGE_PER_CELLS && n > 0) {
-    std::vector<unsigned long long> hc(n);
-    CK(cudaMemcpy(hc.data(), cnt, sizeof(unsigned long long) * n,
-                  cudaMemcpyDeviceToHost));
-    for (int p = 0; p < n; p++)
-      if (hc[p] == 0) return fail(MG_ERR_ARG, "sphere %d covers no cell centre", p);
-  }
+  if (check && c->h_norm[1] >= 0.0)
+    return fail(MG_ERR_ARG, "sphere %d covers no cell centre", (int)c->h_norm[1]);
   return MG_OK;
 }
 
@@ -1463,6 +1463,27 @@ int mg_solve_async(mg_ctx *c, const double *f, int where_f, double *phi_out,
       return rc;
     }
   }
+  return MG_OK;
+}
+
+int mg_get_solution_async(mg_ctx *c, double *out, int where) {
+  if (!c) return fail(MG_ERR_ARG, "null ctx");
+  if (!out) return fail(MG_ERR_ARG, "null out");
+  if (where != MG_HOST && where != MG_DEVICE) return fail(MG_ERR_ARG, "bad 'where'");
+  if (where == MG_DEVICE) return unpack0(c, MG_FIELD_PHI, out);
+  const size_t n = level_cells_held(c, 0);
+  int rc;
+  if ((rc = async_setup(c, n * sizeof(double)))) return rc;
+  const int q = (int)(c->async_k++ % 3);
+  double *stg = c->astg[q];
+  // the slot's previous download must have left it before it is rewritten
+  if (c->d2h_used[q]) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[q], 0));
+  if ((rc = unpack0(c, MG_FIELD_PHI, stg))) return rc;
+  CK(cudaEventRecord(c->ev_out[q], c->stream));
+  CK(cudaStreamWaitEvent(c->s_d2h, c->ev_out[q], 0));
+  CK(cudaMemcpyAsync(out, stg, n * sizeof(double), cudaMemcpyDeviceToHost, c->s_d2h));
+  CK(cudaEventRecord(c->ev_d2h[q], c->s_d2h));
+  c->d2h_used[q] = true;
   return MG_OK;
 }
 

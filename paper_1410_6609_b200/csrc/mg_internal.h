@@ -152,6 +152,9 @@ void launch_sum_ordered(const double *parts, int n, double *out,
 // host memory)
 void launch_publish(const double *src, double *dev_dst, double *host_dst,
                     cudaStream_t s);
+// first sphere index with a zero covered count (-1: none) -> mapped host word
+void launch_first_empty(const unsigned long long *counts, int n, double *host_dst,
+                        cudaStream_t s);
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s);
 size_t coarse_cg_scratch_doubles(const Grid &g);

@@ -355,6 +355,27 @@ void launch_publish(const double *src, double *dev_dst, double *host_dst,
   k_publish<<<1, 1, 0, s>>>(src, dev_dst, host_dst);
 }
 
+// index of the first sphere whose covered count is 0 (or -1), written to
+// mapped host memory like k_publish (no copy-engine transfer)
+__global__ void __launch_bounds__(kThreads)
+    k_first_empty(const unsigned long long *counts, int n, double *host_dst) {
+  __shared__ int first;
+  if (threadIdx.x == 0) first = n;
+  __syncthreads();
+  for (int p = threadIdx.x; p < n; p += blockDim.x)
+    if (counts[p] == 0ull) atomicMin(&first, p);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    host_dst[0] = first < n ? (double)first : -1.0;
+    __threadfence_system();
+  }
+}
+
+void launch_first_empty(const unsigned long long *counts, int n, double *host_dst,
+                        cudaStream_t s) {
+  if (n > 0) k_first_empty<<<1, kThreads, 0, s>>>(counts, n, host_dst);
+}
+
 // ---------------------------------------------------------------------------
 // Coarsest-grid CG: one CTA, Hestenes-Stiefel from x = 0, stop at
 // ||r|| <= tol ||b|| or maxit.  Vectors in natural order, in shared memory

@@ -109,6 +109,7 @@ def lib():
         L.mg_vcycle.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_solve_async.argtypes = [P, dp, i, dp, i, i]
         L.mg_wait.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
+        L.mg_get_solution_async.argtypes = [P, dp, i]
         L.mg_solve.argtypes = [P, d, ip, dp]
         L.mg_residual_norm.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_get_solution.argtypes = [P, dp, i]
@@ -337,6 +338,14 @@ class Multigrid:
         pp, pw = self._io_args_nosync(phi_out)
         _check(lib().mg_solve_async(self._ctx, fp, fw, pp, pw, int(cycles)),
                self._ctx)
+
+    def get_solution_async(self, out):
+        """Enqueue the copy-out of Phi into `out` (a pinned host or CUDA
+        float64 tensor of the slab's shape) without host synchronisation
+        (mg_get_solution_async); the download overlaps the work enqueued
+        next.  Call wait() before reading `out`."""
+        p, w = self._io_args_nosync(out)
+        _check(lib().mg_get_solution_async(self._ctx, p, w), self._ctx)
 
     def wait(self) -> float:
         r = ctypes.c_double(0.0)

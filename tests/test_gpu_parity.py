@@ -825,6 +825,44 @@ def test_full_sweep_kernels_equal_half_sweeps(mg, shape, bc, h, monkeypatch):
     assert out[0][0] == out[1][0]
 
 
+def test_get_solution_async_overlapped_steps(mg):
+    """mg_get_solution_async: the copy-outs of five consecutive sphere steps
+    (more than the three staging slots), each overlapping the next step's
+    RHS and cycles, equal the synchronous copy-outs bit for bit; also into
+    device memory."""
+    import torch
+    w = W.cfg2(seed=2, shape=(128, 32, 32), n_spheres=20)
+    steps = []
+    for k in range(5):
+        c = w.centers + 0.3 * k
+        steps.append((c, w.radii, w.charges))
+    ref = []
+    s, _ = pair(mg, w.shape, w.h, "channel", min_coarse=4)
+    for c, r, q in steps:
+        s.zero_solution()
+        s.set_rhs_from_spheres(c, r, q)
+        for _ in range(3):
+            s.vcycle()
+        ref.append(s.get_solution())
+    s.close()
+    s, _ = pair(mg, w.shape, w.h, "channel", min_coarse=4)
+    outs = [torch.empty(w.shape, dtype=torch.float64).pin_memory() for _ in steps]
+    for (c, r, q), o in zip(steps, outs):
+        s.zero_solution()
+        s.set_rhs_from_spheres(c, r, q)
+        for _ in range(3):
+            s.vcycle()
+        s.get_solution_async(o)
+    s.wait()
+    for o, e in zip(outs, ref):
+        assert np.array_equal(o.numpy(), e)
+    od = torch.empty(w.shape, dtype=torch.float64, device="cuda")
+    s.get_solution_async(od)
+    s.wait()
+    assert np.array_equal(od.cpu().numpy(), ref[-1])
+    s.close()
+
+
 def test_solve_async_pipelined_equals_sync(mg):
     """mg_solve_async pipelining independent solves (pinned host buffers,
     uploads / downloads on copy streams overlapping the cycles) gives the
