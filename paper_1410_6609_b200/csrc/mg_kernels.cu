@@ -507,10 +507,12 @@ template <bool PER>
 static void launch_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
-  // 256 threads: enough for <= 16 elements per thread at the coarsest sizes,
-  // few warps in each block reduction
+  // 256 threads below 2048 unknowns, 512 from there (more warps hide the smem
+  // latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at
+  // P = 8, 476 vs 557 us; 1024 threads are slower again)
   int threads = (int)((N + 31) / 32 * 32);
-  if (threads > 256) threads = 256;
+  const int cap = N >= 2048 ? 512 : 256;
+  if (threads > cap) threads = cap;
   size_t smem = 0;
   if (N <= kCgSmemMax) {
     // x, r, p, q + neighbour bits (1 byte; 2 with periodic wrap) + centre
