@@ -610,11 +610,23 @@ int prolong_red_level(mg_ctx *c, int l) {
   return halo(c, l, 0);  // black is recomputed by the next half-sweep
 }
 
+// MG_CG_CLUSTER=0 keeps the single-CTA CG on the large coarsest grids too
+bool cg_cluster_on() {
+  static const bool on = [] {
+    const char *e = getenv("MG_CG_CLUSTER");
+    return !(e && atoi(e) == 0);
+  }();
+  return on;
+}
+
 int coarse_solve(mg_ctx *c) {
   const Grid &g = c->g[c->pl.L - 1][0];
   if (c->masked)
     mg::launch_coarse_cg_var(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
                              c->cg_iters, c->stream);
+  else if (cg_cluster_on() && mg::coarse_cg_cluster_supported(g))
+    mg::launch_coarse_cg_cluster(g, c->o.coarse_tol, c->o.coarse_maxit, c->cg_iters,
+                                 c->stream);
   else
     mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
                          c->cg_iters, c->stream);

@@ -1,0 +1,211 @@
+// Coarsest-grid CG on a thread-block cluster (sm_100a): the same
+// Hestenes-Stiefel iteration as k_coarse_cg -- x = 0, r = p = b, q = A p,
+// alpha = rho / (p.q), x += alpha p, r -= alpha q, stop at
+// sqrt(rho') <= tol ||b|| or maxit, p = r + beta p -- with the unknowns
+// (natural order) split into kCK contiguous chunks, one per CTA of the
+// cluster, each chunk's vectors in that CTA's shared memory.  The matrix-
+// vector product reads neighbour values of other chunks through distributed
+// shared memory; dot products are per-CTA partials (warp-shuffle tree, warps
+// in order) that every thread sums in cluster-rank order after a cluster
+// barrier, so all CTAs take the same decisions.  Three cluster barriers per
+// iteration replace the single-CTA kernel's serial per-thread loops: the
+// large coarsest grids of agglomerated multi-GPU runs (64 x 8 x 8 at P = 8)
+// spread over kCK SMs.  Measured (scripts/cg_probe.py): 0.42 ms vs 0.48 ms
+// for 64 x 8 x 8; clusters of 4 (0.51) and 16 (0.45, non-portable) slower.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <type_traits>
+
+#include "mg_internal.h"
+
+namespace cgr = cooperative_groups;
+
+namespace mg {
+
+namespace {
+
+constexpr int kCK = 8;          // CTAs per cluster (portable size)
+constexpr int kCT = 512;        // threads per CTA
+constexpr int kChunkMax = 4096; // unknowns per CTA
+
+__device__ __forceinline__ int centre_dc(const Grid &g, int i, int j, int z) {
+  int d = 6;
+  if (i == 0) d += g.dface[0];
+  if (i == g.nx - 1) d += g.dface[1];
+  if (j == 0) d += g.dface[2];
+  if (j == g.ny - 1) d += g.dface[3];
+  if (z == 0) d += g.dface[4];
+  if (z == g.nz - 1) d += g.dface[5];
+  return d;
+}
+
+__device__ __forceinline__ long long split_at(const Grid &g, int n, int *col) {
+  const int z = n % g.nz, t = n / g.nz;
+  const int j = t % g.ny, i = t / g.ny;
+  *col = (g.x0 + i + j + z) & 1;
+  return (long long)(i + 1) * g.plane + (long long)(j + 1) * g.pz + (z >> 1);
+}
+
+// this CTA's partial of a dot product (thread 0's return value is valid)
+__device__ __forceinline__ double cta_partial(double v, double *wpart) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = v;
+  __syncthreads();
+  double s = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s = s + wpart[w];
+  return s;
+}
+
+}  // namespace
+
+template <bool PER>
+__global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
+    k_coarse_cg_cluster(Grid g, double tol, int maxit, int *iters_out, int chunk) {
+  using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
+  cgr::cluster_group cl = cgr::this_cluster();
+  const int rank = (int)cl.block_rank();
+  extern __shared__ __align__(16) double cgs[];
+  __shared__ double part[2];            // this CTA's partials: [0] p.q, [1] r.r
+  __shared__ double wpart[kCT / 32];
+  __shared__ const double *rp[kCK];     // every CTA's p (distributed smem)
+  __shared__ const double *rpart[kCK];  // every CTA's partials
+
+  const int N = g.nx * g.ny * g.nz;
+  const int n0 = rank * chunk;
+  const int nl = max(0, min(chunk, N - n0));  // unknowns of this CTA
+  double *p = cgs, *x = cgs + chunk, *r = cgs + 2 * chunk, *q = cgs + 3 * chunk;
+  NB *nb = reinterpret_cast<NB *>(cgs + 4 * chunk);
+  signed char *dc = reinterpret_cast<signed char *>(nb + chunk);
+  if (threadIdx.x < kCK) {
+    rp[threadIdx.x] = cl.map_shared_rank(p, (int)threadIdx.x);
+    rpart[threadIdx.x] = cl.map_shared_rank(part, (int)threadIdx.x);
+  }
+  const int sx = g.ny * g.nz, sy = g.nz;
+  const int wx = (g.nx - 1) * sx, wy = (g.ny - 1) * sy, wz = g.nz - 1;
+
+  // geometry (neighbour bits as k_coarse_cg: 0-5 inside, 6-11 periodic) and b
+  double acc = 0.0;
+  for (int e = threadIdx.x; e < nl; e += blockDim.x) {
+    const int n = n0 + e;
+    const int z = n % g.nz, t = n / g.nz;
+    const int j = t % g.ny, i = t / g.ny;
+    const int in[6] = {i > 0, i < g.nx - 1, j > 0, j < g.ny - 1, z > 0, z < g.nz - 1};
+    unsigned m = 0;
+#pragma unroll
+    for (int a = 0; a < 6; a++)
+      m |= in[a] ? (1u << a) : ((PER && g.per[a >> 1]) ? (64u << a) : 0u);
+    nb[e] = (NB)m;
+    dc[e] = (signed char)centre_dc(g, i, j, z);
+    int col;
+    const long long idx = split_at(g, n, &col);
+    const double b = col ? g.fB[idx] : g.fR[idx];
+    x[e] = 0.0;
+    r[e] = b;
+    p[e] = b;
+    acc = acc + b * b;
+  }
+  auto cluster_sum = [&](double v, int slot) {
+    const double s = cta_partial(v, wpart);
+    if (threadIdx.x == 0) part[slot] = s;
+    cl.sync();
+    double tot = 0.0;
+#pragma unroll
+    for (int k = 0; k < kCK; k++) tot = tot + rpart[k][slot];
+    return tot;
+  };
+  // p of global unknown m (own chunk from local smem, else the owner's)
+  auto pv = [&](int m) {
+    const int k = m / chunk;
+    return k == rank ? p[m - n0] : rp[k][m - k * chunk];
+  };
+  double rho = cluster_sum(acc, 1);  // the barrier also publishes p, rp
+  const double bnorm = sqrt(rho);
+  const double c = g.c;
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      acc = 0.0;
+      for (int e = threadIdx.x; e < nl; e += blockDim.x) {
+        const int n = n0 + e;
+        const unsigned m = nb[e];
+        const double xm = (m & 1) ? pv(n - sx) : ((PER && (m & 64)) ? pv(n + wx) : 0.0);
+        const double xp = (m & 2) ? pv(n + sx) : ((PER && (m & 128)) ? pv(n - wx) : 0.0);
+        const double ym = (m & 4) ? pv(n - sy) : ((PER && (m & 256)) ? pv(n + wy) : 0.0);
+        const double yp = (m & 8) ? pv(n + sy) : ((PER && (m & 512)) ? pv(n - wy) : 0.0);
+        const double zm = (m & 16) ? pv(n - 1) : ((PER && (m & 1024)) ? pv(n + wz) : 0.0);
+        const double zp = (m & 32) ? pv(n + 1) : ((PER && (m & 2048)) ? pv(n - wz) : 0.0);
+        const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
+        const double pn = p[e];
+        const double qn = c * ((double)dc[e] * pn - s);
+        q[e] = qn;
+        acc = acc + pn * qn;
+      }
+      const double pq = cluster_sum(acc, 0);
+      const double a = rho / pq;
+      acc = 0.0;
+      for (int e = threadIdx.x; e < nl; e += blockDim.x) {
+        x[e] = x[e] + a * p[e];
+        const double rn = r[e] - a * q[e];
+        r[e] = rn;
+        acc = acc + rn * rn;
+      }
+      const double rho1 = cluster_sum(acc, 1);
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      const double beta = rho1 / rho;
+      for (int e = threadIdx.x; e < nl; e += blockDim.x) p[e] = r[e] + beta * p[e];
+      cl.sync();  // p complete (every CTA) before the next matrix-vector product
+      rho = rho1;
+    }
+  }
+  for (int e = threadIdx.x; e < nl; e += blockDim.x) {
+    int col;
+    const long long idx = split_at(g, n0 + e, &col);
+    (col ? g.phiB : g.phiR)[idx] = x[e];
+  }
+  if (rank == 0 && threadIdx.x == 0 && iters_out) *iters_out = it;
+  cl.sync();  // no CTA exits while another may still read its smem
+}
+
+bool coarse_cg_cluster_supported(const Grid &g) {
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  // from 4096 unknowns (64 x 8 x 8: 0.42 vs 0.48 ms single-CTA); on 32 x 8 x 8
+  // the three cluster barriers per iteration cost more than they save
+  return g.nxl == g.nx && g.x0 == 0 && N >= 4096 && (N + kCK - 1) / kCK <= kChunkMax;
+}
+
+template <bool PER>
+static void launch_cc(const Grid &g, double tol, int maxit, int *iters_out,
+                      cudaStream_t s) {
+  const int N = g.nx * g.ny * g.nz;
+  const int chunk = (N + kCK - 1) / kCK;
+  using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
+  const size_t smem = (size_t)chunk * (4 * sizeof(double) + sizeof(NB) + 1);
+  static size_t configured = 0;
+  static bool nonportable = false;
+  if (kCK > 8 && !nonportable) {
+    cudaFuncSetAttribute(k_coarse_cg_cluster<PER>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    nonportable = true;
+  }
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_coarse_cg_cluster<PER>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    configured = smem;
+  }
+  const int threads = chunk < kCT ? (chunk + 31) / 32 * 32 : kCT;
+  k_coarse_cg_cluster<PER><<<kCK, threads, smem, s>>>(g, tol, maxit, iters_out, chunk);
+}
+
+void launch_coarse_cg_cluster(const Grid &g, double tol, int maxit, int *iters_out,
+                              cudaStream_t s) {
+  if (is_periodic(g))
+    launch_cc<true>(g, tol, maxit, iters_out, s);
+  else
+    launch_cc<false>(g, tol, maxit, iters_out, s);
+}
+
+}  // namespace mg

@@ -150,6 +150,11 @@ void launch_sum_ordered(const double *parts, int n, double *out,
                         cudaStream_t s);
 // dev_dst[0] = host_dst[0] = src[0] (host_dst: device view of mapped pinned
 // host memory)
+// coarsest CG on a thread-block cluster (mg_cg_cluster.cu): grids held
+// whole with 4096 .. 8 x 4096 unknowns
+bool coarse_cg_cluster_supported(const Grid &g);
+void launch_coarse_cg_cluster(const Grid &g, double tol, int maxit, int *iters_out,
+                              cudaStream_t s);
 void launch_publish(const double *src, double *dev_dst, double *host_dst,
                     cudaStream_t s);
 // first sphere index with a zero covered count (-1: none) -> mapped host word

@@ -192,6 +192,35 @@ def test_coarse_cg(mg):
     assert rel(s.get_field(L, mg.MG_FIELD_PHI), o.phi(L)) < 1e-11
 
 
+@pytest.mark.parametrize("shape,bt,bv", [
+    ((64, 8, 8), [N, N, D, D, N, N], [0, 0, 0, 1, 0, 0]),     # config 4 P=8 coarsest
+    ((64, 16, 8), [N, D, N, D, N, D], [0.25, 1.0, -0.5, -1.0, 2.0, 0.0]),
+    ((16, 16, 24), [2, 2, D, N, 2, 2], [0, 0, 0.5, -0.25, 0, 0]),  # x, z periodic
+    ((40, 10, 22), [D] * 6, [1.0, -2.0, 0.5, 3.0, -1.0, 2.0]),   # ragged chunks
+])
+def test_coarse_cg_cluster(mg, shape, bt, bv, monkeypatch):
+    """The cluster CG (8 CTAs, distributed shared memory) on large coarsest
+    grids: the oracle's CG solution to 1e-11, iteration counts within 2 (the
+    dot products sum in another order), and the single-CTA kernel's
+    solution (MG_CG_CLUSTER=0) to 1e-12."""
+    f = np.random.default_rng(9).uniform(-1, 1, shape)
+    o = oracle.Oracle(shape, 1.0, bt, bv, max_levels=1)
+    o.set_rhs_raw(f, 0)
+    ito = o.cg(0, 1e-12, 1000)
+    out = []
+    for cluster in (True, False):
+        if not cluster:
+            monkeypatch.setenv("MG_CG_CLUSTER", "0")
+        s = mg.Multigrid(shape, 1.0, bt, bv, max_levels=1)
+        s.set_field(0, mg.MG_FIELD_RHS, f)
+        it = s.coarse_solve()
+        out.append((it, s.get_field(0, mg.MG_FIELD_PHI)))
+        s.close()
+    assert abs(out[0][0] - ito) <= 2 and abs(out[1][0] - ito) <= 2
+    assert rel(out[0][1], o.phi(0)) < 1e-11
+    assert rel(out[0][1], out[1][1]) < 1e-12
+
+
 def check_history(hg, ho):
     assert len(hg) == len(ho)
     r0 = ho[0]
