@@ -12,6 +12,7 @@
 // Hence no stencil is stored: the centre comes from the cell position.
 #include <cuda_runtime.h>
 
+#include <cstdint>
 #include <type_traits>
 
 #include "mg_internal.h"
@@ -736,16 +737,69 @@ __global__ void __launch_bounds__(kThreads)
   nat[t] = src[idx];
 }
 
+// even nz: one CTA per row (il, j), thread k moves the natural pair
+// (2k, 2k+1) -- one 16-byte access -- to half-index k of both colour arrays
+// (no 64-bit index division per cell)
+__global__ void __launch_bounds__(kThreads)
+    k_pack_rows(Grid g, int field, const double *nat) {
+  const int j = (int)(blockIdx.x % (unsigned)g.ny);
+  const int il = (int)(blockIdx.x / (unsigned)g.ny);
+  const bool p0 = (g.x0 + il + j) & 1;  // colour of z = 2k
+  const double2 *src = reinterpret_cast<const double2 *>(nat + (long long)blockIdx.x * g.nz);
+  const long long rb = rowbase(g, il, j);
+  double *R = (field ? g.fR : g.phiR) + rb;
+  double *B = (field ? g.fB : g.phiB) + rb;
+  for (int k = threadIdx.x; k < g.nzh; k += blockDim.x) {
+    const double2 v = src[k];
+    R[k] = p0 ? v.y : v.x;
+    B[k] = p0 ? v.x : v.y;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_unpack_rows(Grid g, int field, double *nat) {
+  const int j = (int)(blockIdx.x % (unsigned)g.ny);
+  const int il = (int)(blockIdx.x / (unsigned)g.ny);
+  const bool p0 = (g.x0 + il + j) & 1;
+  double2 *dst = reinterpret_cast<double2 *>(nat + (long long)blockIdx.x * g.nz);
+  const long long rb = rowbase(g, il, j);
+  const double *R = (field ? g.fR : g.phiR) + rb;
+  const double *B = (field ? g.fB : g.phiB) + rb;
+  for (int k = threadIdx.x; k < g.nzh; k += blockDim.x) {
+    const double r = R[k], b = B[k];
+    dst[k] = p0 ? make_double2(b, r) : make_double2(r, b);
+  }
+}
+
+static unsigned row_threads(int n) {
+  return n < kThreads ? (unsigned)((n + 31) / 32 * 32) : (unsigned)kThreads;
+}
+
+// natural buffers from the caller (torch / cudaMalloc) are 16-byte aligned;
+// the row kernels need even nz and an aligned base, else the per-cell ones
+static bool rows_ok(const Grid &g, const void *nat) {
+  return (g.nz % 2) == 0 && ((reinterpret_cast<uintptr_t>(nat) & 15) == 0) &&
+         (long long)g.nxl * g.ny < (1LL << 31);
+}
+
 void launch_pack(const Grid &g, int field, const double *nat, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * g.nz;
   if (total <= 0) return;
-  k_pack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field, nat);
+  if (rows_ok(g, nat))
+    k_pack_rows<<<(unsigned)(g.nxl * g.ny), row_threads(g.nzh), 0, s>>>(g, field, nat);
+  else
+    k_pack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field,
+                                                                               nat);
 }
 
 void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * g.nz;
   if (total <= 0) return;
-  k_unpack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field, nat);
+  if (rows_ok(g, nat))
+    k_unpack_rows<<<(unsigned)(g.nxl * g.ny), row_threads(g.nzh), 0, s>>>(g, field, nat);
+  else
+    k_unpack<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g, field,
+                                                                                 nat);
 }
 
 // ---------------------------------------------------------------------------
