@@ -695,7 +695,7 @@ __global__ void __launch_bounds__(1024)
 // to k_coarse_cg_var (neighbour order, products, the fixed reduction tree).
 static constexpr int kCgVarSmem = 2304;  // 11 doubles + 1 byte per unknown
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512)
     k_coarse_cg_var_smem(Grid g, double tol, int maxit, int *iters_out) {
   extern __shared__ double sm[];
   __shared__ double part[2][32];
@@ -797,7 +797,8 @@ void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
       configured = smem;
     }
     int threads = (int)((N + 31) / 32 * 32);
-    if (threads > 256) threads = 256;
+    const int cap = N >= 2048 ? 512 : 256;  // as k_coarse_cg (more warps)
+    if (threads > cap) threads = cap;
     k_coarse_cg_var_smem<<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
     return;
   }
