@@ -7,6 +7,10 @@ times (one B200; CUDA graph; the default kernels).
   cores); Phi rel-L2 <= 1e-10 and the residual-history clause.
 * 1024^3 (the largest cube kept on one B200 here): cycle reduction and
   sampled half-sweep cells, as for config 5.
+* the 512^3 variants of SURVEY 8(f) N3 (periodic channel) and N4 (variable
+  permittivity, 78.5:1 jumps): a black half-sweep after one V-cycle, sampled
+  cells (periodic faces included) bitwise against the oracle on a 3^3 box
+  taken with wrap-around on periodic axes.
 * config 5 (2048 x 512 x 512, beam mask + 50,000 spheres, V(3,3)): too large
   for a whole-grid oracle run inside the test budget, so sampled outputs are
   checked one by one: for each sampled cell (or coarse cell) the oracle runs
@@ -199,3 +203,78 @@ def test_max_size_1024_cubed_sampled(mg):
         checked += 1
     assert checked >= 20
     s.close()
+
+
+# --------------------------------------------------------------------------
+# the 512^3 variants (N3 periodic channel, N4 variable permittivity): sampled
+# half-sweep cells against the oracle on a 3^3 box around each (periodic
+# axes: the box is taken with wrap-around, so cells on a periodic face see
+# their opposite-side neighbours)
+# --------------------------------------------------------------------------
+def wrapped_box(shape, cell, bc_type):
+    idx, lo_edge, hi_edge = [], [], []
+    for a, (x, n) in enumerate(zip(cell, shape)):
+        if bc_type[2 * a] == 2:  # periodic axis: always x-1 .. x+1, wrapped
+            idx.append(np.arange(x - 1, x + 2) % n)
+            lo_edge.append(False)
+            hi_edge.append(False)
+        else:
+            lo, hi = max(0, x - 1), min(n, x + 2)
+            idx.append(np.arange(lo, hi))
+            lo_edge.append(lo == 0)
+            hi_edge.append(hi == n)
+    return idx, lo_edge, hi_edge
+
+
+def box_bc(bc_type, lo_edge, hi_edge):
+    bt = []
+    for a in range(3):
+        bt.append(bc_type[2 * a] if lo_edge[a] else 0)
+        bt.append(bc_type[2 * a + 1] if hi_edge[a] else 0)
+    return bt
+
+
+@pytest.mark.parametrize("variant", ["periodic", "permittivity"])
+def test_variants_512_sampled_half_sweep(mg, variant):
+    n = 512
+    shape = (n, n, n)
+    D, N, P = 0, 1, 2
+    if variant == "periodic":
+        bt, bv = [P, P, D, D, P, P], [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+        eps = None
+    else:
+        bt, bv = [N, N, D, D, N, N], [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+        rng = np.random.default_rng(1)
+        eps = np.where(rng.uniform(size=shape) < 0.3, 78.5, 1.0)
+    import torch
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=8, stream=torch.cuda.Stream())
+    if eps is not None:
+        s.set_permittivity(eps)
+    s.set_rhs(np.random.default_rng(0).uniform(-1, 1, shape))
+    s.vcycle()
+    phi0 = s.get_solution()
+    f0 = s.get_field(0, mg.MG_FIELD_RHS)
+    s.smooth_half(0, 1)  # black, the TMA-marching / variable-coefficient kernel
+    phi1 = s.get_solution()
+    s.close()
+    rng = np.random.default_rng(11)
+    pts = [tuple(int(x) for x in rng.integers(0, n, 3)) for _ in range(80)]
+    pts += [(0, 7, 0), (n - 1, 0, 5), (3, n - 1, n - 1), (n - 1, n - 1, 0),
+            (0, 0, 1), (256, 1, n - 1)]
+    checked = 0
+    for (i, j, k) in pts:
+        if not (i + j + k) & 1:
+            continue
+        idx, lo_e, hi_e = wrapped_box(shape, (i, j, k), bt)
+        ix = np.ix_(*idx)
+        o = oracle.Oracle(tuple(len(a) for a in idx), 1.0, box_bc(bt, lo_e, hi_e),
+                          [0.0] * 6, min_coarse=1, max_levels=1)
+        if eps is not None:
+            o.set_permittivity(np.ascontiguousarray(eps[ix]))
+        o.set_phi(np.ascontiguousarray(phi0[ix]))
+        o.set_rhs_raw(np.ascontiguousarray(f0[ix]))
+        c = [int(np.where(a == x)[0][0]) for a, x in zip(idx, (i, j, k))]
+        o.smooth_half(0, 1 ^ ((int(idx[0][0]) + int(idx[1][0]) + int(idx[2][0])) & 1))
+        assert o.phi()[c[0], c[1], c[2]] == phi1[i, j, k], (variant, i, j, k)
+        checked += 1
+    assert checked >= 30
