@@ -8,8 +8,9 @@ times (one B200; CUDA graph; the default kernels).
 * 1024^3 (the largest cube kept on one B200 here): cycle reduction and
   sampled half-sweep cells, as for config 5.
 * the 512^3 variants of SURVEY 8(f) N3 (periodic channel) and N4 (variable
-  permittivity, 78.5:1 jumps): a black half-sweep after one V-cycle, sampled
-  cells (periodic faces included) bitwise against the oracle on a 3^3 box
+  permittivity, 78.5:1 jumps): a black half-sweep after one V-cycle and the
+  residual + restriction that follows, sampled cells and coarse cells
+  (periodic faces included) bitwise against the oracle on 3^3 / 8^3 boxes
   taken with wrap-around on periodic axes.
 * config 5 (2048 x 512 x 512, beam mask + 50,000 spheres, V(3,3)): too large
   for a whole-grid oracle run inside the test budget, so sampled outputs are
@@ -278,3 +279,41 @@ def test_variants_512_sampled_half_sweep(mg, variant):
         assert o.phi()[c[0], c[1], c[2]] == phi1[i, j, k], (variant, i, j, k)
         checked += 1
     assert checked >= 30
+    # residual + restriction of the full grid (TMA residual kernel; periodic z
+    # wrap values prefetched a plane ahead): coarse cells on an 8^3 box of
+    # fine cells starting at 2X - 2 (wrapped on periodic axes)
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=8, stream=torch.cuda.Stream())
+    if eps is not None:
+        s.set_permittivity(eps)
+    s.set_field(0, mg.MG_FIELD_RHS, f0)
+    s.set_solution(phi1)
+    s.residual_restrict(0)
+    f1 = s.get_field(1, mg.MG_FIELD_RHS)
+    s.close()
+    for (i, j, k) in pts[:40] + pts[-6:]:
+        X = (i // 2, j // 2, k // 2)
+        idx, lo_e, hi_e = [], [], []
+        for a, (Xa, na) in enumerate(zip(X, shape)):
+            if bt[2 * a] == P:
+                idx.append(np.arange(2 * Xa - 2, 2 * Xa + 6) % na)
+                lo_e.append(False)
+                hi_e.append(False)
+            else:
+                st = min(max(0, 2 * Xa - 2), na - 8)
+                st -= st & 1
+                idx.append(np.arange(st, st + 8))
+                lo_e.append(st == 0)
+                hi_e.append(st + 8 == na)
+        ix = np.ix_(*idx)
+        o = oracle.Oracle((8, 8, 8), 1.0, box_bc(bt, lo_e, hi_e), [0.0] * 6,
+                          min_coarse=1, max_levels=2)
+        assert o.nlevels == 2
+        if eps is not None:
+            o.set_permittivity(np.ascontiguousarray(eps[ix]))
+        o.set_phi(np.ascontiguousarray(phi1[ix]))
+        o.set_rhs_raw(np.ascontiguousarray(f0[ix]))
+        o.restrict_residual(0)
+        loc = [int(np.where(a == 2 * x)[0][0]) // 2 for a, x in zip(idx, X)]
+        got = f1[X]
+        exp = o.rhs(1)[loc[0], loc[1], loc[2]]
+        assert got == exp, (variant, X, got, exp)
