@@ -195,7 +195,10 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         apply_e(1, E0);
       }
       apply_e(q + 1, E);
-      if (q + 2 < nplanes) load_e(q + 2, E);
+      // fine planes 2I and 2I+1 share the parent plane I: keep E (the same
+      // tasks, the same coarse values) instead of loading it again
+      const int ia = g.x0 + i0 + q, ib = ia + 1;  // global planes q+1, q+2
+      if (q + 2 < nplanes && (ia >> 1) != (ib >> 1)) load_e(q + 2, E);
       __syncthreads();
     }
 
