@@ -128,6 +128,15 @@ __device__ __forceinline__ double div_centre(double a, double d) {
   return d == 6.0 ? div_small(a, 6.0, kRcp6) : a / d;
 }
 
+// RN(1/d), d = 0..15 (entry 0 unused), in constant memory (one copy per
+// translation unit); the initialisers are IEEE divisions, so div_small with
+// these reciprocals is exactly RN(a/d).  A warp-uniform index (the interior
+// centre 6) is a broadcast.
+static __constant__ double c_rcp16[16] = {0.0,      1.0 / 1,  1.0 / 2,  1.0 / 3,
+                                          1.0 / 4,  1.0 / 5,  1.0 / 6,  1.0 / 7,
+                                          1.0 / 8,  1.0 / 9,  1.0 / 10, 1.0 / 11,
+                                          1.0 / 12, 1.0 / 13, 1.0 / 14, 1.0 / 15};
+
 // RN(1/d) for d = 0..15 into a shared table (IEEE division; entry 0 unused)
 __device__ __forceinline__ void fill_rcp16(double *rcp) {
   if (threadIdx.x < 16) rcp[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;

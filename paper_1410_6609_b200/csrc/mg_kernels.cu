@@ -53,9 +53,6 @@ __device__ __forceinline__ double2 ld2(const double *p) {
 template <bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_smooth(Grid g, int color, int from_zero) {
-  __shared__ double rcp[16];  // RN(1/d) for the exact division
-  fill_rcp16(rcp);
-  __syncthreads();
   const int nk2 = (g.nzh + 1) >> 1;  // odd nzh: the last pair is half used
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   const long long total = (long long)g.nxl * g.ny * nk2;
@@ -101,8 +98,8 @@ __global__ void __launch_bounds__(kThreads)
   const double d0 = (double)centre_d(g, i, j, z0);
   const double d1 = (double)centre_d(g, i, j, z0 + 2);
   double2 out;
-  out.x = div_small(fo.x * g.w + s0, d0, rcp[(int)d0]);
-  out.y = div_small(fo.y * g.w + s1, d1, rcp[(int)d1]);
+  out.x = div_small(fo.x * g.w + s0, d0, c_rcp16[(int)d0]);
+  out.y = div_small(fo.y * g.w + s1, d1, c_rcp16[(int)d1]);
   if (k + 1 < g.nzh) {
     *reinterpret_cast<double2 *>(own + b + k) = out;
     if (PER) ghost_copies(g, own, il, j, k, out);
