@@ -89,25 +89,32 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   // cells without reading them (and a write-back would race with the TMA
   // halo reads of neighbouring CTAs).  The coarse values are loaded one plane
   // ahead (load_e) so their latency hides behind the previous plane's work.
-  // Work split: task t = (row rr, 64-wide chunk c), t = warp + TY*m.
-  constexpr int ntask = (kTY + 2) * NCH;
+  // Work split: task t = (coarse row jr, 64-wide chunk c), t = warp + TY*m:
+  // the tile rows j0-1 .. j0+TY have the parent rows J = j0/2 - 1 + jr,
+  // jr = 0 .. TY/2 + 1; the two sibling rows 2J, 2J+1 (tile rows 2jr-1,
+  // 2jr, where inside the tile) share the coarse values, loaded once.
+  constexpr int kJR = kTY / 2 + 2;
+  constexpr int ntask = kJR * NCH;
   constexpr int kTPW = (ntask + kTY - 1) / kTY;  // tasks per warp
-  // per-task constants (task t = warp + TY*m: row rr = t / NCH, chunk t % NCH)
-  int tRow[kTPW], tK[kTPW], tCoff[kTPW], tJp[kTPW];
-  bool tOk[kTPW];
+  int tK[kTPW], tCoff[kTPW], tJp[kTPW], tRowA[kTPW];
+  bool tOkA[kTPW], tOkB[kTPW];
+  auto row_valid = [&](int jj) {
+    // rows of the level, plus (y periodic) the ghost rows -1 / ny that hold
+    // the opposite side's cells and need their parents' correction too
+    return (PER && g.per[1]) ? (jj >= -1 && jj <= g.ny) : (jj >= 0 && jj < g.ny);
+  };
 #pragma unroll
   for (int m = 0; m < kTPW; m++) {
     const int t = warp + kTY * m;
-    const int rr = t / NCH, c = t % NCH;
-    const int jj = j0 - 1 + rr;
+    const int jr = t / NCH, c = t % NCH;
+    const int J = (j0 >> 1) - 1 + jr;
     const int k = 2 * lane + 64 * c;
-    // rows of the level, plus (y periodic) the ghost rows -1 / ny that hold
-    // the opposite side's cells and need their parents' correction too
-    tOk[m] = PROLONG && t < ntask && k < g.nzh &&
-             ((PER && g.per[1]) ? (jj >= -1 && jj <= g.ny) : (jj >= 0 && jj < g.ny));
-    tRow[m] = rr * pz;
+    const bool ok = PROLONG && t < ntask && k < g.nzh;
+    const int rrA = 2 * jr - 1, rrB = 2 * jr;  // tile rows of 2J, 2J+1
+    tOkA[m] = ok && rrA >= 0 && row_valid(2 * J);
+    tOkB[m] = ok && rrB <= kTY + 1 && row_valid(2 * J + 1);
+    tRowA[m] = rrA * pz;
     tK[m] = k;
-    const int J = jj >> 1;
     tCoff[m] = (J + 1) * C.pz + (k >> 1);
     tJp[m] = J & 1;
   }
@@ -122,7 +129,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
 #pragma unroll
     for (int m = 0; m < kTPW; m++) {
       E[m] = make_double2(0.0, 0.0);
-      if (!(pok && tOk[m])) continue;
+      if (!(pok && (tOkA[m] || tOkB[m]))) continue;
       // parents of half-indices k, k+1 are coarse z = k, k+1: one red and
       // one black coarse cell at coarse half-index k/2 (k even)
       const int c0 = (Ip + tJp[m]) & 1;
@@ -138,18 +145,19 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     const int i = g.x0 + i0 - 1 + q;
     if (!(PER && g.per[0]) && (i < 0 || i >= g.nx)) return;  // physical ghost: 0
     double *slot = ring + (size_t)(q % kSlots) * sd;
-#pragma unroll
-    for (int m = 0; m < kTPW; m++) {
-      if (!tOk[m]) continue;
-      double *row = slot + tRow[m];
-      const int k = tK[m];
+    auto add = [&](double *row, int k, const double2 e) {
       double2 v = lds2(row + k);
-      v.x = v.x + alpha * E[m].x;
-      v.y = v.y + alpha * E[m].y;
+      v.x = v.x + alpha * e.x;
+      v.y = v.y + alpha * e.y;
       if (k + 1 < g.nzh)
         *reinterpret_cast<double2 *>(row + k) = v;
       else
         row[k] = v.x;
+    };
+#pragma unroll
+    for (int m = 0; m < kTPW; m++) {
+      if (tOkA[m]) add(slot + tRowA[m], tK[m], E[m]);
+      if (tOkB[m]) add(slot + tRowA[m] + pz, tK[m], E[m]);
     }
   };
   double2 E[kTPW];
