@@ -39,8 +39,10 @@ namespace mg {
 // time variants, so the box-domain kernel carries neither code path
 enum { VAR_BOX = 0, VAR_MASK = 1, VAR_PER = 2 };
 
+// rows of <= 128 half-entries (NCH <= 2: level 1 and below at 512^3) fit 3
+// CTAs per SM (<= 85 registers, no spills; 4 spilled and were no faster)
 template <bool PROLONG, int NCH, int VAR>
-__global__ void __launch_bounds__(kThreadsM, 2)
+__global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
                    int color, Grid C, double alpha) {
   constexpr bool MASK = VAR == VAR_MASK;
