@@ -487,6 +487,9 @@ def run_cuda(args):
                      "avg_launch_ms": round(per_launch_ms, 5),
                      "share_of_cycle": round(sm0 / cyc_prof, 4),
                      "peak_source": peak_src,
+                     "peak_note": "measured copy bandwidth (1:1 read/write); the "
+                                  "half-sweep reads 2 B per B written and the "
+                                  "cycle model can exceed it slightly",
                      "cycle_model_frac": round(cycle_frac, 4),
                      "breakdown_ms": {k: round(float(np.mean([p[k] for p in prof])), 4)
                                       for k in prof[0]},
