@@ -114,15 +114,22 @@ __device__ __forceinline__ void gradient(const Grid &g, const unsigned char *sol
 __device__ __forceinline__ void gradient_interior(const Grid &g, double h, int i,
                                                   int j, int k, double *gr) {
   const long long base = (long long)(i - g.x0 + 1) * g.plane + (long long)(j + 1) * g.pz;
-  const int kh[3] = {(k - 1) >> 1, k >> 1, (k + 1) >> 1};
   const int c0 = (i + j + k) & 1;
+  // same-colour neighbours (offset parity even) in the own array, the others
+  // in the other one: two row pointers, no per-load colour select
+  const double *own = (c0 ? g.phiB : g.phiR) + base;
+  const double *oth = (c0 ? g.phiR : g.phiB) + base;
+  const long long P = g.plane, Z = g.pz;
+  const int kh0 = k >> 1;
+  // half-index of z + dk relative to the row: (k + dk) >> 1
+  const int khm = (k - 1) >> 1, khp = (k + 1) >> 1;
   double S[3] = {0.0, 0.0, 0.0};
 #pragma unroll
   for (int q = 0; q < 18; q++) {
     const int di = kq(q, 0), dj = kq(q, 1), dk = kq(q, 2);
-    const int col = c0 ^ ((di + dj + dk) & 1);
-    const double *arr = col ? g.phiB : g.phiR;
-    const double v = arr[base + di * g.plane + dj * g.pz + kh[dk + 1]];
+    const double *arr = ((di + dj + dk) & 1) ? oth : own;
+    const int kh = dk < 0 ? khm : (dk > 0 ? khp : kh0);
+    const double v = arr[di * P + dj * Z + kh];
     const double w = q < 6 ? 1.0 / 18.0 : 1.0 / 36.0;
 #pragma unroll
     for (int a = 0; a < 3; a++) {
