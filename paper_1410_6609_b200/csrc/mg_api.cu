@@ -1891,7 +1891,8 @@ int mg_set_face_values(mg_ctx *c, int face, const double *values) {
 static int coulomb_forces(mg_ctx *c, int n, const double *centers,
                           const double *radii, const double *charges,
                           int normalization, int subsample, double *forces_out,
-                          const unsigned long long *counts);
+                          const unsigned long long *counts,
+                          const double *dsph_given = nullptr);
 
 int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
                       const double *radii, const double *charges,
@@ -1905,7 +1906,8 @@ int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
 static int coulomb_forces(mg_ctx *c, int n, const double *centers,
                           const double *radii, const double *charges,
                           int normalization, int subsample, double *forces_out,
-                          const unsigned long long *counts) {
+                          const unsigned long long *counts,
+                          const double *dsph_given) {
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (n < 0 || (n > 0 && (!centers || !radii || !charges || !forces_out)))
     return fail(MG_ERR_ARG, "bad arrays");
@@ -1914,12 +1916,15 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
   if (normalization != MG_CHARGE_PER_CELLS && normalization != MG_CHARGE_PER_VOLUME)
     return fail(MG_ERR_ARG, "bad normalization");
   if (n == 0) return MG_OK;
-  std::vector<double> h5(5 * (size_t)n);
-  for (int p = 0; p < n; p++) {
-    if (int rc = check_sphere(c, p, centers + 3 * (size_t)p, radii[p])) return rc;
-    for (int q = 0; q < 3; q++) h5[5 * (size_t)p + q] = centers[3 * (size_t)p + q];
-    h5[5 * (size_t)p + 3] = radii[p];
-    h5[5 * (size_t)p + 4] = charges[p];
+  std::vector<double> h5;
+  if (!dsph_given) {  // (a given device list was checked when it was uploaded)
+    h5.resize(5 * (size_t)n);
+    for (int p = 0; p < n; p++) {
+      if (int rc = check_sphere(c, p, centers + 3 * (size_t)p, radii[p])) return rc;
+      for (int q = 0; q < 3; q++) h5[5 * (size_t)p + q] = centers[3 * (size_t)p + q];
+      h5[5 * (size_t)p + 3] = radii[p];
+      h5[5 * (size_t)p + 4] = charges[p];
+    }
   }
   int rc;
   // both colours' ghost planes current (the gradient reads across slabs)
@@ -1939,9 +1944,12 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
   double *buf = c->fbuf;
   double *dsph = buf, *dpart = buf + 5 * (size_t)n, *dall = dpart + nrow * ns;
   std::vector<double> hp;
-  if (cudaMemcpyAsync(dsph, h5.data(), 5 * (size_t)n * sizeof(double),
-                      cudaMemcpyHostToDevice, c->stream) != cudaSuccess)
+  if (dsph_given) {
+    dsph = const_cast<double *>(dsph_given);
+  } else if (cudaMemcpyAsync(dsph, h5.data(), 5 * (size_t)n * sizeof(double),
+                             cudaMemcpyHostToDevice, c->stream) != cudaSuccess) {
     return fail(MG_ERR_CUDA, "copy of the sphere list failed");
+  }
   for (size_t s = 0; s < ns; s++)
     mg::launch_coulomb(c->g[0][s], c->dsolid, c->h, subsample, n, dsph,
                        normalization, dpart + nrow * s, counts, c->stream);
@@ -2005,8 +2013,10 @@ int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
         (force_subsample == subsample && n > 0)
             ? reinterpret_cast<const unsigned long long *>(c->sph + 5 * c->sph_cap)
             : nullptr;
+    // ... and the same sphere list is already on the device (c->sph)
     const int frc = coulomb_forces(c, n, centers, radii, charges, normalization,
-                                   force_subsample, forces_out, cnt);
+                                   force_subsample, forces_out, cnt,
+                                   n > 0 ? c->sph : nullptr);
     if (frc) return frc;
   }
   return rc;
