@@ -240,6 +240,8 @@ struct mg_ctx {
   double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
   double *fbuf = nullptr;      // force step: sphere list + partial sums
+  double *hpin = nullptr;      // pinned host staging for sphere lists and
+  size_t hpin_cap = 0;         // force partials (doubles), grown, kept
   size_t fbuf_cap = 0;         // (doubles), grown on demand, kept
   unsigned long long *counts = nullptr;
   cudaGraphExec_t graph = nullptr;
@@ -864,6 +866,20 @@ int stage_for(mg_ctx *c, size_t bytes) {
   return MG_OK;
 }
 
+// pinned host staging of >= n doubles; returned idle: no copy enqueued on
+// the context's stream reads or writes it any more
+double *host_pinned(mg_ctx *c, size_t n) {
+  if (cudaStreamSynchronize(c->stream) != cudaSuccess) return nullptr;
+  if (n > c->hpin_cap) {
+    if (c->hpin) cudaFreeHost(c->hpin);
+    c->hpin = nullptr;
+    c->hpin_cap = 0;
+    if (cudaMallocHost(&c->hpin, n * sizeof(double)) != cudaSuccess) return nullptr;
+    c->hpin_cap = n;
+  }
+  return c->hpin;
+}
+
 size_t level_cells_held(const mg_ctx *c, int l) {
   size_t n = 0;
   for (const Grid &g : c->g[l]) n += (size_t)g.nxl * g.ny * g.nz;
@@ -1285,6 +1301,7 @@ void mg_destroy(mg_ctx *c) {
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   if (c->sph) cudaFree(c->sph);
   if (c->fbuf) cudaFree(c->fbuf);
+  if (c->hpin) cudaFreeHost(c->hpin);
   for (void *p : c->mask_bufs) cudaFree(p);
   if (c->h_norm) cudaFreeHost(c->h_norm);
   if (c->own_ws && c->ws) cudaFree(c->ws);
@@ -1319,9 +1336,12 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   if (normalization != MG_CHARGE_PER_CELLS && normalization != MG_CHARGE_PER_VOLUME)
     return fail(MG_ERR_ARG, "bad normalization");
   if (n > 0 && (!centers || !radii || !charges)) return fail(MG_ERR_ARG, "null array");
-  std::vector<double> h5(5 * (size_t)n);
-  for (int p = 0; p < n; p++) {
+  for (int p = 0; p < n; p++)
     if (int rc = check_sphere(c, p, centers + 3 * (size_t)p, radii[p])) return rc;
+  // the sphere list through pinned staging (an asynchronous upload)
+  double *h5 = n > 0 ? host_pinned(c, 5 * (size_t)n) : nullptr;
+  if (n > 0 && !h5) return fail(MG_ERR_CUDA, "pinned staging allocation failed");
+  for (int p = 0; p < n; p++) {
     for (int a = 0; a < 3; a++) h5[5 * (size_t)p + a] = centers[3 * (size_t)p + a];
     h5[5 * (size_t)p + 3] = radii[p];
     h5[5 * (size_t)p + 4] = charges[p];
@@ -1339,7 +1359,7 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
   }
   if (n > 0) {
-    CK(cudaMemcpyAsync(c->sph, h5.data(), sizeof(double) * 5 * (size_t)n,
+    CK(cudaMemcpyAsync(c->sph, h5, sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
     for (const Grid &g : c->g[0])
       mg::launch_spheres(g, c->h, subsample, n, c->sph, normalization, cnt,
@@ -1943,7 +1963,6 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
   }
   double *buf = c->fbuf;
   double *dsph = buf, *dpart = buf + 5 * (size_t)n, *dall = dpart + nrow * ns;
-  std::vector<double> hp;
   if (dsph_given) {
     dsph = const_cast<double *>(dsph_given);
   } else if (cudaMemcpyAsync(dsph, h5.data(), 5 * (size_t)n * sizeof(double),
@@ -1961,10 +1980,11 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
     nparts = (size_t)c->P;
     src = dall;
   }
+  double *hq = nullptr;
   if (!rc) {
-    hp.resize(nrow * nparts);
-    if (cudaMemcpyAsync(hp.data(), src, hp.size() * sizeof(double),
-                        cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
+    hq = host_pinned(c, nrow * nparts);
+    if (!hq || cudaMemcpyAsync(hq, src, nrow * nparts * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream) != cudaSuccess ||
         cudaStreamSynchronize(c->stream) != cudaSuccess)
       rc = fail(MG_ERR_CUDA, "force readback failed");
   }
@@ -1972,7 +1992,7 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
   const double h3 = c->h * c->h * c->h;
   for (size_t r = 0; r < nrow; r++) {
     double s = 0.0;
-    for (size_t k = 0; k < nparts; k++) s = s + hp[k * nrow + r];  // slab order
+    for (size_t k = 0; k < nparts; k++) s = s + hq[k * nrow + r];  // slab order
     forces_out[r] = -h3 * s;
   }
   return MG_OK;
