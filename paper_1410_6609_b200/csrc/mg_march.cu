@@ -444,6 +444,13 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       const size_t om = (size_t)((q - 1) % kSlots) * sd + (warp + 1) * W + zoff;
       const size_t op = (size_t)((q + 1) % kSlots) * sd + (warp + 1) * W + zoff;
       const double wlo[2] = {wr[0], wr[1]}, whi[2] = {wr[2], wr[3]};  // [own colour]
+      // the centre's x / y face terms are the row's (hoisted); z adds only at
+      // the row ends -- the same integer as centre_dm
+      const int dxy = 6 + (i == 0 ? g.dface[0] : 0) + (i == g.nx - 1 ? g.dface[1] : 0) +
+                      (j == 0 ? g.dface[2] : 0) + (j == g.ny - 1 ? g.dface[3] : 0);
+      auto dcen = [&](int z) {
+        return (double)(dxy + (z == 0 ? g.dface[4] : 0) + (z == g.nz - 1 ? g.dface[5] : 0));
+      };
 #pragma unroll
       for (int c = 0; c < 2; c++) {
         const int kl = 2 * lane + 64 * c;  // tile-relative half-index
@@ -499,8 +506,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           } else {
             s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
             s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
-            d0 = (double)centre_dm(g, i, j, z0);
-            d1 = (double)centre_dm(g, i, j, z0 + 2);
+            d0 = dcen(z0);
+            d1 = dcen(z0 + 2);
           }
           const double t0 = d0 * u.x - s0;
           const double t1 = d1 * u.y - s1;
