@@ -321,7 +321,10 @@ int mg_wait(mg_ctx *ctx, double *res_norm_out);
  * NULL.  MG_OK, MG_ERR_NOTCONV at max_cycles, or MG_ERR_DIVERGED. */
 int mg_solve(mg_ctx *ctx, double tol, int *cycles_out, double *res_hist);
 
-/* ||f - A Phi||_2 for the current Phi (finest level). */
+/* ||f - A Phi||_2 for the current Phi on the finest level, unscaled (Alg.1
+ * "residual"; reading c10), summed in a fixed order (per-CTA partials,
+ * then in CTA and, for NCCL contexts, rank order).  Synchronises the stream.
+ * Errors: null ctx / out (MG_ERR_ARG), MG_ERR_CUDA, MG_ERR_NCCL. */
 int mg_residual_norm(mg_ctx *ctx, double *out);
 
 /* ---- solution I/O -------------------------------------------------------- */

@@ -34,6 +34,29 @@ def test_library_exports_every_declared_symbol():
         assert hasattr(L, n), n
 
 
+def test_every_declaration_is_documented():
+    """Each entry point of include/mg.h is preceded by a comment block (its
+    semantics, arguments, errors; the paper passage where there is one), and
+    the header cites the paper (P:line) for the operations it defines."""
+    src = open(os.path.join(ROOT, "include", "mg.h")).read()
+    decls = list(re.finditer(r"^(?:int|void|size_t|const char \*|void \*)\s*\**\s*"
+                             r"(mg_[a-z_0-9]+)\s*\(", src, flags=re.M))
+    assert len(decls) >= 20
+    for m in decls:
+        # a comment block ends right above the declaration or above the
+        # contiguous group of declarations it belongs to (no blank line)
+        end = src.rfind("*/", 0, m.start())
+        gap = src[end + 2:m.start()]
+        assert end >= 0 and "\n\n" not in gap, "undocumented: " + m.group(1)
+    cites = re.findall(r"P:\d+", src)
+    assert len(cites) >= 20
+    for op in ("mg_set_rhs_from_spheres", "mg_vcycle", "mg_solve", "mg_coulomb_forces",
+               "mg_timestep", "mg_set_permittivity", "mg_residual_norm"):
+        i = src.index(op + "(")
+        block = src[src.rindex("/*", 0, i):i]
+        assert "P:" in block or "Alg." in block or "reading" in block, op
+
+
 def test_no_oracle_in_product():
     """The product never references the oracle (no shared code)."""
     pkg = os.path.join(ROOT, "paper_1410_6609_b200")
