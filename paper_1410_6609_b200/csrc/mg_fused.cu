@@ -224,10 +224,11 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         const double s0 = ((((a.x + bb.x) + ym.x) + yp.x) + zm0) + zp0;
         const double s1 = ((((a.y + bb.y) + ym.y) + yp.y) + zm1) + zp1;
         const int z0 = 2 * k + p;
-        const double d0 = (double)(tdr[m] + dpl + dz(z0));
-        const double d1 = (double)(tdr[m] + dpl + dz(z0 + 2));
-        out.x = (fBt[m].x * w + s0) / d0;
-        out.y = (k + 1 < g.nzh) ? (fBt[m].y * w + s1) / d1 : 0.0;
+        // exact division (bitwise IEEE) with the constant-memory RN(1/d)
+        const int i0d = tdr[m] + dpl + dz(z0), i1d = tdr[m] + dpl + dz(z0 + 2);
+        out.x = div_small(fBt[m].x * w + s0, (double)i0d, c_rcp16[i0d]);
+        out.y = (k + 1 < g.nzh) ? div_small(fBt[m].y * w + s1, (double)i1d, c_rcp16[i1d])
+                                : 0.0;
         if (own_plane && jj >= j0 && jj < j0 + kTY) {
           double *dst = g.phiB + goff(bq, jj);
           if (k + 1 < g.nzh)
@@ -250,8 +251,8 @@ __global__ void __launch_bounds__(kThreadsM, 2)
                            cur[hk + W]) +
                           zm) +
                          zp;
-        const double d = (double)(hdr + dpl + dz(z));
-        v = (fBh * w + s) / d;
+        const int di = hdr + dpl + dz(z);
+        v = div_small(fBh * w + s, (double)di, c_rcp16[di]);
       }
       Bc[hbo + hk] = v;
     }
