@@ -181,6 +181,9 @@ __device__ __forceinline__ void bsum3(double *v, double (*sh)[32]) {
 // 4 CTAs per SM (64 registers, a few spilled): the per-sphere CTAs are
 // latency-bound, so residency beats registers (0.92 vs 1.23 ms for the
 // 7,417 spheres of the time-stepping regime)
+// PER: periodic images (up to 27); otherwise the sphere itself only, without
+// the 27-entry image array (registers / stack of the common case)
+template <bool PER>
 __global__ void __launch_bounds__(kTF, 4)
     k_coulomb(Grid g, const unsigned char *solid, double h, int s,
               const double *sph, int normalization, double *part,
@@ -191,8 +194,16 @@ __global__ void __launch_bounds__(kTF, 4)
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
   const double R2 = R * R;
   const double hs = h / (double)s;
-  double img[27][3];
-  const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
+  double img[PER ? 27 : 1][3];
+  int nimg = 1;
+  if (PER) {
+    nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2],
+                       reinterpret_cast<double(*)[3]>(img));
+  } else {
+    img[0][0] = sph[5 * p];
+    img[0][1] = sph[5 * p + 1];
+    img[0][2] = sph[5 * p + 2];
+  }
   long long cnt = 0;  // threads own (j, k) columns of the box, walk along x
   for (int m = 0; !counts && m < nimg; m++) {
     const sph::Box bx = sph::box_of(g, h, img[m], R);
@@ -256,8 +267,12 @@ void launch_coulomb(const Grid &g, const unsigned char *solid_global, double h,
                     double *partials, const unsigned long long *counts,
                     cudaStream_t s) {
   if (n <= 0) return;
-  k_coulomb<<<n, kTF, 0, s>>>(g, solid_global, h, subsample, sph, normalization,
-                              partials, counts);
+  if (is_periodic(g))
+    k_coulomb<true><<<n, kTF, 0, s>>>(g, solid_global, h, subsample, sph,
+                                      normalization, partials, counts);
+  else
+    k_coulomb<false><<<n, kTF, 0, s>>>(g, solid_global, h, subsample, sph,
+                                       normalization, partials, counts);
 }
 
 }  // namespace mg
