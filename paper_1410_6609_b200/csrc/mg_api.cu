@@ -190,6 +190,7 @@ struct mg_ctx {
   int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
   int use_t4 = 0;     // temporally blocked V(2,2) passes (opt-in: MG_T4=1)
   int use_s2 = 0;     // one full sweep (red + black) per kernel (MG_S2=1)
+  int split_off = 0;  // split norm: partials written by the last black sweep
   // multi-slab overlap (MG_NO_OVERLAP=1: off): boundary planes first, the
   // ghost exchange on s_comm while the interior planes are swept
   int overlap = 1;
@@ -314,8 +315,9 @@ size_t carve(mg_ctx *c, char *base) {
   }
   size_t npart = kNormBlocks;
   for (const Grid &g : c->g[0]) {
+    // residual-kernel partials, plus (split norm) the smoother's, fewer
     const size_t nb = (size_t)mg::norm_march_blocks(g);
-    npart += nb > (size_t)kNormBlocks ? nb : (size_t)kNormBlocks;
+    npart += 2 * (nb > (size_t)kNormBlocks ? nb : (size_t)kNormBlocks);
   }
   c->partials = (double *)cv.take(sizeof(double) * npart);
   c->normv = (double *)cv.take(sizeof(double) * (2 + c->P));
@@ -705,6 +707,22 @@ bool use_s2(const mg_ctx *c, int l) {
   return c->tm[l][0].ok_s2 && mg::sweep2_supported(c->g[l][0]);
 }
 
+// split cycle-end norm: the last black half-sweep of level 0 sums the black
+// residuals (k_smooth_march<..., NORM>), a red-only residual pass the rest:
+// 12 + 12 instead of 12 + 16 B/cell for that pair (MG_SPLIT_NORM=0: off)
+bool split_norm_ok(const mg_ctx *c) {
+  static const bool on = [] {
+    const char *e = getenv("MG_SPLIT_NORM");
+    return !(e && atoi(e) == 0);
+  }();
+  if (!on || fused_norm_on(c) || c->pl.L < 2 || c->o.nu2 < 1) return false;
+  if (c->g[0].size() != 1 || !c->use_march || can_fuse_resid(c, 0)) return false;
+  if (use_t4(c, 0) || use_s2(c, 0)) return false;
+  const Grid &g = c->g[0][0];
+  const TmPair &t = c->tm[0][0];
+  return t.ok && t.ok_resid && (!c->masked || g.codeR);
+}
+
 int s2_pre(mg_ctx *c, int l) {
   const Grid &g = c->g[l][0];
   const TmPair &t = c->tm[l][0];
@@ -820,11 +838,34 @@ int enqueue_vcycle(mg_ctx *c) {
       if ((rc = prolong_level(c, l))) return rc;
     }
     const bool fuse_n = l == 0 && c->o.nu2 >= 1 && can_fuse_resid(c, 0);
+    const bool split_n = l == 0 && split_norm_ok(c);
     for (int s = 0; s < c->o.nu2; s++) {
       if (!(fuse && s == 0))
         if ((rc = smooth_half(c, l, 0, 0))) return rc;
       if (fuse_n && s == c->o.nu2 - 1) break;
+      if (split_n && s == c->o.nu2 - 1) {  // last black: + black residuals
+        mark(c, CAT_NONE);
+        c->split_off = mg::launch_smooth_norm_march(c->g[0][0], c->tm[0][0].r, 1,
+                                                    c->partials, c->stream);
+        c->launches++;
+        mark(c, CAT_SMOOTH0);
+        CK(cudaGetLastError());
+        break;
+      }
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
+    }
+    if (split_n) {  // + red residuals, then the ordered sum as enqueue_norm
+      mark(c, CAT_NONE);
+      const int off = c->split_off +
+                      mg::launch_norm_red_march(c->g[0][0], c->tm[0][0].rr,
+                                                c->tm[0][0].rb,
+                                                c->partials + c->split_off, c->stream);
+      c->launches++;
+      CK(cudaGetLastError());
+      if ((rc = finish_norm(c, off))) return rc;
+      c->cycle_launches = c->launches;
+      c->prof_last = c->prof;
+      return MG_OK;
     }
     if (fuse_n) {  // last black half-sweep + residual norm in one pass
       mark(c, CAT_NONE);

@@ -192,6 +192,13 @@ bool make_tmap_resid(const Grid &g, const double *base, void *out128);
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
                                  const void *tmB, cudaStream_t s);
 int norm_march_blocks(const Grid &g);
+// split norm of a cycle's end: the last black half-sweep with the black
+// residuals' partials, then the red residuals' partials (12 B/cell); both
+// return their partial counts
+int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
+                             double *partials, cudaStream_t s);
+int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
+                          double *partials, cudaStream_t s);
 // residual + restriction that also writes the norm partials of that residual
 // (one per CTA, fixed order); returns the partial count
 int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,

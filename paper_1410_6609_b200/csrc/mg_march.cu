@@ -41,10 +41,15 @@ enum { VAR_BOX = 0, VAR_MASK = 1, VAR_PER = 2 };
 
 // rows of <= 128 half-entries (NCH <= 2: level 1 and below at 512^3) fit 3
 // CTAs per SM (<= 85 registers, no spills; 4 spilled and were no faster)
-template <bool PROLONG, int NCH, int VAR>
+// NORM: also the residual of every updated cell after the sweep (its
+// neighbours are the other colour, final), f - c (d u - s) with the residual
+// kernels' expression, r^2 summed into one partial per CTA (fixed order) --
+// the last black half-sweep of a cycle then leaves only the red residuals to
+// the norm pass (12 instead of 16 B/cell)
+template <bool PROLONG, int NCH, int VAR, bool NORM = false>
 __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
-                   int color, Grid C, double alpha) {
+                   int color, Grid C, double alpha, double *partials) {
   constexpr bool MASK = VAR == VAR_MASK;
   constexpr bool PER = VAR == VAR_PER;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -180,6 +185,7 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
     }
   }
 
+  double nacc = 0.0;  // NORM: sum of r^2 of this thread's updated cells
   for (int il = i0; il < i1; il++) {
     const int q = il - i0 + 1;  // ring index of the current plane
     __syncthreads();            // everybody is done with plane q-2's slot
@@ -285,6 +291,13 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
         // cells)
         out.x = div_small(fr[c].x * g.w + s0, d0, c_rcp16[(int)d0]);
         out.y = div_small(fr[c].y * g.w + s1, d1, c_rcp16[(int)d1]);
+        if (NORM) {
+          const double r0 = (cd0 & 64) ? fr[c].x - g.c * (d0 * out.x - s0) : 0.0;
+          const double r1 =
+              (k + 1 < g.nzh && (cd1 & 64)) ? fr[c].y - g.c * (d1 * out.y - s1) : 0.0;
+          nacc = nacc + r0 * r0;
+          nacc = nacc + r1 * r1;
+        }
         const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
         if (both) {
           *reinterpret_cast<double2 *>(orow + k) = out;
@@ -302,6 +315,19 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       cr[c] = cn[c];
     }
   }
+  if (NORM) {  // deterministic block reduction (warp tree, warps in order)
+    __shared__ double nred[kTY];
+    double v = nacc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+    if (lane == 0) nred[warp] = v;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double sum = 0.0;
+      for (int w = 0; w < kTY; w++) sum = sum + nred[w];
+      partials[blockIdx.x] = sum;
+    }
+  }
 }
 
 // ============================================================================
@@ -310,7 +336,9 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
 // ============================================================================
 // MODE_BOTH: restriction plus the norm partials of the same residual (the
 // fused termination norm, reading c11)
-enum { MODE_RESTRICT = 0, MODE_NORM = 1, MODE_BOTH = 2 };
+// MODE_NORM_RED: the norm partials of the red residuals only (the black ones
+// were summed by the last black half-sweep, k_smooth_march<..., NORM>)
+enum { MODE_RESTRICT = 0, MODE_NORM = 1, MODE_BOTH = 2, MODE_NORM_RED = 3 };
 
 template <int MODE, int VAR>
 __global__ void __launch_bounds__(kThreadsM, 2)
@@ -377,7 +405,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
     if (row_ok && k < g.nzh) {
       const long long o = (long long)(i0 + 1) * g.plane + (long long)(j + 1) * g.pz + k;
       fR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
-      fB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+      if (MODE != MODE_NORM_RED) fB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
       if (MASK) {
         cR[c] = *reinterpret_cast<const unsigned short *>(g.codeR + o);
         cB[c] = *reinterpret_cast<const unsigned short *>(g.codeB + o);
@@ -428,7 +456,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       if (more && row_ok && k < g.nzh) {
         const long long o = (long long)(il + 2) * g.plane + (long long)(j + 1) * g.pz + k;
         nR[c] = *reinterpret_cast<const double2 *>(g.fR + o);
-        nB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
+        if (MODE != MODE_NORM_RED) nB[c] = *reinterpret_cast<const double2 *>(g.fB + o);
         if (MASK) {
           ncR[c] = *reinterpret_cast<const unsigned short *>(g.codeR + o);
           ncB[c] = *reinterpret_cast<const unsigned short *>(g.codeB + o);
@@ -460,9 +488,9 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         // the plain-box arithmetic gives the same bits (see the smoother)
         const bool open =
             MASK && __all_sync(__activemask(), cR[c] == kOpenPair && cB[c] == kOpenPair);
-        double r[2][2];  // [colour][element]
+        double r[2][2] = {{0.0, 0.0}, {0.0, 0.0}};  // [colour][element]
 #pragma unroll
-        for (int col = 0; col < 2; col++) {
+        for (int col = 0; col < (MODE == MODE_NORM_RED ? 1 : 2); col++) {
           const double *O = col ? ringR : ringB;  // other colour's ring
           const double *M = col ? ringB : ringR;  // own colour's ring
           const int p = (i + j + col) & 1;
@@ -521,7 +549,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
           acc = acc + r[1][0] * r[1][0];
           acc = acc + r[1][1] * r[1][1];
         }
-        if (MODE != MODE_NORM) {
+        if ((MODE == MODE_RESTRICT || MODE == MODE_BOTH)) {
           // z-children of coarse K = k are the red and black cells at
           // half-index k (commutative pair: r_dz0 + r_dz1)
           pr[c][0] = r[0][0] + r[1][0];
@@ -529,7 +557,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
         }
       }
     }
-    if (MODE != MODE_NORM) {
+    if ((MODE == MODE_RESTRICT || MODE == MODE_BOTH)) {
       // y-children: rows 2J (even warp) + 2J+1 (odd warp), in that order
       if (warp & 1) {
 #pragma unroll
@@ -683,27 +711,33 @@ static void set_smem(K kernel, size_t bytes, size_t *configured) {
   }
 }
 
-template <bool P, int NCH, int M>
-static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
-                      int color, double alpha, cudaStream_t s) {
+static int smooth_blocks(const Grid &g) {
   const int nrt = (g.ny + kTY - 1) / kTY;
   const int ich = chunk_planes(g.nxl, nrt);
-  const int nxc = (g.nxl + ich - 1) / ich;
-  const size_t smem = smooth_smem_bytes(g);
-  static size_t configured = 0;
-  set_smem(k_smooth_march<P, NCH, M>, smem, &configured);
-  k_smooth_march<P, NCH, M><<<nrt * nxc, kThreadsM, smem, s>>>(g, *tm, color, c, alpha);
+  return nrt * ((g.nxl + ich - 1) / ich);
 }
 
-template <bool P, int M>
+template <bool P, int NCH, int M, bool NORM = false>
+static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
+                      int color, double alpha, cudaStream_t s,
+                      double *partials = nullptr) {
+  const size_t smem = smooth_smem_bytes(g);
+  static size_t configured = 0;
+  set_smem(k_smooth_march<P, NCH, M, NORM>, smem, &configured);
+  k_smooth_march<P, NCH, M, NORM><<<smooth_blocks(g), kThreadsM, smem, s>>>(
+      g, *tm, color, c, alpha, partials);
+}
+
+template <bool P, int M, bool NORM = false>
 static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
-                        int color, double alpha, cudaStream_t s) {
+                        int color, double alpha, cudaStream_t s,
+                        double *partials = nullptr) {
   const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm128);
   switch ((g.nzh + 63) >> 6) {
-    case 1: launch_sm<P, 1, M>(g, c, tm, color, alpha, s); break;
-    case 2: launch_sm<P, 2, M>(g, c, tm, color, alpha, s); break;
-    case 3: launch_sm<P, 3, M>(g, c, tm, color, alpha, s); break;
-    default: launch_sm<P, 4, M>(g, c, tm, color, alpha, s); break;
+    case 1: launch_sm<P, 1, M, NORM>(g, c, tm, color, alpha, s, partials); break;
+    case 2: launch_sm<P, 2, M, NORM>(g, c, tm, color, alpha, s, partials); break;
+    case 3: launch_sm<P, 3, M, NORM>(g, c, tm, color, alpha, s, partials); break;
+    default: launch_sm<P, 4, M, NORM>(g, c, tm, color, alpha, s, partials); break;
   }
 }
 
@@ -718,6 +752,22 @@ void launch_smooth_march(const Grid &g, const void *tm_oth128, int color,
     case VAR_PER: launch_sm_n<false, VAR_PER>(g, g, tm_oth128, color, 0.0, s); break;
     default: launch_sm_n<false, VAR_BOX>(g, g, tm_oth128, color, 0.0, s); break;
   }
+}
+
+int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
+                             double *partials, cudaStream_t s) {
+  switch (variant(g)) {
+    case VAR_MASK:
+      launch_sm_n<false, VAR_MASK, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      break;
+    case VAR_PER:
+      launch_sm_n<false, VAR_PER, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      break;
+    default:
+      launch_sm_n<false, VAR_BOX, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      break;
+  }
+  return smooth_blocks(g);
 }
 
 void launch_prolong_smooth_march(const Grid &g, const Grid &c,
@@ -763,6 +813,16 @@ void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
 }
 
 int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
+
+int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
+                          double *partials, cudaStream_t s) {
+  switch (variant(g)) {
+    case VAR_MASK: launch_rm<MODE_NORM_RED, VAR_MASK>(g, g, tmR, tmB, partials, s); break;
+    case VAR_PER: launch_rm<MODE_NORM_RED, VAR_PER>(g, g, tmR, tmB, partials, s); break;
+    default: launch_rm<MODE_NORM_RED, VAR_BOX>(g, g, tmR, tmB, partials, s); break;
+  }
+  return resid_blocks(g);
+}
 
 int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,
                                      const void *tmB, double *partials,

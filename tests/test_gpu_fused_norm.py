@@ -108,7 +108,7 @@ def test_fused_norm_cycles_match_oracle(mg, case):
     s.set_rhs(f)
     hd = [s.vcycle() for _ in range(4)]
     assert np.array_equal(s.get_solution(), phi_fused)
-    assert hd[-1] == s.residual_norm()
+    assert abs(hd[-1] - s.residual_norm()) <= 1e-13 * hd[-1]  # summation order
     s.close()
 
 
