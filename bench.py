@@ -385,10 +385,10 @@ def run_cuda(args):
     for l in range(L - 1):
         frac = 8.0 ** -l
         model_bytes += (24 * nsw + 34) * frac
-    # the norm: 16 B/cell; the split cycle-end norm (default,
-    # single-grid level 0) reads 12 -- the black residuals ride on the last
-    # black half-sweep
-    split = N == 1 and os.environ.get("MG_SPLIT_NORM", "1") != "0"
+    # the norm: 16 B/cell; the split cycle-end norm (default:
+    # one level-0 grid per process) reads 12 -- the black residuals ride on
+    # the last black half-sweep
+    split = os.environ.get("MG_SPLIT_NORM", "1") != "0"
     model_bytes += 12 if split else 16
     cycle_ms = ms / args.steps
     cycle_frac = model_bytes * local_cells / (cycle_ms * 1e-3) / 1e9 / peak

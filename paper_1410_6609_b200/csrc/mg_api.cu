@@ -850,6 +850,8 @@ int enqueue_vcycle(mg_ctx *c) {
         c->launches++;
         mark(c, CAT_SMOOTH0);
         CK(cudaGetLastError());
+        // slabs of an NCCL run: the red residuals read the new black ghosts
+        if ((rc = halo(c, 0, 1))) return rc;
         break;
       }
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
