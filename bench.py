@@ -112,25 +112,62 @@ def dist_env():
     return ws, rank, local
 
 
-def cpu_baseline(n_sample=256, cycles=2):
-    """The oracle as it stands on a bounded sample of the config-3 recipe:
-    n_sample^3 cells, V(2,2) to 8^3, one warm-up cycle then `cycles` timed."""
+CPU_SAMPLE = 256  # oracle sample edge for cpu_baseline and --impl reference
+
+
+def oracle_rate(n_sample, warm, cycles):
+    """Mcells/s of the oracle (as it stands) on the config-3 recipe at
+    n_sample^3: `warm` untimed then `cycles` timed V(2,2)-cycles (each with
+    its residual norm), and the seconds they took."""
     import oracle
     from paper_1410_6609_b200 import workloads as W
+    oracle.build()
     w = W.cfg3(n_sample, seed=0)
     o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
     o.set_rhs(w.rhs)
-    o.vcycle()
+    for _ in range(warm):
+        o.vcycle()
     t0 = time.perf_counter()
     for _ in range(cycles):
         o.vcycle()
     dt = time.perf_counter() - t0
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
-    return {"value": round(w.cells * cycles / dt / 1e6, 3), "unit": UNIT,
+    return w.cells * cycles / dt / 1e6, dt, o.nlevels
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(n_sample=CPU_SAMPLE, cycles=2):
+    """The oracle as it stands on a bounded sample of the config-3 recipe:
+    n_sample^3 cells, V(2,2) to 8^3, one warm-up cycle then `cycles` timed --
+    the OpenMP build on all host cores (the headline baseline) and, in a
+    child process with OMP_NUM_THREADS=1, single-threaded."""
+    cores = int(os.environ.get("OMP_NUM_THREADS", host_cores()))
+    val, _, _ = oracle_rate(n_sample, 1, cycles)
+    single = None
+    try:
+        env = dict(os.environ, OMP_NUM_THREADS="1")
+        out = subprocess.run(
+            [sys.executable, "-c",
+             "import sys; sys.path.insert(0, %r); import bench; "
+             "print(bench.oracle_rate(%d, 1, 1)[0])" % (ROOT, n_sample)],
+            env=env, capture_output=True, text=True, timeout=600)
+        single = round(float(out.stdout.strip().splitlines()[-1]), 3)
+    except Exception:
+        single = None
+    return {"value": round(val, 3), "unit": UNIT,
             "cores": cores, "kind": "oracle",
+            "single_thread_value": single,
+            "host_cores": host_cores(),
             "sample": "config-3 recipe at %d^3 (h=1/%d, U[-1,1], V(2,2) to 8^3), "
                       "1 warm-up + %d timed V-cycles incl. residual norm, "
-                      "OpenMP threads=%d" % (n_sample, n_sample, cycles, cores)}
+                      "OpenMP threads=%d; single_thread_value: the same sample, "
+                      "1 warm-up + 1 timed cycle, OMP_NUM_THREADS=1"
+                      % (n_sample, n_sample, cycles, cores)}
 
 
 def timestep_regime(mg, W, stream, local, steps=10, warm=2):
@@ -228,21 +265,9 @@ def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return 0
-    import oracle
-    from paper_1410_6609_b200 import workloads as W
-    oracle.build()
     n = args.ref_size
-    w = W.cfg3(n, seed=0)
-    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8)
-    o.set_rhs(w.rhs)
-    for _ in range(args.warmup):
-        o.vcycle()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        o.vcycle()
-    dt = time.perf_counter() - t0
-    val = w.cells * args.steps / dt / 1e6
-    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    val, dt, nlev = oracle_rate(n, args.warmup, args.steps)
+    cores = int(os.environ.get("OMP_NUM_THREADS", host_cores()))
     full = args.size ** 3 * max(args.gpus, 1)
     line = {
         "impl": "reference", "metric": METRIC, "value": round(val, 3),
@@ -252,7 +277,7 @@ def run_reference(args):
         "dtype": "f64", "data": "synthetic",
         "config": {"workload": "cfg3 recipe, CPU oracle sample %d^3 of the %d-cell workload"
                                % (n, full),
-                   "schedule": "V(2,2)", "levels": o.nlevels},
+                   "schedule": "V(2,2)", "levels": nlev},
         "cpu_baseline": {"value": round(val, 3), "unit": UNIT, "cores": cores,
                          "kind": "oracle",
                          "sample": "%d^3 cells per step (one V(2,2)-cycle incl. norm)" % n},
@@ -360,13 +385,12 @@ def run_cuda(args):
     s.set_profiling(False)
     sm0 = np.mean([p["smooth0_ms"] for p in prof])
     nsm = prof[0]["smooth0_launches"]
-    hs_per_launch = prof[0]["smooth0_halfsweeps"] / nsm  # 4: temporally blocked
     cyc_prof = np.mean([p["cycle_ms"] for p in prof])
     per_launch_ms = sm0 / nsm
     local_cells = cells // N
-    # SURVEY 8(d) per-unit figure (12 B per cell and half-sweep) x the
-    # half-sweeps one launch performs
-    alg_bytes = int(HALF_SWEEP_BYTES_PER_CELL * hs_per_launch * local_cells)
+    # SURVEY 8(d) per-unit figure (12 B per cell and half-sweep) x the cells
+    # one launch updates (the rank's level-0 slab)
+    alg_bytes = int(HALF_SWEEP_BYTES_PER_CELL * local_cells)
     achieved = alg_bytes / (per_launch_ms * 1e-3) / 1e9
     peak, peak_src = peaks()
     traffic = None
@@ -374,8 +398,7 @@ def run_cuda(args):
     if os.path.exists(tf):
         try:
             tj = json.load(open(tf))
-            kname = "k_sweep4" if hs_per_launch == 4 else "k_smooth_march"
-            if tj.get("cells") == local_cells and tj.get("kernel") == kname:
+            if tj.get("cells") == local_cells and tj.get("kernel") == "k_smooth_march":
                 traffic = tj.get("bytes_per_launch")
         except Exception:
             traffic = None
@@ -385,10 +408,10 @@ def run_cuda(args):
     for l in range(L - 1):
         frac = 8.0 ** -l
         model_bytes += (24 * nsw + 34) * frac
-    # the norm: 16 B/cell; the split cycle-end norm (default:
-    # one level-0 grid per process) reads 12 -- the black residuals ride on
-    # the last black half-sweep
-    split = os.environ.get("MG_SPLIT_NORM", "1") != "0"
+    # the norm: 16 B/cell; the split cycle-end norm reads 12 --
+    # the black residuals ride on the last black half-sweep.  The library
+    # reports which path the recorded cycle took (mg_cycle_paths).
+    split = bool(s.cycle_paths & mg.MG_PATH_SPLIT_NORM)
     model_bytes += 12 if split else 16
     cycle_ms = ms / args.steps
     cycle_frac = model_bytes * local_cells / (cycle_ms * 1e-3) / 1e9 / peak
@@ -481,10 +504,7 @@ def run_cuda(args):
                    "l2": "inputs larger than L2 (hierarchy %.2f GB vs 126 MB L2); no flush"
                          % (mg.workspace_bytes(shape, min_coarse=8) / 1e9 / N)},
         "roofline": {"bound": "hbm",
-                     "kernel": ("k_sweep4 (level-0 V(2,2) pre-smoothing pass: 4 RBGS "
-                                "half-sweeps, temporally blocked)" if hs_per_launch == 4
-                                else "k_smooth_march (level-0 RBGS half-sweep)"),
-                     "halfsweeps_per_launch": int(hs_per_launch),
+                     "kernel": "k_smooth_march (level-0 RBGS half-sweep)",
                      "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                      "frac": round(achieved / peak, 4), "traffic": traffic,
                      "alg_bytes_per_launch": alg_bytes,
@@ -538,8 +558,8 @@ def main():
     ap.add_argument("--impl", default="cuda", choices=["cuda", "reference"])
     ap.add_argument("--workload", default=None, choices=[None, "cfg3", "cfg4", "cfg5"])
     ap.add_argument("--size", type=int, default=512)
-    ap.add_argument("--cpu-size", type=int, default=256)
-    ap.add_argument("--ref-size", type=int, default=128)
+    ap.add_argument("--cpu-size", type=int, default=CPU_SAMPLE)
+    ap.add_argument("--ref-size", type=int, default=CPU_SAMPLE)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-ts", action="store_true",

@@ -108,7 +108,30 @@ typedef struct {
                          separate pass in both modes; a single-level
                          hierarchy always reports the post-cycle norm.  The
                          iterates are identical in both modes.              */
+  int disable;        /* bitmask of MG_OFF_* (default 0: every fast path the
+                         grid allows).  Each bit selects an equivalent slower
+                         path -- used to test that the paths agree: the
+                         per-cell arithmetic is identical, so iterates are
+                         bitwise equal; only reductions may round
+                         differently.  Which paths a recorded V-cycle took is
+                         reported by mg_cycle_paths().                      */
 } mg_opts;
+
+/* mg_opts.disable bits */
+#define MG_OFF_MARCH 1       /* TMA plane-marching kernels -> direct loads    */
+#define MG_OFF_OVERLAP 2     /* multi-slab halo / interior overlap -> serial  */
+#define MG_OFF_SPLIT_NORM 4  /* split cycle-end norm -> one full norm pass    */
+#define MG_OFF_CG_CLUSTER 8  /* 8-CTA cluster CG -> single-CTA CG             */
+#define MG_OFF_MASK_CODES 16 /* masked levels: byte codes -> float records    */
+
+/* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
+#define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
+#define MG_PATH_OVERLAP 2        /* halo exchange overlapped with interiors   */
+#define MG_PATH_SPLIT_NORM 4     /* norm split over the last black sweep      */
+#define MG_PATH_CG_CLUSTER 8     /* coarsest CG on a thread-block cluster     */
+#define MG_PATH_CG_VAR 16        /* variable-coefficient coarsest CG          */
+#define MG_PATH_PROLONG_FUSED 32 /* prolongation fused with the red sweep     */
+#define MG_PATH_FUSED_NORM 64    /* norm from the in-cycle residual (c11)     */
 
 typedef struct mg_ctx mg_ctx;
 
@@ -367,13 +390,13 @@ int mg_set_profiling(mg_ctx *ctx, int on);
 int mg_last_cycle_times(mg_ctx *ctx, double out[8]);
 /* As mg_last_cycle_times, n >= 10 outputs, plus
  *   out[8] level-0 smoothing launches timed in out[0]
- *   out[9] level-0 half-sweeps they perform (4 per launch with the
- *          temporally blocked V(2,2) passes; 1 otherwise)
- * With the temporally blocked passes out[0] times the pre-smoothing pass and
- * out[3] the prolongation + post-smoothing pass of level 0. */
+ *   out[9] level-0 half-sweeps they perform (one per launch) */
 int mg_last_cycle_times_ex(mg_ctx *ctx, double *out, int n);
 /* Number of kernels one mg_vcycle launches (counted when it is recorded). */
 int mg_cycle_launches(const mg_ctx *ctx);
+/* MG_PATH_* bits of the kernel paths the last recorded V-cycle took (0
+ * before the first cycle); MG_ERR_ARG for a null ctx. */
+int mg_cycle_paths(const mg_ctx *ctx);
 /* cudaStream_t of the context (for event timing by the caller). */
 void *mg_stream(const mg_ctx *ctx);
 

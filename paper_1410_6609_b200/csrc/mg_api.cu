@@ -174,31 +174,24 @@ struct TmPair {
   alignas(64) unsigned char b[128];
   alignas(64) unsigned char rr[128];  // z-tiled boxes (residual kernels)
   alignas(64) unsigned char rb[128];
-  alignas(64) unsigned char r12[128]; // 12-row red boxes (fused kernels)
-  alignas(64) unsigned char t4a[256]; // temporally blocked pass: input phiB
-  alignas(64) unsigned char t4b[256]; //                         input phiB2
-  alignas(64) unsigned char rb2[128]; // z-tiled boxes of phiB2 (residual)
-  alignas(64) unsigned char s2a[128]; // full-sweep kernel: input phiB
-  alignas(64) unsigned char s2b[128]; //                   input phiB2
-  bool ok = false, ok_resid = false, ok_fused = false, ok_t4 = false, ok_s2 = false;
+  bool ok = false, ok_resid = false;
 };
 
 struct mg_ctx {
   Plan pl;
   std::vector<std::vector<TmPair>> tm;
-  int use_march = 1;
-  int use_fused = 0;  // MG_FUSED=1: last-black + residual fusion (slower today)
-  int use_t4 = 0;     // temporally blocked V(2,2) passes (opt-in: MG_T4=1)
-  int use_s2 = 0;     // one full sweep (red + black) per kernel (MG_S2=1)
+  // kernel paths (mg_opts.disable clears them; include/mg.h MG_OFF_*)
+  int use_march = 1;  // TMA plane-marching kernels where the grid allows
   int split_off = 0;  // split norm: partials written by the last black sweep
-  // multi-slab overlap (MG_NO_OVERLAP=1: off): boundary planes first, the
-  // ghost exchange on s_comm while the interior planes are swept
+  // multi-slab overlap: boundary planes first, the ghost exchange on s_comm
+  // while the interior planes are swept
   int overlap = 1;
+  int paths = 0;      // MG_PATH_* taken by the last recorded V-cycle
+  int nsm = 148;      // SMs of the device (cudaDevAttrMultiProcessorCount)
   cudaStream_t s_comm = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<std::vector<Grid>> vlo, vhi, vin;   // per level, slab: views
   std::vector<std::vector<TmPair>> tmin;          // TMA maps of the interior views
-  int t4_ty = 16;     // their tile rows (MG_T4_TY=8|16)
   bool masked = false;            // variable coefficients (mask and/or patches)
   std::vector<void *> mask_bufs;  // codes / coefficients (library-owned)
   std::vector<uint8_t> solid_h;   // global solid mask (empty: none)
@@ -220,7 +213,7 @@ struct mg_ctx {
   char *ws = nullptr;
   size_t ws_bytes = 0;
   bool own_ws = false;
-  double *partials = nullptr;  // kNormBlocks per held slab
+  double *partials = nullptr;  // norm partial sums (carve: upper bound)
   double *normv = nullptr;     // [0] local sum, [1] global sum, [2..2+P) gathered
   double *cg_scr = nullptr;
   int *cg_iters = nullptr;
@@ -236,7 +229,10 @@ struct mg_ctx {
   size_t astg_bytes = 0;
   cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
   cudaEvent_t ev_in[3] = {}, ev_out[3] = {}, ev_d2h[3] = {};
-  bool d2h_used[3] = {false, false, false};
+  // ev_free[q]: recorded on the context's stream after its last read of slot
+  // q (the RHS conversion); the next upload into the slot waits for it
+  cudaEvent_t ev_free[3] = {};
+  bool d2h_used[3] = {false, false, false}, free_used[3] = {false, false, false};
   unsigned long long async_k = 0;
   double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
@@ -260,7 +256,9 @@ struct mg_ctx {
 
 namespace {
 
-constexpr int kNormBlocks = 148 * 8;
+// partial sums of the grid-stride norm kernels: 8 per SM, for up to 256 SMs
+// (the workspace size must not depend on a device query)
+constexpr int kMaxNormBlocks = 8 * 256;
 
 // bump allocation over the workspace; with base == nullptr only sizes
 struct Carver {
@@ -274,18 +272,6 @@ struct Carver {
   }
 };
 
-// the temporally blocked V(2,2) passes (mg_t4.cu) are opt-in: correct and
-// bitwise equal, but slower than four marching half-sweeps on B200 today
-// (DESIGN.md); their second black arrays are only carved when requested
-bool t4_requested() {
-  const char *e = getenv("MG_T4");
-  return e && atoi(e) != 0;
-}
-bool s2_requested() {
-  const char *e = getenv("MG_S2");
-  return e && atoi(e) != 0;
-}
-
 size_t carve(mg_ctx *c, char *base) {
   Carver cv{base};
   const int L = c->pl.L;
@@ -298,6 +284,7 @@ size_t carve(mg_ctx *c, char *base) {
     const int ns = l < c->pl.nd ? c->nslab : 1;
     for (int s = 0; s < ns; s++) {
       Grid gr = make_grid(c->pl, l, l < c->pl.nd ? c->slab0 + s : 0, c->h, dface);
+      gr.nsm = c->nsm;
       for (int a = 0; a < 3; a++) gr.per[a] = c->bc[2 * a].type == MG_PERIODIC;
       gr.gx = gr.per[0] && gr.nxl == gr.nx;  // whole grid: own x ghosts
       const size_t bytes = (size_t)mg::grid_elems(gr) * sizeof(double);
@@ -305,19 +292,14 @@ size_t carve(mg_ctx *c, char *base) {
       gr.phiB = (double *)cv.take(bytes);
       gr.fR = (double *)cv.take(bytes);
       gr.fB = (double *)cv.take(bytes);
-      // second black array for the temporally blocked passes (levels held
-      // whole: one slab, or agglomerated)
-      gr.phiB2 = (gr.nxl == gr.nx && (t4_requested() || s2_requested()))
-                     ? (double *)cv.take(bytes)
-                     : nullptr;
       c->g[l].push_back(gr);
     }
   }
-  size_t npart = kNormBlocks;
+  size_t npart = kMaxNormBlocks;
   for (const Grid &g : c->g[0]) {
     // residual-kernel partials, plus (split norm) the smoother's, fewer
-    const size_t nb = (size_t)mg::norm_march_blocks(g);
-    npart += 2 * (nb > (size_t)kNormBlocks ? nb : (size_t)kNormBlocks);
+    const size_t nb = (size_t)mg::march_blocks_max(g);
+    npart += 2 * (nb > (size_t)kMaxNormBlocks ? nb : (size_t)kMaxNormBlocks);
   }
   c->partials = (double *)cv.take(sizeof(double) * npart);
   c->normv = (double *)cv.take(sizeof(double) * (2 + c->P));
@@ -441,7 +423,6 @@ Grid plane_view(const Grid &g, int pb, int n) {
   v.phiB += off;
   v.fR += off;
   v.fB += off;
-  v.phiB2 = nullptr;
   v.nxl = n;
   v.x0 = g.x0 + pb;
   return v;
@@ -485,6 +466,7 @@ int smooth_half_overlap(mg_ctx *c, int l, int color, int from_zero) {
 
 int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
   if (overlap_level(c, l)) {
+    c->paths |= MG_PATH_OVERLAP;
     if (l == 0) mark(c, CAT_NONE);
     int rc = smooth_half_overlap(c, l, color, from_zero);
     if (l == 0) mark(c, CAT_SMOOTH0);
@@ -570,27 +552,6 @@ int prolong_level(mg_ctx *c, int l) {
   return halo(c, l, 1);  // the next red half-sweep reads black ghosts
 }
 
-// can level l use the fused last-black + residual epilogue kernels?
-bool can_fuse_resid(const mg_ctx *c, int l) {
-  if (!c->use_march || !c->use_fused || c->masked || distributed(c, l) ||
-      any_periodic(c) || fused_norm_on(c))
-    return false;
-  for (const TmPair &t : c->tm[l])
-    if (!t.ok_fused) return false;
-  return c->g[l].size() == 1;
-}
-
-// last pre-smoothing black half-sweep fused with f_{l+1} = R(f_l - A Phi_l)
-int black_restrict_level(mg_ctx *c, int l) {
-  if (l == 0) mark(c, CAT_NONE);
-  mg::launch_black_restrict(c->g[l][0], coarse_of(c, l, 0), c->tm[l][0].r12,
-                            c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_RESTRICT0);
-  CK(cudaGetLastError());
-  return MG_OK;
-}
-
 // can level l use the fused prolongation + first post-smoothing red sweep?
 bool can_fuse_prolong(const mg_ctx *c, int l) {
   if (!c->use_march || c->o.nu2 < 1) return false;
@@ -609,31 +570,32 @@ int prolong_red_level(mg_ctx *c, int l) {
                                     c->tm[l][s].b, 0, c->o.alpha, c->stream);
     c->launches++;
   }
-  if (l == 0) mark(c, CAT_PROLONG0);
+  if (l == 0) {
+    mark(c, CAT_PROLONG0);
+    c->paths |= MG_PATH_PROLONG_FUSED;
+  }
   CK(cudaGetLastError());
   return halo(c, l, 0);  // black is recomputed by the next half-sweep
 }
 
-// MG_CG_CLUSTER=0 keeps the single-CTA CG on the large coarsest grids too
-bool cg_cluster_on() {
-  static const bool on = [] {
-    const char *e = getenv("MG_CG_CLUSTER");
-    return !(e && atoi(e) == 0);
-  }();
-  return on;
-}
+// the coarsest grids of agglomerated runs (>= 4,096 unknowns) run CG on an
+// 8-CTA cluster unless mg_opts.disable has MG_OFF_CG_CLUSTER
+bool cg_cluster_on(const mg_ctx *c) { return !(c->o.disable & MG_OFF_CG_CLUSTER); }
 
 int coarse_solve(mg_ctx *c) {
   const Grid &g = c->g[c->pl.L - 1][0];
-  if (c->masked)
+  if (c->masked) {
     mg::launch_coarse_cg_var(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
                              c->cg_iters, c->stream);
-  else if (cg_cluster_on() && mg::coarse_cg_cluster_supported(g))
+    c->paths |= MG_PATH_CG_VAR;
+  } else if (cg_cluster_on(c) && mg::coarse_cg_cluster_supported(g)) {
     mg::launch_coarse_cg_cluster(g, c->o.coarse_tol, c->o.coarse_maxit, c->cg_iters,
                                  c->stream);
-  else
+    c->paths |= MG_PATH_CG_CLUSTER;
+  } else {
     mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
                          c->cg_iters, c->stream);
+  }
   c->launches++;
   periodic_fill(c, c->pl.L - 1);  // the prolongation reads coarse ghosts
   CK(cudaGetLastError());
@@ -687,104 +649,47 @@ int finish_norm(mg_ctx *c, int off) {
   return MG_OK;
 }
 
-// temporally blocked V(2,2) passes on level l (mg_t4.cu)?
-bool use_t4(const mg_ctx *c, int l) {
-  if (!c->use_t4 || !c->use_march || c->masked || any_periodic(c) || fused_norm_on(c))
-    return false;
-  if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
-  const Grid &g = c->g[l][0];
-  // large levels only: on the small ones the per-half-sweep kernels (or their
-  // launch latency) cost less than the wavefront's halo work
-  return c->tm[l][0].ok_t4 && mg::sweep4_supported(g) && g.nzh >= 64 && g.ny >= 32;
-}
-
-// full-sweep kernels (mg_sweep2.cu) on level l?  V(2,2) only: the two
-// sweeps of a pass alternate the black arrays (phiB -> phiB2 -> phiB)
-bool use_s2(const mg_ctx *c, int l) {
-  if (!c->use_s2 || !c->use_march || c->masked || any_periodic(c) || fused_norm_on(c))
-    return false;
-  if (c->o.nu1 != 2 || c->o.nu2 != 2 || c->g[l].size() != 1) return false;
-  return c->tm[l][0].ok_s2 && mg::sweep2_supported(c->g[l][0]);
-}
-
 // split cycle-end norm: the last black half-sweep of level 0 sums the black
 // residuals (k_smooth_march<..., NORM>), a red-only residual pass the rest:
-// 12 + 12 instead of 12 + 16 B/cell for that pair (MG_SPLIT_NORM=0: off)
+// 12 + 12 instead of 12 + 16 B/cell for that pair.  Every level-0 slab needs
+// both marching kernels; MG_OFF_SPLIT_NORM turns it off.
 bool split_norm_ok(const mg_ctx *c) {
-  static const bool on = [] {
-    const char *e = getenv("MG_SPLIT_NORM");
-    return !(e && atoi(e) == 0);
-  }();
-  if (!on || fused_norm_on(c) || c->pl.L < 2 || c->o.nu2 < 1) return false;
-  if (c->g[0].size() != 1 || !c->use_march || can_fuse_resid(c, 0)) return false;
-  if (use_t4(c, 0) || use_s2(c, 0)) return false;
-  const Grid &g = c->g[0][0];
-  const TmPair &t = c->tm[0][0];
-  return t.ok && t.ok_resid && (!c->masked || g.codeR);
+  if ((c->o.disable & MG_OFF_SPLIT_NORM) || fused_norm_on(c) || c->pl.L < 2 ||
+      c->o.nu2 < 1 || !c->use_march)
+    return false;
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    const TmPair &t = c->tm[0][s];
+    if (!(t.ok && t.ok_resid && (!c->masked || c->g[0][s].codeR))) return false;
+  }
+  return true;
 }
 
-int s2_pre(mg_ctx *c, int l) {
-  const Grid &g = c->g[l][0];
-  const TmPair &t = c->tm[l][0];
-  if (l == 0) mark(c, CAT_NONE);
-  mg::launch_sweep2(g, g, t.s2a, g.phiB2, false, l > 0, 0.0, c->stream);
-  if (l == 0) mark(c, CAT_SMOOTH0);
-  mg::launch_sweep2(g, g, t.s2b, g.phiB, false, false, 0.0, c->stream);
-  c->launches += 2;
-  if (l == 0) mark(c, CAT_SMOOTH0);
+// the split norm's two passes, after the last red post-smoothing half-sweep
+// of level 0: black sweep + black residual partials on every slab, the black
+// ghost exchange (the red residuals read the new black ghosts), red residual
+// partials, the ordered sum
+int split_norm_tail(mg_ctx *c) {
+  mark(c, CAT_NONE);
+  int off = 0;
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    off += mg::launch_smooth_norm_march(c->g[0][s], c->tm[0][s].r, 1, c->partials + off,
+                                        c->stream);
+    c->launches++;
+  }
+  mark(c, CAT_SMOOTH0);
   CK(cudaGetLastError());
-  return restrict_level(c, l);
-}
-
-int s2_post(mg_ctx *c, int l) {
-  const Grid &g = c->g[l][0];
-  const TmPair &t = c->tm[l][0];
-  if (l == 0) mark(c, CAT_NONE);
-  mg::launch_sweep2(g, coarse_of(c, l, 0), t.s2a, g.phiB2, true, false, c->o.alpha,
-                    c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_PROLONG0);
-  mg::launch_sweep2(g, g, t.s2b, g.phiB, false, false, 0.0, c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_SMOOTH0);
+  int rc;
+  if ((rc = halo(c, 0, 1))) return rc;
+  c->split_off = off;
+  mark(c, CAT_NONE);
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    off += mg::launch_norm_red_march(c->g[0][s], c->tm[0][s].rr, c->tm[0][s].rb,
+                                     c->partials + off, c->stream);
+    c->launches++;
+  }
   CK(cudaGetLastError());
-  return MG_OK;
-}
-
-// pre-smoothing (4 half-sweeps) -> red in phiR, black in phiB2; then
-// f_{l+1} = R (f_l - A_l Phi_l) reading black from phiB2
-int t4_pre_restrict(mg_ctx *c, int l) {
-  const Grid &g = c->g[l][0];
-  const TmPair &t = c->tm[l][0];
-  Grid go = g;
-  go.phiB = g.phiB2;
-  if (l == 0) mark(c, CAT_NONE);
-  mg::launch_sweep4(go, g, t.t4a, false, l > 0, 0.0, c->t4_ty, c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_SMOOTH0);
-  CK(cudaGetLastError());
-  const Grid &cg = coarse_of(c, l, 0);
-  if (t.ok_resid && c->use_march)
-    mg::launch_resid_restrict_march(go, cg, t.rr, t.rb2, c->stream);
-  else
-    mg::launch_resid_restrict(go, cg, 0, c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_RESTRICT0);
-  CK(cudaGetLastError());
-  return MG_OK;
-}
-
-// prolongation + magnified correction of the black from phiB2, then the 4
-// post-smoothing half-sweeps -> red in phiR, black back in phiB
-int t4_prolong_post(mg_ctx *c, int l) {
-  const Grid &g = c->g[l][0];
-  if (l == 0) mark(c, CAT_NONE);
-  mg::launch_sweep4(g, coarse_of(c, l, 0), c->tm[l][0].t4b, true, false, c->o.alpha,
-                    c->t4_ty, c->stream);
-  c->launches++;
-  if (l == 0) mark(c, CAT_PROLONG0);
-  CK(cudaGetLastError());
-  return MG_OK;
+  c->paths |= MG_PATH_SPLIT_NORM;
+  return finish_norm(c, off);
 }
 
 int enqueue_vcycle(mg_ctx *c) {
@@ -792,6 +697,9 @@ int enqueue_vcycle(mg_ctx *c) {
   int rc;
   c->launches = 0;
   c->nev = 0;
+  c->paths = 0;
+  if (c->use_march && !c->tm[0].empty() && c->tm[0][0].ok) c->paths |= MG_PATH_MARCH;
+  if (fused_norm_on(c)) c->paths |= MG_PATH_FUSED_NORM;
   for (int l = 0; l < L - 1; l++) {
     if (l == 1) mark(c, CAT_NONE);
     if (c->o.nu1 == 0 && l > 0)
@@ -799,87 +707,31 @@ int enqueue_vcycle(mg_ctx *c) {
         CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
         CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
       }
-    if (use_t4(c, l)) {
-      if ((rc = t4_pre_restrict(c, l))) return rc;
-      continue;
-    }
-    if (use_s2(c, l)) {
-      if ((rc = s2_pre(c, l))) return rc;
-      continue;
-    }
-    const bool fuse_r = c->o.nu1 >= 1 && can_fuse_resid(c, l);
     for (int s = 0; s < c->o.nu1; s++) {
       if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
-      if (fuse_r && s == c->o.nu1 - 1) break;
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
     }
-    if (fuse_r) {
-      if ((rc = black_restrict_level(c, l))) return rc;
-    } else {
-      if ((rc = restrict_level(c, l))) return rc;
-    }
+    if ((rc = restrict_level(c, l))) return rc;
   }
   if (L == 1) mark(c, CAT_NONE);
   if ((rc = coarse_solve(c))) return rc;
   for (int l = L - 2; l >= 0; l--) {
     if (l == 0) mark(c, CAT_COARSE);
-    if (use_t4(c, l)) {
-      if ((rc = t4_prolong_post(c, l))) return rc;
-      continue;
-    }
-    if (use_s2(c, l)) {
-      if ((rc = s2_post(c, l))) return rc;
-      continue;
-    }
     const bool fuse = can_fuse_prolong(c, l);
     if (fuse) {
       if ((rc = prolong_red_level(c, l))) return rc;
     } else {
       if ((rc = prolong_level(c, l))) return rc;
     }
-    const bool fuse_n = l == 0 && c->o.nu2 >= 1 && can_fuse_resid(c, 0);
     const bool split_n = l == 0 && split_norm_ok(c);
     for (int s = 0; s < c->o.nu2; s++) {
       if (!(fuse && s == 0))
         if ((rc = smooth_half(c, l, 0, 0))) return rc;
-      if (fuse_n && s == c->o.nu2 - 1) break;
-      if (split_n && s == c->o.nu2 - 1) {  // last black: + black residuals
-        mark(c, CAT_NONE);
-        c->split_off = mg::launch_smooth_norm_march(c->g[0][0], c->tm[0][0].r, 1,
-                                                    c->partials, c->stream);
-        c->launches++;
-        mark(c, CAT_SMOOTH0);
-        CK(cudaGetLastError());
-        // slabs of an NCCL run: the red residuals read the new black ghosts
-        if ((rc = halo(c, 0, 1))) return rc;
-        break;
-      }
+      if (split_n && s == c->o.nu2 - 1) break;  // the last black: split_norm_tail
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
     }
-    if (split_n) {  // + red residuals, then the ordered sum as enqueue_norm
-      mark(c, CAT_NONE);
-      const int off = c->split_off +
-                      mg::launch_norm_red_march(c->g[0][0], c->tm[0][0].rr,
-                                                c->tm[0][0].rb,
-                                                c->partials + c->split_off, c->stream);
-      c->launches++;
-      CK(cudaGetLastError());
-      if ((rc = finish_norm(c, off))) return rc;
-      c->cycle_launches = c->launches;
-      c->prof_last = c->prof;
-      return MG_OK;
-    }
-    if (fuse_n) {  // last black half-sweep + residual norm in one pass
-      mark(c, CAT_NONE);
-      const int nb = mg::launch_black_norm(c->g[0][0], c->tm[0][0].r12,
-                                           c->partials, c->stream);
-      c->launches++;
-      mg::launch_sum_ordered(c->partials, nb, c->normv, c->stream);
-      c->launches++;
-      mg::launch_publish(c->normv, c->normv + 1, c->h_norm_dev, c->stream);
-      c->launches++;
-      CK(cudaGetLastError());
-      mark(c, CAT_NORM);
+    if (split_n) {
+      if ((rc = split_norm_tail(c))) return rc;
       c->cycle_launches = c->launches;
       c->prof_last = c->prof;
       return MG_OK;
@@ -1197,6 +1049,9 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
   };
   cudaError_t e = cudaSetDevice(c->dev);
   if (e != cudaSuccess) return bail(e, "cudaSetDevice");
+  e = cudaDeviceGetAttribute(&c->nsm, cudaDevAttrMultiProcessorCount, c->dev);
+  if (e != cudaSuccess) return bail(e, "cudaDeviceGetAttribute(SM count)");
+  if (c->nsm > 256) c->nsm = 256;  // kMaxNormBlocks bounds 8 CTAs per SM
   if (opts->stream) {
     c->stream = (cudaStream_t)opts->stream;
   } else {
@@ -1243,20 +1098,11 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
       t.ok_resid = mg::resid_march_supported(g) &&
                    mg::make_tmap_resid(g, g.phiR, t.rr) &&
                    mg::make_tmap_resid(g, g.phiB, t.rb);
-      t.ok_fused = t.ok_resid && mg::fused_supported(g) &&
-                   mg::make_tmap_red12(g, g.phiR, t.r12);
-      t.ok_s2 = g.phiB2 && mg::sweep2_supported(g) &&
-                mg::make_tmap_sweep2(g, g.phiB, t.s2a) &&
-                mg::make_tmap_sweep2(g, g.phiB2, t.s2b);
-      t.ok_t4 = g.phiB2 && mg::sweep4_supported(g) &&
-                mg::make_tmap_sweep4(g, g.phiB, t.t4a) &&
-                mg::make_tmap_sweep4(g, g.phiB2, t.t4b) &&
-                (!t.ok_resid || mg::make_tmap_resid(g, g.phiB2, t.rb2));
     }
   }
   // multi-slab overlap: views of the boundary / interior planes of every
   // distributed level (slabs of >= 4 planes), a communication stream
-  if (c->P > 1 && !getenv("MG_NO_OVERLAP")) {
+  if (c->P > 1 && !(opts->disable & MG_OFF_OVERLAP)) {
     c->vlo.assign(c->pl.L, {});
     c->vhi.assign(c->pl.L, {});
     c->vin.assign(c->pl.L, {});
@@ -1284,11 +1130,7 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
   } else {
     c->overlap = 0;
   }
-  if (getenv("MG_NO_MARCH")) c->use_march = 0;
-  if (getenv("MG_FUSED")) c->use_fused = 1;
-  if (t4_requested()) c->use_t4 = 1;
-  if (s2_requested()) c->use_s2 = 1;
-  if (const char *e = getenv("MG_T4_TY")) c->t4_ty = atoi(e) == 8 ? 8 : 16;
+  if (opts->disable & MG_OFF_MARCH) c->use_march = 0;
   e = cudaMemsetAsync(base, 0, need - 256, c->stream);
   if (e != cudaSuccess) return bail(e, "cudaMemsetAsync");
   e = cudaHostAlloc(&c->h_norm, sizeof(double) * 2, cudaHostAllocMapped);
@@ -1339,6 +1181,7 @@ void mg_destroy(mg_ctx *c) {
     if (c->ev_in[q]) cudaEventDestroy(c->ev_in[q]);
     if (c->ev_out[q]) cudaEventDestroy(c->ev_out[q]);
     if (c->ev_d2h[q]) cudaEventDestroy(c->ev_d2h[q]);
+    if (c->ev_free[q]) cudaEventDestroy(c->ev_free[q]);
   }
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
@@ -1404,9 +1247,10 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   if (n > 0) {
     CK(cudaMemcpyAsync(c->sph, h5, sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
+    mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, c->sph, cnt, c->stream);
     for (const Grid &g : c->g[0])
-      mg::launch_spheres(g, c->h, subsample, n, c->sph, normalization, cnt,
-                         c->stream);
+      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt,
+                                c->stream);
     CK(cudaGetLastError());
   }
   int rc = bc_adapt(c);
@@ -1471,6 +1315,7 @@ static int async_setup(mg_ctx *c, size_t bytes) {
       CK(cudaEventCreateWithFlags(&c->ev_in[q], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_out[q], cudaEventDisableTiming));
       CK(cudaEventCreateWithFlags(&c->ev_d2h[q], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&c->ev_free[q], cudaEventDisableTiming));
     }
   }
   if (c->astg_bytes < bytes) {
@@ -1481,6 +1326,7 @@ static int async_setup(mg_ctx *c, size_t bytes) {
       if (c->astg[q]) cudaFree(c->astg[q]);
       c->astg[q] = nullptr;
       c->d2h_used[q] = false;
+      c->free_used[q] = false;
     }
     c->astg_bytes = 0;
     for (int q = 0; q < 3; q++) CK(cudaMalloc(&c->astg[q], bytes));
@@ -1509,11 +1355,17 @@ int mg_solve_async(mg_ctx *c, const double *f, int where_f, double *phi_out,
   const int q = (int)(c->async_k++ % 3);
   double *stg = c->astg[q];
   if (where_f == MG_HOST) {
+    // the slot's previous users must be done with it: a download of Phi
+    // (ev_d2h) and the context stream's last read of it (ev_free: an RHS
+    // conversion, whatever the previous problem's phi_out was)
     if (c->d2h_used[q]) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_d2h[q], 0));
+    if (c->free_used[q]) CK(cudaStreamWaitEvent(c->s_h2d, c->ev_free[q], 0));
     CK(cudaMemcpyAsync(stg, f, n * sizeof(double), cudaMemcpyHostToDevice, c->s_h2d));
     CK(cudaEventRecord(c->ev_in[q], c->s_h2d));
     CK(cudaStreamWaitEvent(c->stream, c->ev_in[q], 0));
     if ((rc = pack0(c, MG_FIELD_RHS, stg))) return rc;
+    CK(cudaEventRecord(c->ev_free[q], c->stream));
+    c->free_used[q] = true;
   } else if ((rc = pack0(c, MG_FIELD_RHS, f))) {
     return rc;
   }
@@ -1838,7 +1690,7 @@ int rebuild_coefficients(mg_ctx *c) {
     CK(cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost,
                        c->stream));
     CK(cudaStreamSynchronize(c->stream));
-    if (!hfail && !getenv("MG_NO_MASK_CODES"))
+    if (!hfail && !(c->o.disable & MG_OFF_MASK_CODES))
       for (size_t s = 0; s < c->g[l].size(); s++) {
         Grid &g = c->g[l][s];
         g.codeR = codes[s].first;
@@ -2144,12 +1996,14 @@ int mg_last_cycle_times_ex(mg_ctx *c, double *out, int n) {
   if (!c || !out || n < 10) return fail(MG_ERR_ARG, "need 10 outputs");
   int rc = mg_last_cycle_times(c, out);
   if (rc) return rc;
-  out[8] = out[1];                               // level-0 smoothing launches
-  out[9] = out[1] * (use_t4(c, 0) ? 4.0 : (use_s2(c, 0) ? 2.0 : 1.0));
+  out[8] = out[1];  // level-0 smoothing launches
+  out[9] = out[1];  // half-sweeps they perform (one per launch)
   return MG_OK;
 }
 
 int mg_cycle_launches(const mg_ctx *c) { return c ? c->cycle_launches : MG_ERR_ARG; }
+
+int mg_cycle_paths(const mg_ctx *c) { return c ? c->paths : MG_ERR_ARG; }
 
 void *mg_stream(const mg_ctx *c) { return c ? (void *)c->stream : nullptr; }
 

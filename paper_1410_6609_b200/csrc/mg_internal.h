@@ -48,10 +48,9 @@ struct Grid {
   // has no ghosts: kernels wrap the half-index of z neighbours (per[2]).
   int per[3];
   int gx;  // x periodic and the grid held whole: its writers fill x ghosts
-  // second black array (temporally blocked smoother, mg_t4.cu): the fused
-  // pre-smoothing pass writes its final black values here, the fused
-  // post-smoothing pass reads them back (null: not allocated)
-  double *phiB2;
+  // streaming multiprocessors of the context's device (grid sizing of the
+  // plane-marching and reduction kernels; cudaDevAttrMultiProcessorCount)
+  int nsm;
 };
 
 __host__ __device__ inline long long grid_elems(const Grid &g) {
@@ -112,7 +111,7 @@ __device__ __forceinline__ double z_hi0(const Grid &g, const double *row, int k,
 // an ulp of 1/d -- is RN(a/d) (no overflow / underflow at the smoothers'
 // magnitudes).  Bitwise equal to IEEE a / d (except possibly the sign of an
 // exact zero) at a quarter of the instructions; the half-sweep parity tests
-// and test_temporal_blocking_equals_half_sweeps check it against `/`.
+// check it against the oracle's IEEE `/`.
 __device__ __forceinline__ double div_small(double a, double d, double rd) {
   const double q0 = __dmul_rn(a, rd);
   const double r0 = __fma_rn(-q0, d, a);
@@ -141,6 +140,10 @@ static __constant__ double c_rcp16[16] = {0.0,      1.0 / 1,  1.0 / 2,  1.0 / 3,
 __device__ __forceinline__ void fill_rcp16(double *rcp) {
   if (threadIdx.x < 16) rcp[threadIdx.x] = threadIdx.x ? 1.0 / (double)threadIdx.x : 0.0;
 }
+
+// upper bound of the grid-stride norm kernels' CTA count (8 per SM): the
+// number of partial sums they write
+__host__ __device__ inline int norm_blocks_max(const Grid &g) { return 8 * g.nsm; }
 
 __host__ __device__ inline bool is_periodic(const Grid &g) {
   return g.per[0] || g.per[1] || g.per[2];
@@ -172,9 +175,15 @@ void launch_first_empty(const unsigned long long *counts, int n, double *host_ds
 void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s);
 size_t coarse_cg_scratch_doubles(const Grid &g);
-void launch_spheres(const Grid &g, double h, int subsample, int n,
-                    const double *sph, int normalization,
-                    unsigned long long *counts, cudaStream_t s);
+// sphere RHS (mg_kernels.cu): covered sub-cell counts of the whole domain
+// (any grid of level 0), then the density of grid g's covered cells, each
+// cell written once in ascending sphere order (deterministic)
+void launch_sphere_counts(const Grid &g, double h, int subsample, int n,
+                          const double *sph, unsigned long long *counts,
+                          cudaStream_t s);
+void launch_sphere_scatter(const Grid &g, double h, int subsample, int n,
+                           const double *sph, int normalization,
+                           const unsigned long long *counts, cudaStream_t s);
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);
 // plane-marching TMA half-sweep (mg_march.cu)
@@ -192,6 +201,7 @@ bool make_tmap_resid(const Grid &g, const double *base, void *out128);
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
                                  const void *tmB, cudaStream_t s);
 int norm_march_blocks(const Grid &g);
+int march_blocks_max(const Grid &g);
 // split norm of a cycle's end: the last black half-sweep with the black
 // residuals' partials, then the red residuals' partials (12 B/cell); both
 // return their partial counts
@@ -208,29 +218,6 @@ void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s);
 bool encode_box(const Grid &g, const double *base, void *out128, unsigned box0,
                 unsigned box1);
-// fused last black half-sweep + residual epilogue (mg_fused.cu)
-bool fused_supported(const Grid &g);
-bool make_tmap_red12(const Grid &g, const double *base, void *out128);
-void launch_black_restrict(const Grid &g, const Grid &c, const void *tm_red12,
-                           cudaStream_t s);
-int launch_black_norm(const Grid &g, const void *tm_red12, double *partials,
-                      cudaStream_t s);
-// temporally blocked V(2,2) smoothing pass (mg_t4.cu): 4 half-sweeps
-// (red, black, red, black) in one kernel; reads black from the array of
-// tm256 (two tensor maps: 8- and 16-row tiles), writes red to g.phiR and the
-// final black to g.phiB.  prolong: first add alpha * e(parent) to the input
-// black; from_zero: the input black is 0 (first pre-smoothing on a coarse
-// level).  ty: tile rows (8 or 16).
-bool sweep4_supported(const Grid &g);
-bool make_tmap_sweep4(const Grid &g, const double *base, void *out256);
-void launch_sweep4(const Grid &g, const Grid &c, const void *tm256, bool prolong,
-                   bool from_zero, double alpha, int ty, cudaStream_t s);
-// one full RBGS sweep (red then black) per kernel (mg_sweep2.cu): black read
-// through tm_in128 (box 136 x 12), red written to g.phiR, black to bout
-bool sweep2_supported(const Grid &g);
-bool make_tmap_sweep2(const Grid &g, const double *base, void *out128);
-void launch_sweep2(const Grid &g, const Grid &c, const void *tm_in128, double *bout,
-                   bool prolong, bool from_zero, double alpha, cudaStream_t s);
 // per-face-cell boundary conditions (mg_set_bc_patch); null = face-uniform.
 // Face q cell (a, b): q<2 -> (j, z), q<4 -> (i, z), else (i, j); index a*nb+b
 struct FaceBC {

@@ -243,8 +243,6 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
   return v;
 }
 
-static constexpr int kNormBlocks = 148 * 8;
-
 // residual of the two cells of colour `col` at half-indices k, k+1 of row
 // (il, j): same expression as resid_at, vectorised along the row
 template <bool PER>
@@ -315,7 +313,7 @@ __global__ void __launch_bounds__(kThreads)
 int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * ((g.nzh + 1) >> 1);
   long long nb = (total + kThreads - 1) / kThreads;
-  if (nb > kNormBlocks) nb = kNormBlocks;
+  if (nb > norm_blocks_max(g)) nb = norm_blocks_max(g);
   if (nb < 1) nb = 1;
   if (is_periodic(g))
     k_norm_partials<true><<<(unsigned)nb, kThreads, 0, s>>>(g, partials);
@@ -535,24 +533,32 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
 
 // ---------------------------------------------------------------------------
 // RHS from charged spheres (centre rule P:273, inclusive c13;
-// subsampling P:485-489; periodic images P:441-443).  One CTA per sphere:
-// count the covered sub-cells of the whole (global) domain over all images,
-// then add rho_p to the covered cells of this slab.  The inside tests use
-// per-axis tables of squared distances (mg_sphere.cuh, bitwise the direct
-// test).  sph holds (cx, cy, cz, R, Q) per sphere.  f must be zero
-// beforehand; non-overlapping spheres give 0 + rho exactly, as the oracle.
+// subsampling P:485-489; periodic images P:441-443).  Two kernels, one CTA
+// per sphere each:
+//   k_sphere_count    n_p = covered sub-cells of the whole (global) domain
+//                     over all images (per-axis tables, mg_sphere.cuh)
+//   k_sphere_scatter  the density of the covered cells of this slab.  A cell
+//                     covered by several spheres is written once, by the
+//                     lowest-index one, as ((0 + rho_p1) + rho_p2) + ... in
+//                     ascending sphere order -- the oracle's "overlapping
+//                     spheres add in sphere order" exactly, and deterministic
+//                     (no atomics).  The other spheres that can reach a cell
+//                     of sphere p are found first by a conservative distance
+//                     test against every sphere (ascending list in shared
+//                     memory; beyond kNbMax entries every cell scans all
+//                     spheres instead -- slow, still exact).
+// sph holds (cx, cy, cz, R, Q) per sphere.  Every cell not covered keeps the
+// value it has (the caller zeroes f first).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads)
-    k_spheres(Grid g, double h, int s, const double *sph, int normalization,
-              unsigned long long *counts) {
+    k_sphere_count(Grid g, double h, int s, const double *sph,
+                   unsigned long long *counts) {
   __shared__ double sh[32];
   __shared__ sph::Tab tab;
-  __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
   const int p = blockIdx.x;
-  const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
+  const double R = sph[5 * p + 3];
   const double R2 = R * R;
   const double hs = h / (double)s;
-  const int s3 = s * s * s;
   double img[27][3];
   const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
   // threads own (j, k) columns of the box and walk along x: no per-cell
@@ -573,17 +579,107 @@ __global__ void __launch_bounds__(kThreads)
   }
   const double np = block_sum((double)cnt, sh);
   if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
-  if (normalization != 1 && np == 0.0) return;
-  const double rho0 = Q / ((4.0 / 3.0) * kPi * (R * R * R));
-  // the oracle's expressions: (Q cnt)/(n_p h^3) or rho0 (cnt / s^3), per
-  // possible count (tabulated when s^3 < kVal)
-  auto value = [&](int c) {
-    return (normalization == 1) ? rho0 * ((double)c / (double)s3)
-                                : (Q * (double)c) / (np * (h * h * h));
-  };
+}
+
+static constexpr int kNbMax = 128;  // neighbour list entries per sphere
+
+// can spheres a and b cover a common sub-cell centre?  Conservative: per
+// axis the (minimum-image on periodic axes) centre distance <= Ra + Rb + 2h
+__device__ __forceinline__ bool spheres_near(const Grid &g, double h, const double *a,
+                                             const double *b) {
+  const int ext[3] = {g.nx, g.ny, g.nz};
+  const double lim = a[3] + b[3] + 2.0 * h;
+#pragma unroll
+  for (int ax = 0; ax < 3; ax++) {
+    double d = fabs(b[ax] - a[ax]);
+    if (g.per[ax]) {
+      const double L = (double)ext[ax] * h;
+      if (d > 0.5 * L) d = L - d;
+    }
+    if (d > lim) return false;
+  }
+  return true;
+}
+
+// covered sub-cell centres of cell (i,j,k) by sphere q: the image nearest to
+// the cell on periodic axes (the oracle's image coordinate c + m (n h); the
+// images of one sphere reach disjoint cells, so at most this one covers it)
+__device__ __forceinline__ int cover_count(const Grid &g, double h, int s, double hs,
+                                           const double *q, int i, int j, int k) {
+  const int ext[3] = {g.nx, g.ny, g.nz};
+  const int ic[3] = {i, j, k};
+  double c[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ax++) {
+    const double x = ((double)ic[ax] + 0.5) * h;
+    double best = q[ax];
+    if (g.per[ax]) {
+      const double L = (double)ext[ax] * h;
+      const double lo = q[ax] + -1.0 * L, hi = q[ax] + 1.0 * L;
+      if (fabs(x - lo) < fabs(x - best)) best = lo;
+      if (fabs(x - hi) < fabs(x - best)) best = hi;
+    }
+    if (fabs(x - best) > q[3] + h) return 0;  // no sub-centre within R
+    c[ax] = best;
+  }
+  return sph::sub_count(i, j, k, s, hs, c[0], c[1], c[2], q[3]);
+}
+
+// the oracle's cell value of sphere q for `cnt` covered sub-cells
+__device__ __forceinline__ double sphere_value(const double *q, double np, int cnt,
+                                               int s3, double h, int normalization) {
+  if (normalization == 1) {
+    const double R = q[3];
+    const double rho0 = q[4] / ((4.0 / 3.0) * kPi * (R * R * R));
+    return rho0 * ((double)cnt / (double)s3);
+  }
+  return (q[4] * (double)cnt) / (np * (h * h * h));
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_sphere_scatter(Grid g, double h, int s, int n, const double *sph,
+                     int normalization, const unsigned long long *counts) {
+  __shared__ sph::Tab tab;
+  __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
+  __shared__ int nbl[kNbMax];
+  __shared__ int wcnt[kThreads / 32];
+  __shared__ int nbn;
+  const int p = blockIdx.x;
+  const double *me = sph + 5 * p;
+  const double R = me[3];
+  const double R2 = R * R;
+  const double hs = h / (double)s;
+  const int s3 = s * s * s;
+  const double np = (double)counts[p];
+  if (normalization != 1 && np == 0.0) return;  // covers nothing
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // spheres that may share a cell with p, ascending
+  if (threadIdx.x == 0) nbn = 0;
+  __syncthreads();
+  for (int base = 0; base < n; base += blockDim.x) {
+    const int q = base + threadIdx.x;
+    const bool hit = q < n && q != p && spheres_near(g, h, me, sph + 5 * q);
+    const unsigned bal = __ballot_sync(0xffffffffu, hit);
+    if (lane == 0) wcnt[warp] = __popc(bal);
+    __syncthreads();
+    int off = nbn;
+    for (int w = 0; w < warp; w++) off += wcnt[w];
+    off += __popc(bal & ((1u << lane) - 1u));
+    if (hit && off < kNbMax) nbl[off] = q;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int w = 0; w < (int)(blockDim.x >> 5); w++) nbn += wcnt[w];
+    __syncthreads();
+  }
+  const int nn = nbn;
+  const bool scan_all = nn > kNbMax;  // list overflow: every sphere per cell
+  const int ntry = scan_all ? n : nn;
   const bool vtab = s3 < sph::kVal;
   if (vtab)
-    for (int c = threadIdx.x; c <= s3; c += blockDim.x) vt[c] = value(c);
+    for (int c = threadIdx.x; c <= s3; c += blockDim.x)
+      vt[c] = sphere_value(me, np, c, s3, h, normalization);
+  double img[27][3];
+  const int nimg = sph::images(g, h, me[0], me[1], me[2], img);
   for (int m = 0; m < nimg; m++) {
     sph::Box bx = sph::box_of(g, h, img[m], R);
     // this slab's planes of the box
@@ -600,20 +696,51 @@ __global__ void __launch_bounds__(kThreads)
                          : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
                                           img[m][2], R);
         if (!c) continue;
-        const double v = vtab ? vt[c] : value(c);
+        // the lowest-index covering sphere writes the cell
+        bool mine = true;
+        int t = 0;
+        for (; t < ntry; t++) {
+          const int q = scan_all ? t : nbl[t];
+          if (q >= p) break;
+          if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
+          const double *sq = sph + 5 * q;
+          if (normalization != 1 && counts[q] == 0ull) continue;
+          if (cover_count(g, h, s, hs, sq, i, j, k)) {
+            mine = false;
+            break;
+          }
+        }
+        if (!mine) continue;
+        double v = 0.0;
+        v = v + (vtab ? vt[c] : sphere_value(me, np, c, s3, h, normalization));
+        for (; t < ntry; t++) {
+          const int q = scan_all ? t : nbl[t];
+          if (q == p) continue;
+          if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
+          const double *sq = sph + 5 * q;
+          const double nq = (double)counts[q];
+          if (normalization != 1 && nq == 0.0) continue;
+          const int cq = cover_count(g, h, s, hs, sq, i, j, k);
+          if (cq) v = v + sphere_value(sq, nq, cq, s3, h, normalization);
+        }
         const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
-        double *f = ((i + j + k) & 1) ? g.fB : g.fR;
-        atomicAdd(f + idx, v);
+        (((i + j + k) & 1) ? g.fB : g.fR)[idx] = v;
       }
     }
   }
 }
 
-void launch_spheres(const Grid &g, double h, int s, int n, const double *sph,
-                    int normalization, unsigned long long *counts,
-                    cudaStream_t st) {
+void launch_sphere_counts(const Grid &g, double h, int s, int n, const double *sph,
+                          unsigned long long *counts, cudaStream_t st) {
   if (n <= 0) return;
-  k_spheres<<<n, kThreads, 0, st>>>(g, h, s, sph, normalization, counts);
+  k_sphere_count<<<n, kThreads, 0, st>>>(g, h, s, sph, counts);
+}
+
+void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *sph,
+                           int normalization, const unsigned long long *counts,
+                           cudaStream_t st) {
+  if (n <= 0) return;
+  k_sphere_scatter<<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts);
 }
 
 // ---------------------------------------------------------------------------

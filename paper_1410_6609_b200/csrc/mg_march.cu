@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
   const unsigned box_bytes = (unsigned)((kTY + 2) * pz * 8);
 
   const int nrt = (g.ny + kTY - 1) / kTY;
-  const int ich = chunk_planes(g.nxl, nrt);
+  const int ich = chunk_planes(g.nxl, nrt, g.nsm);
   const int rt = blockIdx.x % nrt;
   const int xc = blockIdx.x / nrt;
   const int j0 = rt * kTY;
@@ -365,7 +365,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   b /= nzt;
   const int rt = b % nrt;
   const int xc = b / nrt;
-  const int ich = chunk_planes(g.nxl, nrt * nzt);
+  const int ich = chunk_planes(g.nxl, nrt * nzt, g.nsm);
   const int kz0 = zt * kZT;
   const int c0z = rtile_c0(g, kz0);
   const int zoff = kz0 - c0z;  // smem column of half-index kz0
@@ -713,7 +713,7 @@ static void set_smem(K kernel, size_t bytes, size_t *configured) {
 
 static int smooth_blocks(const Grid &g) {
   const int nrt = (g.ny + kTY - 1) / kTY;
-  const int ich = chunk_planes(g.nxl, nrt);
+  const int ich = chunk_planes(g.nxl, nrt, g.nsm);
   return nrt * ((g.nxl + ich - 1) / ich);
 }
 
@@ -783,7 +783,7 @@ void launch_prolong_smooth_march(const Grid &g, const Grid &c,
 static int resid_blocks(const Grid &g) {
   const int nzt = rntiles(g);
   const int nrt = (g.ny + kTY - 1) / kTY;
-  const int ich = chunk_planes(g.nxl, nrt * nzt);
+  const int ich = chunk_planes(g.nxl, nrt * nzt, g.nsm);
   const int nxc = (g.nxl + ich - 1) / ich;
   return nzt * nrt * nxc;
 }
@@ -813,6 +813,13 @@ void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
 }
 
 int norm_march_blocks(const Grid &g) { return resid_blocks(g); }
+
+// CTA count of the marching kernels for any SM count (x-chunks of 2 planes,
+// the shortest chunk_planes picks): sizes the partial-sum buffers without a
+// device query
+int march_blocks_max(const Grid &g) {
+  return rntiles(g) * ((g.ny + kTY - 1) / kTY) * ((g.nxl + 1) / 2);
+}
 
 int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
                           double *partials, cudaStream_t s) {

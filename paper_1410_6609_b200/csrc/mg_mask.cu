@@ -562,8 +562,6 @@ void launch_prolong_var(const Grid &f, const Grid &c, double alpha, cudaStream_t
 }
 
 // ---- residual norm partials -------------------------------------------------------
-static constexpr int kNormBlocksV = 148 * 8;
-
 __global__ void __launch_bounds__(kT) k_norm_var(Grid g, double *partials) {
   __shared__ double sh[32];
   const long long total = (long long)g.nxl * g.ny * g.nz;
@@ -584,7 +582,7 @@ __global__ void __launch_bounds__(kT) k_norm_var(Grid g, double *partials) {
 int launch_norm_partials_var(const Grid &g, double *partials, cudaStream_t s) {
   const long long total = (long long)g.nxl * g.ny * g.nz;
   long long nb = (total + kT - 1) / kT;
-  if (nb > kNormBlocksV) nb = kNormBlocksV;
+  if (nb > norm_blocks_max(g)) nb = norm_blocks_max(g);
   if (nb < 1) nb = 1;
   k_norm_var<<<(unsigned)nb, kT, 0, s>>>(g, partials);
   return (int)nb;

@@ -1,5 +1,5 @@
-// Shared device helpers of the plane-marching TMA kernels (mg_march.cu,
-// mg_fused.cu): mbarrier / TMA PTX wrappers, tile geometry.
+// Shared device helpers of the plane-marching TMA kernels (mg_march.cu):
+// mbarrier / TMA PTX wrappers, tile geometry.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -132,10 +132,11 @@ __host__ __device__ inline int rslot_doubles() {
 }
 
 // x-chunk length: 16 planes, halved (down to 2, even for the restriction
-// pairs) while the grid would have fewer than ~8 CTAs per SM
-__host__ __device__ inline int chunk_planes(int nxl, int tiles_per_plane_set) {
+// pairs) while the grid would have fewer than ~8 CTAs per SM (nsm: the
+// device's SM count)
+__host__ __device__ inline int chunk_planes(int nxl, int tiles_per_plane_set, int nsm) {
   int ich = kICH;
-  while (ich > 2 && (long long)((nxl + ich - 1) / ich) * tiles_per_plane_set < 148 * 8)
+  while (ich > 2 && (long long)((nxl + ich - 1) / ich) * tiles_per_plane_set < nsm * 8)
     ich >>= 1;
   return ich;
 }

@@ -30,7 +30,6 @@ MG_ERR_NOTCONV = -8
 MG_DIRICHLET = 0
 MG_NEUMANN = 1
 MG_PERIODIC = 2
-MG_PERIODIC = 2
 MG_HOST = 0
 MG_DEVICE = 1
 MG_CHARGE_PER_CELLS = 0
@@ -40,6 +39,11 @@ MG_FIELD_RHS = 1
 MG_HALO_NONE = 0
 MG_HALO_NCCL = 1
 MG_HALO_LOOPBACK = 2
+# mg_opts.disable bits / mg_cycle_paths bits (include/mg.h)
+MG_OFF_MARCH, MG_OFF_OVERLAP, MG_OFF_SPLIT_NORM = 1, 2, 4
+MG_OFF_CG_CLUSTER, MG_OFF_MASK_CODES = 8, 16
+MG_PATH_MARCH, MG_PATH_OVERLAP, MG_PATH_SPLIT_NORM, MG_PATH_CG_CLUSTER = 1, 2, 4, 8
+MG_PATH_CG_VAR, MG_PATH_PROLONG_FUSED, MG_PATH_FUSED_NORM = 16, 32, 64
 
 _HALO = {"none": MG_HALO_NONE, "nccl": MG_HALO_NCCL, "loopback": MG_HALO_LOOPBACK}
 
@@ -66,7 +70,8 @@ class mg_opts(ctypes.Structure):
                 ("nccl_id", ctypes.c_ubyte * 128),
                 ("workspace", ctypes.c_void_p),
                 ("workspace_bytes", ctypes.c_size_t),
-                ("use_graph", ctypes.c_int), ("fused_norm", ctypes.c_int)]
+                ("use_graph", ctypes.c_int), ("fused_norm", ctypes.c_int),
+                ("disable", ctypes.c_int)]
 
 
 _lib = None
@@ -135,6 +140,7 @@ def lib():
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
         L.mg_last_cycle_times_ex.argtypes = [P, ctypes.c_double * 10, i]
         L.mg_cycle_launches.argtypes = [P]
+        L.mg_cycle_paths.argtypes = [P]
         L.mg_stream.argtypes = [P]
         L.mg_stream.restype = ctypes.c_void_p
         _lib = L
@@ -172,7 +178,7 @@ def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
               agglomerate_below=64 ** 3, coarse_tol=1e-12, coarse_maxit=1000,
               max_cycles=100, device=0, rank=0, nranks=1, halo="none",
               nccl_id: Optional[bytes] = None, use_graph=True,
-              fused_norm=False) -> mg_opts:
+              fused_norm=False, disable=0) -> mg_opts:
     o = default_opts()
     o.nu1, o.nu2, o.alpha = nu1, nu2, alpha
     o.min_coarse, o.max_levels = min_coarse, max_levels
@@ -184,6 +190,7 @@ def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
         ctypes.memmove(o.nccl_id, bytes(nccl_id), 128)
     o.use_graph = 1 if use_graph else 0
     o.fused_norm = 1 if fused_norm else 0  # reading c11 (include/mg.h)
+    o.disable = int(disable)  # MG_OFF_* bits
     return o
 
 
@@ -237,6 +244,10 @@ class Multigrid:
                             for t, v in zip(bc_type, bc_value)])
         self.shape = tuple(int(s) for s in shape)
         o = make_opts(device=device, **kw)
+        self._plan_kw = {k: v for k, v in kw.items()
+                         if k in ("min_coarse", "max_levels", "agglomerate_below",
+                                  "nranks", "rank", "halo")}
+        self._plan = None
         self._stream = stream  # a torch.cuda.Stream kept alive while in use
         if stream is not None:
             o.stream = stream.cuda_stream
@@ -283,24 +294,32 @@ class Multigrid:
 
     def local_shape(self, level: int = 0):
         """Shape of the arrays exchanged for `level` (the slab for NCCL)."""
-        dims, lnx, agg = plan(self.level_dims(0), nranks=self.nranks,
-                              halo=self.halo)
-        d = self.level_dims(level)
+        if self._plan is None:
+            self._plan = plan(self.shape, **self._plan_kw)
+        dims, lnx, agg = self._plan
+        d = dims[level]
         if self.nranks > 1 and self.halo == MG_HALO_NCCL and level < agg:
             return (lnx[level], d[1], d[2])
         return d
 
     # -- data movement (host numpy arrays or torch CUDA tensors) -------------
-    def _io_args(self, a):
+    def _io_args(self, a, level=0):
+        """Pointer and MG_HOST / MG_DEVICE of a natural-layout buffer of
+        `level` (the library copies prod(local_shape(level)) doubles)."""
         torch = self._torch
+        n = int(np.prod(self.local_shape(level)))
         if isinstance(a, torch.Tensor):
             assert a.dtype == torch.float64 and a.is_contiguous()
+            if a.numel() != n:
+                raise MGError(MG_ERR_ARG, "buffer of %d values, need %d" % (a.numel(), n))
             if a.is_cuda:
                 torch.cuda.current_stream(a.device).synchronize()
                 return a.data_ptr(), MG_DEVICE
             return a.data_ptr(), MG_HOST
         assert isinstance(a, np.ndarray) and a.dtype == np.float64 \
             and a.flags["C_CONTIGUOUS"]
+        if a.size != n:
+            raise MGError(MG_ERR_ARG, "buffer of %d values, need %d" % (a.size, n))
         return _host_ptr(a), MG_HOST
 
     def set_rhs(self, f):
@@ -353,12 +372,23 @@ class Multigrid:
         return r.value
 
     def _io_args_nosync(self, a):
+        """Pointer of a level-0 slab buffer for the asynchronous calls: the
+        library copies prod(local_shape(0)) doubles through it, so the size
+        is checked here (an undersized buffer would be read or written out
+        of bounds long after the call returned)."""
+        if a is None:
+            return None, MG_HOST
         torch = self._torch
+        n = int(np.prod(self.local_shape(0)))
         if isinstance(a, torch.Tensor):
             assert a.dtype == torch.float64 and a.is_contiguous()
+            if a.numel() != n:
+                raise MGError(MG_ERR_ARG, "buffer of %d values, need %d" % (a.numel(), n))
             return a.data_ptr(), (MG_DEVICE if a.is_cuda else MG_HOST)
         assert isinstance(a, np.ndarray) and a.dtype == np.float64 \
             and a.flags["C_CONTIGUOUS"]
+        if a.size != n:
+            raise MGError(MG_ERR_ARG, "buffer of %d values, need %d" % (a.size, n))
         return _host_ptr(a), MG_HOST
 
     def timestep(self, centers, radii, charges, cycles=1, abs_tol=0.0,
@@ -401,12 +431,12 @@ class Multigrid:
     def get_field(self, level, field, out=None):
         if out is None:
             out = np.empty(self.local_shape(level), np.float64)
-        ptr, where = self._io_args(out)
+        ptr, where = self._io_args(out, level)
         _check(lib().mg_get_field(self._ctx, level, field, ptr, where), self._ctx)
         return out
 
     def set_field(self, level, field, a):
-        ptr, where = self._io_args(a)
+        ptr, where = self._io_args(a, level)
         _check(lib().mg_set_field(self._ctx, level, field, ptr, where), self._ctx)
 
     def set_mask(self, solid):
@@ -496,6 +526,11 @@ class Multigrid:
     @property
     def cycle_launches(self) -> int:
         return lib().mg_cycle_launches(self._ctx)
+
+    @property
+    def cycle_paths(self) -> int:
+        """MG_PATH_* bits of the kernel paths the last recorded cycle took."""
+        return lib().mg_cycle_paths(self._ctx)
 
     @property
     def stream_ptr(self) -> int:

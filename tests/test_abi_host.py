@@ -121,9 +121,8 @@ def test_plan_errors():
 
 
 def test_workspace_bytes_model():
-    """Split layout: 4 fields per level (the opt-in temporally blocked
-    passes, MG_T4=1, add a second black array), ghost planes/rows, pitch
-    nz/2 -> x4."""
+    """Split layout: 4 fields per level, ghost planes/rows, pitch
+    nz/2 -> x4; no device query (the same bytes on any SM count)."""
     nb = mg.workspace_bytes((512, 512, 512), min_coarse=8)
     fine = 4 * 514 * 514 * 256 * 8
     assert fine < nb < fine * 1.2
@@ -132,6 +131,19 @@ def test_workspace_bytes_model():
     slab = 4 * 514 * 514 * 256 * 8
     assert slab < nb2 < slab * 1.2
     assert mg.workspace_bytes((7, 8, 8)) == 0
+
+
+def test_opts_struct_matches_header():
+    """The ctypes mirror of mg_opts ends with the fields mg.h declares last,
+    and the MG_OFF_* / MG_PATH_* bits equal the header's."""
+    src = open(os.path.join(ROOT, "include", "mg.h")).read()
+    body = src[src.index("typedef struct {\n  int nu1"):src.index("} mg_opts;")]
+    body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
+    fields = re.findall(r"(\w+)(?:\[\d+\])?;", body)
+    names = [n for n, _ in mg.mg_opts._fields_]
+    assert fields[-3:] == names[-3:] == ["use_graph", "fused_norm", "disable"]
+    for m in re.finditer(r"#define (MG_(?:OFF|PATH)_\w+) (\d+)", src):
+        assert getattr(mg, m.group(1)) == int(m.group(2)), m.group(1)
 
 
 def test_nccl_unique_id_on_cpu():

@@ -164,6 +164,62 @@ def test_sphere_rhs_bitwise(mg, norm, sub):
     assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
 
 
+def overlapping_spheres(L):
+    """Clusters of 3-6 spheres around common centres (cells covered by up
+    to 6 spheres), charges of mixed sign and magnitude so that the order of
+    the additions changes the rounded sums."""
+    rng = np.random.default_rng(31)
+    c, R, q = [], [], []
+    for base in ([0.3, 0.5, 0.5], [0.7, 0.4, 0.6], [0.5, 0.8, 0.3]):
+        for m in range(3 + len(c) % 4):
+            c.append(np.array(base) * L + rng.uniform(-1.5, 1.5, 3))
+            R.append(rng.uniform(3.0, 5.0))
+            q.append(rng.choice([-1, 1]) * 10.0 ** rng.uniform(-3, 1))
+    # interleave the clusters so that covering spheres are not consecutive
+    order = rng.permutation(len(c))
+    return np.array(c)[order], np.array(R)[order], np.array(q)[order]
+
+
+@pytest.mark.parametrize("norm", [0, 1])
+@pytest.mark.parametrize("sub", [1, 2])
+@pytest.mark.parametrize("P", [1, 2])
+def test_sphere_rhs_overlapping_bitwise(mg, norm, sub, P):
+    """Cells covered by 3 or more spheres: the GPU adds the densities in
+    sphere order, like the oracle ("overlapping spheres add in sphere
+    order"), so f is bitwise equal and run-to-run deterministic (P:480-489);
+    also on loopback slabs."""
+    shape = (48, 32, 40)
+    c, R, q = overlapping_spheres(np.array(shape, float))
+    kw = dict(nranks=P, halo="loopback", agglomerate_below=64) if P > 1 else {}
+    s, o = pair(mg, shape, 1.0, "channel", min_coarse=4, **kw)
+    o.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+    ref = o.rhs(0)
+    cover = sum((oracle.sphere_density(shape, 1.0, c[p:p + 1], R[p:p + 1], [1.0],
+                                       normalization=1) != 0).astype(int)
+                for p in range(len(R)))
+    assert cover.max() >= 4
+    for _ in range(2):
+        s.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+        assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), ref)
+
+
+def test_sphere_rhs_overlapping_periodic(mg):
+    """Overlapping spheres whose periodic images wrap (x and z periodic)."""
+    shape = (32, 24, 40)
+    bt = [2, 2, D, D, 2, 2]
+    bv = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+    c = np.array([[0.4, 12.0, 1.0], [1.5, 11.0, 39.5], [31.0, 12.5, 0.5],
+                  [0.9, 12.2, 38.8], [2.0, 13.0, 2.5]])
+    R = np.array([4.0, 3.5, 4.5, 3.0, 4.2])
+    q = np.array([1.0, -0.37, 2.9e-2, 5.1, -1.3])
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=4)
+    o = oracle.Oracle(shape, 1.0, bt, bv, min_coarse=4)
+    for sub in (1, 3):
+        s.set_rhs_from_spheres(c, R, q, subsample=sub)
+        o.set_rhs_from_spheres(c, R, q, subsample=sub)
+        assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+
+
 def test_sphere_rhs_physical_units_and_errors(mg):
     shape, h = (32, 16, 24), 0.125
     c, q = W.random_spheres(np.array(shape) * h, 0.5, 6, seed=2)
@@ -198,27 +254,27 @@ def test_coarse_cg(mg):
     ((16, 16, 24), [2, 2, D, N, 2, 2], [0, 0, 0.5, -0.25, 0, 0]),  # x, z periodic
     ((40, 10, 22), [D] * 6, [1.0, -2.0, 0.5, 3.0, -1.0, 2.0]),   # ragged chunks
 ])
-def test_coarse_cg_cluster(mg, shape, bt, bv, monkeypatch):
+def test_coarse_cg_cluster(mg, shape, bt, bv):
     """The cluster CG (8 CTAs, distributed shared memory) on large coarsest
-    grids: the oracle's CG solution to 1e-11, iteration counts within 2 (the
-    dot products sum in another order), and the single-CTA kernel's
-    solution (MG_CG_CLUSTER=0) to 1e-12."""
+    grids and the single-CTA CG (mg_opts.disable = MG_OFF_CG_CLUSTER): both
+    the oracle's CG solution to 1e-11, iteration counts within 2 (the dot
+    products sum in another order); the paths taken are checked."""
     f = np.random.default_rng(9).uniform(-1, 1, shape)
     o = oracle.Oracle(shape, 1.0, bt, bv, max_levels=1)
     o.set_rhs_raw(f, 0)
     ito = o.cg(0, 1e-12, 1000)
     out = []
     for cluster in (True, False):
-        if not cluster:
-            monkeypatch.setenv("MG_CG_CLUSTER", "0")
-        s = mg.Multigrid(shape, 1.0, bt, bv, max_levels=1)
+        s = mg.Multigrid(shape, 1.0, bt, bv, max_levels=1,
+                         disable=0 if cluster else mg.MG_OFF_CG_CLUSTER)
         s.set_field(0, mg.MG_FIELD_RHS, f)
         it = s.coarse_solve()
+        assert bool(s.cycle_paths & mg.MG_PATH_CG_CLUSTER) == cluster
         out.append((it, s.get_field(0, mg.MG_FIELD_PHI)))
         s.close()
     assert abs(out[0][0] - ito) <= 2 and abs(out[1][0] - ito) <= 2
     assert rel(out[0][1], o.phi(0)) < 1e-11
-    assert rel(out[0][1], out[1][1]) < 1e-12
+    assert rel(out[1][1], o.phi(0)) < 1e-11
 
 
 def check_history(hg, ho):
@@ -358,22 +414,20 @@ def test_errors(mg):
                                       ((16, 16, 512), "dirichlet"),
                                       ((36, 20, 264), "channel"),
                                       ((128, 64, 128), "mixed")])
-@pytest.mark.parametrize("fused", [False, True])
-def test_march_kernels_equal_direct_kernels(mg, shape, bc, fused, monkeypatch):
+def test_march_kernels_equal_direct_kernels(mg, shape, bc):
     """The TMA-marching kernels (half-sweep, prolongation fused with the
-    first post-smoothing red sweep, residual+restriction, norm, and with
-    MG_FUSED=1 the last-black + residual epilogue kernels) give the same
-    V-cycle iterates as the direct-load kernels, bit for bit."""
+    first post-smoothing red sweep, residual+restriction, split norm) give
+    the same V-cycle iterates as the direct-load kernels (mg_opts.disable =
+    MG_OFF_MARCH), bit for bit."""
     f = np.random.default_rng(12).uniform(-1, 1, shape)
     out = []
-    if fused:
-        monkeypatch.setenv("MG_FUSED", "1")
     for no_march in (False, True):
-        if no_march:
-            monkeypatch.setenv("MG_NO_MARCH", "1")
-        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2)
+        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2,
+                    disable=mg.MG_OFF_MARCH if no_march else 0)
         s.set_rhs(f)
         r = [s.vcycle() for _ in range(3)]
+        march = mg.MG_PATH_MARCH | mg.MG_PATH_PROLONG_FUSED | mg.MG_PATH_SPLIT_NORM
+        assert (s.cycle_paths & march) == (0 if no_march else march), s.cycle_paths
         out.append((r, s.get_solution()))
     assert np.array_equal(out[0][1], out[1][1])
     assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
@@ -502,18 +556,18 @@ def test_config5_march_codes_parity(mg, scale):
 
 
 @pytest.mark.parametrize("codes", [True, False])
-def test_mask_march_equals_var_kernels(mg, codes, monkeypatch):
+def test_mask_march_equals_var_kernels(mg, codes):
     """Masked V-cycles: byte-code marching kernels == variable-coefficient
-    direct kernels, bit for bit (random mask: coarse levels not aligned)."""
+    direct kernels (MG_OFF_MARCH), bit for bit (random mask: coarse levels
+    not aligned)."""
     shape = (32, 16, 256)
     solid = random_mask(shape, 0.1, 7) if not codes else W.beam_mask(shape)
     f = np.random.default_rng(14).uniform(-1, 1, shape)
     out = []
     for no_march in (False, True):
-        if no_march:
-            monkeypatch.setenv("MG_NO_MARCH", "1")
         bt, bv = BCS["channel"]
-        s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=2, nu1=3, nu2=3)
+        s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=2, nu1=3, nu2=3,
+                         disable=mg.MG_OFF_MARCH if no_march else 0)
         s.set_mask(solid)
         s.set_rhs(f)
         r = [s.vcycle() for _ in range(3)]
@@ -795,67 +849,6 @@ def test_coulomb_force_homogeneous_field_table5(mg):
                     assert abs(e) < 0.08, (R, sF, sP, e)
 
 
-@pytest.mark.parametrize("shape,bc,h", [((256, 128, 128), "mixed", 1.0),
-                                        ((128, 64, 256), "channel", 0.5),
-                                        ((64, 96, 130), "dirichlet", 0.25)])
-def test_temporal_blocking_equals_half_sweeps(mg, shape, bc, h, monkeypatch):
-    """The temporally blocked V(2,2) passes (opt-in MG_T4=1: 4 half-sweeps
-    per kernel, its own reciprocal-based correctly rounded division) give the
-    same V-cycle iterates as the one-half-sweep-per-kernel path, bit for
-    bit."""
-    f = np.random.default_rng(21).uniform(-1, 1, shape)
-    out = []
-    for t4 in (True, False):
-        if t4:
-            monkeypatch.setenv("MG_T4", "1")
-        else:
-            monkeypatch.delenv("MG_T4")
-        s, _ = pair(mg, shape, h, bc, min_coarse=2)
-        s.set_rhs(f)
-        r = [s.vcycle() for _ in range(3)]
-        out.append((r, s.get_solution()))
-        s.close()
-    assert np.array_equal(out[0][1], out[1][1])
-    # norms: the cycle-end norm's partial sums follow the kernel path
-    assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
-
-
-@pytest.mark.parametrize("shape,bc,h", [((256, 128, 128), "mixed", 1.0),
-                                        ((128, 60, 300), "channel", 0.5),
-                                        ((68, 96, 132), "dirichlet", 0.25)])
-def test_full_sweep_kernels_equal_half_sweeps(mg, shape, bc, h, monkeypatch):
-    """The full-sweep kernels (opt-in MG_S2=1: red and black of one RBGS
-    sweep in one plane-marching kernel, red recomputed on the tile halo) give
-    the same V-cycle iterates as the one-half-sweep-per-kernel path, bit for
-    bit -- ragged row tiles (ny = 60), ragged z tiles (nz = 300, 130) and an
-    x extent that leaves a short last chunk included."""
-    f = np.random.default_rng(23).uniform(-1, 1, shape)
-    out = []
-    for s2 in (True, False):
-        if s2:
-            monkeypatch.setenv("MG_S2", "1")
-        else:
-            monkeypatch.delenv("MG_S2")
-        s, _ = pair(mg, shape, h, bc, min_coarse=2)
-        s.set_rhs(f)
-        s.set_profiling(True)
-        r = [s.vcycle() for _ in range(3)]
-        t = s.last_cycle_times()
-        s.set_profiling(False)
-        # level 0 smoothing launches outside the prolongation kernel: 4 + 3
-        # half-sweep kernels, or 2 + 1 full-sweep kernels
-        if s2:
-            assert t["smooth0_launches_ex"] == 3, t
-            assert t["smooth0_halfsweeps"] == 6, t
-        else:
-            assert t["smooth0_launches_ex"] == 7, t
-        out.append((r, s.get_solution()))
-        s.close()
-    assert np.array_equal(out[0][1], out[1][1])
-    # norms: the cycle-end norm's partial sums follow the kernel path
-    assert np.allclose(out[0][0], out[1][0], rtol=1e-13, atol=0)
-
-
 def test_get_solution_async_overlapped_steps(mg):
     """mg_get_solution_async: the copy-outs of five consecutive sphere steps
     (more than the three staging slots), each overlapping the next step's
@@ -944,41 +937,97 @@ def test_solve_async_pipelined_equals_sync(mg):
         assert np.array_equal(out2[k].numpy(), ref[k][1])
 
 
+def test_solve_async_slot_reuse_device_or_null_output(mg):
+    """Seven pipelined solves from pinned host RHS with device or NULL
+    outputs: the staging slot of problem k is rewritten by the upload of
+    problem k + 3 only after problem k's RHS conversion has read it (ADVICE
+    r1: with a NULL / device phi_out nothing else orders the two).  Each
+    device output and the last residual equal the synchronous solves."""
+    import torch
+    shape = (128, 64, 128)
+    bt, bv = BCS["channel"]
+    fs = [np.random.default_rng(60 + k).uniform(-1, 1, shape) for k in range(7)]
+    ref = []
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=2)
+    for f in fs:
+        s.zero_solution()
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(8)][-1]
+        ref.append((r, s.get_solution()))
+    s.close()
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=2)
+    fh = [torch.from_numpy(f).pin_memory() for f in fs]
+    outs = [torch.empty(shape, dtype=torch.float64, device="cuda")
+            if k % 2 == 0 or k == len(fs) - 1 else None for k in range(len(fs))]
+    for k in range(len(fs)):
+        s.solve_async(fh[k], outs[k], 8)
+    assert s.wait() == ref[-1][0]
+    for k, o in enumerate(outs):
+        if o is not None:
+            assert np.array_equal(o.cpu().numpy(), ref[k][1]), k
+    s.close()
+
+
+def test_async_buffer_size_checked(mg):
+    import torch
+    s = mg.Multigrid((16, 16, 16), 1.0, [D] * 6, min_coarse=2)
+    with pytest.raises(mg.MGError):
+        s.solve_async(torch.zeros(16 * 16 * 15, dtype=torch.float64).pin_memory(),
+                      None, 1)
+    with pytest.raises(mg.MGError):
+        s.get_solution_async(torch.zeros(10, dtype=torch.float64, device="cuda"))
+    with pytest.raises(mg.MGError):
+        s.get_field(1, mg.MG_FIELD_PHI, np.zeros((16, 16, 16)))
+    s.close()
+
+
 @pytest.mark.parametrize("P", [2, 4])
-def test_loopback_overlapped_exchange_equals_serial(mg, P, monkeypatch):
+def test_loopback_overlapped_exchange_equals_serial(mg, P):
     """Multi-slab half-sweeps with the ghost exchange overlapped (boundary
     planes first, exchange on the communication stream while the interior
-    planes are swept) give the serial-exchange iterates bit for bit."""
+    planes are swept) give the serial-exchange iterates (MG_OFF_OVERLAP) bit
+    for bit."""
     shape = (256, 64, 128)
     f = np.random.default_rng(44).uniform(-1, 1, shape)
     out = []
     for no_overlap in (False, True):
-        if no_overlap:
-            monkeypatch.setenv("MG_NO_OVERLAP", "1")
         s, _ = pair(mg, shape, 1.0, "channel", min_coarse=4, nranks=P,
-                    halo="loopback", agglomerate_below=4096)
+                    halo="loopback", agglomerate_below=4096,
+                    disable=mg.MG_OFF_OVERLAP if no_overlap else 0)
         s.set_rhs(f)
         r = [s.vcycle() for _ in range(3)]
+        assert bool(s.cycle_paths & mg.MG_PATH_OVERLAP) == (not no_overlap)
         out.append((r, s.get_solution()))
         s.close()
     assert np.array_equal(out[0][1], out[1][1])
     assert out[0][0] == out[1][0]
 
 
-@pytest.mark.parametrize("shape,bc", [((32, 24, 256), "mixed"), ((36, 20, 264), "channel"),
-                                      ((66, 34, 20), "mixed")])
-def test_split_cycle_end_norm(mg, shape, bc, monkeypatch):
+@pytest.mark.parametrize("shape,bc,P", [((32, 24, 256), "mixed", 1),
+                                        ((36, 20, 264), "channel", 1),
+                                        ((66, 34, 20), "mixed", 1),
+                                        ((64, 24, 256), "mixed", 2),
+                                        ((128, 16, 136), "channel", 4)])
+def test_split_cycle_end_norm(mg, shape, bc, P):
     """The cycle-end norm split between the last black half-sweep (black
     residuals) and a red-only residual pass equals the full residual pass on
     the same state to rounding (1e-13), and the iterates are those of the
-    unsplit cycle (MG_SPLIT_NORM=0) bit for bit."""
+    unsplit cycle (MG_OFF_SPLIT_NORM) bit for bit -- also on loopback slabs,
+    where the red residuals read the black ghosts exchanged after the last
+    black sweep."""
     f = np.random.default_rng(14).uniform(-1, 1, shape)
     out = []
+    kw = dict(nranks=P, halo="loopback", agglomerate_below=512) if P > 1 else {}
     for split in (True, False):
-        if not split:
-            monkeypatch.setenv("MG_SPLIT_NORM", "0")
-        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2)
+        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2,
+                    disable=0 if split else mg.MG_OFF_SPLIT_NORM, **kw)
         s.set_rhs(f)
+        s.vcycle()
+        # nzh < 64 grids have no marching kernels, hence no split
+        expect = split and shape[2] // 2 >= 64
+        assert bool(s.cycle_paths & mg.MG_PATH_SPLIT_NORM) == expect
+        s.set_rhs(f)
+        s.zero_solution()
         r = []
         for _ in range(3):
             r.append(s.vcycle())

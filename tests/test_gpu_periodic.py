@@ -198,13 +198,12 @@ def test_periodic_loopback_slabs_equal_single(mg, Pn):
 @pytest.mark.parametrize("shape,bc", [((32, 24, 256), "xy"),
                                       ((64, 16, 128), "chan"),
                                       ((36, 20, 264), "z")])
-def test_periodic_march_equals_direct(mg, shape, bc, monkeypatch):
+def test_periodic_march_equals_direct(mg, shape, bc):
     f = np.random.default_rng(26).uniform(-1, 1, shape)
     out = []
     for no_march in (False, True):
-        if no_march:
-            monkeypatch.setenv("MG_NO_MARCH", "1")
-        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2)
+        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2,
+                    disable=mg.MG_OFF_MARCH if no_march else 0)
         s.set_rhs(f)
         r = [s.vcycle() for _ in range(3)]
         out.append((r, s.get_solution()))
