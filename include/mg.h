@@ -27,7 +27,8 @@
  *    [r*nx/P, (r+1)*nx/P) of every distributed level; caller arrays are then
  *    the rank's slab (nx/P * ny * nz values).  With the LOOPBACK backend one
  *    process holds all P slabs on one GPU (used to test the decomposition)
- *    and caller arrays cover the whole domain.
+ *    and caller arrays cover the whole domain (likewise EMULATE, which also
+ *    keeps one copy of the agglomerated levels per emulated rank).
  *  - Pointers marked "where" are host pointers (MG_HOST, any host memory;
  *    pinned memory gives full PCIe bandwidth) or device pointers (MG_DEVICE).
  *    The library never keeps or frees caller pointers.
@@ -78,6 +79,12 @@ typedef struct {
 #define MG_HALO_NONE 0     /* single slab (nranks must be 1)                  */
 #define MG_HALO_NCCL 1     /* one process per GPU, NCCL send/recv over NVLink */
 #define MG_HALO_LOOPBACK 2 /* all nranks slabs in this process on one GPU     */
+#define MG_HALO_EMULATE 3  /* all nranks ranks in this process on one GPU with
+                              NCCL's data layout: one copy of every
+                              agglomerated level per rank, the halo schedule
+                              (mg_halo_schedule) and the all-gathers executed
+                              as device copies with NCCL's matching and
+                              indexing -- tests the NCCL layout on one GPU  */
 
 typedef struct {
   int nu1, nu2;       /* pre/post RBGS sweeps (default 2, 2)      */
@@ -115,6 +122,10 @@ typedef struct {
                          bitwise equal; only reductions may round
                          differently.  Which paths a recorded V-cycle took is
                          reported by mg_cycle_paths().                      */
+  int nccl_timeout_ms; /* NCCL contexts: a synchronising call that sees no
+                         progress for this long, or an asynchronous NCCL
+                         error, aborts the communicator and returns
+                         MG_ERR_NCCL (default 600000; 0 = wait forever)     */
 } mg_opts;
 
 /* mg_opts.disable bits */

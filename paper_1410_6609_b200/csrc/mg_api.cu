@@ -7,6 +7,9 @@
 //                    copy and computes it redundantly (agglomeration by
 //                    in-place all-gather of the restricted RHS, P:746 /
 //                    north_star "agglomerated onto one GPU" -- DESIGN.md).
+//                    LOOPBACK shares one copy among its slabs; EMULATE keeps
+//                    one copy per emulated rank, gathered by device copies
+//                    with NCCL's indexing (the NCCL data layout, one GPU).
 // With P == 1, nd = 0: every level is a single grid.
 //
 // The V-cycle is recorded once into a CUDA graph and replayed.
@@ -19,6 +22,10 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <nvtx3/nvToolsExt.h>
+#include <time.h>
+
+#include <chrono>
 #include <string>
 #include <vector>
 
@@ -28,6 +35,13 @@
 using mg::Grid;
 
 namespace {
+
+// NVTX range around a public call (SURVEY 5 tracing; header-only NVTX v3:
+// a no-op unless a profiler injects itself)
+struct Nvtx {
+  explicit Nvtx(const char *name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
 
 thread_local std::string g_err;
 thread_local int g_err_code = 0;
@@ -58,6 +72,8 @@ struct Nccl {
   ncclResult_t (*GroupStart)();
   ncclResult_t (*GroupEnd)();
   const char *(*GetErrorString)(ncclResult_t);
+  ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t *);
+  ncclResult_t (*CommAbort)(ncclComm_t);
 };
 Nccl g_nccl;
 
@@ -79,6 +95,8 @@ bool load_nccl() {
   SYM("ncclGroupStart", GroupStart);
   SYM("ncclGroupEnd", GroupEnd);
   SYM("ncclGetErrorString", GetErrorString);
+  SYM("ncclCommGetAsyncError", CommGetAsyncError);
+  SYM("ncclCommAbort", CommAbort);
 #undef SYM
   g_nccl.ok = true;
   return true;
@@ -182,7 +200,6 @@ struct mg_ctx {
   std::vector<std::vector<TmPair>> tm;
   // kernel paths (mg_opts.disable clears them; include/mg.h MG_OFF_*)
   int use_march = 1;  // TMA plane-marching kernels where the grid allows
-  int split_off = 0;  // split norm: partials written by the last black sweep
   // multi-slab overlap: boundary planes first, the ghost exchange on s_comm
   // while the interior planes are swept
   int overlap = 1;
@@ -190,6 +207,7 @@ struct mg_ctx {
   int nsm = 148;      // SMs of the device (cudaDevAttrMultiProcessorCount)
   cudaStream_t s_comm = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_sync = nullptr;  // NCCL contexts: polled by sync()
   std::vector<std::vector<Grid>> vlo, vhi, vin;   // per level, slab: views
   std::vector<std::vector<TmPair>> tmin;          // TMA maps of the interior views
   bool masked = false;            // variable coefficients (mask and/or patches)
@@ -207,6 +225,8 @@ struct mg_ctx {
   mg_opts o;
   int P = 1, rank = 0, backend = MG_HALO_NONE;
   int nslab = 1, slab0 = 0;  // slabs held on distributed levels
+  int ncopy = 1;             // copies of each agglomerated level (EMULATE: P)
+  std::vector<size_t> pbase; // norm partials of level-0 slab s at partials + pbase[s]
   std::vector<std::vector<Grid>> g;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
@@ -281,7 +301,7 @@ size_t carve(mg_ctx *c, char *base) {
   for (int q = 0; q < 6; q++)
     dface[q] = c->bc[q].type == MG_DIRICHLET ? 1 : (c->bc[q].type == MG_NEUMANN ? -1 : 0);
   for (int l = 0; l < L; l++) {
-    const int ns = l < c->pl.nd ? c->nslab : 1;
+    const int ns = l < c->pl.nd ? c->nslab : c->ncopy;
     for (int s = 0; s < ns; s++) {
       Grid gr = make_grid(c->pl, l, l < c->pl.nd ? c->slab0 + s : 0, c->h, dface);
       gr.nsm = c->nsm;
@@ -295,9 +315,12 @@ size_t carve(mg_ctx *c, char *base) {
       c->g[l].push_back(gr);
     }
   }
-  size_t npart = kMaxNormBlocks;
+  // one region of norm partials per level-0 slab: residual-kernel partials
+  // plus (split norm) the smoother's, or the grid-stride kernels' (fewer)
+  size_t npart = 0;
+  c->pbase.clear();
   for (const Grid &g : c->g[0]) {
-    // residual-kernel partials, plus (split norm) the smoother's, fewer
+    c->pbase.push_back(npart);
     const size_t nb = (size_t)mg::march_blocks_max(g);
     npart += 2 * (nb > (size_t)kMaxNormBlocks ? nb : (size_t)kMaxNormBlocks);
   }
@@ -342,8 +365,17 @@ void mark(mg_ctx *c, int cat) {
   c->nev++;
 }
 
+// the grid slab / copy s of level l restricts to and prolongs from: its
+// own slab on distributed levels, else the agglomerated level (EMULATE: the
+// copy of rank s)
 const Grid &coarse_of(const mg_ctx *c, int l, int s) {
-  return (l + 1 < c->pl.nd) ? c->g[l + 1][s] : c->g[l + 1][0];
+  return (l + 1 < c->pl.nd) ? c->g[l + 1][s] : c->g[l + 1][c->ncopy > 1 ? s : 0];
+}
+
+// grids of level l whose cells the caller's arrays hold: the slabs of a
+// distributed level, one copy of an agglomerated level
+size_t io_grids(const mg_ctx *c, int l) {
+  return l < c->pl.nd ? c->g[l].size() : 1;
 }
 
 bool periodic_x(const mg_ctx *c) { return c->bc[0].type == MG_PERIODIC; }
@@ -357,7 +389,8 @@ bool any_periodic(const mg_ctx *c) {
 // for the restriction (after pre-smoothing); one level has no restriction
 bool fused_norm_on(const mg_ctx *c) { return c->o.fused_norm && c->pl.L > 1; }
 int norm_partials(mg_ctx *c, size_t s, double *partials);
-int finish_norm(mg_ctx *c, int off);
+int finish_norm(mg_ctx *c, const int *cnt);
+constexpr int kMaxSlabs = 64;  // level-0 slabs held by one context
 
 // ghost-plane exchange of one colour array (0 phiR, 1 phiB) on level l.  On a
 // periodic x axis the first and last slabs are neighbours too (P:692-693:
@@ -384,6 +417,35 @@ int halo(mg_ctx *c, int l, int which, cudaStream_t st = nullptr) {
     }
     return MG_OK;
   }
+  auto plane_of = [](const Grid &g, int code) {
+    return code == MG_PLANE_FIRST ? 1
+           : code == MG_PLANE_LAST ? g.nxl
+           : code == MG_GHOST_LO   ? 0
+                                   : g.nxl + 1;
+  };
+  if (c->backend == MG_HALO_EMULATE) {
+    // every emulated rank's schedule executed as NCCL would match it: the
+    // k-th receive of rank r from peer q takes the k-th send of q to r
+    int ops[kMaxSlabs][4][3], nops[kMaxSlabs];
+    for (int r = 0; r < c->P; r++) nops[r] = mg_halo_schedule(c->P, r, wrap ? 1 : 0, ops[r]);
+    for (int r = 0; r < c->P; r++) {
+      for (int k = 0; k < nops[r]; k++) {
+        if (ops[r][k][0] != MG_OP_RECV) continue;
+        const int q = ops[r][k][1];
+        int nth = 0;
+        for (int m = 0; m < k; m++) nth += ops[r][m][0] == MG_OP_RECV && ops[r][m][1] == q;
+        int src = -1;
+        for (int m = 0, seen = 0; m < nops[q]; m++)
+          if (ops[q][m][0] == MG_OP_SEND && ops[q][m][1] == r && seen++ == nth) src = m;
+        if (src < 0) return fail(MG_ERR_NCCL, "halo schedule: unmatched receive");
+        const Grid &gr = c->g[l][r], &gq = c->g[l][q];
+        CK(cudaMemcpyAsync(arr(gr) + (long long)plane_of(gr, ops[r][k][2]) * gr.plane,
+                           arr(gq) + (long long)plane_of(gq, ops[q][src][2]) * gq.plane,
+                           sizeof(double) * gr.plane, cudaMemcpyDeviceToDevice, st));
+      }
+    }
+    return MG_OK;
+  }
   const Grid &g = c->g[l][0];
   double *A = arr(g);
   const size_t n = (size_t)g.plane;
@@ -392,17 +454,46 @@ int halo(mg_ctx *c, int l, int which, cudaStream_t st = nullptr) {
   int rc;
   if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
   for (int k = 0; k < nops; k++) {
-    const int pl = ops[k][2] == MG_PLANE_FIRST  ? 1
-                   : ops[k][2] == MG_PLANE_LAST ? g.nxl
-                   : ops[k][2] == MG_GHOST_LO   ? 0
-                                                : g.nxl + 1;
-    double *buf = A + (long long)pl * g.plane;
+    double *buf = A + (long long)plane_of(g, ops[k][2]) * g.plane;
     if (ops[k][0] == MG_OP_SEND)
       g_nccl.Send(buf, n, ncclDouble, ops[k][1], c->comm, st);
     else
       g_nccl.Recv(buf, n, ncclDouble, ops[k][1], c->comm, st);
   }
   return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(halo)");
+}
+
+// Agglomeration of level l (held whole): rank r computed the planes
+// [1 + r nx/P, 1 + (r+1) nx/P) of `narr` arrays (elements of `esize` bytes,
+// base(g, a) the array a of grid g); every rank receives the others'
+// portions.  NCCL: in-place all-gathers in one group; EMULATE: the same
+// byte ranges copied between the ranks' copies; LOOPBACK: nothing (one
+// shared copy).
+template <typename Base>
+int gather_portions(mg_ctx *c, int l, int narr, size_t esize, Base base) {
+  if (c->P == 1 || c->backend == MG_HALO_LOOPBACK) return MG_OK;
+  const Grid &G = c->g[l][0];
+  const size_t cnt = (size_t)(G.nx / c->P) * G.plane * esize;  // bytes per rank
+  const size_t first = (size_t)G.plane * esize;                  // ghost plane 0
+  if (c->backend == MG_HALO_EMULATE) {
+    for (int r = 0; r < c->P; r++)
+      for (int t = 0; t < c->P; t++) {
+        if (t == r) continue;
+        for (int a = 0; a < narr; a++) {
+          char *src = (char *)base(c->g[l][r], a) + first + r * cnt;
+          char *dst = (char *)base(c->g[l][t], a) + first + r * cnt;
+          CK(cudaMemcpyAsync(dst, src, cnt, cudaMemcpyDeviceToDevice, c->stream));
+        }
+      }
+    return MG_OK;
+  }
+  int rc;
+  if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
+  for (int a = 0; a < narr; a++) {
+    char *b = (char *)base(G, a) + first;
+    g_nccl.AllGather(b + c->rank * cnt, b, cnt, ncclChar, c->comm, c->stream);
+  }
+  return nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(agglomerate)");
 }
 
 // periodic ghost rows / planes of the grids of level l held here, for the
@@ -494,21 +585,22 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
 int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_NONE);
   const bool with_norm = l == 0 && fused_norm_on(c);
-  int off = 0;  // norm partials written so far (fused norm, reading c11)
+  int cnt[kMaxSlabs] = {0};  // norm partials per slab (fused norm, reading c11)
   for (int s = 0; s < (int)c->g[l].size(); s++) {
     const TmPair &t = c->tm[l][s];
     const bool march = t.ok_resid && c->use_march;
+    double *part = with_norm ? c->partials + c->pbase[s] : nullptr;
     if (with_norm && !(march && (!c->masked || c->g[l][s].codeR))) {
       // no fused kernel for this grid: the same residual's norm, one pass
-      off += norm_partials(c, s, c->partials + off);
+      cnt[s] = norm_partials(c, s, part);
       c->launches++;
     }
     if (c->masked && !(c->g[l][s].codeR && march)) {
       mg::launch_resid_restrict_var(c->g[l][s], coarse_of(c, l, s), c->stream);
     } else if (march) {
       if (with_norm)
-        off += mg::launch_resid_restrict_norm_march(c->g[l][s], coarse_of(c, l, s), t.rr,
-                                                    t.rb, c->partials + off, c->stream);
+        cnt[s] = mg::launch_resid_restrict_norm_march(c->g[l][s], coarse_of(c, l, s), t.rr,
+                                                      t.rb, part, c->stream);
       else
         mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
                                         c->stream);
@@ -520,20 +612,13 @@ int restrict_level(mg_ctx *c, int l) {
   if (l == 0) mark(c, CAT_RESTRICT0);
   CK(cudaGetLastError());
   if (with_norm) {
-    int rc = finish_norm(c, off);
+    int rc = finish_norm(c, cnt);
     if (rc) return rc;
   }
-  if (l + 1 == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
-    const Grid &G = c->g[l + 1][0];
-    const size_t cnt = (size_t)(G.nx / c->P) * G.plane;
-    int rc;
-    if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-    g_nccl.AllGather(G.fR + G.plane + c->rank * cnt, G.fR + G.plane, cnt,
-                     ncclDouble, c->comm, c->stream);
-    g_nccl.AllGather(G.fB + G.plane + c->rank * cnt, G.fB + G.plane, cnt,
-                     ncclDouble, c->comm, c->stream);
-    if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(agglomerate)"))) return rc;
-  }
+  if (l + 1 == c->pl.nd && c->P > 1)
+    return gather_portions(c, l + 1, 2, sizeof(double), [](const Grid &g, int a) {
+      return (void *)(a ? g.fB : g.fR);
+    });
   return MG_OK;
 }
 
@@ -583,20 +668,22 @@ int prolong_red_level(mg_ctx *c, int l) {
 bool cg_cluster_on(const mg_ctx *c) { return !(c->o.disable & MG_OFF_CG_CLUSTER); }
 
 int coarse_solve(mg_ctx *c) {
-  const Grid &g = c->g[c->pl.L - 1][0];
-  if (c->masked) {
-    mg::launch_coarse_cg_var(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
-                             c->cg_iters, c->stream);
-    c->paths |= MG_PATH_CG_VAR;
-  } else if (cg_cluster_on(c) && mg::coarse_cg_cluster_supported(g)) {
-    mg::launch_coarse_cg_cluster(g, c->o.coarse_tol, c->o.coarse_maxit, c->cg_iters,
-                                 c->stream);
-    c->paths |= MG_PATH_CG_CLUSTER;
-  } else {
-    mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
-                         c->cg_iters, c->stream);
+  // every copy of the coarsest level (EMULATE: one per rank, redundantly)
+  for (const Grid &g : c->g[c->pl.L - 1]) {
+    if (c->masked) {
+      mg::launch_coarse_cg_var(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
+                               c->cg_iters, c->stream);
+      c->paths |= MG_PATH_CG_VAR;
+    } else if (cg_cluster_on(c) && mg::coarse_cg_cluster_supported(g)) {
+      mg::launch_coarse_cg_cluster(g, c->o.coarse_tol, c->o.coarse_maxit, c->cg_iters,
+                                   c->stream);
+      c->paths |= MG_PATH_CG_CLUSTER;
+    } else {
+      mg::launch_coarse_cg(g, c->cg_scr, c->o.coarse_tol, c->o.coarse_maxit,
+                           c->cg_iters, c->stream);
+    }
+    c->launches++;
   }
-  c->launches++;
   periodic_fill(c, c->pl.L - 1);  // the prolongation reads coarse ghosts
   CK(cudaGetLastError());
   return MG_OK;
@@ -617,33 +704,42 @@ int norm_partials(mg_ctx *c, size_t s, double *partials) {
 }
 
 int enqueue_norm(mg_ctx *c) {
-  int off = 0;
+  int cnt[kMaxSlabs] = {0};
   mark(c, CAT_NONE);
   for (size_t s = 0; s < c->g[0].size(); s++) {
-    off += norm_partials(c, s, c->partials + off);
+    cnt[s] = norm_partials(c, s, c->partials + c->pbase[s]);
     c->launches++;
   }
-  return finish_norm(c, off);
+  return finish_norm(c, cnt);
 }
 
-// ordered sum of `off` partials (+ the rank-ordered all-gather), published to
-// the mapped host word
-int finish_norm(mg_ctx *c, int off) {
-  mg::launch_sum_ordered(c->partials, off, c->normv, c->stream);
-  c->launches++;
-  CK(cudaGetLastError());
-  if (c->P > 1 && c->backend == MG_HALO_NCCL) {
-    int rc = nccl_ck(g_nccl.AllGather(c->normv, c->normv + 2, 1, ncclDouble,
-                                      c->comm, c->stream),
-                     "ncclAllGather(norm)");
-    if (rc) return rc;
-    mg::launch_sum_ordered(c->normv + 2, c->P, c->normv + 1, c->stream);
-    c->launches++;
-    mg::launch_publish(c->normv + 1, c->normv + 1, c->h_norm_dev, c->stream);
-  } else {
+// ||r||^2 from the partials (cnt[s] of them for level-0 slab s, at
+// partials + pbase[s]), published to the mapped host word.  One slab: their
+// ordered sum.  P slabs / ranks: per slab (rank) the ordered sum into
+// normv[2 + rank], an in-place all-gather of the P values (NCCL), then their
+// sum in rank order -- the same roundings in every backend.
+int finish_norm(mg_ctx *c, const int *cnt) {
+  if (c->P == 1) {
+    mg::launch_sum_ordered(c->partials + c->pbase[0], cnt[0], c->normv, c->stream);
     mg::launch_publish(c->normv, c->normv + 1, c->h_norm_dev, c->stream);
+    c->launches += 2;
+  } else {
+    for (size_t s = 0; s < c->g[0].size(); s++) {
+      mg::launch_sum_ordered(c->partials + c->pbase[s], cnt[s],
+                             c->normv + 2 + c->slab0 + s, c->stream);
+      c->launches++;
+    }
+    CK(cudaGetLastError());
+    if (c->backend == MG_HALO_NCCL) {
+      int rc = nccl_ck(g_nccl.AllGather(c->normv + 2 + c->rank, c->normv + 2, 1,
+                                        ncclDouble, c->comm, c->stream),
+                       "ncclAllGather(norm)");
+      if (rc) return rc;
+    }
+    mg::launch_sum_ordered(c->normv + 2, c->P, c->normv + 1, c->stream);
+    mg::launch_publish(c->normv + 1, c->normv + 1, c->h_norm_dev, c->stream);
+    c->launches += 2;
   }
-  c->launches++;
   mark(c, CAT_NORM);
   CK(cudaGetLastError());
   return MG_OK;
@@ -670,26 +766,25 @@ bool split_norm_ok(const mg_ctx *c) {
 // partials, the ordered sum
 int split_norm_tail(mg_ctx *c) {
   mark(c, CAT_NONE);
-  int off = 0;
+  int cnt[kMaxSlabs] = {0};
   for (size_t s = 0; s < c->g[0].size(); s++) {
-    off += mg::launch_smooth_norm_march(c->g[0][s], c->tm[0][s].r, 1, c->partials + off,
-                                        c->stream);
+    cnt[s] = mg::launch_smooth_norm_march(c->g[0][s], c->tm[0][s].r, 1,
+                                          c->partials + c->pbase[s], c->stream);
     c->launches++;
   }
   mark(c, CAT_SMOOTH0);
   CK(cudaGetLastError());
   int rc;
   if ((rc = halo(c, 0, 1))) return rc;
-  c->split_off = off;
   mark(c, CAT_NONE);
   for (size_t s = 0; s < c->g[0].size(); s++) {
-    off += mg::launch_norm_red_march(c->g[0][s], c->tm[0][s].rr, c->tm[0][s].rb,
-                                     c->partials + off, c->stream);
+    cnt[s] += mg::launch_norm_red_march(c->g[0][s], c->tm[0][s].rr, c->tm[0][s].rb,
+                                        c->partials + c->pbase[s] + cnt[s], c->stream);
     c->launches++;
   }
   CK(cudaGetLastError());
   c->paths |= MG_PATH_SPLIT_NORM;
-  return finish_norm(c, off);
+  return finish_norm(c, cnt);
 }
 
 int enqueue_vcycle(mg_ctx *c) {
@@ -745,9 +840,43 @@ int enqueue_vcycle(mg_ctx *c) {
   return rc;
 }
 
+// Wait for the context's stream.  NCCL contexts poll instead of blocking
+// (failure detection): the stream's completion, the
+// communicator's asynchronous error and a timeout (mg_opts.nccl_timeout_ms);
+// a failed or timed-out communicator is aborted -- so that a dead peer does
+// not hang the caller -- and the call returns MG_ERR_NCCL (the context can
+// then only be destroyed).
 int sync(mg_ctx *c) {
-  CK(cudaStreamSynchronize(c->stream));
-  return MG_OK;
+  if (c->backend != MG_HALO_NCCL || c->P == 1) {
+    CK(cudaStreamSynchronize(c->stream));
+    return MG_OK;
+  }
+  if (!c->comm) return fail(MG_ERR_NCCL, "the communicator was aborted");
+  CK(cudaEventRecord(c->ev_sync, c->stream));
+  const auto t0 = std::chrono::steady_clock::now();
+  for (long spin = 0;; spin++) {
+    const cudaError_t e = cudaEventQuery(c->ev_sync);
+    if (e == cudaSuccess) return MG_OK;
+    if (e != cudaErrorNotReady) return ck(e, "cudaEventQuery") ? MG_OK : MG_ERR_CUDA;
+    ncclResult_t ae = ncclSuccess;
+    const bool nccl_err = g_nccl.CommGetAsyncError(c->comm, &ae) != ncclSuccess ||
+                          (ae != ncclSuccess && ae != ncclInProgress);
+    const double ms = std::chrono::duration<double, std::milli>(
+                          std::chrono::steady_clock::now() - t0).count();
+    const bool late = c->o.nccl_timeout_ms > 0 && ms > c->o.nccl_timeout_ms;
+    if (nccl_err || late) {
+      g_nccl.CommAbort(c->comm);
+      c->comm = nullptr;
+      return nccl_err ? fail(MG_ERR_NCCL, "communicator error: %s",
+                             g_nccl.GetErrorString(ae))
+                      : fail(MG_ERR_NCCL, "no progress for %d ms (a peer died?); "
+                             "communicator aborted", c->o.nccl_timeout_ms);
+    }
+    if (spin > 64) {  // past the first microseconds: yield the core
+      const timespec ts{0, 20000};
+      nanosleep(&ts, nullptr);
+    }
+  }
 }
 
 // staging buffer for natural-layout host/device transfers of level l
@@ -777,7 +906,10 @@ double *host_pinned(mg_ctx *c, size_t n) {
 
 size_t level_cells_held(const mg_ctx *c, int l) {
   size_t n = 0;
-  for (const Grid &g : c->g[l]) n += (size_t)g.nxl * g.ny * g.nz;
+  for (size_t s = 0; s < io_grids(c, l); s++) {
+    const Grid &g = c->g[l][s];
+    n += (size_t)g.nxl * g.ny * g.nz;
+  }
   return n;
 }
 
@@ -800,12 +932,13 @@ int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in,
     return fail(MG_ERR_ARG, "bad 'where' %d", where);
   }
   size_t off = 0;
-  for (const Grid &g : c->g[l]) {
+  for (size_t s = 0; s < c->g[l].size(); s++) {
+    const Grid &g = c->g[l][s];
     if (in)
-      mg::launch_pack(g, field, dev + off, c->stream);
-    else
+      mg::launch_pack(g, field, dev + off, c->stream);  // every copy
+    else if (s < io_grids(c, l))
       mg::launch_unpack(g, field, dev + off, c->stream);
-    off += (size_t)g.nxl * g.ny * g.nz;
+    if (s + 1 < io_grids(c, l)) off += (size_t)g.nxl * g.ny * g.nz;
   }
   CK(cudaGetLastError());
   if (in) {
@@ -904,6 +1037,7 @@ void mg_default_opts(mg_opts *o) {
   o->workspace = nullptr;
   o->workspace_bytes = 0;
   o->use_graph = 1;
+  o->nccl_timeout_ms = 600000;
 }
 
 const char *mg_strerror(int code) {
@@ -985,8 +1119,10 @@ static int validate(int nx, int ny, int nz, double h, const mg_bc *bc,
   if (o->nranks < 1 || o->rank < 0 || o->rank >= o->nranks)
     return fail(MG_ERR_ARG, "bad rank %d / nranks %d", o->rank, o->nranks);
   if (o->nranks > 1 && o->halo_backend != MG_HALO_NCCL &&
-      o->halo_backend != MG_HALO_LOOPBACK)
-    return fail(MG_ERR_ARG, "nranks > 1 needs the NCCL or LOOPBACK backend");
+      o->halo_backend != MG_HALO_LOOPBACK && o->halo_backend != MG_HALO_EMULATE)
+    return fail(MG_ERR_ARG, "nranks > 1 needs the NCCL, LOOPBACK or EMULATE backend");
+  if (o->nranks > kMaxSlabs && o->halo_backend != MG_HALO_NCCL)
+    return fail(MG_ERR_ARG, "at most %d slabs in one process", kMaxSlabs);
   (void)nx;
   (void)ny;
   (void)nz;
@@ -1002,8 +1138,10 @@ size_t mg_workspace_bytes(int nx, int ny, int nz, const mg_opts *o) {
   mg_ctx c;
   if (make_plan(nx, ny, nz, o, &c.pl)) return 0;
   c.P = c.pl.P;
-  c.nslab = (o->halo_backend == MG_HALO_LOOPBACK) ? c.P : 1;
-  c.slab0 = (o->halo_backend == MG_HALO_LOOPBACK) ? 0 : o->rank;
+  const bool local = c.P > 1 && o->halo_backend != MG_HALO_NCCL;
+  c.nslab = local ? c.P : 1;
+  c.slab0 = local ? 0 : o->rank;
+  c.ncopy = (c.P > 1 && o->halo_backend == MG_HALO_EMULATE) ? c.P : 1;
   c.h = 1.0;
   for (int q = 0; q < 6; q++) c.bc[q].type = MG_DIRICHLET;
   return carve(&c, nullptr);
@@ -1039,8 +1177,9 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
   c->P = c->pl.P;
   c->rank = opts->rank;
   c->backend = c->P > 1 ? opts->halo_backend : MG_HALO_NONE;
-  c->nslab = c->backend == MG_HALO_LOOPBACK ? c->P : 1;
+  c->nslab = (c->backend == MG_HALO_LOOPBACK || c->backend == MG_HALO_EMULATE) ? c->P : 1;
   c->slab0 = c->backend == MG_HALO_NCCL ? c->rank : 0;
+  c->ncopy = c->backend == MG_HALO_EMULATE ? c->P : 1;
   c->dev = opts->device;
   auto bail = [&](cudaError_t e, const char *what) -> mg_ctx * {
     fail(MG_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
@@ -1145,6 +1284,8 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
       mg_destroy(c);
       return nullptr;
     }
+    e = cudaEventCreateWithFlags(&c->ev_sync, cudaEventDisableTiming);
+    if (e != cudaSuccess) return bail(e, "cudaEventCreate(sync)");
     ncclUniqueId id;
     memcpy(&id, opts->nccl_id, sizeof id);
     if (nccl_ck(g_nccl.CommInitRank(&c->comm, c->P, id, c->rank),
@@ -1174,6 +1315,7 @@ void mg_destroy(mg_ctx *c) {
   }
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->ev_sync) cudaEventDestroy(c->ev_sync);
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
   for (int q = 0; q < 3; q++) {
@@ -1215,6 +1357,7 @@ int mg_set_rhs(mg_ctx *c, const double *f, int where) {
 int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
                             const double *radii, const double *charges,
                             int normalization, int subsample) {
+  Nvtx nv("mg_set_rhs_from_spheres");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (n < 0) return fail(MG_ERR_ARG, "n < 0");
   if (subsample < 1 || subsample > 16)
@@ -1343,6 +1486,7 @@ static int async_setup(mg_ctx *c, size_t bytes) {
 // serialised on one stream.
 int mg_solve_async(mg_ctx *c, const double *f, int where_f, double *phi_out,
                    int where_phi, int cycles) {
+  Nvtx nv("mg_solve_async");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (cycles < 0) return fail(MG_ERR_ARG, "cycles < 0");
   if (!f) return fail(MG_ERR_ARG, "null f");
@@ -1427,6 +1571,7 @@ int mg_wait(mg_ctx *c, double *res_norm_out) {
 }
 
 int mg_vcycle(mg_ctx *c, double *res_norm_out) {
+  Nvtx nv("mg_vcycle");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   int rc;
   if ((rc = enqueue_cycle(c))) return rc;
@@ -1441,11 +1586,13 @@ int mg_vcycle(mg_ctx *c, double *res_norm_out) {
 }
 
 int mg_residual_norm(mg_ctx *c, double *out) {
+  Nvtx nv("mg_residual_norm");
   if (!c || !out) return fail(MG_ERR_ARG, "null pointer");
   return residual_norm_now(c, out);
 }
 
 int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
+  Nvtx nv("mg_solve");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   double r0;
   int rc = residual_norm_now(c, &r0);
@@ -1612,17 +1759,11 @@ int rebuild_coefficients(mg_ctx *c) {
         mg::launch_coarse_coef64(c->g[l - 1][s], cg, const_cast<double *>(cg.c64R),
                                  const_cast<double *>(cg.c64B), c->stream);
       }
-      if (l == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
-        const Grid &G = c->g[l][0];
-        const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
-        double *R = const_cast<double *>(G.c64R), *B = const_cast<double *>(G.c64B);
-        int rc;
-        if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-        g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
-                         ncclDouble, c->comm, c->stream);
-        g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
-                         ncclDouble, c->comm, c->stream);
-        if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef64)"))) return rc;
+      if (l == c->pl.nd && c->P > 1) {  // records: 8 doubles per element
+        int rc = gather_portions(c, l, 2, 8 * sizeof(double), [](const Grid &g, int a) {
+          return (void *)(a ? g.c64B : g.c64R);
+        });
+        if (rc) return rc;
       }
     }
     CK(cudaGetLastError());
@@ -1658,17 +1799,11 @@ int rebuild_coefficients(mg_ctx *c) {
         mg::launch_coarse_coef(c->g[l - 1][s], cg, const_cast<float *>(cg.coefR),
                                const_cast<float *>(cg.coefB), c->stream);
       }
-      if (l == c->pl.nd && c->P > 1 && c->backend == MG_HALO_NCCL) {
-        const Grid &G = c->g[l][0];
-        const size_t cnt = (size_t)(G.nx / c->P) * G.plane * 8;
-        float *R = const_cast<float *>(G.coefR), *B = const_cast<float *>(G.coefB);
-        int rc;
-        if ((rc = nccl_ck(g_nccl.GroupStart(), "ncclGroupStart"))) return rc;
-        g_nccl.AllGather(R + 8 * G.plane + c->rank * cnt, R + 8 * G.plane, cnt,
-                         ncclFloat, c->comm, c->stream);
-        g_nccl.AllGather(B + 8 * G.plane + c->rank * cnt, B + 8 * G.plane, cnt,
-                         ncclFloat, c->comm, c->stream);
-        if ((rc = nccl_ck(g_nccl.GroupEnd(), "ncclGroupEnd(coef)"))) return rc;
+      if (l == c->pl.nd && c->P > 1) {  // records: 8 floats per element
+        int rc = gather_portions(c, l, 2, 8 * sizeof(float), [](const Grid &g, int a) {
+          return (void *)(a ? g.coefB : g.coefR);
+        });
+        if (rc) return rc;
       }
     }
     // level l aligned (every kappa 0 or 1, delta from the position)?  codes
@@ -1812,6 +1947,7 @@ static int coulomb_forces(mg_ctx *c, int n, const double *centers,
 int mg_coulomb_forces(mg_ctx *c, int n, const double *centers,
                       const double *radii, const double *charges,
                       int normalization, int subsample, double *forces_out) {
+  Nvtx nv("mg_coulomb_forces");
   return coulomb_forces(c, n, centers, radii, charges, normalization, subsample,
                         forces_out, nullptr);
 }
@@ -1897,6 +2033,7 @@ int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
                 const double *charges, int normalization, int subsample,
                 int cycles, double abs_tol, double *forces_out,
                 int force_subsample, int *cycles_out, double *res_out) {
+  Nvtx nv("mg_timestep");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   if (cycles < 0) return fail(MG_ERR_ARG, "cycles < 0");
   if (cycles == 0 && !(abs_tol > 0.0))
@@ -1947,7 +2084,8 @@ int mg_get_stencil(mg_ctx *c, int l, double *out, int where) {
     dev = c->stage;
   }
   size_t off = 0;
-  for (const Grid &g : c->g[l]) {
+  for (size_t s = 0; s < io_grids(c, l); s++) {
+    const Grid &g = c->g[l][s];
     mg::launch_get_stencil(g, dev + 7 * off, c->stream);
     off += (size_t)g.nxl * g.ny * g.nz;
   }

@@ -2,8 +2,12 @@
 
 The x-slab decomposition (P:570-571 ghost exchange per level,
 P:622-624, P:692-693 periodic arrangement) runs P slabs in one process on
-one GPU (halo backend LOOPBACK: ghost planes by device copies, one shared
-agglomerated hierarchy).  Each run here is compared with the single-domain
+one GPU, with two halo backends: LOOPBACK (ghost planes by device copies,
+one shared agglomerated hierarchy) and EMULATE (NCCL's data layout: one
+copy of the agglomerated levels per rank, the halo schedule mg_halo_schedule
+matched message by message and the in-place all-gathers of the restricted
+RHS, of the coarse operator records and of the norm executed as device
+copies with NCCL's indexing).  Each run here is compared with the single-domain
 CPU oracle -- not with the 1-slab CUDA run -- at sizes where level 0 takes
 the TMA-marching kernels (nz/2 >= 64) and the coarse levels are agglomerated
 (local cells < 64^3): Phi rel-L2 <= 1e-10, equal cycle counts and the
@@ -19,7 +23,7 @@ from paper_1410_6609_b200 import workloads as W
 
 pytestmark = pytest.mark.gpu
 
-BACKENDS = ["loopback"]
+BACKENDS = ["loopback", "emulate"]
 
 
 @pytest.fixture(scope="module")
@@ -126,3 +130,33 @@ def test_slabs_steps_bitwise_vs_oracle(mg, P, backend):
     o.prolong_correct(0, 2.0)
     assert np.array_equal(s.get_solution(), o.phi())
     s.close()
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("kind", ["box", "periodic", "permittivity", "masked"])
+def test_emulate_equals_loopback(mg, P, kind):
+    """The NCCL layout (EMULATE) and the shared-copy layout (LOOPBACK) give
+    the same iterates bit for bit and the same cycle norms (both sum the
+    norm per rank, then in rank order)."""
+    shape = (128, 32, 128)
+    bt, bv = W.channel_bc(1.0)
+    if kind == "periodic":
+        bt, bv = W.periodic_channel_bc(1.0)
+    f = np.random.default_rng(8).uniform(-1, 1, shape)
+    out = []
+    for backend in ("loopback", "emulate"):
+        s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=4, nranks=P, halo=backend,
+                         agglomerate_below=2048)
+        if kind == "permittivity":
+            eps = np.where(np.arange(shape[1])[None, :, None] < 16, 1.0, 78.5) \
+                * np.ones(shape)
+            s.set_permittivity(eps)
+        if kind == "masked":
+            s.set_mask(W.beam_mask(shape))
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(3)]
+        out.append((r, s.get_solution(), s.get_field(s.nlevels - 1, mg.MG_FIELD_PHI)))
+        s.close()
+    assert np.array_equal(out[0][1], out[1][1])
+    assert np.array_equal(out[0][2], out[1][2])
+    assert out[0][0] == out[1][0]
