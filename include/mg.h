@@ -401,7 +401,12 @@ int mg_set_profiling(mg_ctx *ctx, int on);
 int mg_last_cycle_times(mg_ctx *ctx, double out[8]);
 /* As mg_last_cycle_times, n >= 10 outputs, plus
  *   out[8] level-0 smoothing launches timed in out[0]
- *   out[9] level-0 half-sweeps they perform (one per launch) */
+ *   out[9] level-0 half-sweeps they perform (one per launch)
+ * and with n >= 12
+ *   out[10] levels >= 1 held whole on every rank (the agglomerated levels;
+ *           every level >= 1 of a single slab) incl. the coarsest solve
+ *   out[11] the coarsest-grid CG alone
+ * (LOOPBACK / NCCL: one copy; EMULATE times every rank's copy). */
 int mg_last_cycle_times_ex(mg_ctx *ctx, double *out, int n);
 /* Number of kernels one mg_vcycle launches (counted when it is recorded). */
 int mg_cycle_launches(const mg_ctx *ctx);

@@ -352,8 +352,11 @@ int nccl_ck(ncclResult_t r, const char *what) {
 bool distributed(const mg_ctx *c, int l) { return l < c->pl.nd && c->P > 1; }
 
 // profiling categories (mg_last_cycle_times)
+// CAT_COARSE: distributed levels >= 1; CAT_AGG: levels >= 1 held whole
+// (agglomerated, or every level >= 1 of a single slab) without the CG;
+// CAT_CG: the coarsest-grid solve
 enum { CAT_NONE = -1, CAT_SMOOTH0 = 0, CAT_RESTRICT0 = 2, CAT_PROLONG0 = 3,
-       CAT_NORM = 4, CAT_COARSE = 5 };
+       CAT_NORM = 4, CAT_COARSE = 5, CAT_AGG = 6, CAT_CG = 7, kNumCat = 8 };
 constexpr int kMaxMarks = 512;
 
 // record an event closing an interval of category `cat` (CAT_NONE opens one)
@@ -787,6 +790,12 @@ int split_norm_tail(mg_ctx *c) {
   return finish_norm(c, cnt);
 }
 
+// profiling category of the work on level l >= 1 (not level 0)
+int level_cat(const mg_ctx *c, int l) {
+  if (l < 1 || l > c->pl.L - 2) return CAT_NONE;
+  return distributed(c, l) ? CAT_COARSE : CAT_AGG;
+}
+
 int enqueue_vcycle(mg_ctx *c) {
   const int L = c->pl.L;
   int rc;
@@ -796,7 +805,7 @@ int enqueue_vcycle(mg_ctx *c) {
   if (c->use_march && !c->tm[0].empty() && c->tm[0][0].ok) c->paths |= MG_PATH_MARCH;
   if (fused_norm_on(c)) c->paths |= MG_PATH_FUSED_NORM;
   for (int l = 0; l < L - 1; l++) {
-    if (l == 1) mark(c, CAT_NONE);
+    if (l >= 1) mark(c, level_cat(c, l - 1));  // closes level l-1's down part
     if (c->o.nu1 == 0 && l > 0)
       for (const Grid &g : c->g[l]) {
         CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
@@ -808,10 +817,11 @@ int enqueue_vcycle(mg_ctx *c) {
     }
     if ((rc = restrict_level(c, l))) return rc;
   }
-  if (L == 1) mark(c, CAT_NONE);
+  mark(c, level_cat(c, L - 2));
   if ((rc = coarse_solve(c))) return rc;
+  mark(c, CAT_CG);
   for (int l = L - 2; l >= 0; l--) {
-    if (l == 0) mark(c, CAT_COARSE);
+    if (l < L - 2) mark(c, level_cat(c, l + 1));  // closes level l+1's up part
     const bool fuse = can_fuse_prolong(c, l);
     if (fuse) {
       if ((rc = prolong_red_level(c, l))) return rc;
@@ -832,7 +842,6 @@ int enqueue_vcycle(mg_ctx *c) {
       return MG_OK;
     }
   }
-  if (L == 1) mark(c, CAT_COARSE);
   // fused norm (c11): already published by the level-0 restriction
   rc = fused_norm_on(c) ? MG_OK : enqueue_norm(c);
   c->cycle_launches = c->launches;
@@ -2111,20 +2120,38 @@ int mg_set_profiling(mg_ctx *c, int on) {
   return MG_OK;
 }
 
-int mg_last_cycle_times(mg_ctx *c, double out[8]) {
-  if (!c || !out) return fail(MG_ERR_ARG, "null pointer");
+// per-category sums of the last profiled cycle's intervals (ms), and the
+// number of level-0 half-sweep intervals
+static int cycle_cats(mg_ctx *c, double cat_ms[kNumCat], int *nsmooth, double *total) {
   if (!c->prof_last || c->nev < 2) return fail(MG_ERR_ARG, "profiling was off");
-  for (int q = 0; q < 8; q++) out[q] = 0.0;
+  for (int q = 0; q < kNumCat; q++) cat_ms[q] = 0.0;
+  *nsmooth = 0;
   for (int i = 1; i < c->nev; i++) {
     const int cat = c->mark_cat[i];
     if (cat == CAT_NONE) continue;
     float ms = 0.f;
     CK(cudaEventElapsedTime(&ms, c->ev[i - 1], c->ev[i]));
-    out[cat] += ms;
-    if (cat == CAT_SMOOTH0) out[1] += 1.0;
+    cat_ms[cat] += ms;
+    if (cat == CAT_SMOOTH0) (*nsmooth)++;
   }
   float tot = 0.f;
   CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[c->nev - 1]));
+  *total = tot;
+  return MG_OK;
+}
+
+int mg_last_cycle_times(mg_ctx *c, double out[8]) {
+  if (!c || !out) return fail(MG_ERR_ARG, "null pointer");
+  double cat[kNumCat], tot;
+  int ns;
+  int rc = cycle_cats(c, cat, &ns, &tot);
+  if (rc) return rc;
+  out[0] = cat[CAT_SMOOTH0];
+  out[1] = ns;
+  out[2] = cat[CAT_RESTRICT0];
+  out[3] = cat[CAT_PROLONG0];
+  out[4] = cat[CAT_NORM];
+  out[5] = cat[CAT_COARSE] + cat[CAT_AGG] + cat[CAT_CG];  // levels >= 1 incl. CG
   out[6] = tot;
   out[7] = c->cycle_launches;
   return MG_OK;
@@ -2136,6 +2163,13 @@ int mg_last_cycle_times_ex(mg_ctx *c, double *out, int n) {
   if (rc) return rc;
   out[8] = out[1];  // level-0 smoothing launches
   out[9] = out[1];  // half-sweeps they perform (one per launch)
+  if (n >= 12) {
+    double cat[kNumCat], tot;
+    int ns;
+    if ((rc = cycle_cats(c, cat, &ns, &tot))) return rc;
+    out[10] = cat[CAT_AGG] + cat[CAT_CG];  // levels >= 1 held whole, incl. CG
+    out[11] = cat[CAT_CG];                 // the coarsest-grid solve
+  }
   return MG_OK;
 }
 

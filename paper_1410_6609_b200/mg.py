@@ -140,7 +140,7 @@ def lib():
         L.mg_get_stencil.argtypes = [P, i, dp, i]
         L.mg_set_profiling.argtypes = [P, i]
         L.mg_last_cycle_times.argtypes = [P, ctypes.c_double * 8]
-        L.mg_last_cycle_times_ex.argtypes = [P, ctypes.c_double * 10, i]
+        L.mg_last_cycle_times_ex.argtypes = [P, ctypes.c_double * 12, i]
         L.mg_cycle_launches.argtypes = [P]
         L.mg_cycle_paths.argtypes = [P]
         L.mg_stream.argtypes = [P]
@@ -519,11 +519,12 @@ class Multigrid:
         _check(lib().mg_set_profiling(self._ctx, int(bool(on))), self._ctx)
 
     def last_cycle_times(self) -> dict:
-        out = (ctypes.c_double * 10)()
-        _check(lib().mg_last_cycle_times_ex(self._ctx, out, 10), self._ctx)
+        out = (ctypes.c_double * 12)()
+        _check(lib().mg_last_cycle_times_ex(self._ctx, out, 12), self._ctx)
         keys = ["smooth0_ms", "smooth0_launches", "restrict0_ms", "prolong0_ms",
                 "norm_ms", "coarse_ms", "cycle_ms", "launches",
-                "smooth0_launches_ex", "smooth0_halfsweeps"]
+                "smooth0_launches_ex", "smooth0_halfsweeps", "whole_levels_ms",
+                "cg_ms"]
         return dict(zip(keys, list(out)))
 
     @property
