@@ -256,6 +256,8 @@ struct mg_ctx {
   unsigned long long async_k = 0;
   double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
+  int *bins = nullptr;         // sphere bins (counts + items), grown on demand
+  size_t bins_cap = 0;         // ints
   double *fbuf = nullptr;      // force step: sphere list + partial sums
   double *hpin = nullptr;      // pinned host staging for sphere lists and
   size_t hpin_cap = 0;         // force partials (doubles), grown, kept
@@ -1337,6 +1339,7 @@ void mg_destroy(mg_ctx *c) {
   if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
   if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   if (c->sph) cudaFree(c->sph);
+  if (c->bins) cudaFree(c->bins);
   if (c->fbuf) cudaFree(c->fbuf);
   if (c->hpin) cudaFreeHost(c->hpin);
   for (void *p : c->mask_bufs) cudaFree(p);
@@ -1399,9 +1402,39 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   if (n > 0) {
     CK(cudaMemcpyAsync(c->sph, h5, sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
+    // bins of the centres for the scatter's neighbour search: wider than
+    // 2 R_max + 2 cells, at most 64 per axis; on periodic axes the bin width
+    // divides the extent (exact wrap of bin indices)
+    mg::SphereBins B;
+    B.rmax = 0.0;
+    for (int p = 0; p < n; p++) B.rmax = radii[p] > B.rmax ? radii[p] : B.rmax;
+    const int bcmin = (int)ceil(2.0 * B.rmax / c->h) + 2;
+    size_t nbins = 1;
+    for (int a = 0; a < 3; a++) {
+      const int ext = c->pl.dims[0][a];
+      int bc = bcmin > (ext + 63) / 64 ? bcmin : (ext + 63) / 64;
+      if (bc > ext) bc = ext;
+      if (c->bc[2 * a].type == MG_PERIODIC)
+        while (ext % bc) bc++;
+      B.bc[a] = bc;
+      B.nb[a] = (ext + bc - 1) / bc;
+      nbins *= (size_t)B.nb[a];
+    }
+    const size_t need = nbins * (1 + mg::kBinCap);
+    if (need > c->bins_cap) {
+      if (c->bins) cudaFree(c->bins);
+      c->bins = nullptr;
+      c->bins_cap = 0;
+      CK(cudaMalloc(&c->bins, need * sizeof(int)));
+      c->bins_cap = need;
+    }
+    B.count = c->bins;
+    B.items = c->bins + nbins;
+    CK(cudaMemsetAsync(B.count, 0, nbins * sizeof(int), c->stream));
+    mg::launch_sphere_bin(c->g[0][0], c->h, n, c->sph, B, c->stream);
     mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, c->sph, cnt, c->stream);
     for (const Grid &g : c->g[0])
-      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt,
+      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt, B,
                                 c->stream);
     CK(cudaGetLastError());
   }

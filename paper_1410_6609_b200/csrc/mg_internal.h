@@ -181,9 +181,22 @@ size_t coarse_cg_scratch_doubles(const Grid &g);
 void launch_sphere_counts(const Grid &g, double h, int subsample, int n,
                           const double *sph, unsigned long long *counts,
                           cudaStream_t s);
+// uniform bins of sphere centres for the neighbour search of the scatter:
+// nb[a] bins of bc[a] cells per axis (on periodic axes bc divides the
+// extent), count[bin] (zeroed by the caller) and up to kBinCap sphere
+// indices per bin; rmax = the largest radius
+constexpr int kBinCap = 16;
+struct SphereBins {
+  int nb[3], bc[3];
+  int *count, *items;
+  double rmax;
+};
+void launch_sphere_bin(const Grid &g, double h, int n, const double *sph,
+                       const SphereBins &B, cudaStream_t s);
 void launch_sphere_scatter(const Grid &g, double h, int subsample, int n,
                            const double *sph, int normalization,
-                           const unsigned long long *counts, cudaStream_t s);
+                           const unsigned long long *counts, const SphereBins &B,
+                           cudaStream_t s);
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);
 // plane-marching TMA half-sweep (mg_march.cu)

@@ -543,10 +543,13 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
 //                     ascending sphere order -- the oracle's "overlapping
 //                     spheres add in sphere order" exactly, and deterministic
 //                     (no atomics).  The other spheres that can reach a cell
-//                     of sphere p are found first by a conservative distance
-//                     test against every sphere (ascending list in shared
-//                     memory; beyond kNbMax entries every cell scans all
-//                     spheres instead -- slow, still exact).
+//                     of sphere p are found first: a uniform grid of bins
+//                     (k_sphere_bin, bins wider than any two radii) gives the
+//                     candidates of the bins around p, which pass a
+//                     conservative distance test and are sorted into an
+//                     ascending list in shared memory.  A full bin or more
+//                     than kNbMax neighbours make every cell scan all spheres
+//                     instead -- slow, still exact.
 // sph holds (cx, cy, cz, R, Q) per sphere.  Every cell not covered keeps the
 // value it has (the caller zeroes f first).
 // ---------------------------------------------------------------------------
@@ -582,6 +585,32 @@ __global__ void __launch_bounds__(kThreads)
 }
 
 static constexpr int kNbMax = 128;  // neighbour list entries per sphere
+
+// floor division for possibly negative cell indices
+__device__ __forceinline__ int fdiv(int a, int b) {
+  return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+
+// the bin of a sphere centre: cell index floor(c / h) per axis (clamped to
+// the domain), bc cells per bin
+__device__ __forceinline__ int bin_axis(const SphereBins &B, const Grid &g, int ax,
+                                        double c, double h) {
+  const int ext[3] = {g.nx, g.ny, g.nz};
+  int ic = (int)floor(c / h);
+  ic = min(max(ic, 0), ext[ax] - 1);
+  return min(ic / B.bc[ax], B.nb[ax] - 1);
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_sphere_bin(Grid g, double h, int n, const double *sph, SphereBins B) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int b = (bin_axis(B, g, 0, sph[5 * p], h) * B.nb[1] +
+                 bin_axis(B, g, 1, sph[5 * p + 1], h)) * B.nb[2] +
+                bin_axis(B, g, 2, sph[5 * p + 2], h);
+  const int slot = atomicAdd(B.count + b, 1);
+  if (slot < kBinCap) B.items[(size_t)b * kBinCap + slot] = p;
+}
 
 // can spheres a and b cover a common sub-cell centre?  Conservative: per
 // axis the (minimum-image on periodic axes) centre distance <= Ra + Rb + 2h
@@ -638,11 +667,11 @@ __device__ __forceinline__ double sphere_value(const double *q, double np, int c
 
 __global__ void __launch_bounds__(kThreads)
     k_sphere_scatter(Grid g, double h, int s, int n, const double *sph,
-                     int normalization, const unsigned long long *counts) {
+                     int normalization, const unsigned long long *counts,
+                     SphereBins B) {
   __shared__ sph::Tab tab;
   __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
   __shared__ int nbl[kNbMax];
-  __shared__ int wcnt[kThreads / 32];
   __shared__ int nbn;
   const int p = blockIdx.x;
   const double *me = sph + 5 * p;
@@ -652,25 +681,66 @@ __global__ void __launch_bounds__(kThreads)
   const int s3 = s * s * s;
   const double np = (double)counts[p];
   if (normalization != 1 && np == 0.0) return;  // covers nothing
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  // spheres that may share a cell with p, ascending
-  if (threadIdx.x == 0) nbn = 0;
-  __syncthreads();
-  for (int base = 0; base < n; base += blockDim.x) {
-    const int q = base + threadIdx.x;
-    const bool hit = q < n && q != p && spheres_near(g, h, me, sph + 5 * q);
-    const unsigned bal = __ballot_sync(0xffffffffu, hit);
-    if (lane == 0) wcnt[warp] = __popc(bal);
-    __syncthreads();
-    int off = nbn;
-    for (int w = 0; w < warp; w++) off += wcnt[w];
-    off += __popc(bal & ((1u << lane) - 1u));
-    if (hit && off < kNbMax) nbl[off] = q;
-    __syncthreads();
-    if (threadIdx.x == 0)
-      for (int w = 0; w < (int)(blockDim.x >> 5); w++) nbn += wcnt[w];
-    __syncthreads();
+  // spheres that may share a cell with p: the candidates of the bins within
+  // R_p + R_max + 2h (+ 2 cells of margin) of p's centre cell on every axis
+  // (periodic axes wrap; their bins divide the axis), then the distance
+  // test, then an ascending sort (ranks; the entries are distinct)
+  __shared__ int cand[kNbMax];
+  __shared__ int ncand, overflow;
+  if (threadIdx.x == 0) {
+    ncand = 0;
+    overflow = 0;
   }
+  __syncthreads();
+  {
+    const int ext[3] = {g.nx, g.ny, g.nz};
+    int b0[3], nbr[3];
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+      int ic = (int)floor(me[ax] / h);
+      ic = min(max(ic, 0), ext[ax] - 1);
+      const int E = (int)((me[3] + B.rmax + 2.0 * h) / h) + 2;
+      int lo = fdiv(ic - E, B.bc[ax]), hi = fdiv(ic + E, B.bc[ax]);
+      if (!g.per[ax]) {
+        lo = max(lo, 0);
+        hi = min(hi, B.nb[ax] - 1);
+      }
+      nbr[ax] = min(hi - lo + 1, B.nb[ax]);
+      b0[ax] = lo;
+    }
+    const int nbins = nbr[0] * nbr[1] * nbr[2];
+    for (int t = threadIdx.x; t < nbins; t += blockDim.x) {
+      int bb[3] = {t / (nbr[1] * nbr[2]), (t / nbr[2]) % nbr[1], t % nbr[2]};
+#pragma unroll
+      for (int ax = 0; ax < 3; ax++) {
+        bb[ax] += b0[ax];
+        if (g.per[ax]) bb[ax] = ((bb[ax] % B.nb[ax]) + B.nb[ax]) % B.nb[ax];
+      }
+      const int b = (bb[0] * B.nb[1] + bb[1]) * B.nb[2] + bb[2];
+      const int m = B.count[b];
+      if (m > kBinCap) {
+        overflow = 1;
+        continue;
+      }
+      for (int e = 0; e < m; e++) {
+        const int q = B.items[(size_t)b * kBinCap + e];
+        if (q == p || !spheres_near(g, h, me, sph + 5 * q)) continue;
+        const int slot = atomicAdd(&ncand, 1);
+        if (slot < kNbMax) cand[slot] = q;
+      }
+    }
+  }
+  __syncthreads();
+  const int nc = ncand;
+  if (nc <= kNbMax)
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+      const int q = cand[t];
+      int r = 0;
+      for (int u = 0; u < nc; u++) r += cand[u] < q;
+      nbl[r] = q;
+    }
+  if (threadIdx.x == 0) nbn = (overflow || nc > kNbMax) ? kNbMax + 1 : nc;
+  __syncthreads();
   const int nn = nbn;
   const bool scan_all = nn > kNbMax;  // list overflow: every sphere per cell
   const int ntry = scan_all ? n : nn;
@@ -736,11 +806,17 @@ void launch_sphere_counts(const Grid &g, double h, int s, int n, const double *s
   k_sphere_count<<<n, kThreads, 0, st>>>(g, h, s, sph, counts);
 }
 
+void launch_sphere_bin(const Grid &g, double h, int n, const double *sph,
+                       const SphereBins &B, cudaStream_t st) {
+  if (n <= 0) return;
+  k_sphere_bin<<<(n + kThreads - 1) / kThreads, kThreads, 0, st>>>(g, h, n, sph, B);
+}
+
 void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *sph,
                            int normalization, const unsigned long long *counts,
-                           cudaStream_t st) {
+                           const SphereBins &B, cudaStream_t st) {
   if (n <= 0) return;
-  k_sphere_scatter<<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts);
+  k_sphere_scatter<<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts, B);
 }
 
 // ---------------------------------------------------------------------------
