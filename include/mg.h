@@ -126,6 +126,13 @@ typedef struct {
                          progress for this long, or an asynchronous NCCL
                          error, aborts the communicator and returns
                          MG_ERR_NCCL (default 600000; 0 = wait forever)     */
+  long long tail_cells; /* the coarse end of each V-cycle -- every level from
+                         the first one held whole with at most this many
+                         cells, down to the coarsest solve and back -- runs
+                         as ONE persistent thread-block-cluster kernel
+                         instead of a launch per step (box / periodic grids
+                         whose coarsest solve is the single-CTA CG; 0 =
+                         default 32768 = 32^3; MG_OFF_TAIL disables it)     */
 } mg_opts;
 
 /* mg_opts.disable bits */
@@ -134,6 +141,7 @@ typedef struct {
 #define MG_OFF_SPLIT_NORM 4  /* split cycle-end norm -> one full norm pass    */
 #define MG_OFF_CG_CLUSTER 8  /* 8-CTA cluster CG -> single-CTA CG             */
 #define MG_OFF_MASK_CODES 16 /* masked levels: byte codes -> float records    */
+#define MG_OFF_TAIL 32       /* persistent tail kernel -> a launch per step   */
 
 /* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
 #define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
@@ -143,6 +151,7 @@ typedef struct {
 #define MG_PATH_CG_VAR 16        /* variable-coefficient coarsest CG          */
 #define MG_PATH_PROLONG_FUSED 32 /* prolongation fused with the red sweep     */
 #define MG_PATH_FUSED_NORM 64    /* norm from the in-cycle residual (c11)     */
+#define MG_PATH_TAIL 128         /* coarse levels in the persistent tail      */
 
 typedef struct mg_ctx mg_ctx;
 

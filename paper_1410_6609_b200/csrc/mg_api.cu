@@ -792,6 +792,43 @@ int split_norm_tail(mg_ctx *c) {
   return finish_norm(c, cnt);
 }
 
+// first level of the persistent tail kernel (k_vcycle_tail), or L for none:
+// the first level >= 1 held whole on every rank with at most
+// mg_opts.tail_cells cells, if the levels from there down are box or
+// periodic grids whose coarsest solve is the single-CTA CG
+int tail_level(const mg_ctx *c) {
+  const int L = c->pl.L;
+  if ((c->o.disable & MG_OFF_TAIL) || c->masked || L < 3) return L;
+  const long long cap = c->o.tail_cells > 0 ? c->o.tail_cells : 32768;
+  int ls = L;
+  for (int l = c->pl.nd > 1 ? c->pl.nd : 1; l < L - 1; l++)
+    if ((long long)c->pl.dims[l][0] * c->pl.dims[l][1] * c->pl.dims[l][2] <= cap) {
+      ls = l;
+      break;
+    }
+  if (ls >= L - 1 || L - ls > mg::kTailMax) return L;
+  const Grid &gc = c->g[L - 1][0];
+  if (!mg::vcycle_tail_supported(gc)) return L;
+  if (cg_cluster_on(c) && mg::coarse_cg_cluster_supported(gc)) return L;
+  return ls;
+}
+
+// levels ls..L-1 (copy s of each) in one persistent cluster kernel
+int tail_launch(mg_ctx *c, int ls) {
+  for (int s = 0; s < c->ncopy; s++) {
+    mg::TailLevels T;
+    T.n = c->pl.L - ls;
+    for (int k = 0; k < T.n; k++) T.g[k] = c->g[ls + k][c->ncopy > 1 ? s : 0];
+    if (mg::launch_vcycle_tail(T, c->o.nu1, c->o.nu2, c->o.alpha, c->o.coarse_tol,
+                               c->o.coarse_maxit, c->cg_scr, c->cg_iters, c->stream))
+      return fail(MG_ERR_CUDA, "tail kernel launch: %s",
+                  cudaGetErrorString(cudaGetLastError()));
+    c->launches++;
+  }
+  c->paths |= MG_PATH_TAIL;
+  return MG_OK;
+}
+
 // profiling category of the work on level l >= 1 (not level 0)
 int level_cat(const mg_ctx *c, int l) {
   if (l < 1 || l > c->pl.L - 2) return CAT_NONE;
@@ -806,7 +843,10 @@ int enqueue_vcycle(mg_ctx *c) {
   c->paths = 0;
   if (c->use_march && !c->tm[0].empty() && c->tm[0][0].ok) c->paths |= MG_PATH_MARCH;
   if (fused_norm_on(c)) c->paths |= MG_PATH_FUSED_NORM;
-  for (int l = 0; l < L - 1; l++) {
+  // levels top..L-1 are the tail kernel's (or just the coarsest's CG)
+  const int ls = tail_level(c);
+  const int top = ls < L ? ls : L - 1;
+  for (int l = 0; l < top; l++) {
     if (l >= 1) mark(c, level_cat(c, l - 1));  // closes level l-1's down part
     if (c->o.nu1 == 0 && l > 0)
       for (const Grid &g : c->g[l]) {
@@ -819,11 +859,16 @@ int enqueue_vcycle(mg_ctx *c) {
     }
     if ((rc = restrict_level(c, l))) return rc;
   }
-  mark(c, level_cat(c, L - 2));
-  if ((rc = coarse_solve(c))) return rc;
-  mark(c, CAT_CG);
-  for (int l = L - 2; l >= 0; l--) {
-    if (l < L - 2) mark(c, level_cat(c, l + 1));  // closes level l+1's up part
+  mark(c, level_cat(c, top - 1));
+  if (ls < L) {
+    if ((rc = tail_launch(c, ls))) return rc;
+    mark(c, CAT_AGG);
+  } else {
+    if ((rc = coarse_solve(c))) return rc;
+    mark(c, CAT_CG);
+  }
+  for (int l = top - 1; l >= 0; l--) {
+    if (l < top - 1) mark(c, level_cat(c, l + 1));  // closes level l+1's up part
     const bool fuse = can_fuse_prolong(c, l);
     if (fuse) {
       if ((rc = prolong_red_level(c, l))) return rc;

@@ -7,11 +7,11 @@
 // vector product reads neighbour values of other chunks through distributed
 // shared memory; dot products are per-CTA partials (warp-shuffle tree, warps
 // in order) that every thread sums in cluster-rank order after a cluster
-// barrier, so all CTAs take the same decisions.  Three cluster barriers per
-// iteration replace the single-CTA kernel's serial per-thread loops: the
-// large coarsest grids of agglomerated multi-GPU runs (64 x 8 x 8 at P = 8)
-// spread over kCK SMs.  Measured (scripts/cg_probe.py): 0.42 ms vs 0.48 ms
-// for 64 x 8 x 8; clusters of 4 (0.51) and 16 (0.45, non-portable) slower.
+// barrier, so all CTAs take the same decisions.  The large coarsest grids of
+// agglomerated multi-GPU runs (64 x 8 x 8 at P = 8) spread over kCK SMs.
+// Round 1 (three cluster barriers per iteration, partials read remotely):
+// 0.42 ms for 64 x 8 x 8 vs 0.48 ms single-CTA; clusters of 4 (0.51) and 16
+// (0.45, non-portable) were slower.
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -61,6 +61,13 @@ __device__ __forceinline__ double cta_partial(double v, double *wpart) {
 
 }  // namespace
 
+// Two cluster barriers per iteration: (1) the direction p = r + beta p_old
+// is formed where the matrix-vector product needs it (own cell and the six
+// neighbours, read from the owners' r and p_old -- the same expression, so
+// the same bits as a separate update pass) and stored into the other of two
+// p buffers; (2) each CTA pushes its dot-product partial into slot [rank] of
+// every CTA's shared memory before the barrier, so that after it the sum in
+// rank order reads local shared memory only.
 template <bool PER>
 __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
     k_coarse_cg_cluster(Grid g, double tol, int maxit, int *iters_out, int chunk) {
@@ -68,20 +75,25 @@ __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
   cgr::cluster_group cl = cgr::this_cluster();
   const int rank = (int)cl.block_rank();
   extern __shared__ __align__(16) double cgs[];
-  __shared__ double part[2];            // this CTA's partials: [0] p.q, [1] r.r
+  __shared__ double slots[2][kCK];        // every CTA's partials (pushed here)
   __shared__ double wpart[kCT / 32];
-  __shared__ const double *rp[kCK];     // every CTA's p (distributed smem)
-  __shared__ const double *rpart[kCK];  // every CTA's partials
+  __shared__ const double *rr[kCK];       // every CTA's r (distributed smem)
+  __shared__ const double *rpa[kCK];      // every CTA's p buffers
+  __shared__ const double *rpb[kCK];
+  __shared__ double *rslot[kCK];          // every CTA's slots
 
   const int N = g.nx * g.ny * g.nz;
   const int n0 = rank * chunk;
   const int nl = max(0, min(chunk, N - n0));  // unknowns of this CTA
-  double *p = cgs, *x = cgs + chunk, *r = cgs + 2 * chunk, *q = cgs + 3 * chunk;
-  NB *nb = reinterpret_cast<NB *>(cgs + 4 * chunk);
+  double *pa = cgs, *pb = cgs + chunk, *x = cgs + 2 * chunk, *r = cgs + 3 * chunk,
+         *q = cgs + 4 * chunk;
+  NB *nb = reinterpret_cast<NB *>(cgs + 5 * chunk);
   signed char *dc = reinterpret_cast<signed char *>(nb + chunk);
   if (threadIdx.x < kCK) {
-    rp[threadIdx.x] = cl.map_shared_rank(p, (int)threadIdx.x);
-    rpart[threadIdx.x] = cl.map_shared_rank(part, (int)threadIdx.x);
+    rr[threadIdx.x] = cl.map_shared_rank(r, (int)threadIdx.x);
+    rpa[threadIdx.x] = cl.map_shared_rank(pa, (int)threadIdx.x);
+    rpb[threadIdx.x] = cl.map_shared_rank(pb, (int)threadIdx.x);
+    rslot[threadIdx.x] = cl.map_shared_rank(&slots[0][0], (int)threadIdx.x);
   }
   const int sx = g.ny * g.nz, sy = g.nz;
   const int wx = (g.nx - 1) * sx, wy = (g.ny - 1) * sy, wz = g.nz - 1;
@@ -104,60 +116,72 @@ __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
     const double b = col ? g.fB[idx] : g.fR[idx];
     x[e] = 0.0;
     r[e] = b;
-    p[e] = b;
     acc = acc + b * b;
   }
-  auto cluster_sum = [&](double v, int slot) {
+  __syncthreads();  // the pointer tables
+  int sl = 0;
+  // sum over the cluster in rank order; one CTA barrier + one cluster barrier
+  auto cluster_sum = [&](double v) {
     const double s = cta_partial(v, wpart);
-    if (threadIdx.x == 0) part[slot] = s;
+    if (threadIdx.x == 0)
+#pragma unroll
+      for (int k = 0; k < kCK; k++) rslot[k][sl * kCK + rank] = s;
     cl.sync();
     double tot = 0.0;
 #pragma unroll
-    for (int k = 0; k < kCK; k++) tot = tot + rpart[k][slot];
+    for (int k = 0; k < kCK; k++) tot = tot + slots[sl][k];
+    sl ^= 1;
     return tot;
   };
-  // p of global unknown m (own chunk from local smem, else the owner's)
-  auto pv = [&](int m) {
-    const int k = m / chunk;
-    return k == rank ? p[m - n0] : rp[k][m - k * chunk];
-  };
-  double rho = cluster_sum(acc, 1);  // the barrier also publishes p, rp
+  double rho = cluster_sum(acc);  // the barrier also publishes r
   const double bnorm = sqrt(rho);
   const double c = g.c;
+  double beta = 0.0;
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
+      const bool first = it == 0;
+      // p_old in buffer a on odd iterations, b on even ones (p_new the other)
+      const bool old_a = (it & 1) != 0;
+      double *pn = old_a ? pb : pa;
+      // p = r or r + beta p_old of global unknown m (own chunk locally)
+      auto P = [&](int m) {
+        const int k = m / chunk, e = m - k * chunk;
+        const double *rk = k == rank ? r : rr[k];
+        if (first) return rk[e];
+        const double *pk = k == rank ? (old_a ? pa : pb) : (old_a ? rpa[k] : rpb[k]);
+        return rk[e] + beta * pk[e];
+      };
       acc = 0.0;
       for (int e = threadIdx.x; e < nl; e += blockDim.x) {
         const int n = n0 + e;
         const unsigned m = nb[e];
-        const double xm = (m & 1) ? pv(n - sx) : ((PER && (m & 64)) ? pv(n + wx) : 0.0);
-        const double xp = (m & 2) ? pv(n + sx) : ((PER && (m & 128)) ? pv(n - wx) : 0.0);
-        const double ym = (m & 4) ? pv(n - sy) : ((PER && (m & 256)) ? pv(n + wy) : 0.0);
-        const double yp = (m & 8) ? pv(n + sy) : ((PER && (m & 512)) ? pv(n - wy) : 0.0);
-        const double zm = (m & 16) ? pv(n - 1) : ((PER && (m & 1024)) ? pv(n + wz) : 0.0);
-        const double zp = (m & 32) ? pv(n + 1) : ((PER && (m & 2048)) ? pv(n - wz) : 0.0);
+        const double xm = (m & 1) ? P(n - sx) : ((PER && (m & 64)) ? P(n + wx) : 0.0);
+        const double xp = (m & 2) ? P(n + sx) : ((PER && (m & 128)) ? P(n - wx) : 0.0);
+        const double ym = (m & 4) ? P(n - sy) : ((PER && (m & 256)) ? P(n + wy) : 0.0);
+        const double yp = (m & 8) ? P(n + sy) : ((PER && (m & 512)) ? P(n - wy) : 0.0);
+        const double zm = (m & 16) ? P(n - 1) : ((PER && (m & 1024)) ? P(n + wz) : 0.0);
+        const double zp = (m & 32) ? P(n + 1) : ((PER && (m & 2048)) ? P(n - wz) : 0.0);
         const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
-        const double pn = p[e];
-        const double qn = c * ((double)dc[e] * pn - s);
+        const double p = P(n);
+        pn[e] = p;
+        const double qn = c * ((double)dc[e] * p - s);
         q[e] = qn;
-        acc = acc + pn * qn;
+        acc = acc + p * qn;
       }
-      const double pq = cluster_sum(acc, 0);
+      const double pq = cluster_sum(acc);
       const double a = rho / pq;
       acc = 0.0;
       for (int e = threadIdx.x; e < nl; e += blockDim.x) {
-        x[e] = x[e] + a * p[e];
+        x[e] = x[e] + a * pn[e];
         const double rn = r[e] - a * q[e];
         r[e] = rn;
         acc = acc + rn * rn;
       }
-      const double rho1 = cluster_sum(acc, 1);
+      const double rho1 = cluster_sum(acc);
       it++;
       if (sqrt(rho1) <= tol * bnorm) break;
-      const double beta = rho1 / rho;
-      for (int e = threadIdx.x; e < nl; e += blockDim.x) p[e] = r[e] + beta * p[e];
-      cl.sync();  // p complete (every CTA) before the next matrix-vector product
+      beta = rho1 / rho;
       rho = rho1;
     }
   }
@@ -183,7 +207,7 @@ static void launch_cc(const Grid &g, double tol, int maxit, int *iters_out,
   const int N = g.nx * g.ny * g.nz;
   const int chunk = (N + kCK - 1) / kCK;
   using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
-  const size_t smem = (size_t)chunk * (4 * sizeof(double) + sizeof(NB) + 1);
+  const size_t smem = (size_t)chunk * (5 * sizeof(double) + sizeof(NB) + 1);
   static size_t configured = 0;
   static bool nonportable = false;
   if (kCK > 8 && !nonportable) {

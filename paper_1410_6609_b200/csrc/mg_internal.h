@@ -150,6 +150,20 @@ __host__ __device__ inline bool is_periodic(const Grid &g) {
 }
 
 // ---- kernel launchers (mg_kernels.cu) ---------------------------------------
+// the coarse end of a V-cycle in one persistent cluster kernel: levels
+// g[0..n-1] (whole grids, g[n-1] the coarsest), see k_vcycle_tail
+constexpr int kTailMax = 12;
+constexpr int kTailThreads = 512;
+struct TailLevels {
+  Grid g[kTailMax];
+  int n;
+};
+// CTAs of the tail's cluster on this device (0: clusters unavailable)
+int tail_cluster_ctas();
+bool vcycle_tail_supported(const Grid &coarsest);
+// 0, or -1 if the launch failed
+int launch_vcycle_tail(const TailLevels &T, int nu1, int nu2, double alpha, double tol,
+                       int maxit, double *cg_scr, int *iters_out, cudaStream_t s);
 void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s);
 void launch_resid_restrict(const Grid &f, const Grid &c, int cofs,
                            cudaStream_t s);

@@ -10,6 +10,7 @@
 // S_l the folded integer 7-point stencil of the level's own grid: centre
 // d = 6 + sum over touched faces (+1 Dirichlet, -1 Neumann), neighbours -1.
 // Hence no stencil is stored: the centre comes from the cell position.
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -50,22 +51,26 @@ __device__ __forceinline__ double2 ld2(const double *p) {
 // c_l is a power of two.  The other colour's x/y neighbours share
 // the half-index k; the z neighbours are O(k-1+p), O(k+p), p = z & 1.
 // ---------------------------------------------------------------------------
+// pairs (row, half-index pair) a half-sweep of g updates, one per thread
+__host__ __device__ inline long long smooth_items(const Grid &g) {
+  return (long long)g.nxl * g.ny * ((g.nzh + 1) >> 1);
+}
+
+// the two cells of pair t (no __restrict__: the persistent tail kernel
+// calls it on arrays other CTAs of its cluster wrote before a barrier)
 template <bool PER>
-__global__ void __launch_bounds__(kThreads)
-    k_smooth(Grid g, int color, int from_zero) {
+__device__ __forceinline__ void smooth_pair(const Grid &g, int color, int from_zero,
+                                            long long t) {
   const int nk2 = (g.nzh + 1) >> 1;  // odd nzh: the last pair is half used
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)g.nxl * g.ny * nk2;
-  if (t >= total) return;
   const int k2 = (int)(t % nk2);
   const long long r = t / nk2;
   const int j = (int)(r % g.ny);
   const int il = (int)(r / g.ny);
   const int i = g.x0 + il;
   const int p = (i + j + color) & 1;
-  double *__restrict__ own = color ? g.phiB : g.phiR;
-  const double *__restrict__ oth = color ? g.phiR : g.phiB;
-  const double *__restrict__ f = color ? g.fB : g.fR;
+  double *own = color ? g.phiB : g.phiR;
+  const double *oth = color ? g.phiR : g.phiB;
+  const double *f = color ? g.fB : g.fR;
   const long long b = rowbase(g, il, j);
   const int k = 2 * k2;
   const double2 fo = ld2(f + b + k);
@@ -107,6 +112,13 @@ __global__ void __launch_bounds__(kThreads)
     own[b + k] = out.x;
     if (PER) ghost_copies(g, own, il, j, k, out.x);
   }
+}
+
+template <bool PER>
+__global__ void __launch_bounds__(kThreads)
+    k_smooth(Grid g, int color, int from_zero) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < smooth_items(g)) smooth_pair<PER>(g, color, from_zero, t);
 }
 
 void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s) {
@@ -151,13 +163,13 @@ __device__ __forceinline__ double resid_at(const Grid &g, int il, int j,
 // residuals of C's 8 children, child bits (dx,dy,dz), dz fastest.  The fine
 // residual is never stored.  One thread per coarse cell.
 // ---------------------------------------------------------------------------
+__host__ __device__ inline long long restrict_items(const Grid &F) {
+  return (long long)(F.nxl >> 1) * (F.ny >> 1) * (F.nz >> 1);
+}
+
 template <bool PER>
-__global__ void __launch_bounds__(kThreads)
-    k_resid_restrict(Grid F, Grid C) {
-  const int ncz = F.nz >> 1, ncy = F.ny >> 1, ncx = F.nxl >> 1;
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)ncx * ncy * ncz;
-  if (t >= total) return;
+__device__ __forceinline__ void restrict_cell(const Grid &F, const Grid &C, long long t) {
+  const int ncz = F.nz >> 1, ncy = F.ny >> 1;
   const int K = (int)(t % ncz);
   const long long q = t / ncz;
   const int J = (int)(q % ncy);
@@ -177,6 +189,13 @@ __global__ void __launch_bounds__(kThreads)
   cf[rowbase(C, Ig - C.x0, J) + (K >> 1)] = 0.125 * s;
 }
 
+template <bool PER>
+__global__ void __launch_bounds__(kThreads)
+    k_resid_restrict(Grid F, Grid C) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < restrict_items(F)) restrict_cell<PER>(F, C, t);
+}
+
 void launch_resid_restrict(const Grid &f, const Grid &c, int /*cofs*/,
                            cudaStream_t s) {
   const long long total =
@@ -194,11 +213,12 @@ void launch_resid_restrict(const Grid &f, const Grid &c, int /*cofs*/,
 //     Phi(c) = Phi(c) + alpha * e(parent(c)),  parent = (i/2, j/2, z/2).
 // Red and black cells with half-index k both have parent z-index Z = k.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads)
-    k_prolong(Grid F, Grid C, double alpha) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long total = (long long)F.nxl * F.ny * F.nzh;
-  if (t >= total) return;
+__host__ __device__ inline long long prolong_items(const Grid &F) {
+  return (long long)F.nxl * F.ny * F.nzh;
+}
+
+__device__ __forceinline__ void prolong_cell(const Grid &F, const Grid &C, double alpha,
+                                             long long t) {
   const int k = (int)(t % F.nzh);
   const long long q = t / F.nzh;
   const int j = (int)(q % F.ny);
@@ -209,6 +229,12 @@ __global__ void __launch_bounds__(kThreads)
   const long long b = rowbase(F, il, j) + k;
   F.phiR[b] = F.phiR[b] + alpha * e;
   F.phiB[b] = F.phiB[b] + alpha * e;
+}
+
+__global__ void __launch_bounds__(kThreads)
+    k_prolong(Grid F, Grid C, double alpha) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < prolong_items(F)) prolong_cell(F, C, alpha, t);
 }
 
 void launch_prolong(const Grid &f, const Grid &c, int /*cofs*/, double alpha,
@@ -379,9 +405,14 @@ void launch_first_empty(const unsigned long long *counts, int n, double *host_ds
 // closed form as the smoother.  Dot products: per-thread partials in a fixed
 // order, warp shuffle tree, then every thread sums the warp partials in
 // warp order (one barrier per dot; two alternating partial arrays).
+// Two barriers per iteration: the direction p = r + beta p is not formed in
+// a pass of its own but where the next matrix-vector product needs it --
+// each thread evaluates r[k] + beta * p_old[k] (the same expression, hence
+// the same bits) for its cell and the six neighbours and stores its own
+// p_new in the other of two p buffers (p_old stays readable: no barrier).
 // ---------------------------------------------------------------------------
 static constexpr int kCgThreads = 1024;
-static constexpr long long kCgSmemMax = 6144;  // unknowns with smem vectors
+static constexpr long long kCgSmemMax = 4096;  // unknowns with smem vectors
 
 __device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
                                                  int z, int *col) {
@@ -401,36 +432,45 @@ __device__ __forceinline__ double cg_allsum(double v, double *part) {
   return s;
 }
 
+// doubles of a CG work area for N unknowns: x, r, two p buffers, q, then the
+// per-element neighbour bits (2 bytes) and centre (1 byte)
+__host__ __device__ inline size_t cg_area_doubles(long long N) {
+  return 5 * (size_t)N + ((size_t)N * 3 + 7) / 8;
+}
+
+// CG on grid g by the calling CTA (every thread must call it; the first
+// nthr of them hold elements -- the others add zeros to the dot products,
+// which leaves the sums' bits unchanged); `base`: a work area of
+// cg_area_doubles(N) (shared or global memory); part: 2 x 32 doubles of
+// shared memory
 template <bool PER>
-__global__ void __launch_bounds__(kCgThreads)
-    k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
+__device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*part)[32],
+                                       double tol, int maxit, int *iters_out,
+                                       int nthr) {
   using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
-  extern __shared__ double cg_sm[];
-  __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
-  const bool in_smem = N <= kCgSmemMax;
-  double *base = in_smem ? cg_sm : scr;
-  double *x = base, *r = base + N, *p = base + 2 * N, *q = base + 3 * N;
+  double *x = base, *r = base + N, *pa = base + 2 * N, *pbuf = base + 3 * N,
+         *q = base + 4 * N;
   // per-element geometry, computed once: neighbour bits (x-,x+,y-,y+,z-,z+):
   // bits 0-5 neighbour inside the level, bits 6-11 neighbour across a
   // periodic face (the opposite side's cell); and the centre d
   // (closed-form operator A = c (d - neighbours))
-  NB *nb = reinterpret_cast<NB *>(in_smem ? cg_sm + 4 * N : scr + 4 * N);
+  NB *nb = reinterpret_cast<NB *>(base + 5 * N);
   signed char *dc = reinterpret_cast<signed char *>(nb + N);
   const long long sx = (long long)g.ny * g.nz, sy = g.nz;
   const long long wx = (long long)(g.nx - 1) * sx, wy = (long long)(g.ny - 1) * sy,
                   wz = g.nz - 1;
   int pb = 0;
   double acc = 0.0;
-  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+  for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
     const int z = (int)(n % g.nz);
     const long long t = n / g.nz;
     const int j = (int)(t % g.ny), i = (int)(t / g.ny);
     const int in[6] = {i > 0, i < g.nx - 1, j > 0, j < g.ny - 1, z > 0, z < g.nz - 1};
     unsigned m = 0;
 #pragma unroll
-    for (int q = 0; q < 6; q++)
-      m |= in[q] ? (1u << q) : ((PER && g.per[q >> 1]) ? (64u << q) : 0u);
+    for (int a = 0; a < 6; a++)
+      m |= in[a] ? (1u << a) : ((PER && g.per[a >> 1]) ? (64u << a) : 0u);
     nb[n] = (NB)m;
     dc[n] = (signed char)centre_d(g, i, j, z);
     int col;
@@ -438,37 +478,42 @@ __global__ void __launch_bounds__(kCgThreads)
     const double b = col ? g.fB[idx] : g.fR[idx];
     x[n] = 0.0;
     r[n] = b;
-    p[n] = b;
     acc = acc + b * b;
   }
-  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes p, nb, dc
+  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes r, nb, dc
   pb ^= 1;
   const double bnorm = sqrt(rho);
   const double c = g.c;
+  double beta = 0.0;
+  double *po = pa, *pn = pbuf;  // p of the last iteration / of this one
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
+      // p = r (first iteration) or r + beta p_old, at any index
+      const bool first = it == 0;
+      auto P = [&](long long k) { return first ? r[k] : r[k] + beta * po[k]; };
       acc = 0.0;
-      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+      for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
         const unsigned m = nb[n];
-        const double xm = (m & 1) ? p[n - sx] : ((PER && (m & 64)) ? p[n + wx] : 0.0);
-        const double xp = (m & 2) ? p[n + sx] : ((PER && (m & 128)) ? p[n - wx] : 0.0);
-        const double ym = (m & 4) ? p[n - sy] : ((PER && (m & 256)) ? p[n + wy] : 0.0);
-        const double yp = (m & 8) ? p[n + sy] : ((PER && (m & 512)) ? p[n - wy] : 0.0);
-        const double zm = (m & 16) ? p[n - 1] : ((PER && (m & 1024)) ? p[n + wz] : 0.0);
-        const double zp = (m & 32) ? p[n + 1] : ((PER && (m & 2048)) ? p[n - wz] : 0.0);
+        const double xm = (m & 1) ? P(n - sx) : ((PER && (m & 64)) ? P(n + wx) : 0.0);
+        const double xp = (m & 2) ? P(n + sx) : ((PER && (m & 128)) ? P(n - wx) : 0.0);
+        const double ym = (m & 4) ? P(n - sy) : ((PER && (m & 256)) ? P(n + wy) : 0.0);
+        const double yp = (m & 8) ? P(n + sy) : ((PER && (m & 512)) ? P(n - wy) : 0.0);
+        const double zm = (m & 16) ? P(n - 1) : ((PER && (m & 1024)) ? P(n + wz) : 0.0);
+        const double zp = (m & 32) ? P(n + 1) : ((PER && (m & 2048)) ? P(n - wz) : 0.0);
         const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
-        const double pn = p[n];
-        const double qn = c * ((double)dc[n] * pn - s);
+        const double p = P(n);
+        pn[n] = p;
+        const double qn = c * ((double)dc[n] * p - s);
         q[n] = qn;
-        acc = acc + pn * qn;
+        acc = acc + p * qn;
       }
       const double pq = cg_allsum(acc, part[pb]);
       pb ^= 1;
       const double a = rho / pq;
       acc = 0.0;
-      for (long long n = threadIdx.x; n < N; n += blockDim.x) {
-        x[n] = x[n] + a * p[n];
+      for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
+        x[n] = x[n] + a * pn[n];
         const double rn = r[n] - a * q[n];
         r[n] = rn;
         acc = acc + rn * rn;
@@ -477,14 +522,15 @@ __global__ void __launch_bounds__(kCgThreads)
       pb ^= 1;
       it++;
       if (sqrt(rho1) <= tol * bnorm) break;
-      const double beta = rho1 / rho;
-      for (long long n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
-      __syncthreads();  // p complete before the next matrix-vector product
+      beta = rho1 / rho;
       rho = rho1;
+      double *t = po;
+      po = pn;
+      pn = t;
     }
   }
   __syncthreads();
-  for (long long n = threadIdx.x; n < N; n += blockDim.x) {
+  for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
     const int z = (int)(n % g.nz);
     const long long t = n / g.nz;
     int col;
@@ -494,25 +540,37 @@ __global__ void __launch_bounds__(kCgThreads)
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
+template <bool PER>
+__global__ void __launch_bounds__(kCgThreads)
+    k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
+  extern __shared__ double cg_sm[];
+  __shared__ double part[2][32];
+  const long long N = (long long)g.nx * g.ny * g.nz;
+  cg_cta<PER>(g, N <= kCgSmemMax ? cg_sm : scr, part, tol, maxit, iters_out,
+              (int)blockDim.x);
+}
+
 size_t coarse_cg_scratch_doubles(const Grid &g) {
-  // x, r, p, q + two bytes of neighbour bits and one of centre per element
-  return 5 * (size_t)g.nx * g.ny * g.nz;
+  return cg_area_doubles((long long)g.nx * g.ny * g.nz);
+}
+
+// 256 threads below 2048 unknowns, 512 from there (more warps hide the smem
+// latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at P = 8,
+// 476 vs 557 us in round 1; 1024 threads are slower again)
+static int cg_threads(long long N) {
+  int threads = (int)((N + 31) / 32 * 32);
+  const int cap = N >= 2048 ? 512 : 256;
+  return threads > cap ? cap : threads;
 }
 
 template <bool PER>
 static void launch_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
-  // 256 threads below 2048 unknowns, 512 from there (more warps hide the smem
-  // latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at
-  // P = 8, 476 vs 557 us; 1024 threads are slower again)
-  int threads = (int)((N + 31) / 32 * 32);
-  const int cap = N >= 2048 ? 512 : 256;
-  if (threads > cap) threads = cap;
+  const int threads = cg_threads(N);
   size_t smem = 0;
   if (N <= kCgSmemMax) {
-    // x, r, p, q + neighbour bits (1 byte; 2 with periodic wrap) + centre
-    smem = 4 * (size_t)N * sizeof(double) + (PER ? 3 : 2) * (size_t)N;
+    smem = cg_area_doubles(N) * sizeof(double);
     static size_t configured = 48 * 1024;
     if (smem > configured) {
       cudaFuncSetAttribute(k_coarse_cg<PER>,
@@ -1010,11 +1068,13 @@ void launch_unpack(const Grid &g, int field, double *nat, cudaStream_t s) {
 // planes 0 / nxl+1 incl. their ghost rows (x periodic, grid held whole).
 // Sources are interior elements only, so one pass needs no ordering.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) k_periodic_fill(Grid g) {
+__host__ __device__ inline long long periodic_fill_items(const Grid &g) {
+  if (!(g.gx || g.per[1])) return 0;
+  return ((g.gx ? 2LL * (g.ny + 2) : 0) + (g.per[1] ? 2LL * g.nxl : 0)) * g.nzh;
+}
+
+__device__ __forceinline__ void periodic_fill_elem(const Grid &g, long long t) {
   const long long rowsx = g.gx ? 2LL * (g.ny + 2) : 0;        // planes 0, nxl+1
-  const long long rowsy = g.per[1] ? 2LL * g.nxl : 0;          // rows 0, ny+1
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (rowsx + rowsy) * g.nzh) return;
   const int k = (int)(t % g.nzh);
   const long long r = t / g.nzh;
   int ap, ar;  // ghost element's array plane / row
@@ -1036,12 +1096,173 @@ __global__ void __launch_bounds__(kThreads) k_periodic_fill(Grid g) {
   g.phiB[dst] = g.phiB[src];
 }
 
+__global__ void __launch_bounds__(kThreads) k_periodic_fill(Grid g) {
+  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < periodic_fill_items(g)) periodic_fill_elem(g, t);
+}
+
 void launch_periodic_fill(const Grid &g, cudaStream_t s) {
   if (!(g.gx || g.per[1])) return;
   const long long rows = (g.gx ? 2LL * (g.ny + 2) : 0) + (g.per[1] ? 2LL * g.nxl : 0);
   const long long total = rows * g.nzh;
   if (total <= 0) return;
   k_periodic_fill<<<(unsigned)((total + kThreads - 1) / kThreads), kThreads, 0, s>>>(g);
+}
+
+
+
+// ---------------------------------------------------------------------------
+// The coarse end of the V-cycle in one persistent kernel (the "tail"): the
+// levels ls..L-1 of a cycle -- pre-smoothing, residual + restriction down to
+// the coarsest grid, CG there, prolongation + correction and post-smoothing
+// back up to level ls -- run by one thread-block
+// cluster, the steps separated by cluster barriers (barrier.cluster
+// arrive.release / wait.acquire: the global-memory writes of one step are
+// visible to every CTA of the cluster in the next).  On these small,
+// L2-resident levels (<= 32^3 cells) every step of the launch-per-step path
+// costs a kernel launch of a few microseconds for well under a microsecond
+// of work.  The per-cell arithmetic is the device functions the per-step
+// kernels use (smooth_pair, restrict_cell, prolong_cell, periodic_fill_elem,
+// cg_cta with the standalone CG's thread count), so the iterates are bitwise
+// those of the per-step path.
+// ---------------------------------------------------------------------------
+namespace {
+namespace cgr = cooperative_groups;
+}
+
+template <bool PER>
+__global__ void __launch_bounds__(kTailThreads)
+    k_vcycle_tail(TailLevels T, int nu1, int nu2, double alpha, double tol, int maxit,
+                  int cg_nthr, double *cg_scr, int *iters_out) {
+  extern __shared__ double tail_sm[];
+  __shared__ double part[2][32];
+  cgr::cluster_group cl = cgr::this_cluster();
+  const long long t0 = (long long)cl.block_rank() * blockDim.x + threadIdx.x;
+  const long long nt = (long long)cl.num_blocks() * blockDim.x;
+  auto half = [&](const Grid &g, int color, int from_zero) {
+    const long long n = smooth_items(g);
+    for (long long t = t0; t < n; t += nt) smooth_pair<PER>(g, color, from_zero, t);
+    cl.sync();
+  };
+  auto fill = [&](const Grid &g) {
+    if (!PER) return;
+    const long long n = periodic_fill_items(g);
+    if (n == 0) return;
+    for (long long t = t0; t < n; t += nt) periodic_fill_elem(g, t);
+    cl.sync();
+  };
+  for (int l = 0; l + 1 < T.n; l++) {
+    const Grid &g = T.g[l];
+    if (nu1 == 0) {  // Phi of a coarse level starts from 0
+      const long long ne = grid_elems(g);
+      for (long long e = t0; e < ne; e += nt) {
+        g.phiR[e] = 0.0;
+        g.phiB[e] = 0.0;
+      }
+      cl.sync();
+    }
+    for (int s = 0; s < nu1; s++) {
+      half(g, 0, s == 0);  // the first red sweep from Phi = 0
+      half(g, 1, 0);
+    }
+    const long long n = restrict_items(g);
+    for (long long t = t0; t < n; t += nt) restrict_cell<PER>(g, T.g[l + 1], t);
+    cl.sync();
+  }
+  const Grid &gc = T.g[T.n - 1];
+  if (cl.block_rank() == 0) {
+    const long long N = (long long)gc.nx * gc.ny * gc.nz;
+    cg_cta<PER>(gc, N <= kCgSmemMax ? tail_sm : cg_scr, part, tol, maxit, iters_out,
+                cg_nthr);
+  }
+  cl.sync();
+  fill(gc);
+  for (int l = T.n - 2; l >= 0; l--) {
+    const Grid &g = T.g[l];
+    const long long n = prolong_items(g);
+    for (long long t = t0; t < n; t += nt) prolong_cell(g, T.g[l + 1], alpha, t);
+    cl.sync();
+    fill(g);
+    for (int s = 0; s < nu2; s++) {
+      half(g, 0, 0);
+      half(g, 1, 0);
+    }
+  }
+}
+
+int tail_cluster_ctas() {
+  static int n = -1;
+  if (n < 0) {
+    // the largest cluster (<= 16, non-portable above 8) the device runs
+    cudaFuncSetAttribute(k_vcycle_tail<false>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    cudaFuncSetAttribute(k_vcycle_tail<true>,
+                         cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    n = 0;
+    for (int c = 16; c >= 1 && n == 0; c /= 2) {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(c);
+      cfg.blockDim = dim3(kTailThreads);
+      cfg.dynamicSmemBytes = 0;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = c;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, k_vcycle_tail<false>, &cfg) ==
+              cudaSuccess &&
+          ncl > 0)
+        n = c;
+    }
+    cudaGetLastError();
+  }
+  return n;
+}
+
+bool vcycle_tail_supported(const Grid &coarsest) {
+  const long long N = (long long)coarsest.nx * coarsest.ny * coarsest.nz;
+  return tail_cluster_ctas() > 0 && N <= kCgSmemMax && coarsest.nxl == coarsest.nx;
+}
+
+template <bool PER>
+static int launch_tail(const TailLevels &T, int nu1, int nu2, double alpha, double tol,
+                       int maxit, double *cg_scr, int *iters_out, cudaStream_t s) {
+  const Grid &gc = T.g[T.n - 1];
+  const long long N = (long long)gc.nx * gc.ny * gc.nz;
+  const size_t smem = cg_area_doubles(N) * sizeof(double);
+  static size_t configured = 48 * 1024;
+  if (smem > configured) {
+    cudaFuncSetAttribute(k_vcycle_tail<PER>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    configured = smem;
+  }
+  const int nc = tail_cluster_ctas();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nc);
+  cfg.blockDim = dim3(kTailThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = nc;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k_vcycle_tail<PER>, T, nu1, nu2, alpha, tol, maxit,
+                            cg_threads(N), cg_scr, iters_out) == cudaSuccess
+             ? 0
+             : -1;
+}
+
+int launch_vcycle_tail(const TailLevels &T, int nu1, int nu2, double alpha, double tol,
+                       int maxit, double *cg_scr, int *iters_out, cudaStream_t s) {
+  if (is_periodic(T.g[0]))
+    return launch_tail<true>(T, nu1, nu2, alpha, tol, maxit, cg_scr, iters_out, s);
+  return launch_tail<false>(T, nu1, nu2, alpha, tol, maxit, cg_scr, iters_out, s);
 }
 
 }  // namespace mg
