@@ -550,6 +550,32 @@ def test_bc_patch_dense_direct_solve():
     assert np.linalg.norm(o.phi() - u) / np.linalg.norm(u) < 1e-12
 
 
+def test_face_values_equal_ghost_cell_construction():
+    """Per-cell boundary values (orc_set_face_values, the Eq.18 Dirichlet data
+    of the Table 4 validation): the adapted RHS equals the
+    ghost-cell construction with per-cell values on every face,
+    Dirichlet and Neumann alike, and the solve matches the dense solution."""
+    shape, h = (8, 8, 4), 0.5
+    bt = [D, N, D, D, N, D]
+    o = oracle.Oracle(shape, h, bt, [0.0] * 6, min_coarse=1)
+    rng = np.random.default_rng(12)
+    ext = [(shape[1], shape[2]), (shape[1], shape[2]), (shape[0], shape[2]),
+           (shape[0], shape[2]), (shape[0], shape[1]), (shape[0], shape[1])]
+    va = [rng.uniform(-1, 1, e) for e in ext]
+    for q in range(6):
+        o.set_face_values(q, va[q])
+    ty = [np.full(e, t) for e, t in zip(ext, bt)]
+    f = rng.uniform(-1, 1, shape)
+    o.set_rhs(f)
+    b = f - dense.neg_laplacian_ghost(np.zeros(shape), h, ty, va, homogeneous=False)
+    assert np.allclose(o.rhs(0), b, rtol=0, atol=1e-13)
+    A = dense.dense_operator(shape, h, bt)
+    u = np.linalg.solve(A, b.reshape(-1)).reshape(shape)
+    st, cyc, hist = o.solve(1e-13, 80)
+    assert st == 0
+    assert np.linalg.norm(o.phi() - u) / np.linalg.norm(u) < 1e-11
+
+
 # --------------------------------------------------------------------------
 # Subsampling (P:485-489, Table 4) -- §8(f) N1
 # --------------------------------------------------------------------------
