@@ -116,6 +116,7 @@ __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
     const double b = col ? g.fB[idx] : g.fR[idx];
     x[e] = 0.0;
     r[e] = b;
+    pb[e] = 0.0;  // p_old of the first iteration: p = r + 0 * 0 = r
     acc = acc + b * b;
   }
   __syncthreads();  // the pointer tables
@@ -140,17 +141,18 @@ __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
-      const bool first = it == 0;
       // p_old in buffer a on odd iterations, b on even ones (p_new the other)
       const bool old_a = (it & 1) != 0;
       double *pn = old_a ? pb : pa;
-      // p = r or r + beta p_old of global unknown m (own chunk locally)
+      const double *po = old_a ? pa : pb;
+      // p = r + beta p_old of global unknown m: own chunk from local shared
+      // memory (shared-memory loads), other chunks through DSMEM
       auto P = [&](int m) {
-        const int k = m / chunk, e = m - k * chunk;
-        const double *rk = k == rank ? r : rr[k];
-        if (first) return rk[e];
-        const double *pk = k == rank ? (old_a ? pa : pb) : (old_a ? rpa[k] : rpb[k]);
-        return rk[e] + beta * pk[e];
+        const int e = m - n0;
+        if ((unsigned)e < (unsigned)chunk) return r[e] + beta * po[e];
+        const int k = m / chunk, ek = m - k * chunk;
+        const double *pk = old_a ? rpa[k] : rpb[k];
+        return rr[k][ek] + beta * pk[ek];
       };
       acc = 0.0;
       for (int e = threadIdx.x; e < nl; e += blockDim.x) {

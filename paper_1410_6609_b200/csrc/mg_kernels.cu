@@ -441,14 +441,17 @@ __host__ __device__ inline size_t cg_area_doubles(long long N) {
 // CG on grid g by the calling CTA (every thread must call it; the first
 // nthr of them hold elements -- the others add zeros to the dot products,
 // which leaves the sums' bits unchanged); `base`: a work area of
-// cg_area_doubles(N) (shared or global memory); part: 2 x 32 doubles of
-// shared memory
+// cg_area_doubles(N) (shared or global memory: callers pass a __shared__
+// array and a global pointer in separate calls, so that the inlined copy
+// for shared memory uses shared-memory loads); part: 2 x 32 doubles of
+// shared memory.  The neighbour values are loaded unconditionally from a
+// valid index and selected (no branches in the matrix-vector product).
 template <bool PER>
 __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*part)[32],
                                        double tol, int maxit, int *iters_out,
                                        int nthr) {
   using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
-  const long long N = (long long)g.nx * g.ny * g.nz;
+  const int N = g.nx * g.ny * g.nz;
   double *x = base, *r = base + N, *pa = base + 2 * N, *pbuf = base + 3 * N,
          *q = base + 4 * N;
   // per-element geometry, computed once: neighbour bits (x-,x+,y-,y+,z-,z+):
@@ -457,15 +460,15 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   // (closed-form operator A = c (d - neighbours))
   NB *nb = reinterpret_cast<NB *>(base + 5 * N);
   signed char *dc = reinterpret_cast<signed char *>(nb + N);
-  const long long sx = (long long)g.ny * g.nz, sy = g.nz;
-  const long long wx = (long long)(g.nx - 1) * sx, wy = (long long)(g.ny - 1) * sy,
-                  wz = g.nz - 1;
+  const int sx = g.ny * g.nz, sy = g.nz;
+  const int wx = (g.nx - 1) * sx, wy = (g.ny - 1) * sy, wz = g.nz - 1;
+  const int nend = (int)threadIdx.x < nthr ? N : 0;  // idle threads: no elements
   int pb = 0;
   double acc = 0.0;
-  for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
-    const int z = (int)(n % g.nz);
-    const long long t = n / g.nz;
-    const int j = (int)(t % g.ny), i = (int)(t / g.ny);
+  for (int n = threadIdx.x; n < nend; n += nthr) {
+    const int z = n % g.nz;
+    const int t = n / g.nz;
+    const int j = t % g.ny, i = t / g.ny;
     const int in[6] = {i > 0, i < g.nx - 1, j > 0, j < g.ny - 1, z > 0, z < g.nz - 1};
     unsigned m = 0;
 #pragma unroll
@@ -478,6 +481,7 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
     const double b = col ? g.fB[idx] : g.fR[idx];
     x[n] = 0.0;
     r[n] = b;
+    pa[n] = 0.0;  // p_old of the first iteration: p = r + 0 * 0 = r
     acc = acc + b * b;
   }
   double rho = cg_allsum(acc, part[pb]);  // barrier also publishes r, nb, dc
@@ -489,20 +493,26 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   int it = 0;
   if (bnorm > 0.0) {
     while (it < maxit) {
-      // p = r (first iteration) or r + beta p_old, at any index
-      const bool first = it == 0;
-      auto P = [&](long long k) { return first ? r[k] : r[k] + beta * po[k]; };
       acc = 0.0;
-      for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
+      for (int n = threadIdx.x; n < nend; n += nthr) {
         const unsigned m = nb[n];
-        const double xm = (m & 1) ? P(n - sx) : ((PER && (m & 64)) ? P(n + wx) : 0.0);
-        const double xp = (m & 2) ? P(n + sx) : ((PER && (m & 128)) ? P(n - wx) : 0.0);
-        const double ym = (m & 4) ? P(n - sy) : ((PER && (m & 256)) ? P(n + wy) : 0.0);
-        const double yp = (m & 8) ? P(n + sy) : ((PER && (m & 512)) ? P(n - wy) : 0.0);
-        const double zm = (m & 16) ? P(n - 1) : ((PER && (m & 1024)) ? P(n + wz) : 0.0);
-        const double zp = (m & 32) ? P(n + 1) : ((PER && (m & 2048)) ? P(n - wz) : 0.0);
+        // p = r + beta p_old at neighbour (bit `in`: inside; bit `pe`: across
+        // a periodic face) -- a valid index is loaded either way, the value
+        // selected
+        auto nbr = [&](unsigned in, unsigned pe, int kin, int kpe) {
+          const bool vi = (m & in) != 0, vp = PER && (m & pe) != 0;
+          const int k = vi ? kin : (vp ? kpe : n);
+          const double v = r[k] + beta * po[k];
+          return (vi || vp) ? v : 0.0;
+        };
+        const double xm = nbr(1, 64, n - sx, n + wx);
+        const double xp = nbr(2, 128, n + sx, n - wx);
+        const double ym = nbr(4, 256, n - sy, n + wy);
+        const double yp = nbr(8, 512, n + sy, n - wy);
+        const double zm = nbr(16, 1024, n - 1, n + wz);
+        const double zp = nbr(32, 2048, n + 1, n - wz);
         const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
-        const double p = P(n);
+        const double p = r[n] + beta * po[n];
         pn[n] = p;
         const double qn = c * ((double)dc[n] * p - s);
         q[n] = qn;
@@ -512,7 +522,7 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
       pb ^= 1;
       const double a = rho / pq;
       acc = 0.0;
-      for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
+      for (int n = threadIdx.x; n < nend; n += nthr) {
         x[n] = x[n] + a * pn[n];
         const double rn = r[n] - a * q[n];
         r[n] = rn;
@@ -530,11 +540,11 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
     }
   }
   __syncthreads();
-  for (long long n = threadIdx.x; n < (threadIdx.x < nthr ? N : 0); n += nthr) {
-    const int z = (int)(n % g.nz);
-    const long long t = n / g.nz;
+  for (int n = threadIdx.x; n < nend; n += nthr) {
+    const int z = n % g.nz;
+    const int t = n / g.nz;
     int col;
-    const long long idx = split_index(g, (int)(t / g.ny), (int)(t % g.ny), z, &col);
+    const long long idx = split_index(g, t / g.ny, t % g.ny, z, &col);
     (col ? g.phiB : g.phiR)[idx] = x[n];
   }
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
@@ -546,8 +556,10 @@ __global__ void __launch_bounds__(kCgThreads)
   extern __shared__ double cg_sm[];
   __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
-  cg_cta<PER>(g, N <= kCgSmemMax ? cg_sm : scr, part, tol, maxit, iters_out,
-              (int)blockDim.x);
+  if (N <= kCgSmemMax)
+    cg_cta<PER>(g, cg_sm, part, tol, maxit, iters_out, (int)blockDim.x);
+  else
+    cg_cta<PER>(g, scr, part, tol, maxit, iters_out, (int)blockDim.x);
 }
 
 size_t coarse_cg_scratch_doubles(const Grid &g) {
@@ -1172,8 +1184,10 @@ __global__ void __launch_bounds__(kTailThreads)
   const Grid &gc = T.g[T.n - 1];
   if (cl.block_rank() == 0) {
     const long long N = (long long)gc.nx * gc.ny * gc.nz;
-    cg_cta<PER>(gc, N <= kCgSmemMax ? tail_sm : cg_scr, part, tol, maxit, iters_out,
-                cg_nthr);
+    if (N <= kCgSmemMax)
+      cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
+    else
+      cg_cta<PER>(gc, cg_scr, part, tol, maxit, iters_out, cg_nthr);
   }
   cl.sync();
   fill(gc);
