@@ -5,9 +5,10 @@
 // (natural order) split into kCK contiguous chunks, one per CTA of the
 // cluster, each chunk's vectors in that CTA's shared memory.  The matrix-
 // vector product reads neighbour values of other chunks through distributed
-// shared memory; dot products are per-CTA partials (warp-shuffle tree, warps
-// in order) that every thread sums in cluster-rank order after a cluster
-// barrier, so all CTAs take the same decisions.  The large coarsest grids of
+// shared memory; dot products are per-CTA partials (fixed shuffle trees over
+// the warp and over the warps) that every thread sums by a fixed pairwise
+// tree in cluster-rank order after a cluster barrier, so all CTAs take the
+// same decisions.  The large coarsest grids of
 // agglomerated multi-GPU runs (64 x 8 x 8 at P = 8) spread over kCK SMs.
 // Round 1 (three cluster barriers per iteration, partials read remotely):
 // 0.42 ms for 64 x 8 x 8 vs 0.48 ms single-CTA; clusters of 4 (0.51) and 16
@@ -47,15 +48,19 @@ __device__ __forceinline__ long long split_at(const Grid &g, int n, int *col) {
   return (long long)(i + 1) * g.plane + (long long)(j + 1) * g.pz + (z >> 1);
 }
 
-// this CTA's partial of a dot product (thread 0's return value is valid)
+// this CTA's partial of a dot product (valid in warp 0): fixed butterfly
+// trees over the warp, then over the warp partials (zero-padded to 32)
 __device__ __forceinline__ double cta_partial(double v, double *wpart) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) wpart[threadIdx.x >> 5] = v;
   __syncthreads();
   double s = 0.0;
-  if (threadIdx.x == 0)
-    for (int w = 0; w < (int)(blockDim.x >> 5); w++) s = s + wpart[w];
+  if (threadIdx.x < 32) {
+    s = threadIdx.x < (blockDim.x >> 5) ? wpart[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  }
   return s;
 }
 
@@ -128,11 +133,16 @@ __global__ void __cluster_dims__(kCK, 1, 1) __launch_bounds__(kCT)
 #pragma unroll
       for (int k = 0; k < kCK; k++) rslot[k][sl * kCK + rank] = s;
     cl.sync();
-    double tot = 0.0;
+    // the CTA partials in rank order, as a fixed pairwise tree
+    double t[kCK];
 #pragma unroll
-    for (int k = 0; k < kCK; k++) tot = tot + slots[sl][k];
+    for (int k = 0; k < kCK; k++) t[k] = slots[sl][k];
+#pragma unroll
+    for (int w = 1; w < kCK; w <<= 1)
+#pragma unroll
+      for (int k = 0; k + w < kCK; k += 2 * w) t[k] = t[k] + t[k + w];
     sl ^= 1;
-    return tot;
+    return t[0];
   };
   double rho = cluster_sum(acc);  // the barrier also publishes r
   const double bnorm = sqrt(rho);

@@ -420,15 +420,21 @@ __device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
   return rowbase(g, il, j) + (z >> 1);
 }
 
-// sum over the block of per-thread values; one barrier; all threads get it
+// sum over the block of per-thread values; one barrier; all threads get it.
+// Fixed trees: the warp's butterfly, then the warp partials (zero-padded to
+// 32) by a butterfly in every warp -- log-depth dependency chains, where a
+// serial sum over the warps would put nw dependent fp64 additions on the
+// CG's critical path every iteration.
 __device__ __forceinline__ double cg_allsum(double v, double *part) {
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = v;
   __syncthreads();
   const int nw = (blockDim.x + 31) >> 5;
-  double s = 0.0;
-  for (int w = 0; w < nw; w++) s = s + part[w];
+  const int lane = threadIdx.x & 31;
+  double s = lane < nw ? part[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   return s;
 }
 

@@ -47,7 +47,7 @@ def check_history(hg, ho):
     assert len(hg) == len(ho)
     r0 = ho[0]
     for a, b in zip(hg, ho):
-        assert abs(a - b) <= 1e-8 * b + 1e-14 * r0, (a, b)
+        assert abs(a - b) <= 1e-8 * b + 1e-15 * r0, (a, b)
 
 
 def bench_solver(mg, w, **kw):

@@ -46,7 +46,7 @@ def check_history(hg, ho):
     assert len(hg) == len(ho)
     r0 = ho[0]
     for a, b in zip(hg, ho):
-        assert abs(a - b) <= 1e-8 * b + 1e-14 * r0, (a, b)
+        assert abs(a - b) <= 1e-8 * b + 1e-15 * r0, (a, b)
 
 
 def setup(M, shape, h, bc, fused, solid=None, eps=None, oracle_too=True, **kw):
@@ -147,21 +147,25 @@ def test_fused_norm_loopback_slabs(mg, Pn):
 
 
 def test_fused_norm_config3_size(mg):
-    """512^3 (the bench workload): the fused kernel's norm of cycle k equals
-    the separate norm pass on the pre-smoothed iterate, reproduced through
-    the step API from the previous iterate."""
-    w = W.cfg3(256, seed=0, cycles=3)
-    s, _ = setup(mg, w.shape, w.h, "mixed", True, oracle_too=False, min_coarse=8)
+    """512^3, the bench's config-3 workload in the bench's launch
+    configuration (own stream, graph): the fused kernel's norm of cycle k
+    equals the ORACLE's norm of the pre-smoothed iterate -- the oracle takes
+    the GPU's iterate of cycle k-1 (per-cell steps are bitwise, so its two
+    red/black pairs reproduce the GPU's pre-smoothed state exactly) and sums
+    the residual serially (reading c11)."""
+    import torch
+    w = W.cfg3(512, seed=0, cycles=2)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8, fused_norm=True,
+                     stream=torch.cuda.Stream())
     s.set_rhs(w.rhs)
-    t, _ = setup(mg, w.shape, w.h, "mixed", False, oracle_too=False, min_coarse=8)
-    t.set_rhs(w.rhs)
-    for _ in range(3):
-        t.set_solution(s.get_solution())
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=8, max_levels=1)
+    o.set_rhs(w.rhs)
+    for _ in range(w.cycles):
+        o.set_phi(s.get_solution())
         r = s.vcycle()
         for _ in range(2):
-            t.smooth_half(0, 0)
-            t.smooth_half(0, 1)
-        ref = t.residual_norm()
+            o.smooth_half(0, 0)
+            o.smooth_half(0, 1)
+        ref = o.residual_norm()
         assert abs(r - ref) <= 1e-12 * ref, (r, ref)
     s.close()
-    t.close()

@@ -62,7 +62,7 @@ def test_timestep_parity_channel(mg):
     r0 = res[0][2]
     for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
         assert ncyc == (5 if k == 0 else 1)
-        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (k, rg, ro)
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-15 * r0, (k, rg, ro)
         assert rel(pg, po) <= 1e-10
         assert np.abs(Fo).max() > 0
         assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
@@ -81,7 +81,7 @@ def test_timestep_parity_periodic_channel(mg):
     res = run_steps(mg, w, 4, periodic=(True, False, True), amplitude=0.8)
     r0 = res[0][2]
     for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
-        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (k, rg, ro)
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-15 * r0, (k, rg, ro)
         assert rel(pg, po) <= 1e-10
         assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
 
@@ -111,7 +111,7 @@ def test_timestep_tolerance_mode(mg):
             r = o.vcycle()
             n += 1
         assert ncyc == n and rg <= tol
-        assert abs(rg - r) <= 1e-8 * r + 1e-14 * r0
+        assert abs(rg - r) <= 1e-8 * r + 1e-15 * r0
 
 
 def test_timestep_errors(mg):
