@@ -575,6 +575,8 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
 // 256 threads below 2048 unknowns, 512 from there (more warps hide the smem
 // latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at P = 8,
 // 476 vs 557 us in round 1; 1024 threads are slower again)
+// (round 2 A/B, scripts/cg_probe.py: caps of 64/128 per block are slower,
+// 512/1024 no faster -- the iteration is bound by its dependency chain)
 static int cg_threads(long long N) {
   int threads = (int)((N + 31) / 32 * 32);
   const int cap = N >= 2048 ? 512 : 256;

@@ -4,7 +4,7 @@ Per-cell steps (smoother half-sweeps, residual + restriction, prolongation,
 sphere RHS, BC adaptation, layout conversion) must be BITWISE equal for
 power-of-two h ("Parity contract"); whole V-cycles must match in
 Phi to relative L2 1e-10 and in residual history to 1e-8 relative (north_star)
-with the rounding-floor clause |dr_k| <= 1e-8 r_k + 1e-14 r_0 (reading c21,
+with the rounding-floor clause |dr_k| <= 1e-8 r_k + 1e-15 r_0 (reading c21,
 DESIGN.md: per-cell steps are bitwise, so the only differences are the CG and
 norm reductions; an ulp-level difference in Phi moves the residual by about
 eps*||A||*||Phi||, measured at 1.2e-16 r_0 on config 1).
