@@ -75,6 +75,16 @@ def run_oracle(w, solid=None, max_cycles=60):
     return hist, o.phi(), dt
 
 
+def floor_cycle(hist):
+    """The cycle at which the residual reaches the fp64 rounding floor
+    (reading c21): the first cycle whose reduction factor r_k / r_{k-1}
+    exceeds 0.5 (the V-cycle's own factor is 0.04-0.2); None if none."""
+    for k in range(1, len(hist)):
+        if hist[k] > 0.5 * hist[k - 1]:
+            return k
+    return None
+
+
 def factor(hist):
     h = np.asarray(hist)
     h = h[h > 1e-13 * h[0]]
@@ -85,7 +95,7 @@ def factor(hist):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "r01_configs.md"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_configs.md"))
     ap.add_argument("--full", action="store_true",
                     help="also run configs 3/4/5 at full size on the GPU")
     a = ap.parse_args()
@@ -101,9 +111,9 @@ def main():
     w5 = W.cfg5(scale=8, n_spheres=int(round(50000 / 512)))
     cases.append(("cfg5 reduced 256x64x64 beam mask + spheres, V(3,3) to 1e-8", w5, w5.solid, True))
     if a.full:
-        cases.append(("cfg3 512^3 random, V(2,2), 20 cycles (full size)", W.cfg3(512), None, False))
+        cases.append(("cfg3 512^3 random, V(2,2), 20 cycles (full size)", W.cfg3(512), None, True))
         cases.append(("cfg4 512^3 channel + 7417 spheres R=6, V(2,2) to 1e-8 (P=1, full size)",
-                      W.cfg4(P=1, n=512), None, False))
+                      W.cfg4(P=1, n=512), None, True))
         w5f = W.cfg5(scale=1)
         cases.append(("cfg5 2048x512x512 beam mask + 50k spheres, V(3,3) to 1e-8 (P=1, full size)",
                       w5f, w5f.solid, False))
@@ -116,7 +126,9 @@ def main():
                    mcells_s=cells / (res["ms_per_cycle"] * 1e-3) / 1e6,
                    factor=factor(res["hist"]), final_rel=res["hist"][-1] / res["hist"][0],
                    launches=res["launches"], levels=len(res["levels"]),
-                   coarsest=res["levels"][-1])
+                   coarsest=res["levels"][-1], floor_cycle=floor_cycle(res["hist"]))
+        fc = row["floor_cycle"]
+        row["floor_rel"] = res["hist"][fc] / res["hist"][0] if fc else None
         if with_oracle:
             ho, po, dt = run_oracle(w, solid)
             n = min(len(ho), len(res["hist"]))
@@ -124,22 +136,31 @@ def main():
             row["phi_rel_l2"] = float(np.linalg.norm(phi - po) / np.linalg.norm(po))
             row["hist_max_rel"] = float(max(abs(a - b) / b for a, b in
                                             zip(res["hist"][:n], ho[:n])))
+            # the history clause |dr_k| <= 1e-8 r_k + c r_0: the smallest c
+            row["hist_floor_c"] = float(max(max(abs(a - b) - 1e-8 * b, 0.0) / ho[0]
+                                            for a, b in zip(res["hist"][:n], ho[:n])))
             row["oracle_s"] = dt
         rows.append(row)
         print(json.dumps(row), flush=True)
-    md = ["# Config runs on one B200 (round 1)", "",
+    md = ["# Config runs on one B200 (round 2)", "",
           "Per-cycle time: median of CUDA events around `mg_vcycle` (graph "
           "launch + norm readback).  Oracle columns: the CPU oracle on the same "
-          "inputs (host cores of the GPU box).", "",
+          "inputs (host cores of the GPU box).  `floor at` = the cycle where the "
+          "residual reaches the fp64 rounding floor (first cycle with r_k > 0.5 "
+          "r_{k-1}, reading c21) and r_k/r_0 there; `clause c` = the smallest c with "
+          "|r_k(GPU) - r_k(oracle)| <= 1e-8 r_k + c r_0 over the history (the tests "
+          "use c = 1e-15).", "",
           "| config | cells | levels (coarsest) | cycles | ms/cycle | Mcells/s | "
-          "factor | r_k/r_0 | Phi rel-L2 vs oracle | max hist rel diff | oracle cycles |",
-          "|---|---|---|---|---|---|---|---|---|---|---|"]
+          "factor | r_k/r_0 | floor at (r/r_0) | Phi rel-L2 vs oracle | clause c | "
+          "oracle cycles |",
+          "|---|---|---|---|---|---|---|---|---|---|---|---|"]
     for r in rows:
-        md.append("| %s | %d | %d %s | %d | %.3f | %.0f | %.3f | %.1e | %s | %s | %s |" % (
+        md.append("| %s | %d | %d %s | %d | %.3f | %.0f | %.3f | %.1e | %s | %s | %s | %s |" % (
             r["name"], int(np.prod(r["shape"])), r["levels"], tuple(r["coarsest"]),
             r["cycles"], r["ms_per_cycle"], r["mcells_s"], r["factor"], r["final_rel"],
+            ("%d (%.1e)" % (r["floor_cycle"], r["floor_rel"])) if r["floor_cycle"] else "not reached",
             "%.1e" % r["phi_rel_l2"] if "phi_rel_l2" in r else "-",
-            "%.1e" % r["hist_max_rel"] if "hist_max_rel" in r else "-",
+            "%.1e" % r["hist_floor_c"] if "hist_floor_c" in r else "-",
             r.get("oracle_cycles", "-")))
     os.makedirs(os.path.dirname(a.out), exist_ok=True)
     with open(a.out, "w") as fh:
