@@ -94,10 +94,8 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
   // j0-1 .. j0+TY).  The corrected other colour is NOT written back: the
   // half-sweep of the other colour that follows overwrites every one of its
   // cells without reading them (and a write-back would race with the TMA
-  // halo reads of neighbouring CTAs).  Iteration q corrects ring plane q+2
-  // (read from iteration q+1 on, after that iteration's top barrier -- no
-  // barrier of its own), and the coarse values are loaded one plane ahead of
-  // that (load_e) so their latency hides behind a plane's work.
+  // halo reads of neighbouring CTAs).  The coarse values are loaded one plane
+  // ahead (load_e) so their latency hides behind the previous plane's work.
   // Work split: task t = (coarse row jr, 64-wide chunk c), t = warp + TY*m:
   // the tile rows j0-1 .. j0+TY have the parent rows J = j0/2 - 1 + jr,
   // jr = 0 .. TY/2 + 1; the two sibling rows 2J, 2J+1 (tile rows 2jr-1,
@@ -169,11 +167,8 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       if (tOkB[m]) add(slot + tRowA[m] + pz, tK[m], E[m]);
     }
   };
-  // coarse values of the next plane to correct: the loop corrects plane
-  // q+2 in iteration q (no barrier of its own: the next iteration's top
-  // barrier publishes it), so E runs three planes ahead of the sweep
   double2 E[kTPW];
-  if (PROLONG && nplanes > 3) load_e(3, E);
+  if (PROLONG && nplanes > 2) load_e(2, E);
 
   // f (and, masked, the own face codes) of the first plane into registers
   double2 fr[NCH];
@@ -207,23 +202,19 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
     }
     mbar_wait(&bars[(q + 1) % kSlots], ((q + 1) / kSlots) & 1);
     if (PROLONG) {
-      if (q == 1) {  // planes 0, 1, 2: corrected before the first sweep
+      if (q == 1) {
         double2 E0[kTPW];
-        for (int p = 0; p < 3 && p < nplanes; p++) {
-          load_e(p, E0);
-          apply_e(p, E0);
-        }
-        __syncthreads();
+        load_e(0, E0);
+        apply_e(0, E0);
+        load_e(1, E0);
+        apply_e(1, E0);
       }
-      // plane q+2 (not read in this iteration; TMA issued one iteration ago)
-      if (q + 2 < nplanes) {
-        mbar_wait(&bars[(q + 2) % kSlots], ((q + 2) / kSlots) & 1);
-        apply_e(q + 2, E);
-        // fine planes 2I and 2I+1 share the parent plane I: keep E (the same
-        // tasks, the same coarse values) instead of loading it again
-        const int ia = g.x0 + i0 + q + 1, ib = ia + 1;  // global planes q+2, q+3
-        if (q + 3 < nplanes && (ia >> 1) != (ib >> 1)) load_e(q + 3, E);
-      }
+      apply_e(q + 1, E);
+      // fine planes 2I and 2I+1 share the parent plane I: keep E (the same
+      // tasks, the same coarse values) instead of loading it again
+      const int ia = g.x0 + i0 + q, ib = ia + 1;  // global planes q+1, q+2
+      if (q + 2 < nplanes && (ia >> 1) != (ib >> 1)) load_e(q + 2, E);
+      __syncthreads();
     }
 
     // prefetch f of the next plane
