@@ -1465,7 +1465,8 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
       B.nb[a] = (ext + bc - 1) / bc;
       nbins *= (size_t)B.nb[a];
     }
-    const size_t need = nbins * (1 + mg::kBinCap);
+    // + neighbour lists: nn[n], nbr[n kNbMax], list[2n], nlist[2]
+    const size_t need = nbins * (1 + mg::kBinCap) + (size_t)n * (3 + mg::kNbMax) + 2;
     if (need > c->bins_cap) {
       if (c->bins) cudaFree(c->bins);
       c->bins = nullptr;
@@ -1475,11 +1476,18 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     }
     B.count = c->bins;
     B.items = c->bins + nbins;
+    mg::SphereLists S;
+    S.nn = B.items + nbins * mg::kBinCap;
+    S.nbr = S.nn + n;
+    S.list = S.nbr + (size_t)n * mg::kNbMax;
+    S.nlist = S.list + 2 * (size_t)n;
     CK(cudaMemsetAsync(B.count, 0, nbins * sizeof(int), c->stream));
+    CK(cudaMemsetAsync(S.nlist, 0, 2 * sizeof(int), c->stream));
     mg::launch_sphere_bin(c->g[0][0], c->h, n, c->sph, B, c->stream);
+    mg::launch_sphere_neighbours(c->g[0][0], c->h, n, c->sph, B, S, c->stream);
     mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, c->sph, cnt, c->stream);
     for (const Grid &g : c->g[0])
-      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt, B,
+      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt, S,
                                 c->stream);
     CK(cudaGetLastError());
   }

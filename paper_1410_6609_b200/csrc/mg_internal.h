@@ -205,11 +205,20 @@ struct SphereBins {
   int *count, *items;
   double rmax;
 };
+// per-sphere neighbour lists (kNbMax entries each), their lengths, and the
+// spheres split into isolated ones (list[0..nlist[0])) and the others
+// (list[n..n+nlist[1])); nlist zeroed by the caller
+constexpr int kNbMax = 128;
+struct SphereLists {
+  int *nn, *nbr, *list, *nlist;
+};
 void launch_sphere_bin(const Grid &g, double h, int n, const double *sph,
                        const SphereBins &B, cudaStream_t s);
+void launch_sphere_neighbours(const Grid &g, double h, int n, const double *sph,
+                              const SphereBins &B, const SphereLists &S, cudaStream_t st);
 void launch_sphere_scatter(const Grid &g, double h, int subsample, int n,
                            const double *sph, int normalization,
-                           const unsigned long long *counts, const SphereBins &B,
+                           const unsigned long long *counts, const SphereLists &S,
                            cudaStream_t s);
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);

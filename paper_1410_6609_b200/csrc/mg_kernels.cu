@@ -500,6 +500,29 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   if (bnorm > 0.0) {
     while (it < maxit) {
       acc = 0.0;
+#ifdef MG_CG_SEPARATE_P
+      for (int n = threadIdx.x; n < nend; n += nthr) {
+        const unsigned m = nb[n];
+        auto nbr = [&](unsigned in, unsigned pe, int kin, int kpe) {
+          const bool vi = (m & in) != 0, vp = PER && (m & pe) != 0;
+          const int k = vi ? kin : (vp ? kpe : n);
+          const double v = po[k];
+          return (vi || vp) ? v : 0.0;
+        };
+        const double xm = nbr(1, 64, n - sx, n + wx);
+        const double xp = nbr(2, 128, n + sx, n - wx);
+        const double ym = nbr(4, 256, n - sy, n + wy);
+        const double yp = nbr(8, 512, n + sy, n - wy);
+        const double zm = nbr(16, 1024, n - 1, n + wz);
+        const double zp = nbr(32, 2048, n + 1, n - wz);
+        const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
+        const double p = po[n];
+        const double qn = c * ((double)dc[n] * p - s);
+        q[n] = qn;
+        acc = acc + p * qn;
+      }
+      pn = po;
+#else
       for (int n = threadIdx.x; n < nend; n += nthr) {
         const unsigned m = nb[n];
         // p = r + beta p_old at neighbour (bit `in`: inside; bit `pe`: across
@@ -524,6 +547,7 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
         q[n] = qn;
         acc = acc + p * qn;
       }
+#endif
       const double pq = cg_allsum(acc, part[pb]);
       pb ^= 1;
       const double a = rho / pq;
@@ -540,6 +564,11 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
       if (sqrt(rho1) <= tol * bnorm) break;
       beta = rho1 / rho;
       rho = rho1;
+#ifdef MG_CG_SEPARATE_P
+      for (int n = threadIdx.x; n < nend; n += nthr) po[n] = r[n] + beta * po[n];
+      __syncthreads();  // p complete before the next matrix-vector product
+      continue;
+#endif
       double *t = po;
       po = pn;
       pn = t;
@@ -621,16 +650,18 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
 //                     ascending sphere order -- the oracle's "overlapping
 //                     spheres add in sphere order" exactly, and deterministic
 //                     (no atomics).  The other spheres that can reach a cell
-//                     of sphere p are found first: a uniform grid of bins
-//                     (k_sphere_bin, bins wider than any two radii) gives the
-//                     candidates of the bins around p, which pass a
-//                     conservative distance test and are sorted into an
-//                     ascending list in shared memory.  A full bin or more
-//                     than kNbMax neighbours make every cell scan all spheres
-//                     instead -- slow, still exact.
+//                     of sphere p are found first (k_sphere_neighbours): a
+//                     uniform grid of bins (k_sphere_bin, bins wider than any
+//                     two radii) gives the candidates of the bins around p,
+//                     which pass a conservative distance test and are sorted
+//                     into an ascending list.  A full bin or more than kNbMax
+//                     neighbours make every cell scan all spheres instead --
+//                     slow, still exact.  Isolated spheres (the common case)
+//                     take a lean scatter kernel of their own.
 // sph holds (cx, cy, cz, R, Q) per sphere.  Every cell not covered keeps the
 // value it has (the caller zeroes f first).
 // ---------------------------------------------------------------------------
+template <bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_sphere_count(Grid g, double h, int s, const double *sph,
                    unsigned long long *counts) {
@@ -640,8 +671,10 @@ __global__ void __launch_bounds__(kThreads)
   const double R = sph[5 * p + 3];
   const double R2 = R * R;
   const double hs = h / (double)s;
-  double img[27][3];
-  const int nimg = sph::images(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], img);
+  sph::Images<PER> im;
+  sph::make_images<PER>(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], im);
+  const int nimg = im.n;
+  auto &img = im.c;
   // threads own (j, k) columns of the box and walk along x: no per-cell
   // index division; integer counts are exact in any order
   long long cnt = 0;
@@ -662,7 +695,6 @@ __global__ void __launch_bounds__(kThreads)
   if (threadIdx.x == 0) counts[p] = (unsigned long long)np;
 }
 
-static constexpr int kNbMax = 128;  // neighbour list entries per sphere
 
 // floor division for possibly negative cell indices
 __device__ __forceinline__ int fdiv(int a, int b) {
@@ -743,15 +775,96 @@ __device__ __forceinline__ double sphere_value(const double *q, double np, int c
   return (q[4] * (double)cnt) / (np * (h * h * h));
 }
 
+// neighbour lists: for sphere p the spheres that may share a cell with it --
+// the candidates of the bins within R_p + R_max + 2h (+ 2 cells of margin)
+// of p's centre cell on every axis (periodic axes wrap; their bins divide
+// the axis), then the distance test, then an ascending sort (ranks; the
+// entries are distinct).  nn[p] = their number (kNbMax + 1: a full bin or
+// more than kNbMax neighbours -- the scatter then scans every sphere);
+// p is appended to the list of isolated spheres (nn = 0) or of the others.
+constexpr int kNbThreads = 64;
+
+__global__ void __launch_bounds__(kNbThreads)
+    k_sphere_neighbours(Grid g, double h, int n, const double *sph, SphereBins B,
+                        SphereLists S) {
+  __shared__ int cand[kNbMax];
+  __shared__ int ncand, overflow;
+  const int p = blockIdx.x;
+  const double *me = sph + 5 * p;
+  if (threadIdx.x == 0) {
+    ncand = 0;
+    overflow = 0;
+  }
+  __syncthreads();
+  const int ext[3] = {g.nx, g.ny, g.nz};
+  int b0[3], nbr[3];
+#pragma unroll
+  for (int ax = 0; ax < 3; ax++) {
+    int ic = (int)floor(me[ax] / h);
+    ic = min(max(ic, 0), ext[ax] - 1);
+    const int E = (int)((me[3] + B.rmax + 2.0 * h) / h) + 2;
+    int lo = fdiv(ic - E, B.bc[ax]), hi = fdiv(ic + E, B.bc[ax]);
+    if (!g.per[ax]) {
+      lo = max(lo, 0);
+      hi = min(hi, B.nb[ax] - 1);
+    }
+    nbr[ax] = min(hi - lo + 1, B.nb[ax]);
+    b0[ax] = lo;
+  }
+  const int nbins = nbr[0] * nbr[1] * nbr[2];
+  for (int t = threadIdx.x; t < nbins; t += blockDim.x) {
+    int bb[3] = {t / (nbr[1] * nbr[2]), (t / nbr[2]) % nbr[1], t % nbr[2]};
+#pragma unroll
+    for (int ax = 0; ax < 3; ax++) {
+      bb[ax] += b0[ax];
+      if (g.per[ax]) bb[ax] = ((bb[ax] % B.nb[ax]) + B.nb[ax]) % B.nb[ax];
+    }
+    const int b = (bb[0] * B.nb[1] + bb[1]) * B.nb[2] + bb[2];
+    const int m = B.count[b];
+    if (m > kBinCap) {
+      overflow = 1;
+      continue;
+    }
+    for (int e = 0; e < m; e++) {
+      const int q = B.items[(size_t)b * kBinCap + e];
+      if (q == p || !spheres_near(g, h, me, sph + 5 * q)) continue;
+      const int slot = atomicAdd(&ncand, 1);
+      if (slot < kNbMax) cand[slot] = q;
+    }
+  }
+  __syncthreads();
+  const int nc = ncand;
+  int *out = S.nbr + (size_t)p * kNbMax;
+  if (nc <= kNbMax)
+    for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+      const int q = cand[t];
+      int r = 0;
+      for (int u = 0; u < nc; u++) r += cand[u] < q;
+      out[r] = q;
+    }
+  if (threadIdx.x == 0) {
+    const int nn = (overflow || nc > kNbMax) ? kNbMax + 1 : nc;
+    S.nn[p] = nn;
+    const int k = nn ? 1 : 0;
+    S.list[(size_t)k * n + atomicAdd(S.nlist + k, 1)] = p;
+  }
+}
+
+// The density of the covered cells of this slab for the spheres of list
+// `k` (0: isolated spheres -- every covered cell is the sphere's alone, one
+// plain store per cell; 1: spheres with neighbours -- the cell is written by
+// its lowest-index covering sphere with the ordered sum).  One CTA per list
+// entry; the grid covers all n spheres, the surplus CTAs return.
+template <bool OVERLAP, bool PER>
 __global__ void __launch_bounds__(kThreads)
     k_sphere_scatter(Grid g, double h, int s, int n, const double *sph,
                      int normalization, const unsigned long long *counts,
-                     SphereBins B) {
+                     SphereLists S) {
   __shared__ sph::Tab tab;
   __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
-  __shared__ int nbl[kNbMax];
-  __shared__ int nbn;
-  const int p = blockIdx.x;
+  const int k = OVERLAP ? 1 : 0;
+  if ((int)blockIdx.x >= S.nlist[k]) return;
+  const int p = S.list[(size_t)k * n + blockIdx.x];
   const double *me = sph + 5 * p;
   const double R = me[3];
   const double R2 = R * R;
@@ -759,75 +872,18 @@ __global__ void __launch_bounds__(kThreads)
   const int s3 = s * s * s;
   const double np = (double)counts[p];
   if (normalization != 1 && np == 0.0) return;  // covers nothing
-  // spheres that may share a cell with p: the candidates of the bins within
-  // R_p + R_max + 2h (+ 2 cells of margin) of p's centre cell on every axis
-  // (periodic axes wrap; their bins divide the axis), then the distance
-  // test, then an ascending sort (ranks; the entries are distinct)
-  __shared__ int cand[kNbMax];
-  __shared__ int ncand, overflow;
-  if (threadIdx.x == 0) {
-    ncand = 0;
-    overflow = 0;
-  }
-  __syncthreads();
-  {
-    const int ext[3] = {g.nx, g.ny, g.nz};
-    int b0[3], nbr[3];
-#pragma unroll
-    for (int ax = 0; ax < 3; ax++) {
-      int ic = (int)floor(me[ax] / h);
-      ic = min(max(ic, 0), ext[ax] - 1);
-      const int E = (int)((me[3] + B.rmax + 2.0 * h) / h) + 2;
-      int lo = fdiv(ic - E, B.bc[ax]), hi = fdiv(ic + E, B.bc[ax]);
-      if (!g.per[ax]) {
-        lo = max(lo, 0);
-        hi = min(hi, B.nb[ax] - 1);
-      }
-      nbr[ax] = min(hi - lo + 1, B.nb[ax]);
-      b0[ax] = lo;
-    }
-    const int nbins = nbr[0] * nbr[1] * nbr[2];
-    for (int t = threadIdx.x; t < nbins; t += blockDim.x) {
-      int bb[3] = {t / (nbr[1] * nbr[2]), (t / nbr[2]) % nbr[1], t % nbr[2]};
-#pragma unroll
-      for (int ax = 0; ax < 3; ax++) {
-        bb[ax] += b0[ax];
-        if (g.per[ax]) bb[ax] = ((bb[ax] % B.nb[ax]) + B.nb[ax]) % B.nb[ax];
-      }
-      const int b = (bb[0] * B.nb[1] + bb[1]) * B.nb[2] + bb[2];
-      const int m = B.count[b];
-      if (m > kBinCap) {
-        overflow = 1;
-        continue;
-      }
-      for (int e = 0; e < m; e++) {
-        const int q = B.items[(size_t)b * kBinCap + e];
-        if (q == p || !spheres_near(g, h, me, sph + 5 * q)) continue;
-        const int slot = atomicAdd(&ncand, 1);
-        if (slot < kNbMax) cand[slot] = q;
-      }
-    }
-  }
-  __syncthreads();
-  const int nc = ncand;
-  if (nc <= kNbMax)
-    for (int t = threadIdx.x; t < nc; t += blockDim.x) {
-      const int q = cand[t];
-      int r = 0;
-      for (int u = 0; u < nc; u++) r += cand[u] < q;
-      nbl[r] = q;
-    }
-  if (threadIdx.x == 0) nbn = (overflow || nc > kNbMax) ? kNbMax + 1 : nc;
-  __syncthreads();
-  const int nn = nbn;
+  const int nn = OVERLAP ? S.nn[p] : 0;
+  const int *nbl = S.nbr + (size_t)p * kNbMax;
   const bool scan_all = nn > kNbMax;  // list overflow: every sphere per cell
   const int ntry = scan_all ? n : nn;
   const bool vtab = s3 < sph::kVal;
   if (vtab)
     for (int c = threadIdx.x; c <= s3; c += blockDim.x)
       vt[c] = sphere_value(me, np, c, s3, h, normalization);
-  double img[27][3];
-  const int nimg = sph::images(g, h, me[0], me[1], me[2], img);
+  sph::Images<PER> im;
+  sph::make_images<PER>(g, h, me[0], me[1], me[2], im);
+  const int nimg = im.n;
+  auto &img = im.c;
   for (int m = 0; m < nimg; m++) {
     sph::Box bx = sph::box_of(g, h, img[m], R);
     // this slab's planes of the box
@@ -838,41 +894,45 @@ __global__ void __launch_bounds__(kThreads)
     const int ncol = bx.n[1] * bx.n[2];
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
-      const int j = bx.lo[1] + cj, k = bx.lo[2] + ck;
+      const int j = bx.lo[1] + cj, kz = bx.lo[2] + ck;
       for (int i = xa; i <= xb; i++) {
         const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
-                         : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
+                         : sph::sub_count(i, j, kz, s, hs, img[m][0], img[m][1],
                                           img[m][2], R);
         if (!c) continue;
-        // the lowest-index covering sphere writes the cell
-        bool mine = true;
-        int t = 0;
-        for (; t < ntry; t++) {
-          const int q = scan_all ? t : nbl[t];
-          if (q >= p) break;
-          if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
-          const double *sq = sph + 5 * q;
-          if (normalization != 1 && counts[q] == 0ull) continue;
-          if (cover_count(g, h, s, hs, sq, i, j, k)) {
-            mine = false;
-            break;
-          }
-        }
-        if (!mine) continue;
         double v = 0.0;
-        v = v + (vtab ? vt[c] : sphere_value(me, np, c, s3, h, normalization));
-        for (; t < ntry; t++) {
-          const int q = scan_all ? t : nbl[t];
-          if (q == p) continue;
-          if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
-          const double *sq = sph + 5 * q;
-          const double nq = (double)counts[q];
-          if (normalization != 1 && nq == 0.0) continue;
-          const int cq = cover_count(g, h, s, hs, sq, i, j, k);
-          if (cq) v = v + sphere_value(sq, nq, cq, s3, h, normalization);
+        if (OVERLAP) {
+          // the lowest-index covering sphere writes the cell
+          bool mine = true;
+          int t = 0;
+          for (; t < ntry; t++) {
+            const int q = scan_all ? t : nbl[t];
+            if (q >= p) break;
+            if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
+            const double *sq = sph + 5 * q;
+            if (normalization != 1 && counts[q] == 0ull) continue;
+            if (cover_count(g, h, s, hs, sq, i, j, kz)) {
+              mine = false;
+              break;
+            }
+          }
+          if (!mine) continue;
+          v = v + (vtab ? vt[c] : sphere_value(me, np, c, s3, h, normalization));
+          for (; t < ntry; t++) {
+            const int q = scan_all ? t : nbl[t];
+            if (q == p) continue;
+            if (scan_all && !spheres_near(g, h, me, sph + 5 * q)) continue;
+            const double *sq = sph + 5 * q;
+            const double nq = (double)counts[q];
+            if (normalization != 1 && nq == 0.0) continue;
+            const int cq = cover_count(g, h, s, hs, sq, i, j, kz);
+            if (cq) v = v + sphere_value(sq, nq, cq, s3, h, normalization);
+          }
+        } else {
+          v = v + (vtab ? vt[c] : sphere_value(me, np, c, s3, h, normalization));
         }
-        const long long idx = rowbase(g, i - g.x0, j) + (k >> 1);
-        (((i + j + k) & 1) ? g.fB : g.fR)[idx] = v;
+        const long long idx = rowbase(g, i - g.x0, j) + (kz >> 1);
+        (((i + j + kz) & 1) ? g.fB : g.fR)[idx] = v;
       }
     }
   }
@@ -881,7 +941,10 @@ __global__ void __launch_bounds__(kThreads)
 void launch_sphere_counts(const Grid &g, double h, int s, int n, const double *sph,
                           unsigned long long *counts, cudaStream_t st) {
   if (n <= 0) return;
-  k_sphere_count<<<n, kThreads, 0, st>>>(g, h, s, sph, counts);
+  if (is_periodic(g))
+    k_sphere_count<true><<<n, kThreads, 0, st>>>(g, h, s, sph, counts);
+  else
+    k_sphere_count<false><<<n, kThreads, 0, st>>>(g, h, s, sph, counts);
 }
 
 void launch_sphere_bin(const Grid &g, double h, int n, const double *sph,
@@ -890,13 +953,28 @@ void launch_sphere_bin(const Grid &g, double h, int n, const double *sph,
   k_sphere_bin<<<(n + kThreads - 1) / kThreads, kThreads, 0, st>>>(g, h, n, sph, B);
 }
 
-void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *sph,
-                           int normalization, const unsigned long long *counts,
-                           const SphereBins &B, cudaStream_t st) {
+void launch_sphere_neighbours(const Grid &g, double h, int n, const double *sph,
+                              const SphereBins &B, const SphereLists &S, cudaStream_t st) {
   if (n <= 0) return;
-  k_sphere_scatter<<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts, B);
+  k_sphere_neighbours<<<n, kNbThreads, 0, st>>>(g, h, n, sph, B, S);
 }
 
+void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *sph,
+                           int normalization, const unsigned long long *counts,
+                           const SphereLists &S, cudaStream_t st) {
+  if (n <= 0) return;
+  if (is_periodic(g)) {
+    k_sphere_scatter<false, true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
+                                                          counts, S);
+    k_sphere_scatter<true, true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
+                                                         counts, S);
+  } else {
+    k_sphere_scatter<false, false><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
+                                                           counts, S);
+    k_sphere_scatter<true, false><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
+                                                          counts, S);
+  }
+}
 // ---------------------------------------------------------------------------
 // Finest-grid RHS adaptation: f -= term_q for every
 // face q the cell touches, in face order.  term_q = (2 alpha) g_d for

@@ -77,6 +77,26 @@ __device__ __forceinline__ int images(const Grid &g, double h, double cx,
   return n;
 }
 
+// the images of a sphere centre: 27 on grids with periodic axes, the
+// centre itself otherwise (then no local-memory array)
+template <bool PER>
+struct Images {
+  double c[PER ? 27 : 1][3];
+  int n;
+};
+template <bool PER>
+__device__ __forceinline__ void make_images(const Grid &g, double h, double cx, double cy,
+                                            double cz, Images<PER> &im) {
+  if constexpr (PER) {
+    im.n = images(g, h, cx, cy, cz, im.c);
+  } else {
+    im.c[0][0] = cx;
+    im.c[0][1] = cy;
+    im.c[0][2] = cz;
+    im.n = 1;
+  }
+}
+
 // bounding box of one image: lo[a], n[a] cells per axis (0 if empty)
 struct Box {
   int lo[3], n[3];
