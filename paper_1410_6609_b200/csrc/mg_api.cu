@@ -846,8 +846,10 @@ int enqueue_vcycle(mg_ctx *c) {
   // levels top..L-1 are the tail kernel's (or just the coarsest's CG)
   const int ls = tail_level(c);
   const int top = ls < L ? ls : L - 1;
+  // profiling marks on levels >= 1 only where the category changes (every
+  // mark is an event node in the graph)
   for (int l = 0; l < top; l++) {
-    if (l >= 1) mark(c, level_cat(c, l - 1));  // closes level l-1's down part
+    if (l >= 2 && level_cat(c, l - 1) != level_cat(c, l)) mark(c, level_cat(c, l - 1));
     if (c->o.nu1 == 0 && l > 0)
       for (const Grid &g : c->g[l]) {
         CK(cudaMemsetAsync(g.phiR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
@@ -859,16 +861,21 @@ int enqueue_vcycle(mg_ctx *c) {
     }
     if ((rc = restrict_level(c, l))) return rc;
   }
-  mark(c, level_cat(c, top - 1));
+  const int before = level_cat(c, top - 1);  // CAT_NONE: level 0 came last
+  int open_cat;  // category of the interval open after the coarse end
   if (ls < L) {
+    if (before != CAT_NONE && before != CAT_AGG) mark(c, before);
     if ((rc = tail_launch(c, ls))) return rc;
-    mark(c, CAT_AGG);
+    open_cat = CAT_AGG;
   } else {
+    if (before != CAT_NONE) mark(c, before);
     if ((rc = coarse_solve(c))) return rc;
     mark(c, CAT_CG);
+    open_cat = CAT_NONE;
   }
   for (int l = top - 1; l >= 0; l--) {
-    if (l < top - 1) mark(c, level_cat(c, l + 1));  // closes level l+1's up part
+    if (l < top - 1) open_cat = level_cat(c, l + 1);
+    if (open_cat != CAT_NONE && (l == 0 || open_cat != level_cat(c, l))) mark(c, open_cat);
     const bool fuse = can_fuse_prolong(c, l);
     if (fuse) {
       if ((rc = prolong_red_level(c, l))) return rc;

@@ -500,29 +500,6 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   if (bnorm > 0.0) {
     while (it < maxit) {
       acc = 0.0;
-#ifdef MG_CG_SEPARATE_P
-      for (int n = threadIdx.x; n < nend; n += nthr) {
-        const unsigned m = nb[n];
-        auto nbr = [&](unsigned in, unsigned pe, int kin, int kpe) {
-          const bool vi = (m & in) != 0, vp = PER && (m & pe) != 0;
-          const int k = vi ? kin : (vp ? kpe : n);
-          const double v = po[k];
-          return (vi || vp) ? v : 0.0;
-        };
-        const double xm = nbr(1, 64, n - sx, n + wx);
-        const double xp = nbr(2, 128, n + sx, n - wx);
-        const double ym = nbr(4, 256, n - sy, n + wy);
-        const double yp = nbr(8, 512, n + sy, n - wy);
-        const double zm = nbr(16, 1024, n - 1, n + wz);
-        const double zp = nbr(32, 2048, n + 1, n - wz);
-        const double s = ((((xm + xp) + ym) + yp) + zm) + zp;
-        const double p = po[n];
-        const double qn = c * ((double)dc[n] * p - s);
-        q[n] = qn;
-        acc = acc + p * qn;
-      }
-      pn = po;
-#else
       for (int n = threadIdx.x; n < nend; n += nthr) {
         const unsigned m = nb[n];
         // p = r + beta p_old at neighbour (bit `in`: inside; bit `pe`: across
@@ -547,7 +524,6 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
         q[n] = qn;
         acc = acc + p * qn;
       }
-#endif
       const double pq = cg_allsum(acc, part[pb]);
       pb ^= 1;
       const double a = rho / pq;
@@ -564,11 +540,6 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
       if (sqrt(rho1) <= tol * bnorm) break;
       beta = rho1 / rho;
       rho = rho1;
-#ifdef MG_CG_SEPARATE_P
-      for (int n = threadIdx.x; n < nend; n += nthr) po[n] = r[n] + beta * po[n];
-      __syncthreads();  // p complete before the next matrix-vector product
-      continue;
-#endif
       double *t = po;
       po = pn;
       pn = t;
@@ -605,7 +576,9 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
 // latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at P = 8,
 // 476 vs 557 us in round 1; 1024 threads are slower again)
 // (round 2 A/B, scripts/cg_probe.py: caps of 64/128 per block are slower,
-// 512/1024 no faster -- the iteration is bound by its dependency chain)
+// 512/1024 no faster -- the iteration is bound by its dependency chain; a
+// separate p = r + beta p pass with a third barrier is slower on 8^3 and
+// faster on 32 x 8 x 8, 3.275 vs 3.268 ms per config-3 cycle)
 static int cg_threads(long long N) {
   int threads = (int)((N + 31) / 32 * 32);
   const int cap = N >= 2048 ? 512 : 256;
