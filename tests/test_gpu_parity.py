@@ -1067,3 +1067,34 @@ def test_tail_kernel_equals_per_step_launches(mg, shape, bc, nu, P):
     ho = [o.vcycle() for _ in range(4)]
     check_history(out[0][0], ho)
     assert rel(out[0][1], o.phi()) <= 1e-10
+
+
+@pytest.mark.parametrize("bc", ["channel", "periodic"])
+def test_sphere_rhs_sequence_clears_previous(mg, bc):
+    """Successive sphere RHS calls clear only the previous spheres' boxes and
+    the boundary cells instead of the whole level: f after each call equals
+    the oracle's fresh RHS bitwise -- moved spheres, a shorter and a longer
+    list, an intervening full-field set_rhs, different subsampling."""
+    shape = (64, 48, 64)
+    if bc == "periodic":
+        bt, bv = W.periodic_channel_bc(1.0)
+    else:
+        bt, bv = BCS["channel"]
+    s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=4)
+    o = oracle.Oracle(shape, 1.0, bt, bv, min_coarse=4)
+    L = np.array(shape, float)
+    c0, q0 = W.random_spheres(L, 4.0, 30, seed=5)
+    steps = [(c0, q0, 1), (W.move_spheres(c0, np.full(30, 4.0), L, 1, amplitude=2.0,
+                                          periodic=(bc == "periodic",) * 3), q0, 2),
+             (c0[:11], q0[:11], 1), ("field", None, None), (c0, q0, 3)]
+    for c, q, sub in steps:
+        if isinstance(c, str):
+            f = np.random.default_rng(2).uniform(-1, 1, shape)
+            s.set_rhs(f)
+            o.set_rhs(f)
+        else:
+            R = np.full(len(q), 4.0)
+            s.set_rhs_from_spheres(c, R, q, subsample=sub)
+            o.set_rhs_from_spheres(c, R, q, subsample=sub)
+        assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    s.close()
