@@ -77,10 +77,11 @@ def run_oracle(w, solid=None, max_cycles=60):
 
 def floor_cycle(hist):
     """The cycle at which the residual reaches the fp64 rounding floor
-    (reading c21): the first cycle whose reduction factor r_k / r_{k-1}
-    exceeds 0.5 (the V-cycle's own factor is 0.04-0.2); None if none."""
+    (reading c21): the first cycle below 1e-10 r_0 whose reduction factor
+    r_k / r_{k-1} exceeds 0.5 (the V-cycle's own factor is 0.04-0.2); None
+    if none."""
     for k in range(1, len(hist)):
-        if hist[k] > 0.5 * hist[k - 1]:
+        if hist[k - 1] < 1e-10 * hist[0] and hist[k] > 0.5 * hist[k - 1]:
             return k
     return None
 
@@ -147,7 +148,7 @@ def main():
           "launch + norm readback).  Oracle columns: the CPU oracle on the same "
           "inputs (host cores of the GPU box).  `floor at` = the cycle where the "
           "residual reaches the fp64 rounding floor (first cycle with r_k > 0.5 "
-          "r_{k-1}, reading c21) and r_k/r_0 there; `clause c` = the smallest c with "
+          "r_{k-1} once below 1e-10 r_0, reading c21) and r_k/r_0 there; `clause c` = the smallest c with "
           "|r_k(GPU) - r_k(oracle)| <= 1e-8 r_k + c r_0 over the history (the tests "
           "use c = 1e-15).", "",
           "| config | cells | levels (coarsest) | cycles | ms/cycle | Mcells/s | "
