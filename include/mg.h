@@ -133,13 +133,6 @@ typedef struct {
                          instead of a launch per step (box / periodic grids
                          whose coarsest solve is the single-CTA CG; 0 =
                          default 32768 = 32^3; MG_OFF_TAIL disables it)     */
-  long long mid_cells; /* the levels between the fine ones and the tail,
-                         from the first one held whole with at most this
-                         many cells, run as two persistent cooperative
-                         kernels (the down and the up half of the cycle,
-                         grid-wide barriers between the steps) instead of a
-                         launch per step; only together with the tail (0 =
-                         default 2097152 = 128^3; MG_OFF_MID disables it)  */
 } mg_opts;
 
 /* mg_opts.disable bits */
@@ -149,7 +142,6 @@ typedef struct {
 #define MG_OFF_CG_CLUSTER 8  /* 8-CTA cluster CG -> single-CTA CG             */
 #define MG_OFF_MASK_CODES 16 /* masked levels: byte codes -> float records    */
 #define MG_OFF_TAIL 32       /* persistent tail kernel -> a launch per step   */
-#define MG_OFF_MID 64        /* persistent middle kernels -> launch per step  */
 
 /* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
 #define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
@@ -160,7 +152,6 @@ typedef struct {
 #define MG_PATH_PROLONG_FUSED 32 /* prolongation fused with the red sweep     */
 #define MG_PATH_FUSED_NORM 64    /* norm from the in-cycle residual (c11)     */
 #define MG_PATH_TAIL 128         /* coarse levels in the persistent tail      */
-#define MG_PATH_MID 256          /* middle levels in the cooperative kernels  */
 
 typedef struct mg_ctx mg_ctx;
 

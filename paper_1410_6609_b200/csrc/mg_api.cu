@@ -837,35 +837,6 @@ int tail_launch(mg_ctx *c, int ls) {
   return MG_OK;
 }
 
-// first of the middle levels run by the persistent cooperative kernels
-// (k_vcycle_mid_down / _up) when the tail kernel starts at level ls: the
-// first level >= 1 held whole on every rank with at most mg_opts.mid_cells
-// cells (ls: none)
-int mid_level(const mg_ctx *c, int ls) {
-  if (ls >= c->pl.L || (c->o.disable & MG_OFF_MID)) return ls;
-  const long long cap = c->o.mid_cells > 0 ? c->o.mid_cells : 128LL * 128 * 128;
-  for (int l = c->pl.nd > 1 ? c->pl.nd : 1; l < ls; l++)
-    if ((long long)c->pl.dims[l][0] * c->pl.dims[l][1] * c->pl.dims[l][2] <= cap)
-      return ls - l > mg::kMidMax ? ls : l;
-  return ls;
-}
-
-// levels lm..ls-1 (copy s of each) down (pre-smoothing + restrictions into
-// level ls) or up (prolongations from level ls + post-smoothing)
-int mid_launch(mg_ctx *c, int lm, int ls, bool down) {
-  for (int s = 0; s < c->ncopy; s++) {
-    mg::MidLevels T;
-    T.n = ls - lm;
-    for (int k = 0; k <= T.n; k++) T.g[k] = c->g[lm + k][c->ncopy > 1 ? s : 0];
-    if (mg::launch_vcycle_mid(T, down, down ? c->o.nu1 : c->o.nu2, c->o.alpha, c->stream))
-      return fail(MG_ERR_CUDA, "middle-level kernel launch: %s",
-                  cudaGetErrorString(cudaGetLastError()));
-    c->launches++;
-  }
-  c->paths |= MG_PATH_MID;
-  return MG_OK;
-}
-
 // profiling category of the work on level l >= 1 (not level 0)
 int level_cat(const mg_ctx *c, int l) {
   if (l < 1 || l > c->pl.L - 2) return CAT_NONE;
@@ -882,8 +853,7 @@ int enqueue_vcycle(mg_ctx *c) {
   if (fused_norm_on(c)) c->paths |= MG_PATH_FUSED_NORM;
   // levels top..L-1 are the tail kernel's (or just the coarsest's CG)
   const int ls = tail_level(c);
-  const int lm = mid_level(c, ls);  // levels lm..ls-1: the middle kernels
-  const int top = ls < L ? lm : L - 1;
+  const int top = ls < L ? ls : L - 1;
   // profiling marks on levels >= 1 only where the category changes (every
   // mark is an event node in the graph)
   for (int l = 0; l < top; l++) {
@@ -903,9 +873,7 @@ int enqueue_vcycle(mg_ctx *c) {
   int open_cat;  // category of the interval open after the coarse end
   if (ls < L) {
     if (before != CAT_NONE && before != CAT_AGG) mark(c, before);
-    if (lm < ls && (rc = mid_launch(c, lm, ls, true))) return rc;
     if ((rc = tail_launch(c, ls))) return rc;
-    if (lm < ls && (rc = mid_launch(c, lm, ls, false))) return rc;
     open_cat = CAT_AGG;
   } else {
     if (before != CAT_NONE) mark(c, before);

@@ -42,10 +42,9 @@ MG_HALO_LOOPBACK = 2
 MG_HALO_EMULATE = 3
 # mg_opts.disable bits / mg_cycle_paths bits (include/mg.h)
 MG_OFF_MARCH, MG_OFF_OVERLAP, MG_OFF_SPLIT_NORM = 1, 2, 4
-MG_OFF_CG_CLUSTER, MG_OFF_MASK_CODES, MG_OFF_TAIL, MG_OFF_MID = 8, 16, 32, 64
+MG_OFF_CG_CLUSTER, MG_OFF_MASK_CODES, MG_OFF_TAIL = 8, 16, 32
 MG_PATH_MARCH, MG_PATH_OVERLAP, MG_PATH_SPLIT_NORM, MG_PATH_CG_CLUSTER = 1, 2, 4, 8
 MG_PATH_CG_VAR, MG_PATH_PROLONG_FUSED, MG_PATH_FUSED_NORM, MG_PATH_TAIL = 16, 32, 64, 128
-MG_PATH_MID = 256
 
 _HALO = {"none": MG_HALO_NONE, "nccl": MG_HALO_NCCL, "loopback": MG_HALO_LOOPBACK,
          "emulate": MG_HALO_EMULATE}
@@ -75,7 +74,7 @@ class mg_opts(ctypes.Structure):
                 ("workspace_bytes", ctypes.c_size_t),
                 ("use_graph", ctypes.c_int), ("fused_norm", ctypes.c_int),
                 ("disable", ctypes.c_int), ("nccl_timeout_ms", ctypes.c_int),
-                ("tail_cells", ctypes.c_longlong), ("mid_cells", ctypes.c_longlong)]
+                ("tail_cells", ctypes.c_longlong)]
 
 
 _lib = None
@@ -183,7 +182,7 @@ def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
               max_cycles=100, device=0, rank=0, nranks=1, halo="none",
               nccl_id: Optional[bytes] = None, use_graph=True,
               fused_norm=False, disable=0, nccl_timeout_ms=600000,
-              tail_cells=0, mid_cells=0) -> mg_opts:
+              tail_cells=0) -> mg_opts:
     o = default_opts()
     o.nu1, o.nu2, o.alpha = nu1, nu2, alpha
     o.min_coarse, o.max_levels = min_coarse, max_levels
@@ -198,7 +197,6 @@ def make_opts(nu1=2, nu2=2, alpha=2.0, min_coarse=4, max_levels=0,
     o.disable = int(disable)  # MG_OFF_* bits
     o.nccl_timeout_ms = int(nccl_timeout_ms)
     o.tail_cells = int(tail_cells)
-    o.mid_cells = int(mid_cells)
     return o
 
 

@@ -141,8 +141,8 @@ def test_opts_struct_matches_header():
     body = re.sub(r"/\*.*?\*/", "", body, flags=re.S)
     fields = re.findall(r"(\w+)(?:\[\d+\])?;", body)
     names = [n for n, _ in mg.mg_opts._fields_]
-    assert fields[-6:] == names[-6:] == ["use_graph", "fused_norm", "disable",
-                                         "nccl_timeout_ms", "tail_cells", "mid_cells"]
+    assert fields[-5:] == names[-5:] == ["use_graph", "fused_norm", "disable",
+                                         "nccl_timeout_ms", "tail_cells"]
     for m in re.finditer(r"#define (MG_(?:OFF|PATH)_\w+) (\d+)", src):
         assert getattr(mg, m.group(1)) == int(m.group(2)), m.group(1)
 

@@ -296,18 +296,17 @@ def test_periodic_errors(mg):
 
 @pytest.mark.parametrize("bc", ["xy", "chan", "z"])
 def test_periodic_tail_kernel_equals_per_step(mg, bc):
-    """Periodic coarse levels in the persistent middle and tail kernels
-    (ghost copies by the smoother, ghost refresh after the prolongation and
-    the CG) == the per-step launches, bit for bit."""
-    shape = (128, 64, 128)
+    """Periodic coarse levels in the persistent tail kernel (ghost copies by
+    the smoother, ghost refresh after the prolongation and the CG) == the
+    per-step launches, bit for bit."""
+    shape = (64, 32, 64)
     f = np.random.default_rng(27).uniform(-1, 1, shape)
     out = []
-    for off in (0, mg.MG_OFF_TAIL | mg.MG_OFF_MID):
+    for off in (0, mg.MG_OFF_TAIL):
         s, _ = pair(mg, shape, 1.0, bc, min_coarse=2, disable=off)
         s.set_rhs(f)
         r = [s.vcycle() for _ in range(3)]
         assert bool(s.cycle_paths & mg.MG_PATH_TAIL) == (off == 0)
-        assert bool(s.cycle_paths & mg.MG_PATH_MID) == (off == 0)
         out.append((r, s.get_solution()))
         s.close()
     assert np.array_equal(out[0][1], out[1][1])
