@@ -158,17 +158,6 @@ struct TailLevels {
   Grid g[kTailMax];
   int n;
 };
-// the middle levels in two persistent cooperative kernels: g[0..n-1] the
-// middle levels, g[n] the first tail level (restriction target,
-// prolongation source); down: pre-smoothing + restrictions, up:
-// prolongations + post-smoothing.  0, or -1 if the launch failed
-constexpr int kMidMax = 8;
-constexpr int kMidThreads = 256;
-struct MidLevels {
-  Grid g[kMidMax + 1];
-  int n;
-};
-int launch_vcycle_mid(const MidLevels &T, bool down, int nu, double alpha, cudaStream_t s);
 // CTAs of the tail's cluster on this device (0: clusters unavailable)
 int tail_cluster_ctas();
 bool vcycle_tail_supported(const Grid &coarsest);

@@ -1303,115 +1303,6 @@ __global__ void __launch_bounds__(kTailThreads)
   }
 }
 
-// ---------------------------------------------------------------------------
-// The middle levels of the V-cycle in two persistent cooperative kernels: the
-// levels between the fine ones (TMA-marching kernels, a launch per step) and
-// the tail (k_vcycle_tail) -- e.g. 128^3 and 64^3 at 512^3.  They are
-// L2-resident and too small to fill the GPU with one launch per half-sweep,
-// too large for one cluster: the whole grid works on every step, the steps
-// separated by grid-wide barriers (cooperative launch).  k_vcycle_mid_down
-// runs the pre-smoothing and the residual + restriction of the middle levels
-// down to the tail's first level, k_vcycle_mid_up the prolongations and
-// post-smoothing back up; the tail kernel runs in between.  The per-cell
-// arithmetic is the per-step kernels' device functions (bitwise the same
-// iterates).
-// ---------------------------------------------------------------------------
-template <bool PER>
-__global__ void __launch_bounds__(kMidThreads)
-    k_vcycle_mid_down(MidLevels T, int nu1) {
-  cgr::grid_group grid = cgr::this_grid();
-  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nt = (long long)gridDim.x * blockDim.x;
-  for (int l = 0; l < T.n; l++) {
-    const Grid &g = T.g[l];
-    if (nu1 == 0) {  // Phi of a coarse level starts from 0
-      const long long ne = grid_elems(g);
-      for (long long e = t0; e < ne; e += nt) {
-        g.phiR[e] = 0.0;
-        g.phiB[e] = 0.0;
-      }
-      grid.sync();
-    }
-    for (int s = 0; s < nu1; s++) {
-      for (int color = 0; color < 2; color++) {
-        const long long n = smooth_items(g);
-        const int fz = color == 0 && s == 0;  // the first red sweep from Phi = 0
-        for (long long t = t0; t < n; t += nt) smooth_pair<PER>(g, color, fz, t);
-        grid.sync();
-      }
-    }
-    const long long n = restrict_items(g);
-    for (long long t = t0; t < n; t += nt) restrict_cell<PER>(g, T.g[l + 1], t);
-    if (l + 1 < T.n) grid.sync();
-  }
-}
-
-template <bool PER>
-__global__ void __launch_bounds__(kMidThreads)
-    k_vcycle_mid_up(MidLevels T, int nu2, double alpha) {
-  cgr::grid_group grid = cgr::this_grid();
-  const long long t0 = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  const long long nt = (long long)gridDim.x * blockDim.x;
-  for (int l = T.n - 1; l >= 0; l--) {
-    const Grid &g = T.g[l];
-    const long long n = prolong_items(g);
-    for (long long t = t0; t < n; t += nt) prolong_cell(g, T.g[l + 1], alpha, t);
-    grid.sync();
-    if (PER && periodic_fill_items(g)) {
-      const long long m = periodic_fill_items(g);
-      for (long long t = t0; t < m; t += nt) periodic_fill_elem(g, t);
-      grid.sync();
-    }
-    for (int s = 0; s < nu2; s++) {
-      for (int color = 0; color < 2; color++) {
-        const long long m = smooth_items(g);
-        for (long long t = t0; t < m; t += nt) smooth_pair<PER>(g, color, 0, t);
-        if (!(l == 0 && s == nu2 - 1 && color == 1)) grid.sync();
-      }
-    }
-  }
-}
-
-template <class K>
-static int mid_blocks(K kernel) {
-  static int nb = -1;
-  if (nb < 0) {
-    int dev = 0, nsm = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, kMidThreads, 0);
-    nb = per * nsm;
-    cudaGetLastError();
-  }
-  return nb;
-}
-
-template <bool PER>
-static int launch_mid(const MidLevels &T, bool down, int nu, double alpha, cudaStream_t s) {
-  cudaLaunchConfig_t cfg = {};
-  cfg.blockDim = dim3(kMidThreads);
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  cudaError_t e;
-  if (down) {
-    cfg.gridDim = dim3(mid_blocks(k_vcycle_mid_down<PER>));
-    e = cudaLaunchKernelEx(&cfg, k_vcycle_mid_down<PER>, T, nu);
-  } else {
-    cfg.gridDim = dim3(mid_blocks(k_vcycle_mid_up<PER>));
-    e = cudaLaunchKernelEx(&cfg, k_vcycle_mid_up<PER>, T, nu, alpha);
-  }
-  return e == cudaSuccess ? 0 : -1;
-}
-
-int launch_vcycle_mid(const MidLevels &T, bool down, int nu, double alpha, cudaStream_t s) {
-  if (is_periodic(T.g[0])) return launch_mid<true>(T, down, nu, alpha, s);
-  return launch_mid<false>(T, down, nu, alpha, s);
-}
-
 int tail_cluster_ctas() {
   static int n = -1;
   if (n < 0) {
