@@ -254,16 +254,8 @@ struct mg_ctx {
   cudaEvent_t ev_free[3] = {};
   bool d2h_used[3] = {false, false, false}, free_used[3] = {false, false, false};
   unsigned long long async_k = 0;
-  // sphere lists: two slots of sph_cap (cx, cy, cz, R, Q) records -- the
-  // current RHS's and the previous one's -- then sph_cap covered counts
-  double *sph = nullptr;
+  double *sph = nullptr;       // lazily allocated sphere list
   size_t sph_cap = 0;
-  int sph_cur = 0;        // slot of the list of the last sphere RHS
-  int sph_prev_n = -1;    // its length; -1: level-0 f was written otherwise
-  double *sph_list(int slot) const { return sph + 5 * sph_cap * (size_t)slot; }
-  unsigned long long *sph_counts() const {
-    return reinterpret_cast<unsigned long long *>(sph + 10 * sph_cap);
-  }
   int *bins = nullptr;         // sphere bins (counts + items), grown on demand
   size_t bins_cap = 0;         // ints
   double *fbuf = nullptr;      // force step: sphere list + partial sums
@@ -993,7 +985,6 @@ int field_io(mg_ctx *c, int l, int field, double *buf, int where, bool in,
   const size_t n = level_cells_held(c, l);
   double *dev = buf;
   int rc;
-  if (in && l == 0 && field == MG_FIELD_RHS) c->sph_prev_n = -1;  // f overwritten
   if (where == MG_HOST) {
     if ((rc = stage_for(c, n * sizeof(double)))) return rc;
     dev = c->stage;
@@ -1449,35 +1440,19 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     h5[5 * (size_t)p + 4] = charges[p];
   }
   if ((size_t)n > c->sph_cap) {
-    CK(cudaStreamSynchronize(c->stream));
     if (c->sph) cudaFree(c->sph);
     c->sph = nullptr;
     c->sph_cap = 0;
-    c->sph_prev_n = -1;  // the previous list is gone: clear f whole
-    CK(cudaMalloc(&c->sph, (sizeof(double) * 10 + sizeof(unsigned long long)) * (size_t)n));
+    CK(cudaMalloc(&c->sph, sizeof(double) * 5 * (size_t)n + sizeof(unsigned long long) * (size_t)n));
     c->sph_cap = (size_t)n;
   }
-  unsigned long long *cnt = c->sph_counts();
-  const int slot = 1 - c->sph_cur;  // the previous list stays in sph_cur
-  double *dsph = c->sph_list(slot);
-  // f := 0: when the last writer of f was a sphere RHS, only its spheres'
-  // bounding boxes and the boundary cells (BC terms) are non-zero
-  if (c->sph_prev_n >= 0) {
-    for (const Grid &g : c->g[0]) {
-      mg::launch_sphere_clear(g, c->h, c->sph_prev_n, c->sph_list(c->sph_cur), c->stream);
-      mg::launch_bc_adapt(g, nullptr, nullptr, c->stream);
-    }
-    CK(cudaGetLastError());
-  } else {
-    for (const Grid &g : c->g[0]) {
-      CK(cudaMemsetAsync(g.fR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
-      CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
-    }
+  unsigned long long *cnt = (unsigned long long *)(c->sph + 5 * c->sph_cap);
+  for (const Grid &g : c->g[0]) {
+    CK(cudaMemsetAsync(g.fR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+    CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
   }
-  c->sph_cur = slot;
-  c->sph_prev_n = n;
   if (n > 0) {
-    CK(cudaMemcpyAsync(dsph, h5, sizeof(double) * 5 * (size_t)n,
+    CK(cudaMemcpyAsync(c->sph, h5, sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
     // bins of the centres for the scatter's neighbour search: wider than
     // 2 R_max + 2 cells, at most 64 per axis; on periodic axes the bin width
@@ -1515,11 +1490,11 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     S.nlist = S.list + 2 * (size_t)n;
     CK(cudaMemsetAsync(B.count, 0, nbins * sizeof(int), c->stream));
     CK(cudaMemsetAsync(S.nlist, 0, 2 * sizeof(int), c->stream));
-    mg::launch_sphere_bin(c->g[0][0], c->h, n, dsph, B, c->stream);
-    mg::launch_sphere_neighbours(c->g[0][0], c->h, n, dsph, B, S, c->stream);
-    mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, dsph, cnt, c->stream);
+    mg::launch_sphere_bin(c->g[0][0], c->h, n, c->sph, B, c->stream);
+    mg::launch_sphere_neighbours(c->g[0][0], c->h, n, c->sph, B, S, c->stream);
+    mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, c->sph, cnt, c->stream);
     for (const Grid &g : c->g[0])
-      mg::launch_sphere_scatter(g, c->h, subsample, n, dsph, normalization, cnt, S,
+      mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt, S,
                                 c->stream);
     CK(cudaGetLastError());
   }
@@ -1625,7 +1600,6 @@ int mg_solve_async(mg_ctx *c, const double *f, int where_f, double *phi_out,
   if ((rc = async_setup(c, n * sizeof(double)))) return rc;
   const int q = (int)(c->async_k++ % 3);
   double *stg = c->astg[q];
-  c->sph_prev_n = -1;  // f overwritten by the problem's field
   if (where_f == MG_HOST) {
     // the slot's previous users must be done with it: a download of Phi
     // (ev_d2h) and the context stream's last read of it (ev_free: an RHS
@@ -2191,12 +2165,12 @@ int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
     // the RHS kernel counted the spheres' covered sub-cells already
     const unsigned long long *cnt =
         (force_subsample == subsample && n > 0)
-            ? c->sph_counts()
+            ? reinterpret_cast<const unsigned long long *>(c->sph + 5 * c->sph_cap)
             : nullptr;
     // ... and the same sphere list is already on the device (c->sph)
     const int frc = coulomb_forces(c, n, centers, radii, charges, normalization,
                                    force_subsample, forces_out, cnt,
-                                   n > 0 ? c->sph_list(c->sph_cur) : nullptr);
+                                   n > 0 ? c->sph : nullptr);
     if (frc) return frc;
   }
   return rc;

@@ -220,12 +220,8 @@ void launch_sphere_scatter(const Grid &g, double h, int subsample, int n,
                            const double *sph, int normalization,
                            const unsigned long long *counts, const SphereLists &S,
                            cudaStream_t s);
-// terms == null: set every boundary cell of the level to 0 instead
 void launch_bc_adapt(const Grid &g, const double *terms, const int *types,
                      cudaStream_t s);
-// f := 0 on the bounding boxes of the spheres sph[5n] (a previous RHS)
-void launch_sphere_clear(const Grid &g, double h, int n, const double *sph,
-                         cudaStream_t s);
 // plane-marching TMA half-sweep (mg_march.cu)
 bool march_supported(const Grid &g);
 bool make_tmap_field(const Grid &g, const double *base, void *out128);

@@ -911,40 +911,6 @@ __global__ void __launch_bounds__(kThreads)
   }
 }
 
-// f := 0 on the bounding boxes (all images) of the spheres of a previous
-// RHS within this slab: with the domain's boundary cells (launch_bc_adapt
-// with no terms) this restores f = 0 wherever that RHS wrote, far fewer
-// bytes than clearing the whole level
-template <bool PER>
-__global__ void __launch_bounds__(kThreads)
-    k_sphere_clear(Grid g, double h, const double *sph) {
-  const int p = blockIdx.x;
-  const double *me = sph + 5 * p;
-  sph::Images<PER> im;
-  sph::make_images<PER>(g, h, me[0], me[1], me[2], im);
-  for (int m = 0; m < im.n; m++) {
-    const sph::Box bx = sph::box_of(g, h, im.c[m], me[3]);
-    const int xa = bx.lo[0] > g.x0 ? bx.lo[0] : g.x0;
-    const int xb = min(bx.lo[0] + bx.n[0] - 1, g.x0 + g.nxl - 1);
-    if (bx.cells() == 0 || xa > xb) continue;
-    const int ncol = bx.n[1] * bx.n[2];
-    for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
-      const int j = bx.lo[1] + col / bx.n[2], k = bx.lo[2] + col % bx.n[2];
-      for (int i = xa; i <= xb; i++)
-        (((i + j + k) & 1) ? g.fB : g.fR)[rowbase(g, i - g.x0, j) + (k >> 1)] = 0.0;
-    }
-  }
-}
-
-void launch_sphere_clear(const Grid &g, double h, int n, const double *sph,
-                         cudaStream_t st) {
-  if (n <= 0) return;
-  if (is_periodic(g))
-    k_sphere_clear<true><<<n, kThreads, 0, st>>>(g, h, sph);
-  else
-    k_sphere_clear<false><<<n, kThreads, 0, st>>>(g, h, sph);
-}
-
 void launch_sphere_counts(const Grid &g, double h, int s, int n, const double *sph,
                           unsigned long long *counts, cudaStream_t st) {
   if (n <= 0) return;
@@ -991,20 +957,15 @@ void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *
 // ---------------------------------------------------------------------------
 struct Terms {
   double t[6];
-  int zero;  // 1: set the boundary cells to 0 instead (the RHS clear)
 };
 
 __device__ __forceinline__ void bc_cell(const Grid &g, const Terms &T, int il,
                                         int j, int z) {
   const int i = g.x0 + il;
   const long long e = rowbase(g, il, j) + (z >> 1);
-  double *f = ((i + j + z) & 1) ? g.fB : g.fR;
-  if (T.zero) {
-    f[e] = 0.0;
-    return;
-  }
   // masked cells are not unknowns (their f stays 0)
   if (g.codeR && !((((i + j + z) & 1) ? g.codeB : g.codeR)[e] & 64)) return;
+  double *f = ((i + j + z) & 1) ? g.fB : g.fR;
   double v = f[e];
   const bool on[6] = {i == 0, i == g.nx - 1, j == 0,
                       j == g.ny - 1, z == 0, z == g.nz - 1};
@@ -1055,8 +1016,7 @@ __global__ void __launch_bounds__(kThreads)
 void launch_bc_adapt(const Grid &g, const double *terms, const int * /*types*/,
                      cudaStream_t s) {
   Terms T;
-  for (int q = 0; q < 6; q++) T.t[q] = terms ? terms[q] : 0.0;
-  T.zero = terms ? 0 : 1;
+  for (int q = 0; q < 6; q++) T.t[q] = terms[q];
   const long long nzi = g.nz > 2 ? g.nz - 2 : 0;
   const long long nA = 2LL * g.nxl * g.ny;
   const long long nB = g.ny > 0 ? 2LL * g.nxl * nzi : 0;
