@@ -1071,8 +1071,7 @@ def test_tail_kernel_equals_per_step_launches(mg, shape, bc, nu, P):
 
 @pytest.mark.parametrize("bc", ["channel", "periodic"])
 def test_sphere_rhs_sequence_clears_previous(mg, bc):
-    """Successive sphere RHS calls clear only the previous spheres' boxes and
-    the boundary cells instead of the whole level: f after each call equals
+    """Successive sphere RHS calls on one context: f after each call equals
     the oracle's fresh RHS bitwise -- moved spheres, a shorter and a longer
     list, an intervening full-field set_rhs, different subsampling."""
     shape = (64, 48, 64)
