@@ -1083,8 +1083,9 @@ def test_sphere_rhs_sequence_clears_previous(mg, bc):
     o = oracle.Oracle(shape, 1.0, bt, bv, min_coarse=4)
     L = np.array(shape, float)
     c0, q0 = W.random_spheres(L, 4.0, 30, seed=5)
+    per = (True, False, True) if bc == "periodic" else (False, False, False)
     steps = [(c0, q0, 1), (W.move_spheres(c0, np.full(30, 4.0), L, 1, amplitude=2.0,
-                                          periodic=(bc == "periodic",) * 3), q0, 2),
+                                          periodic=per), q0, 2),
              (c0[:11], q0[:11], 1), ("field", None, None), (c0, q0, 3)]
     for c, q, sub in steps:
         if isinstance(c, str):
