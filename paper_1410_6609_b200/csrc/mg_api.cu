@@ -206,6 +206,10 @@ struct mg_ctx {
   int paths = 0;      // MG_PATH_* taken by the last recorded V-cycle
   int nsm = 148;      // SMs of the device (cudaDevAttrMultiProcessorCount)
   cudaStream_t s_comm = nullptr;
+  // sphere RHS: the clear of f runs on s_aux while the sphere kernels that do
+  // not touch f (bins, neighbour lists, counts) run on the context's stream
+  cudaStream_t s_aux = nullptr;
+  cudaEvent_t ev_aux0 = nullptr, ev_aux1 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaEvent_t ev_sync = nullptr;  // NCCL contexts: polled by sync()
   std::vector<std::vector<Grid>> vlo, vhi, vin;   // per level, slab: views
@@ -1379,6 +1383,12 @@ void mg_destroy(mg_ctx *c) {
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->ev_sync) cudaEventDestroy(c->ev_sync);
+  if (c->s_aux) {
+    cudaStreamSynchronize(c->s_aux);
+    cudaStreamDestroy(c->s_aux);
+  }
+  if (c->ev_aux0) cudaEventDestroy(c->ev_aux0);
+  if (c->ev_aux1) cudaEventDestroy(c->ev_aux1);
   if (c->s_h2d) cudaStreamSynchronize(c->s_h2d);
   if (c->s_d2h) cudaStreamSynchronize(c->s_d2h);
   for (int q = 0; q < 3; q++) {
@@ -1447,10 +1457,21 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     c->sph_cap = (size_t)n;
   }
   unsigned long long *cnt = (unsigned long long *)(c->sph + 5 * c->sph_cap);
-  for (const Grid &g : c->g[0]) {
-    CK(cudaMemsetAsync(g.fR, 0, sizeof(double) * mg::grid_elems(g), c->stream));
-    CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
+  // f := 0 on the side stream (bandwidth-bound) overlapping the bins,
+  // neighbour lists and counts (ALU-bound, not touching f); joined before
+  // the scatter
+  if (!c->s_aux) {
+    CK(cudaStreamCreateWithFlags(&c->s_aux, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&c->ev_aux0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&c->ev_aux1, cudaEventDisableTiming));
   }
+  CK(cudaEventRecord(c->ev_aux0, c->stream));
+  CK(cudaStreamWaitEvent(c->s_aux, c->ev_aux0, 0));
+  for (const Grid &g : c->g[0]) {
+    CK(cudaMemsetAsync(g.fR, 0, sizeof(double) * mg::grid_elems(g), c->s_aux));
+    CK(cudaMemsetAsync(g.fB, 0, sizeof(double) * mg::grid_elems(g), c->s_aux));
+  }
+  CK(cudaEventRecord(c->ev_aux1, c->s_aux));
   if (n > 0) {
     CK(cudaMemcpyAsync(c->sph, h5, sizeof(double) * 5 * (size_t)n,
                        cudaMemcpyHostToDevice, c->stream));
@@ -1493,11 +1514,13 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
     mg::launch_sphere_bin(c->g[0][0], c->h, n, c->sph, B, c->stream);
     mg::launch_sphere_neighbours(c->g[0][0], c->h, n, c->sph, B, S, c->stream);
     mg::launch_sphere_counts(c->g[0][0], c->h, subsample, n, c->sph, cnt, c->stream);
+    CK(cudaStreamWaitEvent(c->stream, c->ev_aux1, 0));  // f cleared
     for (const Grid &g : c->g[0])
       mg::launch_sphere_scatter(g, c->h, subsample, n, c->sph, normalization, cnt, S,
                                 c->stream);
     CK(cudaGetLastError());
   }
+  CK(cudaStreamWaitEvent(c->stream, c->ev_aux1, 0));  // (n == 0: the clear alone)
   int rc = bc_adapt(c);
   if (rc) return rc;
   c->prev_norm = -1.0;
