@@ -142,6 +142,8 @@ typedef struct {
 #define MG_OFF_CG_CLUSTER 8  /* 8-CTA cluster CG -> single-CTA CG             */
 #define MG_OFF_MASK_CODES 16 /* masked levels: byte codes -> float records    */
 #define MG_OFF_TAIL 32       /* persistent tail kernel -> a launch per step   */
+#define MG_OFF_RED0 64       /* restriction + next level's first red sweep
+                                (from Phi = 0) -> two kernels               */
 
 /* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
 #define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
@@ -152,6 +154,7 @@ typedef struct {
 #define MG_PATH_PROLONG_FUSED 32 /* prolongation fused with the red sweep     */
 #define MG_PATH_FUSED_NORM 64    /* norm from the in-cycle residual (c11)     */
 #define MG_PATH_TAIL 128         /* coarse levels in the persistent tail      */
+#define MG_PATH_RED0 256         /* a restriction did the next red sweep      */
 
 typedef struct mg_ctx mg_ctx;
 

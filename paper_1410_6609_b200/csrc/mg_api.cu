@@ -591,7 +591,9 @@ int smooth_half(mg_ctx *c, int l, int color, int from_zero) {
 
 // f_{l+1} = R (f_l - A Phi_l); at the agglomeration level every rank then
 // all-gathers the restricted RHS (in place) so that each holds the whole level
-int restrict_level(mg_ctx *c, int l) {
+// red0: the restriction also performs level l+1's first red half-sweep from
+// Phi = 0 (box domains; mg_opts.disable MG_OFF_RED0 turns it off)
+int restrict_level(mg_ctx *c, int l, bool red0 = false) {
   if (l == 0) mark(c, CAT_NONE);
   const bool with_norm = l == 0 && fused_norm_on(c);
   int cnt[kMaxSlabs] = {0};  // norm partials per slab (fused norm, reading c11)
@@ -609,12 +611,12 @@ int restrict_level(mg_ctx *c, int l) {
     } else if (march) {
       if (with_norm)
         cnt[s] = mg::launch_resid_restrict_norm_march(c->g[l][s], coarse_of(c, l, s), t.rr,
-                                                      t.rb, part, c->stream);
+                                                      t.rb, part, c->stream, red0);
       else
         mg::launch_resid_restrict_march(c->g[l][s], coarse_of(c, l, s), t.rr, t.rb,
-                                        c->stream);
+                                        c->stream, red0);
     } else {
-      mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), 0, c->stream);
+      mg::launch_resid_restrict(c->g[l][s], coarse_of(c, l, s), red0, c->stream);
     }
     c->launches++;
   }
@@ -628,7 +630,20 @@ int restrict_level(mg_ctx *c, int l) {
     return gather_portions(c, l + 1, 2, sizeof(double), [](const Grid &g, int a) {
       return (void *)(a ? g.fB : g.fR);
     });
+  if (red0) {  // the red half-sweep's ghost exchange
+    c->paths |= MG_PATH_RED0;
+    return halo(c, l + 1, 0);
+  }
   return MG_OK;
+}
+
+// may the restriction of level l perform level l+1's first red half-sweep
+// (from Phi = 0)?  Levels above `top` (the tail's first level), box grids
+// without mask, not into the first agglomerated level (its red Phi would
+// need the gather too), pre-smoothing on
+bool red0_fused(const mg_ctx *c, int l, int top) {
+  return !(c->o.disable & MG_OFF_RED0) && c->o.nu1 >= 1 && !c->masked && !any_periodic(c) &&
+         l + 1 < top && !(c->P > 1 && l + 1 == c->pl.nd);
 }
 
 int prolong_level(mg_ctx *c, int l) {
@@ -860,10 +875,12 @@ int enqueue_vcycle(mg_ctx *c) {
         CK(cudaMemsetAsync(g.phiB, 0, sizeof(double) * mg::grid_elems(g), c->stream));
       }
     for (int s = 0; s < c->o.nu1; s++) {
-      if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
+      // (l > 0, s == 0: from Phi = 0 -- done by the restriction of level l-1)
+      if (!(s == 0 && l > 0 && red0_fused(c, l - 1, top)))
+        if ((rc = smooth_half(c, l, 0, (l > 0 && s == 0) ? 1 : 0))) return rc;
       if ((rc = smooth_half(c, l, 1, 0))) return rc;
     }
-    if ((rc = restrict_level(c, l))) return rc;
+    if ((rc = restrict_level(c, l, red0_fused(c, l, top)))) return rc;
   }
   const int before = level_cat(c, top - 1);  // CAT_NONE: level 0 came last
   int open_cat;  // category of the interval open after the coarse end

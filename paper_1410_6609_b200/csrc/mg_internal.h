@@ -165,7 +165,9 @@ bool vcycle_tail_supported(const Grid &coarsest);
 int launch_vcycle_tail(const TailLevels &T, int nu1, int nu2, double alpha, double tol,
                        int maxit, double *cg_scr, int *iters_out, cudaStream_t s);
 void launch_smooth(const Grid &g, int color, int from_zero, cudaStream_t s);
-void launch_resid_restrict(const Grid &f, const Grid &c, int cofs,
+// red0 != 0 (box domains): also the coarse level's first red half-sweep
+// from Phi = 0 (the coarse red Phi from the restricted f alone)
+void launch_resid_restrict(const Grid &f, const Grid &c, int red0,
                            cudaStream_t s);
 void launch_prolong(const Grid &f, const Grid &c, int cofs, double alpha,
                     cudaStream_t s);
@@ -235,7 +237,7 @@ void launch_prolong_smooth_march(const Grid &g, const Grid &c,
 bool resid_march_supported(const Grid &g);
 bool make_tmap_resid(const Grid &g, const double *base, void *out128);
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
-                                 const void *tmB, cudaStream_t s);
+                                 const void *tmB, cudaStream_t s, int red0 = 0);
 int norm_march_blocks(const Grid &g);
 int march_blocks_max(const Grid &g);
 // split norm of a cycle's end: the last black half-sweep with the black
@@ -249,7 +251,7 @@ int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
 // (one per CTA, fixed order); returns the partial count
 int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,
                                      const void *tmB, double *partials,
-                                     cudaStream_t s);
+                                     cudaStream_t s, int red0 = 0);
 void launch_norm_march(const Grid &g, const void *tmR, const void *tmB,
                        double *partials, cudaStream_t s);
 bool encode_box(const Grid &g, const double *base, void *out128, unsigned box0,

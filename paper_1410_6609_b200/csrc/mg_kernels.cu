@@ -167,8 +167,11 @@ __host__ __device__ inline long long restrict_items(const Grid &F) {
   return (long long)(F.nxl >> 1) * (F.ny >> 1) * (F.nz >> 1);
 }
 
+// red0: also the coarse level's first red half-sweep from Phi = 0 on the
+// coarse cell if it is red (box domains; the from-zero sweep's expression)
 template <bool PER>
-__device__ __forceinline__ void restrict_cell(const Grid &F, const Grid &C, long long t) {
+__device__ __forceinline__ void restrict_cell(const Grid &F, const Grid &C, long long t,
+                                              int red0 = 0) {
   const int ncz = F.nz >> 1, ncy = F.ny >> 1;
   const int K = (int)(t % ncz);
   const long long q = t / ncz;
@@ -186,26 +189,32 @@ __device__ __forceinline__ void restrict_cell(const Grid &F, const Grid &C, long
   const int Ig = (F.x0 >> 1) + Il;
   const int col = (Ig + J + K) & 1;
   double *cf = col ? C.fB : C.fR;
-  cf[rowbase(C, Ig - C.x0, J) + (K >> 1)] = 0.125 * s;
+  const double fc = 0.125 * s;
+  cf[rowbase(C, Ig - C.x0, J) + (K >> 1)] = fc;
+  if (red0 && col == 0) {
+    const double d = (double)centre_d(C, Ig, J, K);
+    C.phiR[rowbase(C, Ig - C.x0, J) + (K >> 1)] = div_small(fc * C.w + 0.0, d,
+                                                             c_rcp16[(int)d]);
+  }
 }
 
 template <bool PER>
 __global__ void __launch_bounds__(kThreads)
-    k_resid_restrict(Grid F, Grid C) {
+    k_resid_restrict(Grid F, Grid C, int red0) {
   const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t < restrict_items(F)) restrict_cell<PER>(F, C, t);
+  if (t < restrict_items(F)) restrict_cell<PER>(F, C, t, red0);
 }
 
-void launch_resid_restrict(const Grid &f, const Grid &c, int /*cofs*/,
+void launch_resid_restrict(const Grid &f, const Grid &c, int red0,
                            cudaStream_t s) {
   const long long total =
       (long long)(f.nxl >> 1) * (f.ny >> 1) * (f.nz >> 1);
   if (total <= 0) return;
   const unsigned blocks = (unsigned)((total + kThreads - 1) / kThreads);
   if (is_periodic(f))
-    k_resid_restrict<true><<<blocks, kThreads, 0, s>>>(f, c);
+    k_resid_restrict<true><<<blocks, kThreads, 0, s>>>(f, c, 0);
   else
-    k_resid_restrict<false><<<blocks, kThreads, 0, s>>>(f, c);
+    k_resid_restrict<false><<<blocks, kThreads, 0, s>>>(f, c, red0);
 }
 
 // ---------------------------------------------------------------------------

@@ -344,7 +344,7 @@ template <int MODE, int VAR>
 __global__ void __launch_bounds__(kThreadsM, 2)
     k_resid_march(Grid g, const __grid_constant__ CUtensorMap tmR,
                   const __grid_constant__ CUtensorMap tmB, Grid C,
-                  double *partials) {
+                  double *partials, int red0) {
   constexpr bool MASK = VAR == VAR_MASK;
   constexpr bool PER = VAR == VAR_PER;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -587,8 +587,21 @@ __global__ void __launch_bounds__(kThreadsM, 2)
             const long long cb = (long long)(I - C.x0 + 1) * C.plane +
                                  (long long)(J + 1) * C.pz + (k >> 1);
             const int c0 = (I + J + k) & 1;
-            (c0 ? C.fB : C.fR)[cb] = 0.125 * (sdx0[c][0] + s0);
-            if (k + 1 < g.nzh) (c0 ? C.fR : C.fB)[cb] = 0.125 * (sdx0[c][1] + s1);
+            const double fk0 = 0.125 * (sdx0[c][0] + s0);
+            const double fk1 = 0.125 * (sdx0[c][1] + s1);
+            (c0 ? C.fB : C.fR)[cb] = fk0;
+            if (k + 1 < g.nzh) (c0 ? C.fR : C.fB)[cb] = fk1;
+            if (red0) {
+              // the coarse level's first red half-sweep from Phi = 0:
+              // Phi_red = (f w + 0) / d, the expression of k_smooth's
+              // from-zero sweep on the red cell among K = k, k+1
+              const int kr = c0 ? k + 1 : k;
+              if (kr < C.nz) {
+                const double fr = c0 ? fk1 : fk0;
+                const double d = (double)centre_dm(C, I, J, kr);
+                C.phiR[cb] = div_small(fr * C.w + 0.0, d, c_rcp16[(int)d]);
+              }
+            }
           }
         }
       }
@@ -795,20 +808,20 @@ bool resid_march_supported(const Grid &g) {
 
 template <int MODE, int M>
 static void launch_rm(const Grid &g, const Grid &c, const void *tmR,
-                      const void *tmB, double *partials, cudaStream_t s) {
+                      const void *tmB, double *partials, cudaStream_t s, int red0 = 0) {
   static size_t configured = 0;
   set_smem(k_resid_march<MODE, M>, resid_smem_bytes(), &configured);
   k_resid_march<MODE, M><<<resid_blocks(g), kThreadsM, resid_smem_bytes(), s>>>(
       g, *reinterpret_cast<const CUtensorMap *>(tmR),
-      *reinterpret_cast<const CUtensorMap *>(tmB), c, partials);
+      *reinterpret_cast<const CUtensorMap *>(tmB), c, partials, red0);
 }
 
 void launch_resid_restrict_march(const Grid &g, const Grid &c, const void *tmR,
-                                 const void *tmB, cudaStream_t s) {
+                                 const void *tmB, cudaStream_t s, int red0) {
   switch (variant(g)) {
     case VAR_MASK: launch_rm<MODE_RESTRICT, VAR_MASK>(g, c, tmR, tmB, nullptr, s); break;
     case VAR_PER: launch_rm<MODE_RESTRICT, VAR_PER>(g, c, tmR, tmB, nullptr, s); break;
-    default: launch_rm<MODE_RESTRICT, VAR_BOX>(g, c, tmR, tmB, nullptr, s); break;
+    default: launch_rm<MODE_RESTRICT, VAR_BOX>(g, c, tmR, tmB, nullptr, s, red0); break;
   }
 }
 
@@ -833,11 +846,11 @@ int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
 
 int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,
                                      const void *tmB, double *partials,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, int red0) {
   switch (variant(g)) {
     case VAR_MASK: launch_rm<MODE_BOTH, VAR_MASK>(g, c, tmR, tmB, partials, s); break;
     case VAR_PER: launch_rm<MODE_BOTH, VAR_PER>(g, c, tmR, tmB, partials, s); break;
-    default: launch_rm<MODE_BOTH, VAR_BOX>(g, c, tmR, tmB, partials, s); break;
+    default: launch_rm<MODE_BOTH, VAR_BOX>(g, c, tmR, tmB, partials, s, red0); break;
   }
   return resid_blocks(g);
 }

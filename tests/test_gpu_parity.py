@@ -1098,3 +1098,27 @@ def test_sphere_rhs_sequence_clears_previous(mg, bc):
             o.set_rhs_from_spheres(c, R, q, subsample=sub)
         assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
     s.close()
+
+
+@pytest.mark.parametrize("shape,bc,nu,P", [((256, 128, 128), "dirichlet0", (2, 2), 1),
+                                          ((128, 64, 130), "mixed", (3, 3), 1),
+                                          ((256, 64, 128), "channel", (2, 2), 2),
+                                          ((256, 64, 128), "channel", (1, 2), 4)])
+def test_restriction_with_first_red_sweep_equals_separate(mg, shape, bc, nu, P):
+    """The restriction that also performs the next level's first red
+    half-sweep from Phi = 0 (Phi_red = f w / d from the restricted f) gives
+    the separate kernels' iterates and norms bit for bit (MG_OFF_RED0), also
+    on EMULATE slabs (the red ghost exchange after the restriction)."""
+    f = np.random.default_rng(19).uniform(-1, 1, shape)
+    kw = dict(nranks=P, halo="emulate", agglomerate_below=4096) if P > 1 else {}
+    out = []
+    for off in (0, mg.MG_OFF_RED0):
+        s, _ = pair(mg, shape, 1.0, bc, min_coarse=2, nu1=nu[0], nu2=nu[1],
+                    disable=off, **kw)
+        s.set_rhs(f)
+        r = [s.vcycle() for _ in range(3)]
+        assert bool(s.cycle_paths & mg.MG_PATH_RED0) == (off == 0)
+        out.append((r, s.get_solution()))
+        s.close()
+    assert np.array_equal(out[0][1], out[1][1])
+    assert out[0][0] == out[1][0]
