@@ -35,4 +35,16 @@ for name, f, outs in (("host", fh, outs_h), ("device", fd, outs_d)):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / nsteps
         print("%-6s cycles %2d: %.2f ms per solve" % (name, cycles, ms))
+# the same cycles through mg_vcycle (a host synchronisation per cycle)
+s.set_rhs(fd)
+for _ in range(3):
+    s.vcycle()
+e0 = torch.cuda.Event(enable_timing=True)
+e1 = torch.cuda.Event(enable_timing=True)
+e0.record(stream)
+for _ in range(20):
+    s.vcycle()
+e1.record(stream)
+torch.cuda.synchronize()
+print("mg_vcycle x20: %.3f ms per cycle" % (e0.elapsed_time(e1) / 20))
 s.close()

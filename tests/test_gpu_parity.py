@@ -1101,7 +1101,7 @@ def test_sphere_rhs_sequence_clears_previous(mg, bc):
 
 
 @pytest.mark.parametrize("shape,bc,nu,P", [((256, 128, 128), "dirichlet0", (2, 2), 1),
-                                          ((128, 64, 130), "mixed", (3, 3), 1),
+                                          ((128, 64, 136), "mixed", (3, 3), 1),
                                           ((256, 64, 128), "channel", (2, 2), 2),
                                           ((256, 64, 128), "channel", (1, 2), 4)])
 def test_restriction_with_first_red_sweep_equals_separate(mg, shape, bc, nu, P):
