@@ -1,0 +1,86 @@
+"""Randomised GPU-vs-oracle parity (hypothesis, derandomised, bounded
+examples): random even shapes, boundary types per face (Dirichlet, Neumann,
+periodic pairs; at least one Dirichlet face), power-of-two spacings,
+schedules V(nu1, nu2), coarsest sizes, sphere or noise right-hand sides and
+slab counts.  Three cycles on both sides: Phi rel-L2 <= 1e-10 and the
+residual-history clause (reading c21); the per-cell steps are bitwise, so
+any indexing or boundary slip in a rarely exercised combination shows here.
+"""
+import numpy as np
+import pytest
+
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+hyp = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+D, N, P = 0, 1, 2
+
+
+@pytest.fixture(scope="module")
+def mg():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_1410_6609_b200 import _build
+    _build.build()
+    from paper_1410_6609_b200 import mg as M
+    return M
+
+
+@st.composite
+def problems(draw):
+    dims = [2 * draw(st.integers(1, 24)) for _ in range(3)]
+    if draw(st.booleans()):
+        dims[2] = 2 * draw(st.integers(32, 72))  # rows that take the marching kernels
+    bt = []
+    for a in range(3):
+        kind = draw(st.sampled_from(["dd", "dn", "nd", "nn", "pp"]))
+        bt += {"dd": [D, D], "dn": [D, N], "nd": [N, D], "nn": [N, N], "pp": [P, P]}[kind]
+    if D not in bt:
+        bt[draw(st.sampled_from([q for q in range(6) if bt[q] != P] or [2]))] = D
+        if bt.count(P) % 2:  # keep periodic pairs
+            bt = [D if t == P else t for t in bt]
+    bv = [0.0 if t == P else draw(st.floats(-2, 2)) for t in bt]
+    h = 2.0 ** draw(st.integers(-5, 1))
+    nu1 = draw(st.integers(0, 3))
+    nu2 = draw(st.integers(0 if nu1 else 1, 3))
+    mc = draw(st.sampled_from([1, 2, 4]))
+    slabs = draw(st.sampled_from([1, 1, 2]))
+    if dims[0] % (2 * slabs) or dims[0] // slabs < 4:
+        slabs = 1
+    seed = draw(st.integers(0, 2 ** 16))
+    return tuple(dims), bt, bv, h, nu1, nu2, mc, slabs, seed
+
+
+@settings(max_examples=40, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(problems())
+def test_random_problems_match_oracle(mg, prob):
+    shape, bt, bv, h, nu1, nu2, mc, slabs, seed = prob
+    kw = dict(min_coarse=mc, nu1=nu1, nu2=nu2)
+    try:
+        o = oracle.Oracle(shape, h, bt, bv, **kw)
+    except ValueError:
+        return
+    extra = dict(nranks=slabs, halo="loopback", agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, h, bt, bv, **kw, **extra)
+    except mg.MGError:
+        # the decomposition needs even slabs on the distributed levels
+        assert slabs > 1
+        return
+    f = np.random.default_rng(seed).uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
+    for a, b in zip(hg, ho):
+        assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob, hg, ho)
+    po = o.phi()
+    err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
+    assert err <= 1e-10, (prob, err)
+    s.close()
