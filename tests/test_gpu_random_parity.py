@@ -78,13 +78,17 @@ def test_random_problems_match_oracle(mg, prob):
     assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
     hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
     ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
-    # rounding-floor term (reading c21): 1e-15 r0 when the cycle has bitwise
-    # smoothing levels; a single-level hierarchy is the CG alone, whose dot
-    # products round differently on both sides (measured 1.7e-15 r0 on 2x4x2)
-    floor = 1e-15 if s.nlevels > 1 else 1e-14
-    for a, b in zip(hg, ho):
-        assert abs(a - b) <= 1e-8 * b + floor * ho[0], (prob, hg, ho)
     po = o.phi()
     err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
-    assert err <= 1e-10, (prob, err)
+    if s.nlevels == 1:
+        # a single-level hierarchy is the CG alone: both sides stop
+        # at ||r|| <= tau_c ||b|| (reading c8) at iterations whose residuals
+        # differ within that tolerance, not by rounding
+        tol = 1e-12 * ho[0]
+        assert all(x <= tol for x in hg[1:]) and all(x <= tol for x in ho[1:]), (prob, hg, ho)
+        assert err <= 1e-8, (prob, err)
+    else:
+        for a, b in zip(hg, ho):  # the history clause of reading c21
+            assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob, hg, ho)
+        assert err <= 1e-10, (prob, err)
     s.close()
