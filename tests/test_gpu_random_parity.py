@@ -82,9 +82,11 @@ def test_random_problems_match_oracle(mg, prob):
     err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
     if s.nlevels == 1:
         # a single-level hierarchy is the CG alone: both sides stop
-        # at ||r|| <= tau_c ||b|| (reading c8) at iterations whose residuals
-        # differ within that tolerance, not by rounding
-        tol = 1e-12 * ho[0]
+        # when the recursively updated residual is <= tau_c ||b|| (reading
+        # c8), at iterations whose residuals differ within that tolerance, not
+        # by rounding; the true residual reported here may exceed the
+        # recursive one by the recurrence's drift (a factor 4 allowed)
+        tol = 4e-12 * ho[0]
         assert all(x <= tol for x in hg[1:]) and all(x <= tol for x in ho[1:]), (prob, hg, ho)
         assert err <= 1e-8, (prob, err)
     else:
