@@ -144,6 +144,9 @@ typedef struct {
 #define MG_OFF_TAIL 32       /* persistent tail kernel -> a launch per step   */
 #define MG_OFF_RED0 64       /* restriction + next level's first red sweep
                                 (from Phi = 0) -> two kernels               */
+#define MG_OFF_LOOKAHEAD 128 /* look-ahead red sweep (the cycle-end norm's red
+                                residuals from the next cycle's first red
+                                half-sweep) -> a red residual pass          */
 
 /* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
 #define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
@@ -155,6 +158,7 @@ typedef struct {
 #define MG_PATH_FUSED_NORM 64    /* norm from the in-cycle residual (c11)     */
 #define MG_PATH_TAIL 128         /* coarse levels in the persistent tail      */
 #define MG_PATH_RED0 256         /* a restriction did the next red sweep      */
+#define MG_PATH_LOOKAHEAD 512    /* the cycle ended with the look-ahead sweep */
 
 typedef struct mg_ctx mg_ctx;
 

@@ -247,6 +247,12 @@ int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
                              double *partials, cudaStream_t s);
 int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
                           double *partials, cudaStream_t s);
+// the look-ahead red half-sweep: the next cycle's first red half-sweep
+// written to g.phiR (a second buffer) from the current Phi^R in oldv, with the
+// current iterate's red residual partials; returns their count
+int launch_smooth_lookahead_march(const Grid &g, const void *tm_oth128,
+                                  const double *oldv, double *partials,
+                                  cudaStream_t s);
 // residual + restriction that also writes the norm partials of that residual
 // (one per CTA, fixed order); returns the partial count
 int launch_resid_restrict_norm_march(const Grid &g, const Grid &c, const void *tmR,

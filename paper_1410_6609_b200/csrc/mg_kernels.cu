@@ -420,7 +420,7 @@ void launch_first_empty(const unsigned long long *counts, int n, double *host_ds
 // the same bits) for its cell and the six neighbours and stores its own
 // p_new in the other of two p buffers (p_old stays readable: no barrier).
 // ---------------------------------------------------------------------------
-static constexpr int kCgThreads = 1024;
+static constexpr int kCgThreads = 512;  // cg_threads' largest count
 static constexpr long long kCgSmemMax = 4096;  // unknowns with smem vectors
 
 __device__ __forceinline__ long long split_index(const Grid &g, int il, int j,
@@ -565,16 +565,164 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
+// doubles of the register-resident CG's shared area: r and two p buffers,
+// each with a zero slot at index N
+__host__ __device__ inline size_t cg_reg_doubles(long long N) { return 3 * (size_t)(N + 1); }
+
+// The same iteration as cg_cta with every per-element quantity the thread
+// owns in registers: element n = threadIdx.x + e * nthr (e < E, the strided
+// order of cg_cta, so the per-thread partial sums and the tree -- hence every
+// bit of the iterates -- are cg_cta's), x and the own r, p_old in registers,
+// the six neighbour offsets computed once (a neighbour outside the level
+// points at a zero slot whose r and p stay 0: r[k] + beta * 0 = +0, the value
+// cg_cta selects).  Shared memory holds what neighbours read: r and the two
+// p buffers.  Requires N <= E * nthr.
+template <bool PER, int E>
+__device__ __forceinline__ void cg_cta_reg(const Grid &g, double *sm, double (*part)[32],
+                                           double tol, int maxit, int *iters_out,
+                                           int nthr) {
+  const int N = g.nx * g.ny * g.nz;
+  double *rs = sm, *pA = sm + (N + 1), *pB = sm + 2 * (N + 1);
+  const int sx = g.ny * g.nz, sy = g.nz;
+  const int wx = (g.nx - 1) * sx, wy = (g.ny - 1) * sy, wz = g.nz - 1;
+  unsigned nb[E][3];  // six 16-bit offsets (N <= kCgSmemMax < 65536)
+  double x[E], r[E], po[E], dd[E];
+  bool act[E];
+  double acc = 0.0;
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int n = (int)threadIdx.x + e * nthr;
+    act[e] = (int)threadIdx.x < nthr && n < N;
+    x[e] = 0.0;
+    po[e] = 0.0;
+    r[e] = 0.0;
+    dd[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) nb[e][a] = (unsigned)N * 0x10001u;
+    if (act[e]) {
+      const int z = n % g.nz;
+      const int t = n / g.nz;
+      const int j = t % g.ny, i = t / g.ny;
+      const bool in[6] = {i > 0, i < g.nx - 1, j > 0, j < g.ny - 1, z > 0, z < g.nz - 1};
+      const int kin[6] = {n - sx, n + sx, n - sy, n + sy, n - 1, n + 1};
+      const int kpe[6] = {n + wx, n - wx, n + wy, n - wy, n + wz, n - wz};
+      int k6[6];
+#pragma unroll
+      for (int a = 0; a < 6; a++)
+        k6[a] = in[a] ? kin[a] : ((PER && g.per[a >> 1]) ? kpe[a] : N);
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+        nb[e][a] = (unsigned)k6[2 * a] | ((unsigned)k6[2 * a + 1] << 16);
+      dd[e] = (double)centre_d(g, i, j, z);
+      int col;
+      const long long idx = split_index(g, i, j, z, &col);
+      const double b = col ? g.fB[idx] : g.fR[idx];
+      r[e] = b;
+      rs[n] = b;
+      pA[n] = 0.0;  // p_old of the first iteration: p = r + 0 * 0 = r
+      acc = acc + b * b;
+    }
+  }
+  if (threadIdx.x == 0) {
+    rs[N] = 0.0;
+    pA[N] = 0.0;
+    pB[N] = 0.0;
+  }
+  int pb = 0;
+  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes r, p_old
+  pb ^= 1;
+  const double bnorm = sqrt(rho);
+  const double c = g.c;
+  double beta = 0.0;
+  double *pso = pA, *psn = pB;  // p of the last iteration / of this one
+  int it = 0;
+  if (bnorm > 0.0) {
+    while (it < maxit) {
+      double p[E], q[E];
+      acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        auto v = [&](int a) {
+          const int k = (int)((nb[e][a >> 1] >> (16 * (a & 1))) & 0xffffu);
+          return rs[k] + beta * pso[k];
+        };
+        const double s = ((((v(0) + v(1)) + v(2)) + v(3)) + v(4)) + v(5);
+        p[e] = r[e] + beta * po[e];
+        q[e] = c * (dd[e] * p[e] - s);
+        if (act[e]) {
+          psn[(int)threadIdx.x + e * nthr] = p[e];
+          acc = acc + p[e] * q[e];
+        }
+      }
+      const double pq = cg_allsum(acc, part[pb]);
+      pb ^= 1;
+      const double a = rho / pq;
+      acc = 0.0;
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        if (act[e]) {
+          x[e] = x[e] + a * p[e];
+          r[e] = r[e] - a * q[e];
+          rs[(int)threadIdx.x + e * nthr] = r[e];
+          acc = acc + r[e] * r[e];
+        }
+        po[e] = p[e];
+      }
+      const double rho1 = cg_allsum(acc, part[pb]);
+      pb ^= 1;
+      it++;
+      if (sqrt(rho1) <= tol * bnorm) break;
+      beta = rho1 / rho;
+      rho = rho1;
+      double *t = pso;
+      pso = psn;
+      psn = t;
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    if (!act[e]) continue;
+    const int n = (int)threadIdx.x + e * nthr;
+    const int z = n % g.nz;
+    const int t = n / g.nz;
+    int col;
+    const long long idx = split_index(g, t / g.ny, t % g.ny, z, &col);
+    (col ? g.phiB : g.phiR)[idx] = x[e];
+  }
+  if (threadIdx.x == 0 && iters_out) *iters_out = it;
+}
+
+// the register-resident CG for the elements per thread N needs (<= 4), else
+// false (the caller runs cg_cta)
+template <bool PER, int MAXE = 4>
+__device__ __forceinline__ bool cg_cta_fast(const Grid &g, double *sm, double (*part)[32],
+                                            double tol, int maxit, int *iters_out,
+                                            int nthr) {
+  const int N = g.nx * g.ny * g.nz;
+  const int E = (N + nthr - 1) / nthr;
+  if (E <= 1)
+    cg_cta_reg<PER, 1>(g, sm, part, tol, maxit, iters_out, nthr);
+  else if (E <= 2)
+    cg_cta_reg<PER, 2>(g, sm, part, tol, maxit, iters_out, nthr);
+  else if (MAXE >= 4 && E <= 4)
+    cg_cta_reg<PER, 4>(g, sm, part, tol, maxit, iters_out, nthr);
+  else
+    return false;
+  return true;
+}
+
 template <bool PER>
 __global__ void __launch_bounds__(kCgThreads)
     k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
   extern __shared__ double cg_sm[];
   __shared__ double part[2][32];
   const long long N = (long long)g.nx * g.ny * g.nz;
-  if (N <= kCgSmemMax)
-    cg_cta<PER>(g, cg_sm, part, tol, maxit, iters_out, (int)blockDim.x);
-  else
+  if (N <= kCgSmemMax) {
+    if (!cg_cta_fast<PER>(g, cg_sm, part, tol, maxit, iters_out, (int)blockDim.x))
+      cg_cta<PER>(g, cg_sm, part, tol, maxit, iters_out, (int)blockDim.x);
+  } else {
     cg_cta<PER>(g, scr, part, tol, maxit, iters_out, (int)blockDim.x);
+  }
 }
 
 size_t coarse_cg_scratch_doubles(const Grid &g) {
@@ -1252,9 +1400,12 @@ __global__ void __launch_bounds__(kTailThreads)
   const Grid &gc = T.g[T.n - 1];
   if (cl.block_rank() == 0) {
     const long long N = (long long)gc.nx * gc.ny * gc.nz;
-    if (N <= kCgSmemMax)
-      cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
-    else
+    if (N <= kCgSmemMax) {
+      // (at most two elements per thread here: the tail kernel's other
+      // steps leave no registers for four)
+      if (!cg_cta_fast<PER, 2>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr))
+        cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
+    } else
       cg_cta<PER>(gc, cg_scr, part, tol, maxit, iters_out, cg_nthr);
   }
   cl.sync();

@@ -41,15 +41,21 @@ enum { VAR_BOX = 0, VAR_MASK = 1, VAR_PER = 2 };
 
 // rows of <= 128 half-entries (NCH <= 2: level 1 and below at 512^3) fit 3
 // CTAs per SM (<= 85 registers, no spills; 4 spilled and were no faster)
-// NORM: also the residual of every updated cell after the sweep (its
+// NORM 1: also the residual of every updated cell after the sweep (its
 // neighbours are the other colour, final), f - c (d u - s) with the residual
 // kernels' expression, r^2 summed into one partial per CTA (fixed order) --
 // the last black half-sweep of a cycle then leaves only the red residuals to
-// the norm pass (12 instead of 16 B/cell)
-template <bool PROLONG, int NCH, int VAR, bool NORM = false>
+// the norm pass (12 instead of 16 B/cell).
+// NORM 2 (the look-ahead red sweep): the residual of each updated
+// cell BEFORE the sweep, u = oldv (the own colour's current values; the sweep
+// writes its results to g's own array, a different buffer): the same s and
+// d serve the residual and the update, so the red residuals of the iterate
+// cost 4 B/cell more than the sweep instead of a 12 B/cell pass.
+template <bool PROLONG, int NCH, int VAR, int NORM = 0>
 __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
     k_smooth_march(Grid g, const __grid_constant__ CUtensorMap tm_oth,
-                   int color, Grid C, double alpha, double *partials) {
+                   int color, Grid C, double alpha, double *partials,
+                   const double *__restrict__ oldv) {
   constexpr bool MASK = VAR == VAR_MASK;
   constexpr bool PER = VAR == VAR_PER;
   extern __shared__ __align__(128) unsigned char smem[];
@@ -195,6 +201,19 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       mbar_expect_tx(&bars[s], box_bytes);
       tma_load_3d(ring + (size_t)s * sd, &tm_oth, 0, j0, i0 + q + 3, &bars[s]);
     }
+    // NORM 2: the own colour's values before the sweep (issued before the
+    // ring waits, so that their latency overlaps them)
+    double2 ov[NCH];
+    if (NORM == 2) {
+#pragma unroll
+      for (int c = 0; c < NCH; c++) {
+        const int k = 2 * lane + 64 * c;
+        ov[c] = make_double2(0.0, 0.0);
+        if (row_ok && k < g.nzh)
+          ov[c] = *reinterpret_cast<const double2 *>(
+              oldv + (long long)(il + 1) * g.plane + (long long)(j + 1) * pz + k);
+      }
+    }
     // wait for planes q-1 (first step only), q (first step only), q+1
     if (q == 1) {
       mbar_wait(&bars[0], 0);
@@ -292,9 +311,11 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
         out.x = div_small(fr[c].x * g.w + s0, d0, c_rcp16[(int)d0]);
         out.y = div_small(fr[c].y * g.w + s1, d1, c_rcp16[(int)d1]);
         if (NORM) {
-          const double r0 = (cd0 & 64) ? fr[c].x - g.c * (d0 * out.x - s0) : 0.0;
+          const double u0 = NORM == 2 ? ov[c].x : out.x;
+          const double u1 = NORM == 2 ? ov[c].y : out.y;
+          const double r0 = (cd0 & 64) ? fr[c].x - g.c * (d0 * u0 - s0) : 0.0;
           const double r1 =
-              (k + 1 < g.nzh && (cd1 & 64)) ? fr[c].y - g.c * (d1 * out.y - s1) : 0.0;
+              (k + 1 < g.nzh && (cd1 & 64)) ? fr[c].y - g.c * (d1 * u1 - s1) : 0.0;
           nacc = nacc + r0 * r0;
           nacc = nacc + r1 * r1;
         }
@@ -730,27 +751,27 @@ static int smooth_blocks(const Grid &g) {
   return nrt * ((g.nxl + ich - 1) / ich);
 }
 
-template <bool P, int NCH, int M, bool NORM = false>
+template <bool P, int NCH, int M, int NORM = 0>
 static void launch_sm(const Grid &g, const Grid &c, const CUtensorMap *tm,
                       int color, double alpha, cudaStream_t s,
-                      double *partials = nullptr) {
+                      double *partials = nullptr, const double *oldv = nullptr) {
   const size_t smem = smooth_smem_bytes(g);
   static size_t configured = 0;
   set_smem(k_smooth_march<P, NCH, M, NORM>, smem, &configured);
   k_smooth_march<P, NCH, M, NORM><<<smooth_blocks(g), kThreadsM, smem, s>>>(
-      g, *tm, color, c, alpha, partials);
+      g, *tm, color, c, alpha, partials, oldv);
 }
 
-template <bool P, int M, bool NORM = false>
+template <bool P, int M, int NORM = 0>
 static void launch_sm_n(const Grid &g, const Grid &c, const void *tm128,
                         int color, double alpha, cudaStream_t s,
-                        double *partials = nullptr) {
+                        double *partials = nullptr, const double *oldv = nullptr) {
   const CUtensorMap *tm = reinterpret_cast<const CUtensorMap *>(tm128);
   switch ((g.nzh + 63) >> 6) {
-    case 1: launch_sm<P, 1, M, NORM>(g, c, tm, color, alpha, s, partials); break;
-    case 2: launch_sm<P, 2, M, NORM>(g, c, tm, color, alpha, s, partials); break;
-    case 3: launch_sm<P, 3, M, NORM>(g, c, tm, color, alpha, s, partials); break;
-    default: launch_sm<P, 4, M, NORM>(g, c, tm, color, alpha, s, partials); break;
+    case 1: launch_sm<P, 1, M, NORM>(g, c, tm, color, alpha, s, partials, oldv); break;
+    case 2: launch_sm<P, 2, M, NORM>(g, c, tm, color, alpha, s, partials, oldv); break;
+    case 3: launch_sm<P, 3, M, NORM>(g, c, tm, color, alpha, s, partials, oldv); break;
+    default: launch_sm<P, 4, M, NORM>(g, c, tm, color, alpha, s, partials, oldv); break;
   }
 }
 
@@ -771,15 +792,29 @@ int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
                              double *partials, cudaStream_t s) {
   switch (variant(g)) {
     case VAR_MASK:
-      launch_sm_n<false, VAR_MASK, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      launch_sm_n<false, VAR_MASK, 1>(g, g, tm_oth128, color, 0.0, s, partials);
       break;
     case VAR_PER:
-      launch_sm_n<false, VAR_PER, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      launch_sm_n<false, VAR_PER, 1>(g, g, tm_oth128, color, 0.0, s, partials);
       break;
     default:
-      launch_sm_n<false, VAR_BOX, true>(g, g, tm_oth128, color, 0.0, s, partials);
+      launch_sm_n<false, VAR_BOX, 1>(g, g, tm_oth128, color, 0.0, s, partials);
       break;
   }
+  return smooth_blocks(g);
+}
+
+// the look-ahead red half-sweep (NORM 2): reads Phi^B (ring), f^R and the
+// current Phi^R (oldv), writes the swept Phi^R to g.phiR (another buffer)
+// and the red residual partials of the current iterate; box and periodic
+// grids (no mask)
+int launch_smooth_lookahead_march(const Grid &g, const void *tm_oth128,
+                                  const double *oldv, double *partials,
+                                  cudaStream_t s) {
+  if (variant(g) == VAR_PER)
+    launch_sm_n<false, VAR_PER, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv);
+  else
+    launch_sm_n<false, VAR_BOX, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv);
   return smooth_blocks(g);
 }
 

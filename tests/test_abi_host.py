@@ -122,10 +122,14 @@ def test_plan_errors():
 
 def test_workspace_bytes_model():
     """Split layout: 4 fields per level, ghost planes/rows, pitch
-    nz/2 -> x4; no device query (the same bytes on any SM count)."""
+    nz/2 -> x4; no device query (the same bytes on any SM count).  One
+    level-0 slab: a fifth level-0 array, the look-ahead red buffer."""
     nb = mg.workspace_bytes((512, 512, 512), min_coarse=8)
-    fine = 4 * 514 * 514 * 256 * 8
+    fine = 5 * 514 * 514 * 256 * 8
     assert fine < nb < fine * 1.2
+    nb1 = mg.workspace_bytes((512, 512, 512), min_coarse=8, disable=mg.MG_OFF_LOOKAHEAD)
+    assert nb - nb1 == 514 * 514 * 256 * 8
+    assert mg.workspace_bytes((512, 512, 512), min_coarse=8, fused_norm=True) == nb1
     nb2 = mg.workspace_bytes((1024, 512, 512), min_coarse=8, nranks=2,
                              halo="nccl")
     slab = 4 * 514 * 514 * 256 * 8
