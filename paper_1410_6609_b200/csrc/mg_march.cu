@@ -173,6 +173,19 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       if (tOkB[m]) add(slot + tRowA[m] + pz, tK[m], E[m]);
     }
   };
+  // parent rows J = j0/2 - 1 .. j0/2 + TY/2 of coarse plane i >> 1 (array
+  // rows J + 1, contiguous), both colours
+  auto prefetch_parent_rows = [&](int i) {
+    if (!((PER && g.per[0]) || (i >= 0 && i < g.nx))) return;
+    const long long off =
+        (long long)((i >> 1) - C.x0 + 1) * C.plane + (long long)(j0 >> 1) * C.pz;
+    const int rows = min(kJR, C.ny + 2 - (j0 >> 1));
+    const unsigned bytes = (unsigned)(rows * C.pz * 8);
+    prefetch_l2_bulk(C.phiR + off, bytes);
+    prefetch_l2_bulk(C.phiB + off, bytes);
+  };
+  if (PROLONG && threadIdx.x == 0)
+    for (int q = 0; q < 4 && q < nplanes; q += 2) prefetch_parent_rows(g.x0 + i0 - 1 + q);
   double2 E[kTPW];
   if (PROLONG && nplanes > 2) load_e(2, E);
 
@@ -192,6 +205,10 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
   }
 
   double nacc = 0.0;  // NORM: sum of r^2 of this thread's updated cells
+  if (NORM == 2 && threadIdx.x == 0)  // the first two planes' own rows
+    for (int il = i0; il < i1 && il < i0 + 2; il++)
+      prefetch_l2_bulk(oldv + (long long)(il + 1) * g.plane + (long long)(j0 + 1) * pz,
+                       (unsigned)(min(kTY, g.ny - j0) * pz * 8));
   for (int il = i0; il < i1; il++) {
     const int q = il - i0 + 1;  // ring index of the current plane
     __syncthreads();            // everybody is done with plane q-2's slot
@@ -201,8 +218,18 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       mbar_expect_tx(&bars[s], box_bytes);
       tma_load_3d(ring + (size_t)s * sd, &tm_oth, 0, j0, i0 + q + 3, &bars[s]);
     }
-    // NORM 2: the own colour's values before the sweep (issued before the
-    // ring waits, so that their latency overlaps them)
+    // NORM 2: the tile's rows of the own colour two planes ahead into L2 (one
+    // bulk prefetch: the rows are contiguous), then this plane's values into
+    // registers (issued before the ring waits)
+    if (NORM == 2 && threadIdx.x == 0 && il + 2 < i1)
+      prefetch_l2_bulk(oldv + (long long)(il + 3) * g.plane + (long long)(j0 + 1) * pz,
+                       (unsigned)(min(kTY, g.ny - j0) * pz * 8));
+    // PROLONG: the parent rows of local plane q + 4 (both colours) into L2,
+    // once per coarse plane, ahead of load_e's register loads
+    if (PROLONG && threadIdx.x == 0 && q + 4 < nplanes) {
+      const int i4 = g.x0 + i0 - 1 + q + 4;
+      if (!(i4 & 1) || q == 1) prefetch_parent_rows(i4);
+    }
     double2 ov[NCH];
     if (NORM == 2) {
 #pragma unroll
@@ -453,6 +480,16 @@ __global__ void __launch_bounds__(kThreadsM, 2)
   };
   if (PER) load_wrap(i0, wr);
 
+  // f of the row tile's rows (all z-tiles: contiguous rows) two planes
+  // ahead into L2, by the z-tile 0 CTA, ahead of the register prefetch
+  auto prefetch_f = [&](int il) {
+    const long long o = (long long)(il + 1) * g.plane + (long long)(j0 + 1) * g.pz;
+    const unsigned bytes = (unsigned)(min(kTY, g.ny - j0) * g.pz * 8);
+    prefetch_l2_bulk(g.fR + o, bytes);
+    if (MODE != MODE_NORM_RED) prefetch_l2_bulk(g.fB + o, bytes);
+  };
+  if (zt == 0 && threadIdx.x == 0)
+    for (int il = i0 + 1; il < i1 && il < i0 + 3; il++) prefetch_f(il);
   for (int il = i0; il < i1; il++) {
     const int q = il - i0 + 1;
     __syncthreads();
@@ -460,6 +497,7 @@ __global__ void __launch_bounds__(kThreadsM, 2)
       fence_proxy_async();
       issue(q + 3);
     }
+    if (zt == 0 && threadIdx.x == 0 && il + 3 < i1) prefetch_f(il + 3);
     if (q == 1) {
       mbar_wait(&bars[0], 0);
       mbar_wait(&bars[1], 0);

@@ -61,6 +61,12 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
 
+// bulk prefetch of `bytes` (a multiple of 16) of global memory into L2
+__device__ __forceinline__ void prefetch_l2_bulk(const void *p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes)
+               : "memory");
+}
+
 __device__ __forceinline__ int centre_dm(const Grid &g, int i, int j, int z) {
   int d = 6;
   if (i == 0) d += g.dface[0];
