@@ -353,6 +353,21 @@ def run_cuda(args):
     # ---- warm-up (includes graph capture) ----
     for _ in range(args.warmup):
         s.vcycle()
+    # ---- roofline of the dominant kernel (level-0 RBGS half-sweep), live:
+    # CUDA events between the phases of recorded cycles (a graph of its own,
+    # with event nodes), run right after the warm-up from the same idle state
+    # as the timed region (a pause between the two lets the board's power
+    # management recover from these cycles) ----
+    s.set_profiling(True)
+    prof = []
+    for _ in range(max(3, min(args.steps, 10))):
+        s.vcycle()
+        prof.append(s.last_cycle_times())
+    s.set_profiling(False)
+    for _ in range(2):  # re-record the cycle graphs (one per red buffer)
+        s.vcycle()
+    torch.cuda.synchronize()
+    time.sleep(1.0)
     # ---- timed region: K V-cycles, barrier + sync on both sides ----
     clocks = ClockSampler(local)
     clocks.start()
@@ -406,13 +421,6 @@ def run_cuda(args):
                      "note": "cycles back to back for ~0.5 s after the timed region; "
                              "steady = the last %d (power-capped clocks)" % tail}
 
-    # ---- roofline of the dominant kernel (level-0 RBGS half-sweep), live ----
-    s.set_profiling(True)
-    prof = []
-    for _ in range(max(3, min(args.steps, 10))):
-        s.vcycle()
-        prof.append(s.last_cycle_times())
-    s.set_profiling(False)
     sm0 = np.mean([p["smooth0_ms"] for p in prof])
     nsm = prof[0]["smooth0_launches"]
     cyc_prof = np.mean([p["cycle_ms"] for p in prof])
@@ -439,10 +447,13 @@ def run_cuda(args):
         frac = 8.0 ** -l
         model_bytes += (24 * nsw + 34) * frac
     # the norm: 16 B/cell; the split cycle-end norm reads 12 --
-    # the black residuals ride on the last black half-sweep.  The library
-    # reports which path the recorded cycle took (mg_cycle_paths).
+    # the black residuals ride on the last black half-sweep; with the
+    # look-ahead red sweep the red residuals cost its read of the current
+    # red values, 4.  The library reports which path the recorded cycle took
+    # (mg_cycle_paths).
     split = bool(s.cycle_paths & mg.MG_PATH_SPLIT_NORM)
-    model_bytes += 12 if split else 16
+    lookahead = bool(s.cycle_paths & mg.MG_PATH_LOOKAHEAD)
+    model_bytes += 4 if lookahead else (12 if split else 16)
     cycle_ms = ms / args.steps
     cycle_frac = model_bytes * local_cells / (cycle_ms * 1e-3) / 1e9 / peak
 
@@ -547,7 +558,9 @@ def run_cuda(args):
                      "cycle_model_frac": round(cycle_frac, 4),
                      "breakdown_ms": {k: round(float(np.mean([p[k] for p in prof])), 4)
                                       for k in prof[0]},
-                     "cycle_model_bytes_per_cell": round(model_bytes, 2)},
+                     "cycle_model_bytes_per_cell": round(model_bytes, 2),
+                     "norm_path": ("look-ahead red sweep" if lookahead else
+                                   "split" if split else "full pass")},
         "gpu_launches": int(launches * args.steps),
         "clocks": ck,
         "e2e": e2e,
