@@ -108,7 +108,8 @@ typedef struct {
   int use_graph;      /* capture one V-cycle as a CUDA graph (default 1)     */
   int fused_norm;     /* reading c11 (Alg.1):
                          0 (default) = mg_vcycle returns ||f - A Phi|| of the
-                         new iterate (a separate 16 B/cell pass);
+                         new iterate (4, 12 or 16 B/cell of extra traffic:
+                         look-ahead sweep, split norm, full pass);
                          1 = it returns the norm of the level-0 residual the
                          cycle computes after pre-smoothing for the
                          restriction (no extra pass).  mg_solve's r_0 is a
@@ -334,9 +335,16 @@ int mg_timestep(mg_ctx *ctx, int n, const double *centers, const double *radii,
                 int force_subsample, int *cycles_out, double *res_out);
 
 /* ---- solve --------------------------------------------------------------- */
-/* One V(nu1,nu2)-cycle; *res_norm_out (may be NULL) = ||f - A Phi||_2 over
- * all cells after the cycle (unscaled, reading c10).  Synchronises.
- * MG_ERR_DIVERGED if the norm is NaN or > 10x the previous cycle's. */
+/* One V(nu1,nu2)-cycle (Alg.1); *res_norm_out (may be NULL)
+ * = ||f - A Phi||_2 over all cells after the cycle (unscaled, reading c10).
+ * Synchronises.  MG_ERR_DIVERGED if the norm is NaN or > 10x the previous
+ * cycle's.  On one level-0 slab (nu1, nu2 >= 1, no mask, true cycle-end
+ * norm) the cycle ends with the look-ahead red sweep: the next cycle's first
+ * red half-sweep is computed into a second red buffer together with the red
+ * residuals of the new iterate; Phi as seen by every
+ * other call is the cycle's iterate.  Any call that changes Phi, f, the BCs
+ * or the operator discards the look-ahead (the next cycle recomputes it);
+ * MG_OFF_LOOKAHEAD turns it off. */
 int mg_vcycle(mg_ctx *ctx, double *res_norm_out);
 
 /* Asynchronous fixed-count solve, for pipelining independent problems:
