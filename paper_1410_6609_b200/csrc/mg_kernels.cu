@@ -408,8 +408,10 @@ void launch_first_empty(const unsigned long long *counts, int n, double *host_ds
 }
 
 // ---------------------------------------------------------------------------
-// Coarsest-grid CG: one CTA, Hestenes-Stiefel from x = 0, stop at
-// ||r|| <= tol ||b|| or maxit.  Vectors in natural order, in shared memory
+// Coarsest-grid CG: one CTA, from x = 0, stop at ||r|| <= tol
+// ||b|| or maxit.  Up to kCgSmemMax unknowns and eight per thread: the
+// register-resident Chronopoulos-Gear form below (cg_cta_cg); otherwise this
+// Hestenes-Stiefel loop.  Vectors in natural order, in shared memory
 // when they fit (else in `scratch`, L1/L2-resident); the operator is the same
 // closed form as the smoother.  Dot products: per-thread partials in a fixed
 // order, warp shuffle tree, then every thread sums the warp partials in
@@ -462,7 +464,7 @@ __host__ __device__ inline size_t cg_area_doubles(long long N) {
 // shared memory.  The neighbour values are loaded unconditionally from a
 // valid index and selected (no branches in the matrix-vector product).
 template <bool PER>
-__device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*part)[32],
+__device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*part)[64],
                                        double tol, int maxit, int *iters_out,
                                        int nthr) {
   using NB = typename std::conditional<PER, unsigned short, unsigned char>::type;
@@ -565,38 +567,76 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
-// doubles of the register-resident CG's shared area: r and two p buffers,
-// each with a zero slot at index N
-__host__ __device__ inline size_t cg_reg_doubles(long long N) { return 3 * (size_t)(N + 1); }
+// sums over the block of two per-thread values at once; one barrier; every
+// thread gets both.  part: 64 doubles.  Up to 16 warps the warp partials are
+// read by lanes l and l + 16 alike, so four butterfly levels give every lane
+// the same bits; up to 32 warps, five levels.
+__device__ __forceinline__ double2 cg_allsum2(double v0, double v1, double *part) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
+    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    part[w] = v0;
+    part[32 + w] = v1;
+  }
+  __syncthreads();
+  const int nw = (blockDim.x + 31) >> 5;
+  if (nw <= 16) {
+    const int l = lane & 15;
+    double s0 = l < nw ? part[l] : 0.0, s1 = l < nw ? part[32 + l] : 0.0;
+#pragma unroll
+    for (int o = 8; o > 0; o >>= 1) {
+      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+    }
+    return make_double2(s0, s1);
+  }
+  double s0 = lane < nw ? part[lane] : 0.0, s1 = lane < nw ? part[32 + lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+  }
+  return make_double2(s0, s1);
+}
 
-// The same iteration as cg_cta with every per-element quantity the thread
-// owns in registers: element n = threadIdx.x + e * nthr (e < E, the strided
-// order of cg_cta, so the per-thread partial sums and the tree -- hence every
-// bit of the iterates -- are cg_cta's), x and the own r, p_old in registers,
-// the six neighbour offsets computed once (a neighbour outside the level
-// points at a zero slot whose r and p stay 0: r[k] + beta * 0 = +0, the value
-// cg_cta selects).  Shared memory holds what neighbours read: r and the two
-// p buffers.  Requires N <= E * nthr.
+// doubles of the register-resident CG's shared area: r with a zero slot at
+// N, then x
+__host__ __device__ inline size_t cg_reg_doubles(long long N) { return 2 * (size_t)N + 1; }
+
+// CG on grid g by the calling CTA, N <= E * nthr unknowns held in registers
+// (element n = threadIdx.x + e * nthr): the Chronopoulos-Gear arrangement of
+// the conjugate-gradient recurrences (reading c8): w = A r, gamma = (r, r)
+// and delta = (w, r) summed in ONE reduction, then
+//     beta = gamma / gamma_old,  alpha = gamma / (delta - beta gamma / alpha_old),
+//     p = r + beta p,  s = w + beta s (= A p),  x += alpha p,  r -= alpha s,
+// the same iterates as Hestenes-Stiefel in exact arithmetic (the stopping
+// test on the recursively updated r, ||r|| <= tol ||b||, and the iteration
+// count as cg_cta).  Shared memory holds r for the neighbours (the six
+// neighbour offsets are computed once; outside the level they point at a
+// zero slot) and x (updated off the dependency chain: registers for eight
+// elements per thread would spill).  One reduction and one plain barrier per iteration instead of
+// two reductions, six neighbour loads instead of twelve.
 template <bool PER, int E>
-__device__ __forceinline__ void cg_cta_reg(const Grid &g, double *sm, double (*part)[32],
-                                           double tol, int maxit, int *iters_out,
-                                           int nthr) {
+__device__ __forceinline__ void cg_cta_cg(const Grid &g, double *sm, double (*part)[64],
+                                          double tol, int maxit, int *iters_out,
+                                          int nthr) {
   const int N = g.nx * g.ny * g.nz;
-  double *rs = sm, *pA = sm + (N + 1), *pB = sm + 2 * (N + 1);
+  double *rs = sm, *xs = sm + N + 1;
   const int sx = g.ny * g.nz, sy = g.nz;
   const int wx = (g.nx - 1) * sx, wy = (g.ny - 1) * sy, wz = g.nz - 1;
   unsigned nb[E][3];  // six 16-bit offsets (N <= kCgSmemMax < 65536)
-  double x[E], r[E], po[E], dd[E];
+  double r[E], p[E], sv[E], w[E];
+  unsigned long long dpk = 0;  // the centre integers d (<= 12), 4 bits each
   bool act[E];
-  double acc = 0.0;
 #pragma unroll
   for (int e = 0; e < E; e++) {
     const int n = (int)threadIdx.x + e * nthr;
     act[e] = (int)threadIdx.x < nthr && n < N;
-    x[e] = 0.0;
-    po[e] = 0.0;
-    r[e] = 0.0;
-    dd[e] = 0.0;
+    r[e] = p[e] = sv[e] = w[e] = 0.0;
 #pragma unroll
     for (int a = 0; a < 3; a++) nb[e][a] = (unsigned)N * 0x10001u;
     if (act[e]) {
@@ -613,70 +653,76 @@ __device__ __forceinline__ void cg_cta_reg(const Grid &g, double *sm, double (*p
 #pragma unroll
       for (int a = 0; a < 3; a++)
         nb[e][a] = (unsigned)k6[2 * a] | ((unsigned)k6[2 * a + 1] << 16);
-      dd[e] = (double)centre_d(g, i, j, z);
+      dpk |= (unsigned long long)centre_d(g, i, j, z) << (4 * e);
       int col;
       const long long idx = split_index(g, i, j, z, &col);
       const double b = col ? g.fB[idx] : g.fR[idx];
       r[e] = b;
       rs[n] = b;
-      pA[n] = 0.0;  // p_old of the first iteration: p = r + 0 * 0 = r
-      acc = acc + b * b;
+      xs[n] = 0.0;
     }
   }
-  if (threadIdx.x == 0) {
-    rs[N] = 0.0;
-    pA[N] = 0.0;
-    pB[N] = 0.0;
-  }
-  int pb = 0;
-  double rho = cg_allsum(acc, part[pb]);  // barrier also publishes r, p_old
-  pb ^= 1;
-  const double bnorm = sqrt(rho);
+  if (threadIdx.x == 0) rs[N] = 0.0;
   const double c = g.c;
-  double beta = 0.0;
-  double *pso = pA, *psn = pB;  // p of the last iteration / of this one
+  int pb = 0;
+  // w = A r from the published r; partial sums of (r, r) and (w, r)
+  auto matvec = [&](double &gg, double &dl) {
+    gg = 0.0;
+    dl = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      auto v = [&](int a) {
+        return rs[(int)((nb[e][a >> 1] >> (16 * (a & 1))) & 0xffffu)];
+      };
+      const double s = ((((v(0) + v(1)) + v(2)) + v(3)) + v(4)) + v(5);
+      const double d = (double)(int)((dpk >> (4 * e)) & 15u);
+      w[e] = c * (d * r[e] - s);
+      if (act[e]) {
+        gg = gg + r[e] * r[e];
+        dl = dl + w[e] * r[e];
+      }
+    }
+  };
+  __syncthreads();  // r published
+  double gg, dl;
+  matvec(gg, dl);
+  double2 gd = cg_allsum2(gg, dl, part[pb]);
+  pb ^= 1;
+  double gamma = gd.x;
+  const double bnorm = sqrt(gamma);
   int it = 0;
   if (bnorm > 0.0) {
+    double alpha = gamma / gd.y;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      p[e] = r[e];
+      sv[e] = w[e];
+    }
     while (it < maxit) {
-      double p[E], q[E];
-      acc = 0.0;
 #pragma unroll
       for (int e = 0; e < E; e++) {
-        auto v = [&](int a) {
-          const int k = (int)((nb[e][a >> 1] >> (16 * (a & 1))) & 0xffffu);
-          return rs[k] + beta * pso[k];
-        };
-        const double s = ((((v(0) + v(1)) + v(2)) + v(3)) + v(4)) + v(5);
-        p[e] = r[e] + beta * po[e];
-        q[e] = c * (dd[e] * p[e] - s);
+        r[e] = r[e] - alpha * sv[e];
         if (act[e]) {
-          psn[(int)threadIdx.x + e * nthr] = p[e];
-          acc = acc + p[e] * q[e];
+          const int n = (int)threadIdx.x + e * nthr;
+          rs[n] = r[e];
+          xs[n] = xs[n] + alpha * p[e];
         }
       }
-      const double pq = cg_allsum(acc, part[pb]);
-      pb ^= 1;
-      const double a = rho / pq;
-      acc = 0.0;
-#pragma unroll
-      for (int e = 0; e < E; e++) {
-        if (act[e]) {
-          x[e] = x[e] + a * p[e];
-          r[e] = r[e] - a * q[e];
-          rs[(int)threadIdx.x + e * nthr] = r[e];
-          acc = acc + r[e] * r[e];
-        }
-        po[e] = p[e];
-      }
-      const double rho1 = cg_allsum(acc, part[pb]);
-      pb ^= 1;
+      __syncthreads();  // r published (the reads of the last product are done:
+                        // they precede the reduction's barrier)
       it++;
-      if (sqrt(rho1) <= tol * bnorm) break;
-      beta = rho1 / rho;
-      rho = rho1;
-      double *t = pso;
-      pso = psn;
-      psn = t;
+      matvec(gg, dl);
+      gd = cg_allsum2(gg, dl, part[pb]);
+      pb ^= 1;
+      if (sqrt(gd.x) <= tol * bnorm) break;
+      const double beta = gd.x / gamma;
+      alpha = gd.x / (gd.y - beta * (gd.x / alpha));
+      gamma = gd.x;
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        p[e] = r[e] + beta * p[e];
+        sv[e] = w[e] + beta * sv[e];
+      }
     }
   }
 #pragma unroll
@@ -687,25 +733,27 @@ __device__ __forceinline__ void cg_cta_reg(const Grid &g, double *sm, double (*p
     const int t = n / g.nz;
     int col;
     const long long idx = split_index(g, t / g.ny, t % g.ny, z, &col);
-    (col ? g.phiB : g.phiR)[idx] = x[e];
+    (col ? g.phiB : g.phiR)[idx] = xs[n];
   }
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
-// the register-resident CG for the elements per thread N needs (<= 4), else
-// false (the caller runs cg_cta)
-template <bool PER, int MAXE = 4>
-__device__ __forceinline__ bool cg_cta_fast(const Grid &g, double *sm, double (*part)[32],
+// the register-resident CG for the elements per thread N needs (<= MAXE,
+// at most 8), else false (the caller runs cg_cta)
+template <bool PER, int MAXE = 8>
+__device__ __forceinline__ bool cg_cta_fast(const Grid &g, double *sm, double (*part)[64],
                                             double tol, int maxit, int *iters_out,
                                             int nthr) {
   const int N = g.nx * g.ny * g.nz;
   const int E = (N + nthr - 1) / nthr;
   if (E <= 1)
-    cg_cta_reg<PER, 1>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 1>(g, sm, part, tol, maxit, iters_out, nthr);
   else if (E <= 2)
-    cg_cta_reg<PER, 2>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 2>(g, sm, part, tol, maxit, iters_out, nthr);
   else if (MAXE >= 4 && E <= 4)
-    cg_cta_reg<PER, 4>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 4>(g, sm, part, tol, maxit, iters_out, nthr);
+  else if (MAXE >= 8 && E <= 8)
+    cg_cta_cg<PER, 8>(g, sm, part, tol, maxit, iters_out, nthr);
   else
     return false;
   return true;
@@ -715,7 +763,7 @@ template <bool PER>
 __global__ void __launch_bounds__(kCgThreads)
     k_coarse_cg(Grid g, double *scr, double tol, int maxit, int *iters_out) {
   extern __shared__ double cg_sm[];
-  __shared__ double part[2][32];
+  __shared__ double part[2][64];
   const long long N = (long long)g.nx * g.ny * g.nz;
   if (N <= kCgSmemMax) {
     if (!cg_cta_fast<PER>(g, cg_sm, part, tol, maxit, iters_out, (int)blockDim.x))
@@ -729,6 +777,10 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
   return cg_area_doubles((long long)g.nx * g.ny * g.nz);
 }
 
+// (round 2, Chronopoulos-Gear, scripts/cg_probe.py: unknowns per thread
+// capped at 2 / 4 / 8 / 16 instead -- i.e. fewer threads -- are slower or no
+// faster on 8^3, 32 x 8 x 8, 64 x 8 x 8; one z-row per thread with its z
+// neighbours in registers is slower too: 68 vs 57 us on 8^3)
 // 256 threads below 2048 unknowns, 512 from there (more warps hide the smem
 // latency of the per-thread loops: 64 x 8 x 8, config 4's coarsest at P = 8,
 // 476 vs 557 us in round 1; 1024 threads are slower again)
@@ -736,7 +788,8 @@ size_t coarse_cg_scratch_doubles(const Grid &g) {
 // 512/1024 no faster -- the iteration is bound by its dependency chain; a
 // separate p = r + beta p pass with a third barrier is slower on 8^3 and
 // faster on 32 x 8 x 8, 3.275 vs 3.268 ms per config-3 cycle)
-static int cg_threads(long long N) {
+static int cg_threads(const Grid &g) {
+  const long long N = (long long)g.nx * g.ny * g.nz;
   int threads = (int)((N + 31) / 32 * 32);
   const int cap = N >= 2048 ? 512 : 256;
   return threads > cap ? cap : threads;
@@ -746,7 +799,7 @@ template <bool PER>
 static void launch_cg(const Grid &g, double *scratch, double tol, int maxit,
                       int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
-  const int threads = cg_threads(N);
+  const int threads = cg_threads(g);
   size_t smem = 0;
   if (N <= kCgSmemMax) {
     smem = cg_area_doubles(N) * sizeof(double);
@@ -1363,7 +1416,7 @@ __global__ void __launch_bounds__(kTailThreads)
     k_vcycle_tail(TailLevels T, int nu1, int nu2, double alpha, double tol, int maxit,
                   int cg_nthr, double *cg_scr, int *iters_out) {
   extern __shared__ double tail_sm[];
-  __shared__ double part[2][32];
+  __shared__ double part[2][64];
   cgr::cluster_group cl = cgr::this_cluster();
   const long long t0 = (long long)cl.block_rank() * blockDim.x + threadIdx.x;
   const long long nt = (long long)cl.num_blocks() * blockDim.x;
@@ -1401,9 +1454,10 @@ __global__ void __launch_bounds__(kTailThreads)
   if (cl.block_rank() == 0) {
     const long long N = (long long)gc.nx * gc.ny * gc.nz;
     if (N <= kCgSmemMax) {
-      // (at most two elements per thread here: the tail kernel's other
-      // steps leave no registers for four)
-      if (!cg_cta_fast<PER, 2>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr))
+      // (at most four elements per thread here -- eight would spill --:
+      // vcycle_tail_supported keeps larger coarsest grids out of the tail,
+      // so that the tail and the standalone CG run the same arithmetic)
+      if (!cg_cta_fast<PER, 4>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr))
         cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
     } else
       cg_cta<PER>(gc, cg_scr, part, tol, maxit, iters_out, cg_nthr);
@@ -1457,7 +1511,10 @@ int tail_cluster_ctas() {
 
 bool vcycle_tail_supported(const Grid &coarsest) {
   const long long N = (long long)coarsest.nx * coarsest.ny * coarsest.nz;
-  return tail_cluster_ctas() > 0 && N <= kCgSmemMax && coarsest.nxl == coarsest.nx;
+  const int thr = cg_threads(coarsest);
+  return tail_cluster_ctas() > 0 && N <= kCgSmemMax && thr <= kTailThreads &&
+         (N + thr - 1) / thr <= 4 &&
+         coarsest.nxl == coarsest.nx;
 }
 
 template <bool PER>
@@ -1486,7 +1543,7 @@ static int launch_tail(const TailLevels &T, int nu1, int nu2, double alpha, doub
   cfg.attrs = at;
   cfg.numAttrs = 1;
   return cudaLaunchKernelEx(&cfg, k_vcycle_tail<PER>, T, nu1, nu2, alpha, tol, maxit,
-                            cg_threads(N), cg_scr, iters_out) == cudaSuccess
+                            cg_threads(gc), cg_scr, iters_out) == cudaSuccess
              ? 0
              : -1;
 }
