@@ -375,9 +375,15 @@ int mg_get_solution_async(mg_ctx *ctx, double *out, int where);
 int mg_wait(mg_ctx *ctx, double *res_norm_out);
 
 /* r0 = norm of the current Phi; V-cycles while r_k > tol*r0 (Alg.1,
- * P:547-550).  *cycles_out and res_hist[0..cycles] (len max_cycles+1) may be
+ * P:547-550), at most mg_opts.max_cycles.  *cycles_out and
+ * res_hist[0..cycles] (the caller's array of max_cycles+1 doubles) may be
  * NULL.  MG_OK, MG_ERR_NOTCONV at max_cycles, or MG_ERR_DIVERGED. */
 int mg_solve(mg_ctx *ctx, double tol, int *cycles_out, double *res_hist);
+/* mg_solve with an explicit cycle limit: max_cycles > 0 replaces
+ * mg_opts.max_cycles for this call (res_hist: max_cycles+1 doubles); <= 0
+ * uses mg_opts.max_cycles. */
+int mg_solve_n(mg_ctx *ctx, double tol, int max_cycles, int *cycles_out,
+               double *res_hist);
 
 /* ||f - A Phi||_2 for the current Phi on the finest level, unscaled (Alg.1
  * "residual"; reading c10), summed in a fixed order (per-CTA partials,

@@ -389,7 +389,13 @@ constexpr int kMaxMarks = 512;
 void mark(mg_ctx *c, int cat) {
   if (!c->prof || c->nev >= kMaxMarks) return;
   // external record: a real event node when the stream is being captured
-  cudaEventRecordWithFlags(c->ev[c->nev], c->stream, cudaEventRecordExternal);
+  // (outside a capture -- eager cycles, single steps -- a plain record)
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(c->stream, &cs);
+  if (cs == cudaStreamCaptureStatusActive)
+    cudaEventRecordWithFlags(c->ev[c->nev], c->stream, cudaEventRecordExternal);
+  else
+    cudaEventRecord(c->ev[c->nev], c->stream);
   c->mark_cat[c->nev] = cat;
   c->nev++;
 }
@@ -1162,6 +1168,15 @@ void free_mask(mg_ctx *c) {
   c->masked = false;
 }
 
+// the look-ahead view of level 0 = the committed view with the other red
+// buffer (after any change of the level-0 grid's coefficient fields)
+void sync_alt_view(mg_ctx *c) {
+  if (!c->red0_alt) return;
+  double *alt = c->g0alt.phiR;
+  c->g0alt = c->g[0][0];
+  c->g0alt.phiR = alt;
+}
+
 int residual_norm_now(mg_ctx *c, double *out) {
   int rc = enqueue_norm(c);
   if (rc) return rc;
@@ -1871,9 +1886,10 @@ int mg_residual_norm(mg_ctx *c, double *out) {
   return residual_norm_now(c, out);
 }
 
-int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
+int mg_solve_n(mg_ctx *c, double tol, int max_cycles, int *cycles_out, double *hist) {
   Nvtx nv("mg_solve");
   if (!c) return fail(MG_ERR_ARG, "null ctx");
+  const int kmax = max_cycles > 0 ? max_cycles : c->o.max_cycles;
   double r0;
   int rc = residual_norm_now(c, &r0);
   if (rc) return rc;
@@ -1881,7 +1897,7 @@ int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
   c->prev_norm = r0;
   int k = 0;
   int status = r0 == 0.0 ? MG_OK : MG_ERR_NOTCONV;
-  while (status == MG_ERR_NOTCONV && k < c->o.max_cycles) {
+  while (status == MG_ERR_NOTCONV && k < kmax) {
     double rk;
     rc = mg_vcycle(c, &rk);
     k++;
@@ -1896,6 +1912,10 @@ int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
   if (status == MG_ERR_NOTCONV)
     fail(MG_ERR_NOTCONV, "not converged after %d cycles", k);
   return status;
+}
+
+int mg_solve(mg_ctx *c, double tol, int *cycles_out, double *hist) {
+  return mg_solve_n(c, tol, 0, cycles_out, hist);
 }
 
 int mg_get_solution(mg_ctx *c, double *out, int where) {
@@ -1977,7 +1997,13 @@ namespace {
 // the face-cell BCs: level-0 float records (mask + patch types), Galerkin
 // coarse records level by level, and byte codes on every level whose records
 // all have kappa in {0,1} and position-derived delta.
+int rebuild_coefficients_(mg_ctx *c);
 int rebuild_coefficients(mg_ctx *c) {
+  const int rc = rebuild_coefficients_(c);
+  sync_alt_view(c);
+  return rc;
+}
+int rebuild_coefficients_(mg_ctx *c) {
   CK(cudaStreamSynchronize(c->stream));
   drop_graphs(c);
   free_mask(c);

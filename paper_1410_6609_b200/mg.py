@@ -121,6 +121,7 @@ def lib():
         L.mg_wait.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_get_solution_async.argtypes = [P, dp, i]
         L.mg_solve.argtypes = [P, d, ip, dp]
+        L.mg_solve_n.argtypes = [P, d, i, ip, dp]
         L.mg_residual_norm.argtypes = [P, ctypes.POINTER(ctypes.c_double)]
         L.mg_get_solution.argtypes = [P, dp, i]
         L.mg_set_solution.argtypes = [P, dp, i]
@@ -495,10 +496,13 @@ class Multigrid:
         return r.value
 
     def solve(self, tol: float, max_cycles: int = 100, raise_notconv=False):
+        max_cycles = int(max_cycles)
+        if max_cycles < 1:
+            raise MGError(MG_ERR_ARG, "max_cycles must be >= 1")
         hist = np.zeros(max_cycles + 1, np.float64)
         cyc = ctypes.c_int()
-        rc = lib().mg_solve(self._ctx, float(tol), ctypes.byref(cyc),
-                            _host_ptr(hist))
+        rc = lib().mg_solve_n(self._ctx, float(tol), max_cycles, ctypes.byref(cyc),
+                              _host_ptr(hist))
         if rc != MG_OK and (rc != MG_ERR_NOTCONV or raise_notconv):
             _check(rc, self._ctx)
         return rc, cyc.value, hist[:cyc.value + 1].copy()

@@ -181,3 +181,73 @@ def test_timestep_single_cycle_plain(mg):
     same(a, b)
     a.close()
     b.close()
+
+
+hyp = pytest.importorskip("hypothesis")
+from hypothesis import HealthCheck, given, settings, strategies as st  # noqa: E402
+
+OPS = ["vcycle", "vcycle", "vcycle", "set_rhs", "set_solution", "zero", "smooth0",
+       "smooth1", "residual_norm", "get_solution", "solve", "profiling", "mask_bc",
+       "solve_async"]
+
+
+@settings(max_examples=12, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(st.sampled_from(sorted(CASES)), st.lists(st.sampled_from(OPS), min_size=4, max_size=14),
+       st.integers(0, 2 ** 16))
+def test_lookahead_random_call_sequences(mg, case, ops, seed):
+    """Random sequences of API calls on a look-ahead context and a plain one
+    (MG_OFF_LOOKAHEAD): after every call Phi is bitwise equal and the
+    returned norms agree to 1e-13."""
+    shape, bt, bv, h = CASES[case]
+    rng = np.random.default_rng(seed)
+    a, b = pair(mg, case)
+    f = rng.uniform(-1, 1, shape)
+    for s in (a, b):
+        s.set_rhs(f)
+    prof = False
+    for op in ops:
+        if op == "vcycle":
+            ra, rb = a.vcycle(), b.vcycle()
+            assert abs(ra - rb) <= 1e-13 * rb
+        elif op == "set_rhs":
+            f = rng.uniform(-1, 1, shape)
+            a.set_rhs(f)
+            b.set_rhs(f)
+        elif op == "set_solution":
+            x = rng.uniform(-1, 1, shape)
+            a.set_solution(x)
+            b.set_solution(x)
+        elif op == "zero":
+            a.zero_solution()
+            b.zero_solution()
+        elif op in ("smooth0", "smooth1"):
+            a.smooth_half(0, int(op[-1]))
+            b.smooth_half(0, int(op[-1]))
+        elif op == "residual_norm":
+            assert a.residual_norm() == b.residual_norm()
+        elif op == "get_solution":
+            pass
+        elif op == "solve":
+            ra, rb = a.solve(1e-5, 6), b.solve(1e-5, 6)
+            assert ra[1] == rb[1]
+        elif op == "profiling":
+            prof = not prof
+            a.set_profiling(prof)
+            b.set_profiling(prof)
+        elif op == "mask_bc":
+            # new boundary values on one face (f changes by the BC adaptation)
+            if bt[1] != P:
+                v = rng.uniform(-1, 1, (shape[1], shape[2]))
+                a.set_face_values(1, v)
+                b.set_face_values(1, v)
+        elif op == "solve_async":
+            outs = [np.empty(shape), np.empty(shape)]
+            a.solve_async(f, outs[0], 2)
+            b.solve_async(f, outs[1], 2)
+            a.wait()
+            b.wait()
+            assert np.array_equal(outs[0], outs[1])
+        same(a, b)
+    a.close()
+    b.close()
