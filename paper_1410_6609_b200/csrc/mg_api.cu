@@ -268,13 +268,14 @@ struct mg_ctx {
   size_t fbuf_cap = 0;         // (doubles), grown on demand, kept
   unsigned long long *counts = nullptr;
   cudaGraphExec_t graph = nullptr;
-  // look-ahead red sweep: a second level-0 red buffer; g[0][0] /
-  // tm[0][0] view the committed iterate, g0alt / tm0alt the other buffer,
-  // which holds the next cycle's first red half-sweep when la_valid.  One
-  // graph per orientation (red0: which buffer g[0][0] views).
-  double *red0_alt = nullptr;
-  Grid g0alt{};
-  TmPair tm0alt;
+  // look-ahead red sweep: a second level-0 red buffer per slab;
+  // g[0] / tm[0] (and the level-0 overlap views) view the committed iterate,
+  // g0alt / tm0alt (vlo0alt, ...) the other buffers, which hold the next
+  // cycle's first red half-sweep when la_valid.  One graph per orientation
+  // (red0: which buffers g[0] views).
+  std::vector<double *> red0_alt;
+  std::vector<Grid> g0alt, vlo0alt, vhi0alt, vin0alt;
+  std::vector<TmPair> tm0alt, tmin0alt;
   int red0 = 0;
   bool la_valid = false;
   cudaGraphExec_t graph_la[2] = {nullptr, nullptr};
@@ -308,11 +309,11 @@ struct Carver {
   }
 };
 
-// contexts that get the look-ahead red sweep's second buffer: one level-0
-// slab, a pre-smoothing red sweep to look ahead to, the true cycle-end norm
+// contexts that get the look-ahead red sweep's second buffers: a
+// pre-smoothing red sweep to look ahead to, the true cycle-end norm
 bool lookahead_capable(const mg_ctx *c) {
-  return c->P == 1 && c->pl.L >= 2 && c->o.nu1 >= 1 && c->o.nu2 >= 1 &&
-         !c->o.fused_norm && !(c->o.disable & MG_OFF_LOOKAHEAD);
+  return c->pl.L >= 2 && c->o.nu1 >= 1 && c->o.nu2 >= 1 && !c->o.fused_norm &&
+         !(c->o.disable & MG_OFF_LOOKAHEAD);
 }
 
 size_t carve(mg_ctx *c, char *base) {
@@ -338,9 +339,11 @@ size_t carve(mg_ctx *c, char *base) {
       c->g[l].push_back(gr);
     }
   }
-  // look-ahead red sweep: a second red array for level 0 (one slab only)
+  // look-ahead red sweep: a second red array per level-0 slab
+  c->red0_alt.clear();
   if (lookahead_capable(c))
-    c->red0_alt = (double *)cv.take((size_t)mg::grid_elems(c->g[0][0]) * sizeof(double));
+    for (const Grid &g : c->g[0])
+      c->red0_alt.push_back((double *)cv.take((size_t)mg::grid_elems(g) * sizeof(double)));
   // one region of norm partials per level-0 slab: residual-kernel partials
   // plus (split norm) the smoother's, or the grid-stride kernels' (fewer)
   size_t npart = 0;
@@ -848,8 +851,11 @@ int split_norm_tail(mg_ctx *c) {
 // skips that sweep.  Anything that changes Phi, f or the operator on level
 // 0 drops the look-ahead (la_drop); the next cycle then runs it first.
 bool lookahead_ok(const mg_ctx *c) {
-  return c->red0_alt && c->nslab == 1 && !c->masked && split_norm_ok(c) &&
-         c->tm0alt.ok && c->tm0alt.ok_resid;
+  if (c->red0_alt.empty() || c->masked || !split_norm_ok(c)) return false;
+  for (const TmPair &t : c->tm0alt)
+    if (!(t.ok && t.ok_resid)) return false;
+  // the overlapped half-sweeps need the other buffers' interior views too
+  return !overlap_level(c, 0) || c->vin0alt.size() == c->g[0].size();
 }
 
 void la_drop(mg_ctx *c) { c->la_valid = false; }
@@ -866,37 +872,66 @@ void drop_graphs(mg_ctx *c) {
 
 // committed view <-> look-ahead view
 void la_swap(mg_ctx *c) {
-  std::swap(c->g[0][0], c->g0alt);
-  std::swap(c->tm[0][0], c->tm0alt);
+  std::swap(c->g[0], c->g0alt);
+  std::swap(c->tm[0], c->tm0alt);
+  if (!c->vin0alt.empty()) {
+    std::swap(c->vlo[0], c->vlo0alt);
+    std::swap(c->vhi[0], c->vhi0alt);
+    std::swap(c->vin[0], c->vin0alt);
+    std::swap(c->tmin[0], c->tmin0alt);
+  }
   c->red0 ^= 1;
 }
 
-// the look-ahead sweep of the committed iterate (eager: before the first
-// look-ahead cycle after a change); its residual partials are not used
-int la_prologue(mg_ctx *c) {
-  mg::launch_smooth_lookahead_march(c->g0alt, c->tm[0][0].b, c->g[0][0].phiR,
-                                    c->partials + c->pbase[0], c->stream);
+// the look-ahead sweeps of every level-0 slab, from the committed red
+// values into the other buffers, with their red residual partials (cnt[s]
+// of slab s at partials + pbase[s] + off[s]); then the red ghost exchange
+// of the other buffers (the next cycle's black sweep reads them)
+int lookahead_sweeps(mg_ctx *c, int *cnt) {
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    cnt[s] += mg::launch_smooth_lookahead_march(c->g0alt[s], c->tm[0][s].b,
+                                                c->g[0][s].phiR,
+                                                c->partials + c->pbase[s] + cnt[s],
+                                                c->stream);
+    c->launches++;
+  }
   CK(cudaGetLastError());
+  la_swap(c);
+  const int rc = halo(c, 0, 0);
+  la_swap(c);
+  return rc;
+}
+
+// the look-ahead of the committed iterate (eager: before the first
+// look-ahead cycle after a change); its residual partials are not used.
+// The black ghosts are exchanged first (the committed iterate may come
+// from mg_set_solution or a single step).
+int la_prologue(mg_ctx *c) {
+  int rc;
+  if ((rc = halo(c, 0, 1))) return rc;
+  int cnt[kMaxSlabs] = {0};
+  if ((rc = lookahead_sweeps(c, cnt))) return rc;
   c->la_valid = true;
   return MG_OK;
 }
 
 // the end of a look-ahead cycle, after the last red post-smoothing
-// half-sweep: black sweep + black residual partials, the look-ahead red
-// sweep into the other buffer + red residual partials, the ordered sum
+// half-sweep: black sweep + black residual partials on every slab, the black
+// ghost exchange, the look-ahead red sweeps into the other buffers + red
+// residual partials, their ghost exchange, the ordered sums
 int lookahead_tail(mg_ctx *c) {
   mark(c, CAT_NONE);
   int cnt[kMaxSlabs] = {0};
-  cnt[0] = mg::launch_smooth_norm_march(c->g[0][0], c->tm[0][0].r, 1,
-                                        c->partials + c->pbase[0], c->stream);
-  c->launches++;
+  for (size_t s = 0; s < c->g[0].size(); s++) {
+    cnt[s] = mg::launch_smooth_norm_march(c->g[0][s], c->tm[0][s].r, 1,
+                                          c->partials + c->pbase[s], c->stream);
+    c->launches++;
+  }
+  CK(cudaGetLastError());
+  int rc;
+  if ((rc = halo(c, 0, 1))) return rc;
   mark(c, CAT_SMOOTH0);
-  CK(cudaGetLastError());
-  cnt[0] += mg::launch_smooth_lookahead_march(c->g0alt, c->tm[0][0].b, c->g[0][0].phiR,
-                                              c->partials + c->pbase[0] + cnt[0],
-                                              c->stream);
-  c->launches++;
-  CK(cudaGetLastError());
+  if ((rc = lookahead_sweeps(c, cnt))) return rc;
   c->paths |= MG_PATH_SPLIT_NORM | MG_PATH_LOOKAHEAD;
   return finish_norm(c, cnt);
 }
@@ -1171,10 +1206,11 @@ void free_mask(mg_ctx *c) {
 // the look-ahead view of level 0 = the committed view with the other red
 // buffer (after any change of the level-0 grid's coefficient fields)
 void sync_alt_view(mg_ctx *c) {
-  if (!c->red0_alt) return;
-  double *alt = c->g0alt.phiR;
-  c->g0alt = c->g[0][0];
-  c->g0alt.phiR = alt;
+  for (size_t s = 0; s < c->g0alt.size(); s++) {
+    double *alt = c->g0alt[s].phiR;
+    c->g0alt[s] = c->g[0][s];
+    c->g0alt[s].phiR = alt;
+  }
 }
 
 int residual_norm_now(mg_ctx *c, double *out) {
@@ -1427,14 +1463,15 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
                    mg::make_tmap_resid(g, g.phiB, t.rb);
     }
   }
-  if (c->red0_alt) {
-    c->g0alt = c->g[0][0];
-    c->g0alt.phiR = c->red0_alt;
-    const TmPair &t0 = c->tm[0][0];
-    TmPair &t = c->tm0alt;
-    t = t0;  // the Phi^B maps are shared
-    t.ok = t0.ok && mg::make_tmap_field(c->g0alt, c->red0_alt, t.r);
-    t.ok_resid = t0.ok_resid && mg::make_tmap_resid(c->g0alt, c->red0_alt, t.rr);
+  for (size_t s = 0; s < c->red0_alt.size(); s++) {
+    Grid ga = c->g[0][s];
+    ga.phiR = c->red0_alt[s];
+    c->g0alt.push_back(ga);
+    const TmPair &t0 = c->tm[0][s];
+    TmPair t = t0;  // the Phi^B maps are shared
+    t.ok = t0.ok && mg::make_tmap_field(ga, ga.phiR, t.r);
+    t.ok_resid = t0.ok_resid && mg::make_tmap_resid(ga, ga.phiR, t.rr);
+    c->tm0alt.push_back(t);
   }
   // multi-slab overlap: views of the boundary / interior planes of every
   // distributed level (slabs of >= 4 planes), a communication stream
@@ -1455,6 +1492,20 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
         TmPair &t = c->tmin[l][s];
         t.ok = mg::march_supported(vi) && mg::make_tmap_field(vi, vi.phiR, t.r) &&
                mg::make_tmap_field(vi, vi.phiB, t.b);
+      }
+    }
+    // the same views of the look-ahead buffers (level 0)
+    if (!c->g0alt.empty() && !c->vin[0].empty()) {
+      for (size_t s = 0; s < c->g0alt.size(); s++) {
+        const Grid &g = c->g0alt[s];
+        c->vlo0alt.push_back(plane_view(g, 0, 1));
+        c->vhi0alt.push_back(plane_view(g, g.nxl - 1, 1));
+        const Grid vi = plane_view(g, 1, g.nxl - 2);
+        c->vin0alt.push_back(vi);
+        TmPair t;
+        t.ok = mg::march_supported(vi) && mg::make_tmap_field(vi, vi.phiR, t.r) &&
+               mg::make_tmap_field(vi, vi.phiB, t.b);
+        c->tmin0alt.push_back(t);
       }
     }
     e = cudaStreamCreateWithFlags(&c->s_comm, cudaStreamNonBlocking);

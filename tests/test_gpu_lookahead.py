@@ -80,6 +80,49 @@ def test_lookahead_equals_plain_and_oracle(mg, case):
     b.close()
 
 
+@pytest.mark.parametrize("halo", ["loopback", "emulate"])
+@pytest.mark.parametrize("nranks", [2, 4])
+@pytest.mark.parametrize("case", ["box", "periodic"])
+@pytest.mark.parametrize("overlap", [True, False])
+def test_lookahead_slabs(mg, halo, nranks, case, overlap):
+    """x-slabs (the NCCL data layout on one GPU for EMULATE): the look-ahead
+    sweeps of every slab, the black ghost exchange before them and the red
+    ghost exchange of the other buffers after them -- bitwise equal to the
+    plain cycle, the norm to 1e-13, and to the oracle (history clause)."""
+    shape, bt, bv, h = CASES[case]
+    if shape[0] % (2 * nranks):
+        pytest.skip("slabs of an odd plane count")
+    kw = dict(nranks=nranks, halo=halo, agglomerate_below=4096,
+              disable=0 if overlap else mg.MG_OFF_OVERLAP)
+    a = mg.Multigrid(shape, h, bt, bv, min_coarse=4, **kw)
+    kw["disable"] |= mg.MG_OFF_LOOKAHEAD
+    b = mg.Multigrid(shape, h, bt, bv, min_coarse=4, **kw)
+    f = np.random.default_rng(11).uniform(-1, 1, shape)
+    o = oracle.Oracle(shape, h, bt, bv, min_coarse=4)
+    for s in (a, b):
+        s.set_rhs(f)
+    o.set_rhs(f)
+    ho = [o.residual_norm()]
+    for k in range(3):
+        ra, rb = a.vcycle(), b.vcycle()
+        ho.append(o.vcycle())
+        same(a, b)
+        assert abs(ra - rb) <= 1e-13 * rb
+        assert abs(ra - ho[-1]) <= 1e-8 * ho[-1] + 1e-15 * ho[0]
+    assert a.cycle_paths & mg.MG_PATH_LOOKAHEAD
+    assert bool(a.cycle_paths & mg.MG_PATH_OVERLAP) == overlap
+    # a new iterate between cycles drops the look-ahead (the prologue runs
+    # the exchanges itself)
+    x = np.random.default_rng(12).uniform(-1, 1, shape)
+    for s in (a, b):
+        s.set_solution(x)
+    for _ in range(2):
+        ra, rb = a.vcycle(), b.vcycle()
+        same(a, b)
+    a.close()
+    b.close()
+
+
 def test_lookahead_interleaved_api_calls(mg):
     shape = CASES["box"][0]
     rng = np.random.default_rng(9)
