@@ -214,6 +214,13 @@ def timestep_regime(mg, W, stream, local, steps=10, warm=2):
         torch.cuda.synchronize()
         for i, key in enumerate(parts):
             parts[key].append(ev[i].elapsed_time(ev[i + 1]))
+    # the step's residual reduction: ||r|| after the cycle over ||r|| of the
+    # warm start against the moved spheres' f
+    rel = []
+    for k in range(warm + 4, warm + 7):
+        s.set_rhs_from_spheres(pos[k], w.radii, w.charges, subsample=2)
+        r0 = s.residual_norm()
+        rel.append(s.vcycle() / r0)
     s.close()
     cells = w.cells
     return {"metric": "MLUPS per time step (paper's MG metric, P:1303-1306)",
@@ -224,6 +231,10 @@ def timestep_regime(mg, W, stream, local, steps=10, warm=2):
                     % len(w.radii),
             "workload": "cfg4 box 512^3, channel BCs, 5% spheres, 7 levels",
             "residual_mean": float(np.mean(res)), "residual_max": float(np.max(res)),
+            "residual_over_r0_mean": float(np.mean(rel)),
+            "residual_note": "absolute ||f - A Phi|| after the step's cycle (the paper "
+                             "monitors 1.5e-8 absolute, P:1323-1324); over_r0: the same "
+                             "over the warm start's residual for the moved spheres",
             "breakdown_ms": {k: round(float(np.mean(v)), 3) for k, v in parts.items()},
             "paper_context": "91.8 MLUPS per SuperMUC node, 16 Sandy Bridge cores "
                              "(P:1346); context only"}

@@ -851,7 +851,8 @@ int split_norm_tail(mg_ctx *c) {
 // skips that sweep.  Anything that changes Phi, f or the operator on level
 // 0 drops the look-ahead (la_drop); the next cycle then runs it first.
 bool lookahead_ok(const mg_ctx *c) {
-  if (c->red0_alt.empty() || c->masked || !split_norm_ok(c)) return false;
+  // (masked levels: split_norm_ok requires the byte codes on every slab)
+  if (c->red0_alt.empty() || !split_norm_ok(c)) return false;
   for (const TmPair &t : c->tm0alt)
     if (!(t.ok && t.ok_resid)) return false;
   // the overlapped half-sweeps need the other buffers' interior views too

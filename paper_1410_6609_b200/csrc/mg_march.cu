@@ -346,6 +346,14 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
           nacc = nacc + r0 * r0;
           nacc = nacc + r1 * r1;
         }
+        if (NORM == 2 && MASK) {
+          // the look-ahead writes another buffer: a cell that is not an
+          // unknown (solid) keeps its value there too
+          if (!(cd0 & 64)) out.x = ov[c].x;
+          if (!(cd1 & 64)) out.y = ov[c].y;
+          cd0 = 64;
+          cd1 = k + 1 < g.nzh ? 64u : 0u;
+        }
         const bool both = k + 1 < g.nzh && (cd0 & 64) && (cd1 & 64);
         if (both) {
           *reinterpret_cast<double2 *>(orow + k) = out;
@@ -844,15 +852,16 @@ int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
 
 // the look-ahead red half-sweep (NORM 2): reads Phi^B (ring), f^R and the
 // current Phi^R (oldv), writes the swept Phi^R to g.phiR (another buffer)
-// and the red residual partials of the current iterate; box and periodic
-// grids (no mask)
+// and the red residual partials of the current iterate; box, periodic and
+// masked (byte-code) grids
 int launch_smooth_lookahead_march(const Grid &g, const void *tm_oth128,
                                   const double *oldv, double *partials,
                                   cudaStream_t s) {
-  if (variant(g) == VAR_PER)
-    launch_sm_n<false, VAR_PER, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv);
-  else
-    launch_sm_n<false, VAR_BOX, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv);
+  switch (variant(g)) {
+    case VAR_MASK: launch_sm_n<false, VAR_MASK, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv); break;
+    case VAR_PER: launch_sm_n<false, VAR_PER, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv); break;
+    default: launch_sm_n<false, VAR_BOX, 2>(g, g, tm_oth128, 0, 0.0, s, partials, oldv); break;
+  }
   return smooth_blocks(g);
 }
 

@@ -123,6 +123,51 @@ def test_lookahead_slabs(mg, halo, nranks, case, overlap):
     b.close()
 
 
+@pytest.mark.parametrize("kind", ["beam", "random"])
+def test_lookahead_masked(mg, kind):
+    """Solid masks (byte-code levels, config 5's setting): the look-ahead
+    sweep skips the solid cells' residuals and copies their values into the
+    other buffer, so Phi -- solid cells included, whatever set_solution put
+    there -- stays bitwise the plain cycle's; both against the oracle."""
+    shape = (64, 32, 128)
+    bt = [N, N, D, D, N, N]
+    bv = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+    if kind == "beam":
+        solid = W.beam_mask(shape)
+    else:
+        solid = (np.random.default_rng(3).uniform(size=shape) < 0.1).astype(np.uint8)
+    a = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=4, nu1=3, nu2=3)
+    b = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=4, nu1=3, nu2=3,
+                     disable=mg.MG_OFF_LOOKAHEAD)
+    o = oracle.Oracle(shape, 1.0, bt, bv, solid=solid, min_coarse=4, nu1=3, nu2=3)
+    rng = np.random.default_rng(4)
+    f = rng.uniform(-1, 1, shape)
+    for s in (a, b):
+        s.set_mask(solid)
+        s.set_rhs(f)
+    o.set_rhs(f)
+    ho = [o.residual_norm()]
+    for _ in range(3):
+        ra, rb = a.vcycle(), b.vcycle()
+        ho.append(o.vcycle())
+        same(a, b)
+        assert abs(ra - rb) <= 1e-13 * rb
+        assert abs(ra - ho[-1]) <= 1e-8 * ho[-1] + 1e-15 * ho[0]
+    assert a.cycle_paths & mg.MG_PATH_LOOKAHEAD
+    po = o.phi()
+    assert np.linalg.norm(a.get_solution() - po) <= 1e-10 * np.linalg.norm(po)
+    # nonzero values in solid cells survive the cycles on both paths alike
+    x = rng.uniform(-1, 1, shape)
+    for s in (a, b):
+        s.set_solution(x)
+    for _ in range(2):
+        a.vcycle()
+        b.vcycle()
+        same(a, b)
+    a.close()
+    b.close()
+
+
 def test_lookahead_interleaved_api_calls(mg):
     shape = CASES["box"][0]
     rng = np.random.default_rng(9)
