@@ -43,21 +43,21 @@ def main():
     D, N, P = mg.MG_DIRICHLET, mg.MG_NEUMANN, mg.MG_PERIODIC
     rng = np.random.default_rng(1)
     eps = np.where(rng.uniform(size=shape) < 0.3, 78.5, 1.0)
+    # (name, bt, bv, solid, eps, half-sweep, restriction, prolongation B/cell,
+    #  norm B/cell by path: look-ahead / split / full pass)
     cases = [
-        ("box (config 3 BCs)", [D] * 6, [0.0] * 6, None, None,
-         model_bytes(7, 12, 17, 17, 16)),
+        ("box (config 3 BCs)", [D] * 6, [0.0] * 6, None, None, 12, 17, 17, (4, 12, 16)),
         ("periodic channel: x, z periodic, y Dirichlet 0/1 (N3)",
-         [P, P, D, D, P, P], [0, 0, 0, 1, 0, 0], None, None,
-         model_bytes(7, 12, 17, 17, 16)),
+         [P, P, D, D, P, P], [0, 0, 0, 1, 0, 0], None, None, 12, 17, 17, (4, 12, 16)),
         ("solid beam mask, channel BCs (config-5 geometry)",
          [N, N, D, D, N, N], [0, 0, 0, 1, 0, 0], W.beam_mask(shape), None,
-         model_bytes(7, 12.5, 18, 17.5, 17)),
+         12.5, 18, 17.5, (4.5, 12.5, 17)),
         ("variable permittivity, 78.5:1 jumps, channel BCs (N4)",
-         [N, N, D, D, N, N], [0, 0, 0, 1, 0, 0], None, eps,
-         model_bytes(7, 12 + 32, 17 + 64, 17, 16 + 64)),
+         [N, N, D, D, N, N], [0, 0, 0, 1, 0, 0], None, eps, 12 + 32, 17 + 64, 17,
+         (4, 12 + 32, 16 + 64)),
     ]
     rows = []
-    for name, bt, bv, solid, ep, mb in cases:
+    for name, bt, bv, solid, ep, hs, rr, pr, norms in cases:
         stream = torch.cuda.Stream()
         s = mg.Multigrid(shape, 1.0, bt, bv, min_coarse=8, stream=stream)
         if solid is not None:
@@ -76,6 +76,10 @@ def main():
             torch.cuda.synchronize()
             times.append(e0.elapsed_time(e1))
         ms = float(np.median(times))
+        paths = s.cycle_paths
+        norm = norms[0] if paths & mg.MG_PATH_LOOKAHEAD else (
+            norms[1] if paths & mg.MG_PATH_SPLIT_NORM else norms[2])
+        mb = model_bytes(s.nlevels, hs, rr, pr, norm)
         frac = mb * n ** 3 / (ms * 1e-3) / 1e9 / peak
         fac = (res[-1] / res[0]) ** (1.0 / (len(res) - 1))
         rows.append((name, ms, n ** 3 / (ms * 1e-3) / 1e6, mb, frac, fac,
@@ -83,14 +87,16 @@ def main():
         s.close()
         del s
         torch.cuda.empty_cache()
-    md = ["# Solver variants on one B200, %d^3, V(2,2) (round 1)" % n, "",
+    md = ["# Solver variants on one B200, %d^3, V(2,2) (round 2)" % n, "",
           "Median CUDA-event time of `mg_vcycle` (graph launch + residual norm "
           "readback) over %d cycles after one warm-up; byte model = the "
           "variant's algorithmic bytes per fine cell and cycle (SURVEY 8(d) "
           "plus the operator data the variant must read: 0.5 B/cell of face "
           "codes per half-sweep for the mask, 64 B per cell of fp64 records "
           "for the permittivity in the smoother, residual and norm -- the "
-          "prolongation needs none without a mask); fraction at the measured peak %.1f GB/s." % (a.cycles, peak),
+          "prolongation needs none without a mask; the norm: 4 B/cell with the "
+          "look-ahead red sweep, else the split or full pass, as the recorded "
+          "cycle took it); fraction at the measured peak %.1f GB/s." % (a.cycles, peak),
           "",
           "| variant | ms/cycle | Mcells/s | model B/cell | model-roofline fraction | factor/cycle | launches |",
           "|---|---|---|---|---|---|---|"]
