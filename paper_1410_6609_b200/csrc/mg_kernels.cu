@@ -567,42 +567,6 @@ __device__ __forceinline__ void cg_cta(const Grid &g, double *base, double (*par
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
-// sums over the block of two per-thread values at once; one barrier; every
-// thread gets both.  part: 64 doubles.  Up to 16 warps the warp partials are
-// read by lanes l and l + 16 alike, so four butterfly levels give every lane
-// the same bits; up to 32 warps, five levels.
-__device__ __forceinline__ double2 cg_allsum2(double v0, double v1, double *part) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    v0 += __shfl_xor_sync(0xffffffffu, v0, o);
-    v1 += __shfl_xor_sync(0xffffffffu, v1, o);
-  }
-  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  if (lane == 0) {
-    part[w] = v0;
-    part[32 + w] = v1;
-  }
-  __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
-  if (nw <= 16) {
-    const int l = lane & 15;
-    double s0 = l < nw ? part[l] : 0.0, s1 = l < nw ? part[32 + l] : 0.0;
-#pragma unroll
-    for (int o = 8; o > 0; o >>= 1) {
-      s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-      s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-    }
-    return make_double2(s0, s1);
-  }
-  double s0 = lane < nw ? part[lane] : 0.0, s1 = lane < nw ? part[32 + lane] : 0.0;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_xor_sync(0xffffffffu, s0, o);
-    s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-  }
-  return make_double2(s0, s1);
-}
-
 // doubles of the register-resident CG's shared area: r with a zero slot at
 // N, then x
 __host__ __device__ inline size_t cg_reg_doubles(long long N) { return 2 * (size_t)N + 1; }

@@ -687,98 +687,134 @@ __global__ void __launch_bounds__(1024)
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
 
-// The same CG with everything in shared memory (coarsest levels up to
-// kCgVarSmem unknowns): per element the 6 kappa and D (doubles), neighbour
-// bits, and the four vectors; one CTA of 256 threads.  Identical arithmetic
-// to k_coarse_cg_var (neighbour order, products, the fixed reduction tree).
-static constexpr int kCgVarSmem = 2304;  // 11 doubles + 1 byte per unknown
+// coarsest levels up to kCgVarSmem unknowns: the register-resident kernel
+// below (9 doubles of shared memory per unknown: r, x, 6 kappa, D)
+static constexpr int kCgVarSmem = 2304;
 
+// The Chronopoulos-Gear form of the same CG (reading c8; k_coarse_cg's
+// cg_cta_cg): per unknown n = threadIdx.x + e * blockDim (e < E) r, p,
+// s = A p, w = A r in registers, the coefficients (6 kappa, D), r for the
+// neighbours (zero slot at N) and x in shared memory; one two-value
+// reduction and one barrier per iteration.  A solid cell (D = 0) has b = 0
+// and a zero row, so its r, p, x stay 0.
+template <int E>
 __global__ void __launch_bounds__(512)
-    k_coarse_cg_var_smem(Grid g, double tol, int maxit, int *iters_out) {
+    k_coarse_cg_var_cg(Grid g, double tol, int maxit, int *iters_out) {
   extern __shared__ double sm[];
-  __shared__ double part[2][32];
+  __shared__ double part[2][64];
   const int N = g.nx * g.ny * g.nz;
-  double *x = sm, *r = sm + N, *p = sm + 2 * N, *q = sm + 3 * N;
-  double *kap = sm + 4 * N;   // [6][N]
-  double *Dd = sm + 10 * N;   // [N]
-  unsigned char *nb = reinterpret_cast<unsigned char *>(sm + 11 * N);
+  double *rs = sm, *xs = sm + N + 1;
+  double *kap = sm + 2 * N + 1;  // [6][N]
+  double *Dd = kap + 6 * N;      // [N]
   const int sx = g.ny * g.nz, sy = g.nz;
-  int pb = 0;
-  double acc = 0.0;
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
-    const int z = n % g.nz;
-    const int t = n / g.nz;
-    const int j = t % g.ny, i = t / g.ny;
-    const int col = (i + j + z) & 1;
-    const long long e = rb(g, i, j) + (z >> 1);
-    Coef C;
-    coef_at(g, col, e, i, j, z, C);
-    for (int f = 0; f < 6; f++) kap[f * N + n] = C.k[f];
-    Dd[n] = C.D;
-    nb[n] = (unsigned char)((i > 0) | ((i < g.nx - 1) << 1) | ((j > 0) << 2) |
-                            ((j < g.ny - 1) << 3) | ((z > 0) << 4) |
-                            ((z < g.nz - 1) << 5));
-    const double b = (C.D == 0.0) ? 0.0 : (col ? g.fB[e] : g.fR[e]);
-    x[n] = 0.0;
-    r[n] = b;
-    p[n] = b;
-    acc = acc + b * b;
+  const int nthr = (int)blockDim.x;
+  unsigned nb[E][3];  // six 16-bit neighbour indices (N <= kCgVarSmem)
+  double r[E], p[E], sv[E], w[E];
+  bool act[E];
+#pragma unroll
+  for (int e = 0; e < E; e++) {
+    const int n = (int)threadIdx.x + e * nthr;
+    act[e] = n < N;
+    r[e] = p[e] = sv[e] = w[e] = 0.0;
+#pragma unroll
+    for (int a = 0; a < 3; a++) nb[e][a] = (unsigned)N * 0x10001u;
+    if (act[e]) {
+      const int z = n % g.nz;
+      const int t = n / g.nz;
+      const int j = t % g.ny, i = t / g.ny;
+      const int col = (i + j + z) & 1;
+      const long long el = rb(g, i, j) + (z >> 1);
+      Coef C;
+      coef_at(g, col, el, i, j, z, C);
+      for (int f = 0; f < 6; f++) kap[f * N + n] = C.k[f];
+      Dd[n] = C.D;
+      const int k6[6] = {i > 0 ? n - sx : N, i < g.nx - 1 ? n + sx : N,
+                         j > 0 ? n - sy : N, j < g.ny - 1 ? n + sy : N,
+                         z > 0 ? n - 1 : N,  z < g.nz - 1 ? n + 1 : N};
+#pragma unroll
+      for (int a = 0; a < 3; a++)
+        nb[e][a] = (unsigned)k6[2 * a] | ((unsigned)k6[2 * a + 1] << 16);
+      const double b = (C.D == 0.0) ? 0.0 : (col ? g.fB[el] : g.fR[el]);
+      r[e] = b;
+      rs[n] = b;
+      xs[n] = 0.0;
+    }
   }
-  double rho = cg_sum_v(acc, part[pb]);  // barrier also publishes the arrays
-  pb ^= 1;
-  const double bnorm = sqrt(rho);
+  if (threadIdx.x == 0) rs[N] = 0.0;
   const double c = g.c;
+  int pb = 0;
+  auto matvec = [&](double &gg, double &dl) {
+    gg = 0.0;
+    dl = 0.0;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      if (!act[e]) continue;
+      const int n = (int)threadIdx.x + e * nthr;
+      auto v = [&](int a) {
+        return rs[(int)((nb[e][a >> 1] >> (16 * (a & 1))) & 0xffffu)];
+      };
+      const double D = Dd[n];
+      double wn = 0.0;
+      if (D != 0.0) {
+        const double t = ((((kap[n] * v(0) + kap[N + n] * v(1)) + kap[2 * N + n] * v(2)) +
+                           kap[3 * N + n] * v(3)) +
+                          kap[4 * N + n] * v(4)) +
+                         kap[5 * N + n] * v(5);
+        wn = c * (D * r[e] - t);
+      }
+      w[e] = wn;
+      gg = gg + r[e] * r[e];
+      dl = dl + wn * r[e];
+    }
+  };
+  __syncthreads();  // r and the coefficients published
+  double gg, dl;
+  matvec(gg, dl);
+  double2 gd = cg_allsum2(gg, dl, part[pb]);
+  pb ^= 1;
+  double gamma = gd.x;
+  const double bnorm = sqrt(gamma);
   int it = 0;
   if (bnorm > 0.0) {
+    double alpha = gamma / gd.y;
+#pragma unroll
+    for (int e = 0; e < E; e++) {
+      p[e] = r[e];
+      sv[e] = w[e];
+    }
     while (it < maxit) {
-      acc = 0.0;
-      for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        double qn = 0.0;
-        const double pn = p[n];
-        if (Dd[n] != 0.0) {
-          const unsigned m = nb[n];
-          const double xm = (m & 1) ? p[n - sx] : 0.0;
-          const double xp = (m & 2) ? p[n + sx] : 0.0;
-          const double ym = (m & 4) ? p[n - sy] : 0.0;
-          const double yp = (m & 8) ? p[n + sy] : 0.0;
-          const double zm = (m & 16) ? p[n - 1] : 0.0;
-          const double zp = (m & 32) ? p[n + 1] : 0.0;
-          const double t = ((((kap[n] * xm + kap[N + n] * xp) + kap[2 * N + n] * ym) +
-                             kap[3 * N + n] * yp) +
-                            kap[4 * N + n] * zm) +
-                           kap[5 * N + n] * zp;
-          qn = c * (Dd[n] * pn - t);
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        r[e] = r[e] - alpha * sv[e];
+        if (act[e]) {
+          const int n = (int)threadIdx.x + e * nthr;
+          rs[n] = r[e];
+          xs[n] = xs[n] + alpha * p[e];
         }
-        q[n] = qn;
-        acc = acc + pn * qn;
       }
-      const double pq = cg_sum_v(acc, part[pb]);
-      pb ^= 1;
-      const double a = rho / pq;
-      acc = 0.0;
-      for (int n = threadIdx.x; n < N; n += blockDim.x) {
-        x[n] = x[n] + a * p[n];
-        const double rn = r[n] - a * q[n];
-        r[n] = rn;
-        acc = acc + rn * rn;
-      }
-      const double rho1 = cg_sum_v(acc, part[pb]);
-      pb ^= 1;
+      __syncthreads();  // r published
       it++;
-      if (sqrt(rho1) <= tol * bnorm) break;
-      const double beta = rho1 / rho;
-      for (int n = threadIdx.x; n < N; n += blockDim.x) p[n] = r[n] + beta * p[n];
-      __syncthreads();
-      rho = rho1;
+      matvec(gg, dl);
+      gd = cg_allsum2(gg, dl, part[pb]);
+      pb ^= 1;
+      if (sqrt(gd.x) <= tol * bnorm) break;
+      const double beta = gd.x / gamma;
+      alpha = gd.x / (gd.y - beta * (gd.x / alpha));
+      gamma = gd.x;
+#pragma unroll
+      for (int e = 0; e < E; e++) {
+        p[e] = r[e] + beta * p[e];
+        sv[e] = w[e] + beta * sv[e];
+      }
     }
   }
   __syncthreads();
-  for (int n = threadIdx.x; n < N; n += blockDim.x) {
+  for (int n = threadIdx.x; n < N; n += nthr) {
     const int z = n % g.nz;
     const int t = n / g.nz;
     const int j = t % g.ny, i = t / g.ny;
     const int col = (i + j + z) & 1;
-    (col ? g.phiB : g.phiR)[rb(g, i, j) + (z >> 1)] = x[n];
+    (col ? g.phiB : g.phiR)[rb(g, i, j) + (z >> 1)] = xs[n];
   }
   if (threadIdx.x == 0 && iters_out) *iters_out = it;
 }
@@ -787,17 +823,28 @@ void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
                           int *iters_out, cudaStream_t s) {
   const long long N = (long long)g.nx * g.ny * g.nz;
   if (N <= kCgVarSmem) {
-    const size_t smem = 11 * (size_t)N * sizeof(double) + (size_t)N;
+    // the Chronopoulos-Gear kernel: up to 8 unknowns per thread
+    int threads = (int)((N + 31) / 32 * 32);
+    const int cap = N >= 2048 ? 512 : 256;  // as k_coarse_cg
+    if (threads > cap) threads = cap;
+    const int E = (int)((N + threads - 1) / threads);
+    const size_t smem = (9 * (size_t)N + 1) * sizeof(double);
     static size_t configured = 48 * 1024;
     if (smem > configured) {
-      cudaFuncSetAttribute(k_coarse_cg_var_smem,
-                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_coarse_cg_var_cg<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_coarse_cg_var_cg<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_coarse_cg_var_cg<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(k_coarse_cg_var_cg<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       configured = smem;
     }
-    int threads = (int)((N + 31) / 32 * 32);
-    const int cap = N >= 2048 ? 512 : 256;  // as k_coarse_cg (more warps)
-    if (threads > cap) threads = cap;
-    k_coarse_cg_var_smem<<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
+    if (E <= 1)
+      k_coarse_cg_var_cg<1><<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
+    else if (E <= 2)
+      k_coarse_cg_var_cg<2><<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
+    else if (E <= 4)
+      k_coarse_cg_var_cg<4><<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
+    else
+      k_coarse_cg_var_cg<8><<<1, threads, smem, s>>>(g, tol, maxit, iters_out);
     return;
   }
   int threads = (int)((N + 31) / 32 * 32);
