@@ -148,9 +148,6 @@ typedef struct {
 #define MG_OFF_LOOKAHEAD 128 /* look-ahead red sweep (the cycle-end norm's red
                                 residuals from the next cycle's first red
                                 half-sweep) -> a red residual pass          */
-#define MG_OFF_FUSED_END 256 /* the last black + look-ahead red half-sweeps
-                                in one kernel (box level 0 held whole) ->
-                                two kernels                                 */
 
 /* mg_cycle_paths() bits: the paths the last recorded V-cycle took */
 #define MG_PATH_MARCH 1          /* level 0 smoothed by the marching kernel   */
@@ -163,7 +160,6 @@ typedef struct {
 #define MG_PATH_TAIL 128         /* coarse levels in the persistent tail      */
 #define MG_PATH_RED0 256         /* a restriction did the next red sweep      */
 #define MG_PATH_LOOKAHEAD 512    /* the cycle ended with the look-ahead sweep */
-#define MG_PATH_FUSED_END 1024   /* ... fused with the last black half-sweep  */
 
 typedef struct mg_ctx mg_ctx;
 

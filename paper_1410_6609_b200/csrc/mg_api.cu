@@ -192,8 +192,7 @@ struct TmPair {
   alignas(64) unsigned char b[128];
   alignas(64) unsigned char rr[128];  // z-tiled boxes (residual kernels)
   alignas(64) unsigned char rb[128];
-  alignas(64) unsigned char r12[128];  // red, (TY + 4)-row boxes (fused end)
-  bool ok = false, ok_resid = false, ok12 = false;
+  bool ok = false, ok_resid = false;
 };
 
 struct mg_ctx {
@@ -921,24 +920,9 @@ int la_prologue(mg_ctx *c) {
 // half-sweep: black sweep + black residual partials on every slab, the black
 // ghost exchange, the look-ahead red sweeps into the other buffers + red
 // residual partials, their ghost exchange, the ordered sums
-bool fused_end_ok(const mg_ctx *c) {
-  return !(c->o.disable & MG_OFF_FUSED_END) && c->g[0].size() == 1 && c->P == 1 &&
-         c->tm[0][0].ok12 && c->tm0alt[0].ok12 &&
-         mg::black_lookahead_supported(c->g[0][0]);
-}
-
 int lookahead_tail(mg_ctx *c) {
   mark(c, CAT_NONE);
   int cnt[kMaxSlabs] = {0};
-  if (fused_end_ok(c)) {
-    cnt[0] = mg::launch_black_lookahead(c->g[0][0], c->tm[0][0].r12, c->g0alt[0].phiR,
-                                        c->partials + c->pbase[0], c->stream);
-    c->launches++;
-    CK(cudaGetLastError());
-    mark(c, CAT_SMOOTH0);
-    c->paths |= MG_PATH_SPLIT_NORM | MG_PATH_LOOKAHEAD | MG_PATH_FUSED_END;
-    return finish_norm(c, cnt);
-  }
   for (size_t s = 0; s < c->g[0].size(); s++) {
     cnt[s] = mg::launch_smooth_norm_march(c->g[0][s], c->tm[0][s].r, 1,
                                           c->partials + c->pbase[s], c->stream);
@@ -1488,13 +1472,6 @@ mg_ctx *mg_create_ex(int nx, int ny, int nz, double h, const mg_bc *bc,
     TmPair t = t0;  // the Phi^B maps are shared
     t.ok = t0.ok && mg::make_tmap_field(ga, ga.phiR, t.r);
     t.ok_resid = t0.ok_resid && mg::make_tmap_resid(ga, ga.phiR, t.rr);
-    // the fused end of a look-ahead cycle (one slab held whole): 12-row red
-    // boxes of both red buffers
-    if (c->red0_alt.size() == 1 && c->P == 1) {
-      TmPair &tc = c->tm[0][s];
-      tc.ok12 = mg::make_tmap_red12(c->g[0][s], c->g[0][s].phiR, tc.r12);
-      t.ok12 = mg::make_tmap_red12(ga, ga.phiR, t.r12);
-    }
     c->tm0alt.push_back(t);
   }
   // multi-slab overlap: views of the boundary / interior planes of every

@@ -283,15 +283,6 @@ int launch_smooth_norm_march(const Grid &g, const void *tm_oth128, int color,
                              double *partials, cudaStream_t s);
 int launch_norm_red_march(const Grid &g, const void *tmR, const void *tmB,
                           double *partials, cudaStream_t s);
-// the last black half-sweep and the look-ahead red half-sweep of a box
-// level-0 slab held whole, fused (mg_fuse.cu): black in place with its
-// residual partials, the look-ahead red into red_out with the red residual
-// partials of the iterate (one partial per CTA, returns their count).
-// tm_red12: the current red array with (TY + 4)-row boxes (make_tmap_red12)
-bool black_lookahead_supported(const Grid &g);
-bool make_tmap_red12(const Grid &g, const double *base, void *out128);
-int launch_black_lookahead(const Grid &g, const void *tm_red12, double *red_out,
-                           double *partials, cudaStream_t s);
 // the look-ahead red half-sweep: the next cycle's first red half-sweep
 // written to g.phiR (a second buffer) from the current Phi^R in oldv, with the
 // current iterate's red residual partials; returns their count

@@ -47,7 +47,6 @@ MG_PATH_MARCH, MG_PATH_OVERLAP, MG_PATH_SPLIT_NORM, MG_PATH_CG_CLUSTER = 1, 2, 4
 MG_PATH_CG_VAR, MG_PATH_PROLONG_FUSED, MG_PATH_FUSED_NORM, MG_PATH_TAIL = 16, 32, 64, 128
 MG_PATH_RED0 = 256
 MG_OFF_LOOKAHEAD, MG_PATH_LOOKAHEAD = 128, 512
-MG_OFF_FUSED_END, MG_PATH_FUSED_END = 256, 1024
 
 _HALO = {"none": MG_HALO_NONE, "nccl": MG_HALO_NCCL, "loopback": MG_HALO_LOOPBACK,
          "emulate": MG_HALO_EMULATE}
