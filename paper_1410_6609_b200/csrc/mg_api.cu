@@ -268,6 +268,7 @@ struct mg_ctx {
   size_t fbuf_cap = 0;         // (doubles), grown on demand, kept
   unsigned long long *counts = nullptr;
   cudaGraphExec_t graph = nullptr;
+  bool in_cycle = false;  // enqueue_vcycle is recording (vs a single step)
   // look-ahead red sweep: a second level-0 red buffer per slab;
   // g[0] / tm[0] (and the level-0 overlap views) view the committed iterate,
   // g0alt / tm0alt (vlo0alt, ...) the other buffers, which hold the next
@@ -687,7 +688,12 @@ int prolong_level(mg_ctx *c, int l) {
   periodic_fill(c, l);
   if (l == 0) mark(c, CAT_PROLONG0);
   CK(cudaGetLastError());
-  return halo(c, l, 1);  // the next red half-sweep reads black ghosts
+  // both colours' ghosts: the next red half-sweep reads the black ones, and
+  // without post-smoothing (nu2 = 0, or a single step) the norm or the next
+  // step reads the red ones too
+  int rc = halo(c, l, 1);
+  if (!rc && (c->o.nu2 == 0 || !c->in_cycle)) rc = halo(c, l, 0);
+  return rc;
 }
 
 // can level l use the fused prolongation + first post-smoothing red sweep?
@@ -983,7 +989,14 @@ int level_cat(const mg_ctx *c, int l) {
 // la: a look-ahead cycle (lookahead_ok): level 0's first red half-sweep was
 // done by the previous cycle (or la_prologue), the cycle ends with
 // lookahead_tail
+int enqueue_vcycle_(mg_ctx *c, bool la);
 int enqueue_vcycle(mg_ctx *c, bool la = false) {
+  c->in_cycle = true;
+  const int rc = enqueue_vcycle_(c, la);
+  c->in_cycle = false;
+  return rc;
+}
+int enqueue_vcycle_(mg_ctx *c, bool la) {
   const int L = c->pl.L;
   int rc;
   c->launches = 0;

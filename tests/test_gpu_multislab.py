@@ -160,3 +160,26 @@ def test_emulate_equals_loopback(mg, P, kind):
     assert np.array_equal(out[0][1], out[1][1])
     assert np.array_equal(out[0][2], out[1][2])
     assert out[0][0] == out[1][0]
+
+
+@pytest.mark.parametrize("halo", BACKENDS)
+@pytest.mark.parametrize("nu", [(1, 0), (2, 0), (0, 1)])
+def test_no_post_or_pre_smoothing_on_slabs(mg, halo, nu):
+    """V(nu1, 0) on slabs: with no post-smoothing after the prolongation, the
+    cycle-end norm reads the corrected red ghost planes -- the prolongation
+    exchanges both colours (a case the deep randomised run found: (8, 4, 64),
+    z periodic, V(1,0), 2 slabs); V(0, 1) for symmetry."""
+    shape = (16, 8, 128)
+    bt, bv = [0, 0, 0, 0, 2, 2], [0.0] * 6
+    nu1, nu2 = nu
+    kw = dict(min_coarse=2, nu1=nu1, nu2=nu2)
+    f = np.random.default_rng(0).uniform(-1, 1, shape)
+    o = oracle.Oracle(shape, 1.0, bt, bv, **kw)
+    o.set_rhs(f)
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
+    s = mg.Multigrid(shape, 1.0, bt, bv, nranks=2, halo=halo, agglomerate_below=512, **kw)
+    s.set_rhs(f)
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
+    check_history(hg, ho)
+    assert rel(s.get_solution(), o.phi()) <= 1e-10
+    s.close()
