@@ -279,7 +279,7 @@ OPS = ["vcycle", "vcycle", "vcycle", "set_rhs", "set_solution", "zero", "smooth0
        "solve_async"]
 
 
-@settings(max_examples=12, deadline=None, derandomize=True,
+@settings(max_examples=30, deadline=None, derandomize=True,
           suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 @given(st.sampled_from(sorted(CASES)), st.lists(st.sampled_from(OPS), min_size=4, max_size=14),
        st.integers(0, 2 ** 16))

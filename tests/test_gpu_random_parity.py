@@ -55,7 +55,7 @@ def problems(draw):
     return tuple(dims), bt, bv, h, nu1, nu2, mc, slabs, seed
 
 
-@settings(max_examples=80, deadline=None, derandomize=True,
+@settings(max_examples=200, deadline=None, derandomize=True,
           suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
 @given(problems())
 def test_random_problems_match_oracle(mg, prob):
