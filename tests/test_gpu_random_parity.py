@@ -98,3 +98,62 @@ def test_random_problems_match_oracle(mg, prob):
             assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob, hg, ho)
         assert err <= 1e-10, (prob, err)
     s.close()
+
+
+@st.composite
+def path_problems(draw):
+    """A problem of `problems` plus the path switches: a random subset of the
+    MG_OFF_* bits, the multi-slab backend and slab count (up to 4), the fused
+    termination norm (reading c11) and eager (graph-less) cycles."""
+    shape, bt, bv, h, nu1, nu2, mc, _, seed = draw(problems())
+    slabs = draw(st.sampled_from([1, 2, 4]))
+    if shape[0] % (2 * slabs) or shape[0] // slabs < 4:
+        slabs = 1
+    halo = draw(st.sampled_from(["loopback", "emulate"]))
+    disable = 0
+    for bit in (1, 2, 4, 8, 16, 32, 64, 128):
+        if draw(st.integers(0, 3)) == 0:
+            disable |= bit
+    fused = draw(st.integers(0, 5)) == 0
+    graph = draw(st.integers(0, 4)) != 0
+    return shape, bt, bv, h, nu1, nu2, mc, slabs, seed, halo, disable, fused, graph
+
+
+@settings(max_examples=100, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(path_problems())
+def test_random_paths_match_oracle(mg, prob):
+    """Random problems under random path switches: three cycles against the
+    oracle (the history clause, Phi <= 1e-10; single-level hierarchies under
+    the CG contract) -- every combination of the fast paths must agree with
+    the paper's arithmetic."""
+    shape, bt, bv, h, nu1, nu2, mc, slabs, seed, halo, disable, fused, graph = prob
+    kw = dict(min_coarse=mc, nu1=nu1, nu2=nu2)
+    try:
+        o = oracle.Oracle(shape, h, bt, bv, fused_norm=fused, **kw)
+    except ValueError:
+        return
+    extra = dict(nranks=slabs, halo=halo, agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, h, bt, bv, disable=disable, fused_norm=fused,
+                         use_graph=graph, **kw, **extra)
+    except mg.MGError:
+        assert slabs > 1
+        return
+    f = np.random.default_rng(seed).uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
+    po = o.phi()
+    err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
+    if s.nlevels == 1:
+        assert all(x <= 1e-11 * ho[0] for x in ho[1:]), (prob, ho)
+        tol = max(4e-12 * ho[0], 2.0 * max(ho[1:]))
+        assert all(x <= tol for x in hg[1:]), (prob, hg, ho)
+        assert err <= 1e-8, (prob, err)
+    else:
+        for a, b in zip(hg, ho):
+            assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob, hg, ho)
+        assert err <= 1e-10, (prob, err)
+    s.close()
