@@ -157,3 +157,71 @@ def test_random_paths_match_oracle(mg, prob):
             assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob, hg, ho)
         assert err <= 1e-10, (prob, err)
     s.close()
+
+
+@st.composite
+def sphere_problems(draw):
+    """Random spheres on random grids: 1-24 spheres of radius 0.6-6 cells
+    (centres anywhere in the domain, periodic images across periodic faces,
+    overlaps and spheres cut by the walls included), subsampling 1-3, both
+    normalisations, 1, 2 or 4 slabs."""
+    dims = [2 * draw(st.integers(4, 20)) for _ in range(3)]
+    bt = []
+    for a in range(3):
+        bt += draw(st.sampled_from([[D, D], [D, N], [N, N], [P, P]]))
+    if D not in bt:
+        bt[2], bt[3] = D, D
+    bv = [0.0 if t == P else draw(st.floats(-1, 1)) for t in bt]
+    h = 2.0 ** draw(st.integers(-3, 1))
+    L = np.array(dims, float) * h
+    n = draw(st.integers(1, 24))
+    rmax = 0.5 * (float(min(dims)) - 2.0) * h  # 2R + 2h <= n h on periodic axes
+    radii = [min(draw(st.floats(0.6, 6.0)) * h, rmax) for _ in range(n)]
+    centers = [[draw(st.floats(0.0, 0.999)) * L[a] for a in range(3)] for _ in range(n)]
+    charges = [draw(st.floats(-2.0, 2.0)) for _ in range(n)]
+    sub = draw(st.integers(1, 3))
+    norm = draw(st.integers(0, 1))
+    slabs = draw(st.sampled_from([1, 2, 4]))
+    if dims[0] % (2 * slabs) or dims[0] // slabs < 4:
+        slabs = 1
+    return (tuple(dims), bt, bv, h, np.array(centers), np.array(radii), np.array(charges),
+            sub, norm, slabs)
+
+
+@settings(max_examples=60, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(sphere_problems())
+def test_random_spheres_match_oracle(mg, prob):
+    """Row a2 (RHS from spheres) and N2 (Eq.14-15 forces) on random
+    geometry: f bitwise equal to the oracle's (the per-sphere counts,
+    subsampling, images and ordered overlaps), then one V-cycle and the forces
+    on the same Phi to 1e-12 of the largest force."""
+    shape, bt, bv, h, c, R, q, sub, norm, slabs = prob
+    try:
+        o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    except ValueError:
+        return
+    extra = dict(nranks=slabs, halo="loopback", agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, h, bt, bv, min_coarse=2, **extra)
+    except mg.MGError:
+        assert slabs > 1
+        return
+    try:
+        o.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+    except ValueError:  # a sphere covering no cell centre (per-cells normalisation)
+        with pytest.raises(mg.MGError):
+            s.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+        s.close()
+        return
+    s.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0)), prob
+    s.vcycle()
+    o.vcycle()
+    phi = s.get_solution()
+    o.set_phi(phi)
+    fg = s.coulomb_forces(c, R, q, normalization=norm, subsample=sub)
+    fo = o.coulomb_forces(c, R, q, normalization=norm, subsample=sub)
+    scale = max(np.abs(fo).max(), 1e-300)
+    assert np.abs(fg - fo).max() <= 1e-12 * scale, prob
+    s.close()
