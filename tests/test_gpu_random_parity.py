@@ -225,3 +225,72 @@ def test_random_spheres_match_oracle(mg, prob):
     scale = max(np.abs(fo).max(), 1e-300)
     assert np.abs(fg - fo).max() <= 1e-12 * scale, prob
     s.close()
+
+
+@st.composite
+def masked_problems(draw):
+    """Channel problems (Dirichlet 0 / 1 on the y faces, Neumann on x and z)
+    with 1-2 random solid boxes strictly inside in y, neither spanning both
+    the x and the z extent, so every fluid region touches a Dirichlet face
+    (config 5's setting, d5)."""
+    dims = [8 * draw(st.integers(1, 6)), 8 * draw(st.integers(1, 4)),
+            8 * draw(st.integers(1, 18))]  # multiples of 8: several levels
+    solid = np.zeros(dims, np.uint8)
+    for _ in range(draw(st.integers(1, 2))):
+        lo, hi = [], []
+        for a in range(3):
+            n = dims[a]
+            a0 = draw(st.integers(1 if a == 1 else 0, n - 2))
+            a1 = draw(st.integers(a0 + 1, n - 1 if a == 1 else n))
+            lo.append(a0)
+            hi.append(a1)
+        if lo[0] == 0 and hi[0] == dims[0] and lo[2] == 0 and hi[2] == dims[2]:
+            hi[2] -= 1
+        solid[lo[0]:hi[0], lo[1]:hi[1], lo[2]:hi[2]] = 1
+    nu1 = draw(st.integers(1, 3))
+    nu2 = draw(st.integers(1, 3))
+    mc = draw(st.sampled_from([2, 4]))
+    slabs = draw(st.sampled_from([1, 1, 2]))
+    if dims[0] % (2 * slabs) or dims[0] // slabs < 4:
+        slabs = 1
+    disable = draw(st.sampled_from([0, 0, 1, 16, 128]))
+    seed = draw(st.integers(0, 2 ** 16))
+    return tuple(dims), solid, nu1, nu2, mc, slabs, disable, seed
+
+
+@settings(max_examples=40, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(masked_problems())
+def test_random_masked_match_oracle(mg, prob):
+    """Random solid masks: the masked Galerkin hierarchy, the mask kernels
+    (byte codes or float records), the variable-coefficient CG and the
+    masked look-ahead -- three cycles against the oracle."""
+    shape, solid, nu1, nu2, mc, slabs, disable, seed = prob
+    bt = [N, N, D, D, N, N]
+    bv = [0.0, 0.0, 0.0, 1.0, 0.0, 0.0]
+    kw = dict(min_coarse=mc, nu1=nu1, nu2=nu2)
+    try:
+        o = oracle.Oracle(shape, 1.0, bt, bv, solid=solid, **kw)
+    except ValueError:
+        return
+    extra = dict(nranks=slabs, halo="loopback", agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, 1.0, bt, bv, disable=disable, **kw, **extra)
+    except mg.MGError:
+        assert slabs > 1
+        return
+    s.set_mask(solid)
+    f = np.random.default_rng(seed).uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
+    po = o.phi()
+    err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
+    if s.nlevels == 1:
+        assert err <= 1e-8, (prob[0], err)
+    else:
+        for a, b in zip(hg, ho):
+            assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob[0], hg, ho)
+        assert err <= 1e-10, (prob[0], err)
+    s.close()
