@@ -294,3 +294,95 @@ def test_random_masked_match_oracle(mg, prob):
             assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob[0], hg, ho)
         assert err <= 1e-10, (prob[0], err)
     s.close()
+
+
+@st.composite
+def coefficient_problems(draw):
+    """Boundary patches (Dirichlet or Neumann rectangles), per-cell face
+    values and variable permittivity on random grids (no periodic face; face
+    2 (y-) stays Dirichlet over at least one cell row so the operator is
+    SPD)."""
+    dims = [8 * draw(st.integers(1, 6)), 8 * draw(st.integers(1, 4)),
+            8 * draw(st.integers(1, 18))]
+    bt = [draw(st.sampled_from([D, N])) for _ in range(6)]
+    bt[2] = D
+    bv = [draw(st.floats(-1, 1)) for _ in range(6)]
+    ext = dims
+    patches = []
+    for _ in range(draw(st.integers(0, 3))):
+        q = draw(st.integers(0, 5))
+        ax = q // 2
+        na = ext[1] if ax == 0 else ext[0]
+        nb = ext[1] if ax == 2 else ext[2]
+        a0 = draw(st.integers(0, na - 1))
+        a1 = draw(st.integers(a0 + 1, na))
+        b0 = draw(st.integers(0, nb - 1))
+        b1 = draw(st.integers(b0 + 1, nb))
+        t = D if q == 2 else draw(st.sampled_from([D, N]))
+        if q == 2 and (a0, a1, b0, b1) == (0, na, 0, nb):
+            t = D
+        patches.append((q, a0, a1, b0, b1, t, draw(st.floats(-1, 1))))
+    faces = []
+    for _ in range(draw(st.integers(0, 2))):
+        q = draw(st.integers(0, 5))
+        ax = q // 2
+        na = ext[1] if ax == 0 else ext[0]
+        nb = ext[1] if ax == 2 else ext[2]
+        faces.append((q, (na, nb)))
+    eps_kind = draw(st.sampled_from(["none", "none", "jump", "lognormal"]))
+    nu1 = draw(st.integers(1, 3))
+    nu2 = draw(st.integers(1, 3))
+    mc = draw(st.sampled_from([2, 4]))
+    slabs = draw(st.sampled_from([1, 1, 2]))
+    if dims[0] % (2 * slabs) or dims[0] // slabs < 4:
+        slabs = 1
+    seed = draw(st.integers(0, 2 ** 16))
+    return tuple(dims), bt, bv, patches, faces, eps_kind, nu1, nu2, mc, slabs, seed
+
+
+@settings(max_examples=40, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(coefficient_problems())
+def test_random_coefficients_match_oracle(mg, prob):
+    """Random boundary patches, face values and permittivity (N1's
+    mg_set_bc_patch / mg_set_face_values, N4's mg_set_permittivity): the
+    variable-coefficient records, their Galerkin hierarchy, the BC adaptation
+    of the RHS and the variable-coefficient CG -- three cycles against the
+    oracle."""
+    shape, bt, bv, patches, faces, eps_kind, nu1, nu2, mc, slabs, seed = prob
+    rng = np.random.default_rng(seed)
+    kw = dict(min_coarse=mc, nu1=nu1, nu2=nu2)
+    o = oracle.Oracle(shape, 1.0, bt, bv, **kw)
+    extra = dict(nranks=slabs, halo="loopback", agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, 1.0, bt, bv, **kw, **extra)
+    except mg.MGError:
+        assert slabs > 1
+        return
+    for p in patches:
+        o.set_bc_patch(*p)
+        s.set_bc_patch(*p)
+    for q, (na, nb) in faces:
+        v = rng.uniform(-1, 1, (na, nb))
+        o.set_face_values(q, v)
+        s.set_face_values(q, v)
+    if eps_kind != "none":
+        eps = (np.where(rng.uniform(size=shape) < 0.3, 78.5, 1.0) if eps_kind == "jump"
+               else np.exp(rng.normal(0.0, 1.0, shape)))
+        o.set_permittivity(eps)
+        s.set_permittivity(eps)
+    f = rng.uniform(-1, 1, shape)
+    s.set_rhs(f)
+    o.set_rhs(f)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    hg = [s.residual_norm()] + [s.vcycle() for _ in range(3)]
+    ho = [o.residual_norm()] + [o.vcycle() for _ in range(3)]
+    po = o.phi()
+    err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
+    if s.nlevels == 1:
+        assert err <= 1e-8, (prob[:6], err)
+    else:
+        for a, b in zip(hg, ho):
+            assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob[:6], hg, ho)
+        assert err <= 1e-10, (prob[:6], err)
+    s.close()
