@@ -779,9 +779,9 @@ int enqueue_norm(mg_ctx *c) {
 // sum in rank order -- the same roundings in every backend.
 int finish_norm(mg_ctx *c, const int *cnt) {
   if (c->P == 1) {
-    mg::launch_sum_ordered(c->partials + c->pbase[0], cnt[0], c->normv, c->stream);
-    mg::launch_publish(c->normv, c->normv + 1, c->h_norm_dev, c->stream);
-    c->launches += 2;
+    mg::launch_sum_publish(c->partials + c->pbase[0], cnt[0], c->normv, c->normv + 1,
+                           c->h_norm_dev, c->stream);
+    c->launches++;
   } else {
     for (size_t s = 0; s < c->g[0].size(); s++) {
       mg::launch_sum_ordered(c->partials + c->pbase[s], cnt[s],

@@ -212,6 +212,8 @@ int launch_norm_partials(const Grid &g, double *partials, cudaStream_t s);
 // out[0] = sum of parts[0..n) in a fixed order
 void launch_sum_ordered(const double *parts, int n, double *out,
                         cudaStream_t s);
+void launch_sum_publish(const double *parts, int n, double *out, double *dev_dst,
+                        double *host_dst, cudaStream_t s);
 // dev_dst[0] = host_dst[0] = src[0] (host_dst: device view of mapped pinned
 // host memory)
 // coarsest CG on a thread-block cluster (mg_cg_cluster.cu): grids held

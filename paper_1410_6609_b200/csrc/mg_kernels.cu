@@ -371,6 +371,28 @@ void launch_sum_ordered(const double *parts, int n, double *out,
   k_sum_ordered<<<1, kThreads, 0, s>>>(parts, n, out);
 }
 
+// k_sum_ordered and k_publish in one launch (one slab): out[0] = dev_dst[0]
+// = host_dst[0] = the ordered sum
+__global__ void __launch_bounds__(kThreads)
+    k_sum_publish(const double *parts, int n, double *out, double *dev_dst,
+                  double *host_dst) {
+  __shared__ double sh[32];
+  double acc = 0.0;
+  for (int t = threadIdx.x; t < n; t += blockDim.x) acc = acc + parts[t];
+  const double v = block_sum(acc, sh);
+  if (threadIdx.x == 0) {
+    out[0] = v;
+    dev_dst[0] = v;
+    host_dst[0] = v;
+    __threadfence_system();
+  }
+}
+
+void launch_sum_publish(const double *parts, int n, double *out, double *dev_dst,
+                        double *host_dst, cudaStream_t s) {
+  k_sum_publish<<<1, kThreads, 0, s>>>(parts, n, out, dev_dst, host_dst);
+}
+
 // dev_dst[0] = host_dst[0] = src[0]; host_dst is mapped pinned memory, so
 // the value reaches the host without a copy-engine transfer (which would
 // queue behind bulk copies on the same engine)
