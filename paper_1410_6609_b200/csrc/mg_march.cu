@@ -284,10 +284,6 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
       const int i = g.x0 + il;
       const int p = (i + j + color) & 1;
       double *orow = own + (long long)(il + 1) * g.plane + (long long)(j + 1) * pz;
-      // the centre's x / y face terms are the row's: only z adds per cell
-      // (the same integer as centre_dm; the reciprocal indexed by it)
-      const int dxy = 6 + (i == 0 ? g.dface[0] : 0) + (i == g.nx - 1 ? g.dface[1] : 0) +
-                      (j == 0 ? g.dface[2] : 0) + (j == g.ny - 1 ? g.dface[3] : 0);
 #pragma unroll
       for (int c = 0; c < NCH; c++) {
         const int k = 2 * lane + 64 * c;
@@ -310,7 +306,7 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
           zp1 = z_hi<PER>(g, cur, k);
         }
         const int z0 = 2 * k + p;
-        double s0, s1, d0, d1, rd0, rd1;
+        double s0, s1, d0, d1;
         unsigned cd0 = 64, cd1 = 64;
         if (MASK && !__all_sync(__activemask(), cr[c] == kOpenPair)) {
           const unsigned cc2 = cr[c];
@@ -320,8 +316,6 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
           s1 = ksum(cd1, a.y, b.y, ym.y, yp.y, zm1, zp1);
           d0 = kdiag(g, cd0, i, j, z0);
           d1 = kdiag(g, cd1, i, j, z0 + 2);
-          rd0 = c_rcp16[(int)d0];
-          rd1 = c_rcp16[(int)d1];
         } else if (MASK) {
           // the whole warp on fluid cells with all six faces open (the bulk
           // of a masked level): kappa = 1 everywhere and no domain face, so
@@ -330,25 +324,19 @@ __global__ void __launch_bounds__(kThreadsM, NCH <= 2 ? 3 : 2)
           s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
           s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
           d0 = d1 = 6.0;
-          rd0 = rd1 = c_rcp16[6];
         } else {
           s0 = ((((a.x + b.x) + ym.x) + yp.x) + zm0) + zp0;
           s1 = ((((a.y + b.y) + ym.y) + yp.y) + zm1) + zp1;
-          // (z0 + 2 >= 2: never the z = 0 face)
-          const int di0 = dxy + (z0 == 0 ? g.dface[4] : 0) + (z0 == g.nz - 1 ? g.dface[5] : 0);
-          const int di1 = dxy + (z0 + 2 == g.nz - 1 ? g.dface[5] : 0);
-          d0 = (double)di0;
-          d1 = (double)di1;
-          rd0 = c_rcp16[di0];
-          rd1 = c_rcp16[di1];
+          d0 = (double)centre_dm(g, i, j, z0);
+          d1 = (double)centre_dm(g, i, j, z0 + 2);
         }
         double2 out;
         // exact division (bitwise IEEE) with RN(1/d) from the constant-memory
         // table (a broadcast for the warp-uniform interior d = 6; measured
         // faster than a shared-memory table or an IEEE division on boundary
         // cells)
-        out.x = div_small(fr[c].x * g.w + s0, d0, rd0);
-        out.y = div_small(fr[c].y * g.w + s1, d1, rd1);
+        out.x = div_small(fr[c].x * g.w + s0, d0, c_rcp16[(int)d0]);
+        out.y = div_small(fr[c].y * g.w + s1, d1, c_rcp16[(int)d1]);
         if (NORM) {
           const double u0 = NORM == 2 ? ov[c].x : out.x;
           const double u1 = NORM == 2 ? ov[c].y : out.y;
