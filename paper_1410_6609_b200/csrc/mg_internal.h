@@ -86,7 +86,18 @@ __device__ __forceinline__ void ghost_copies(const Grid &g, double *arr, int il,
 // thread gets both.  part: 64 doubles.  Up to 16 warps the warp partials are
 // read by lanes l and l + 16 alike, so four butterfly levels give every lane
 // the same bits; up to 32 warps, five levels.
-__device__ __forceinline__ double2 cg_allsum2(double v0, double v1, double *part) {
+// a barrier of the first cnt threads of the block (id 0: the whole block)
+__device__ __forceinline__ void bar_part(int id, int cnt) {
+  if (id == 0)
+    __syncthreads();
+  else
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(cnt) : "memory");
+}
+
+// (bar, cnt: the barrier of the participating threads -- the first cnt of
+// the block, a multiple of 32 -- when not the whole block)
+__device__ __forceinline__ double2 cg_allsum2(double v0, double v1, double *part,
+                                              int bar = 0, int cnt = 0) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     v0 += __shfl_xor_sync(0xffffffffu, v0, o);
@@ -97,8 +108,8 @@ __device__ __forceinline__ double2 cg_allsum2(double v0, double v1, double *part
     part[w] = v0;
     part[32 + w] = v1;
   }
-  __syncthreads();
-  const int nw = (blockDim.x + 31) >> 5;
+  bar_part(bar, cnt);
+  const int nw = ((bar ? cnt : (int)blockDim.x) + 31) >> 5;
   if (nw <= 16) {
     const int l = lane & 15;
     double s0 = l < nw ? part[l] : 0.0, s1 = l < nw ? part[32 + l] : 0.0;

@@ -609,7 +609,7 @@ __host__ __device__ inline size_t cg_reg_doubles(long long N) { return 2 * (size
 template <bool PER, int E>
 __device__ __forceinline__ void cg_cta_cg(const Grid &g, double *sm, double (*part)[64],
                                           double tol, int maxit, int *iters_out,
-                                          int nthr) {
+                                          int nthr, int bar, int bcnt) {
   const int N = g.nx * g.ny * g.nz;
   double *rs = sm, *xs = sm + N + 1;
   const int sx = g.ny * g.nz, sy = g.nz;
@@ -669,16 +669,19 @@ __device__ __forceinline__ void cg_cta_cg(const Grid &g, double *sm, double (*pa
       }
     }
   };
-  __syncthreads();  // r published
+  bar_part(bar, bcnt);  // r published
   double gg, dl;
   matvec(gg, dl);
-  double2 gd = cg_allsum2(gg, dl, part[pb]);
+  double2 gd = cg_allsum2(gg, dl, part[pb], bar, bcnt);
   pb ^= 1;
   double gamma = gd.x;
   const double bnorm = sqrt(gamma);
   int it = 0;
   if (bnorm > 0.0) {
     double alpha = gamma / gd.y;
+    // beta gamma / alpha_old = gamma^2 k with k = 1 / (gamma_old alpha_old),
+    // formed a step ahead: one division on the chain after the reduction
+    double kinv = 1.0 / (gamma * alpha);
 #pragma unroll
     for (int e = 0; e < E; e++) {
       p[e] = r[e];
@@ -694,15 +697,16 @@ __device__ __forceinline__ void cg_cta_cg(const Grid &g, double *sm, double (*pa
           xs[n] = xs[n] + alpha * p[e];
         }
       }
-      __syncthreads();  // r published (the reads of the last product are done:
-                        // they precede the reduction's barrier)
+      bar_part(bar, bcnt);  // r published (the reads of the last product are
+                            // done: they precede the reduction's barrier)
       it++;
       matvec(gg, dl);
-      gd = cg_allsum2(gg, dl, part[pb]);
+      gd = cg_allsum2(gg, dl, part[pb], bar, bcnt);
       pb ^= 1;
       if (sqrt(gd.x) <= tol * bnorm) break;
       const double beta = gd.x / gamma;
-      alpha = gd.x / (gd.y - beta * (gd.x / alpha));
+      alpha = gd.x / (gd.y - (gd.x * gd.x) * kinv);
+      kinv = 1.0 / (gd.x * alpha);
       gamma = gd.x;
 #pragma unroll
       for (int e = 0; e < E; e++) {
@@ -729,17 +733,17 @@ __device__ __forceinline__ void cg_cta_cg(const Grid &g, double *sm, double (*pa
 template <bool PER, int MAXE = 8>
 __device__ __forceinline__ bool cg_cta_fast(const Grid &g, double *sm, double (*part)[64],
                                             double tol, int maxit, int *iters_out,
-                                            int nthr) {
+                                            int nthr, int bar = 0, int bcnt = 0) {
   const int N = g.nx * g.ny * g.nz;
   const int E = (N + nthr - 1) / nthr;
   if (E <= 1)
-    cg_cta_cg<PER, 1>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 1>(g, sm, part, tol, maxit, iters_out, nthr, bar, bcnt);
   else if (E <= 2)
-    cg_cta_cg<PER, 2>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 2>(g, sm, part, tol, maxit, iters_out, nthr, bar, bcnt);
   else if (MAXE >= 4 && E <= 4)
-    cg_cta_cg<PER, 4>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 4>(g, sm, part, tol, maxit, iters_out, nthr, bar, bcnt);
   else if (MAXE >= 8 && E <= 8)
-    cg_cta_cg<PER, 8>(g, sm, part, tol, maxit, iters_out, nthr);
+    cg_cta_cg<PER, 8>(g, sm, part, tol, maxit, iters_out, nthr, bar, bcnt);
   else
     return false;
   return true;
@@ -1439,14 +1443,21 @@ __global__ void __launch_bounds__(kTailThreads)
   const Grid &gc = T.g[T.n - 1];
   if (cl.block_rank() == 0) {
     const long long N = (long long)gc.nx * gc.ny * gc.nz;
-    if (N <= kCgSmemMax) {
-      // (at most four elements per thread here -- eight would spill --:
-      // vcycle_tail_supported keeps larger coarsest grids out of the tail,
-      // so that the tail and the standalone CG run the same arithmetic)
-      if (!cg_cta_fast<PER, 4>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr))
-        cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
-    } else
+    // (at most four elements per thread here -- eight would spill --:
+    // vcycle_tail_supported keeps larger coarsest grids out of the tail, so
+    // that the tail and the standalone CG run the same arithmetic.)  Only
+    // the standalone CG's threads take part, behind barrier 1: the same
+    // warps, so the same reduction trees, with fewer warps to wait for.
+    const int pad = (cg_nthr + 31) / 32 * 32;
+    if (N <= kCgSmemMax && (N + cg_nthr - 1) / cg_nthr <= 4) {
+      if ((int)threadIdx.x < pad)
+        cg_cta_fast<PER, 4>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr,
+                            pad < (int)blockDim.x ? 1 : 0, pad);
+    } else if (N <= kCgSmemMax) {
+      cg_cta<PER>(gc, tail_sm, part, tol, maxit, iters_out, cg_nthr);
+    } else {
       cg_cta<PER>(gc, cg_scr, part, tol, maxit, iters_out, cg_nthr);
+    }
   }
   cl.sync();
   fill(gc);
