@@ -176,11 +176,77 @@ __device__ __forceinline__ void bsum3(double *v, double (*sh)[32]) {
 
 }  // namespace
 
+// padded per-cell counts of one box image (2 rim cells per side)
+constexpr int kPad = 12288;
+
+// The force of one sphere image over an interior box (every cell of the box
+// and its D3Q19 neighbours inside the level, no mask, no wrap) in adjoint
+// form.  The gradient is linear in Phi, so
+//   sum_b c_b S_a(b) = sum_b c_b sum_q w_q e_qa Phi(b + e_q)
+//                    = (1/36) sum_y Phi(y) K_a(y),
+//   K_a(y) = sum_q m_q e_qa c(y - e_q),  m = 2 (faces), 1 (edges),
+// an integer stencil of the covered counts c (exact).  K vanishes wherever
+// the 3^3 neighbourhood is uniformly covered or empty, so only the cells of
+// a shell around the sphere surface load Phi -- once each, instead of once
+// per covered neighbour.  cc: the counts on the padded box, x planes outside
+// [xa, xb] zero.  Returns sum_y Phi(y) K_a(y) per component (the caller
+// scales by (3 / h) (1 / 36) rho_per_count); the sum is reordered against
+// the oracle's cell-by-cell one (rounding only).
+__device__ __forceinline__ void adjoint_force(const Grid &g, const sph::Box &bx, int xa,
+                                              int xb, const unsigned short *cc, double *G) {
+  const int Q2 = bx.n[2] + 4, Q1 = bx.n[1] + 4;
+  const int X = Q1 * Q2, Y = Q2;
+  const int nv = bx.n[1] + 2, nw = bx.n[2] + 2, nu = xb - xa + 3;
+  const int tot = nu * nv * nw;
+  // thread t's cell (uo, v, w) of the rim box, advanced by blockDim.x per
+  // step with carries (no division in the loop)
+  const int B = blockDim.x;
+  const int dw = B % nw, dv = (B / nw) % nv, du = B / (nw * nv);
+  int w = threadIdx.x % nw, v = (threadIdx.x / nw) % nv, uo = threadIdx.x / (nw * nv);
+  const int u0 = xa - bx.lo[0] - 1;
+  for (int t = threadIdx.x; t < tot; t += B) {
+    const int u = u0 + uo;
+    const int idx = ((u + 2) * Q1 + v + 1) * Q2 + w + 1;
+    const unsigned short *q = cc + idx;
+    // faces (weight 2), then the 12 edges, each added to the two components
+    // it points along
+    int kx = 2 * ((int)q[-X] - (int)q[X]);
+    int ky = 2 * ((int)q[-Y] - (int)q[Y]);
+    int kz = 2 * ((int)q[-1] - (int)q[1]);
+    int e;
+    e = q[-X - Y]; kx += e; ky += e;
+    e = q[-X + Y]; kx += e; ky -= e;
+    e = q[X - Y];  kx -= e; ky += e;
+    e = q[X + Y];  kx -= e; ky -= e;
+    e = q[-X - 1]; kx += e; kz += e;
+    e = q[-X + 1]; kx += e; kz -= e;
+    e = q[X - 1];  kx -= e; kz += e;
+    e = q[X + 1];  kx -= e; kz -= e;
+    e = q[-Y - 1]; ky += e; kz += e;
+    e = q[-Y + 1]; ky += e; kz -= e;
+    e = q[Y - 1];  ky -= e; kz += e;
+    e = q[Y + 1];  ky -= e; kz -= e;
+    if ((kx | ky | kz) != 0) {
+      const int i = bx.lo[0] + u, j = bx.lo[1] + v - 1, k = bx.lo[2] + w - 1;
+      const long long o = (long long)(i - g.x0 + 1) * g.plane + (long long)(j + 1) * g.pz +
+                          (k >> 1);
+      const double phi = (((i + j + k) & 1) ? g.phiB : g.phiR)[o];
+      G[0] = G[0] + phi * (double)kx;
+      G[1] = G[1] + phi * (double)ky;
+      G[2] = G[2] + phi * (double)kz;
+    }
+    w += dw;
+    if (w >= nw) { w -= nw; v++; }
+    v += dv;
+    if (v >= nv) { v -= nv; uo++; }
+    uo += du;
+  }
+}
+
 // counts: the global covered sub-cell count of each sphere if already known
 // (the RHS kernel of the same step, same subsampling), else null
-// 4 CTAs per SM (64 registers, a few spilled): the per-sphere CTAs are
-// latency-bound, so residency beats registers (0.92 vs 1.23 ms for the
-// 7,417 spheres of the time-stepping regime)
+// 4 CTAs per SM: the per-sphere CTAs are latency-bound, so residency beats
+// registers
 // PER: periodic images (up to 27); otherwise the sphere itself only, without
 // the 27-entry image array (registers / stack of the common case)
 template <bool PER>
@@ -190,6 +256,7 @@ __global__ void __launch_bounds__(kTF, 4)
               const unsigned long long *counts) {
   __shared__ double sh[32];
   __shared__ sph::Tab tab;
+  __shared__ unsigned short cc[kPad];
   const int p = blockIdx.x;
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
   const double R2 = R * R;
@@ -204,22 +271,24 @@ __global__ void __launch_bounds__(kTF, 4)
     img[0][1] = sph[5 * p + 1];
     img[0][2] = sph[5 * p + 2];
   }
-  long long cnt = 0;  // threads own (j, k) columns of the box, walk along x
+  long long cnt = 0;  // the sphere's covered sub-cells of the whole domain
   for (int m = 0; !counts && m < nimg; m++) {
     const sph::Box bx = sph::box_of(g, h, img[m], R);
     if (bx.cells() == 0) continue;
-    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
+    if (sph::tables(tab, bx, s, hs, img[m])) {
+      cnt += sph::image_count(tab, bx, s, R2);
+      continue;
+    }
     const int ncol = bx.n[1] * bx.n[2];
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
       for (int ci = 0; ci < bx.n[0]; ci++)
-        cnt += tb ? sph::count_tab(tab, ci, cj, ck, s, R2)
-                  : sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s,
-                                   hs, img[m][0], img[m][1], img[m][2], R);
+        cnt += sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s, hs,
+                              img[m][0], img[m][1], img[m][2], R);
     }
   }
   const double np = counts ? (double)counts[p] : bsum((double)cnt, sh);
-  double F[3] = {0.0, 0.0, 0.0};
+  double F[3] = {0.0, 0.0, 0.0}, G[3] = {0.0, 0.0, 0.0};
   const bool any = np > 0.0 || normalization == 1;
   const double rho0 = Q / ((4.0 / 3.0) * 3.14159265358979323846 * (R * R * R));
   for (int m = 0; any && m < nimg; m++) {
@@ -227,22 +296,41 @@ __global__ void __launch_bounds__(kTF, 4)
     const int xa = bx.lo[0] > g.x0 ? bx.lo[0] : g.x0;
     const int xb = min(bx.lo[0] + bx.n[0] - 1, g.x0 + g.nxl - 1);
     if (bx.cells() == 0 || xa > xb) continue;
-    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
-    auto ld_glb = [&](int x, int y, int z) { return phi_at(g, x, y, z); };
+    const int Q1 = bx.n[1] + 4, Q2 = bx.n[2] + 4;
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]) &&
+                    (long long)(bx.n[0] + 4) * Q1 * Q2 <= kPad;
     // every cell of this box (and its D3Q19 neighbours) inside the level,
-    // no mask, no wrap: the direct-addressed gradient applies to all of them
+    // no mask, no wrap: the adjoint form applies
     const bool interior = !solid && !is_periodic(g) && xa - 1 >= 0 && xb + 1 < g.nx &&
                           bx.lo[1] - 1 >= 0 && bx.lo[1] + bx.n[1] < g.ny &&
                           bx.lo[2] - 1 >= 0 && bx.lo[2] + bx.n[2] < g.nz;
     const int ncol = bx.n[1] * bx.n[2];
+    if (tb) {  // the slab's covered counts on the padded box
+      if (interior) {
+        for (int e = threadIdx.x; e < (bx.n[0] + 4) * Q1 * Q2; e += blockDim.x) cc[e] = 0;
+        __syncthreads();
+      }
+      for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
+        const int cj = col / bx.n[2], ck = col % bx.n[2];
+        sph::column_counts(tab, bx, s, R2, cj, ck, cc, (2 * Q1 + cj + 2) * Q2 + ck + 2,
+                           Q1 * Q2, xa - bx.lo[0], xb - bx.lo[0]);
+      }
+      if (interior) {
+        __syncthreads();
+        adjoint_force(g, bx, xa, xb, cc, G);
+        continue;
+      }
+    }
+    auto ld_glb = [&](int x, int y, int z) { return phi_at(g, x, y, z); };
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
       const int j = bx.lo[1] + cj, k = bx.lo[2] + ck;
       for (int i = xa; i <= xb; i++) {
-        const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
+        // (the thread's own column of cc)
+        const int c = tb ? (int)cc[((i - bx.lo[0] + 2) * Q1 + cj + 2) * Q2 + ck + 2]
                          : sph::sub_count(i, j, k, s, hs, img[m][0], img[m][1],
                                           img[m][2], R);
-        if (!c || (!interior && !valid_cell(g, solid, i, j, k))) continue;
+        if (!c || !valid_cell(g, solid, i, j, k)) continue;
         const double rho = (normalization == 1)
                                ? rho0 * ((double)c / (double)(s * s * s))
                                : (Q * (double)c) / (np * (h * h * h));
@@ -256,6 +344,13 @@ __global__ void __launch_bounds__(kTF, 4)
       }
     }
   }
+  // the adjoint sums: F += (3 / h) (1 / 36) rho_per_count sum_y Phi K
+  const double unit = !any ? 0.0
+                     : (normalization == 1) ? rho0 / (double)(s * s * s)
+                                            : Q / (np * (h * h * h));
+  const double scale = ((3.0 / h) / 36.0) * unit;
+#pragma unroll
+  for (int a = 0; a < 3; a++) F[a] = F[a] + G[a] * scale;
   __shared__ double sh3[3][32];
   bsum3(F, sh3);
   if (threadIdx.x == 0)

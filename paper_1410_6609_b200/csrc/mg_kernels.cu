@@ -848,20 +848,22 @@ __global__ void __launch_bounds__(kThreads)
   sph::make_images<PER>(g, h, sph[5 * p], sph[5 * p + 1], sph[5 * p + 2], im);
   const int nimg = im.n;
   auto &img = im.c;
-  // threads own (j, k) columns of the box and walk along x: no per-cell
-  // index division; integer counts are exact in any order
+  // threads share the (y, z) sub-rows of the box: each adds the length of
+  // its x interval (sph::x_interval); integer counts are exact in any order
   long long cnt = 0;
   for (int m = 0; m < nimg; m++) {
     const sph::Box bx = sph::box_of(g, h, img[m], R);
     if (bx.cells() == 0) continue;
-    const bool tb = sph::tables(tab, bx, s, hs, img[m]);
-    const int ncol = bx.n[1] * bx.n[2];
+    if (sph::tables(tab, bx, s, hs, img[m])) {
+      cnt += sph::image_count(tab, bx, s, R2);
+      continue;
+    }
+    const int ncol = bx.n[1] * bx.n[2];  // (a box too long for the tables)
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
       for (int ci = 0; ci < bx.n[0]; ci++)
-        cnt += tb ? sph::count_tab(tab, ci, cj, ck, s, R2)
-                  : sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s,
-                                   hs, img[m][0], img[m][1], img[m][2], R);
+        cnt += sph::sub_count(bx.lo[0] + ci, bx.lo[1] + cj, bx.lo[2] + ck, s, hs,
+                              img[m][0], img[m][1], img[m][2], R);
     }
   }
   const double np = block_sum((double)cnt, sh);
@@ -895,12 +897,15 @@ __global__ void __launch_bounds__(kThreads)
   if (slot < kBinCap) B.items[(size_t)b * kBinCap + slot] = p;
 }
 
-// can spheres a and b cover a common sub-cell centre?  Conservative: per
-// axis the (minimum-image on periodic axes) centre distance <= Ra + Rb + 2h
+// can spheres a and b cover sub-cell centres of a common cell?  Then the
+// centres are at most Ra + Rb + sqrt(3) h apart (two points of one cell);
+// conservative: the (minimum-image on periodic axes) centre distance
+// <= Ra + Rb + 2h
 __device__ __forceinline__ bool spheres_near(const Grid &g, double h, const double *a,
                                              const double *b) {
   const int ext[3] = {g.nx, g.ny, g.nz};
   const double lim = a[3] + b[3] + 2.0 * h;
+  double d2 = 0.0;
 #pragma unroll
   for (int ax = 0; ax < 3; ax++) {
     double d = fabs(b[ax] - a[ax]);
@@ -909,8 +914,9 @@ __device__ __forceinline__ bool spheres_near(const Grid &g, double h, const doub
       if (d > 0.5 * L) d = L - d;
     }
     if (d > lim) return false;
+    d2 += d * d;
   }
-  return true;
+  return d2 <= lim * lim;
 }
 
 // covered sub-cell centres of cell (i,j,k) by sphere q: the image nearest to
@@ -1035,6 +1041,7 @@ __global__ void __launch_bounds__(kThreads)
                      SphereLists S) {
   __shared__ sph::Tab tab;
   __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
+  __shared__ unsigned short cc[sph::kCells];  // covered counts of the box cells
   const int k = OVERLAP ? 1 : 0;
   if ((int)blockIdx.x >= S.nlist[k]) return;
   const int p = S.list[(size_t)k * n + blockIdx.x];
@@ -1063,13 +1070,19 @@ __global__ void __launch_bounds__(kThreads)
     const int xa = bx.lo[0] > g.x0 ? bx.lo[0] : g.x0;
     const int xb = min(bx.lo[0] + bx.n[0] - 1, g.x0 + g.nxl - 1);
     if (bx.cells() == 0 || xa > xb) continue;
-    const bool tb = sph::tables(tab, bx, s, hs, img[m]);  // (also publishes vt)
+    // (tables() also publishes vt)
+    const bool tb = sph::tables(tab, bx, s, hs, img[m]) && bx.cells() <= sph::kCells;
     const int ncol = bx.n[1] * bx.n[2];
     for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
       const int cj = col / bx.n[2], ck = col % bx.n[2];
       const int j = bx.lo[1] + cj, kz = bx.lo[2] + ck;
+      // the column's counts from its sub-rows' x intervals (the thread's own
+      // entries of cc: no barrier)
+      if (tb)
+        sph::column_counts(tab, bx, s, R2, cj, ck, cc, col, ncol, xa - bx.lo[0],
+                           xb - bx.lo[0]);
       for (int i = xa; i <= xb; i++) {
-        const int c = tb ? sph::count_tab(tab, i - bx.lo[0], cj, ck, s, R2)
+        const int c = tb ? (int)cc[col + (i - bx.lo[0]) * ncol]
                          : sph::sub_count(i, j, kz, s, hs, img[m][0], img[m][1],
                                           img[m][2], R);
         if (!c) continue;

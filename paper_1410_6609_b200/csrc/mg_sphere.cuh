@@ -22,12 +22,16 @@ constexpr int kTab = 512;  // table entries per axis: (bbox cells) * s
 constexpr int kVal = 513;  // tabulated cell values per covered count (s <= 8)
 
 // shared-memory tables of one sphere image: per axis the squared distances
-// of the sub-cell centre coordinates (d[a][(i - lo) s + sub]) and, per cell,
-// their minimum / maximum over the cell's s sub-positions
+// of the sub-cell centre coordinates (d[a][(i - lo) s + sub]); emin = the x
+// entry of least distance (the d[0] entries do not increase before it and do
+// not decrease from it on)
 struct Tab {
   double d[3][kTab];
-  double mn[3][kTab], mx[3][kTab];
+  int emin;
 };
+
+// per-cell covered counts of one box, in shared memory (box cells <= kCells)
+constexpr int kCells = 12288;
 
 __device__ __forceinline__ bool inside(int i, int j, int k, double h, double cx,
                                        double cy, double cz, double R) {
@@ -124,45 +128,107 @@ __device__ __forceinline__ bool tables(Tab &T, const Box &b, int s, double hs,
   __syncthreads();
   for (int a = 0; a < 3; a++)
     if (b.n[a] * s > kTab) return false;
-  for (int a = 0; a < 3; a++) {
-    for (int e = threadIdx.x; e < b.n[a] * s; e += blockDim.x) {
-      const int i = b.lo[a] + e / s, sub = e % s;
+  // one thread per (axis, cell), the cell's s entries in a loop
+  const int nc = b.n[0] + b.n[1] + b.n[2];
+  for (int t = threadIdx.x; t < nc; t += blockDim.x) {
+    const int a = t < b.n[0] ? 0 : (t < b.n[0] + b.n[1] ? 1 : 2);
+    const int ci = t - (a > 0 ? b.n[0] : 0) - (a > 1 ? b.n[1] : 0);
+    const int i = b.lo[a] + ci;
+    for (int sub = 0; sub < s; sub++) {
+      const int e = ci * s + sub;
       const double d = ((double)(i * s + sub) + 0.5) * hs - c[a];
       T.d[a][e] = d * d;
-    }
-    for (int ci = threadIdx.x; ci < b.n[a]; ci += blockDim.x) {
-      double lo = 0.0, hi = 0.0;
-      for (int sub = 0; sub < s; sub++) {  // the same products as T.d
-        const double d = ((double)((b.lo[a] + ci) * s + sub) + 0.5) * hs - c[a];
-        const double q = d * d;
-        lo = sub ? fmin(lo, q) : q;
-        hi = sub ? fmax(hi, q) : q;
+      // x: the first entry whose coordinate is >= the centre (x strictly
+      // increases with e): the least square is there or just before it
+      if (a == 0) {
+        const bool first = d >= 0.0 && (e == 0 || ((double)(i * s + sub) - 0.5) * hs - c[a] < 0.0);
+        const bool none = e == b.n[0] * s - 1 && d < 0.0;  // all left of c
+        if (first || none) T.emin = none ? e + 1 : e;
       }
-      T.mn[a][ci] = lo;
-      T.mx[a][ci] = hi;
     }
+  }
+  __syncthreads();
+  const int ne = b.n[0] * s;
+  if (ne > 0) {
+    const int e0 = T.emin;  // (every thread reads it; one more barrier)
+    __syncthreads();
+    if (threadIdx.x == 0)
+      T.emin = (e0 > 0 && (e0 == ne || T.d[0][e0 - 1] <= T.d[0][e0])) ? e0 - 1 : e0;
   }
   __syncthreads();
   return true;
 }
 
-// covered sub-cells of box cell (ci, cj, ck) (box-relative) from the tables.
-// IEEE addition is monotonic, so fl(fl(x+y)+z) of the per-axis minima
-// (maxima) bounds every sub-centre's d2 from below (above): a cell whose
-// lower bound exceeds R^2 has no covered sub-centre, one whose upper bound
-// is <= R^2 has all s^3 -- exactly what the per-sub-centre test gives.
-__device__ __forceinline__ int count_tab(const Tab &T, int ci, int cj, int ck,
-                                         int s, double R2) {
-  if ((T.mn[0][ci] + T.mn[1][cj]) + T.mn[2][ck] > R2) return 0;
-  if ((T.mx[0][ci] + T.mx[1][cj]) + T.mx[2][ck] <= R2) return s * s * s;
-  int cnt = 0;
-  const double *tx = T.d[0] + ci * s, *ty = T.d[1] + cj * s, *tz = T.d[2] + ck * s;
-  for (int a = 0; a < s; a++)
-    for (int b = 0; b < s; b++) {
-      const double t = tx[a] + ty[b];
-      for (int c = 0; c < s; c++) cnt += (t + tz[c] <= R2) ? 1 : 0;
+// floor(x / s) for 0 <= x < 2^10, s <= 16, with M = ceil(2^16 / s): the
+// multiplier's excess adds less than x 2^-16 < 1/s to x / s
+__device__ __forceinline__ int div_s(int x, unsigned M) { return (int)(((unsigned)x * M) >> 16); }
+__host__ __device__ constexpr unsigned div_magic(int s) { return (65536u + (unsigned)s - 1u) / (unsigned)s; }
+
+// The x sub-positions e (box-relative) of one sub-row -- fixed y and z
+// squares ty, tz -- inside the sphere: (d[0][e] + ty) + tz <= R^2, the
+// inside test's own operations.  IEEE addition is monotonic, so the test
+// holds on an interval around emin, found by two binary searches.  Returns
+// the interval [lo, hi] (hi < lo: empty).
+__device__ __forceinline__ int2 x_interval(const Tab &T, int ne, double ty, double tz,
+                                           double R2) {
+  const double *dx = T.d[0];
+  const int em = T.emin;
+  if (!((dx[em] + ty) + tz <= R2)) return make_int2(1, 0);
+  int a = 0, z = em;  // first inside position in [0, em]
+  while (a < z) {
+    const int m = (a + z) >> 1;
+    if ((dx[m] + ty) + tz <= R2) z = m; else a = m + 1;
+  }
+  const int lo = a;
+  a = em;
+  z = ne - 1;  // last inside position in [em, ne)
+  while (a < z) {
+    const int m = (a + z + 1) >> 1;
+    if ((dx[m] + ty) + tz <= R2) a = m; else z = m - 1;
+  }
+  return make_int2(lo, a);
+}
+
+// covered sub-cell count of every cell ci = 0..n0-1 of box column (cj, ck):
+// cnt[base + ci * st] (cells with ci outside [sa, sb] -- another slab's --
+// are stored as 0); returns the column's total over all ci.  Exactly the
+// per-sub-centre test: the s^2 sub-rows' x intervals added cell by cell.
+__device__ __forceinline__ int column_counts(const Tab &T, const Box &b, int s, double R2,
+                                             int cj, int ck, unsigned short *cnt,
+                                             int base, int st, int sa, int sb) {
+  const int n0 = b.n[0], ne = n0 * s;
+  const unsigned M = div_magic(s);
+  for (int ci = 0; ci < n0; ci++) cnt[base + ci * st] = 0;
+  int tot = 0;
+  for (int y = 0; y < s; y++) {
+    const double ty = T.d[1][cj * s + y];
+    for (int z = 0; z < s; z++) {
+      const int2 iv = x_interval(T, ne, ty, T.d[2][ck * s + z], R2);
+      if (iv.y < iv.x) continue;
+      tot += iv.y - iv.x + 1;
+      const int c0 = max(div_s(iv.x, M), sa), c1 = min(div_s(iv.y, M), sb);
+      for (int ci = c0; ci <= c1; ci++) {
+        const int n = min(iv.y, ci * s + s - 1) - max(iv.x, ci * s) + 1;
+        cnt[base + ci * st] = (unsigned short)(cnt[base + ci * st] + n);
+      }
     }
-  return cnt;
+  }
+  return tot;
+}
+
+// the covered sub-cell total of one image: warps take the y sub-rows, lanes
+// the z sub-rows
+__device__ __forceinline__ long long image_count(const Tab &T, const Box &b, int s,
+                                                 double R2) {
+  const int ny = b.n[1] * s, nz = b.n[2] * s, ne = b.n[0] * s;
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  long long tot = 0;
+  for (int y = threadIdx.x >> 5; y < ny; y += nw)
+    for (int z = lane; z < nz; z += 32) {
+      const int2 iv = x_interval(T, ne, T.d[1][y], T.d[2][z], R2);
+      if (iv.y >= iv.x) tot += iv.y - iv.x + 1;
+    }
+  return tot;
 }
 
 }  // namespace sph
