@@ -179,6 +179,27 @@ __device__ __forceinline__ void bsum3(double *v, double (*sh)[32]) {
 // padded per-cell counts of one box image (2 rim cells per side)
 constexpr int kPad = 12288;
 
+// The K stencil at padded index idx (see adjoint_force below).
+__device__ __forceinline__ void k_stencil(const unsigned short *q, int X, int Y, int &kx,
+                                          int &ky, int &kz) {
+  kx = 2 * ((int)q[-X] - (int)q[X]);
+  ky = 2 * ((int)q[-Y] - (int)q[Y]);
+  kz = 2 * ((int)q[-1] - (int)q[1]);
+  int e;
+  e = q[-X - Y]; kx += e; ky += e;
+  e = q[-X + Y]; kx += e; ky -= e;
+  e = q[X - Y];  kx -= e; ky += e;
+  e = q[X + Y];  kx -= e; ky -= e;
+  e = q[-X - 1]; kx += e; kz += e;
+  e = q[-X + 1]; kx += e; kz -= e;
+  e = q[X - 1];  kx -= e; kz += e;
+  e = q[X + 1];  kx -= e; kz -= e;
+  e = q[-Y - 1]; ky += e; kz += e;
+  e = q[-Y + 1]; ky += e; kz -= e;
+  e = q[Y - 1];  ky -= e; kz += e;
+  e = q[Y + 1];  ky -= e; kz -= e;
+}
+
 // The force of one sphere image over an interior box (every cell of the box
 // and its D3Q19 neighbours inside the level, no mask, no wrap) in adjoint
 // form.  The gradient is linear in Phi, so
@@ -204,36 +225,20 @@ __device__ __forceinline__ void adjoint_force(const Grid &g, const sph::Box &bx,
   const int dw = B % nw, dv = (B / nw) % nv, du = B / (nw * nv);
   int w = threadIdx.x % nw, v = (threadIdx.x / nw) % nv, uo = threadIdx.x / (nw * nv);
   const int u0 = xa - bx.lo[0] - 1;
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0;  // (registers, added to G at the end)
   for (int t = threadIdx.x; t < tot; t += B) {
     const int u = u0 + uo;
     const int idx = ((u + 2) * Q1 + v + 1) * Q2 + w + 1;
-    const unsigned short *q = cc + idx;
-    // faces (weight 2), then the 12 edges, each added to the two components
-    // it points along
-    int kx = 2 * ((int)q[-X] - (int)q[X]);
-    int ky = 2 * ((int)q[-Y] - (int)q[Y]);
-    int kz = 2 * ((int)q[-1] - (int)q[1]);
-    int e;
-    e = q[-X - Y]; kx += e; ky += e;
-    e = q[-X + Y]; kx += e; ky -= e;
-    e = q[X - Y];  kx -= e; ky += e;
-    e = q[X + Y];  kx -= e; ky -= e;
-    e = q[-X - 1]; kx += e; kz += e;
-    e = q[-X + 1]; kx += e; kz -= e;
-    e = q[X - 1];  kx -= e; kz += e;
-    e = q[X + 1];  kx -= e; kz -= e;
-    e = q[-Y - 1]; ky += e; kz += e;
-    e = q[-Y + 1]; ky += e; kz -= e;
-    e = q[Y - 1];  ky -= e; kz += e;
-    e = q[Y + 1];  ky -= e; kz -= e;
+    int kx, ky, kz;
+    k_stencil(cc + idx, X, Y, kx, ky, kz);
     if ((kx | ky | kz) != 0) {
       const int i = bx.lo[0] + u, j = bx.lo[1] + v - 1, k = bx.lo[2] + w - 1;
       const long long o = (long long)(i - g.x0 + 1) * g.plane + (long long)(j + 1) * g.pz +
                           (k >> 1);
       const double phi = (((i + j + k) & 1) ? g.phiB : g.phiR)[o];
-      G[0] = G[0] + phi * (double)kx;
-      G[1] = G[1] + phi * (double)ky;
-      G[2] = G[2] + phi * (double)kz;
+      g0 = g0 + phi * (double)kx;
+      g1 = g1 + phi * (double)ky;
+      g2 = g2 + phi * (double)kz;
     }
     w += dw;
     if (w >= nw) { w -= nw; v++; }
@@ -241,6 +246,106 @@ __device__ __forceinline__ void adjoint_force(const Grid &g, const sph::Box &bx,
     if (v >= nv) { v -= nv; uo++; }
     uo += du;
   }
+  G[0] = G[0] + g0;
+  G[1] = G[1] + g1;
+  G[2] = G[2] + g2;
+}
+
+constexpr int kShellRounds = 4;  // column rounds of the shell list (ncol <= 4 blockDim)
+
+// Shell form of adjoint_force: K(y) vanishes unless y lies within one cell
+// of a covered cell and not amid full ones, so the rim-box columns first
+// mark their candidate cells -- from per-column bit masks of the covered
+// (cm) and fully covered (fm) cells of the 3 x 3 neighbouring columns --
+// and append them to a shared list (warp scans + per-warp totals: a fixed
+// order), which the block then works through evenly.  cm / fm: per padded column ((n1 + 2) x (n2 + 2),
+// rim columns zero), bit ci + 1 for box cell ci.  Returns false (nothing
+// accumulated) when the list would not fit; the caller then runs
+// adjoint_force.
+__device__ __forceinline__ bool adjoint_force_shell(const Grid &g, const sph::Box &bx,
+                                                    const unsigned short *cc,
+                                                    const unsigned *cm, const unsigned *fm,
+                                                    unsigned *list, int cap, int *wsum,
+                                                    double *G) {
+  const int Q2 = bx.n[2] + 4, Q1 = bx.n[1] + 4;
+  const int X = Q1 * Q2, Y = Q2;
+  const int nv = bx.n[1] + 2, nw = bx.n[2] + 2, ncol = nv * nw;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+  // up to kShellRounds column rounds; list order = (round, warp, lane,
+  // bit): a deterministic order, so the sums are reproducible
+  unsigned need[kShellRounds];
+  int excl[kShellRounds];
+#pragma unroll
+  for (int r = 0; r < kShellRounds; r++) {
+    const int t = r * blockDim.x + threadIdx.x;
+    need[r] = 0;
+    if (t < ncol) {
+      const int v = t / nw, w = t - v * nw;
+      unsigned any = 0, all = ~0u;
+#pragma unroll
+      for (int dv = -1; dv <= 1; dv++)
+#pragma unroll
+        for (int dw = -1; dw <= 1; dw++) {
+          const int vv = v + dv, ww = w + dw;
+          if (vv < 0 || vv >= nv || ww < 0 || ww >= nw) {
+            all = 0;
+            continue;
+          }
+          const unsigned c = cm[vv * nw + ww], f = fm[vv * nw + ww];
+          any |= c | (c << 1) | (c >> 1);
+          all &= f & (f << 1) & (f >> 1);
+        }
+      need[r] = any & ~all;
+    }
+    const int cnt = __popc(need[r]);
+    int incl = cnt;  // warp inclusive scan of the counts
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    excl[r] = incl - cnt;
+    if (lane == 31) wsum[r * nwarp + wid] = incl;
+  }
+  __syncthreads();
+  int L = 0;
+  for (int k = 0; k < kShellRounds * nwarp; k++) L += wsum[k];
+  if (L > cap) return false;  // (block-uniform)
+#pragma unroll
+  for (int r = 0; r < kShellRounds; r++) {
+    const int t = r * blockDim.x + threadIdx.x;
+    int base = excl[r];
+    for (int k = 0; k < r * nwarp + wid; k++) base += wsum[k];
+    const int v = t / nw, w = t - v * nw;
+    unsigned nd = need[r];
+    while (nd) {
+      const int b = __ffs(nd) - 1;  // bit b: box-relative x index b - 1
+      nd &= nd - 1;
+      list[base++] = (unsigned)(((b + 1) * Q1 + v + 1) * Q2 + w + 1) | ((unsigned)b << 14) |
+                     ((unsigned)v << 19) | ((unsigned)w << 24);
+    }
+  }
+  __syncthreads();
+  double g0 = 0.0, g1 = 0.0, g2 = 0.0;
+  for (int t = threadIdx.x; t < L; t += blockDim.x) {
+    const unsigned e = list[t];
+    int kx, ky, kz;
+    k_stencil(cc + (e & 0x3fffu), X, Y, kx, ky, kz);
+    if ((kx | ky | kz) == 0) continue;
+    const int i = bx.lo[0] + (int)((e >> 14) & 31u) - 1;
+    const int j = bx.lo[1] + (int)((e >> 19) & 31u) - 1;
+    const int k = bx.lo[2] + (int)((e >> 24) & 31u) - 1;
+    const long long o = (long long)(i - g.x0 + 1) * g.plane + (long long)(j + 1) * g.pz +
+                        (k >> 1);
+    const double phi = (((i + j + k) & 1) ? g.phiB : g.phiR)[o];
+    g0 = g0 + phi * (double)kx;
+    g1 = g1 + phi * (double)ky;
+    g2 = g2 + phi * (double)kz;
+  }
+  G[0] = G[0] + g0;
+  G[1] = G[1] + g1;
+  G[2] = G[2] + g2;
+  return true;
 }
 
 // counts: the global covered sub-cell count of each sphere if already known
@@ -257,6 +362,7 @@ __global__ void __launch_bounds__(kTF, 4)
   __shared__ double sh[32];
   __shared__ sph::Tab tab;
   __shared__ unsigned short cc[kPad];
+  __shared__ int wsum[kShellRounds * (kTF / 32)];
   const int p = blockIdx.x;
   const double R = sph[5 * p + 3], Q = sph[5 * p + 4];
   const double R2 = R * R;
@@ -306,18 +412,40 @@ __global__ void __launch_bounds__(kTF, 4)
                           bx.lo[2] - 1 >= 0 && bx.lo[2] + bx.n[2] < g.nz;
     const int ncol = bx.n[1] * bx.n[2];
     if (tb) {  // the slab's covered counts on the padded box
+      // the shell form's column masks after the padded counts (u32-aligned)
+      const int pv = ((bx.n[0] + 4) * Q1 * Q2 + 1) & ~1;
+      const int nv = bx.n[1] + 2, nw = bx.n[2] + 2;
+      const bool shell = interior && bx.n[0] <= 30 && nv <= 32 && nw <= 32 &&
+                         nv * nw <= kShellRounds * (int)blockDim.x &&
+                         pv + 4 * nv * nw <= kPad;
+      unsigned *cm = reinterpret_cast<unsigned *>(cc + pv), *fm = cm + nv * nw;
       if (interior) {
-        for (int e = threadIdx.x; e < (bx.n[0] + 4) * Q1 * Q2; e += blockDim.x) cc[e] = 0;
+        const int nz = shell ? pv + 4 * nv * nw : (bx.n[0] + 4) * Q1 * Q2;
+        for (int e = threadIdx.x; e < nz; e += blockDim.x) cc[e] = 0;
         __syncthreads();
       }
+      const int s3 = s * s * s;
       for (int col = threadIdx.x; col < ncol; col += blockDim.x) {
         const int cj = col / bx.n[2], ck = col % bx.n[2];
-        sph::column_counts(tab, bx, s, R2, cj, ck, cc, (2 * Q1 + cj + 2) * Q2 + ck + 2,
-                           Q1 * Q2, xa - bx.lo[0], xb - bx.lo[0]);
+        const int base = (2 * Q1 + cj + 2) * Q2 + ck + 2;
+        sph::column_counts(tab, bx, s, R2, cj, ck, cc, base, Q1 * Q2, xa - bx.lo[0],
+                           xb - bx.lo[0]);
+        if (shell) {  // (the thread's own column)
+          unsigned c = 0, f = 0;
+          for (int ci = 0; ci < bx.n[0]; ci++) {
+            const int v = cc[base + ci * Q1 * Q2];
+            c |= (v > 0 ? 2u : 0u) << ci;
+            f |= (v == s3 ? 2u : 0u) << ci;
+          }
+          cm[(cj + 1) * nw + ck + 1] = c;
+          fm[(cj + 1) * nw + ck + 1] = f;
+        }
       }
       if (interior) {
         __syncthreads();
-        adjoint_force(g, bx, xa, xb, cc, G);
+        if (!shell || !adjoint_force_shell(g, bx, cc, cm, fm, reinterpret_cast<unsigned *>(&tab),
+                                           (int)(sizeof(sph::Tab) / sizeof(unsigned)), wsum, G))
+          adjoint_force(g, bx, xa, xb, cc, G);
         continue;
       }
     }

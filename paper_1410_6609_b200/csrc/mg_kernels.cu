@@ -1035,7 +1035,7 @@ __global__ void __launch_bounds__(kNbThreads)
 // its lowest-index covering sphere with the ordered sum).  One CTA per list
 // entry; the grid covers all n spheres, the surplus CTAs return.
 template <bool OVERLAP, bool PER>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreads, 4)
     k_sphere_scatter(Grid g, double h, int s, int n, const double *sph,
                      int normalization, const unsigned long long *counts,
                      SphereLists S) {
@@ -1149,6 +1149,18 @@ void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *
                            int normalization, const unsigned long long *counts,
                            const SphereLists &S, cudaStream_t st) {
   if (n <= 0) return;
+  static bool carve = false;  // 4 CTAs of ~40 KB static shared memory per SM
+  if (!carve) {
+    cudaFuncSetAttribute(k_sphere_scatter<false, false>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_sphere_scatter<true, false>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_sphere_scatter<false, true>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaFuncSetAttribute(k_sphere_scatter<true, true>,
+                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carve = true;
+  }
   if (is_periodic(g)) {
     k_sphere_scatter<false, true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
                                                           counts, S);
