@@ -1029,12 +1029,12 @@ __global__ void __launch_bounds__(kNbThreads)
   }
 }
 
-// The density of the covered cells of this slab for the spheres of list
-// `k` (0: isolated spheres -- every covered cell is the sphere's alone, one
-// plain store per cell; 1: spheres with neighbours -- the cell is written by
-// its lowest-index covering sphere with the ordered sum).  One CTA per list
-// entry; the grid covers all n spheres, the surplus CTAs return.
-template <bool OVERLAP, bool PER>
+// The density of the covered cells of this slab, one CTA per sphere: the
+// spheres with neighbours first (list 1: the cell is written by its
+// lowest-index covering sphere with the ordered sum), then the isolated
+// ones (list 0: every covered cell is the sphere's alone, one plain store
+// per cell) -- the heavier CTAs start first.  Grid = n.
+template <bool PER>
 __global__ void __launch_bounds__(kThreads, 4)
     k_sphere_scatter(Grid g, double h, int s, int n, const double *sph,
                      int normalization, const unsigned long long *counts,
@@ -1042,9 +1042,12 @@ __global__ void __launch_bounds__(kThreads, 4)
   __shared__ sph::Tab tab;
   __shared__ double vt[sph::kVal];  // cell value by covered count (s^3 <= kVal-1)
   __shared__ unsigned short cc[sph::kCells];  // covered counts of the box cells
+  const int n1 = S.nlist[1];
+  const bool OVERLAP = (int)blockIdx.x < n1;
   const int k = OVERLAP ? 1 : 0;
-  if ((int)blockIdx.x >= S.nlist[k]) return;
-  const int p = S.list[(size_t)k * n + blockIdx.x];
+  const int slot = OVERLAP ? (int)blockIdx.x : (int)blockIdx.x - n1;
+  if (slot >= S.nlist[k]) return;
+  const int p = S.list[(size_t)k * n + slot];
   const double *me = sph + 5 * p;
   const double R = me[3];
   const double R2 = R * R;
@@ -1151,27 +1154,16 @@ void launch_sphere_scatter(const Grid &g, double h, int s, int n, const double *
   if (n <= 0) return;
   static bool carve = false;  // 4 CTAs of ~40 KB static shared memory per SM
   if (!carve) {
-    cudaFuncSetAttribute(k_sphere_scatter<false, false>,
+    cudaFuncSetAttribute(k_sphere_scatter<false>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_sphere_scatter<true, false>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_sphere_scatter<false, true>,
-                         cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    cudaFuncSetAttribute(k_sphere_scatter<true, true>,
+    cudaFuncSetAttribute(k_sphere_scatter<true>,
                          cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     carve = true;
   }
-  if (is_periodic(g)) {
-    k_sphere_scatter<false, true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
-                                                          counts, S);
-    k_sphere_scatter<true, true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
-                                                         counts, S);
-  } else {
-    k_sphere_scatter<false, false><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
-                                                           counts, S);
-    k_sphere_scatter<true, false><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization,
-                                                          counts, S);
-  }
+  if (is_periodic(g))
+    k_sphere_scatter<true><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts, S);
+  else
+    k_sphere_scatter<false><<<n, kThreads, 0, st>>>(g, h, s, n, sph, normalization, counts, S);
 }
 // ---------------------------------------------------------------------------
 // Finest-grid RHS adaptation: f -= term_q for every
