@@ -327,6 +327,9 @@ int mg_coulomb_forces(mg_ctx *ctx, int n, const double *centers,
  * max_cycles; then, if forces_out != NULL, the Coulomb forces of the same
  * spheres on the new Phi (mg_coulomb_forces with force_subsample; forces
  * [3n]).  *cycles_out and *res_out (post-step residual norm) may be NULL.
+ * With cycles > 0 the RHS, the cycles and the forces are enqueued back to
+ * back and the host waits once at the end, so a sphere that covers no cell
+ * centre (MG_ERR_ARG) is reported after the step's cycles have run.
  * Returns MG_OK, MG_ERR_NOTCONV (cycles == 0 and max_cycles reached; forces
  * are still computed), or the errors of the calls it makes. */
 int mg_timestep(mg_ctx *ctx, int n, const double *centers, const double *radii,

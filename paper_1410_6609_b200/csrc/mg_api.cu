@@ -1626,10 +1626,12 @@ int mg_set_rhs(mg_ctx *c, const double *f, int where) {
   return sync(c);
 }
 
-int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
-                            const double *radii, const double *charges,
-                            int normalization, int subsample) {
-  Nvtx nv("mg_set_rhs_from_spheres");
+// enqueue the sphere RHS (no host synchronisation); *check: the empty-sphere
+// flag (mapped h_norm[1]) is being computed and must be read after a sync
+static int rhs_from_spheres(mg_ctx *c, int n, const double *centers, const double *radii,
+                            const double *charges, int normalization, int subsample,
+                            bool *check_out) {
+  *check_out = false;
   if (!c) return fail(MG_ERR_ARG, "null ctx");
   la_drop(c);
   if (n < 0) return fail(MG_ERR_ARG, "n < 0");
@@ -1728,10 +1730,26 @@ int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
   const bool check = normalization == MG_CHARGE_PER_CELLS && n > 0;
   if (check) mg::launch_first_empty(cnt, n, c->h_norm_dev + 1, c->stream);
   CK(cudaGetLastError());
-  if ((rc = sync(c))) return rc;
+  *check_out = check;
+  return MG_OK;
+}
+
+// the empty-sphere verdict of rhs_from_spheres (after a sync)
+static int empty_sphere_check(mg_ctx *c, bool check) {
   if (check && c->h_norm[1] >= 0.0)
     return fail(MG_ERR_ARG, "sphere %d covers no cell centre", (int)c->h_norm[1]);
   return MG_OK;
+}
+
+int mg_set_rhs_from_spheres(mg_ctx *c, int n, const double *centers,
+                            const double *radii, const double *charges,
+                            int normalization, int subsample) {
+  Nvtx nv("mg_set_rhs_from_spheres");
+  bool check;
+  int rc = rhs_from_spheres(c, n, centers, radii, charges, normalization, subsample, &check);
+  if (rc) return rc;
+  if ((rc = sync(c))) return rc;
+  return empty_sphere_check(c, check);
 }
 
 // enqueue one V-cycle (graph launch, recorded on first use); no host sync.
@@ -2417,17 +2435,56 @@ int mg_timestep(mg_ctx *c, int n, const double *centers, const double *radii,
   if (cycles < 0) return fail(MG_ERR_ARG, "cycles < 0");
   if (cycles == 0 && !(abs_tol > 0.0))
     return fail(MG_ERR_ARG, "cycles == 0 needs abs_tol > 0");
-  int rc = mg_set_rhs_from_spheres(c, n, centers, radii, charges,
-                                   normalization, subsample);
-  if (rc) return rc;
   int k = 0;
   double r = -1.0;
+  int rc;
   if (cycles > 0) {
-    // one cycle per new RHS: the look-ahead sweep would be discarded by the
-    // next step's RHS (4 B/cell more than the plain cycle's norm pass)
-    for (; k < cycles; k++)
-      if ((rc = vcycle(c, &r, cycles > 1))) break;
-  } else {  // Alg.1: while residual >= tol, perform a V-cycle
+    // The RHS, the cycles and the forces are enqueued back to back; the host
+    // waits once, at the end (the forces' readback or a final sync), and
+    // then checks the empty-sphere flag and the last cycle's norm.  Earlier
+    // cycles of a multi-cycle step keep their per-cycle check.  One cycle
+    // per new RHS takes the plain form: the look-ahead sweep would be
+    // discarded by the next step's RHS (4 B/cell more than the norm pass).
+    bool check;
+    if ((rc = rhs_from_spheres(c, n, centers, radii, charges, normalization, subsample,
+                               &check)))
+      return rc;
+    for (; k < cycles - 1; k++)
+      if ((rc = vcycle(c, &r, true))) break;
+    if (rc) {
+      if (cycles_out) *cycles_out = k;
+      if (res_out) *res_out = r;
+      sync(c);
+      if (int e = empty_sphere_check(c, check)) return e;
+      return rc;
+    }
+    const double prev = c->prev_norm;
+    if ((rc = enqueue_cycle(c, cycles > 1))) return rc;
+    k++;
+    if (forces_out) {
+      const unsigned long long *cnt =
+          (force_subsample == subsample && n > 0)
+              ? reinterpret_cast<const unsigned long long *>(c->sph + 5 * c->sph_cap)
+              : nullptr;
+      rc = coulomb_forces(c, n, centers, radii, charges, normalization, force_subsample,
+                          forces_out, cnt, n > 0 ? c->sph : nullptr);  // (syncs)
+    } else {
+      rc = sync(c);
+    }
+    if (int e = empty_sphere_check(c, check)) return e;
+    if (rc) return rc;
+    r = sqrt(*c->h_norm);
+    c->prev_norm = r;
+    if (cycles_out) *cycles_out = k;
+    if (res_out) *res_out = r;
+    if (!(r == r) || (prev >= 0.0 && r > 10.0 * prev))
+      return fail(MG_ERR_DIVERGED, "residual %g after %g", r, prev);
+    return MG_OK;
+  }
+  if ((rc = mg_set_rhs_from_spheres(c, n, centers, radii, charges, normalization,
+                                    subsample)))
+    return rc;
+  {  // Alg.1: while residual >= tol, perform a V-cycle
     if ((rc = residual_norm_now(c, &r))) return rc;
     c->prev_norm = r;
     while (r > abs_tol && k < c->o.max_cycles) {

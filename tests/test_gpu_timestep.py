@@ -129,3 +129,27 @@ def test_timestep_errors(mg):
     F, n, r = s2.timestep(w.centers, w.radii, w.charges, cycles=0,
                           abs_tol=1e-300, raise_notconv=False)
     assert n == 2 and F.shape == (len(w.radii), 3)
+
+
+@pytest.mark.parametrize("cycles,forces", [(1, True), (1, False), (3, True)])
+def test_timestep_empty_sphere_reported(mg, cycles, forces):
+    """With cycles > 0 the step is enqueued back to back and the host waits
+    once: a sphere that covers no cell centre is still reported (MG_ERR_ARG),
+    after the step; the next valid step equals a fresh context's."""
+    w = W.timestep_workload(n=32, seed=0)
+    c = np.concatenate([w.centers, [[8.0, 8.0, 8.0]]])
+    R = np.concatenate([w.radii, [0.2]])
+    q = np.concatenate([w.charges, [1.0]])
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4)
+    with pytest.raises(mg.MGError) as e:
+        s.timestep(c, R, q, cycles=cycles, forces=forces)
+    assert e.value.code == mg.MG_ERR_ARG
+    # the valid list afterwards: same forces and residual as a fresh context
+    s.zero_solution()
+    F1, n1, r1 = s.timestep(w.centers, w.radii, w.charges, cycles=cycles)
+    s2 = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=4)
+    F2, n2, r2 = s2.timestep(w.centers, w.radii, w.charges, cycles=cycles)
+    assert n1 == n2 == cycles and r1 == r2
+    assert np.array_equal(F1, F2)
+    s.close()
+    s2.close()
