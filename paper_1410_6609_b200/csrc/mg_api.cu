@@ -1212,6 +1212,7 @@ void free_mask(mg_ctx *c) {
       g.codeR = g.codeB = nullptr;
       g.coefR = g.coefB = nullptr;
       g.c64R = g.c64B = nullptr;
+      g.ukR = g.ukB = nullptr;
       g.all_unknown = 0;
     }
   c->masked = false;
@@ -2213,6 +2214,8 @@ int rebuild_coefficients_(mg_ctx *c) {
       CK(cudaMemsetAsync(b, 0, ne, c->stream));
       mg::launch_coef_to_code(g, r, b, dfail, c->stream);
       codes.push_back({r, b});
+      g.ukR = r;  // (bit 6 = D != 0 whether or not the codes are exact)
+      g.ukB = b;
     }
     int hfail = 1;
     CK(cudaMemcpyAsync(&hfail, dfail, sizeof(int), cudaMemcpyDeviceToHost,

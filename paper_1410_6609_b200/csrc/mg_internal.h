@@ -40,6 +40,9 @@ struct Grid {
   // every cell of the level is an unknown (records without a solid mask):
   // kernels that only need the unknown flag skip the records
   int all_unknown;
+  // byte flags of the float records (bit 6 = an unknown, coef D != 0), kept
+  // for kernels that only need that flag when the records are not codes
+  const unsigned char *ukR, *ukB;
   // periodic axes ("accessing unknowns in cells at opposite sides
   // of the domain"): per[a] = 1 for a periodic axis (dface = 0 on its faces).
   // Ghost layers then hold the opposite side's cells: rows 0 / ny+1 mirror

@@ -410,7 +410,7 @@ void launch_publish(const double *src, double *dev_dst, double *host_dst,
 
 // index of the first sphere whose covered count is 0 (or -1), written to
 // mapped host memory like k_publish (no copy-engine transfer)
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(1024)
     k_first_empty(const unsigned long long *counts, int n, double *host_dst) {
   __shared__ int first;
   if (threadIdx.x == 0) first = n;
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(kThreads)
 
 void launch_first_empty(const unsigned long long *counts, int n, double *host_dst,
                         cudaStream_t s) {
-  if (n > 0) k_first_empty<<<1, kThreads, 0, s>>>(counts, n, host_dst);
+  if (n > 0) k_first_empty<<<1, 1024, 0, s>>>(counts, n, host_dst);
 }
 
 // ---------------------------------------------------------------------------

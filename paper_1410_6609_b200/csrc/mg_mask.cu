@@ -853,24 +853,60 @@ void launch_coarse_cg_var(const Grid &g, double *scratch, double tol, int maxit,
 }
 
 // ---- f := 0 on solid cells (the oracle's "masked cells are not unknowns") -----
+// f := 0 on the cells that are not unknowns.  Byte flags (bit 64 <=> an
+// unknown, D != 0 -- the codes, or the flags of the float records): one warp
+// per row (il, j), four flags per 32-bit load (rows start at multiples of 4
+// elements), rows grid-strided over the warps.  Otherwise the records, one
+// CTA per row.
 __global__ void __launch_bounds__(kT) k_zero_solid(Grid g) {
-  const long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (long long)g.nxl * g.ny * g.nz) return;
-  const int z = (int)(t % g.nz);
-  const long long q = t / g.nz;
-  const int j = (int)(q % g.ny);
-  const int il = (int)(q / g.ny);
-  const int i = g.x0 + il;
-  const int col = (i + j + z) & 1;
-  const long long e = rb(g, il, j) + (z >> 1);
-  Coef C;
-  coef_at(g, col, e, i, j, z, C);
-  if (C.D == 0.0) (col ? g.fB : g.fR)[e] = 0.0;
+  const unsigned char *uR = g.coefR ? g.ukR : g.codeR, *uB = g.coefR ? g.ukB : g.codeB;
+  const unsigned rows = (unsigned)g.nxl * (unsigned)g.ny;
+  if (uR && !g.c64R) {
+    const int lane = threadIdx.x & 31;
+    const unsigned nw = gridDim.x * (blockDim.x >> 5);
+    const int nq = (g.nzh + 3) >> 2;  // 4-element groups per row half
+    for (unsigned row = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < rows;
+         row += nw) {
+      const int j = (int)(row % (unsigned)g.ny);
+      const int il = (int)(row / (unsigned)g.ny);
+      const int i = g.x0 + il;
+      const long long r = rb(g, il, j);
+      for (int q = lane; q < nq; q += 32)
+#pragma unroll
+        for (int col = 0; col < 2; col++) {
+          const unsigned w = *reinterpret_cast<const unsigned *>((col ? uB : uR) + r + 4 * q);
+          const int p = (i + j + col) & 1;
+          double *f = (col ? g.fB : g.fR) + r + 4 * q;
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const int z = 2 * (4 * q + b) + p;
+            if (z < g.nz && !((w >> (8 * b)) & 64u)) f[b] = 0.0;
+          }
+        }
+    }
+    return;
+  }
+  for (unsigned row = blockIdx.x; row < rows; row += gridDim.x) {
+    const int j = (int)(row % (unsigned)g.ny);
+    const int il = (int)(row / (unsigned)g.ny);
+    const int i = g.x0 + il;
+    const long long r = rb(g, il, j);
+    for (int z = threadIdx.x; z < g.nz; z += blockDim.x) {
+      const int col = (i + j + z) & 1;
+      const long long e = r + (z >> 1);
+      Coef C;
+      coef_at(g, col, e, i, j, z, C);
+      if (C.D == 0.0) (col ? g.fB : g.fR)[e] = 0.0;
+    }
+  }
 }
 
 void launch_zero_solid(const Grid &g, cudaStream_t s) {
-  const long long n = (long long)g.nxl * g.ny * g.nz;
-  if (n > 0 && (g.codeR || g.coefR || g.c64R)) k_zero_solid<<<nblk(n), kT, 0, s>>>(g);
+  const long long rows = (long long)g.nxl * g.ny;
+  if (rows > 0 && g.nz > 0 && (g.codeR || g.coefR || g.c64R)) {
+    const long long nb = rows < (long long)g.nsm * 8 ? rows : (long long)g.nsm * 8;
+    k_zero_solid<<<(unsigned)nb, kT, 0, s>>>(g);
+  }
 }
 
 // ---- operator of a level as 7 coefficients per cell, natural layout ------------
