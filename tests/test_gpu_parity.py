@@ -786,6 +786,42 @@ def test_coulomb_forces_loopback_slabs(mg, P):
     assert np.allclose(out[0], out[1], rtol=1e-13, atol=1e-13 * np.abs(out[0]).max())
 
 
+@pytest.mark.parametrize("sub,radii", [
+    (1, [7.7, 9.3, 11.2, 2.4]),   # uniform adjoint, direct force, scatter fallback, shell
+    (2, [7.6, 9.4, 4.1]),
+    (16, [2.2, 1.3]),             # counts up to 4096: no value table
+])
+def test_sphere_kernel_paths_large_spheres(mg, sub, radii):
+    """The size-dependent paths of the sphere kernels against the oracle:
+    boxes whose padded counts exceed the shell form's list / mask space (the
+    uniform adjoint sum), exceed the padded count array (the direct D3Q19
+    sum), exceed the scatter's shared count array (per-cell sub-centre
+    tests), and sub-cell counts above the value table (s = 16).  f bitwise,
+    forces to 1e-12 of the largest."""
+    shape, h = (64, 56, 48), 1.0
+    s, o = pair(mg, shape, h, "mixed", min_coarse=4)
+    L = np.array(shape) * h
+    rng = np.random.default_rng(len(radii) + sub)
+    c = np.array([L * [0.3 + 0.4 * k / len(radii), 0.5, 0.5] + rng.uniform(-0.5, 0.5, 3)
+                  for k in range(len(radii))])
+    r = np.array(radii) * h
+    q = rng.uniform(-2, 2, len(radii))
+    s.set_rhs_from_spheres(c, r, q, subsample=sub)
+    o.set_rhs_from_spheres(c, r, q, subsample=sub)
+    assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+    x = [(np.arange(n) + 0.5) * h for n in shape]
+    X = np.meshgrid(*x, indexing="ij")
+    phi = np.sin(0.11 * X[0]) * np.cos(0.07 * X[1]) + 0.02 * X[2] \
+        + 0.01 * rng.uniform(-1, 1, shape)
+    s.set_solution(phi)
+    o.set_phi(phi)
+    Fg = s.coulomb_forces(c, r, q, subsample=sub)
+    Fo = o.coulomb_forces(c, r, q, subsample=sub)
+    assert np.abs(Fo).max() > 0
+    assert np.abs(Fg - Fo).max() <= 1e-12 * np.abs(Fo).max()
+    s.close()
+
+
 def test_coulomb_force_errors(mg):
     s, _ = pair(mg, (8, 8, 8), 1.0, "dirichlet")
     c, r, q = np.zeros((1, 3)) + 4.0, np.array([2.0]), np.array([1.0])
