@@ -32,9 +32,9 @@ def rel(a, b):
 
 
 def run_steps(mg, w, steps, periodic=(False, False, False), sub=2,
-              amplitude=0.3):
+              amplitude=0.3, **kw):
     s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value,
-                     min_coarse=w.min_coarse, nu1=3, nu2=3)
+                     min_coarse=w.min_coarse, nu1=3, nu2=3, **kw)
     o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value,
                       min_coarse=w.min_coarse, nu1=3, nu2=3)
     c = w.centers
@@ -81,6 +81,21 @@ def test_timestep_parity_periodic_channel(mg):
     res = run_steps(mg, w, 4, periodic=(True, False, True), amplitude=0.8)
     r0 = res[0][2]
     for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-15 * r0, (k, rg, ro)
+        assert rel(pg, po) <= 1e-10
+        assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
+
+
+@pytest.mark.parametrize("halo,P", [("loopback", 2), ("loopback", 4), ("emulate", 2)])
+def test_timestep_parity_slabs(mg, halo, P):
+    """x-slab decomposition (one process, LOOPBACK device copies or the NCCL
+    schedule EMULATEd): the batched step (RHS, cycle and forces enqueued
+    back to back, one host wait) against the oracle."""
+    w = W.timestep_workload(n=64, seed=5)
+    res = run_steps(mg, w, 3, nranks=P, halo=halo, agglomerate_below=512)
+    r0 = res[0][2]
+    for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
+        assert ncyc == (5 if k == 0 else 1)
         assert abs(rg - ro) <= 1e-8 * ro + 1e-15 * r0, (k, rg, ro)
         assert rel(pg, po) <= 1e-10
         assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
