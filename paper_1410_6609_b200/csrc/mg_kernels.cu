@@ -830,7 +830,9 @@ void launch_coarse_cg(const Grid &g, double *scratch, double tol, int maxit,
 //                     into an ascending list.  A full bin or more than kNbMax
 //                     neighbours make every cell scan all spheres instead --
 //                     slow, still exact.  Isolated spheres (the common case)
-//                     take a lean scatter kernel of their own.
+//                     store their cells without the neighbour checks.  Per
+//                     box column the covered counts come from the sub-rows'
+//                     x intervals (sph::column_counts, reading d9).
 // sph holds (cx, cy, cz, R, Q) per sphere.  Every cell not covered keeps the
 // value it has (the caller zeroes f first).
 // ---------------------------------------------------------------------------

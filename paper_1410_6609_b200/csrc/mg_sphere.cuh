@@ -1,5 +1,6 @@
-// Sphere geometry shared by the RHS kernel (k_spheres, mg_kernels.cu) and the
-// Coulomb-force kernel (k_coulomb, mg_force.cu): the charge mapping of
+// Sphere geometry shared by the RHS kernels (k_sphere_count,
+// k_sphere_scatter, mg_kernels.cu) and the Coulomb-force kernel (k_coulomb,
+// mg_force.cu): the charge mapping of
 // "each cell whose center is overlapped", inclusive
 // test |x - c|^2 <= R^2 (reading c13), subsampling factor s (the
 // s^3 sub-cell centres ((i s + a + 1/2) h/s, ...)), periodic images
@@ -9,7 +10,8 @@
 // dx = ((double)(i s + a) + 0.5) * hs - cx, each product rounded on its own
 // (-fmad=false).  tables() stores the per-axis products dx*dx of one
 // sphere image in shared memory, so a test is two additions and a compare
-// that reproduce d2 bit for bit.
+// that reproduce d2 bit for bit; x_interval() finds the covered x
+// sub-positions of a (y, z) sub-row as one interval (reading d9).
 #pragma once
 #include <cuda_runtime.h>
 
