@@ -386,3 +386,61 @@ def test_random_coefficients_match_oracle(mg, prob):
             assert abs(a - b) <= 1e-8 * b + 1e-15 * ho[0], (prob[:6], hg, ho)
         assert err <= 1e-10, (prob[:6], err)
     s.close()
+
+
+@settings(max_examples=30, deadline=None, derandomize=True,
+          suppress_health_check=[HealthCheck.too_slow, HealthCheck.function_scoped_fixture])
+@given(sphere_problems(), st.integers(1, 3), st.integers(0, 2 ** 16))
+def test_random_timesteps_match_oracle(mg, prob, cycles, seed):
+    """N3 (Alg.1's potential part) on random geometry: two mg_timestep calls
+    (RHS, `cycles` warm-started cycles and forces enqueued back to back, one
+    host wait) with the spheres moved in between, against the oracle doing
+    the same calls: f bitwise, Phi rel-L2 <= 1e-10, the last cycle's
+    residual within the history clause, forces to 1e-9 of the largest."""
+    shape, bt, bv, h, c, R, q, sub, norm, slabs = prob
+    try:
+        o = oracle.Oracle(shape, h, bt, bv, min_coarse=2)
+    except ValueError:
+        return
+    extra = dict(nranks=slabs, halo="loopback", agglomerate_below=512) if slabs > 1 else {}
+    try:
+        s = mg.Multigrid(shape, h, bt, bv, min_coarse=2, **extra)
+    except mg.MGError:
+        assert slabs > 1
+        return
+    rng = np.random.default_rng(seed)
+    L = np.array(shape, float) * h
+    per = [bt[2 * a] == P for a in range(3)]
+    r0 = None
+    for step in range(2):
+        if step:  # move every sphere by up to half a cell, wrapping periodic axes
+            c = c + rng.uniform(-0.5, 0.5, c.shape) * h
+            for a in range(3):
+                c[:, a] = np.mod(c[:, a], L[a]) if per[a] else np.clip(c[:, a], 0.0, 0.999 * L[a])
+        try:
+            o.set_rhs_from_spheres(c, R, q, normalization=norm, subsample=sub)
+        except ValueError:  # a sphere covering no cell centre
+            with pytest.raises(mg.MGError):
+                s.timestep(c, R, q, cycles=cycles, normalization=norm, subsample=sub)
+            s.close()
+            return
+        if step == 0:
+            r0 = o.residual_norm()  # the history clause's scale (reading c21)
+            if r0 < 1e-140:
+                # (zero charges and boundary values near 1e-155: the squared
+                # norms and the CG's dot products underflow fp64 on both sides)
+                s.close()
+                return
+        ro = None
+        for _ in range(cycles):
+            ro = o.vcycle()
+        Fg, n, rg = s.timestep(c, R, q, cycles=cycles, normalization=norm, subsample=sub)
+        assert n == cycles
+        assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0)), prob
+        pg, po = s.get_solution(), o.phi()
+        assert np.linalg.norm(pg - po) <= 1e-10 * max(np.linalg.norm(po), 1e-300), prob
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (prob, rg, ro)
+        Fo = o.coulomb_forces(c, R, q, normalization=norm, subsample=sub)
+        scale = max(np.abs(Fo).max(), 1e-300)
+        assert np.abs(Fg - Fo).max() <= 1e-9 * scale, prob
+    s.close()
