@@ -438,8 +438,16 @@ def test_random_timesteps_match_oracle(mg, prob, cycles, seed):
         assert n == cycles
         assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0)), prob
         pg, po = s.get_solution(), o.phi()
-        assert np.linalg.norm(pg - po) <= 1e-10 * max(np.linalg.norm(po), 1e-300), prob
-        assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (prob, rg, ro)
+        err = np.linalg.norm(pg - po) / max(np.linalg.norm(po), 1e-300)
+        if s.nlevels == 1:
+            # one level: the cycle is the CG solve of the whole grid, stopped
+            # at tau_c by each side's own recurrence (reading c8): the CG
+            # contract, as in test_random_problems_match_oracle
+            assert rg <= max(4e-12 * r0, 2.0 * ro), (prob, rg, ro)
+            assert err <= 1e-8, (prob, err)
+        else:
+            assert err <= 1e-10, (prob, err)
+            assert abs(rg - ro) <= 1e-8 * ro + 1e-14 * r0, (prob, rg, ro)
         Fo = o.coulomb_forces(c, R, q, normalization=norm, subsample=sub)
         scale = max(np.abs(Fo).max(), 1e-300)
         assert np.abs(Fg - Fo).max() <= 1e-9 * scale, prob
