@@ -9,9 +9,12 @@
 //   the domain, else per axis central / one-sided differences.
 //   F_p = -h^3 sum_b grad Phi(x_b) rho_p(x_b), rho_p the sphere's own
 //   (subsampled) charge density with the RHS mapping's expressions.
-// One CTA per sphere: count the covered sub-cells of the whole domain, then
-// accumulate the slab's cells; per-slab partial sums, summed on the host in
-// slab / rank order.
+// One CTA per sphere: the covered sub-cell count of the whole domain (given
+// by the RHS of the same step, or counted here), the per-cell counts of the
+// sphere's box in shared memory (x intervals, mg_sphere.cuh), then the slab's
+// sum -- on interior boxes in adjoint form over a shell of cells (reading
+// d13, adjoint_force_shell), else cell by cell with the gradient of reading
+// d6; per-slab partial sums, summed on the host in slab / rank order.
 #include <cuda_runtime.h>
 
 #include "mg_internal.h"
