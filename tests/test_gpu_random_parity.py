@@ -87,9 +87,10 @@ def test_random_problems_match_oracle(mg, prob):
         # by rounding; the true residual reported here may exceed the
         # recursive one by the recurrence's rounding drift, which grows with
         # the iteration count and ||A|| ||Phi|| on both sides alike (observed:
-        # 4.03e-12 ||b|| for both at (2, 32, 120), h = 1/32): the oracle's
-        # true residual within 1e-11 ||b||, ours within twice the oracle's
-        assert all(x <= 1e-11 * ho[0] for x in ho[1:]), (prob, ho)
+        # 4.03e-12 ||b|| for both at (2, 32, 120), h = 1/32; 1.07e-11 ||b||
+        # for the oracle at (2, 2, 100), a 100-cell chain): the oracle's true
+        # residual within 1e-10 ||b||, ours within twice the oracle's
+        assert all(x <= 1e-10 * ho[0] for x in ho[1:]), (prob, ho)
         tol = max(4e-12 * ho[0], 2.0 * max(ho[1:]))
         assert all(x <= tol for x in hg[1:]), (prob, hg, ho)
         assert err <= 1e-8, (prob, err)
@@ -148,7 +149,7 @@ def test_random_paths_match_oracle(mg, prob):
     po = o.phi()
     err = np.linalg.norm(s.get_solution() - po) / max(np.linalg.norm(po), 1e-300)
     if s.nlevels == 1:
-        assert all(x <= 1e-11 * ho[0] for x in ho[1:]), (prob, ho)
+        assert all(x <= 1e-10 * ho[0] for x in ho[1:]), (prob, ho)
         tol = max(4e-12 * ho[0], 2.0 * max(ho[1:]))
         assert all(x <= tol for x in hg[1:]), (prob, hg, ho)
         assert err <= 1e-8, (prob, err)
