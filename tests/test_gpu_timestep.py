@@ -168,3 +168,36 @@ def test_timestep_empty_sphere_reported(mg, cycles, forces):
     assert np.array_equal(F1, F2)
     s.close()
     s2.close()
+
+
+def test_timestep_parity_masked(mg):
+    """Config 5's geometry (beam mask, channel walls) in the batched step:
+    RHS with the solid cells zeroed, warm-started V(3,3), forces with solid
+    gradient neighbours (reading d6), against the oracle."""
+    w = W.cfg5(scale=16, n_spheres=40)
+    s = mg.Multigrid(w.shape, w.h, w.bc_type, w.bc_value, min_coarse=w.min_coarse,
+                     nu1=3, nu2=3)
+    s.set_mask(w.solid)
+    o = oracle.Oracle(w.shape, w.h, w.bc_type, w.bc_value, solid=w.solid,
+                      min_coarse=w.min_coarse, nu1=3, nu2=3)
+    c = w.centers
+    r0 = None
+    for k in range(3):
+        if k:
+            c = W.move_spheres(c, w.radii, np.array(w.shape) * w.h, k, seed=11,
+                               amplitude=0.3)
+        cyc = 5 if k == 0 else 1
+        Fg, n, rg = s.timestep(c, w.radii, w.charges, cycles=cyc)
+        o.set_rhs_from_spheres(c, w.radii, w.charges)
+        if r0 is None:
+            r0 = o.residual_norm()
+        ro = None
+        for _ in range(cyc):
+            ro = o.vcycle()
+        Fo = o.coulomb_forces(c, w.radii, w.charges)
+        assert n == cyc
+        assert np.array_equal(s.get_field(0, mg.MG_FIELD_RHS), o.rhs(0))
+        assert abs(rg - ro) <= 1e-8 * ro + 1e-15 * r0, (k, rg, ro)
+        assert rel(s.get_solution(), o.phi()) <= 1e-10
+        assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
+    s.close()
