@@ -86,13 +86,21 @@ def test_timestep_parity_periodic_channel(mg):
         assert np.allclose(Fg, Fo, rtol=1e-9, atol=1e-9 * np.abs(Fo).max())
 
 
-@pytest.mark.parametrize("halo,P", [("loopback", 2), ("loopback", 4), ("emulate", 2)])
-def test_timestep_parity_slabs(mg, halo, P):
+@pytest.mark.parametrize("halo,P,periodic", [("loopback", 2, False), ("loopback", 4, False),
+                                             ("emulate", 2, False), ("loopback", 2, True),
+                                             ("emulate", 4, True)])
+def test_timestep_parity_slabs(mg, halo, P, periodic):
     """x-slab decomposition (one process, LOOPBACK device copies or the NCCL
-    schedule EMULATEd): the batched step (RHS, cycle and forces enqueued
-    back to back, one host wait) against the oracle."""
+    schedule EMULATEd), box and periodic channels: the batched step (RHS,
+    cycle and forces enqueued back to back, one host wait) against the
+    oracle."""
     w = W.timestep_workload(n=64, seed=5)
-    res = run_steps(mg, w, 3, nranks=P, halo=halo, agglomerate_below=512)
+    per = (False, False, False)
+    if periodic:
+        w.bc_type, w.bc_value = W.periodic_channel_bc(1.0)
+        per = (True, False, True)
+    res = run_steps(mg, w, 3, periodic=per, amplitude=0.8 if periodic else 0.3,
+                    nranks=P, halo=halo, agglomerate_below=512)
     r0 = res[0][2]
     for k, (ncyc, rg, ro, Fg, Fo, pg, po) in enumerate(res):
         assert ncyc == (5 if k == 0 else 1)
