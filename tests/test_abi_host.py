@@ -80,6 +80,19 @@ def test_create_without_gpu_fails_loudly():
     assert b"MG_ERR_CUDA" in mg.lib().mg_last_error(None)
 
 
+def test_missing_extension_fails_loudly(monkeypatch, tmp_path):
+    """No CPU fallback: with the shared library absent, loading it (and so
+    every product call) raises ImportError instead of computing anything
+    elsewhere; a solver's construction raises too (MGError first when no
+    device is present, ImportError from the loader on a GPU box)."""
+    monkeypatch.setattr(mg, "_lib", None)
+    monkeypatch.setattr(mg, "LIB_PATH", str(tmp_path / "libmg_cuda.so"))
+    with pytest.raises(ImportError, match="no CPU fallback"):
+        mg.lib()
+    with pytest.raises((ImportError, mg.MGError)):
+        mg.Multigrid((8, 8, 8), 1.0, [0] * 6)
+
+
 @pytest.mark.parametrize("shape,mc", [((32, 32, 32), 4), ((256, 64, 64), 4),
                                       ((512, 512, 512), 8), ((64, 16, 48), 2),
                                       ((24, 24, 24), 2), ((2, 2, 2), 1)])
